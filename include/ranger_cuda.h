@@ -1,0 +1,324 @@
+/*
+ * ranger_cuda.h -- C ABI of the B200-native census template-matching ranger.
+ *
+ * This is the drop-in boundary for the reference's hot path (the header-only
+ * C++ API in proj/include/ranger/ of arxiv/paper_2604_07980).  Every entry
+ * point below names the reference interface it replaces (file:line, relative
+ * to the reference's proj/include/ranger/).  The C++ facade in
+ * include/ranger/ (*.hpp) keeps the reference declarations verbatim and forwards
+ * here; Python binds the same symbols with ctypes.
+ *
+ * Conventions
+ *   - plain pointers and sizes only; no torch / CUDA types in signatures
+ *     (streams are passed as void* = cudaStream_t).
+ *   - every function returns an rg_status; on failure rg_last_error(ctx)
+ *     holds a message.  RG_EINVAL maps to std::invalid_argument in the
+ *     facade (reference: census.hpp:71-74, template_match.hpp:48-61,
+ *     autorect.hpp:25-32, bm.hpp:24-32), everything else to
+ *     std::runtime_error.
+ *   - "host" arguments are ordinary host memory; "d_" arguments are device
+ *     pointers on the context's device.
+ *   - a context is single-writer (one host thread at a time), like the
+ *     reference's CensusCache; create one per host thread for concurrency.
+ */
+#ifndef RANGER_CUDA_H_
+#define RANGER_CUDA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int rg_status;
+#define RG_OK 0
+#define RG_EINVAL 1   /* invalid argument  -> std::invalid_argument */
+#define RG_ECUDA 2    /* CUDA runtime error -> std::runtime_error   */
+#define RG_ENOMEM 3   /* allocation failure -> std::runtime_error   */
+#define RG_EOVERFLOW 4 /* device work list overflowed; call again    */
+
+/* Object kinds, reference census.hpp:143 (enum class ObjectKind). */
+#define RG_KIND_FAR 0
+#define RG_KIND_CLOSE 1
+
+/* Match modes for rg_match_blocks. */
+#define RG_MATCH_FORWARD 0 /* block_match, census.hpp:178-272            */
+#define RG_MATCH_FWD_BWD 1 /* forward_backward_match, census.hpp:281-303 */
+
+typedef struct rg_ctx rg_ctx;
+
+/* ---------------------------------------------------------------- context */
+rg_status rg_ctx_create(int device, rg_ctx** out);
+void rg_ctx_destroy(rg_ctx* ctx);
+const char* rg_last_error(const rg_ctx* ctx);
+/* message of the last failed rg_ctx_create on this thread */
+const char* rg_create_error(void);
+/* library build identification: "sm_100a <git-describe-ish>" */
+const char* rg_build_info(void);
+
+/* Per-stage CUDA-event timing of the batched API (off by default). */
+rg_status rg_set_profiling(rg_ctx* ctx, int on);
+/* Accumulated stage milliseconds and launch counts since the last reset:
+ * times[0..4] = census, plan, match, aggregate, autorect;
+ * launches[0..4] likewise; returns the total kernel launch count in *total. */
+rg_status rg_get_counters(rg_ctx* ctx, double times_ms[5], int64_t launches[5],
+                          int64_t* total_launches);
+rg_status rg_reset_counters(rg_ctx* ctx);
+
+/* ---------------------------------------------------------------- types */
+
+/* CensusRoi (census.hpp:93) and ImageRoi (autorect.hpp:13-17): half-open. */
+typedef struct {
+  int32_t x0, y0, x1, y1;
+} rg_rect;
+
+/* QueryBlock search ranges (census.hpp:146-152), inclusive. */
+typedef struct {
+  int32_t dx_min, dx_max, dy_min, dy_max;
+} rg_search_range;
+
+/* MatchResult (census.hpp:154-163) plus std::optional engagement. */
+typedef struct {
+  int32_t dx_int;
+  int32_t dy_int;
+  double dx_subpix;
+  double cost;
+  double cost_minus;
+  double cost_plus;
+  int32_t valid_points;
+  int32_t verified;
+  int32_t has_value; /* 0 = std::nullopt                                  */
+  int32_t n_points;  /* sampled points of the block (planner path)        */
+} rg_match_result;
+
+/* Detection (detection.hpp:8-12); identical layout to ranger::Detection. */
+typedef struct {
+  double cx, cy, w, h;
+  int32_t class_id;
+  int32_t id;
+} rg_detection;
+
+/* RangerConfig (template_match.hpp:33-46) with FrontalCrop flattened. */
+typedef struct {
+  double tau_s;
+  int32_t close_scale;
+  int32_t grid_side_points;
+  int32_t max_total_points;
+  int32_t close_block_side_points;
+  double tau_d;
+  int32_t n_min;
+  int32_t max_objects;
+  double tau_v;
+  double crop_x0, crop_y0, crop_x1, crop_y1;
+  int32_t dx_max_far;
+  int32_t dx_max_close;
+} rg_ranger_config;
+
+/* ObjectDisparity (template_match.hpp:18-24) plus the range z_cam
+ * (geometry.hpp:142-146, 198-211) when a calibration is supplied. */
+typedef struct {
+  int32_t det_id;
+  int32_t kind;
+  int32_t n_blocks_used;
+  int32_t valid;
+  double disparity;
+  double z_cam; /* 0 when invalid or no calibration */
+} rg_object_disparity;
+
+/* RangerStats (template_match.hpp:236-241). */
+typedef struct {
+  int64_t query_points;
+  int64_t image_pixels;
+  int32_t n_far;
+  int32_t n_close;
+} rg_ranger_stats;
+
+/* CensusCache (template_match.hpp:229-234).  Buffers are caller-owned host
+ * arrays: full_* hold w*h codes, scaled_* hold (w/s)*(h/s) codes.  has_* on
+ * input: the buffer holds codes to be used as-is.  On output has_* is set to
+ * 1 when this call filled the buffers (ROI-masked codes, as the reference). */
+typedef struct {
+  uint32_t* full_left;
+  uint32_t* full_right;
+  uint32_t* scaled_left;
+  uint32_t* scaled_right;
+  int32_t has_full;
+  int32_t has_scaled;
+} rg_census_cache;
+
+/* BmParams (bm.hpp:15-22). */
+typedef struct {
+  int32_t num_disparities;
+  int32_t block_size;
+  int32_t min_disparity;
+  int32_t downscale;
+  double texture_threshold;
+  double uniqueness_ratio;
+} rg_bm_params;
+
+/* ------------------------------------------------------ census (K1) */
+
+/* census_code_at, census.hpp:43-56 */
+rg_status rg_census_code_at(rg_ctx* ctx, const uint8_t* img, int w, int h, int sx,
+                            int sy, uint32_t* code);
+/* census_transform, census.hpp:69-90 (out = src dims gives census.hpp:88-90) */
+rg_status rg_census_transform(rg_ctx* ctx, const uint8_t* img, int w, int h,
+                              int out_w, int out_h, uint32_t* codes);
+/* census_transform_rois, census.hpp:100-138 */
+rg_status rg_census_transform_rois(rg_ctx* ctx, const uint8_t* img, int w, int h,
+                                   int out_w, int out_h, const rg_rect* rois,
+                                   int n_rois, uint32_t* codes);
+
+/* ------------------------------------------------------ matcher (K2) */
+
+/* block_match (census.hpp:178-272), forward_backward_match (:281-303) and
+ * batch_match (:307-315) over n_blocks blocks given in CSR form:
+ * points_xy[2*k], points_xy[2*k+1] for k in [offsets[b], offsets[b+1]).
+ * left/right are census rasters (lw x lh, rw x rh codes, row-major). */
+rg_status rg_match_blocks(rg_ctx* ctx, const uint32_t* left, int lw, int lh,
+                          const uint32_t* right, int rw, int rh,
+                          const int32_t* points_xy, const int64_t* offsets,
+                          const rg_search_range* ranges, int n_blocks, int mode,
+                          double tau_v, rg_match_result* out);
+
+/* ------------------------------------------------------ object ranger */
+
+/* validate(const RangerConfig&), template_match.hpp:48-61 */
+rg_status rg_validate_ranger_config(rg_ctx* ctx, const rg_ranger_config* cfg);
+
+/* select_objects, template_match.hpp:94-114 (priority order, truncated). */
+rg_status rg_select_objects(rg_ctx* ctx, const rg_detection* dets, int n,
+                            const rg_ranger_config* cfg, int32_t* out_idx,
+                            int* n_out);
+/* find_occluders, template_match.hpp:71-89; CSR out, occ_idx capacity n*n. */
+rg_status rg_find_occluders(rg_ctx* ctx, const rg_detection* dets, int n,
+                            int32_t* occ_offsets, int32_t* occ_idx);
+/* sample_query_points, template_match.hpp:155-223.  occluder_boxes holds
+ * n_occ PixelBoxes as (x0,y0,x1,y1) doubles.  Output CSR capacity:
+ * cap_blocks blocks / cap_points points; *n_blocks receives the count. */
+rg_status rg_sample_query_points(rg_ctx* ctx, const rg_detection* det, int kind,
+                                 const double* occluder_boxes, int n_occ,
+                                 const rg_ranger_config* cfg, int img_w, int img_h,
+                                 int64_t* block_offsets, int32_t* points_xy,
+                                 rg_search_range* ranges, int cap_blocks,
+                                 int64_t cap_points, int* n_blocks);
+/* aggregate_close_disparities, template_match.hpp:126-148 */
+rg_status rg_aggregate_close_disparities(rg_ctx* ctx, const double* disps, int n,
+                                         double tau_d, int n_min, int32_t* valid,
+                                         double* disparity, int32_t* run_length);
+
+/* estimate_object_disparities, template_match.hpp:260-363.  out has room for
+ * n_dets entries; *n_out receives the number written (selected objects, in
+ * input order).  cache and stats may be NULL.  focal_px/baseline_m > 0 also
+ * fill z_cam (geometry.hpp:142-146). */
+rg_status rg_estimate_object_disparities(rg_ctx* ctx, const uint8_t* left,
+                                         const uint8_t* right, int w, int h,
+                                         const rg_detection* dets, int n_dets,
+                                         const rg_ranger_config* cfg,
+                                         rg_census_cache* cache, double focal_px,
+                                         double baseline_m, rg_object_disparity* out,
+                                         int* n_out, rg_ranger_stats* stats);
+
+/* Batched frame ranging -- the throughput path (one process per GPU).
+ * Frames f in [0, n_frames): left/right images at base + f*frame_stride,
+ * rows `pitch` bytes apart (pitch >= width, multiple of 16 for the fast
+ * census path).  Detections of frame f: dets[det_offsets[f] .. det_offsets[f+1]).
+ * Results: out[f*out_stride + k] for k < out_count[f] (selected objects in
+ * input order); out_stride >= min(max_dets_per_frame, cfg.max_objects).
+ * All pointers are device pointers; the call is asynchronous on `stream`
+ * except that it returns RG_EOVERFLOW when the previous call on this context
+ * found its internal block list too small (the call is then re-run
+ * synchronously with a grown list). */
+typedef struct {
+  int32_t n_frames;
+  int32_t width;
+  int32_t height;
+  int32_t pitch;
+  int64_t frame_stride;
+  const uint8_t* d_left;
+  const uint8_t* d_right;
+  const rg_detection* d_dets;
+  const int32_t* d_det_offsets; /* n_frames + 1 */
+  int32_t max_dets_per_frame;
+  int32_t out_stride;
+  rg_object_disparity* d_out;
+  int32_t* d_out_count;
+  double focal_px;   /* <= 0: no range */
+  double baseline_m;
+} rg_frame_batch;
+
+rg_status rg_range_frames(rg_ctx* ctx, const rg_frame_batch* batch,
+                          const rg_ranger_config* cfg, void* stream);
+
+/* Host-buffer variant of rg_range_frames: left/right/dets/offsets/out/count are
+ * HOST pointers (pinned memory recommended).  The library streams frames
+ * through device staging in chunks of `chunk` frames with copy/compute
+ * overlap and returns after the results are on the host. */
+rg_status rg_range_frames_host(rg_ctx* ctx, const rg_frame_batch* batch,
+                               const rg_ranger_config* cfg, int chunk, void* stream);
+
+/* ------------------------------------------------------ BM / autorect (K5) */
+
+/* validate(const BmParams&), bm.hpp:24-32 */
+rg_status rg_validate_bm_params(rg_ctx* ctx, const rg_bm_params* p);
+/* bm_disparity, bm.hpp:113-135 (downscale path: image.hpp:98-141) */
+rg_status rg_bm_disparity(rg_ctx* ctx, const uint8_t* left, const uint8_t* right,
+                          int w, int h, const rg_bm_params* p, int16_t* out_raw);
+/* auto_rect_search, autorect.hpp:22-58.  counts (nullable) receives the
+ * per-delta valid counts, delta_max - delta_min + 1 entries. */
+rg_status rg_auto_rect_search(rg_ctx* ctx, const uint8_t* left, const uint8_t* right,
+                              int w, int h, const rg_rect* roi, int delta_min,
+                              int delta_max, const rg_bm_params* p, int32_t* best_delta,
+                              int64_t* counts);
+/* Batched device variant: frames as in rg_frame_batch (d_left/d_right, pitch,
+ * frame_stride); d_best[n_frames], d_counts[n_frames * n_delta] (nullable). */
+rg_status rg_auto_rect_frames(rg_ctx* ctx, const uint8_t* d_left,
+                              const uint8_t* d_right, int n_frames, int64_t frame_stride,
+                              int pitch, int w, int h, const rg_rect* roi, int delta_min,
+                              int delta_max, const rg_bm_params* p, int32_t* d_best,
+                              int64_t* d_counts, void* stream);
+
+/* ------------------------------------------------------ synthetic frames */
+
+/* SceneObject (synth.hpp:25-34) and SceneConfig (synth.hpp:36-52) with the
+ * canonical calibration make_calibration(f, b, cx, cy, h_cam)
+ * (geometry.hpp:130-133).  Used as the input generator for tests/bench. */
+typedef struct {
+  int32_t id;
+  int32_t class_id;
+  double px, py, pz; /* vehicle frame, m */
+  double width_m, height_m, depth_m;
+  double contrast;
+  double disparity_ramp;
+  uint64_t texture_seed;
+} rg_scene_object;
+
+typedef struct {
+  double f, b, cx, cy, h_cam;
+  int32_t width, height;
+  uint64_t background_seed;
+  double background_contrast;
+  int32_t vertical_offset_px;
+  int32_t texture_quant;
+  double disparity_bias_px;
+  double gain, rad_bias, gamma;
+  double noise_sigma;
+  uint64_t seed;
+  double texture_cell_px;
+} rg_scene_config;
+
+/* render_stereo_pair, synth.hpp:142-230 (host, multi-threaded rows). */
+rg_status rg_render_stereo_pair(const rg_scene_config* cfg, const rg_scene_object* objs,
+                                int n_obj, uint8_t* left, uint8_t* right,
+                                double* true_disparity, int32_t* object_id);
+/* ground_truth_detections, synth.hpp:253-274 (capacity n_obj). */
+rg_status rg_ground_truth_detections(const rg_scene_config* cfg,
+                                     const rg_scene_object* objs, int n_obj,
+                                     rg_detection* out, int* n_out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RANGER_CUDA_H_ */

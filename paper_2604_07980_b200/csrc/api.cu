@@ -1,0 +1,1090 @@
+// api.cu -- the C ABI (include/ranger_cuda.h): context, buffers, the
+// reference-compatible synchronous entry points and the batched pipeline.
+//
+// Every compute entry point runs on the GPU; there is no CPU fallback.  Host
+// code here only validates arguments (mirroring the reference's
+// std::invalid_argument checks), moves bytes, and assembles results.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "rg_common.cuh"
+
+#ifndef RG_BUILD_INFO
+#define RG_BUILD_INFO "sm_100a"
+#endif
+
+namespace rg {
+
+rg_status set_err(rg_ctx* ctx, rg_status st, const std::string& msg) {
+  if (ctx) ctx->err = msg;
+  return st;
+}
+
+rg_status cuda_err(rg_ctx* ctx, cudaError_t e, const char* what) {
+  if (ctx) ctx->err = std::string(what) + ": " + cudaGetErrorString(e);
+  return e == cudaErrorMemoryAllocation ? RG_ENOMEM : RG_ECUDA;
+}
+
+void* dev_buf(rg_ctx* ctx, int id, size_t bytes) {
+  if (bytes == 0) bytes = 16;
+  if (ctx->cap[id] >= bytes) return ctx->buf[id];
+  if (ctx->buf[id]) {
+    cudaStreamSynchronize(ctx->stream);
+    cudaFree(ctx->buf[id]);
+    ctx->buf[id] = nullptr;
+    ctx->cap[id] = 0;
+  }
+  const size_t want = std::max(bytes, ctx->cap[id] + ctx->cap[id] / 4);
+  void* p = nullptr;
+  if (cudaMalloc(&p, want) != cudaSuccess) {
+    cudaGetLastError();
+    if (cudaMalloc(&p, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    ctx->cap[id] = bytes;
+  } else {
+    ctx->cap[id] = want;
+  }
+  ctx->buf[id] = p;
+  if (id == B_MAPX || id == B_MAPY) ctx->map_key[0] = -1;  // contents lost
+  return p;
+}
+
+void* host_buf(rg_ctx* ctx, int id, size_t bytes) {
+  if (bytes == 0) bytes = 16;
+  if (ctx->hcap[id] >= bytes) return ctx->hbuf[id];
+  if (ctx->hbuf[id]) {
+    cudaStreamSynchronize(ctx->stream);
+    cudaFreeHost(ctx->hbuf[id]);
+    ctx->hbuf[id] = nullptr;
+    ctx->hcap[id] = 0;
+  }
+  void* p = nullptr;
+  if (cudaMallocHost(&p, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  ctx->hbuf[id] = p;
+  ctx->hcap[id] = bytes;
+  return p;
+}
+
+void count_launch(rg_ctx* ctx, int stage, int n) {
+  ctx->stage_launches[stage] += n;
+  ctx->total_launches += n;
+}
+
+}  // namespace rg
+
+using namespace rg;
+
+namespace {
+
+thread_local std::string g_create_err;
+
+#define DBUF(T, ctx, id, n)                                                          \
+  static_cast<T*>(rg::dev_buf(ctx, id, sizeof(T) * (size_t)(n)))
+#define NEED(ptr)                                                                    \
+  do {                                                                               \
+    if (!(ptr)) return set_err(ctx, RG_ENOMEM, "device allocation failed");          \
+  } while (0)
+#define TRY(expr)                                                                    \
+  do {                                                                               \
+    rg_status _s = (expr);                                                           \
+    if (_s != RG_OK) return _s;                                                      \
+  } while (0)
+
+enum Stage { ST_CENSUS = 0, ST_PLAN = 1, ST_MATCH = 2, ST_AGG = 3, ST_RECT = 4 };
+
+rg_status bind(rg_ctx* ctx) {
+  if (!ctx) return RG_EINVAL;
+  cudaError_t e = cudaSetDevice(ctx->device);
+  if (e != cudaSuccess) return cuda_err(ctx, e, "cudaSetDevice");
+  return RG_OK;
+}
+
+// census.hpp:59-64 detail::scaled_coords
+std::vector<int32_t> scaled_coords(int out, int src) {
+  std::vector<int32_t> m(static_cast<size_t>(out));
+  for (int i = 0; i < out; ++i)
+    m[i] = (out == src) ? i : int(std::lround(i * double(src) / double(out)));
+  return m;
+}
+
+// inverse of the reduced-raster gather maps: inv[src] = out index or -1.
+// Cached per geometry; the maps only depend on (w, h, ow, oh).
+rg_status upload_inverse_maps(rg_ctx* ctx, int w, int h, int ow, int oh, cudaStream_t s,
+                              int32_t** inv_x, int32_t** inv_y) {
+  const bool hit = ctx->map_key[0] == w && ctx->map_key[1] == h && ctx->map_key[2] == ow &&
+                   ctx->map_key[3] == oh;
+  int32_t* dx = DBUF(int32_t, ctx, B_MAPX, w);
+  int32_t* dy = DBUF(int32_t, ctx, B_MAPY, h);
+  NEED(dx);
+  NEED(dy);
+  if (!hit) {
+    std::vector<int32_t> ix(static_cast<size_t>(w), -1), iy(static_cast<size_t>(h), -1);
+    const auto mx = scaled_coords(ow, w), my = scaled_coords(oh, h);
+    for (int i = 0; i < ow; ++i) ix[mx[i]] = i;
+    for (int i = 0; i < oh; ++i) iy[my[i]] = i;
+    RG_CUDA(ctx, cudaMemcpyAsync(dx, ix.data(), sizeof(int32_t) * w, cudaMemcpyHostToDevice, s));
+    RG_CUDA(ctx, cudaMemcpyAsync(dy, iy.data(), sizeof(int32_t) * h, cudaMemcpyHostToDevice, s));
+    RG_CUDA(ctx, cudaStreamSynchronize(s));  // host vectors die at scope exit
+    ctx->map_key[0] = w;
+    ctx->map_key[1] = h;
+    ctx->map_key[2] = ow;
+    ctx->map_key[3] = oh;
+  }
+  *inv_x = dx;
+  *inv_y = dy;
+  return RG_OK;
+}
+
+// upload a packed (w*h) host image into a device buffer with the same layout
+rg_status upload_image(rg_ctx* ctx, int id, const uint8_t* img, int w, int h, uint8_t** out) {
+  uint8_t* d = DBUF(uint8_t, ctx, id, (size_t)w * h);
+  NEED(d);
+  RG_CUDA(ctx, cudaMemcpyAsync(d, img, (size_t)w * h, cudaMemcpyHostToDevice, ctx->stream));
+  *out = d;
+  return RG_OK;
+}
+
+// one-image census into full (w*h) and optional reduced (ow*oh) device buffers
+rg_status census_one(rg_ctx* ctx, const uint8_t* d_img, int w, int h, int ow, int oh,
+                     uint32_t* d_full, uint32_t* d_red) {
+  int32_t *ix = nullptr, *iy = nullptr;
+  TRY(upload_inverse_maps(ctx, w, h, ow, oh, ctx->stream, &ix, &iy));
+  RG_CUDA(ctx, launch_census_frames(d_img, nullptr, 1, 0, w, w, h, d_full, nullptr, d_red,
+                                    nullptr, ow, oh, ix, iy, ctx->stream));
+  count_launch(ctx, ST_CENSUS);
+  return RG_OK;
+}
+
+rg_status check_cfg(rg_ctx* ctx, const rg_ranger_config* c) {  // template_match.hpp:48-61
+  if (!c) return set_err(ctx, RG_EINVAL, "RangerConfig: null");
+  if (c->tau_s <= 0 || c->tau_d <= 0 || c->tau_v < 0)
+    return set_err(ctx, RG_EINVAL, "RangerConfig: thresholds must be positive");
+  if (c->n_min < 1) return set_err(ctx, RG_EINVAL, "RangerConfig: n_min must be >= 1");
+  if (c->close_scale < 1) return set_err(ctx, RG_EINVAL, "RangerConfig: close_scale must be >= 1");
+  if (c->grid_side_points < 1 || c->max_total_points < 1 || c->close_block_side_points < 1)
+    return set_err(ctx, RG_EINVAL, "RangerConfig: point counts must be >= 1");
+  if (c->max_objects < 0) return set_err(ctx, RG_EINVAL, "RangerConfig: max_objects must be >= 0");
+  if (c->dx_max_far < 0 || c->dx_max_close < 0)
+    return set_err(ctx, RG_EINVAL, "RangerConfig: search ceilings must be >= 0");
+  return RG_OK;
+}
+
+rg_status check_bm(rg_ctx* ctx, const rg_bm_params* p) {  // bm.hpp:24-32
+  if (!p) return set_err(ctx, RG_EINVAL, "BmParams: null");
+  if (p->block_size < 3 || p->block_size % 2 == 0)
+    return set_err(ctx, RG_EINVAL, "BmParams: block_size must be odd and >= 3");
+  if (p->num_disparities < 1) return set_err(ctx, RG_EINVAL, "BmParams: num_disparities must be >= 1");
+  if (p->uniqueness_ratio < 0) return set_err(ctx, RG_EINVAL, "BmParams: uniqueness_ratio must be >= 0");
+  if (p->downscale < 1) return set_err(ctx, RG_EINVAL, "BmParams: downscale must be >= 1");
+  return RG_OK;
+}
+
+// max points of any QueryBlock the planner can generate (template_match.hpp:165-194)
+int planner_max_points(const rg_ranger_config& c) {
+  const int cap = std::max(1, int(std::sqrt(double(c.max_total_points))));
+  const int nf = std::min(c.grid_side_points, cap), nc = std::min(c.close_block_side_points, cap);
+  return std::max(nf * nf, nc * nc);
+}
+
+size_t match_smem_bytes(int maxp, bool with_pts) {
+  const size_t mp = (size_t)((maxp + 3) & ~3);
+  return sizeof(uint32_t) * kWindowCodes + (with_pts ? 8 * mp : 0) + 16 * mp;
+}
+constexpr size_t kSmemLimit = 220 * 1024;
+
+// ------------------------------------------------------------------------
+// The batched pipeline over frames resident on the device.
+struct FrameJob {
+  const uint8_t* left;
+  const uint8_t* right;
+  int n_frames, w, h, pitch;
+  int64_t frame_stride;
+  const rg_detection* dets;
+  const int32_t* det_off;
+  int out_stride;
+  rg_object_disparity* out;
+  int32_t* out_count;
+  rg_ranger_stats* stats;  // device, n_frames entries (nullable)
+  double focal, baseline;
+  // census override (compat path with a pre-filled cache): device codes
+  const uint32_t* full_l = nullptr;
+  const uint32_t* full_r = nullptr;
+  const uint32_t* scaled_l = nullptr;
+  const uint32_t* scaled_r = nullptr;
+};
+
+struct PipelineBufs {
+  uint32_t *fl, *fr, *sl, *sr;
+  ObjEntry* objs;
+  Slot* slots;
+  rg_match_result* res;
+  int32_t* counters;
+  double* scratch;
+  int capacity;
+};
+
+rg_status enqueue_pipeline(rg_ctx* ctx, const FrameJob& J, const rg_ranger_config& cfg,
+                           cudaStream_t s, int32_t* counters, PipelineBufs* pb) {
+  const int w = J.w, h = J.h, sc = cfg.close_scale;
+  const int cw = w / sc, ch = h / sc;
+  const int F = J.n_frames;
+  if (cw < 1 || ch < 1) return set_err(ctx, RG_EINVAL, "estimate_object_disparities: close raster empty");
+  const int maxp = planner_max_points(cfg);
+  if (match_smem_bytes(maxp, true) > kSmemLimit)
+    return set_err(ctx, RG_EINVAL, "RangerConfig: blocks too large for the device matcher");
+  const int64_t full_stride = (int64_t)w * h, scaled_stride = (int64_t)cw * ch;
+  uint32_t* fl = DBUF(uint32_t, ctx, B_CEN_FL, full_stride * F);
+  uint32_t* fr = DBUF(uint32_t, ctx, B_CEN_FR, full_stride * F);
+  uint32_t* sl = DBUF(uint32_t, ctx, B_CEN_SL, scaled_stride * F);
+  uint32_t* sr = DBUF(uint32_t, ctx, B_CEN_SR, scaled_stride * F);
+  NEED(fl);
+  NEED(fr);
+  NEED(sl);
+  NEED(sr);
+  if (ctx->slot_capacity < F * 64) ctx->slot_capacity = F * 64;
+  const int capacity = ctx->slot_capacity;
+  ObjEntry* objs = DBUF(ObjEntry, ctx, B_OBJ, (size_t)F * std::max(J.out_stride, 1));
+  Slot* slots = DBUF(Slot, ctx, B_SLOTS, capacity);
+  rg_match_result* res = DBUF(rg_match_result, ctx, B_SLOT_RES, capacity);
+  double* scratch = DBUF(double, ctx, B_TMP3, 2 * (size_t)capacity);
+  NEED(objs);
+  NEED(slots);
+  NEED(res);
+  NEED(scratch);
+  int32_t *ix = nullptr, *iy = nullptr;
+  TRY(upload_inverse_maps(ctx, w, h, cw, ch, s, &ix, &iy));
+  RG_CUDA(ctx, cudaMemsetAsync(counters, 0, 2 * sizeof(int32_t), s));
+  const bool prof = ctx->profiling;
+  if (prof) RG_CUDA(ctx, cudaEventRecord(ctx->ev[0], s));
+  // K1 census (full + fused reduced raster) of both images of every frame
+  if (!(J.full_l && J.scaled_l)) {
+    RG_CUDA(ctx, launch_census_frames(J.left, J.right, F, J.frame_stride, J.pitch, w, h, fl, fr, sl,
+                                      sr, cw, ch, ix, iy, s));
+    count_launch(ctx, ST_CENSUS);
+  }
+  if (J.full_l) {
+    RG_CUDA(ctx, cudaMemcpyAsync(fl, J.full_l, sizeof(uint32_t) * full_stride, cudaMemcpyDeviceToDevice, s));
+    RG_CUDA(ctx, cudaMemcpyAsync(fr, J.full_r, sizeof(uint32_t) * full_stride, cudaMemcpyDeviceToDevice, s));
+  }
+  if (J.scaled_l) {
+    RG_CUDA(ctx, cudaMemcpyAsync(sl, J.scaled_l, sizeof(uint32_t) * scaled_stride, cudaMemcpyDeviceToDevice, s));
+    RG_CUDA(ctx, cudaMemcpyAsync(sr, J.scaled_r, sizeof(uint32_t) * scaled_stride, cudaMemcpyDeviceToDevice, s));
+  }
+  if (prof) RG_CUDA(ctx, cudaEventRecord(ctx->ev[1], s));
+  // K3 planner
+  RG_CUDA(ctx, launch_plan_frames(J.dets, J.det_off, F, w, h, cfg, J.out_stride, objs, J.out,
+                                  J.out_count, slots, capacity, counters, J.stats, s));
+  count_launch(ctx, ST_PLAN);
+  if (prof) RG_CUDA(ctx, cudaEventRecord(ctx->ev[2], s));
+  // K2 fused sampler + forward/backward matcher, one CTA per slot
+  RG_CUDA(ctx, launch_match_slots(slots, counters, capacity, objs, J.dets, J.det_off, fl, fr, sl, sr,
+                                  w, h, cw, ch, full_stride, scaled_stride, cfg, res, J.stats, maxp, s));
+  count_launch(ctx, ST_MATCH);
+  if (prof) RG_CUDA(ctx, cudaEventRecord(ctx->ev[3], s));
+  // K4 aggregation + range
+  RG_CUDA(ctx, launch_aggregate(objs, J.out_count, F, J.out_stride, res, capacity, cfg, J.focal,
+                                J.baseline, scratch, J.out, s));
+  count_launch(ctx, ST_AGG);
+  if (prof) RG_CUDA(ctx, cudaEventRecord(ctx->ev[4], s));
+  if (pb) *pb = {fl, fr, sl, sr, objs, slots, res, counters, scratch, capacity};
+  return RG_OK;
+}
+
+void accumulate_profile(rg_ctx* ctx) {
+  if (!ctx->profiling) return;
+  for (int i = 0; i < 4; ++i) {
+    float ms = 0;
+    if (cudaEventElapsedTime(&ms, ctx->ev[i], ctx->ev[i + 1]) == cudaSuccess) ctx->stage_ms[i] += ms;
+  }
+  cudaGetLastError();
+}
+
+// Overflow check after an enqueued pipeline: copies the counters back,
+// waits, and on overflow grows the slot list and re-runs synchronously.
+rg_status finish_pipeline(rg_ctx* ctx, const FrameJob& J, const rg_ranger_config& cfg,
+                          cudaStream_t s, int32_t* counters, int32_t* hc, PipelineBufs* pb) {
+  for (int attempt = 0;; ++attempt) {
+    RG_CUDA(ctx, cudaMemcpyAsync(hc, counters, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    RG_CUDA(ctx, cudaStreamSynchronize(s));
+    accumulate_profile(ctx);
+    ctx->last_slots = hc[0];
+    if (!hc[1]) return RG_OK;
+    if (attempt >= 3) return set_err(ctx, RG_EOVERFLOW, "device block list overflow");
+    ctx->slot_capacity = std::max(ctx->slot_capacity * 2, hc[0] + hc[0] / 4 + 64);
+    TRY(enqueue_pipeline(ctx, J, cfg, s, counters, pb));
+  }
+}
+
+// run + overflow check (synchronous)
+rg_status run_pipeline(rg_ctx* ctx, const FrameJob& J, const rg_ranger_config& cfg, cudaStream_t s,
+                       PipelineBufs* pb) {
+  int32_t* counters = DBUF(int32_t, ctx, B_COUNTERS, 2);
+  int32_t* hc = static_cast<int32_t*>(host_buf(ctx, 0, 2 * sizeof(int32_t)));
+  NEED(counters);
+  NEED(hc);
+  TRY(enqueue_pipeline(ctx, J, cfg, s, counters, pb));
+  return finish_pipeline(ctx, J, cfg, s, counters, hc, pb);
+}
+
+}  // namespace
+
+// =========================================================== C ABI: context
+extern "C" {
+
+rg_status rg_ctx_create(int device, rg_ctx** out) {
+  if (!out) return RG_EINVAL;
+  *out = nullptr;
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0) {
+    g_create_err = std::string("no CUDA device: ") + cudaGetErrorString(e);
+    cudaGetLastError();
+    return RG_ECUDA;
+  }
+  if (device < 0 || device >= n) {
+    g_create_err = "device index out of range";
+    return RG_EINVAL;
+  }
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess || prop.major < 10) {
+    g_create_err = "device is not sm_100 (Blackwell); this library is built for sm_100a only";
+    return RG_ECUDA;
+  }
+  e = cudaSetDevice(device);
+  if (e != cudaSuccess) {
+    g_create_err = cudaGetErrorString(e);
+    return RG_ECUDA;
+  }
+  rg_ctx* c = new rg_ctx();
+  c->device = device;
+  if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) != cudaSuccess) {
+    g_create_err = "cudaStreamCreate failed";
+    delete c;
+    return RG_ECUDA;
+  }
+  for (auto& ev : c->ev) cudaEventCreate(&ev);
+  *out = c;
+  return RG_OK;
+}
+
+void rg_ctx_destroy(rg_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  for (int i = 0; i < 32; ++i)
+    if (ctx->buf[i]) cudaFree(ctx->buf[i]);
+  for (int i = 0; i < 8; ++i)
+    if (ctx->hbuf[i]) cudaFreeHost(ctx->hbuf[i]);
+  for (auto& ev : ctx->ev)
+    if (ev) cudaEventDestroy(ev);
+  cudaStreamDestroy(ctx->stream);
+  cudaStreamDestroy(ctx->copy_stream);
+  delete ctx;
+}
+
+const char* rg_last_error(const rg_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+const char* rg_create_error(void) { return g_create_err.c_str(); }
+const char* rg_build_info(void) { return RG_BUILD_INFO; }
+
+rg_status rg_set_profiling(rg_ctx* ctx, int on) {
+  if (!ctx) return RG_EINVAL;
+  ctx->profiling = on != 0;
+  return RG_OK;
+}
+
+rg_status rg_get_counters(rg_ctx* ctx, double times_ms[5], int64_t launches[5], int64_t* total) {
+  if (!ctx) return RG_EINVAL;
+  for (int i = 0; i < 5; ++i) {
+    if (times_ms) times_ms[i] = ctx->stage_ms[i];
+    if (launches) launches[i] = ctx->stage_launches[i];
+  }
+  if (total) *total = ctx->total_launches;
+  return RG_OK;
+}
+
+rg_status rg_reset_counters(rg_ctx* ctx) {
+  if (!ctx) return RG_EINVAL;
+  for (int i = 0; i < 5; ++i) {
+    ctx->stage_ms[i] = 0;
+    ctx->stage_launches[i] = 0;
+  }
+  ctx->total_launches = 0;
+  return RG_OK;
+}
+
+// =========================================================== census
+rg_status rg_census_code_at(rg_ctx* ctx, const uint8_t* img, int w, int h, int sx, int sy,
+                            uint32_t* code) {
+  TRY(bind(ctx));
+  if (!img || !code || w < 1 || h < 1) return set_err(ctx, RG_EINVAL, "census_code_at: bad image");
+  *code = 0;
+  if (sx < 2 || sy < 2 || sx >= w - 2 || sy >= h - 2) return RG_OK;  // census.hpp:44
+  uint8_t patch[25];
+  for (int j = 0; j < 5; ++j) std::memcpy(patch + 5 * j, img + (size_t)(sy - 2 + j) * w + sx - 2, 5);
+  uint8_t* d = nullptr;
+  TRY(upload_image(ctx, B_IMG_L, patch, 5, 5, &d));
+  uint32_t* full = DBUF(uint32_t, ctx, B_TMP0, 25);
+  NEED(full);
+  TRY(census_one(ctx, d, 5, 5, 5, 5, full, nullptr));
+  uint32_t out[25];
+  RG_CUDA(ctx, cudaMemcpyAsync(out, full, sizeof(out), cudaMemcpyDeviceToHost, ctx->stream));
+  RG_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  *code = out[12];
+  return RG_OK;
+}
+
+static rg_status census_common(rg_ctx* ctx, const uint8_t* img, int w, int h, int ow, int oh,
+                               const rg_rect* rois, int n_rois, bool masked, uint32_t* codes,
+                               const char* name) {
+  TRY(bind(ctx));
+  if (!img || !codes || w < 1 || h < 1) return set_err(ctx, RG_EINVAL, std::string(name) + ": bad image");
+  if (ow > w || oh > h) return set_err(ctx, RG_EINVAL, std::string(name) + ": output dims exceed source");
+  if (ow < 1 || oh < 1) return set_err(ctx, RG_EINVAL, std::string(name) + ": empty output");
+  uint8_t* d = nullptr;
+  TRY(upload_image(ctx, B_IMG_L, img, w, h, &d));
+  uint32_t* full = DBUF(uint32_t, ctx, B_TMP0, (size_t)w * h);
+  NEED(full);
+  uint32_t* red = nullptr;
+  if (ow != w || oh != h) {
+    red = DBUF(uint32_t, ctx, B_TMP1, (size_t)ow * oh);
+    NEED(red);
+  }
+  TRY(census_one(ctx, d, w, h, ow, oh, full, red));
+  uint32_t* res = red ? red : full;
+  if (masked) {
+    rg_rect* dr = DBUF(rg_rect, ctx, B_ROIS, std::max(n_rois, 1));
+    NEED(dr);
+    if (n_rois > 0)
+      RG_CUDA(ctx, cudaMemcpyAsync(dr, rois, sizeof(rg_rect) * n_rois, cudaMemcpyHostToDevice, ctx->stream));
+    RG_CUDA(ctx, launch_roi_mask(res, ow, oh, dr, n_rois, ctx->stream));
+    count_launch(ctx, ST_CENSUS);
+  }
+  RG_CUDA(ctx, cudaMemcpyAsync(codes, res, sizeof(uint32_t) * (size_t)ow * oh, cudaMemcpyDeviceToHost, ctx->stream));
+  RG_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return RG_OK;
+}
+
+rg_status rg_census_transform(rg_ctx* ctx, const uint8_t* img, int w, int h, int ow, int oh,
+                              uint32_t* codes) {
+  return census_common(ctx, img, w, h, ow, oh, nullptr, 0, false, codes, "census_transform");
+}
+
+rg_status rg_census_transform_rois(rg_ctx* ctx, const uint8_t* img, int w, int h, int ow, int oh,
+                                   const rg_rect* rois, int n_rois, uint32_t* codes) {
+  if (n_rois < 0 || (n_rois > 0 && !rois)) return set_err(ctx, RG_EINVAL, "census_transform_rois: bad rois");
+  if (ow < 1 || oh < 1) {  // reference builds an empty CensusImage (no empty-output check)
+    if (ow > w || oh > h) return set_err(ctx, RG_EINVAL, "census_transform_rois: output dims exceed source");
+    return RG_OK;
+  }
+  return census_common(ctx, img, w, h, ow, oh, rois, n_rois, true, codes, "census_transform_rois");
+}
+
+// =========================================================== matcher
+rg_status rg_match_blocks(rg_ctx* ctx, const uint32_t* left, int lw, int lh, const uint32_t* right,
+                          int rw, int rh, const int32_t* points_xy, const int64_t* offsets,
+                          const rg_search_range* ranges, int n_blocks, int mode, double tau_v,
+                          rg_match_result* out) {
+  TRY(bind(ctx));
+  if (n_blocks < 0 || (n_blocks > 0 && (!offsets || !ranges || !out)))
+    return set_err(ctx, RG_EINVAL, "match_blocks: bad arguments");
+  if (n_blocks == 0) return RG_OK;
+  if (lw < 0 || lh < 0 || rw < 0 || rh < 0) return set_err(ctx, RG_EINVAL, "match_blocks: bad raster");
+  int64_t maxp = 0;
+  for (int b = 0; b < n_blocks; ++b) {
+    const int64_t np = offsets[b + 1] - offsets[b];
+    if (np < 0) return set_err(ctx, RG_EINVAL, "match_blocks: bad offsets");
+    maxp = std::max(maxp, np);
+    if (np > 0 && (ranges[b].dx_min > ranges[b].dx_max || ranges[b].dy_min > ranges[b].dy_max))
+      return set_err(ctx, RG_EINVAL, "block_match: empty search range");  // census.hpp:182-183
+  }
+  if (match_smem_bytes((int)std::min<int64_t>(maxp, 1 << 20), false) > kSmemLimit)
+    return set_err(ctx, RG_EINVAL, "block_match: block has too many points for the device matcher");
+  const int64_t total = offsets[n_blocks] - offsets[0];
+  const size_t lsz = std::max<size_t>((size_t)lw * lh, 1), rsz = std::max<size_t>((size_t)rw * rh, 1);
+  uint32_t* dl = DBUF(uint32_t, ctx, B_CEN_FL, lsz);
+  uint32_t* dr = DBUF(uint32_t, ctx, B_CEN_FR, rsz);
+  int32_t* dp = DBUF(int32_t, ctx, B_PTS, 2 * std::max<int64_t>(total, 1));
+  int64_t* doff = DBUF(int64_t, ctx, B_OFFS, n_blocks + 1);
+  rg_search_range* drg = DBUF(rg_search_range, ctx, B_RANGES, n_blocks);
+  rg_match_result* dres = DBUF(rg_match_result, ctx, B_MRES, n_blocks);
+  NEED(dl);
+  NEED(dr);
+  NEED(dp);
+  NEED(doff);
+  NEED(drg);
+  NEED(dres);
+  cudaStream_t s = ctx->stream;
+  if ((size_t)lw * lh) RG_CUDA(ctx, cudaMemcpyAsync(dl, left, sizeof(uint32_t) * lw * lh, cudaMemcpyHostToDevice, s));
+  if ((size_t)rw * rh) RG_CUDA(ctx, cudaMemcpyAsync(dr, right, sizeof(uint32_t) * rw * rh, cudaMemcpyHostToDevice, s));
+  if (total > 0)
+    RG_CUDA(ctx, cudaMemcpyAsync(dp, points_xy + 2 * offsets[0], sizeof(int32_t) * 2 * total,
+                                 cudaMemcpyHostToDevice, s));
+  std::vector<int64_t> off0(static_cast<size_t>(n_blocks + 1));
+  for (int b = 0; b <= n_blocks; ++b) off0[b] = offsets[b] - offsets[0];
+  RG_CUDA(ctx, cudaMemcpyAsync(doff, off0.data(), sizeof(int64_t) * (n_blocks + 1), cudaMemcpyHostToDevice, s));
+  RG_CUDA(ctx, cudaMemcpyAsync(drg, ranges, sizeof(rg_search_range) * n_blocks, cudaMemcpyHostToDevice, s));
+  const Raster L = {dl, lw, lh, lw}, R = {dr, rw, rh, rw};
+  RG_CUDA(ctx, launch_match_blocks(L, R, dp, doff, drg, n_blocks, mode, tau_v, dres,
+                                   (int)std::max<int64_t>(maxp, 4), s));
+  count_launch(ctx, ST_MATCH);
+  RG_CUDA(ctx, cudaMemcpyAsync(out, dres, sizeof(rg_match_result) * n_blocks, cudaMemcpyDeviceToHost, s));
+  RG_CUDA(ctx, cudaStreamSynchronize(s));
+  return RG_OK;
+}
+
+// =========================================================== object ranger helpers
+rg_status rg_validate_ranger_config(rg_ctx* ctx, const rg_ranger_config* cfg) {
+  return check_cfg(ctx, cfg);
+}
+
+static rg_status upload_dets(rg_ctx* ctx, const rg_detection* dets, int n, rg_detection** out) {
+  rg_detection* d = DBUF(rg_detection, ctx, B_DETS, std::max(n, 1));
+  NEED(d);
+  if (n > 0)
+    RG_CUDA(ctx, cudaMemcpyAsync(d, dets, sizeof(rg_detection) * n, cudaMemcpyHostToDevice, ctx->stream));
+  *out = d;
+  return RG_OK;
+}
+
+rg_status rg_select_objects(rg_ctx* ctx, const rg_detection* dets, int n, const rg_ranger_config* cfg,
+                            int32_t* out_idx, int* n_out) {
+  TRY(bind(ctx));
+  if (!cfg || !n_out || n < 0 || (n > 0 && (!dets || !out_idx)))
+    return set_err(ctx, RG_EINVAL, "select_objects: bad arguments");
+  *n_out = 0;
+  if (n == 0 || cfg->max_objects <= 0) return RG_OK;
+  rg_detection* d = nullptr;
+  TRY(upload_dets(ctx, dets, n, &d));
+  int32_t* idx = DBUF(int32_t, ctx, B_TMP0, n + 1);
+  NEED(idx);
+  RG_CUDA(ctx, launch_select_objects(d, n, *cfg, idx, idx + n, ctx->stream));
+  count_launch(ctx, ST_PLAN);
+  std::vector<int32_t> h(static_cast<size_t>(n + 1));
+  RG_CUDA(ctx, cudaMemcpyAsync(h.data(), idx, sizeof(int32_t) * (n + 1), cudaMemcpyDeviceToHost, ctx->stream));
+  RG_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  *n_out = h[n];
+  std::copy(h.begin(), h.begin() + h[n], out_idx);
+  return RG_OK;
+}
+
+rg_status rg_find_occluders(rg_ctx* ctx, const rg_detection* dets, int n, int32_t* occ_offsets,
+                            int32_t* occ_idx) {
+  TRY(bind(ctx));
+  if (n < 0 || !occ_offsets || (n > 0 && (!dets || !occ_idx)))
+    return set_err(ctx, RG_EINVAL, "find_occluders: bad arguments");
+  occ_offsets[0] = 0;
+  if (n == 0) return RG_OK;
+  rg_detection* d = nullptr;
+  TRY(upload_dets(ctx, dets, n, &d));
+  int32_t* cnt = DBUF(int32_t, ctx, B_TMP0, n);
+  int32_t* lists = DBUF(int32_t, ctx, B_TMP1, (size_t)n * n);
+  NEED(cnt);
+  NEED(lists);
+  RG_CUDA(ctx, launch_find_occluders(d, n, cnt, lists, ctx->stream));
+  count_launch(ctx, ST_PLAN);
+  std::vector<int32_t> hc(static_cast<size_t>(n)), hl((size_t)n * n);
+  RG_CUDA(ctx, cudaMemcpyAsync(hc.data(), cnt, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, ctx->stream));
+  RG_CUDA(ctx, cudaMemcpyAsync(hl.data(), lists, sizeof(int32_t) * n * n, cudaMemcpyDeviceToHost, ctx->stream));
+  RG_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  int k = 0;
+  for (int i = 0; i < n; ++i) {
+    occ_offsets[i] = k;
+    for (int t = 0; t < hc[i]; ++t) occ_idx[k++] = hl[(size_t)i * n + t];
+  }
+  occ_offsets[n] = k;
+  return RG_OK;
+}
+
+rg_status rg_sample_query_points(rg_ctx* ctx, const rg_detection* det, int kind,
+                                 const double* occluder_boxes, int n_occ, const rg_ranger_config* cfg,
+                                 int img_w, int img_h, int64_t* block_offsets, int32_t* points_xy,
+                                 rg_search_range* ranges, int cap_blocks, int64_t cap_points,
+                                 int* n_blocks) {
+  TRY(bind(ctx));
+  if (!det || !cfg || !block_offsets || !n_blocks || n_occ < 0 || (n_occ > 0 && !occluder_boxes))
+    return set_err(ctx, RG_EINVAL, "sample_query_points: bad arguments");
+  *n_blocks = 0;
+  block_offsets[0] = 0;
+  if (cfg->close_scale < 1 || cfg->max_total_points < 0 || cfg->tau_s <= 0)
+    return set_err(ctx, RG_EINVAL, "sample_query_points: bad config");
+  // grid of sub-blocks (template_match.hpp:189-194), same IEEE ops as the device
+  int rows = 1, cols = 1;
+  if (kind != RG_KIND_FAR) {
+    const double bx0 = (det->cx - det->w / 2) * img_w, bx1 = (det->cx + det->w / 2) * img_w;
+    const double by0 = (det->cy - det->h / 2) * img_h, by1 = (det->cy + det->h / 2) * img_h;
+    const double half_tau = cfg->tau_s / 2;
+    cols = std::max(2, int((bx1 - bx0) / half_tau));
+    rows = std::max(2, int((by1 - by0) / half_tau));
+  }
+  const int cap = std::max(1, int(std::sqrt(double(cfg->max_total_points))));
+  const int q = kind == RG_KIND_FAR ? std::min(cfg->grid_side_points, cap)
+                                    : std::min(cfg->close_block_side_points, cap);
+  const int per_block = std::max(q * q, 1);
+  const int nb = rows * cols;
+  rg_detection* d = nullptr;
+  TRY(upload_dets(ctx, det, 1, &d));
+  double* docc = DBUF(double, ctx, B_TMP2, 4 * std::max(n_occ, 1));
+  int32_t* pts = DBUF(int32_t, ctx, B_TMP0, 2 * (size_t)nb * per_block);
+  int32_t* cnt = DBUF(int32_t, ctx, B_TMP1, nb);
+  NEED(docc);
+  NEED(pts);
+  NEED(cnt);
+  if (n_occ > 0)
+    RG_CUDA(ctx, cudaMemcpyAsync(docc, occluder_boxes, sizeof(double) * 4 * n_occ, cudaMemcpyHostToDevice, ctx->stream));
+  RG_CUDA(ctx, launch_sample_blocks(d, kind, docc, n_occ, *cfg, img_w, img_h, rows, cols, pts, cnt,
+                                    per_block, ctx->stream));
+  count_launch(ctx, ST_PLAN);
+  std::vector<int32_t> hp(2 * (size_t)nb * per_block), hcnt(static_cast<size_t>(nb));
+  RG_CUDA(ctx, cudaMemcpyAsync(hp.data(), pts, sizeof(int32_t) * hp.size(), cudaMemcpyDeviceToHost, ctx->stream));
+  RG_CUDA(ctx, cudaMemcpyAsync(hcnt.data(), cnt, sizeof(int32_t) * nb, cudaMemcpyDeviceToHost, ctx->stream));
+  RG_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  const int s = cfg->close_scale;
+  int out_b = 0;
+  int64_t np = 0;
+  for (int b = 0; b < nb; ++b) {
+    if (hcnt[b] < 4) continue;  // template_match.hpp:185, 219
+    if (out_b >= cap_blocks || np + hcnt[b] > cap_points)
+      return set_err(ctx, RG_EOVERFLOW, "sample_query_points: output capacity");
+    for (int k = 0; k < hcnt[b]; ++k) {
+      points_xy[2 * (np + k)] = hp[2 * ((size_t)b * per_block + k)];
+      points_xy[2 * (np + k) + 1] = hp[2 * ((size_t)b * per_block + k) + 1];
+    }
+    np += hcnt[b];
+    ranges[out_b] = kind == RG_KIND_FAR ? rg_search_range{0, cfg->dx_max_far, -1, 1}
+                                        : rg_search_range{0, (cfg->dx_max_close + s - 1) / s, -1, 1};
+    block_offsets[++out_b] = np;
+  }
+  *n_blocks = out_b;
+  return RG_OK;
+}
+
+rg_status rg_aggregate_close_disparities(rg_ctx* ctx, const double* disps, int n, double tau_d,
+                                         int n_min, int32_t* valid, double* disparity,
+                                         int32_t* run_length) {
+  TRY(bind(ctx));
+  if (n < 0 || (n > 0 && !disps) || !valid || !disparity || !run_length)
+    return set_err(ctx, RG_EINVAL, "aggregate_close_disparities: bad arguments");
+  double* dv = DBUF(double, ctx, B_TMP2, std::max(n, 1));
+  double* scratch = DBUF(double, ctx, B_TMP3, std::max(n, 1));
+  int32_t* oi = DBUF(int32_t, ctx, B_TMP0, 2);
+  double* od = DBUF(double, ctx, B_TMP1, 1);
+  NEED(dv);
+  NEED(scratch);
+  NEED(oi);
+  NEED(od);
+  if (n > 0) RG_CUDA(ctx, cudaMemcpyAsync(dv, disps, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+  RG_CUDA(ctx, launch_aggregate_values(dv, n, tau_d, n_min, scratch, oi, od, ctx->stream));
+  count_launch(ctx, ST_AGG);
+  int32_t hi[2];
+  double hd;
+  RG_CUDA(ctx, cudaMemcpyAsync(hi, oi, sizeof(hi), cudaMemcpyDeviceToHost, ctx->stream));
+  RG_CUDA(ctx, cudaMemcpyAsync(&hd, od, sizeof(hd), cudaMemcpyDeviceToHost, ctx->stream));
+  RG_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  *valid = hi[0];
+  *run_length = hi[1];
+  *disparity = hd;
+  return RG_OK;
+}
+
+// =========================================================== estimate_object_disparities
+rg_status rg_estimate_object_disparities(rg_ctx* ctx, const uint8_t* left, const uint8_t* right, int w,
+                                         int h, const rg_detection* dets, int n_dets,
+                                         const rg_ranger_config* cfg, rg_census_cache* cache,
+                                         double focal_px, double baseline_m, rg_object_disparity* out,
+                                         int* n_out, rg_ranger_stats* stats) {
+  TRY(bind(ctx));
+  TRY(check_cfg(ctx, cfg));
+  if (!left || !right || !n_out || w < 1 || h < 1 || n_dets < 0 || (n_dets > 0 && (!dets || !out)))
+    return set_err(ctx, RG_EINVAL, "estimate_object_disparities: bad arguments");
+  *n_out = 0;
+  if (stats) {
+    stats->query_points = 0;
+    stats->image_pixels = (int64_t)w * h;
+    stats->n_far = stats->n_close = 0;
+  }
+  if (n_dets == 0) return RG_OK;  // template_match.hpp:275
+  if (n_dets > 4096) return set_err(ctx, RG_EINVAL, "estimate_object_disparities: > 4096 detections per frame");
+  const int s = cfg->close_scale, cw = w / s, ch = h / s;
+  cudaStream_t st = ctx->stream;
+  uint8_t *dl = nullptr, *dr = nullptr;
+  TRY(upload_image(ctx, B_IMG_L, left, w, h, &dl));
+  TRY(upload_image(ctx, B_IMG_R, right, w, h, &dr));
+  rg_detection* dd = nullptr;
+  TRY(upload_dets(ctx, dets, n_dets, &dd));
+  int32_t* doff = DBUF(int32_t, ctx, B_DET_OFF, 2);
+  const int out_stride = std::max(1, std::min(n_dets, cfg->max_objects));
+  rg_object_disparity* dout = DBUF(rg_object_disparity, ctx, B_OUT, out_stride);
+  int32_t* dcnt = DBUF(int32_t, ctx, B_OUT_CNT, 1);
+  rg_ranger_stats* dstats = DBUF(rg_ranger_stats, ctx, B_STATS, 1);
+  NEED(doff);
+  NEED(dout);
+  NEED(dcnt);
+  NEED(dstats);
+  const int32_t hoff[2] = {0, n_dets};
+  RG_CUDA(ctx, cudaMemcpyAsync(doff, hoff, sizeof(hoff), cudaMemcpyHostToDevice, st));
+  FrameJob J = {dl, dr, 1, w, h, w, (int64_t)w * h, dd, doff, out_stride, dout, dcnt, dstats,
+                focal_px, baseline_m};
+  // a pre-filled cache is used as-is (template_match.hpp:312, 317)
+  uint32_t* cache_dev = nullptr;
+  if (cache && (cache->has_full || cache->has_scaled)) {
+    const size_t fsz = (size_t)w * h, ssz = (size_t)std::max(cw, 0) * std::max(ch, 0);
+    cache_dev = DBUF(uint32_t, ctx, B_TMP2, 2 * fsz + 2 * ssz + 1);
+    NEED(cache_dev);
+    if (cache->has_full) {
+      RG_CUDA(ctx, cudaMemcpyAsync(cache_dev, cache->full_left, 4 * fsz, cudaMemcpyHostToDevice, st));
+      RG_CUDA(ctx, cudaMemcpyAsync(cache_dev + fsz, cache->full_right, 4 * fsz, cudaMemcpyHostToDevice, st));
+      J.full_l = cache_dev;
+      J.full_r = cache_dev + fsz;
+    }
+    if (cache->has_scaled && ssz) {
+      RG_CUDA(ctx, cudaMemcpyAsync(cache_dev + 2 * fsz, cache->scaled_left, 4 * ssz, cudaMemcpyHostToDevice, st));
+      RG_CUDA(ctx, cudaMemcpyAsync(cache_dev + 2 * fsz + ssz, cache->scaled_right, 4 * ssz, cudaMemcpyHostToDevice, st));
+      J.scaled_l = cache_dev + 2 * fsz;
+      J.scaled_r = cache_dev + 2 * fsz + ssz;
+    }
+  }
+  PipelineBufs pb;
+  TRY(run_pipeline(ctx, J, *cfg, st, &pb));
+  int32_t hcnt = 0;
+  RG_CUDA(ctx, cudaMemcpyAsync(&hcnt, dcnt, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  RG_CUDA(ctx, cudaStreamSynchronize(st));
+  RG_CUDA(ctx, cudaMemcpyAsync(out, dout, sizeof(rg_object_disparity) * hcnt, cudaMemcpyDeviceToHost, st));
+  rg_ranger_stats hs;
+  RG_CUDA(ctx, cudaMemcpyAsync(&hs, dstats, sizeof(hs), cudaMemcpyDeviceToHost, st));
+  RG_CUDA(ctx, cudaStreamSynchronize(st));
+  *n_out = hcnt;
+  if (stats) *stats = hs;
+
+  // fill an empty cache with ROI-masked codes (template_match.hpp:304-321)
+  if (cache && (!cache->has_full || !cache->has_scaled)) {
+    const int nslots = (int)ctx->last_slots;
+    std::vector<ObjEntry> objs(static_cast<size_t>(hcnt));
+    std::vector<rg_match_result> res(static_cast<size_t>(std::max(nslots, 1)));
+    if (hcnt > 0)
+      RG_CUDA(ctx, cudaMemcpyAsync(objs.data(), pb.objs, sizeof(ObjEntry) * hcnt, cudaMemcpyDeviceToHost, st));
+    if (nslots > 0)
+      RG_CUDA(ctx, cudaMemcpyAsync(res.data(), pb.res, sizeof(rg_match_result) * nslots, cudaMemcpyDeviceToHost, st));
+    RG_CUDA(ctx, cudaStreamSynchronize(st));
+    bool any_far = false, any_close = false;
+    std::vector<rg_rect> far_rois, sc_rois;
+    const int dxs = (cfg->dx_max_close + s - 1) / s;
+    for (const ObjEntry& e : objs) {
+      bool has_block = false;
+      for (int t = 0; t < e.n_slots; ++t) has_block |= res[e.slot_base + t].n_points >= 4;
+      const rg_detection& dt = dets[e.det];
+      const double bx0 = (dt.cx - dt.w / 2) * w, bx1 = (dt.cx + dt.w / 2) * w;
+      const double by0 = (dt.cy - dt.h / 2) * h, by1 = (dt.cy + dt.h / 2) * h;
+      auto add_roi = [](std::vector<rg_rect>& v, double x0, double y0, double x1, double y1,
+                        double sx, double sy, int dilx, int dily, int ww, int hh) {
+        rg_rect r;  // template_match.hpp:245-253
+        r.x0 = std::max(0, int(std::floor(x0 * sx)) - dilx);
+        r.x1 = std::min(ww, int(std::ceil(x1 * sx)) + dilx + 1);
+        r.y0 = std::max(0, int(std::floor(y0 * sy)) - dily);
+        r.y1 = std::min(hh, int(std::ceil(y1 * sy)) + dily + 1);
+        v.push_back(r);
+      };
+      if (e.kind == RG_KIND_FAR) {
+        any_far |= has_block;
+        add_roi(far_rois, bx0, by0, bx1, by1, 1, 1, cfg->dx_max_far + 2, 3, w, h);
+      } else {
+        any_close |= has_block;
+        add_roi(sc_rois, bx0, by0, bx1, by1, double(cw) / w, double(ch) / h, dxs + 2, 3, cw, ch);
+      }
+    }
+    auto fill = [&](const uint32_t* src, int ww, int hh, const std::vector<rg_rect>& rois,
+                    uint32_t* host) -> rg_status {
+      uint32_t* tmp = DBUF(uint32_t, ctx, B_TMP1, (size_t)ww * hh);
+      rg_rect* dro = DBUF(rg_rect, ctx, B_ROIS, std::max<size_t>(rois.size(), 1));
+      NEED(tmp);
+      NEED(dro);
+      RG_CUDA(ctx, cudaMemcpyAsync(tmp, src, 4 * (size_t)ww * hh, cudaMemcpyDeviceToDevice, st));
+      if (!rois.empty())
+        RG_CUDA(ctx, cudaMemcpyAsync(dro, rois.data(), sizeof(rg_rect) * rois.size(), cudaMemcpyHostToDevice, st));
+      RG_CUDA(ctx, launch_roi_mask(tmp, ww, hh, dro, (int)rois.size(), st));
+      count_launch(ctx, ST_CENSUS);
+      RG_CUDA(ctx, cudaMemcpyAsync(host, tmp, 4 * (size_t)ww * hh, cudaMemcpyDeviceToHost, st));
+      RG_CUDA(ctx, cudaStreamSynchronize(st));
+      return RG_OK;
+    };
+    if (!cache->has_full && any_far) {
+      TRY(fill(pb.fl, w, h, far_rois, cache->full_left));
+      TRY(fill(pb.fr, w, h, far_rois, cache->full_right));
+      cache->has_full = 1;
+    }
+    if (!cache->has_scaled && any_close) {
+      TRY(fill(pb.sl, cw, ch, sc_rois, cache->scaled_left));
+      TRY(fill(pb.sr, cw, ch, sc_rois, cache->scaled_right));
+      cache->has_scaled = 1;
+    }
+  }
+  return RG_OK;
+}
+
+// =========================================================== batched frames
+rg_status rg_range_frames(rg_ctx* ctx, const rg_frame_batch* b, const rg_ranger_config* cfg,
+                          void* stream) {
+  TRY(bind(ctx));
+  TRY(check_cfg(ctx, cfg));
+  if (!b || b->n_frames < 0 || b->width < 1 || b->height < 1 || b->pitch < b->width)
+    return set_err(ctx, RG_EINVAL, "range_frames: bad batch");
+  if (b->n_frames == 0) return RG_OK;
+  if (b->max_dets_per_frame > 4096) return set_err(ctx, RG_EINVAL, "range_frames: > 4096 detections per frame");
+  if (b->out_stride < std::min(b->max_dets_per_frame, cfg->max_objects))
+    return set_err(ctx, RG_EINVAL, "range_frames: out_stride too small");
+  FrameJob J = {b->d_left, b->d_right, b->n_frames, b->width, b->height, b->pitch, b->frame_stride,
+                b->d_dets, b->d_det_offsets, b->out_stride, b->d_out, b->d_out_count, nullptr,
+                b->focal_px, b->baseline_m};
+  cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+  return run_pipeline(ctx, J, *cfg, s, nullptr);
+}
+
+rg_status rg_range_frames_host(rg_ctx* ctx, const rg_frame_batch* b, const rg_ranger_config* cfg,
+                               int chunk, void* stream) {
+  TRY(bind(ctx));
+  TRY(check_cfg(ctx, cfg));
+  if (!b || b->n_frames < 0 || b->width < 1 || b->height < 1 || b->pitch < b->width)
+    return set_err(ctx, RG_EINVAL, "range_frames_host: bad batch");
+  if (b->n_frames == 0) return RG_OK;
+  if (b->max_dets_per_frame > 4096) return set_err(ctx, RG_EINVAL, "range_frames_host: > 4096 detections per frame");
+  if (b->out_stride < std::min(b->max_dets_per_frame, cfg->max_objects))
+    return set_err(ctx, RG_EINVAL, "range_frames_host: out_stride too small");
+  if (chunk < 1) chunk = 16;
+  const int F = b->n_frames;
+  // compute on `stream` (or the context stream), H2D staging on copy_stream
+  cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+  cudaStream_t cs = ctx->copy_stream;
+  const size_t img_bytes = (size_t)b->pitch * b->height;
+  const int32_t* hoff = b->d_det_offsets;  // host pointers in this variant
+  int max_chunk_dets = 1;
+  for (int c0 = 0; c0 < F; c0 += chunk)
+    max_chunk_dets = std::max(max_chunk_dets, hoff[std::min(F, c0 + chunk)] - hoff[c0]);
+  // double-buffered device staging: images, detections, offsets, results
+  uint8_t* st_l = DBUF(uint8_t, ctx, B_STAGE_L, 2 * img_bytes * chunk);
+  uint8_t* st_r = DBUF(uint8_t, ctx, B_STAGE_R, 2 * img_bytes * chunk);
+  rg_detection* st_d = DBUF(rg_detection, ctx, B_DETS, 2 * (size_t)max_chunk_dets);
+  int32_t* st_o = DBUF(int32_t, ctx, B_DET_OFF, 2 * (size_t)(chunk + 1));
+  rg_object_disparity* st_out = DBUF(rg_object_disparity, ctx, B_OUT, 2 * (size_t)chunk * b->out_stride);
+  int32_t* st_cnt = DBUF(int32_t, ctx, B_OUT_CNT, 2 * (size_t)chunk);
+  int32_t* counters = DBUF(int32_t, ctx, B_COUNTERS, 2);
+  int32_t* hoffs = static_cast<int32_t*>(host_buf(ctx, 1, sizeof(int32_t) * 2 * (chunk + 1)));
+  int32_t* hc = static_cast<int32_t*>(host_buf(ctx, 0, 2 * sizeof(int32_t)));
+  NEED(st_l);
+  NEED(st_r);
+  NEED(st_d);
+  NEED(st_o);
+  NEED(st_out);
+  NEED(st_cnt);
+  NEED(counters);
+  NEED(hoffs);
+  NEED(hc);
+  cudaEvent_t ready[2] = {ctx->ev[6], ctx->ev[7]}, done[2] = {ctx->ev[8], ctx->ev[9]};
+  auto stage = [&](int c0, int k) -> rg_status {  // H2D of one chunk into slot k
+    const int n = std::min(chunk, F - c0);
+    int32_t* ho = hoffs + k * (chunk + 1);
+    for (int i = 0; i <= n; ++i) ho[i] = hoff[c0 + i] - hoff[c0];
+    const size_t stride = (size_t)b->frame_stride;
+    uint8_t* dl = st_l + (size_t)k * img_bytes * chunk;
+    uint8_t* dr = st_r + (size_t)k * img_bytes * chunk;
+    if (stride == img_bytes) {
+      RG_CUDA(ctx, cudaMemcpyAsync(dl, b->d_left + c0 * stride, img_bytes * n, cudaMemcpyHostToDevice, cs));
+      RG_CUDA(ctx, cudaMemcpyAsync(dr, b->d_right + c0 * stride, img_bytes * n, cudaMemcpyHostToDevice, cs));
+    } else {
+      for (int i = 0; i < n; ++i) {
+        RG_CUDA(ctx, cudaMemcpyAsync(dl + i * img_bytes, b->d_left + (c0 + i) * stride, img_bytes, cudaMemcpyHostToDevice, cs));
+        RG_CUDA(ctx, cudaMemcpyAsync(dr + i * img_bytes, b->d_right + (c0 + i) * stride, img_bytes, cudaMemcpyHostToDevice, cs));
+      }
+    }
+    if (ho[n] > 0)
+      RG_CUDA(ctx, cudaMemcpyAsync(st_d + (size_t)k * max_chunk_dets, b->d_dets + hoff[c0],
+                                   sizeof(rg_detection) * ho[n], cudaMemcpyHostToDevice, cs));
+    RG_CUDA(ctx, cudaMemcpyAsync(st_o + k * (chunk + 1), ho, sizeof(int32_t) * (n + 1), cudaMemcpyHostToDevice, cs));
+    RG_CUDA(ctx, cudaEventRecord(ready[k], cs));
+    return RG_OK;
+  };
+  TRY(stage(0, 0));
+  for (int c0 = 0, it = 0; c0 < F; c0 += chunk, ++it) {
+    const int k = it & 1, n = std::min(chunk, F - c0);
+    RG_CUDA(ctx, cudaStreamWaitEvent(s, ready[k], 0));
+    FrameJob J = {st_l + (size_t)k * img_bytes * chunk, st_r + (size_t)k * img_bytes * chunk, n, b->width,
+                  b->height, b->pitch, (int64_t)img_bytes, st_d + (size_t)k * max_chunk_dets,
+                  st_o + k * (chunk + 1), b->out_stride, st_out + (size_t)k * chunk * b->out_stride,
+                  st_cnt + (size_t)k * chunk, nullptr, b->focal_px, b->baseline_m};
+    TRY(enqueue_pipeline(ctx, J, *cfg, s, counters, nullptr));
+    RG_CUDA(ctx, cudaEventRecord(done[k], s));
+    // prefetch the next chunk into the other slot once its previous user is done
+    if (c0 + chunk < F) {
+      if (it >= 1) RG_CUDA(ctx, cudaStreamWaitEvent(cs, done[k ^ 1], 0));
+      TRY(stage(c0 + chunk, k ^ 1));
+    }
+    TRY(finish_pipeline(ctx, J, *cfg, s, counters, hc, nullptr));
+    RG_CUDA(ctx, cudaMemcpyAsync(b->d_out + (size_t)c0 * b->out_stride, J.out,
+                                 sizeof(rg_object_disparity) * (size_t)n * b->out_stride,
+                                 cudaMemcpyDeviceToHost, s));
+    RG_CUDA(ctx, cudaMemcpyAsync(b->d_out_count + c0, J.out_count, sizeof(int32_t) * n,
+                                 cudaMemcpyDeviceToHost, s));
+  }
+  RG_CUDA(ctx, cudaStreamSynchronize(s));
+  RG_CUDA(ctx, cudaStreamSynchronize(cs));
+  return RG_OK;
+}
+
+// =========================================================== BM / autorect
+rg_status rg_validate_bm_params(rg_ctx* ctx, const rg_bm_params* p) { return check_bm(ctx, p); }
+
+// bm_disparity on device images (w x h, packed) into device raw (w x h)
+static rg_status bm_device(rg_ctx* ctx, const uint8_t* dl, const uint8_t* dr, int w, int h,
+                           const rg_bm_params& p, int16_t* draw, cudaStream_t st) {
+  const int s = p.downscale;
+  if (s == 1) {
+    RG_CUDA(ctx, launch_bm(dl, dr, 1, 0, w, h, w, h, 0, 0, 0, 1, p, draw, nullptr, st));
+    count_launch(ctx, ST_RECT);
+    return RG_OK;
+  }
+  const int ow = w / s, oh = h / s;  // image.hpp:98-105
+  if (ow < 1 || oh < 1) return set_err(ctx, RG_EINVAL, "downscale: output would be empty");
+  rg_bm_params q = p;  // bm.hpp:121-125
+  q.downscale = 1;
+  q.min_disparity = (p.min_disparity + s - 1) / s;
+  q.num_disparities = std::max(1, (p.min_disparity + p.num_disparities) / s - q.min_disparity);
+  uint8_t* ql = DBUF(uint8_t, ctx, B_TMP0, (size_t)ow * oh);
+  uint8_t* qr = DBUF(uint8_t, ctx, B_TMP1, (size_t)ow * oh);
+  int16_t* qm = DBUF(int16_t, ctx, B_TMP2, (size_t)ow * oh);
+  NEED(ql);
+  NEED(qr);
+  NEED(qm);
+  RG_CUDA(ctx, launch_downscale(dl, w, h, s, ql, st));
+  RG_CUDA(ctx, launch_downscale(dr, w, h, s, qr, st));
+  RG_CUDA(ctx, launch_bm(ql, qr, 1, 0, ow, oh, ow, oh, 0, 0, 0, 1, q, qm, nullptr, st));
+  RG_CUDA(ctx, launch_upscale(qm, ow, oh, s, q.min_disparity * 16 * s, draw, w, h, st));
+  count_launch(ctx, ST_RECT, 4);
+  return RG_OK;
+}
+
+rg_status rg_bm_disparity(rg_ctx* ctx, const uint8_t* left, const uint8_t* right, int w, int h,
+                          const rg_bm_params* p, int16_t* out_raw) {
+  TRY(bind(ctx));
+  TRY(check_bm(ctx, p));
+  if (!left || !right || !out_raw || w < 1 || h < 1)
+    return set_err(ctx, RG_EINVAL, "bm_disparity: bad arguments");
+  uint8_t *dl = nullptr, *dr = nullptr;
+  TRY(upload_image(ctx, B_BM_L, left, w, h, &dl));
+  TRY(upload_image(ctx, B_BM_R, right, w, h, &dr));
+  int16_t* draw = DBUF(int16_t, ctx, B_BM_OUT, (size_t)w * h);
+  NEED(draw);
+  TRY(bm_device(ctx, dl, dr, w, h, *p, draw, ctx->stream));
+  RG_CUDA(ctx, cudaMemcpyAsync(out_raw, draw, sizeof(int16_t) * w * h, cudaMemcpyDeviceToHost, ctx->stream));
+  RG_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return RG_OK;
+}
+
+static rg_status check_rect(rg_ctx* ctx, int w, int h, const rg_rect* roi, int dmin, int dmax,
+                            const rg_bm_params* p) {  // autorect.hpp:25-32
+  if (!roi || !p) return set_err(ctx, RG_EINVAL, "auto_rect_search: null argument");
+  if (roi->x1 - roi->x0 < p->block_size || roi->y1 - roi->y0 < p->block_size)
+    return set_err(ctx, RG_EINVAL, "auto_rect_search: ROI smaller than the match window");
+  if (roi->x0 < 0 || roi->y0 < 0 || roi->x1 > w || roi->y1 > h)
+    return set_err(ctx, RG_EINVAL, "auto_rect_search: ROI leaves the image");
+  if (dmin > dmax) return set_err(ctx, RG_EINVAL, "auto_rect_search: empty delta range");
+  return check_bm(ctx, p);
+}
+
+rg_status rg_auto_rect_search(rg_ctx* ctx, const uint8_t* left, const uint8_t* right, int w, int h,
+                              const rg_rect* roi, int delta_min, int delta_max, const rg_bm_params* p,
+                              int32_t* best_delta, int64_t* counts) {
+  TRY(bind(ctx));
+  if (!left || !right || !best_delta || w < 1 || h < 1)
+    return set_err(ctx, RG_EINVAL, "auto_rect_search: bad arguments");
+  TRY(check_rect(ctx, w, h, roi, delta_min, delta_max, p));
+  uint8_t *dl = nullptr, *dr = nullptr;
+  TRY(upload_image(ctx, B_BM_L, left, w, h, &dl));
+  TRY(upload_image(ctx, B_BM_R, right, w, h, &dr));
+  const int nd = delta_max - delta_min + 1;
+  int64_t* dc = DBUF(int64_t, ctx, B_BM_CNT, nd);
+  int32_t* db = DBUF(int32_t, ctx, B_TMP3, 1);
+  NEED(dc);
+  NEED(db);
+  cudaStream_t st = ctx->stream;
+  RG_CUDA(ctx, cudaMemsetAsync(dc, 0, sizeof(int64_t) * nd, st));
+  const int rw = roi->x1 - roi->x0, rh = roi->y1 - roi->y0;
+  if (p->downscale == 1) {
+    RG_CUDA(ctx, launch_bm(dl, dr, 1, 0, w, h, rw, rh, roi->x0, roi->y0, delta_min, nd, *p, nullptr, dc, st));
+    count_launch(ctx, ST_RECT);
+  } else {  // per delta: shifted crop -> bm_disparity (downscale path) -> count
+    std::vector<int64_t> hc(static_cast<size_t>(nd));
+    std::vector<int16_t> raw((size_t)rw * rh);
+    std::vector<uint8_t> lc((size_t)rw * rh), rc((size_t)rw * rh);
+    for (int y = 0; y < rh; ++y) std::memcpy(&rc[(size_t)y * rw], right + (size_t)(roi->y0 + y) * w + roi->x0, rw);
+    uint8_t *cl = nullptr, *cr = nullptr;
+    TRY(upload_image(ctx, B_STAGE_R, rc.data(), rw, rh, &cr));
+    int16_t* draw = DBUF(int16_t, ctx, B_BM_OUT, (size_t)rw * rh);
+    NEED(draw);
+    for (int k = 0; k < nd; ++k) {
+      const int delta = delta_min + k;
+      for (int y = 0; y < rh; ++y) {
+        int sy = roi->y0 + y - delta;
+        sy = sy < 0 ? 0 : (sy >= h ? h - 1 : sy);
+        std::memcpy(&lc[(size_t)y * rw], left + (size_t)sy * w + roi->x0, rw);
+      }
+      TRY(upload_image(ctx, B_STAGE_L, lc.data(), rw, rh, &cl));
+      TRY(bm_device(ctx, cl, cr, rw, rh, *p, draw, st));
+      RG_CUDA(ctx, cudaMemcpyAsync(raw.data(), draw, sizeof(int16_t) * raw.size(), cudaMemcpyDeviceToHost, st));
+      RG_CUDA(ctx, cudaStreamSynchronize(st));
+      int64_t c = 0;
+      const int lo = p->min_disparity * 16;
+      for (int16_t v : raw) c += (v != -32768 && v > lo);
+      hc[k] = c;
+    }
+    RG_CUDA(ctx, cudaMemcpyAsync(dc, hc.data(), sizeof(int64_t) * nd, cudaMemcpyHostToDevice, st));
+  }
+  RG_CUDA(ctx, launch_autorect_pick(dc, 1, delta_min, nd, db, st));
+  count_launch(ctx, ST_RECT);
+  RG_CUDA(ctx, cudaMemcpyAsync(best_delta, db, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  if (counts) RG_CUDA(ctx, cudaMemcpyAsync(counts, dc, sizeof(int64_t) * nd, cudaMemcpyDeviceToHost, st));
+  RG_CUDA(ctx, cudaStreamSynchronize(st));
+  return RG_OK;
+}
+
+rg_status rg_auto_rect_frames(rg_ctx* ctx, const uint8_t* d_left, const uint8_t* d_right, int n_frames,
+                              int64_t frame_stride, int pitch, int w, int h, const rg_rect* roi,
+                              int delta_min, int delta_max, const rg_bm_params* p, int32_t* d_best,
+                              int64_t* d_counts, void* stream) {
+  TRY(bind(ctx));
+  if (!d_left || !d_right || !d_best || n_frames < 0 || w < 1 || h < 1 || pitch < w)
+    return set_err(ctx, RG_EINVAL, "auto_rect_frames: bad arguments");
+  TRY(check_rect(ctx, w, h, roi, delta_min, delta_max, p));
+  if (p->downscale != 1) return set_err(ctx, RG_EINVAL, "auto_rect_frames: downscale must be 1 (use rg_auto_rect_search)");
+  if (n_frames == 0) return RG_OK;
+  const int nd = delta_max - delta_min + 1;
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+  int64_t* dc = d_counts;
+  if (!dc) {
+    dc = DBUF(int64_t, ctx, B_BM_CNT, (size_t)n_frames * nd);
+    NEED(dc);
+  }
+  if (ctx->profiling) RG_CUDA(ctx, cudaEventRecord(ctx->ev[10], st));
+  RG_CUDA(ctx, cudaMemsetAsync(dc, 0, sizeof(int64_t) * n_frames * nd, st));
+  RG_CUDA(ctx, launch_bm(d_left, d_right, n_frames, frame_stride, pitch, h, roi->x1 - roi->x0,
+                         roi->y1 - roi->y0, roi->x0, roi->y0, delta_min, nd, *p, nullptr, dc, st));
+  RG_CUDA(ctx, launch_autorect_pick(dc, n_frames, delta_min, nd, d_best, st));
+  count_launch(ctx, ST_RECT, 2);
+  if (ctx->profiling) {
+    RG_CUDA(ctx, cudaEventRecord(ctx->ev[11], st));
+    RG_CUDA(ctx, cudaEventSynchronize(ctx->ev[11]));
+    float ms = 0;
+    if (cudaEventElapsedTime(&ms, ctx->ev[10], ctx->ev[11]) == cudaSuccess) ctx->stage_ms[ST_RECT] += ms;
+  }
+  return RG_OK;
+}
+
+}  // extern "C"

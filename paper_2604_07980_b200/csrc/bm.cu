@@ -1,0 +1,289 @@
+// bm.cu -- K5: SAD block matcher and the auto-rectification offset search.
+//
+// Replaces bm_disparity_at_scale / bm_disparity (reference bm.hpp:37-135),
+// downscale / upscale_disparity (image.hpp:98-141) and the per-delta body of
+// auto_rect_search (autorect.hpp:37-44).  The vertical offset delta is a grid
+// dimension: CTA (tile, frame*n_delta + k) matches the ROI crop of the left
+// image shifted by delta_min + k rows (edge-row clamp, image.hpp:145-154)
+// against the unshifted right crop, entirely in crop-local coordinates
+// (bm.hpp:47-61).  Per disparity the 9x9 SAD is a separable box sum:
+// column sums staged in shared memory, then a running row sum per thread.
+// The per-pixel winner is tracked in streaming form over increasing d:
+// first minimum, its two neighbours, and the second best over |i-best| > 1
+// (via the prefix minimum lagging two indices behind) -- exactly the
+// reference's rules (bm.hpp:75-92).  Valid counts (raw > 16*d_min) are
+// reduced per CTA and added with one integer atomic (deterministic).
+#include "rg_common.cuh"
+
+namespace rg {
+namespace {
+
+constexpr int BT = 256;  // threads
+constexpr int TXB = 64;  // tile columns (8 threads x 8 pixels)
+constexpr int TYB = 32;  // tile rows
+constexpr int kInvalid = -32768;
+constexpr int kBig = 0x7fffffff;
+
+__device__ __forceinline__ double subpix(double cm, double c0, double cp) {  // census.hpp:167-171
+  const double denom = __dsub_rn(__dadd_rn(cm, cp), __dmul_rn(2.0, c0));
+  if (denom <= 0.0) return 0.0;
+  return __ddiv_rn(-__dsub_rn(cp, cm), __dmul_rn(2.0, denom));
+}
+
+// Dynamic smem: L tile [(TYB+2hw) x LW], R tile [(TYB+2hw) x RW], column sums
+// [TYB x CW] ints.
+__global__ void __launch_bounds__(BT) bm_kernel(const uint8_t* __restrict__ left,
+                                                const uint8_t* __restrict__ right, int64_t stride,
+                                                int pitch, int img_h, int W, int H, int x0c,
+                                                int y0c, int delta_min, int n_delta, int bs,
+                                                int d_lo, int nd, double tex, double uniq,
+                                                int16_t* __restrict__ raw,
+                                                int64_t* __restrict__ counts) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int hw = bs / 2;
+  const int frame = blockIdx.z / n_delta, kd = blockIdx.z - frame * n_delta;
+  const int delta = delta_min + kd;
+  const uint8_t* Limg = left + (int64_t)frame * stride;
+  const uint8_t* Rimg = right + (int64_t)frame * stride;
+  const int tx0 = blockIdx.x * TXB, ty0 = blockIdx.y * TYB;
+  const int d_hi = d_lo + nd;
+  const int TR = TYB + 2 * hw;              // tile rows incl. halo
+  const int LW = TXB + 2 * hw;              // left tile columns
+  const int lx0 = tx0 - hw;                 // crop column of L tile col 0
+  const int rx0 = tx0 - hw - (d_hi - 1);    // crop column of R tile col 0
+  const int RW = TXB + 2 * hw + nd - 1;
+  const int CW = LW;                        // column sums per row
+  uint8_t* Lt = smem;
+  uint8_t* Rt = Lt + TR * LW;
+  int* cs = reinterpret_cast<int*>(smem + (((TR * (LW + RW)) + 15) & ~15));
+
+  // stage crops: left rows shifted by delta with edge clamp, right unshifted;
+  // values outside the crop are never used by a defined pixel
+  for (int i = threadIdx.x; i < TR * LW; i += BT) {
+    const int r = i / LW, c = i - r * LW;
+    const int cy = ty0 - hw + r, cx = lx0 + c;
+    uint8_t v = 0;
+    if (cy >= 0 && cy < H && cx >= 0 && cx < W) {
+      int sy = y0c + cy - delta;
+      sy = sy < 0 ? 0 : (sy >= img_h ? img_h - 1 : sy);
+      v = Limg[(int64_t)sy * pitch + x0c + cx];
+    }
+    Lt[i] = v;
+  }
+  for (int i = threadIdx.x; i < TR * RW; i += BT) {
+    const int r = i / RW, c = i - r * RW;
+    const int cy = ty0 - hw + r, cx = rx0 + c;
+    uint8_t v = 0;
+    if (cy >= 0 && cy < H && cx >= 0 && cx < W) v = Rimg[(int64_t)(y0c + cy) * pitch + x0c + cx];
+    Rt[i] = v;
+  }
+  __syncthreads();
+
+  // this thread's 8 pixels: one row, 8 consecutive columns
+  const int seg = threadIdx.x & 7, row = threadIdx.x >> 3;
+  const int y = ty0 + row;
+  const int xs = tx0 + seg * 8;
+  // per-pixel streaming state
+  int best[8], bi[8], second[8], cmv[8], cpv[8], last[8], pm2[8], neval[8];
+  bool defined[8];
+#pragma unroll
+  for (int p = 0; p < 8; ++p) {
+    const int x = xs + p;
+    defined[p] = x >= hw && x < W - hw && y >= hw && y < H - hw;
+    if (defined[p]) {  // texture gate, bm.hpp:50-56
+      long grad = 0;
+      const int lc = x - lx0;
+      for (int j = -hw; j <= hw; ++j) {
+        const uint8_t* r = Lt + (row + hw + j) * LW + lc;
+        for (int i = -hw; i < hw; ++i) grad += abs((int)r[i + 1] - (int)r[i]);
+      }
+      if ((double)grad < tex) defined[p] = false;
+    }
+    best[p] = kBig;
+    bi[p] = -1;
+    second[p] = kBig;
+    cmv[p] = -1;
+    cpv[p] = -1;
+    last[p] = -1;
+    pm2[p] = kBig;
+    neval[p] = 0;
+  }
+
+  for (int idx = 0; idx < nd; ++idx) {
+    const int d = d_lo + idx;
+    // column sums: cs[r][c] = sum_j |L(r+j, c) - R(r+j, c - d)|, c over L tile
+    const int roff = (lx0 - d) - rx0;  // R tile column of L tile column 0
+    for (int it = threadIdx.x; it < CW * (TYB / 8); it += BT) {
+      const int c = it % CW, g = it / CW;
+      const int r0 = g * 8;
+      int s = 0;
+      for (int j = 0; j < bs; ++j)
+        s += abs((int)Lt[(r0 + j) * LW + c] - (int)Rt[(r0 + j) * RW + c + roff]);
+      cs[r0 * CW + c] = s;
+      for (int r = r0 + 1; r < r0 + 8; ++r) {
+        s += abs((int)Lt[(r + bs - 1) * LW + c] - (int)Rt[(r + bs - 1) * RW + c + roff]) -
+             abs((int)Lt[(r - 1) * LW + c] - (int)Rt[(r - 1) * RW + c + roff]);
+        cs[r * CW + c] = s;
+      }
+    }
+    __syncthreads();
+    // row sums over bs columns and the streaming winner update
+    const int* csr = cs + row * CW + seg * 8;  // cs col of pixel xs - hw
+    int sad = 0;
+    for (int i = 0; i < bs; ++i) sad += csr[i];
+#pragma unroll
+    for (int p = 0; p < 8; ++p) {
+      if (p > 0) sad += csr[p - 1 + bs] - csr[p - 1];
+      const int x = xs + p;
+      const bool ev = defined[p] && (x - d - hw >= 0) && (x - d + hw < W);  // bm.hpp:61-64
+      const int v = ev ? sad : -1;
+      if (v >= 0) {
+        ++neval[p];
+        if (v < best[p]) {  // new first minimum at idx
+          second[p] = pm2[p];  // min over indices <= idx-2
+          best[p] = v;
+          bi[p] = idx;
+          cmv[p] = last[p];
+          cpv[p] = -1;
+        } else {
+          if (idx == bi[p] + 1)
+            cpv[p] = v;
+          else if (idx > bi[p] + 1 && v < second[p])
+            second[p] = v;
+        }
+      } else if (idx == bi[p] + 1) {
+        cpv[p] = -1;
+      }
+      // advance the lagged prefix minimum: pm2(idx+1) = min(pm2(idx), sad[idx-1])
+      if (last[p] >= 0 && last[p] < pm2[p]) pm2[p] = last[p];
+      last[p] = v;
+    }
+    __syncthreads();
+  }
+
+  // epilogue: uniqueness, sub-pixel, raw (bm.hpp:74-100)
+  int valid_count = 0;
+  const int lo = d_lo * 16;
+#pragma unroll
+  for (int p = 0; p < 8; ++p) {
+    const int x = xs + p;
+    if (x >= W || y >= H) continue;
+    int out = kInvalid;
+    if (defined[p] && neval[p] > 0) {
+      bool ok = true;
+      if (second[p] != kBig &&
+          __dmul_rn((double)best[p], __dadd_rn(1.0, __ddiv_rn(uniq, 100.0))) >= (double)second[p])
+        ok = false;
+      if (ok) {
+        double d_hat = (double)(d_lo + bi[p]);
+        if (bi[p] > 0 && bi[p] + 1 < nd && cmv[p] >= 0 && cpv[p] >= 0)
+          d_hat = __dadd_rn(d_hat, subpix((double)cmv[p], (double)best[p], (double)cpv[p]));
+        long long r = llround(__dmul_rn(d_hat, 16.0));
+        const long long rlo = (long long)d_lo * 16, rhi = (long long)d_hi * 16 - 1;
+        r = r < rlo ? rlo : (r > rhi ? rhi : r);
+        out = (int)r;
+      }
+    }
+    if (raw) raw[((int64_t)frame * n_delta + kd) * W * H + (int64_t)y * W + x] = (int16_t)out;
+    if (out != kInvalid && out > lo) ++valid_count;
+  }
+  if (counts) {
+    for (int o = 16; o > 0; o >>= 1) valid_count += __shfl_xor_sync(0xffffffffu, valid_count, o);
+    __shared__ int wsum[BT / 32];
+    if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = valid_count;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int t = 0;
+      for (int q = 0; q < BT / 32; ++q) t += wsum[q];
+      if (t) atomicAdd((unsigned long long*)&counts[(int64_t)frame * n_delta + kd], (unsigned long long)t);
+    }
+  }
+}
+
+__global__ void downscale_kernel(const uint8_t* __restrict__ in, int w, int h, int s,
+                                 uint8_t* __restrict__ out) {  // image.hpp:98-116
+  const int ow = w / s, oh = h / s;
+  const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y;
+  if (x >= ow || y >= oh) return;
+  int sum = 0;
+  for (int j = 0; j < s; ++j)
+    for (int i = 0; i < s; ++i) sum += in[(int64_t)(y * s + j) * w + x * s + i];
+  out[(int64_t)y * ow + x] = (uint8_t)llround(__ddiv_rn((double)sum, (double)(s * s)));
+}
+
+__global__ void upscale_kernel(const int16_t* __restrict__ in, int w, int h, int s, int lo,
+                               int16_t* __restrict__ out, int ow, int oh) {  // image.hpp:122-141
+  // out is ow x oh (the original dims); cells past the upscaled extent stay invalid
+  const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y;
+  if (x >= ow || y >= oh) return;
+  int16_t v = (int16_t)kInvalid;
+  const int sx = x / s, sy = y / s;
+  if (sx < w && sy < h) {
+    const int r = in[(int64_t)sy * w + sx];
+    if (r != kInvalid) {
+      const int scaled = r * s;
+      if (scaled >= lo && scaled <= 32767) v = (int16_t)scaled;
+    }
+  }
+  out[(int64_t)y * ow + x] = v;
+}
+
+__global__ void autorect_pick_kernel(const int64_t* __restrict__ counts, int n_frames,
+                                     int delta_min, int n_delta, int32_t* __restrict__ best) {
+  const int f = blockIdx.x * blockDim.x + threadIdx.x;  // autorect.hpp:35-57
+  if (f >= n_frames) return;
+  int bd = 0;
+  long long bc = -1;
+  for (int k = 0; k < n_delta; ++k) {
+    const int delta = delta_min + k;
+    const long long c = counts[(int64_t)f * n_delta + k];
+    bool better = c > bc;
+    if (c == bc) better = abs(delta) < abs(bd) || (abs(delta) == abs(bd) && delta < bd);
+    if (better) {
+      bc = c;
+      bd = delta;
+    }
+  }
+  best[f] = bd;
+}
+
+}  // namespace
+
+cudaError_t launch_bm(const uint8_t* left, const uint8_t* right, int n_frames, int64_t stride,
+                      int pitch, int img_h, int w, int h, int x0, int y0, int delta_min,
+                      int n_delta, rg_bm_params p, int16_t* raw, int64_t* counts, cudaStream_t s) {
+  if (n_frames <= 0 || n_delta <= 0) return cudaSuccess;
+  const int hw = p.block_size / 2;
+  const int TR = TYB + 2 * hw, LW = TXB + 2 * hw, RW = TXB + 2 * hw + p.num_disparities - 1;
+  const size_t smem = (((size_t)TR * (LW + RW)) + 15) / 16 * 16 + sizeof(int) * TYB * LW;
+  cudaError_t e = cudaFuncSetAttribute(bm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  dim3 grid((w + TXB - 1) / TXB, (h + TYB - 1) / TYB, n_frames * n_delta);
+  bm_kernel<<<grid, BT, smem, s>>>(left, right, stride, pitch, img_h, w, h, x0, y0, delta_min,
+                                   n_delta, p.block_size, p.min_disparity, p.num_disparities,
+                                   p.texture_threshold, p.uniqueness_ratio, raw, counts);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_downscale(const uint8_t* in, int w, int h, int s, uint8_t* out, cudaStream_t st) {
+  dim3 grid((w / s + 127) / 128, h / s);
+  downscale_kernel<<<grid, 128, 0, st>>>(in, w, h, s, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_upscale(const int16_t* in, int w, int h, int s, int lo, int16_t* out, int ow,
+                           int oh, cudaStream_t st) {
+  dim3 grid((ow + 127) / 128, oh);
+  upscale_kernel<<<grid, 128, 0, st>>>(in, w, h, s, lo, out, ow, oh);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_autorect_pick(const int64_t* counts, int n_frames, int delta_min, int n_delta,
+                                 int32_t* best, cudaStream_t s) {
+  autorect_pick_kernel<<<(n_frames + 127) / 128, 128, 0, s>>>(counts, n_frames, delta_min, n_delta,
+                                                               best);
+  return cudaGetLastError();
+}
+
+}  // namespace rg

@@ -1,0 +1,302 @@
+// plan.cu -- K3 (object selection / work planning) and K4 (aggregation +
+// range) of the batched object ranger, plus the single-shot kernels behind
+// the reference's helper functions (select_objects, find_occluders,
+// sample_query_points, aggregate_close_disparities).
+//
+// K3, one CTA per frame (template_match.hpp:277-310): priority rank of every
+// detection (select_objects :94-114, as an O(n^2) rank count so the CTA
+// needs no sort), selected set in input order, FAR/CLOSE classification
+// (:63-67), and one "slot" per potential QueryBlock -- FAR objects get one,
+// CLOSE objects rows x cols (:192-197).  Slots are appended to a global list
+// with one atomic per object; the list order does not matter because results
+// are addressed by slot and each object keeps its slot range.
+//
+// K4, one CTA per selected object (template_match.hpp:332-361): FAR takes its
+// single verified block, CLOSE sorts the verified sub-block disparities
+// (x close_scale, :353) and keeps the longest tight run (:126-148); the range
+// z = f / ((1/b) d) is the canonical reprojection (geometry.hpp:124-146).
+#include "rg_common.cuh"
+#include "rg_device.cuh"
+
+namespace rg {
+namespace {
+
+constexpr int PT = 256;
+constexpr int kMaxDetsPerFrame = 4096;
+
+__global__ void __launch_bounds__(PT) plan_frames_kernel(
+    const rg_detection* __restrict__ dets, const int32_t* __restrict__ det_off, int w, int h,
+    rg_ranger_config cfg, int out_stride, ObjEntry* __restrict__ objs,
+    rg_object_disparity* __restrict__ out, int32_t* __restrict__ out_count,
+    Slot* __restrict__ slots, int slot_capacity, int32_t* __restrict__ counters,
+    rg_ranger_stats* __restrict__ stats) {
+  __shared__ unsigned char sel[kMaxDetsPerFrame];
+  __shared__ int warp_tot[PT / 32];
+  const int f = blockIdx.x;
+  const int d0 = det_off[f], n = det_off[f + 1] - d0;
+  const rg_detection* D = dets + d0;
+  // rank of every detection in the priority order; selected iff rank < budget
+  for (int i = threadIdx.x; i < n; i += PT) {
+    const rg_detection di = D[i];
+    int rank = 0;
+    for (int j = 0; j < n && rank < cfg.max_objects; ++j)
+      if (j != i && dev_precedes(D[j], j, di, i, cfg)) ++rank;
+    sel[i] = rank < cfg.max_objects;
+  }
+  __syncthreads();
+  // selected objects in input order: block-wide exclusive scan over chunks
+  int base_k = 0, n_far = 0, n_close = 0;
+  for (int c0 = 0; c0 < n; c0 += PT) {
+    const int i = c0 + threadIdx.x;
+    const int flag = (i < n) ? sel[i] : 0;
+    const unsigned bal = __ballot_sync(0xffffffffu, flag);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0) warp_tot[wid] = __popc(bal);
+    __syncthreads();
+    int before = 0, total = 0;
+    for (int q = 0; q < PT / 32; ++q) {
+      if (q < wid) before += warp_tot[q];
+      total += warp_tot[q];
+    }
+    if (flag) {
+      const int k = base_k + before + __popc(bal & ((1u << lane) - 1u));
+      const rg_detection di = D[i];
+      const int kind = dev_classify(di, w, h, cfg.tau_s);
+      int rows = 1, cols = 1;
+      if (kind == RG_KIND_CLOSE) dev_close_grid(pixel_box(di, w, h), cfg, &rows, &cols);
+      const int ns = rows * cols;
+      const int sb = atomicAdd(&counters[0], ns);
+      ObjEntry e;
+      e.det = d0 + i;
+      e.kind = kind;
+      e.slot_base = sb;
+      e.n_slots = ns;
+      e.rows = rows;
+      e.cols = cols;
+      e.frame = f;
+      e.pad = 0;
+      const int g = f * out_stride + k;
+      objs[g] = e;
+      rg_object_disparity od;
+      od.det_id = di.id;
+      od.kind = kind;
+      od.n_blocks_used = 0;
+      od.valid = 0;
+      od.disparity = 0.0;
+      od.z_cam = 0.0;
+      out[g] = od;
+      if (sb + ns > slot_capacity) {
+        counters[1] = 1;  // overflow: the host grows the list and re-runs
+      } else {
+        for (int t = 0; t < ns; ++t) slots[sb + t] = Slot{f, g, t, 0};
+      }
+      if (kind == RG_KIND_FAR)
+        ++n_far;
+      else
+        ++n_close;
+    }
+    base_k += total;
+    __syncthreads();
+  }
+  // per-frame counters
+  for (int o = 16; o > 0; o >>= 1) {
+    n_far += __shfl_xor_sync(0xffffffffu, n_far, o);
+    n_close += __shfl_xor_sync(0xffffffffu, n_close, o);
+  }
+  __shared__ int tf[PT / 32], tc[PT / 32];
+  if ((threadIdx.x & 31) == 0) {
+    tf[threadIdx.x >> 5] = n_far;
+    tc[threadIdx.x >> 5] = n_close;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int a = 0, b = 0;
+    for (int q = 0; q < PT / 32; ++q) {
+      a += tf[q];
+      b += tc[q];
+    }
+    out_count[f] = base_k;
+    if (stats) {
+      stats[f].query_points = 0;
+      stats[f].image_pixels = (int64_t)w * h;
+      stats[f].n_far = a;
+      stats[f].n_close = b;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(128) aggregate_kernel(
+    const ObjEntry* __restrict__ objs, const int32_t* __restrict__ out_count, int out_stride,
+    const rg_match_result* __restrict__ res, int slot_capacity, rg_ranger_config cfg,
+    double focal, double baseline, double* __restrict__ scratch,
+    rg_object_disparity* __restrict__ out) {
+  __shared__ double vals[kAggCapacity];
+  __shared__ int cnt;
+  const int g = blockIdx.x;
+  const int f = g / out_stride, k = g - f * out_stride;
+  if (k >= out_count[f]) return;
+  const ObjEntry e = objs[g];
+  if (e.slot_base + e.n_slots > slot_capacity) return;  // overflowed batch, re-run follows
+  int valid = 0, used = 0;
+  double disp = 0.0;
+  if (e.kind == RG_KIND_FAR) {
+    // template_match.hpp:338-347: the single FAR block, verified or invalid
+    const rg_match_result r = res[e.slot_base];
+    if (r.n_points >= 4 && r.has_value && r.verified) {
+      valid = 1;
+      disp = r.dx_subpix;
+      used = 1;
+    }
+  } else {
+    if (threadIdx.x == 0) cnt = 0;
+    __syncthreads();
+    const bool big = e.n_slots > kAggCapacity;
+    double* dst = big ? scratch + e.slot_base : vals;
+    for (int t = threadIdx.x; t < e.n_slots; t += blockDim.x) {
+      const rg_match_result r = res[e.slot_base + t];
+      if (r.n_points >= 4 && r.has_value && r.verified)
+        dst[atomicAdd(&cnt, 1)] = __dmul_rn(r.dx_subpix, (double)cfg.close_scale);
+    }
+    __syncthreads();
+    const int m = cnt;
+    if (!big) {
+      dev_bitonic_sort(vals, m);
+    } else {
+      // more CLOSE blocks than fit in smem: values sit in this object's
+      // scratch region [slot_base, +n_slots); rank-sort them into the mirror
+      // region at +slot_capacity (scratch holds 2 * slot_capacity doubles)
+      dev_rank_sort(dst, m, scratch + slot_capacity + e.slot_base);
+      dst = scratch + slot_capacity + e.slot_base;
+    }
+    if (threadIdx.x == 0) dev_runs(big ? dst : vals, m, cfg.tau_d, cfg.n_min, &valid, &disp, &used);
+  }
+  if (threadIdx.x == 0) {
+    rg_object_disparity od = out[g];
+    od.valid = valid;
+    od.disparity = disp;
+    od.n_blocks_used = used;
+    od.z_cam = 0.0;
+    if (valid && disp > 0 && focal > 0 && baseline > 0)
+      od.z_cam = __ddiv_rn(focal, __dmul_rn(__ddiv_rn(1.0, baseline), disp));
+    out[g] = od;
+  }
+}
+
+// ---------------------------------------------------------------- helpers
+__global__ void select_objects_kernel(const rg_detection* __restrict__ dets, int n,
+                                      rg_ranger_config cfg, int32_t* __restrict__ out_idx,
+                                      int32_t* __restrict__ n_out) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    int rank = 0;
+    for (int j = 0; j < n; ++j)
+      if (j != i && dev_precedes(dets[j], j, dets[i], i, cfg)) ++rank;
+    if (rank < cfg.max_objects) out_idx[rank] = i;
+  }
+  if (threadIdx.x == 0) *n_out = n < cfg.max_objects ? n : cfg.max_objects;
+}
+
+__global__ void find_occluders_kernel(const rg_detection* __restrict__ dets, int n,
+                                      int32_t* __restrict__ counts, int32_t* __restrict__ lists) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int c = 0;
+  for (int j = 0; j < n; ++j)
+    if (j != i && dev_occludes(dets[i], dets[j])) lists[(int64_t)i * n + c++] = j;
+  counts[i] = c;
+}
+
+__global__ void sample_blocks_kernel(const rg_detection* __restrict__ det, int kind,
+                                     const double* __restrict__ occ, int n_occ, rg_ranger_config cfg,
+                                     int w, int h, int rows, int cols, int32_t* __restrict__ pts,
+                                     int32_t* __restrict__ counts, int per_block) {
+  extern __shared__ double occ_s[];
+  for (int i = threadIdx.x; i < 4 * n_occ; i += blockDim.x) occ_s[i] = occ[i];
+  __syncthreads();
+  const int b = blockIdx.x;
+  int2* out = reinterpret_cast<int2*>(pts) + (int64_t)b * per_block;
+  const int np = dev_sample_block(*det, kind, b / cols, b % cols, rows, cols, occ_s, n_occ,
+                                  nullptr, 0, -1, cfg, w, h, out);
+  if (threadIdx.x == 0) counts[b] = np;
+}
+
+__global__ void aggregate_values_kernel(const double* __restrict__ v, int n, double tau_d,
+                                        int n_min, double* __restrict__ scratch,
+                                        int32_t* __restrict__ out_i, double* __restrict__ out_d) {
+  __shared__ double vals[kAggCapacity];
+  const bool big = n > kAggCapacity;
+  if (!big) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) vals[i] = v[i];
+    __syncthreads();
+    dev_bitonic_sort(vals, n);
+  } else {
+    dev_rank_sort(v, n, scratch);
+  }
+  if (threadIdx.x == 0) {
+    int valid, len;
+    double d;
+    dev_runs(big ? scratch : vals, n, tau_d, n_min, &valid, &d, &len);
+    out_i[0] = valid;
+    out_i[1] = len;
+    out_d[0] = d;
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_plan_frames(const rg_detection* dets, const int32_t* det_off, int n_frames, int w,
+                               int h, rg_ranger_config cfg, int out_stride, ObjEntry* objs,
+                               rg_object_disparity* out, int32_t* out_count, Slot* slots,
+                               int slot_capacity, int32_t* counters, rg_ranger_stats* stats,
+                               cudaStream_t s) {
+  if (n_frames <= 0) return cudaSuccess;
+  plan_frames_kernel<<<n_frames, PT, 0, s>>>(dets, det_off, w, h, cfg, out_stride, objs, out,
+                                             out_count, slots, slot_capacity, counters, stats);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_aggregate(const ObjEntry* objs, const int32_t* out_count, int n_frames,
+                             int out_stride, const rg_match_result* res, int slot_capacity,
+                             rg_ranger_config cfg, double focal, double baseline, double* scratch,
+                             rg_object_disparity* out, cudaStream_t s) {
+  if (n_frames <= 0 || out_stride <= 0) return cudaSuccess;
+  aggregate_kernel<<<n_frames * out_stride, 128, 0, s>>>(objs, out_count, out_stride, res,
+                                                         slot_capacity, cfg, focal, baseline,
+                                                         scratch, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_select_objects(const rg_detection* dets, int n, rg_ranger_config cfg,
+                                  int32_t* out_idx, int32_t* n_out, cudaStream_t s) {
+  select_objects_kernel<<<1, 256, 0, s>>>(dets, n, cfg, out_idx, n_out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_find_occluders(const rg_detection* dets, int n, int32_t* counts, int32_t* lists,
+                                  cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  find_occluders_kernel<<<(n + 127) / 128, 128, 0, s>>>(dets, n, counts, lists);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sample_blocks(const rg_detection* det, int kind, const double* occ, int n_occ,
+                                 rg_ranger_config cfg, int w, int h, int rows, int cols,
+                                 int32_t* pts, int32_t* counts, int per_block, cudaStream_t s) {
+  const size_t smem = sizeof(double) * 4 * (size_t)(n_occ > 0 ? n_occ : 1);
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(sample_blocks_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  sample_blocks_kernel<<<rows * cols, 128, smem, s>>>(det, kind, occ, n_occ, cfg, w, h, rows, cols,
+                                                      pts, counts, per_block);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_aggregate_values(const double* v, int n, double tau_d, int n_min,
+                                    double* scratch, int32_t* out_i, double* out_d,
+                                    cudaStream_t s) {
+  aggregate_values_kernel<<<1, 256, 0, s>>>(v, n, tau_d, n_min, scratch, out_i, out_d);
+  return cudaGetLastError();
+}
+
+}  // namespace rg

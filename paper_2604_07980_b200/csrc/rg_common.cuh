@@ -1,0 +1,151 @@
+// rg_common.cuh -- shared declarations of the B200 census ranger library.
+//
+// Device-side numerics follow SURVEY.md Appendix A: the whole library is
+// compiled with -fmad=false and every double expression keeps the reference's
+// operation order, so FP64 results (mean costs, sub-pixel offsets, sampling
+// coordinates, ranges) are bit-identical to the reference's x86-64 build.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/ranger_cuda.h"
+
+namespace rg {
+
+// ------------------------------------------------------------ limits
+constexpr int kMatchThreads = 256;     // CTA size of the matcher
+constexpr int kWindowCodes = 12288;    // smem census window (48 KB)
+constexpr int kMaxOccluders = 128;     // per-object occluder boxes kept in smem
+constexpr int kAggCapacity = 4096;     // CLOSE blocks aggregated in smem
+
+// ------------------------------------------------------------ device structs
+struct Raster {  // census raster in device memory
+  const uint32_t* p;
+  int w, h;
+  int pitch;  // elements
+};
+
+// object table entry of the batched planner (one per selected detection)
+struct ObjEntry {
+  int32_t det;        // global detection index
+  int32_t kind;       // RG_KIND_*
+  int32_t slot_base;  // first slot in the global slot list
+  int32_t n_slots;    // FAR 1, CLOSE rows*cols
+  int32_t rows, cols; // CLOSE sub-block grid
+  int32_t frame;
+  int32_t pad;
+};
+
+// a slot = one potential QueryBlock (FAR block or CLOSE sub-block)
+struct Slot {
+  int32_t frame;
+  int32_t obj;  // index into the object table
+  int32_t sub;  // r*cols + c for CLOSE, 0 for FAR
+  int32_t pad;
+};
+
+}  // namespace rg
+
+// ------------------------------------------------------------ context
+struct rg_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;  // stream of the synchronous compat API
+  cudaStream_t copy_stream = nullptr;  // H2D staging of the host-fed batch API
+  int map_key[4] = {-1, -1, -1, -1};  // geometry of the cached inverse maps
+  std::string err;
+  bool profiling = false;
+  double stage_ms[5] = {0, 0, 0, 0, 0};
+  int64_t stage_launches[5] = {0, 0, 0, 0, 0};
+  int64_t total_launches = 0;
+  cudaEvent_t ev[12] = {};
+  int slot_capacity = 0;    // grows on RG_EOVERFLOW
+  int64_t last_slots = 0;   // slots used by the last batch
+  // grow-only device scratch, keyed by role
+  void* buf[32] = {};
+  size_t cap[32] = {};
+  // pinned host scratch
+  void* hbuf[8] = {};
+  size_t hcap[8] = {};
+};
+
+namespace rg {
+
+enum BufId {
+  B_IMG_L, B_IMG_R, B_CEN_FL, B_CEN_FR, B_CEN_SL, B_CEN_SR, B_DETS, B_DET_OFF,
+  B_OBJ, B_SLOTS, B_SLOT_RES, B_OUT, B_OUT_CNT, B_COUNTERS, B_MAPX, B_MAPY,
+  B_PTS, B_OFFS, B_RANGES, B_MRES, B_TMP0, B_TMP1, B_TMP2, B_TMP3, B_STATS,
+  B_BM_L, B_BM_R, B_BM_OUT, B_BM_CNT, B_ROIS, B_STAGE_L, B_STAGE_R,
+};
+
+// error helpers (defined in api.cu)
+rg_status set_err(rg_ctx* ctx, rg_status st, const std::string& msg);
+rg_status cuda_err(rg_ctx* ctx, cudaError_t e, const char* what);
+void* dev_buf(rg_ctx* ctx, int id, size_t bytes);  // nullptr on failure
+void* host_buf(rg_ctx* ctx, int id, size_t bytes);
+void count_launch(rg_ctx* ctx, int stage, int n = 1);
+
+#define RG_CUDA(ctx, expr)                                  \
+  do {                                                      \
+    cudaError_t _e = (expr);                                \
+    if (_e != cudaSuccess) return rg::cuda_err(ctx, _e, #expr); \
+  } while (0)
+
+// ------------------------------------------------------------ launchers
+// census (census.cu)
+cudaError_t launch_census_frames(const uint8_t* left, const uint8_t* right, int n_frames,
+                                 int64_t frame_stride, int pitch, int w, int h,
+                                 uint32_t* fl, uint32_t* fr, uint32_t* sl, uint32_t* sr,
+                                 int cw, int ch, const int32_t* inv_x, const int32_t* inv_y,
+                                 cudaStream_t s);
+cudaError_t launch_roi_mask(uint32_t* codes, int w, int h, const rg_rect* rois, int n_rois,
+                            cudaStream_t s);
+
+// matcher (match.cu)
+cudaError_t launch_match_blocks(Raster L, Raster R, const int32_t* pts, const int64_t* offs,
+                                const rg_search_range* ranges, int n_blocks, int mode,
+                                double tau_v, rg_match_result* out, int max_points,
+                                cudaStream_t s);
+cudaError_t launch_match_slots(const Slot* slots, const int32_t* n_slots_dev, int slot_capacity,
+                               const ObjEntry* objs, const rg_detection* dets,
+                               const int32_t* det_off, const uint32_t* fl, const uint32_t* fr,
+                               const uint32_t* sl, const uint32_t* sr, int w, int h, int cw,
+                               int ch, int64_t full_stride, int64_t scaled_stride,
+                               rg_ranger_config cfg, rg_match_result* res,
+                               rg_ranger_stats* stats, int max_points, cudaStream_t s);
+
+// planner / aggregation / helpers (plan.cu)
+cudaError_t launch_plan_frames(const rg_detection* dets, const int32_t* det_off, int n_frames,
+                               int w, int h, rg_ranger_config cfg, int out_stride, ObjEntry* objs,
+                               rg_object_disparity* out, int32_t* out_count, Slot* slots,
+                               int slot_capacity, int32_t* counters, rg_ranger_stats* stats,
+                               cudaStream_t s);
+cudaError_t launch_aggregate(const ObjEntry* objs, const int32_t* out_count, int n_frames,
+                             int out_stride, const rg_match_result* res, int slot_capacity,
+                             rg_ranger_config cfg, double focal, double baseline, double* scratch,
+                             rg_object_disparity* out, cudaStream_t s);
+cudaError_t launch_select_objects(const rg_detection* dets, int n, rg_ranger_config cfg,
+                                  int32_t* out_idx, int32_t* n_out, cudaStream_t s);
+cudaError_t launch_find_occluders(const rg_detection* dets, int n, int32_t* counts,
+                                  int32_t* lists, cudaStream_t s);
+cudaError_t launch_sample_blocks(const rg_detection* det, int kind, const double* occ, int n_occ,
+                                 rg_ranger_config cfg, int w, int h, int rows, int cols,
+                                 int32_t* pts, int32_t* counts, int per_block, cudaStream_t s);
+cudaError_t launch_aggregate_values(const double* v, int n, double tau_d, int n_min,
+                                    double* scratch, int32_t* out_i, double* out_d,
+                                    cudaStream_t s);
+
+// BM / autorect (bm.cu)
+cudaError_t launch_bm(const uint8_t* left, const uint8_t* right, int n_frames, int64_t stride,
+                      int pitch, int img_h, int w, int h, int x0, int y0, int delta_min,
+                      int n_delta, rg_bm_params p, int16_t* raw, int64_t* counts,
+                      cudaStream_t s);
+cudaError_t launch_downscale(const uint8_t* in, int w, int h, int s, uint8_t* out, cudaStream_t st);
+cudaError_t launch_upscale(const int16_t* in, int w, int h, int s, int lo, int16_t* out, int ow,
+                           int oh, cudaStream_t st);
+cudaError_t launch_autorect_pick(const int64_t* counts, int n_frames, int delta_min, int n_delta,
+                                 int32_t* best, cudaStream_t s);
+
+}  // namespace rg

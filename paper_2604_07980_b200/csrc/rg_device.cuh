@@ -1,0 +1,231 @@
+// rg_device.cuh -- device-side object-ranger geometry shared by the planner,
+// the fused matcher and the aggregation kernels.
+//
+// Every double expression keeps the reference's operation order and is
+// written with explicit _rn intrinsics, so it rounds exactly like the
+// reference's x86-64 build (no FMA contraction regardless of nvcc flags).
+#pragma once
+
+#include "rg_common.cuh"
+
+namespace rg {
+
+struct PBox {
+  double x0, y0, x1, y1;
+};
+
+__device__ __forceinline__ double half_of(double v) { return __ddiv_rn(v, 2.0); }
+__device__ __forceinline__ double dmin(double a, double b) { return b < a ? b : a; }  // std::min
+__device__ __forceinline__ double dmax(double a, double b) { return a < b ? b : a; }  // std::max
+
+// to_pixel_box, detection.hpp:23-30
+__device__ __forceinline__ PBox pixel_box(const rg_detection& d, int w, int h) {
+  PBox b;
+  b.x0 = __dmul_rn(__dsub_rn(d.cx, half_of(d.w)), (double)w);
+  b.x1 = __dmul_rn(__dadd_rn(d.cx, half_of(d.w)), (double)w);
+  b.y0 = __dmul_rn(__dsub_rn(d.cy, half_of(d.h)), (double)h);
+  b.y1 = __dmul_rn(__dadd_rn(d.cy, half_of(d.h)), (double)h);
+  return b;
+}
+
+// PixelBox::contains, detection.hpp:19-21
+__device__ __forceinline__ bool box_contains(double x0, double y0, double x1, double y1, double x,
+                                             double y) {
+  return x >= x0 && x < x1 && y >= y0 && y < y1;
+}
+
+// classify_far_close, template_match.hpp:63-67
+__device__ __forceinline__ int dev_classify(const rg_detection& d, int w, int h, double tau_s) {
+  return dmax(__dmul_rn(d.w, (double)w), __dmul_rn(d.h, (double)h)) < tau_s ? RG_KIND_FAR
+                                                                            : RG_KIND_CLOSE;
+}
+
+// find_occluders predicate, template_match.hpp:75-85: does j occlude i?
+__device__ __forceinline__ bool dev_occludes(const rg_detection& di, const rg_detection& dj) {
+  const double ix0 = __dsub_rn(di.cx, half_of(di.w)), ix1 = __dadd_rn(di.cx, half_of(di.w));
+  const double iy0 = __dsub_rn(di.cy, half_of(di.h)), iy1 = __dadd_rn(di.cy, half_of(di.h));
+  const double jx0 = __dsub_rn(dj.cx, half_of(dj.w)), jx1 = __dadd_rn(dj.cx, half_of(dj.w));
+  const double jy0 = __dsub_rn(dj.cy, half_of(dj.h)), jy1 = __dadd_rn(dj.cy, half_of(dj.h));
+  const double ox = __dsub_rn(dmin(ix1, jx1), dmax(ix0, jx0));
+  const double oy = __dsub_rn(dmin(iy1, jy1), dmax(iy0, jy0));
+  return ox > 0 && oy > 0 && jy1 > iy1;
+}
+
+// select_objects ordering, template_match.hpp:94-114: does a come before b?
+// frontal (centre inside the crop) first by area desc, then the rest by
+// bottom desc; ties by id, then (reference-unspecified) by index.
+__device__ __forceinline__ bool dev_frontal(const rg_detection& d, const rg_ranger_config& c) {
+  return d.cx >= c.crop_x0 && d.cx < c.crop_x1 && d.cy >= c.crop_y0 && d.cy < c.crop_y1;
+}
+__device__ __forceinline__ bool dev_precedes(const rg_detection& a, int ia, const rg_detection& b,
+                                             int ib, const rg_ranger_config& c) {
+  const bool fa = dev_frontal(a, c), fb = dev_frontal(b, c);
+  if (fa != fb) return fa;
+  if (fa) {
+    const double aa = __dmul_rn(a.w, a.h), ab = __dmul_rn(b.w, b.h);
+    if (aa != ab) return aa > ab;
+  } else {
+    const double ba = __dadd_rn(a.cy, half_of(a.h)), bb = __dadd_rn(b.cy, half_of(b.h));
+    if (ba != bb) return ba > bb;
+  }
+  if (a.id != b.id) return a.id < b.id;
+  return ia < ib;
+}
+
+// grid sizes of sample_query_points, template_match.hpp:165-168, 189-194
+__device__ __forceinline__ int dev_cap(const rg_ranger_config& c) {
+  const int cap = (int)__dsqrt_rn((double)c.max_total_points);
+  return cap > 1 ? cap : 1;
+}
+__device__ __forceinline__ void dev_close_grid(const PBox& b, const rg_ranger_config& c, int* rows,
+                                               int* cols) {
+  const double half_tau = __ddiv_rn(c.tau_s, 2.0);
+  const int cc = (int)__ddiv_rn(__dsub_rn(b.x1, b.x0), half_tau);
+  const int rr = (int)__ddiv_rn(__dsub_rn(b.y1, b.y0), half_tau);
+  *cols = cc > 2 ? cc : 2;
+  *rows = rr > 2 ? rr : 2;
+}
+
+// One (sub-)block of sample_query_points (template_match.hpp:155-223),
+// executed by the whole CTA (blockDim a multiple of 32).  Occluded points are
+// tested against `occ` (n_occ PixelBoxes) or, when occ_all != nullptr,
+// against every detection of the frame that occludes `det` (used when the
+// smem list overflowed).  Points are compacted in the reference's grid order
+// (j-major, i-minor) with warp ballots; returns the count (CTA-uniform).
+__device__ __forceinline__ int dev_sample_block(const rg_detection& det, int kind, int r, int c,
+                                                int rows, int cols, const double* occ, int n_occ,
+                                                const rg_detection* occ_all, int n_all, int self,
+                                                const rg_ranger_config& cfg, int w, int h,
+                                                int2* pts) {
+  __shared__ int s_wtot[32];
+  const PBox box = pixel_box(det, w, h);
+  const double bw = __dsub_rn(box.x1, box.x0), bh = __dsub_rn(box.y1, box.y0);
+  const int cap = dev_cap(cfg);
+  const bool far = kind == RG_KIND_FAR;
+  const int n = far ? min(cfg.grid_side_points, cap) : min(cfg.close_block_side_points, cap);
+  const int s = cfg.close_scale;
+  const int cw = w / s, ch = h / s;
+  double sx0 = 0, sy0 = 0, sw = 0, sh = 0;
+  if (!far) {
+    sx0 = __dadd_rn(box.x0, __ddiv_rn(__dmul_rn((double)c, bw), (double)cols));
+    sy0 = __dadd_rn(box.y0, __ddiv_rn(__dmul_rn((double)r, bh), (double)rows));
+    sw = __ddiv_rn(bw, (double)cols);
+    sh = __ddiv_rn(bh, (double)rows);
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int base = 0;
+  for (int c0 = 0; c0 < n * n; c0 += blockDim.x) {
+    const int idx = c0 + threadIdx.x;
+    bool keep = idx < n * n;
+    int px = 0, py = 0;
+    double fx = 0, fy = 0;
+    if (keep) {
+      const int j = idx / n, i = idx - j * n;
+      if (far) {
+        fy = __dadd_rn(box.y0, __ddiv_rn(__dmul_rn(__dadd_rn((double)j, 0.5), bh), (double)n));
+        fx = __dadd_rn(box.x0, __ddiv_rn(__dmul_rn(__dadd_rn((double)i, 0.5), bw), (double)n));
+        px = (int)lround(fx);
+        py = (int)lround(fy);
+        keep = px >= 0 && px < w && py >= 0 && py < h;
+      } else {
+        fy = __dadd_rn(sy0, __ddiv_rn(__dmul_rn(__dadd_rn((double)j, 0.5), sh), (double)n));
+        fx = __dadd_rn(sx0, __ddiv_rn(__dmul_rn(__dadd_rn((double)i, 0.5), sw), (double)n));
+        keep = !(fx < 0 || fx >= w || fy < 0 || fy >= h);
+      }
+    }
+    if (keep) {  // occluded points drop (template_match.hpp:159-163, 181, 212)
+      bool hidden = false;
+      if (occ_all) {
+        for (int k = 0; k < n_all && !hidden; ++k) {
+          if (k == self || !dev_occludes(det, occ_all[k])) continue;
+          const PBox ob = pixel_box(occ_all[k], w, h);
+          hidden = box_contains(ob.x0, ob.y0, ob.x1, ob.y1, fx, fy);
+        }
+      } else {
+        for (int k = 0; k < n_occ && !hidden; ++k)
+          hidden = box_contains(occ[4 * k], occ[4 * k + 1], occ[4 * k + 2], occ[4 * k + 3], fx, fy);
+      }
+      keep = !hidden;
+    }
+    if (keep && !far) {  // map into the reduced raster (template_match.hpp:213-215)
+      px = (int)lround(__ddiv_rn(__dmul_rn(fx, (double)cw), (double)w));
+      py = (int)lround(__ddiv_rn(__dmul_rn(fy, (double)ch), (double)h));
+      keep = px >= 0 && px < cw && py >= 0 && py < ch;
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, keep);
+    if (lane == 0) s_wtot[wid] = __popc(bal);
+    __syncthreads();
+    int before = 0, total = 0;
+    for (int q = 0; q < nw; ++q) {
+      before += q < wid ? s_wtot[q] : 0;
+      total += s_wtot[q];
+    }
+    if (keep) pts[base + before + __popc(bal & ((1u << lane) - 1u))] = make_int2(px, py);
+    base += total;
+    __syncthreads();
+  }
+  return base;
+}
+
+// aggregate_close_disparities core (template_match.hpp:126-148) over values
+// already sorted ascending; single thread.
+__device__ __forceinline__ void dev_runs(const double* v, int n, double tau_d, int n_min,
+                                         int* valid, double* disp, int* run_len) {
+  *valid = 0;
+  *disp = 0.0;
+  *run_len = 0;
+  if (n == 0) return;
+  int best_start = -1, best_len = 0, start = 0;
+  for (int i = 1; i <= n; ++i) {
+    if (i == n || __dsub_rn(v[i], v[i - 1]) >= tau_d) {
+      const int len = i - start;
+      if (len >= best_len) {  // later run = larger disparities wins ties
+        best_len = len;
+        best_start = start;
+      }
+      start = i;
+    }
+  }
+  if (best_len < n_min) return;
+  *valid = 1;
+  *run_len = best_len;
+  *disp = v[best_start + best_len / 2];
+}
+
+// CTA-wide ascending bitonic sort of n <= cap doubles in shared memory
+// (padded with +inf up to the next power of two <= cap).
+__device__ __forceinline__ void dev_bitonic_sort(double* v, int n) {
+  int m = 1;
+  while (m < n) m <<= 1;
+  for (int i = n + threadIdx.x; i < m; i += blockDim.x) v[i] = __longlong_as_double(0x7ff0000000000000LL);
+  __syncthreads();
+  for (int k = 2; k <= m; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < m; i += blockDim.x) {
+        const int p = i ^ j;
+        if (p > i) {
+          const bool up = (i & k) == 0;
+          const double a = v[i], b = v[p];
+          if ((a > b) == up) {
+            v[i] = b;
+            v[p] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// rank sort for large n (values in global scratch): out[rank(i)] = v[i]
+__device__ __forceinline__ void dev_rank_sort(const double* v, int n, double* out) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const double x = v[i];
+    int rank = 0;
+    for (int k = 0; k < n; ++k) rank += (v[k] < x) || (v[k] == x && k < i);
+    out[rank] = x;
+  }
+  __syncthreads();
+}
+
+}  // namespace rg

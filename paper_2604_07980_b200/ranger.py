@@ -1,0 +1,608 @@
+"""Python mirror of the reference's object-ranging API, backed by the CUDA library.
+
+Names, argument meaning, defaults and error behaviour follow the reference's
+header-only C++ API (proj/include/ranger/{census,template_match,bm,autorect}.hpp);
+every call runs on the GPU through the C ABI in include/ranger_cuda.h.  There
+is no CPU fallback: importing works without a GPU (the library is loaded, its
+symbols bound), but the first compute call raises if no sm_100 device exists.
+
+Reference exceptions map as: std::invalid_argument -> InvalidArgument
+(a ValueError), anything else -> RuntimeError.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+import math
+import os
+import threading
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence, Tuple
+
+import numpy as np
+
+from . import _abi
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "lib", "libranger_cuda.so")
+
+SUB_LEVELS = 16          # DisparityMap::kSubLevels, image.hpp:53
+RAW_INVALID = -32768     # DisparityMap::kInvalid, image.hpp:54
+KIND_FAR, KIND_CLOSE = _abi.RG_KIND_FAR, _abi.RG_KIND_CLOSE
+
+
+class InvalidArgument(ValueError):
+    """std::invalid_argument of the reference."""
+
+
+_lib: Optional[C.CDLL] = None
+_lib_lock = threading.Lock()
+
+
+def lib() -> C.CDLL:
+    """The loaded CUDA library (raises loudly if it was not built)."""
+    global _lib
+    if _lib is None:
+        with _lib_lock:
+            if _lib is None:
+                if not os.path.exists(LIB_PATH):
+                    raise RuntimeError(
+                        f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+                        "(there is no CPU fallback)")
+                _lib = _abi.bind(C.CDLL(LIB_PATH))
+    return _lib
+
+
+class Context:
+    """One rg_ctx: a device, its streams and pooled buffers (single-writer)."""
+
+    def __init__(self, device: int = 0):
+        self._h = C.c_void_p()
+        st = lib().rg_ctx_create(device, C.byref(self._h))
+        if st != _abi.RG_OK:
+            msg = lib().rg_create_error().decode()
+            raise RuntimeError(f"rg_ctx_create(device={device}) failed: {msg}")
+        self.device = device
+
+    @property
+    def handle(self) -> C.c_void_p:
+        return self._h
+
+    def check(self, st: int) -> None:
+        if st == _abi.RG_OK:
+            return
+        msg = lib().rg_last_error(self._h).decode()
+        if st == _abi.RG_EINVAL:
+            raise InvalidArgument(msg)
+        raise RuntimeError(f"ranger CUDA library error {st}: {msg}")
+
+    def close(self) -> None:
+        if self._h:
+            lib().rg_ctx_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):  # pragma: no cover - interpreter shutdown order
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # counters / profiling
+    def set_profiling(self, on: bool) -> None:
+        self.check(lib().rg_set_profiling(self._h, 1 if on else 0))
+
+    def counters(self) -> Tuple[List[float], List[int], int]:
+        t = (C.c_double * 5)()
+        n = (C.c_int64 * 5)()
+        tot = C.c_int64()
+        self.check(lib().rg_get_counters(self._h, t, n, C.byref(tot)))
+        return list(t), list(n), tot.value
+
+    def reset_counters(self) -> None:
+        self.check(lib().rg_reset_counters(self._h))
+
+
+_tls = threading.local()
+
+
+def default_context() -> Context:
+    ctx = getattr(_tls, "ctx", None)
+    if ctx is None:
+        ctx = Context(int(os.environ.get("LOCAL_RANK", "0")) if os.environ.get("RG_DEVICE") is None
+                      else int(os.environ["RG_DEVICE"]))
+        _tls.ctx = ctx
+    return ctx
+
+
+def _ptr(a: np.ndarray) -> C.c_void_p:
+    return C.c_void_p(a.ctypes.data)
+
+
+def _gray(img) -> np.ndarray:
+    a = np.ascontiguousarray(img, dtype=np.uint8)
+    if a.ndim != 2 or a.shape[0] < 1 or a.shape[1] < 1:
+        raise InvalidArgument("GrayImage: dims must be >= 1")  # image.hpp:23
+    return a
+
+
+# ============================================================ census.hpp
+@dataclass
+class CensusImage:
+    """census.hpp:21-39: row-major uint32 codes, 0 = undefined."""
+    width: int = 0
+    height: int = 0
+    codes: np.ndarray = field(default_factory=lambda: np.zeros((0, 0), np.uint32))
+    scale_x: float = 1.0
+    scale_y: float = 1.0
+    kSpan = 2
+    kSentinel = 1 << 25
+
+    def code(self, x: int, y: int) -> int:
+        return int(self.codes[y, x])
+
+    def inside(self, x: int, y: int) -> bool:
+        return 0 <= x < self.width and 0 <= y < self.height
+
+
+def census_code_at(img, sx: int, sy: int, ctx: Optional[Context] = None) -> int:
+    """census.hpp:43-56."""
+    ctx = ctx or default_context()
+    a = _gray(img)
+    out = C.c_uint32()
+    ctx.check(lib().rg_census_code_at(ctx.handle, _ptr(a), a.shape[1], a.shape[0], sx, sy, C.byref(out)))
+    return out.value
+
+
+def census_transform(img, out_w: Optional[int] = None, out_h: Optional[int] = None, workers: int = 1,
+                     ctx: Optional[Context] = None) -> CensusImage:
+    """census.hpp:69-90 (workers is accepted for API parity; the grid is the parallelism)."""
+    ctx = ctx or default_context()
+    a = _gray(img)
+    h, w = a.shape
+    ow = w if out_w is None else int(out_w)
+    oh = h if out_h is None else int(out_h)
+    codes = np.zeros((max(oh, 0), max(ow, 0)), np.uint32)
+    ctx.check(lib().rg_census_transform(ctx.handle, _ptr(a), w, h, ow, oh, _ptr(codes)))
+    return CensusImage(ow, oh, codes, ow / w, oh / h)
+
+
+@dataclass
+class CensusRoi:
+    x0: int = 0
+    y0: int = 0
+    x1: int = 0
+    y1: int = 0
+
+
+def census_transform_rois(img, out_w: int, out_h: int, rois: Sequence[CensusRoi], workers: int = 1,
+                          ctx: Optional[Context] = None) -> CensusImage:
+    """census.hpp:100-138."""
+    ctx = ctx or default_context()
+    a = _gray(img)
+    h, w = a.shape
+    r = (_abi.Rect * max(len(rois), 1))(*[_abi.Rect(q.x0, q.y0, q.x1, q.y1) for q in rois])
+    codes = np.zeros((max(out_h, 0), max(out_w, 0)), np.uint32)
+    ctx.check(lib().rg_census_transform_rois(ctx.handle, _ptr(a), w, h, out_w, out_h, r, len(rois), _ptr(codes)))
+    return CensusImage(out_w, out_h, codes, out_w / w, out_h / h)
+
+
+def hamming_cost(a: int, b: int) -> int:
+    """census.hpp:141."""
+    return bin((a ^ b) & 0xFFFFFFFF).count("1")
+
+
+@dataclass
+class QueryBlock:
+    """census.hpp:146-152."""
+    points: List[Tuple[int, int]] = field(default_factory=list)
+    dx_min: int = 0
+    dx_max: int = 0
+    dy_min: int = 0
+    dy_max: int = 0
+    owner: int = -1
+    kind: int = KIND_FAR
+
+
+@dataclass
+class MatchResult:
+    """census.hpp:154-163."""
+    dx_int: int = 0
+    dy_int: int = 0
+    dx_subpix: float = 0.0
+    cost: float = 0.0
+    cost_minus: float = -1.0
+    cost_plus: float = -1.0
+    valid_points: int = 0
+    verified: bool = False
+
+
+def subpixel_refine(cost_minus: float, cost_at: float, cost_plus: float) -> float:
+    """census.hpp:167-171 (pure arithmetic helper)."""
+    denom = cost_minus + cost_plus - 2.0 * cost_at
+    if denom <= 0.0:
+        return 0.0
+    return -(cost_plus - cost_minus) / (2.0 * denom)
+
+
+def _blocks_csr(blocks: Sequence[QueryBlock]):
+    offs = np.zeros(len(blocks) + 1, np.int64)
+    pts: List[Tuple[int, int]] = []
+    for i, b in enumerate(blocks):
+        pts.extend(b.points)
+        offs[i + 1] = len(pts)
+    p = np.asarray(pts, np.int32).reshape(-1, 2) if pts else np.zeros((0, 2), np.int32)
+    rg = (_abi.SearchRange * max(len(blocks), 1))(
+        *[_abi.SearchRange(b.dx_min, b.dx_max, b.dy_min, b.dy_max) for b in blocks])
+    return np.ascontiguousarray(p), offs, rg
+
+
+def _match(blocks, left: CensusImage, right: CensusImage, mode: int, tau_v: float, ctx) -> list:
+    ctx = ctx or default_context()
+    if not blocks:
+        return []
+    pts, offs, rg = _blocks_csr(blocks)
+    L = np.ascontiguousarray(left.codes, np.uint32)
+    R = np.ascontiguousarray(right.codes, np.uint32)
+    out = (_abi.MatchResult * len(blocks))()
+    ctx.check(lib().rg_match_blocks(ctx.handle, _ptr(L), left.width, left.height, _ptr(R), right.width,
+                                    right.height, _ptr(pts), _ptr(offs), rg, len(blocks), mode,
+                                    float(tau_v), out))
+    res = []
+    for r in out:
+        if not r.has_value:
+            res.append(None)
+            continue
+        res.append(MatchResult(r.dx_int, r.dy_int, r.dx_subpix, r.cost, r.cost_minus, r.cost_plus,
+                               r.valid_points, bool(r.verified)))
+    return res
+
+
+def block_match(block: QueryBlock, left: CensusImage, right: CensusImage,
+                ctx: Optional[Context] = None) -> Optional[MatchResult]:
+    """census.hpp:178-272 (None = std::nullopt)."""
+    return _match([block], left, right, _abi.RG_MATCH_FORWARD, 0.0, ctx)[0]
+
+
+def forward_backward_match(block: QueryBlock, left: CensusImage, right: CensusImage, tau_v: float,
+                           ctx: Optional[Context] = None) -> Optional[MatchResult]:
+    """census.hpp:281-303."""
+    return _match([block], left, right, _abi.RG_MATCH_FWD_BWD, tau_v, ctx)[0]
+
+
+def batch_match(blocks: Sequence[QueryBlock], left: CensusImage, right: CensusImage, tau_v: float,
+                workers: int = 1, ctx: Optional[Context] = None) -> List[Optional[MatchResult]]:
+    """census.hpp:307-315: one CTA per block, results by block index."""
+    return _match(list(blocks), left, right, _abi.RG_MATCH_FWD_BWD, tau_v, ctx)
+
+
+# ============================================================ template_match.hpp
+@dataclass
+class Detection:
+    """detection.hpp:8-12 (normalized centre-size box)."""
+    cx: float = 0.0
+    cy: float = 0.0
+    w: float = 0.0
+    h: float = 0.0
+    class_id: int = 0
+    id: int = 0
+
+
+@dataclass
+class PixelBox:
+    x0: float = 0.0
+    y0: float = 0.0
+    x1: float = 0.0
+    y1: float = 0.0
+
+
+@dataclass
+class FrontalCrop:
+    x0: float = 0.25
+    y0: float = 0.25
+    x1: float = 0.75
+    y1: float = 0.75
+
+
+@dataclass
+class RangerConfig:
+    """template_match.hpp:33-46 with the reference's defaults."""
+    tau_s: float = 48
+    close_scale: int = 2
+    grid_side_points: int = 8
+    max_total_points: int = 64
+    close_block_side_points: int = 5
+    tau_d: float = 1.0
+    n_min: int = 3
+    tau_v: float = 1.0
+    max_objects: int = 16
+    frontal_crop: FrontalCrop = field(default_factory=FrontalCrop)
+    dx_max_far: int = 64
+    dx_max_close: int = 192
+
+    def to_c(self) -> _abi.RangerConfig:
+        c = self.frontal_crop
+        return _abi.RangerConfig(float(self.tau_s), self.close_scale, self.grid_side_points,
+                                 self.max_total_points, self.close_block_side_points, float(self.tau_d),
+                                 self.n_min, self.max_objects, float(self.tau_v), c.x0, c.y0, c.x1, c.y1,
+                                 self.dx_max_far, self.dx_max_close)
+
+
+@dataclass
+class ObjectDisparity:
+    """template_match.hpp:18-24 (+ z_cam when a calibration is given)."""
+    det_id: int = -1
+    disparity: float = 0.0
+    kind: int = KIND_FAR
+    n_blocks_used: int = 0
+    valid: bool = False
+    z_cam: float = 0.0
+
+
+@dataclass
+class RangerStats:
+    query_points: int = 0
+    image_pixels: int = 0
+    n_far: int = 0
+    n_close: int = 0
+
+
+@dataclass
+class CensusCache:
+    """template_match.hpp:229-234."""
+    full_left: CensusImage = field(default_factory=CensusImage)
+    full_right: CensusImage = field(default_factory=CensusImage)
+    scaled_left: CensusImage = field(default_factory=CensusImage)
+    scaled_right: CensusImage = field(default_factory=CensusImage)
+    has_full: bool = False
+    has_scaled: bool = False
+
+
+@dataclass
+class AggregationResult:
+    valid: bool = False
+    disparity: float = 0.0
+    run_length: int = 0
+
+
+def dets_array(dets: Sequence[Detection]):
+    arr = (_abi.Detection * max(len(dets), 1))(
+        *[_abi.Detection(d.cx, d.cy, d.w, d.h, d.class_id, d.id) for d in dets])
+    return arr
+
+
+def validate(cfg: RangerConfig, ctx: Optional[Context] = None) -> None:
+    """template_match.hpp:48-61."""
+    ctx = ctx or default_context()
+    c = cfg.to_c()
+    ctx.check(lib().rg_validate_ranger_config(ctx.handle, C.byref(c)))
+
+
+def to_pixel_box(d: Detection, img_w: int, img_h: int) -> PixelBox:
+    """detection.hpp:23-30."""
+    return PixelBox((d.cx - d.w / 2) * img_w, (d.cy - d.h / 2) * img_h, (d.cx + d.w / 2) * img_w,
+                    (d.cy + d.h / 2) * img_h)
+
+
+def classify_far_close(d: Detection, img_w: int, img_h: int, tau_s: float) -> int:
+    """template_match.hpp:63-67."""
+    return KIND_FAR if max(d.w * img_w, d.h * img_h) < tau_s else KIND_CLOSE
+
+
+def select_objects(dets: Sequence[Detection], cfg: RangerConfig, ctx: Optional[Context] = None) -> List[int]:
+    """template_match.hpp:94-114 (runs the device planner's rank kernel)."""
+    ctx = ctx or default_context()
+    n = len(dets)
+    out = np.zeros(max(n, 1), np.int32)
+    cnt = C.c_int()
+    c = cfg.to_c()
+    ctx.check(lib().rg_select_objects(ctx.handle, dets_array(dets), n, C.byref(c), _ptr(out), C.byref(cnt)))
+    return [int(i) for i in out[:cnt.value]]
+
+
+def find_occluders(dets: Sequence[Detection], ctx: Optional[Context] = None) -> List[List[int]]:
+    """template_match.hpp:71-89."""
+    ctx = ctx or default_context()
+    n = len(dets)
+    off = np.zeros(n + 1, np.int32)
+    idx = np.zeros(max(n * n, 1), np.int32)
+    ctx.check(lib().rg_find_occluders(ctx.handle, dets_array(dets), n, _ptr(off), _ptr(idx)))
+    return [[int(j) for j in idx[off[i]:off[i + 1]]] for i in range(n)]
+
+
+def sample_query_points(det: Detection, kind: int, occluder_boxes: Sequence[PixelBox], cfg: RangerConfig,
+                        img_w: int, img_h: int, ctx: Optional[Context] = None) -> List[QueryBlock]:
+    """template_match.hpp:155-223 (runs the device sampler)."""
+    ctx = ctx or default_context()
+    occ = np.asarray([[b.x0, b.y0, b.x1, b.y1] for b in occluder_boxes], np.float64).reshape(-1, 4)
+    occ = np.ascontiguousarray(occ)
+    pb = to_pixel_box(det, img_w, img_h)
+    if kind == KIND_FAR:
+        cap_blocks = 1
+    else:  # template_match.hpp:191-193
+        half = cfg.tau_s / 2
+        cap_blocks = max(2, int((pb.x1 - pb.x0) / half)) * max(2, int((pb.y1 - pb.y0) / half))
+    cap_pts = cap_blocks * max(cfg.max_total_points, 1) + 64
+    boff = np.zeros(cap_blocks + 1, np.int64)
+    pts = np.zeros((cap_pts, 2), np.int32)
+    rg = (_abi.SearchRange * cap_blocks)()
+    nb = C.c_int()
+    c = cfg.to_c()
+    d = dets_array([det])
+    ctx.check(lib().rg_sample_query_points(ctx.handle, d, kind, _ptr(occ) if occ.size else None, len(occ),
+                                           C.byref(c), img_w, img_h, _ptr(boff), _ptr(pts), rg, cap_blocks,
+                                           cap_pts, C.byref(nb)))
+    blocks = []
+    for b in range(nb.value):
+        p = [(int(x), int(y)) for x, y in pts[boff[b]:boff[b + 1]]]
+        blocks.append(QueryBlock(p, rg[b].dx_min, rg[b].dx_max, rg[b].dy_min, rg[b].dy_max, -1, kind))
+    return blocks
+
+
+def aggregate_close_disparities(disps: Sequence[float], tau_d: float, n_min: int,
+                                ctx: Optional[Context] = None) -> AggregationResult:
+    """template_match.hpp:126-148."""
+    ctx = ctx or default_context()
+    v = np.ascontiguousarray(np.asarray(disps, np.float64).reshape(-1))
+    valid, run = C.c_int32(), C.c_int32()
+    disp = C.c_double()
+    ctx.check(lib().rg_aggregate_close_disparities(ctx.handle, _ptr(v) if v.size else None, v.size,
+                                                   float(tau_d), int(n_min), C.byref(valid), C.byref(disp),
+                                                   C.byref(run)))
+    return AggregationResult(bool(valid.value), disp.value, run.value)
+
+
+def estimate_object_disparities(left, right, dets: Sequence[Detection], cfg: RangerConfig,
+                                cache: Optional[CensusCache] = None, workers: int = 1,
+                                stats: Optional[RangerStats] = None, focal_px: float = 0.0,
+                                baseline_m: float = 0.0, ctx: Optional[Context] = None
+                                ) -> List[ObjectDisparity]:
+    """template_match.hpp:260-363: one entry per selected detection, in input order."""
+    ctx = ctx or default_context()
+    L, R = _gray(left), _gray(right)
+    if L.shape != R.shape:
+        raise InvalidArgument("estimate_object_disparities: image dims differ")
+    h, w = L.shape
+    n = len(dets)
+    out = (_abi.ObjectDisparity * max(n, 1))()
+    n_out = C.c_int()
+    st = _abi.RangerStats()
+    c = cfg.to_c()
+    cc = None
+    bufs = []
+    if cache is not None:
+        s = max(cfg.close_scale, 1)
+        cw, ch = w // s, h // s
+        fl = np.ascontiguousarray(cache.full_left.codes, np.uint32) if cache.has_full else np.zeros((h, w), np.uint32)
+        fr = np.ascontiguousarray(cache.full_right.codes, np.uint32) if cache.has_full else np.zeros((h, w), np.uint32)
+        sl = np.ascontiguousarray(cache.scaled_left.codes, np.uint32) if cache.has_scaled else np.zeros((ch, cw), np.uint32)
+        sr = np.ascontiguousarray(cache.scaled_right.codes, np.uint32) if cache.has_scaled else np.zeros((ch, cw), np.uint32)
+        bufs = [fl, fr, sl, sr]
+        cc = _abi.CensusCache(fl.ctypes.data, fr.ctypes.data, sl.ctypes.data, sr.ctypes.data,
+                              int(cache.has_full), int(cache.has_scaled))
+    ctx.check(lib().rg_estimate_object_disparities(ctx.handle, _ptr(L), _ptr(R), w, h, dets_array(dets), n,
+                                                   C.byref(c), C.byref(cc) if cc is not None else None,
+                                                   float(focal_px), float(baseline_m), out, C.byref(n_out),
+                                                   C.byref(st)))
+    if cache is not None:
+        s = max(cfg.close_scale, 1)
+        cw, ch = w // s, h // s
+        if cc.has_full and not cache.has_full:
+            cache.full_left = CensusImage(w, h, bufs[0], 1.0, 1.0)
+            cache.full_right = CensusImage(w, h, bufs[1], 1.0, 1.0)
+            cache.has_full = True
+        if cc.has_scaled and not cache.has_scaled:
+            cache.scaled_left = CensusImage(cw, ch, bufs[2], cw / w, ch / h)
+            cache.scaled_right = CensusImage(cw, ch, bufs[3], cw / w, ch / h)
+            cache.has_scaled = True
+    if stats is not None:
+        stats.query_points, stats.image_pixels = st.query_points, st.image_pixels
+        stats.n_far, stats.n_close = st.n_far, st.n_close
+    return [ObjectDisparity(o.det_id, o.disparity, o.kind, o.n_blocks_used, bool(o.valid), o.z_cam)
+            for o in out[:n_out.value]]
+
+
+# ============================================================ bm.hpp / autorect.hpp
+@dataclass
+class BmParams:
+    """bm.hpp:15-22 with the reference's defaults."""
+    num_disparities: int = 64
+    block_size: int = 9
+    min_disparity: int = 0
+    texture_threshold: float = 10
+    uniqueness_ratio: float = 10
+    downscale: int = 1
+
+    def to_c(self) -> _abi.BmParams:
+        return _abi.BmParams(self.num_disparities, self.block_size, self.min_disparity, self.downscale,
+                             float(self.texture_threshold), float(self.uniqueness_ratio))
+
+
+@dataclass
+class ImageRoi:
+    x0: int = 0
+    y0: int = 0
+    x1: int = 0
+    y1: int = 0
+
+    def width(self) -> int:
+        return self.x1 - self.x0
+
+    def height(self) -> int:
+        return self.y1 - self.y0
+
+
+def validate_bm(p: BmParams, ctx: Optional[Context] = None) -> None:
+    ctx = ctx or default_context()
+    c = p.to_c()
+    ctx.check(lib().rg_validate_bm_params(ctx.handle, C.byref(c)))
+
+
+def bm_disparity(left, right, p: BmParams, workers: int = 1, ctx: Optional[Context] = None) -> np.ndarray:
+    """bm.hpp:113-135: raw int16 map (16 sub-levels, RAW_INVALID = invalid)."""
+    ctx = ctx or default_context()
+    L, R = _gray(left), _gray(right)
+    if L.shape != R.shape:
+        c = p.to_c()
+        ctx.check(lib().rg_validate_bm_params(ctx.handle, C.byref(c)))
+        raise InvalidArgument("bm_disparity: image dims differ")
+    h, w = L.shape
+    out = np.zeros((h, w), np.int16)
+    c = p.to_c()
+    ctx.check(lib().rg_bm_disparity(ctx.handle, _ptr(L), _ptr(R), w, h, C.byref(c), _ptr(out)))
+    return out
+
+
+def auto_rect_search(left, right, roi: ImageRoi, delta_min: int, delta_max: int, bm: BmParams,
+                     workers: int = 1, ctx: Optional[Context] = None, counts_out: Optional[list] = None) -> int:
+    """autorect.hpp:22-58."""
+    ctx = ctx or default_context()
+    L, R = _gray(left), _gray(right)
+    h, w = L.shape
+    r = _abi.Rect(roi.x0, roi.y0, roi.x1, roi.y1)
+    c = bm.to_c()
+    if L.shape != R.shape:
+        if roi.width() < bm.block_size or roi.height() < bm.block_size:
+            raise InvalidArgument("auto_rect_search: ROI smaller than the match window")
+        if roi.x0 < 0 or roi.y0 < 0 or roi.x1 > w or roi.y1 > h:
+            raise InvalidArgument("auto_rect_search: ROI leaves the image")
+        if delta_min > delta_max:
+            raise InvalidArgument("auto_rect_search: empty delta range")
+        raise InvalidArgument("auto_rect_search: image dims differ")
+    best = C.c_int32()
+    nd = max(delta_max - delta_min + 1, 1)
+    counts = np.zeros(nd, np.int64)
+    ctx.check(lib().rg_auto_rect_search(ctx.handle, _ptr(L), _ptr(R), w, h, C.byref(r), delta_min, delta_max,
+                                        C.byref(c), C.byref(best), _ptr(counts)))
+    if counts_out is not None:
+        counts_out[:] = [int(x) for x in counts]
+    return best.value
+
+
+class RectOffsetState:
+    """autorect.hpp:62-75 (host-side sequential consumer of the search)."""
+
+    def __init__(self, k: int = 5, rate: float = 1):
+        if k < 1:
+            raise InvalidArgument("RectOffsetState: window must be >= 1")
+        self.window, self.delta_max, self.current = k, float(rate), 0.0
+        self.history: List[int] = []
+        self.next = 0
+
+
+def filter_offset(st: RectOffsetState, delta_star: int) -> float:
+    """autorect.hpp:77-90: lower median of the window, rate-limited."""
+    if len(st.history) < st.window:
+        st.history.append(delta_star)
+    else:
+        st.history[st.next] = delta_star
+        st.next = (st.next + 1) % len(st.history)
+    srt = sorted(st.history)
+    cand = float(srt[(len(srt) - 1) // 2])
+    step = min(max(cand - st.current, -st.delta_max), st.delta_max)
+    st.current += step
+    return st.current
+
+
+def range_z(disparity: float, focal_px: float, baseline_m: float) -> float:
+    """geometry.hpp:142-146 with the canonical Q (:124-127): z = f / ((1/b) d)."""
+    return focal_px / ((1.0 / baseline_m) * disparity)
