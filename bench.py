@@ -1,0 +1,427 @@
+#!/usr/bin/env python
+"""Benchmark: boxes ranged/s & stereo frames/s at 1920x1080 with 64 boxes
+(BASELINE.json metric, config C2), p50 frame latency, on N GPUs.
+
+One step = the hot path (census -> planner -> fused sampler/matcher with
+forward-backward verification and sub-pixel fit -> aggregation + range) over
+a batch of F synthetic C2 frames resident in HBM, followed by the NCCL gather
+of the per-box results to rank 0 (frames shard across ranks: weak scaling).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--frames F]
+  python bench.py --impl reference      # the reference's CPU path on the host cores
+
+Prints one JSON line (rank 0).  Needs the CUDA library (build() first).
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "boxes ranged/sec & stereo frames/sec at 1920x1080, 64 boxes; p50 frame latency"
+W, H = 1920, 1080
+CENSUS_BYTES_PER_FRAME = 2 * (W * H + 4 * W * H + 4 * (W // 2) * (H // 2))  # 24,883,200
+POPC_PER_CLK_PER_SM = 16  # CUDA programming guide throughput table (cc 8.x-9.0)
+N_SM = 148
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), float(p.get("sm_max_mhz", 1965.0)), "measured"
+    except Exception:
+        return 6650.0, 1965.0, "fallback"
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,utilization.gpu")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        rows = self.rows
+        busy = [r for r in rows if r[6].isdigit() and int(r[6]) > 0] or rows
+        sm = [float(r[0]) for r in busy if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ------------------------------------------------------------------ frames
+def make_frames(n_distinct: int, seed0: int, noise: float = 2.0):
+    """C2 frames: fixed 64-box layout, per-frame noise seed."""
+    from paper_2604_07980_b200 import synth as S
+    from concurrent.futures import ThreadPoolExecutor
+
+    sc0, cfg = S.scene_c2(seed=seed0, noise=noise)
+    dets = S.ground_truth_detections(sc0)
+
+    def render(i):
+        sc, _ = S.scene_c2(seed=seed0 + i, noise=noise)
+        return S.render_stereo_pair(sc)
+
+    with ThreadPoolExecutor(max_workers=2) as ex:  # renderer is itself row-parallel
+        pairs = list(ex.map(render, range(n_distinct)))
+    L = np.stack([p[0] for p in pairs])
+    R = np.stack([p[1] for p in pairs])
+    return L, R, dets, cfg
+
+
+def cpu_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_reference_run(L, R, dets, cfg, seconds: float, threads: int):
+    """Time the reference (oracle/_ref, compiled from the reference headers) on
+    the host cores, frame-parallel (SURVEY 8(d) mode iii), bounded in time."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import oracle_lib
+    from paper_2604_07980_b200 import _abi
+    from paper_2604_07980_b200.engine import OUT_DTYPE, pack_detections
+
+    if oracle_lib.have_reference():
+        chk, kind = oracle_lib.reference(), "reference"
+    else:
+        return None
+    n = L.shape[0]
+    recs, offs = pack_detections([dets] * n)
+    c = cfg.to_c()
+    out_stride = min(len(dets), cfg.max_objects)
+    out = np.zeros(n * out_stride, OUT_DTYPE)
+    cnt = np.zeros(n, np.int32)
+    Lc, Rc = np.ascontiguousarray(L), np.ascontiguousarray(R)
+    frames, wall = 0, 0.0
+    boxes = 0
+    while wall < seconds:
+        t = chk.lib.ref_bench_estimate(Lc.ctypes.data, Rc.ctypes.data, W, H, n, recs.ctypes.data, offs.ctypes.data,
+                                       C.byref(c), threads, out.ctypes.data, out_stride, cnt.ctypes.data)
+        wall += t
+        frames += n
+        boxes += int(cnt.sum())
+    return {"value": boxes / wall, "unit": "boxes/s", "frames_per_sec": frames / wall, "cores": threads,
+            "kind": kind, "sample": f"{frames} C2 frames ({n} distinct, noise 2.0) ranged by the reference's "
+                                    f"estimate_object_disparities, {threads} threads x whole frames at workers=1, "
+                                    f"{wall:.1f} s"}
+
+
+# ------------------------------------------------------------------ reference arm
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    threads = cpu_threads()
+    L, R, dets, cfg = make_frames(max(threads, 8), 1)
+    per_step = []
+    boxes = fps = None
+    for i in range(args.warmup + args.steps):
+        r = cpu_reference_run(L, R, dets, cfg, seconds=args.ref_seconds, threads=threads)
+        if r is None:
+            print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libranger_ref.so not built"}))
+            return 0
+        if i >= args.warmup:
+            per_step.append(r)
+    val = statistics.median([r["value"] for r in per_step])
+    fps = statistics.median([r["frames_per_sec"] for r in per_step])
+    line = {
+        "metric": METRIC, "impl": "reference", "value": val, "unit": "boxes/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * 64 / val,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8/u32/f64",
+        "data": "synthetic", "frames_per_sec": fps,
+        "config": {"workload": "C2: 1920x1080 stereo, 64 boxes (48 FAR + 16 CLOSE), dx_max 256, "
+                               "fwd-bwd + sub-pixel, noise 2.0", "frames_per_step": "time-bounded sample"},
+        "cpu_baseline": {"value": val, "unit": "boxes/s", "cores": threads, "kind": per_step[0]["kind"],
+                         "sample": per_step[0]["sample"]},
+        "e2e": {"value": val, "unit": "boxes/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+# ------------------------------------------------------------------ our arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--frames", type=int, default=256, help="frames per step per GPU")
+    ap.add_argument("--distinct", type=int, default=32, help="distinct rendered frames in the HBM ring")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--ref-seconds", type=float, default=8.0)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--latency-runs", type=int, default=300)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    os.environ["RG_DEVICE"] = str(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_2604_07980_b200 import ranger as rg
+    from paper_2604_07980_b200.engine import DET_DTYPE, OUT_DTYPE, FrameEngine, pack_detections
+    from paper_2604_07980_b200 import synth as S
+
+    F = args.frames
+    L, R, dets, cfg = make_frames(args.distinct, 1 + rank * 100003)
+    n_boxes = len(dets)
+    ctx = rg.Context(local)
+    eng = FrameEngine(W, H, cfg, n_boxes, S.F_PX, S.BASELINE_M, ctx=ctx)
+    dev = torch.device("cuda", local)
+    # HBM ring: F frames (> L2 in bytes), tiled from the distinct renders
+    idx = np.arange(F) % args.distinct
+    dL = torch.from_numpy(L[idx]).to(dev)
+    dR = torch.from_numpy(R[idx]).to(dev)
+    recs, offs = pack_detections([dets] * F)
+    d_dets = torch.from_numpy(recs.view(np.uint8)).to(dev)
+    d_offs = torch.from_numpy(offs).to(dev)
+    d_out = torch.zeros(F * eng.out_stride * OUT_DTYPE.itemsize, dtype=torch.uint8, device=dev)
+    d_cnt = torch.zeros(F, dtype=torch.int32, device=dev)
+    gather = torch.zeros(world * d_out.numel(), dtype=torch.uint8, device=dev) if world > 1 else None
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        eng.range_device(dL, dR, d_dets, d_offs, d_out, d_cnt, stream=stream.cuda_stream)
+        if world > 1:  # per-box results -> every rank's slab on rank 0 (NCCL over NVLink)
+            dist.all_gather_into_tensor(gather, d_out)
+
+    # ---- warmup
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    # parity spot check of the bench frames against the C oracle (frame 0)
+    spot = None
+    if rank == 0:
+        try:
+            sys.path.insert(0, os.path.join(ROOT, "tests"))
+            import oracle_lib
+            from paper_2604_07980_b200 import _abi
+            want, _ = oracle_lib.oracle().estimate(L[0], R[0], [_abi.Detection(d.cx, d.cy, d.w, d.h, d.class_id, d.id)
+                                                                for d in dets], cfg.to_c(), S.F_PX, S.BASELINE_M)
+            got = np.frombuffer(d_out.cpu().numpy().tobytes(), OUT_DTYPE)[:int(d_cnt[0])]
+            spot = bool(len(got) == len(want) and all(bytes(w) == got[i].tobytes() for i, w in enumerate(want)))
+        except Exception as e:  # pragma: no cover
+            spot = f"error: {e}"
+
+    # ---- timed region (device-resident feed)
+    ctx.reset_counters()
+    ctx.set_profiling(True)
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = e0.elapsed_time(e1)
+    clk = clocks.stop()
+    ctx.set_profiling(False)
+    stage_ms, stage_launches, total_launches = ctx.counters()
+    evals, blocks = ctx.work()
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    boxes_step = int(d_cnt.sum().item())
+    total_boxes = boxes_step * args.steps * world
+    value = total_boxes / (ms_max / 1000.0)
+    fps = F * args.steps * world / (ms_max / 1000.0)
+
+    # ---- end-to-end through the public host API (pinned host frames, H2D/D2H inside)
+    keep = []
+
+    def pin(a):  # pinned host copy of any numpy array (structured dtypes included)
+        t = torch.empty(a.nbytes, dtype=torch.uint8).pin_memory()
+        keep.append(t)
+        v = t.numpy().view(a.dtype).reshape(a.shape)
+        v[...] = a
+        return v
+    hL, hR = pin(L[idx]), pin(R[idx])
+    h_recs, h_offs = pin(recs), pin(offs)
+    h_out = pin(np.zeros(F * eng.out_stride, OUT_DTYPE))
+    h_cnt = pin(np.zeros(F, np.int32))
+    for _ in range(2):
+        eng.range_host(hL, hR, h_recs, h_offs, h_out, h_cnt, chunk=32, stream=stream.cuda_stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    e2e_steps = max(2, args.steps // 2)
+    for _ in range(e2e_steps):
+        eng.range_host(hL, hR, h_recs, h_offs, h_out, h_cnt, chunk=32, stream=stream.cuda_stream)
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+    te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = int(h_cnt.sum()) * e2e_steps * world / float(te.item())
+    h2d = int(hL.nbytes + hR.nbytes + h_recs.nbytes + h_offs.nbytes)
+    d2h = int(h_out.nbytes + h_cnt.nbytes)
+
+    # ---- p50 latency: one frame, host in -> per-box results on host
+    lat = []
+    for i in range(args.latency_runs):
+        a = time.perf_counter()
+        eng.range_host(hL[i % F:i % F + 1], hR[i % F:i % F + 1], h_recs[:n_boxes], h_offs[:2] - 0, h_out[:eng.out_stride],
+                       h_cnt[:1], chunk=1, stream=stream.cuda_stream)
+        lat.append(time.perf_counter() - a)
+    lat_dev = []
+    for i in range(max(50, args.latency_runs // 3)):
+        a = time.perf_counter()
+        eng.range_device(dL[i % F:i % F + 1], dR[i % F:i % F + 1], d_dets, d_offs[:2], d_out, d_cnt,
+                         stream=stream.cuda_stream)
+        torch.cuda.synchronize()
+        lat_dev.append(time.perf_counter() - a)
+
+    # ---- auto-rectification offset search (config C4), timed separately
+    rect = None
+    try:
+        nrf = 8
+        best = torch.zeros(nrf, dtype=torch.int32, device=dev)
+        cnts = torch.zeros(nrf * 17, dtype=torch.int64, device=dev)
+        for _ in range(2):
+            eng.auto_rect_device(dL[:nrf], dR[:nrf], S.C4_ROI, -8, 8, S.c4_bm(), best, cnts, stream=stream.cuda_stream)
+        torch.cuda.synchronize()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        reps = 3
+        for _ in range(reps):
+            eng.auto_rect_device(dL[:nrf], dR[:nrf], S.C4_ROI, -8, 8, S.c4_bm(), best, cnts, stream=stream.cuda_stream)
+        a1.record(stream)
+        torch.cuda.synchronize()
+        rms = a0.elapsed_time(a1) / (reps * nrf)
+        cells = 960 * 540 * 32 * 17
+        rect = {"config": "C4: 960x540 ROI, 32 disparities (d_min -4), 9x9 SAD, delta -8..8",
+                "ms_per_frame": rms, "frames_per_sec": 1000.0 / rms,
+                "window_evals_per_sec": cells / (rms / 1000.0), "delta_star_frame0": int(best[0].item())}
+    except Exception as e:  # pragma: no cover
+        rect = {"error": str(e)}
+
+    # ---- roofline of the dominant kernel (stage times from CUDA events on our stream)
+    hbm_peak, sm_max, peak_kind = peaks()
+    census_ms = stage_ms[0] / max(stage_launches[0], 1)
+    match_ms = stage_ms[2] / max(stage_launches[2], 1)
+    census_gbs = CENSUS_BYTES_PER_FRAME * F / (census_ms / 1000.0) / 1e9
+    evals_per_launch = evals / max(stage_launches[2], 1)
+    clk_mhz = clk["sm_mhz"] or sm_max
+    popc_peak = POPC_PER_CLK_PER_SM * N_SM * clk_mhz * 1e6
+    match_rate = evals_per_launch / (match_ms / 1000.0)
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            tr = json.load(f)
+        traffic = tr.get("census_bytes_per_frame", None)
+        traffic = traffic * F if traffic else None
+    except Exception:
+        pass
+    census_roof = {"bound": "hbm", "achieved": census_gbs, "peak": hbm_peak, "unit": "GB/s",
+                   "frac": census_gbs / hbm_peak, "traffic": traffic, "kernel": "census_frames_kernel",
+                   "peak_source": peak_kind, "algorithmic_bytes_per_launch": CENSUS_BYTES_PER_FRAME * F,
+                   "ms_per_launch": census_ms}
+    match_roof = {"bound": "int/popc", "achieved": match_rate / 1e12, "peak": popc_peak / 1e12,
+                  "unit": "Tevals/s", "frac": match_rate / popc_peak, "kernel": "match_slots_kernel",
+                  "hamming_evals_per_launch": evals_per_launch, "ms_per_launch": match_ms,
+                  "peak_source": f"nominal {POPC_PER_CLK_PER_SM} POPC/clk/SM x {N_SM} SMs x {clk_mhz:.0f} MHz"}
+    dominant = census_roof if census_ms >= match_ms else match_roof
+    step_ms = ms_max / args.steps
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_reference_run(L[:min(args.distinct, cpu_threads() * 2)], R[:min(args.distinct, cpu_threads() * 2)],
+                                    dets, cfg, seconds=args.cpu_seconds, threads=cpu_threads())
+        except Exception as e:  # pragma: no cover
+            cpu = {"error": str(e)}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "boxes/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u8/u32/f64", "data": "synthetic",
+            "frames_per_sec": fps, "boxes_per_frame": boxes_step / F,
+            "p50_latency_ms": 1000 * statistics.median(lat), "p50_latency_device_ms": 1000 * statistics.median(lat_dev),
+            "config": {"workload": "C2: 1920x1080 rendered stereo pairs, 64 boxes (48 FAR + 16 CLOSE), "
+                                   "dx_max_far = dx_max_close = 256, tau_v 1.0, fwd-bwd + sub-pixel, range z",
+                       "frames_per_step_per_gpu": F, "distinct_frames": args.distinct, "noise_sigma": 2.0,
+                       "l2": f"inputs {2 * F * W * H / 1e6:.0f} MB + census {F * CENSUS_BYTES_PER_FRAME / 1e6:.0f} MB "
+                             f"per step > 126 MB L2 (no flush needed)",
+                       "parallelism": f"frame-sharded dp{world}, NCCL all_gather of per-box results"},
+            "e2e": {"value": e2e_value, "unit": "boxes/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "api": "rg_range_frames_host (pinned host frames, chunked H2D/compute/D2H)"},
+            "gpu_launches": int(total_launches),
+            "roofline": dominant,
+            "kernels": {"census": census_roof, "matcher": match_roof,
+                        "stage_ms_per_step": {k: v / args.steps for k, v in
+                                              zip(["census", "plan", "match", "aggregate"], stage_ms[:4])}},
+            "hamming_evals_per_frame": evals / max(F * args.steps, 1),
+            "autorect": rect,
+            "clocks": clk,
+            "parity_spot_check_vs_oracle": spot,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

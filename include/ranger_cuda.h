@@ -65,6 +65,10 @@ rg_status rg_set_profiling(rg_ctx* ctx, int on);
 rg_status rg_get_counters(rg_ctx* ctx, double times_ms[5], int64_t launches[5],
                           int64_t* total_launches);
 rg_status rg_reset_counters(rg_ctx* ctx);
+/* Algorithmic work of the batched path since the last reset: Hamming
+ * evaluations (sum over blocks and candidates of contributing points,
+ * census.hpp:209-221, forward + backward) and planned blocks (slots). */
+rg_status rg_get_work(rg_ctx* ctx, int64_t* hamming_evals, int64_t* blocks);
 
 /* ---------------------------------------------------------------- types */
 

@@ -107,6 +107,7 @@ SIGNATURES = {
     "rg_set_profiling": (I, [P, I]),
     "rg_get_counters": (I, [P, P, P, P]),
     "rg_reset_counters": (I, [P]),
+    "rg_get_work": (I, [P, P, P]),
     "rg_census_code_at": (I, [P, P, I, I, I, I, P]),
     "rg_census_transform": (I, [P, P, I, I, I, I, P]),
     "rg_census_transform_rois": (I, [P, P, I, I, I, I, P, I, P]),

@@ -263,7 +263,7 @@ rg_status enqueue_pipeline(rg_ctx* ctx, const FrameJob& J, const rg_ranger_confi
   NEED(scratch);
   int32_t *ix = nullptr, *iy = nullptr;
   TRY(upload_inverse_maps(ctx, w, h, cw, ch, s, &ix, &iy));
-  RG_CUDA(ctx, cudaMemsetAsync(counters, 0, 2 * sizeof(int32_t), s));
+  RG_CUDA(ctx, cudaMemsetAsync(counters, 0, 4 * sizeof(int32_t), s));
   const bool prof = ctx->profiling;
   if (prof) RG_CUDA(ctx, cudaEventRecord(ctx->ev[0], s));
   // K1 census (full + fused reduced raster) of both images of every frame
@@ -314,11 +314,17 @@ void accumulate_profile(rg_ctx* ctx) {
 rg_status finish_pipeline(rg_ctx* ctx, const FrameJob& J, const rg_ranger_config& cfg,
                           cudaStream_t s, int32_t* counters, int32_t* hc, PipelineBufs* pb) {
   for (int attempt = 0;; ++attempt) {
-    RG_CUDA(ctx, cudaMemcpyAsync(hc, counters, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    RG_CUDA(ctx, cudaMemcpyAsync(hc, counters, 4 * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     RG_CUDA(ctx, cudaStreamSynchronize(s));
     accumulate_profile(ctx);
     ctx->last_slots = hc[0];
-    if (!hc[1]) return RG_OK;
+    if (!hc[1]) {
+      int64_t ev;
+      std::memcpy(&ev, hc + 2, sizeof(ev));
+      ctx->hamming_evals += ev;
+      ctx->slots_total += hc[0];
+      return RG_OK;
+    }
     if (attempt >= 3) return set_err(ctx, RG_EOVERFLOW, "device block list overflow");
     ctx->slot_capacity = std::max(ctx->slot_capacity * 2, hc[0] + hc[0] / 4 + 64);
     TRY(enqueue_pipeline(ctx, J, cfg, s, counters, pb));
@@ -328,8 +334,8 @@ rg_status finish_pipeline(rg_ctx* ctx, const FrameJob& J, const rg_ranger_config
 // run + overflow check (synchronous)
 rg_status run_pipeline(rg_ctx* ctx, const FrameJob& J, const rg_ranger_config& cfg, cudaStream_t s,
                        PipelineBufs* pb) {
-  int32_t* counters = DBUF(int32_t, ctx, B_COUNTERS, 2);
-  int32_t* hc = static_cast<int32_t*>(host_buf(ctx, 0, 2 * sizeof(int32_t)));
+  int32_t* counters = DBUF(int32_t, ctx, B_COUNTERS, 4);
+  int32_t* hc = static_cast<int32_t*>(host_buf(ctx, 0, 4 * sizeof(int32_t)));
   NEED(counters);
   NEED(hc);
   TRY(enqueue_pipeline(ctx, J, cfg, s, counters, pb));
@@ -413,8 +419,17 @@ rg_status rg_get_counters(rg_ctx* ctx, double times_ms[5], int64_t launches[5], 
   return RG_OK;
 }
 
+rg_status rg_get_work(rg_ctx* ctx, int64_t* hamming_evals, int64_t* blocks) {
+  if (!ctx) return RG_EINVAL;
+  if (hamming_evals) *hamming_evals = ctx->hamming_evals;
+  if (blocks) *blocks = ctx->slots_total;
+  return RG_OK;
+}
+
 rg_status rg_reset_counters(rg_ctx* ctx) {
   if (!ctx) return RG_EINVAL;
+  ctx->hamming_evals = 0;
+  ctx->slots_total = 0;
   for (int i = 0; i < 5; ++i) {
     ctx->stage_ms[i] = 0;
     ctx->stage_launches[i] = 0;
@@ -876,9 +891,9 @@ rg_status rg_range_frames_host(rg_ctx* ctx, const rg_frame_batch* b, const rg_ra
   int32_t* st_o = DBUF(int32_t, ctx, B_DET_OFF, 2 * (size_t)(chunk + 1));
   rg_object_disparity* st_out = DBUF(rg_object_disparity, ctx, B_OUT, 2 * (size_t)chunk * b->out_stride);
   int32_t* st_cnt = DBUF(int32_t, ctx, B_OUT_CNT, 2 * (size_t)chunk);
-  int32_t* counters = DBUF(int32_t, ctx, B_COUNTERS, 2);
+  int32_t* counters = DBUF(int32_t, ctx, B_COUNTERS, 4);
   int32_t* hoffs = static_cast<int32_t*>(host_buf(ctx, 1, sizeof(int32_t) * 2 * (chunk + 1)));
-  int32_t* hc = static_cast<int32_t*>(host_buf(ctx, 0, 2 * sizeof(int32_t)));
+  int32_t* hc = static_cast<int32_t*>(host_buf(ctx, 0, 4 * sizeof(int32_t)));
   NEED(st_l);
   NEED(st_r);
   NEED(st_d);

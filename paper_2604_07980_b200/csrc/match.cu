@@ -111,7 +111,8 @@ __device__ __forceinline__ uint32_t sample(const Raster& r, int x, int y) {
 // Candidate sweep over one chunk of CPT candidates per thread.
 template <int CPT, int MODE>  // MODE 0: window, no zeros; 1: window with zeros; 2: global
 __device__ __forceinline__ void sweep(const Dyn& S, int nv, const Raster& R, int c0, int nc,
-                                      int ndx, int WW, const rg_search_range& rg, Best& mine) {
+                                      int ndx, int WW, const rg_search_range& rg, Best& mine,
+                                      int& evals) {
   const int tid = threadIdx.x;
   int base[CPT], cdx[CPT], cdy[CPT];
   bool ok[CPT];
@@ -177,6 +178,7 @@ __device__ __forceinline__ void sweep(const Dyn& S, int nv, const Raster& R, int
 #pragma unroll
   for (int j = 0; j < CPT; ++j) {
     if (!ok[j] || n[j] == 0) continue;
+    evals += n[j];  // Hamming evaluations, census.hpp:209-221
     const Best cand = {s[j], n[j], cdx[j], cdy[j]};
     if (better(cand, mine)) mine = cand;
   }
@@ -184,13 +186,13 @@ __device__ __forceinline__ void sweep(const Dyn& S, int nv, const Raster& R, int
 
 template <int MODE>
 __device__ __forceinline__ void sweep_all(const Dyn& S, int nv, const Raster& R, int nc, int ndx,
-                                          int WW, const rg_search_range& rg, Best& mine) {
+                                          int WW, const rg_search_range& rg, Best& mine, int& evals) {
   if (nc <= NT) {
-    sweep<1, MODE>(S, nv, R, 0, nc, ndx, WW, rg, mine);
+    sweep<1, MODE>(S, nv, R, 0, nc, ndx, WW, rg, mine, evals);
   } else if (nc <= 2 * NT) {
-    sweep<2, MODE>(S, nv, R, 0, nc, ndx, WW, rg, mine);
+    sweep<2, MODE>(S, nv, R, 0, nc, ndx, WW, rg, mine, evals);
   } else {
-    for (int c0 = 0; c0 < nc; c0 += 4 * NT) sweep<4, MODE>(S, nv, R, c0, nc, ndx, WW, rg, mine);
+    for (int c0 = 0; c0 < nc; c0 += 4 * NT) sweep<4, MODE>(S, nv, R, c0, nc, ndx, WW, rg, mine, evals);
   }
 }
 
@@ -249,7 +251,7 @@ __device__ void block_sum4(int v[4], Scratch& sc) {
 // (shared or global memory) shifted by (sx, sy).  Writes sc.pass.
 __device__ void match_pass(const int2* pts, int np, int sx, int sy, const Raster& L,
                            const Raster& R, const rg_search_range& rg, const Dyn& S,
-                           Scratch& sc) {
+                           Scratch& sc, int& evals) {
   const int tid = threadIdx.x;
   if (tid == 0) {
     sc.nv = 0;
@@ -305,11 +307,11 @@ __device__ void match_pass(const int2* pts, int np, int sx, int sy, const Raster
   }
   Best mine = {0, 0, 0, 0};
   if (use_win && !any_zero)
-    sweep_all<0>(S, nv, R, nc, ndx, WW, rg, mine);
+    sweep_all<0>(S, nv, R, nc, ndx, WW, rg, mine, evals);
   else if (use_win)
-    sweep_all<1>(S, nv, R, nc, ndx, WW, rg, mine);
+    sweep_all<1>(S, nv, R, nc, ndx, WW, rg, mine, evals);
   else
-    sweep_all<2>(S, nv, R, nc, ndx, WW, rg, mine);
+    sweep_all<2>(S, nv, R, nc, ndx, WW, rg, mine, evals);
   const Best b = block_best(mine, sc);
   if (b.n == 0) {  // no offset had a contributing point
     if (tid == 0) sc.pass.has = 0;
@@ -374,7 +376,8 @@ __device__ void finish_pass(const PassOut& p, rg_match_result& r) {
 // block_match / forward_backward_match of one block; result written by tid 0.
 __device__ void match_block(const int2* pts, int np, const Raster& L, const Raster& R,
                             const rg_search_range& rg, int mode, double tau_v, const Dyn& S,
-                            Scratch& sc, rg_match_result* out) {
+                            Scratch& sc, rg_match_result* out, unsigned long long* eval_counter) {
+  int evals = 0;
   rg_match_result r;
   r.dx_int = 0;
   r.dy_int = 0;
@@ -387,12 +390,12 @@ __device__ void match_block(const int2* pts, int np, const Raster& L, const Rast
   r.has_value = 0;
   r.n_points = np;
   if (np > 0) {
-    match_pass(pts, np, 0, 0, L, R, rg, S, sc);
+    match_pass(pts, np, 0, 0, L, R, rg, S, sc, evals);
     if (sc.pass.has) {
       finish_pass(sc.pass, r);
       if (mode == RG_MATCH_FWD_BWD) {
         const rg_search_range brg = {-rg.dx_max, -rg.dx_min, -r.dy_int, -r.dy_int};
-        match_pass(pts, np, -r.dx_int, r.dy_int, R, L, brg, S, sc);
+        match_pass(pts, np, -r.dx_int, r.dy_int, R, L, brg, S, sc, evals);
         if (sc.pass.has) {
           rg_match_result bwd;
           finish_pass(sc.pass, bwd);
@@ -402,6 +405,10 @@ __device__ void match_block(const int2* pts, int np, const Raster& L, const Rast
     }
   }
   if (threadIdx.x == 0) *out = r;
+  if (eval_counter) {  // algorithmic work of this block, one atomic per CTA
+    for (int o = 16; o > 0; o >>= 1) evals += __shfl_xor_sync(0xffffffffu, evals, o);
+    if ((threadIdx.x & 31) == 0 && evals) atomicAdd(eval_counter, (unsigned long long)evals);
+  }
 }
 
 // ---------------------------------------------------------------- CSR path
@@ -418,7 +425,7 @@ __global__ void __launch_bounds__(NT) match_blocks_kernel(Raster L, Raster R,
   const int64_t o0 = offs[b];
   const int np = (int)(offs[b + 1] - o0);
   match_block(reinterpret_cast<const int2*>(pts) + o0, np, L, R, ranges[b], mode, tau_v, S, sc,
-              &out[b]);
+              &out[b], nullptr);
 }
 
 // ------------------------------------------------------------ planner path
@@ -429,7 +436,7 @@ __global__ void __launch_bounds__(NT) match_slots_kernel(
     const uint32_t* __restrict__ fr, const uint32_t* __restrict__ sl,
     const uint32_t* __restrict__ sr, int w, int h, int cw, int ch, int64_t full_stride,
     int64_t scaled_stride, rg_ranger_config cfg, rg_match_result* __restrict__ res,
-    rg_ranger_stats* __restrict__ stats, int maxp) {
+    rg_ranger_stats* __restrict__ stats, int maxp, int32_t* __restrict__ counters) {
   extern __shared__ __align__(16) unsigned char dyn[];
   __shared__ Scratch sc;
   __shared__ double occ[4 * kMaxOccluders];
@@ -493,7 +500,8 @@ __global__ void __launch_bounds__(NT) match_slots_kernel(
   const rg_search_range rg = e.kind == RG_KIND_FAR
                                  ? rg_search_range{0, cfg.dx_max_far, -1, 1}
                                  : rg_search_range{0, (cfg.dx_max_close + s_close - 1) / s_close, -1, 1};
-  match_block(S.pts, np, L, R, rg, RG_MATCH_FWD_BWD, cfg.tau_v, S, sc, out);
+  match_block(S.pts, np, L, R, rg, RG_MATCH_FWD_BWD, cfg.tau_v, S, sc, out,
+              reinterpret_cast<unsigned long long*>(counters + 2));
 }
 
 size_t dyn_bytes(int maxp, bool with_pts) {
@@ -532,7 +540,8 @@ cudaError_t launch_match_slots(const Slot* slots, const int32_t* n_slots_dev, in
   if (e != cudaSuccess) return e;
   match_slots_kernel<<<slot_capacity, NT, smem, s>>>(slots, n_slots_dev, objs, dets, det_off, fl,
                                                      fr, sl, sr, w, h, cw, ch, full_stride,
-                                                     scaled_stride, cfg, res, stats, maxp);
+                                                     scaled_stride, cfg, res, stats, maxp,
+                                                     const_cast<int32_t*>(n_slots_dev));
   return cudaGetLastError();
 }
 

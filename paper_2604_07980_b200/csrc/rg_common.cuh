@@ -60,6 +60,8 @@ struct rg_ctx {
   double stage_ms[5] = {0, 0, 0, 0, 0};
   int64_t stage_launches[5] = {0, 0, 0, 0, 0};
   int64_t total_launches = 0;
+  int64_t hamming_evals = 0;  // algorithmic matcher work of the batched path
+  int64_t slots_total = 0;    // potential QueryBlocks planned
   cudaEvent_t ev[12] = {};
   int slot_capacity = 0;    // grows on RG_EOVERFLOW
   int64_t last_slots = 0;   // slots used by the last batch

@@ -1,0 +1,92 @@
+"""Batched frame ranging engine: the throughput path (one process per GPU).
+
+Frames live on the device (torch uint8 tensors, shape (F, H, W)); detections
+are a packed array of rg_detection records with per-frame CSR offsets.  One
+call ranges every frame of the batch with four kernel launches (census K1,
+planner K3, fused sampler+matcher K2, aggregation+range K4) through
+rg_range_frames; rg_range_frames_host is the host-fed variant that streams
+pinned host frames through double-buffered device staging.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from . import _abi
+from .ranger import Context, Detection, RangerConfig, default_context, lib
+
+DET_DTYPE = np.dtype([("cx", "<f8"), ("cy", "<f8"), ("w", "<f8"), ("h", "<f8"), ("class_id", "<i4"),
+                      ("id", "<i4")])
+OUT_DTYPE = np.dtype([("det_id", "<i4"), ("kind", "<i4"), ("n_blocks_used", "<i4"), ("valid", "<i4"),
+                      ("disparity", "<f8"), ("z_cam", "<f8")])
+assert DET_DTYPE.itemsize == C.sizeof(_abi.Detection) == 40
+assert OUT_DTYPE.itemsize == C.sizeof(_abi.ObjectDisparity) == 32
+
+
+def pack_detections(frames: Sequence[Sequence[Detection]]):
+    """-> (records[DET_DTYPE], offsets[int32, F+1])"""
+    offs = np.zeros(len(frames) + 1, np.int32)
+    recs = []
+    for f, dets in enumerate(frames):
+        recs.extend((d.cx, d.cy, d.w, d.h, d.class_id, d.id) for d in dets)
+        offs[f + 1] = len(recs)
+    arr = np.array(recs, dtype=DET_DTYPE) if recs else np.zeros(0, DET_DTYPE)
+    return arr, offs
+
+
+class FrameEngine:
+    """Ranges batches of W x H stereo pairs with a fixed RangerConfig."""
+
+    def __init__(self, width: int, height: int, cfg: RangerConfig, max_dets_per_frame: int,
+                 focal_px: float = 0.0, baseline_m: float = 0.0, ctx: Optional[Context] = None):
+        self.ctx = ctx or default_context()
+        self.w, self.h = width, height
+        self.cfg = cfg
+        self._c = cfg.to_c()
+        self.max_dets = max_dets_per_frame
+        self.out_stride = max(1, min(max_dets_per_frame, cfg.max_objects))
+        self.focal, self.baseline = focal_px, baseline_m
+
+    def _batch(self, n_frames, pitch, stride, left, right, dets, offs, out, cnt) -> _abi.FrameBatch:
+        return _abi.FrameBatch(n_frames, self.w, self.h, pitch, stride, left, right, dets, offs, self.max_dets,
+                               self.out_stride, out, cnt, self.focal, self.baseline)
+
+    def range_device(self, left, right, dets, offsets, out, out_count, stream=None) -> None:
+        """All arguments are CUDA torch tensors: left/right uint8 (F, H, pitch);
+        dets uint8 view of DET_DTYPE records; offsets int32 (F+1); out uint8
+        (F * out_stride * 32); out_count int32 (F)."""
+        F = left.shape[0]
+        pitch = left.shape[2] if left.dim() == 3 else self.w
+        b = self._batch(F, pitch, left.stride(0), left.data_ptr(), right.data_ptr(), dets.data_ptr(),
+                        offsets.data_ptr(), out.data_ptr(), out_count.data_ptr())
+        s = C.c_void_p(stream) if stream is not None else None
+        self.ctx.check(lib().rg_range_frames(self.ctx.handle, C.byref(b), C.byref(self._c), s))
+
+    def range_host(self, left: np.ndarray, right: np.ndarray, dets: np.ndarray, offsets: np.ndarray,
+                   out: np.ndarray, out_count: np.ndarray, chunk: int = 16, stream=None) -> None:
+        """Host (ideally pinned) numpy buffers; H2D / compute / D2H inside."""
+        F = left.shape[0]
+        b = self._batch(F, self.w, self.w * self.h, left.ctypes.data, right.ctypes.data,
+                        dets.ctypes.data if dets.size else 0, offsets.ctypes.data, out.ctypes.data,
+                        out_count.ctypes.data)
+        s = C.c_void_p(stream) if stream is not None else None
+        self.ctx.check(lib().rg_range_frames_host(self.ctx.handle, C.byref(b), C.byref(self._c), chunk, s))
+
+    def auto_rect_device(self, left, right, roi, delta_min: int, delta_max: int, bm, best, counts=None,
+                         stream=None) -> None:
+        """rg_auto_rect_frames over device frames (torch tensors)."""
+        F = left.shape[0]
+        r = _abi.Rect(*roi)
+        p = bm.to_c()
+        s = C.c_void_p(stream) if stream is not None else None
+        self.ctx.check(lib().rg_auto_rect_frames(
+            self.ctx.handle, left.data_ptr(), right.data_ptr(), F, left.stride(0), left.shape[2], self.w, self.h,
+            C.byref(r), delta_min, delta_max, C.byref(p), best.data_ptr(),
+            counts.data_ptr() if counts is not None else None, s))
+
+
+def unpack_results(out: np.ndarray, counts: np.ndarray, out_stride: int) -> List[np.ndarray]:
+    recs = np.frombuffer(out.tobytes(), dtype=OUT_DTYPE).reshape(-1, out_stride)
+    return [recs[f, :int(counts[f])] for f in range(len(counts))]

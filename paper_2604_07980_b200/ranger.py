@@ -98,6 +98,12 @@ class Context:
         self.check(lib().rg_get_counters(self._h, t, n, C.byref(tot)))
         return list(t), list(n), tot.value
 
+    def work(self) -> Tuple[int, int]:
+        """(Hamming evaluations, planned blocks) of the batched path since the last reset."""
+        ev, bl = C.c_int64(), C.c_int64()
+        self.check(lib().rg_get_work(self._h, C.byref(ev), C.byref(bl)))
+        return ev.value, bl.value
+
     def reset_counters(self) -> None:
         self.check(lib().rg_reset_counters(self._h))
 
