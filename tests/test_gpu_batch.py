@@ -1,0 +1,102 @@
+"""GPU: the batched throughput APIs (rg_range_frames, rg_range_frames_host,
+rg_auto_rect_frames) against the oracle frame by frame, and the drop-in proof
+binaries (the reference's own unit + acceptance tests compiled against
+include/ranger/)."""
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+import oracle_lib
+from paper_2604_07980_b200 import _abi, ranger as rg, synth as S
+from paper_2604_07980_b200.engine import OUT_DTYPE, FrameEngine, pack_detections
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _frames(fn, n, **kw):
+    Ls, Rs, D = [], [], []
+    for i in range(n):
+        sc, cfg = fn(seed=40 + i, noise=2.0, **kw)
+        L, R = S.render_stereo_pair(sc)
+        Ls.append(L)
+        Rs.append(R)
+        D.append(S.ground_truth_detections(sc))
+    return np.stack(Ls), np.stack(Rs), D, cfg, sc
+
+
+def _want(orc, L, R, dets, cfg):
+    out, _ = orc.estimate(L, R, [_abi.Detection(d.cx, d.cy, d.w, d.h, d.class_id, d.id) for d in dets],
+                          cfg.to_c(), S.F_PX, S.BASELINE_M)
+    return b"".join(bytes(o) for o in out)
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3"])
+def test_range_frames_device_and_host(ctx, orc, name):
+    import torch
+
+    fn = {"c1": S.scene_c1, "c2": S.scene_c2, "c3": S.scene_c3}[name]
+    n = 5 if name != "c3" else 3
+    L, R, D, cfg, sc = _frames(fn, n)
+    # vary the detection lists per frame: drop some boxes, permute others
+    D = [d if i % 2 == 0 else list(reversed(d[: max(1, len(d) - i)])) for i, d in enumerate(D)]
+    maxd = max(len(d) for d in D)
+    eng = FrameEngine(sc.width, sc.height, cfg, maxd, S.F_PX, S.BASELINE_M, ctx=ctx)
+    recs, offs = pack_detections(D)
+    dev = torch.device("cuda", 0)
+    dL, dR = torch.from_numpy(L).to(dev), torch.from_numpy(R).to(dev)
+    out = torch.zeros(n * eng.out_stride * 32, dtype=torch.uint8, device=dev)
+    cnt = torch.zeros(n, dtype=torch.int32, device=dev)
+    eng.range_device(dL, dR, torch.from_numpy(recs.view(np.uint8)).to(dev), torch.from_numpy(offs).to(dev), out, cnt)
+    torch.cuda.synchronize()
+    o = out.cpu().numpy().reshape(n, eng.out_stride * 32)
+    c = cnt.cpu().numpy()
+    h_out = np.zeros(n * eng.out_stride, OUT_DTYPE)
+    h_cnt = np.zeros(n, np.int32)
+    eng.range_host(L, R, recs, offs, h_out, h_cnt, chunk=2)
+    ho = h_out.view(np.uint8).reshape(n, eng.out_stride * 32)
+    for f in range(n):
+        want = _want(orc, L[f], R[f], D[f], cfg)
+        assert int(c[f]) * 32 == len(want) and int(h_cnt[f]) == c[f]
+        assert o[f, :len(want)].tobytes() == want
+        assert ho[f, :len(want)].tobytes() == want
+
+
+def test_auto_rect_frames_equals_single(ctx):
+    import torch
+
+    n = 3
+    Ls, Rs = [], []
+    for i, voff in enumerate((-4, 0, 3)):
+        sc = S.scene_c4(voff, seed=60 + i)
+        L, R = S.render_stereo_pair(sc)
+        Ls.append(L)
+        Rs.append(R)
+    L, R = np.stack(Ls), np.stack(Rs)
+    cfg = rg.RangerConfig()
+    eng = FrameEngine(1920, 1080, cfg, 1, ctx=ctx)
+    dev = torch.device("cuda", 0)
+    best = torch.zeros(n, dtype=torch.int32, device=dev)
+    counts = torch.zeros(n * 17, dtype=torch.int64, device=dev)
+    eng.auto_rect_device(torch.from_numpy(L).to(dev), torch.from_numpy(R).to(dev), S.C4_ROI, -8, 8, S.c4_bm(),
+                         best, counts)
+    torch.cuda.synchronize()
+    for f in range(n):
+        cs = []
+        b = rg.auto_rect_search(L[f], R[f], rg.ImageRoi(*S.C4_ROI), -8, 8, S.c4_bm(), ctx=ctx, counts_out=cs)
+        assert int(best[f]) == b == (-4, 0, 3)[f]
+        assert counts[f * 17:(f + 1) * 17].cpu().tolist() == cs
+
+
+@pytest.mark.parametrize("binary", ["unit_tests", "acceptance_tests"])
+def test_reference_tests_pass_on_the_gpu_path(binary):
+    exe = os.path.join(ROOT, "tests", "dropin", "_bin", binary)
+    if not os.path.exists(exe):
+        pytest.skip("drop-in binaries not built (needs /root/reference at build time)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
+    if binary == "acceptance_tests":
+        for c in (1, 3, 4, 5, 6, 7, 13, 14):
+            assert f"criterion {c:2d}: PASS" in r.stdout
