@@ -229,7 +229,10 @@ def main():
     d_out = torch.zeros(F * eng.out_stride * OUT_DTYPE.itemsize, dtype=torch.uint8, device=dev)
     d_cnt = torch.zeros(F, dtype=torch.int32, device=dev)
     gather = torch.zeros(world * d_out.numel(), dtype=torch.uint8, device=dev) if world > 1 else None
-    stream = torch.cuda.current_stream(dev)
+    # a real (non-legacy-default) stream: the library launches on it and the
+    # CUDA events below are recorded on it
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
 
     def step():
         eng.range_device(dL, dR, d_dets, d_offs, d_out, d_cnt, stream=stream.cuda_stream)

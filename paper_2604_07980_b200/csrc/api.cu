@@ -159,8 +159,8 @@ rg_status census_one(rg_ctx* ctx, const uint8_t* d_img, int w, int h, int ow, in
                      uint32_t* d_full, uint32_t* d_red) {
   int32_t *ix = nullptr, *iy = nullptr;
   TRY(upload_inverse_maps(ctx, w, h, ow, oh, ctx->stream, &ix, &iy));
-  RG_CUDA(ctx, launch_census_frames(d_img, nullptr, 1, 0, w, w, h, d_full, nullptr, d_red,
-                                    nullptr, ow, oh, ix, iy, ctx->stream));
+  RG_CUDA(ctx, launch_census_frames(d_img, nullptr, 1, 0, w, w, h, d_full, nullptr, make_geom(w, h, 0, 0),
+                                    d_red, nullptr, make_geom(ow, oh, 0, 0), ix, iy, ctx->stream));
   count_launch(ctx, ST_CENSUS);
   return RG_OK;
 }
@@ -223,8 +223,14 @@ struct FrameJob {
   const uint32_t* scaled_r = nullptr;
 };
 
+bool same_geom(const PadGeom& a, const PadGeom& b) {
+  return a.w == b.w && a.h == b.h && a.padx == b.padx && a.pady == b.pady && a.pitch == b.pitch &&
+         a.fstride == b.fstride && a.origin == b.origin;
+}
+
 struct PipelineBufs {
   uint32_t *fl, *fr, *sl, *sr;
+  PadGeom gf, gs;
   ObjEntry* objs;
   Slot* slots;
   rg_match_result* res;
@@ -240,17 +246,44 @@ rg_status enqueue_pipeline(rg_ctx* ctx, const FrameJob& J, const rg_ranger_confi
   const int F = J.n_frames;
   if (cw < 1 || ch < 1) return set_err(ctx, RG_EINVAL, "estimate_object_disparities: close raster empty");
   const int maxp = planner_max_points(cfg);
-  if (match_smem_bytes(maxp, true) > kSmemLimit)
+  if (sizeof(int2) * 2 * (size_t)maxp * 4 > kSmemLimit)
     return set_err(ctx, RG_EINVAL, "RangerConfig: blocks too large for the device matcher");
-  const int64_t full_stride = (int64_t)w * h, scaled_stride = (int64_t)cw * ch;
-  uint32_t* fl = DBUF(uint32_t, ctx, B_CEN_FL, full_stride * F);
-  uint32_t* fr = DBUF(uint32_t, ctx, B_CEN_FR, full_stride * F);
-  uint32_t* sl = DBUF(uint32_t, ctx, B_CEN_SL, scaled_stride * F);
-  uint32_t* sr = DBUF(uint32_t, ctx, B_CEN_SR, scaled_stride * F);
+  // zero-padded census rasters: margins cover every sample the search reaches
+  const int dxs = (cfg.dx_max_close + sc - 1) / sc;
+  const int padf = 32 * ((cfg.dx_max_far + 1 + 31) / 32) + 4;
+  const int pads = 32 * ((dxs + 1 + 31) / 32) + 4;
+  PadGeom gf = make_geom(w, h, padf, 2), gs = make_geom(cw, ch, pads, 2);
+  // where a computed code is defined: full [2, W-3] (census.hpp:44); reduced
+  // x' with lround(x' * W / cw) in [2, W-3] (census.hpp:59-64)
+  {
+    const auto mx = scaled_coords(cw, w), my = scaled_coords(ch, h);
+    gf.sx0 = 2, gf.sx1 = w - 3, gf.sy0 = 2, gf.sy1 = h - 3;
+    gs.sx0 = cw, gs.sx1 = -1, gs.sy0 = ch, gs.sy1 = -1;
+    for (int i = 0; i < cw; ++i)
+      if (mx[i] >= 2 && mx[i] <= w - 3) gs.sx0 = std::min(gs.sx0, i), gs.sx1 = std::max(gs.sx1, i);
+    for (int i = 0; i < ch; ++i)
+      if (my[i] >= 2 && my[i] <= h - 3) gs.sy0 = std::min(gs.sy0, i), gs.sy1 = std::max(gs.sy1, i);
+  }
+  const size_t fbytes = sizeof(uint32_t) * (size_t)gf.fstride * F;
+  const size_t sbytes = sizeof(uint32_t) * (size_t)gs.fstride * F;
+  const bool regeom = ctx->cap[B_CEN_FL] < fbytes || ctx->cap[B_CEN_SL] < sbytes ||
+                      !same_geom(ctx->pad_key, gf) || !same_geom(ctx->pad_key_s, gs);
+  uint32_t* fl = DBUF(uint32_t, ctx, B_CEN_FL, gf.fstride * F);
+  uint32_t* fr = DBUF(uint32_t, ctx, B_CEN_FR, gf.fstride * F);
+  uint32_t* sl = DBUF(uint32_t, ctx, B_CEN_SL, gs.fstride * F);
+  uint32_t* sr = DBUF(uint32_t, ctx, B_CEN_SR, gs.fstride * F);
   NEED(fl);
   NEED(fr);
   NEED(sl);
   NEED(sr);
+  if (regeom) {  // margins must read as 0; the census kernels never write them
+    RG_CUDA(ctx, cudaMemsetAsync(fl, 0, ctx->cap[B_CEN_FL], s));
+    RG_CUDA(ctx, cudaMemsetAsync(fr, 0, ctx->cap[B_CEN_FR], s));
+    RG_CUDA(ctx, cudaMemsetAsync(sl, 0, ctx->cap[B_CEN_SL], s));
+    RG_CUDA(ctx, cudaMemsetAsync(sr, 0, ctx->cap[B_CEN_SR], s));
+    ctx->pad_key = gf;
+    ctx->pad_key_s = gs;
+  }
   if (ctx->slot_capacity < F * 64) ctx->slot_capacity = F * 64;
   const int capacity = ctx->slot_capacity;
   ObjEntry* objs = DBUF(ObjEntry, ctx, B_OBJ, (size_t)F * std::max(J.out_stride, 1));
@@ -268,17 +301,23 @@ rg_status enqueue_pipeline(rg_ctx* ctx, const FrameJob& J, const rg_ranger_confi
   if (prof) RG_CUDA(ctx, cudaEventRecord(ctx->ev[0], s));
   // K1 census (full + fused reduced raster) of both images of every frame
   if (!(J.full_l && J.scaled_l)) {
-    RG_CUDA(ctx, launch_census_frames(J.left, J.right, F, J.frame_stride, J.pitch, w, h, fl, fr, sl,
-                                      sr, cw, ch, ix, iy, s));
+    RG_CUDA(ctx, launch_census_frames(J.left, J.right, F, J.frame_stride, J.pitch, w, h, fl, fr, gf, sl,
+                                      sr, gs, ix, iy, s));
     count_launch(ctx, ST_CENSUS);
   }
+  // caller-supplied codes (a pre-filled CensusCache) into the padded layout
+  auto put = [&](uint32_t* dst, const uint32_t* src, const PadGeom& g) -> rg_status {
+    RG_CUDA(ctx, cudaMemcpy2DAsync(dst + g.origin, sizeof(uint32_t) * g.pitch, src, sizeof(uint32_t) * g.w,
+                                   sizeof(uint32_t) * g.w, g.h, cudaMemcpyDefault, s));
+    return RG_OK;
+  };
   if (J.full_l) {
-    RG_CUDA(ctx, cudaMemcpyAsync(fl, J.full_l, sizeof(uint32_t) * full_stride, cudaMemcpyDeviceToDevice, s));
-    RG_CUDA(ctx, cudaMemcpyAsync(fr, J.full_r, sizeof(uint32_t) * full_stride, cudaMemcpyDeviceToDevice, s));
+    TRY(put(fl, J.full_l, gf));
+    TRY(put(fr, J.full_r, gf));
   }
   if (J.scaled_l) {
-    RG_CUDA(ctx, cudaMemcpyAsync(sl, J.scaled_l, sizeof(uint32_t) * scaled_stride, cudaMemcpyDeviceToDevice, s));
-    RG_CUDA(ctx, cudaMemcpyAsync(sr, J.scaled_r, sizeof(uint32_t) * scaled_stride, cudaMemcpyDeviceToDevice, s));
+    TRY(put(sl, J.scaled_l, gs));
+    TRY(put(sr, J.scaled_r, gs));
   }
   if (prof) RG_CUDA(ctx, cudaEventRecord(ctx->ev[1], s));
   // K3 planner
@@ -286,9 +325,10 @@ rg_status enqueue_pipeline(rg_ctx* ctx, const FrameJob& J, const rg_ranger_confi
                                   J.out_count, slots, capacity, counters, J.stats, s));
   count_launch(ctx, ST_PLAN);
   if (prof) RG_CUDA(ctx, cudaEventRecord(ctx->ev[2], s));
-  // K2 fused sampler + forward/backward matcher, one CTA per slot
-  RG_CUDA(ctx, launch_match_slots(slots, counters, capacity, objs, J.dets, J.det_off, fl, fr, sl, sr,
-                                  w, h, cw, ch, full_stride, scaled_stride, cfg, res, J.stats, maxp, s));
+  // K2 fused sampler + forward/backward matcher, one warp per slot
+  const int trusted = !(J.full_l || J.scaled_l);
+  RG_CUDA(ctx, launch_match_slots(slots, counters, capacity, objs, J.dets, J.det_off, fl, fr, gf, sl, sr, gs,
+                                  w, h, trusted, cfg, res, J.stats, maxp, s));
   count_launch(ctx, ST_MATCH);
   if (prof) RG_CUDA(ctx, cudaEventRecord(ctx->ev[3], s));
   // K4 aggregation + range
@@ -296,7 +336,7 @@ rg_status enqueue_pipeline(rg_ctx* ctx, const FrameJob& J, const rg_ranger_confi
                                 J.baseline, scratch, J.out, s));
   count_launch(ctx, ST_AGG);
   if (prof) RG_CUDA(ctx, cudaEventRecord(ctx->ev[4], s));
-  if (pb) *pb = {fl, fr, sl, sr, objs, slots, res, counters, scratch, capacity};
+  if (pb) *pb = {fl, fr, sl, sr, gf, gs, objs, slots, res, counters, scratch, capacity};
   return RG_OK;
 }
 
@@ -750,24 +790,15 @@ rg_status rg_estimate_object_disparities(rg_ctx* ctx, const uint8_t* left, const
   RG_CUDA(ctx, cudaMemcpyAsync(doff, hoff, sizeof(hoff), cudaMemcpyHostToDevice, st));
   FrameJob J = {dl, dr, 1, w, h, w, (int64_t)w * h, dd, doff, out_stride, dout, dcnt, dstats,
                 focal_px, baseline_m};
-  // a pre-filled cache is used as-is (template_match.hpp:312, 317)
-  uint32_t* cache_dev = nullptr;
-  if (cache && (cache->has_full || cache->has_scaled)) {
-    const size_t fsz = (size_t)w * h, ssz = (size_t)std::max(cw, 0) * std::max(ch, 0);
-    cache_dev = DBUF(uint32_t, ctx, B_TMP2, 2 * fsz + 2 * ssz + 1);
-    NEED(cache_dev);
-    if (cache->has_full) {
-      RG_CUDA(ctx, cudaMemcpyAsync(cache_dev, cache->full_left, 4 * fsz, cudaMemcpyHostToDevice, st));
-      RG_CUDA(ctx, cudaMemcpyAsync(cache_dev + fsz, cache->full_right, 4 * fsz, cudaMemcpyHostToDevice, st));
-      J.full_l = cache_dev;
-      J.full_r = cache_dev + fsz;
-    }
-    if (cache->has_scaled && ssz) {
-      RG_CUDA(ctx, cudaMemcpyAsync(cache_dev + 2 * fsz, cache->scaled_left, 4 * ssz, cudaMemcpyHostToDevice, st));
-      RG_CUDA(ctx, cudaMemcpyAsync(cache_dev + 2 * fsz + ssz, cache->scaled_right, 4 * ssz, cudaMemcpyHostToDevice, st));
-      J.scaled_l = cache_dev + 2 * fsz;
-      J.scaled_r = cache_dev + 2 * fsz + ssz;
-    }
+  // a pre-filled cache is used as-is (template_match.hpp:312, 317); its host
+  // codes are copied straight into the padded device rasters
+  if (cache && cache->has_full) {
+    J.full_l = cache->full_left;
+    J.full_r = cache->full_right;
+  }
+  if (cache && cache->has_scaled && cw > 0 && ch > 0) {
+    J.scaled_l = cache->scaled_left;
+    J.scaled_r = cache->scaled_right;
   }
   PipelineBufs pb;
   TRY(run_pipeline(ctx, J, *cfg, st, &pb));
@@ -817,13 +848,15 @@ rg_status rg_estimate_object_disparities(rg_ctx* ctx, const uint8_t* left, const
         add_roi(sc_rois, bx0, by0, bx1, by1, double(cw) / w, double(ch) / h, dxs + 2, 3, cw, ch);
       }
     }
-    auto fill = [&](const uint32_t* src, int ww, int hh, const std::vector<rg_rect>& rois,
+    auto fill = [&](const uint32_t* src, const PadGeom& g, const std::vector<rg_rect>& rois,
                     uint32_t* host) -> rg_status {
+      const int ww = g.w, hh = g.h;
       uint32_t* tmp = DBUF(uint32_t, ctx, B_TMP1, (size_t)ww * hh);
       rg_rect* dro = DBUF(rg_rect, ctx, B_ROIS, std::max<size_t>(rois.size(), 1));
       NEED(tmp);
       NEED(dro);
-      RG_CUDA(ctx, cudaMemcpyAsync(tmp, src, 4 * (size_t)ww * hh, cudaMemcpyDeviceToDevice, st));
+      RG_CUDA(ctx, cudaMemcpy2DAsync(tmp, 4 * (size_t)ww, src + g.origin, 4 * (size_t)g.pitch, 4 * (size_t)ww, hh,
+                                     cudaMemcpyDeviceToDevice, st));
       if (!rois.empty())
         RG_CUDA(ctx, cudaMemcpyAsync(dro, rois.data(), sizeof(rg_rect) * rois.size(), cudaMemcpyHostToDevice, st));
       RG_CUDA(ctx, launch_roi_mask(tmp, ww, hh, dro, (int)rois.size(), st));
@@ -833,13 +866,13 @@ rg_status rg_estimate_object_disparities(rg_ctx* ctx, const uint8_t* left, const
       return RG_OK;
     };
     if (!cache->has_full && any_far) {
-      TRY(fill(pb.fl, w, h, far_rois, cache->full_left));
-      TRY(fill(pb.fr, w, h, far_rois, cache->full_right));
+      TRY(fill(pb.fl, pb.gf, far_rois, cache->full_left));
+      TRY(fill(pb.fr, pb.gf, far_rois, cache->full_right));
       cache->has_full = 1;
     }
     if (!cache->has_scaled && any_close) {
-      TRY(fill(pb.sl, cw, ch, sc_rois, cache->scaled_left));
-      TRY(fill(pb.sr, cw, ch, sc_rois, cache->scaled_right));
+      TRY(fill(pb.sl, pb.gs, sc_rois, cache->scaled_left));
+      TRY(fill(pb.sr, pb.gs, sc_rois, cache->scaled_right));
       cache->has_scaled = 1;
     }
   }

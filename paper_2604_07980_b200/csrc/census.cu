@@ -7,6 +7,8 @@
 // image.  The reduced CLOSE raster is a gather of the full raster at
 // (mx[x'], my[y']) with mx = lround(x' * src/out) (census.hpp:59-64), so the
 // batched kernel writes it from the same registers (inverse index maps).
+#include <cuda_fp16.h>
+
 #include "rg_common.cuh"
 
 namespace rg {
@@ -33,16 +35,16 @@ constexpr int TPB = 256; // threads: 128 x 2 rows at a time
 // when right == nullptr).  grid.z = sides*frame + side.
 __global__ void __launch_bounds__(TPB) census_frames_kernel(
     const uint8_t* __restrict__ left, const uint8_t* __restrict__ right, int64_t frame_stride,
-    int pitch, int w, int h, uint32_t* __restrict__ fl, uint32_t* __restrict__ fr,
-    uint32_t* __restrict__ sl, uint32_t* __restrict__ sr, int cw, int ch,
+    int pitch, int w, int h, uint32_t* __restrict__ fl, uint32_t* __restrict__ fr, PadGeom gf,
+    uint32_t* __restrict__ sl, uint32_t* __restrict__ sr, PadGeom gs,
     const int32_t* __restrict__ inv_x, const int32_t* __restrict__ inv_y) {
   __shared__ __align__(16) uint8_t tile[TY + 4][TX + 8];
   const int sides = right ? 2 : 1;
   const int frame = blockIdx.z / sides, side = blockIdx.z - frame * sides;
   const uint8_t* img = (side ? right : left) + (int64_t)frame * frame_stride;
-  uint32_t* full = (side ? fr : fl) + (int64_t)frame * w * h;
+  uint32_t* full = (side ? fr : fl) + (int64_t)frame * gf.fstride + gf.origin;
   uint32_t* red = (side ? sr : sl);
-  if (red) red += (int64_t)frame * cw * ch;
+  if (red) red += (int64_t)frame * gs.fstride + gs.origin;
   const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
 
   // stage (TY+4) x (TX+4) bytes with a 2-px halo; OOB bytes are never read by
@@ -62,10 +64,154 @@ __global__ void __launch_bounds__(TPB) census_frames_kernel(
     if (x >= w || y >= h) continue;
     uint32_t code = 0;
     if (x >= 2 && y >= 2 && x < w - 2 && y < h - 2) code = census_window(&tile[ty + 2][tx + 2], TX + 8);
-    full[(int64_t)y * w + x] = code;
+    full[(int64_t)y * gf.pitch + x] = code;
     if (red && ix >= 0) {
       const int iy = inv_y[y];
-      if (iy >= 0) red[(int64_t)iy * cw + ix] = code;
+      if (iy >= 0) red[(int64_t)iy * gs.pitch + ix] = code;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Fast path (pitch % 4 == 0, W % 4 == 0, reduced raster = exact half or none):
+// half2 "vertical pair" census.  Pixel rows y and y+1 ride in the two fp16
+// lanes of one register, encoded exactly as 1024 + intensity.  V[r][x] holds
+// (I(x, r), I(x, r+1)), so the window neighbour (i, j) of BOTH pixels of the
+// pair (x, y)/(x, y+1) is the single register V[y+j][x+i]: one HSET2 (n > c,
+// 1.0/0.0 per lane) and one HFMA2 (acc = 2 acc + m) advance two descriptors
+// by one bit.  24 compares go into three fp16 accumulators (1+10, 1+10, 1+5
+// bits, each exact below 2048) that are unpacked into the reference's bit
+// layout at the end; the centre compare (always 0) is folded into a x4 step.
+// V is built once per CTA in shared memory (6 PRMT per 4 entries from the
+// raw image words); each warp then streams a 16-row strip keeping a rolling
+// 5-row window of V in registers (2 new rows per pixel-pair row).
+constexpr int C2_LANES_PAIRS = 4;                 // pixel pairs per lane
+constexpr int C2_TX = 32 * C2_LANES_PAIRS;        // 128 tile columns
+constexpr int C2_WARPS = 8;
+constexpr int C2_PR = 8;                          // pair rows per warp strip
+constexpr int C2_TY = C2_WARPS * C2_PR * 2;       // 128 tile rows
+constexpr int C2_VW = C2_TX + 4;                  // V entries per row (x0-2 .. x0+TX+1)
+constexpr int C2_VR = C2_TY + 3;                  // V rows (y0-2 .. y0+TY)
+constexpr int C2_WORDS = C2_TX / 4 + 2;           // image words per row (x0-4 .. x0+TX+3)
+constexpr size_t C2_SMEM = sizeof(uint32_t) * C2_VR * C2_VW;
+
+__device__ __forceinline__ uint32_t c2_vpair(uint32_t a, uint32_t b, int j) {
+  // entry j of the 4 columns of words a (row r) and b (row r+1): half2(1024+a_j, 1024+b_j)
+  const uint32_t t = __byte_perm(a, b, j < 2 ? 0x5140 : 0x7362);  // a_j b_j a_j+1 b_j+1
+  return __byte_perm(t, 0x64646464u, (j & 1) ? 0x4342 : 0x4140);
+}
+
+__device__ __forceinline__ uint32_t c2_assemble(uint32_t g0, uint32_t g1, uint32_t g2, int hi) {
+  const uint32_t a = (hi ? g0 >> 16 : g0) & 0x3FFu;   // w0..w9
+  const uint32_t b = (hi ? g1 >> 16 : g1) & 0x3FFu;   // w10..w19 (centre bit included)
+  const uint32_t c = ((hi ? g2 >> 16 : g2) >> 5) & 0x1Fu;  // w20..w24
+  return 0x2000000u | (a << 15) | (b << 5) | c;
+}
+
+__global__ void __launch_bounds__(C2_WARPS * 32) census_pairs_kernel(
+    const uint8_t* __restrict__ left, const uint8_t* __restrict__ right, int64_t frame_stride,
+    int pitch, int w, int h, uint32_t* __restrict__ fl, uint32_t* __restrict__ fr, PadGeom gf,
+    uint32_t* __restrict__ sl, uint32_t* __restrict__ sr, PadGeom gs) {
+  extern __shared__ __align__(16) uint32_t V[];  // [C2_VR][C2_VW]
+  const int sides = right ? 2 : 1;
+  const int frame = blockIdx.z / sides, side = blockIdx.z - frame * sides;
+  const uint8_t* img = (side ? right : left) + (int64_t)frame * frame_stride;
+  uint32_t* full = (side ? fr : fl) + (int64_t)frame * gf.fstride + gf.origin;
+  uint32_t* red = side ? sr : sl;
+  if (red) red += (int64_t)frame * gs.fstride + gs.origin;
+  const int x0 = blockIdx.x * C2_TX, y0 = blockIdx.y * C2_TY;
+
+  // ---- phase 1: V rows y0-2 .. y0+TY from the image words; each thread walks
+  // one word column down a run of rows, so every image word is loaded once.
+  // Out-of-image words are clamped: they only feed border codes (forced to 0).
+  const int wmax = (w + 3) / 4 - 1;
+  constexpr int RUNS = (C2_WARPS * 32) / C2_WORDS;         // 7 runs of rows
+  constexpr int RUN_LEN = (C2_VR + RUNS - 1) / RUNS;       // 19 rows per run
+  const int wk = threadIdx.x % C2_WORDS, run = threadIdx.x / C2_WORDS;
+  if (run < RUNS) {
+    const int kw = min(max((x0 - 4) / 4 + wk, 0), wmax);
+    const uint32_t* col = reinterpret_cast<const uint32_t*>(img) + kw;
+    const int pw = pitch / 4;
+    const int r0 = run * RUN_LEN, r1 = min(C2_VR, r0 + RUN_LEN);
+    uint32_t a = __ldg(col + (int64_t)min(max(y0 - 2 + r0, 0), h - 1) * pw);
+    for (int r = r0; r < r1; ++r) {
+      const uint32_t b = __ldg(col + (int64_t)min(max(y0 - 1 + r, 0), h - 1) * pw);
+      uint32_t* vrow = V + r * C2_VW + 4 * wk - 2;  // entries 4wk-2 .. 4wk+1
+      if (wk > 0) *reinterpret_cast<uint2*>(vrow) = make_uint2(c2_vpair(a, b, 0), c2_vpair(a, b, 1));
+      if (wk < C2_WORDS - 1) *reinterpret_cast<uint2*>(vrow + 2) = make_uint2(c2_vpair(a, b, 2), c2_vpair(a, b, 3));
+      a = b;
+    }
+  }
+  __syncthreads();
+
+  // ---- phase 2: warp strip of C2_PR pair rows, lane = 4 pixel pairs
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int xl = x0 + 4 * lane;  // first column of this lane
+  if (xl >= w) return;
+  const __half2 two = __float2half2_rn(2.0f), four = __float2half2_rn(4.0f);
+  const uint32_t one2 = 0x3C003C00u;  // half2(1.0, 1.0)
+  uint32_t win[5][8];
+  const int pr0 = wid * C2_PR;
+  auto load_row = [&](int slot, int vr) {
+    const uint4* src = reinterpret_cast<const uint4*>(V + vr * C2_VW + 4 * lane);
+    const uint4 p = src[0], q = src[1];
+    win[slot][0] = p.x; win[slot][1] = p.y; win[slot][2] = p.z; win[slot][3] = p.w;
+    win[slot][4] = q.x; win[slot][5] = q.y; win[slot][6] = q.z; win[slot][7] = q.w;
+  };
+  if (y0 + 2 * pr0 >= h) return;
+#pragma unroll
+  for (int j = 0; j < 5; ++j) load_row(j, 2 * pr0 + j);
+  const bool xedge = xl < 2 || xl + 3 > w - 3;
+#pragma unroll 1
+  for (int p = pr0; p < pr0 + C2_PR; ++p) {
+    const int y = y0 + 2 * p;
+    if (y >= h) break;
+    uint32_t lo[4], hi[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const __half2 c = *reinterpret_cast<const __half2*>(&win[2][q + 2]);
+      __half2 g[3];
+      g[0] = g[1] = g[2] = *reinterpret_cast<const __half2*>(&one2);
+#pragma unroll
+      for (int wi = 0; wi < 25; ++wi) {
+        if (wi == 12) continue;  // centre: its 0 bit is folded into w13's x4
+        const int j = wi / 5, i = wi % 5;
+        const __half2 m = __hgt2(*reinterpret_cast<const __half2*>(&win[j][q + i]), c);
+        const int gi = wi < 10 ? 0 : (wi < 20 ? 1 : 2);
+        g[gi] = __hfma2(g[gi], wi == 13 ? four : two, m);
+      }
+      const uint32_t g0 = *reinterpret_cast<uint32_t*>(&g[0]);
+      const uint32_t g1 = *reinterpret_cast<uint32_t*>(&g[1]);
+      const uint32_t g2 = *reinterpret_cast<uint32_t*>(&g[2]);
+      lo[q] = c2_assemble(g0, g1, g2, 0);
+      hi[q] = c2_assemble(g0, g1, g2, 1);
+    }
+    // border: codes are 0 where the window leaves the image (census.hpp:44)
+    if (xedge || y < 2 || y + 1 > h - 3) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const bool xin = xl + q >= 2 && xl + q <= w - 3;
+        if (!(xin && y >= 2 && y <= h - 3)) lo[q] = 0u;
+        if (!(xin && y + 1 >= 2 && y + 1 <= h - 3)) hi[q] = 0u;
+      }
+    }
+    uint32_t* o = full + (int64_t)y * gf.pitch + xl;
+    *reinterpret_cast<uint4*>(o) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+    if (y + 1 < h) *reinterpret_cast<uint4*>(o + gf.pitch) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+    if (red) {  // reduced raster = codes at even (x, y): (x/2, y/2)
+      uint32_t* ro = red + (int64_t)(y >> 1) * gs.pitch + (xl >> 1);
+      *reinterpret_cast<uint2*>(ro) = make_uint2(lo[0], lo[2]);
+    }
+    // roll the window down two V rows
+    if (p + 1 < pr0 + C2_PR) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        win[0][k] = win[2][k];
+        win[1][k] = win[3][k];
+        win[2][k] = win[4][k];
+      }
+      load_row(3, 2 * (p + 1) + 3);
+      load_row(4, 2 * (p + 1) + 4);
     }
   }
 }
@@ -88,12 +234,32 @@ __global__ void roi_mask_kernel(uint32_t* __restrict__ codes, int w, int h,
 
 cudaError_t launch_census_frames(const uint8_t* left, const uint8_t* right, int n_frames,
                                  int64_t frame_stride, int pitch, int w, int h, uint32_t* fl,
-                                 uint32_t* fr, uint32_t* sl, uint32_t* sr, int cw, int ch,
-                                 const int32_t* inv_x, const int32_t* inv_y, cudaStream_t s) {
+                                 uint32_t* fr, const PadGeom& gf, uint32_t* sl, uint32_t* sr,
+                                 const PadGeom& gs, const int32_t* inv_x, const int32_t* inv_y,
+                                 cudaStream_t s) {
   if (n_frames <= 0) return cudaSuccess;
-  dim3 grid((w + TX - 1) / TX, (h + TY - 1) / TY, (right ? 2 : 1) * n_frames);
-  census_frames_kernel<<<grid, TPB, 0, s>>>(left, right, frame_stride, pitch, w, h, fl, fr, sl, sr,
-                                            cw, ch, inv_x, inv_y);
+  const int sides = right ? 2 : 1;
+  const bool aligned = (pitch % 4 == 0) && (w % 4 == 0) && (frame_stride % 4 == 0) &&
+                       (reinterpret_cast<uintptr_t>(left) % 4 == 0) &&
+                       (!right || reinterpret_cast<uintptr_t>(right) % 4 == 0) && gf.pitch % 4 == 0 &&
+                       gf.origin % 4 == 0 && w >= 8 && h >= 8;
+  const bool half = !sl || (gs.w * 2 == w && gs.h * 2 == h && gs.pitch % 2 == 0 && gs.origin % 2 == 0);
+  if (aligned && half) {
+    static bool attr = false;
+    if (!attr) {
+      cudaError_t e = cudaFuncSetAttribute(census_pairs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)C2_SMEM);
+      if (e != cudaSuccess) return e;
+      attr = true;
+    }
+    dim3 grid((w + C2_TX - 1) / C2_TX, (h + C2_TY - 1) / C2_TY, sides * n_frames);
+    census_pairs_kernel<<<grid, C2_WARPS * 32, C2_SMEM, s>>>(left, right, frame_stride, pitch, w, h, fl, fr,
+                                                             gf, sl, sr, gs);
+    return cudaGetLastError();
+  }
+  dim3 grid((w + TX - 1) / TX, (h + TY - 1) / TY, sides * n_frames);
+  census_frames_kernel<<<grid, TPB, 0, s>>>(left, right, frame_stride, pitch, w, h, fl, fr, gf, sl,
+                                            sr, gs, inv_x, inv_y);
   return cudaGetLastError();
 }
 

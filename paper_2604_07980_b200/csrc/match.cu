@@ -1,10 +1,9 @@
 // match.cu -- K2: per-block census template matcher on sm_100a.
 //
 // Replaces block_match / forward_backward_match / batch_match (reference
-// census.hpp:178-315) and, in the fused planner path, sample_query_points
-// (template_match.hpp:155-223).  One CTA (256 threads) per QueryBlock:
-//   1. (planner path) sample the block's points in-kernel, dropping points
-//      inside occluder boxes; blocks with < 4 points are dropped.
+// census.hpp:178-315) for arbitrary caller-supplied blocks and rasters (the
+// C-ABI rg_match_blocks path; the fused planner path lives in
+// match_warp.cu).  One CTA (256 threads) per QueryBlock:
 //   2. keep points with a defined left descriptor (census.hpp:195-201).
 //   3. stage the right-census window the block can reach into shared memory
 //      (zero outside the raster -> "undefined", exactly like the reference's
@@ -428,82 +427,6 @@ __global__ void __launch_bounds__(NT) match_blocks_kernel(Raster L, Raster R,
               &out[b], nullptr);
 }
 
-// ------------------------------------------------------------ planner path
-__global__ void __launch_bounds__(NT) match_slots_kernel(
-    const Slot* __restrict__ slots, const int32_t* __restrict__ n_slots_dev,
-    const ObjEntry* __restrict__ objs, const rg_detection* __restrict__ dets,
-    const int32_t* __restrict__ det_off, const uint32_t* __restrict__ fl,
-    const uint32_t* __restrict__ fr, const uint32_t* __restrict__ sl,
-    const uint32_t* __restrict__ sr, int w, int h, int cw, int ch, int64_t full_stride,
-    int64_t scaled_stride, rg_ranger_config cfg, rg_match_result* __restrict__ res,
-    rg_ranger_stats* __restrict__ stats, int maxp, int32_t* __restrict__ counters) {
-  extern __shared__ __align__(16) unsigned char dyn[];
-  __shared__ Scratch sc;
-  __shared__ double occ[4 * kMaxOccluders];
-  __shared__ int n_occ;
-  const int slot = blockIdx.x;
-  if (slot >= *n_slots_dev) return;
-  const Slot s = slots[slot];
-  const ObjEntry e = objs[s.obj];
-  const rg_detection det = dets[e.det];
-  const int d0 = det_off[s.frame], d1 = det_off[s.frame + 1];
-  const Dyn S = carve(dyn, maxp, true);
-  if (threadIdx.x == 0) n_occ = 0;
-  __syncthreads();
-  // occluders of this detection among all detections of the frame
-  bool overflow = false;
-  for (int j = d0 + threadIdx.x; j < d1; j += NT) {
-    if (j == e.det) continue;
-    const rg_detection dj = dets[j];
-    if (dev_occludes(det, dj)) {
-      const int k = atomicAdd(&n_occ, 1);
-      if (k < kMaxOccluders) {
-        const PBox b = pixel_box(dj, w, h);
-        occ[4 * k] = b.x0;
-        occ[4 * k + 1] = b.y0;
-        occ[4 * k + 2] = b.x1;
-        occ[4 * k + 3] = b.y1;
-      } else {
-        overflow = true;
-      }
-    }
-  }
-  // more occluders than fit in smem: test every frame detection per point
-  const bool all = __syncthreads_or(overflow);
-  const int no = min(n_occ, kMaxOccluders);
-  const int sub = s.sub;
-  const int np = dev_sample_block(det, e.kind, sub / max(e.cols, 1), sub % max(e.cols, 1), e.rows,
-                                  e.cols, occ, no, all ? dets + d0 : nullptr, d1 - d0, e.det - d0,
-                                  cfg, w, h, S.pts);
-  rg_match_result* out = &res[slot];
-  if (np < 4) {  // template_match.hpp:185, 219: block dropped
-    if (threadIdx.x == 0) {
-      rg_match_result r = {};
-      r.cost_minus = -1.0;
-      r.cost_plus = -1.0;
-      r.n_points = np;
-      *out = r;
-    }
-    return;
-  }
-  if (threadIdx.x == 0 && stats) atomicAdd((unsigned long long*)&stats[s.frame].query_points,
-                                           (unsigned long long)np);
-  Raster L, R;
-  if (e.kind == RG_KIND_FAR) {
-    L = {fl + (int64_t)s.frame * full_stride, w, h, w};
-    R = {fr + (int64_t)s.frame * full_stride, w, h, w};
-  } else {
-    L = {sl + (int64_t)s.frame * scaled_stride, cw, ch, cw};
-    R = {sr + (int64_t)s.frame * scaled_stride, cw, ch, cw};
-  }
-  const int s_close = cfg.close_scale;
-  const rg_search_range rg = e.kind == RG_KIND_FAR
-                                 ? rg_search_range{0, cfg.dx_max_far, -1, 1}
-                                 : rg_search_range{0, (cfg.dx_max_close + s_close - 1) / s_close, -1, 1};
-  match_block(S.pts, np, L, R, rg, RG_MATCH_FWD_BWD, cfg.tau_v, S, sc, out,
-              reinterpret_cast<unsigned long long*>(counters + 2));
-}
-
 size_t dyn_bytes(int maxp, bool with_pts) {
   return sizeof(uint32_t) * kWindowCodes + (with_pts ? sizeof(int2) * maxp : 0) +
          4 * sizeof(int) * (size_t)maxp;
@@ -522,26 +445,6 @@ cudaError_t launch_match_blocks(Raster L, Raster R, const int32_t* pts, const in
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   match_blocks_kernel<<<n_blocks, NT, smem, s>>>(L, R, pts, offs, ranges, mode, tau_v, maxp, out);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_match_slots(const Slot* slots, const int32_t* n_slots_dev, int slot_capacity,
-                               const ObjEntry* objs, const rg_detection* dets,
-                               const int32_t* det_off, const uint32_t* fl, const uint32_t* fr,
-                               const uint32_t* sl, const uint32_t* sr, int w, int h, int cw,
-                               int ch, int64_t full_stride, int64_t scaled_stride,
-                               rg_ranger_config cfg, rg_match_result* res,
-                               rg_ranger_stats* stats, int max_points, cudaStream_t s) {
-  if (slot_capacity <= 0) return cudaSuccess;
-  const int maxp = (max_points + 3) & ~3;
-  const size_t smem = dyn_bytes(maxp, true);
-  cudaError_t e = cudaFuncSetAttribute(match_slots_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  match_slots_kernel<<<slot_capacity, NT, smem, s>>>(slots, n_slots_dev, objs, dets, det_off, fl,
-                                                     fr, sl, sr, w, h, cw, ch, full_stride,
-                                                     scaled_stride, cfg, res, stats, maxp,
-                                                     const_cast<int32_t*>(n_slots_dev));
   return cudaGetLastError();
 }
 

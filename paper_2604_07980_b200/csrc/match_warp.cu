@@ -1,0 +1,333 @@
+// match_warp.cu -- K2 of the batched object ranger: fused query-point sampler
+// + forward/backward census block matcher, one WARP per QueryBlock.
+//
+// Replaces, per slot planned by K3: sample_query_points (template_match.hpp:
+// 155-223), forward_backward_match (census.hpp:281-303) and its two
+// block_match passes (census.hpp:178-272).  Design (B200):
+//   * warp-local: every stage (occluders, sampling, point filter, sweep,
+//     argmin, neighbours, sub-pixel) is done by one warp with ballots and
+//     shuffles -- no CTA barriers; a CTA carries 4 independent slots.
+//   * the census rasters are zero-padded (PadGeom) so a sample at any offset
+//     the search range reaches is a plain load; an out-of-image sample reads a
+//     0 code, which is exactly the reference's "inside() && code != 0" drop.
+//   * lanes own consecutive dx; each lane sweeps up to 9 chunks of 32 dx for
+//     every point: one LDG (L1-resident row segment, immediate offsets) +
+//     LOP3 + POPC + IADD per Hamming evaluation.  Points are visited in
+//     grid order so each row segment stays L1-hot across the 8 points of a
+//     row and the 3 dy.
+//   * a block whose whole search window lies where the computed census is
+//     defined takes the branch-free path (every point contributes, n = #points);
+//     border blocks and caller-supplied rasters take the checked path.
+//   * argmin of (sum/n, |dx|, dy, dx) by exact rational compare and warp
+//     shuffles; FP64 epilogue in the reference's operation order.
+#include <climits>
+
+#include "rg_common.cuh"
+#include "rg_device.cuh"
+
+namespace rg {
+namespace {
+
+constexpr int WPB = 4;       // warps (slots) per CTA
+constexpr int kWarpOcc = 32; // occluder boxes per warp kept in smem
+constexpr int CMAX = 9;      // 32-wide dx chunks per sweep
+
+struct Cand {
+  int sum, n, dx, dy;  // n == 0: infinite cost
+};
+
+__device__ __forceinline__ bool better(const Cand& a, const Cand& b) {  // census.hpp:225-252
+  if (a.n == 0) return false;
+  if (b.n == 0) return true;
+  const long long l = (long long)a.sum * b.n, r = (long long)b.sum * a.n;
+  if (l != r) return l < r;
+  const int aa = abs(a.dx), ab = abs(b.dx);
+  if (aa != ab) return aa < ab;
+  if (a.dy != b.dy) return a.dy < b.dy;
+  return a.dx < b.dx;
+}
+
+__device__ __forceinline__ double subpixel(double cm, double c0, double cp) {  // census.hpp:167-171
+  const double denom = __dsub_rn(__dadd_rn(cm, cp), __dmul_rn(2.0, c0));
+  if (denom <= 0.0) return 0.0;
+  return __ddiv_rn(-__dsub_rn(cp, cm), __dmul_rn(2.0, denom));
+}
+
+struct Pass {
+  int has, dx, dy, sum, n, interior, cm_sum, cm_n, cp_sum, cp_n;
+};
+
+// One sweep over K dx-chunks for one dy: vp[k] = {raster offset of point k,
+// its left code}; `base` = this lane's sample pointer for chunk c0 at offset 0.
+template <bool FAST, int K>
+__device__ __forceinline__ void sweep(const int2* __restrict__ vp, int nv, const uint32_t* base,
+                                      int lane, int c0, int ndx, int dx_min, int dy, Cand& best,
+                                      int& evals) {
+  int s[K], n[K];
+#pragma unroll
+  for (int c = 0; c < K; ++c) s[c] = n[c] = 0;
+  for (int k = 0; k < nv; ++k) {
+    const int2 q = vp[k];
+    const uint32_t* a = base + q.x;
+    const uint32_t l = (uint32_t)q.y;
+#pragma unroll
+    for (int c = 0; c < K; ++c) {
+      const uint32_t r = __ldg(a - 32 * c);
+      if (FAST) {
+        s[c] += __popc(l ^ r);
+      } else if (r != 0u) {
+        s[c] += __popc(l ^ r);
+        ++n[c];
+      }
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < K; ++c) {
+    const int ix = lane + 32 * (c0 + c);
+    const int nn = FAST ? nv : n[c];
+    if (ix < ndx && nn > 0) {
+      evals += nn;  // Hamming evaluations, census.hpp:209-221
+      const Cand cd = {s[c], nn, dx_min + ix, dy};
+      if (better(cd, best)) best = cd;
+    }
+  }
+}
+
+template <bool FAST>
+__device__ __forceinline__ void sweep_chunks(const int2* vp, int nv, const uint32_t* base, int lane,
+                                             int c0, int k, int ndx, int dx_min, int dy, Cand& best,
+                                             int& evals) {
+  switch (k) {
+#define RG_SWEEP_CASE(K) \
+  case K:                \
+    sweep<FAST, K>(vp, nv, base, lane, c0, ndx, dx_min, dy, best, evals); \
+    break;
+    RG_SWEEP_CASE(1)
+    RG_SWEEP_CASE(2)
+    RG_SWEEP_CASE(3)
+    RG_SWEEP_CASE(4)
+    RG_SWEEP_CASE(5)
+    RG_SWEEP_CASE(6)
+    RG_SWEEP_CASE(7)
+    RG_SWEEP_CASE(8)
+    RG_SWEEP_CASE(9)
+#undef RG_SWEEP_CASE
+    default:
+      break;
+  }
+}
+
+// One block_match pass (census.hpp:178-272) by the calling warp.
+// pts: the block's points (smem), shifted by (sx, sy); L: raster of the left
+// codes, R: raster sampled at (x - dx, y + dy).  Both share geometry g.
+__device__ Pass warp_pass(const int2* pts, int np, int sx, int sy, const uint32_t* L,
+                          const uint32_t* R, const PadGeom& g, bool trusted,
+                          const rg_search_range& rg, int2* vp, int lane, int& evals) {
+  Pass o = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  int nv = 0;
+  int xmin = INT_MAX, xmax = INT_MIN, ymin = INT_MAX, ymax = INT_MIN;
+  for (int b = 0; b < np; b += 32) {  // keep points with a defined left code (:195-201)
+    const int k = b + lane;
+    int x = 0, y = 0;
+    uint32_t code = 0;
+    if (k < np) {
+      const int2 p = pts[k];
+      x = p.x + sx;
+      y = p.y + sy;
+      if (x >= 0 && x < g.w && y >= 0 && y < g.h) code = L[(int64_t)y * g.pitch + x];
+    }
+    const bool ok = code != 0u;
+    const unsigned bal = __ballot_sync(0xffffffffu, ok);
+    if (ok) {
+      vp[nv + __popc(bal & ((1u << lane) - 1u))] = make_int2(y * g.pitch + x, (int)code);
+      xmin = min(xmin, x);
+      xmax = max(xmax, x);
+      ymin = min(ymin, y);
+      ymax = max(ymax, y);
+    }
+    nv += __popc(bal);
+  }
+  __syncwarp();
+  if (nv == 0) return o;  // no contributing point anywhere: nullopt
+  xmin = __reduce_min_sync(0xffffffffu, xmin);
+  ymin = __reduce_min_sync(0xffffffffu, ymin);
+  xmax = __reduce_max_sync(0xffffffffu, xmax);
+  ymax = __reduce_max_sync(0xffffffffu, ymax);
+  const int ndx = rg.dx_max - rg.dx_min + 1;
+  const int nch = (ndx + 31) / 32;
+  // every sample of every real candidate lies where a computed code is defined
+  const bool fast = trusted && xmin - rg.dx_max >= g.sx0 && xmax - rg.dx_min <= g.sx1 &&
+                    ymin + rg.dy_min >= g.sy0 && ymax + rg.dy_max <= g.sy1;
+  Cand best = {0, 0, 0, 0};
+  for (int dy = rg.dy_min; dy <= rg.dy_max; ++dy) {
+    for (int c0 = 0; c0 < nch; c0 += CMAX) {
+      const uint32_t* base = R + (int64_t)dy * g.pitch - rg.dx_min - lane - 32 * c0;
+      const int k = min(CMAX, nch - c0);
+      if (fast)
+        sweep_chunks<true>(vp, nv, base, lane, c0, k, ndx, rg.dx_min, dy, best, evals);
+      else
+        sweep_chunks<false>(vp, nv, base, lane, c0, k, ndx, rg.dx_min, dy, best, evals);
+    }
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {  // warp argmin
+    Cand u;
+    u.sum = __shfl_xor_sync(0xffffffffu, best.sum, off);
+    u.n = __shfl_xor_sync(0xffffffffu, best.n, off);
+    u.dx = __shfl_xor_sync(0xffffffffu, best.dx, off);
+    u.dy = __shfl_xor_sync(0xffffffffu, best.dy, off);
+    if (better(u, best)) best = u;
+  }
+  if (best.n == 0) return o;
+  const int bix = best.dx - rg.dx_min;
+  o.has = 1;
+  o.dx = best.dx;
+  o.dy = best.dy;
+  o.sum = best.sum;
+  o.n = best.n;
+  o.interior = bix > 0 && bix + 1 < ndx;
+  if (o.interior) {  // costs at (dx - 1, dy) and (dx + 1, dy) for the parabola
+    int ms = 0, mn = 0, ps = 0, pn = 0;
+    for (int k = lane; k < nv; k += 32) {
+      const int2 q = vp[k];
+      const uint32_t* a = R + q.x + (int64_t)best.dy * g.pitch - best.dx;
+      const uint32_t rm = a[1], rp = a[-1];
+      if (rm) {
+        ms += __popc((uint32_t)q.y ^ rm);
+        ++mn;
+      }
+      if (rp) {
+        ps += __popc((uint32_t)q.y ^ rp);
+        ++pn;
+      }
+    }
+    o.cm_sum = __reduce_add_sync(0xffffffffu, ms);
+    o.cm_n = __reduce_add_sync(0xffffffffu, mn);
+    o.cp_sum = __reduce_add_sync(0xffffffffu, ps);
+    o.cp_n = __reduce_add_sync(0xffffffffu, pn);
+  }
+  return o;
+}
+
+__device__ __forceinline__ void finish(const Pass& p, rg_match_result& r) {  // census.hpp:255-270
+  r.has_value = 1;
+  r.dx_int = p.dx;
+  r.dy_int = p.dy;
+  r.cost = __ddiv_rn((double)p.sum, (double)p.n);
+  r.valid_points = p.n;
+  r.dx_subpix = (double)p.dx;
+  r.cost_minus = -1.0;
+  r.cost_plus = -1.0;
+  if (p.interior && p.cm_n > 0 && p.cp_n > 0) {
+    const double cm = __ddiv_rn((double)p.cm_sum, (double)p.cm_n);
+    const double cp = __ddiv_rn((double)p.cp_sum, (double)p.cp_n);
+    r.cost_minus = cm;
+    r.cost_plus = cp;
+    r.dx_subpix = __dadd_rn((double)p.dx, subpixel(cm, r.cost, cp));
+  }
+}
+
+__global__ void __launch_bounds__(WPB * 32) match_slots_warp_kernel(
+    const Slot* __restrict__ slots, int32_t* __restrict__ counters, const ObjEntry* __restrict__ objs,
+    const rg_detection* __restrict__ dets, const int32_t* __restrict__ det_off,
+    const uint32_t* __restrict__ fl, const uint32_t* __restrict__ fr, PadGeom gf,
+    const uint32_t* __restrict__ sl, const uint32_t* __restrict__ sr, PadGeom gs, int img_w,
+    int img_h, int trusted, rg_ranger_config cfg, rg_match_result* __restrict__ res,
+    rg_ranger_stats* __restrict__ stats, int maxp) {
+  extern __shared__ __align__(16) int2 wsm[];
+  __shared__ double occ[WPB][4 * kWarpOcc];
+  __shared__ int nocc[WPB];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int slot = blockIdx.x * WPB + warp;
+  if (slot >= counters[0]) return;  // warp-uniform
+  int2* pts = wsm + (size_t)warp * 2 * maxp;
+  int2* vp = pts + maxp;
+  const Slot s = slots[slot];
+  const ObjEntry e = objs[s.obj];
+  const rg_detection det = dets[e.det];
+  const int d0 = det_off[s.frame], d1 = det_off[s.frame + 1];
+  // occluders of this detection among the frame's detections (:71-89)
+  if (lane == 0) nocc[warp] = 0;
+  __syncwarp();
+  bool overflow = false;
+  for (int j = d0 + lane; j < d1; j += 32) {
+    if (j == e.det) continue;
+    const rg_detection dj = dets[j];
+    if (!dev_occludes(det, dj)) continue;
+    const int k = atomicAdd(&nocc[warp], 1);
+    if (k < kWarpOcc) {
+      const PBox b = pixel_box(dj, img_w, img_h);
+      occ[warp][4 * k] = b.x0;
+      occ[warp][4 * k + 1] = b.y0;
+      occ[warp][4 * k + 2] = b.x1;
+      occ[warp][4 * k + 3] = b.y1;
+    } else {
+      overflow = true;
+    }
+  }
+  __syncwarp();
+  const bool all = __any_sync(0xffffffffu, overflow);
+  const int cols = max(e.cols, 1);
+  const int np = dev_sample_block_warp(det, e.kind, s.sub / cols, s.sub % cols, e.rows, e.cols,
+                                       occ[warp], min(nocc[warp], kWarpOcc), all ? dets + d0 : nullptr,
+                                       d1 - d0, e.det - d0, cfg, img_w, img_h, pts);
+  rg_match_result r;
+  r.dx_int = r.dy_int = 0;
+  r.dx_subpix = r.cost = 0.0;
+  r.cost_minus = r.cost_plus = -1.0;
+  r.valid_points = r.verified = r.has_value = 0;
+  r.n_points = np;
+  int evals = 0;
+  if (np >= 4) {  // blocks with < 4 points are dropped (:185, :219)
+    const bool far = e.kind == RG_KIND_FAR;
+    const PadGeom& g = far ? gf : gs;
+    const int64_t fo = (int64_t)s.frame * g.fstride + g.origin;
+    const uint32_t* L = (far ? fl : sl) + fo;
+    const uint32_t* R = (far ? fr : sr) + fo;
+    const int sc = cfg.close_scale;
+    const rg_search_range rg = far ? rg_search_range{0, cfg.dx_max_far, -1, 1}
+                                   : rg_search_range{0, (cfg.dx_max_close + sc - 1) / sc, -1, 1};
+    const Pass f = warp_pass(pts, np, 0, 0, L, R, g, trusted != 0, rg, vp, lane, evals);
+    if (f.has) {
+      finish(f, r);
+      const rg_search_range brg = {-rg.dx_max, -rg.dx_min, -f.dy, -f.dy};
+      const Pass b = warp_pass(pts, np, -f.dx, f.dy, R, L, g, trusted != 0, brg, vp, lane, evals);
+      if (b.has) {
+        rg_match_result rb;
+        finish(b, rb);
+        r.verified = fabs(__dadd_rn(r.dx_subpix, rb.dx_subpix)) < cfg.tau_v;
+      }
+    }
+  }
+  evals = __reduce_add_sync(0xffffffffu, evals);
+  if (lane == 0) {
+    res[slot] = r;
+    if (evals) atomicAdd(reinterpret_cast<unsigned long long*>(counters + 2), (unsigned long long)evals);
+    if (stats && np >= 4) atomicAdd(reinterpret_cast<unsigned long long*>(&stats[s.frame].query_points),
+                                    (unsigned long long)np);
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_match_slots(const Slot* slots, int32_t* counters, int slot_capacity,
+                               const ObjEntry* objs, const rg_detection* dets, const int32_t* det_off,
+                               const uint32_t* fl, const uint32_t* fr, const PadGeom& gf,
+                               const uint32_t* sl, const uint32_t* sr, const PadGeom& gs, int img_w,
+                               int img_h, int trusted, rg_ranger_config cfg, rg_match_result* res,
+                               rg_ranger_stats* stats, int max_points, cudaStream_t s) {
+  if (slot_capacity <= 0) return cudaSuccess;
+  const size_t smem = sizeof(int2) * 2 * (size_t)max_points * WPB;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(match_slots_warp_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  const int grid = (slot_capacity + WPB - 1) / WPB;
+  match_slots_warp_kernel<<<grid, WPB * 32, smem, s>>>(slots, counters, objs, dets, det_off, fl, fr, gf,
+                                                       sl, sr, gs, img_w, img_h, trusted, cfg, res,
+                                                       stats, max_points);
+  return cudaGetLastError();
+}
+
+}  // namespace rg

@@ -28,6 +28,33 @@ struct Raster {  // census raster in device memory
   int pitch;  // elements
 };
 
+// Layout of a census raster in device memory: `w x h` codes at `origin`
+// inside a zero margin of padx columns / pady rows, rows `pitch` apart, frames
+// `fstride` apart.  The batched path pads its rasters so the matcher can read
+// any sample its search range reaches without bounds checks (margin codes are
+// 0 = undefined, exactly the reference's inside() test); [sx0, sx1] x
+// [sy0, sy1] is where a computed code is defined (non-zero).
+struct PadGeom {
+  int w, h, padx, pady, pitch;
+  int64_t fstride, origin;
+  int sx0, sx1, sy0, sy1;
+};
+
+__host__ __device__ inline PadGeom make_geom(int w, int h, int padx, int pady) {
+  PadGeom g;
+  g.w = w;
+  g.h = h;
+  g.padx = padx;
+  g.pady = pady;
+  g.pitch = w + 2 * padx;
+  g.fstride = (int64_t)(h + 2 * pady) * g.pitch;
+  g.origin = (int64_t)pady * g.pitch + padx;
+  g.sx0 = g.sy0 = 0;
+  g.sx1 = w - 1;
+  g.sy1 = h - 1;
+  return g;
+}
+
 // object table entry of the batched planner (one per selected detection)
 struct ObjEntry {
   int32_t det;        // global detection index
@@ -55,6 +82,7 @@ struct rg_ctx {
   cudaStream_t stream = nullptr;  // stream of the synchronous compat API
   cudaStream_t copy_stream = nullptr;  // H2D staging of the host-fed batch API
   int map_key[4] = {-1, -1, -1, -1};  // geometry of the cached inverse maps
+  rg::PadGeom pad_key{}, pad_key_s{};  // layout of the zeroed census rasters
   std::string err;
   bool profiling = false;
   double stage_ms[5] = {0, 0, 0, 0, 0};
@@ -99,9 +127,9 @@ void count_launch(rg_ctx* ctx, int stage, int n = 1);
 // census (census.cu)
 cudaError_t launch_census_frames(const uint8_t* left, const uint8_t* right, int n_frames,
                                  int64_t frame_stride, int pitch, int w, int h,
-                                 uint32_t* fl, uint32_t* fr, uint32_t* sl, uint32_t* sr,
-                                 int cw, int ch, const int32_t* inv_x, const int32_t* inv_y,
-                                 cudaStream_t s);
+                                 uint32_t* fl, uint32_t* fr, const PadGeom& gf, uint32_t* sl,
+                                 uint32_t* sr, const PadGeom& gs, const int32_t* inv_x,
+                                 const int32_t* inv_y, cudaStream_t s);
 cudaError_t launch_roi_mask(uint32_t* codes, int w, int h, const rg_rect* rois, int n_rois,
                             cudaStream_t s);
 
@@ -110,11 +138,11 @@ cudaError_t launch_match_blocks(Raster L, Raster R, const int32_t* pts, const in
                                 const rg_search_range* ranges, int n_blocks, int mode,
                                 double tau_v, rg_match_result* out, int max_points,
                                 cudaStream_t s);
-cudaError_t launch_match_slots(const Slot* slots, const int32_t* n_slots_dev, int slot_capacity,
+cudaError_t launch_match_slots(const Slot* slots, int32_t* counters, int slot_capacity,
                                const ObjEntry* objs, const rg_detection* dets,
                                const int32_t* det_off, const uint32_t* fl, const uint32_t* fr,
-                               const uint32_t* sl, const uint32_t* sr, int w, int h, int cw,
-                               int ch, int64_t full_stride, int64_t scaled_stride,
+                               const PadGeom& gf, const uint32_t* sl, const uint32_t* sr,
+                               const PadGeom& gs, int img_w, int img_h, int trusted,
                                rg_ranger_config cfg, rg_match_result* res,
                                rg_ranger_stats* stats, int max_points, cudaStream_t s);
 

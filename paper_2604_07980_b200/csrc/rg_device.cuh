@@ -86,72 +86,92 @@ __device__ __forceinline__ void dev_close_grid(const PBox& b, const rg_ranger_co
   *rows = rr > 2 ? rr : 2;
 }
 
-// One (sub-)block of sample_query_points (template_match.hpp:155-223),
-// executed by the whole CTA (blockDim a multiple of 32).  Occluded points are
-// tested against `occ` (n_occ PixelBoxes) or, when occ_all != nullptr,
-// against every detection of the frame that occludes `det` (used when the
-// smem list overflowed).  Points are compacted in the reference's grid order
-// (j-major, i-minor) with warp ballots; returns the count (CTA-uniform).
+// Geometry of one (sub-)block of sample_query_points (template_match.hpp:
+// 155-223) and the test of one grid point; shared by the CTA-wide sampler
+// (helper API) and the warp-wide sampler of the fused matcher.
+struct SampleGeom {
+  PBox box;
+  double bw, bh, sx0, sy0, sw, sh;
+  int n, cw, ch;
+  bool far;
+};
+
+__device__ __forceinline__ SampleGeom dev_sample_geom(const rg_detection& det, int kind, int r, int c,
+                                                      int rows, int cols, const rg_ranger_config& cfg,
+                                                      int w, int h) {
+  SampleGeom g;
+  g.box = pixel_box(det, w, h);
+  g.bw = __dsub_rn(g.box.x1, g.box.x0);
+  g.bh = __dsub_rn(g.box.y1, g.box.y0);
+  const int cap = dev_cap(cfg);
+  g.far = kind == RG_KIND_FAR;
+  g.n = g.far ? min(cfg.grid_side_points, cap) : min(cfg.close_block_side_points, cap);
+  g.cw = w / cfg.close_scale;
+  g.ch = h / cfg.close_scale;
+  g.sx0 = g.sy0 = g.sw = g.sh = 0;
+  if (!g.far) {
+    g.sx0 = __dadd_rn(g.box.x0, __ddiv_rn(__dmul_rn((double)c, g.bw), (double)cols));
+    g.sy0 = __dadd_rn(g.box.y0, __ddiv_rn(__dmul_rn((double)r, g.bh), (double)rows));
+    g.sw = __ddiv_rn(g.bw, (double)cols);
+    g.sh = __ddiv_rn(g.bh, (double)rows);
+  }
+  return g;
+}
+
+// Grid point idx (j-major) of the block: true + (px, py) if it survives the
+// image, occlusion and reduced-raster tests.  Occluders: `occ` (n_occ boxes)
+// or, when occ_all != nullptr, every detection of the frame occluding det.
+__device__ __forceinline__ bool dev_sample_point(const SampleGeom& g, int idx, const rg_detection& det,
+                                                 const double* occ, int n_occ, const rg_detection* occ_all,
+                                                 int n_all, int self, int w, int h, int* px, int* py) {
+  const int j = idx / g.n, i = idx - j * g.n;
+  double fx, fy;
+  if (g.far) {
+    fy = __dadd_rn(g.box.y0, __ddiv_rn(__dmul_rn(__dadd_rn((double)j, 0.5), g.bh), (double)g.n));
+    fx = __dadd_rn(g.box.x0, __ddiv_rn(__dmul_rn(__dadd_rn((double)i, 0.5), g.bw), (double)g.n));
+    *px = (int)lround(fx);
+    *py = (int)lround(fy);
+    if (*px < 0 || *px >= w || *py < 0 || *py >= h) return false;
+  } else {
+    fy = __dadd_rn(g.sy0, __ddiv_rn(__dmul_rn(__dadd_rn((double)j, 0.5), g.sh), (double)g.n));
+    fx = __dadd_rn(g.sx0, __ddiv_rn(__dmul_rn(__dadd_rn((double)i, 0.5), g.sw), (double)g.n));
+    if (fx < 0 || fx >= w || fy < 0 || fy >= h) return false;
+  }
+  // occluded points drop (template_match.hpp:159-163, 181, 212)
+  if (occ_all) {
+    for (int k = 0; k < n_all; ++k) {
+      if (k == self || !dev_occludes(det, occ_all[k])) continue;
+      const PBox ob = pixel_box(occ_all[k], w, h);
+      if (box_contains(ob.x0, ob.y0, ob.x1, ob.y1, fx, fy)) return false;
+    }
+  } else {
+    for (int k = 0; k < n_occ; ++k)
+      if (box_contains(occ[4 * k], occ[4 * k + 1], occ[4 * k + 2], occ[4 * k + 3], fx, fy)) return false;
+  }
+  if (!g.far) {  // map into the reduced raster (template_match.hpp:213-215)
+    *px = (int)lround(__ddiv_rn(__dmul_rn(fx, (double)g.cw), (double)w));
+    *py = (int)lround(__ddiv_rn(__dmul_rn(fy, (double)g.ch), (double)h));
+    if (*px < 0 || *px >= g.cw || *py < 0 || *py >= g.ch) return false;
+  }
+  return true;
+}
+
+// CTA-wide sampler (blockDim a multiple of 32): points compacted in the
+// reference's grid order with warp ballots; returns the count (CTA-uniform).
 __device__ __forceinline__ int dev_sample_block(const rg_detection& det, int kind, int r, int c,
                                                 int rows, int cols, const double* occ, int n_occ,
                                                 const rg_detection* occ_all, int n_all, int self,
                                                 const rg_ranger_config& cfg, int w, int h,
                                                 int2* pts) {
   __shared__ int s_wtot[32];
-  const PBox box = pixel_box(det, w, h);
-  const double bw = __dsub_rn(box.x1, box.x0), bh = __dsub_rn(box.y1, box.y0);
-  const int cap = dev_cap(cfg);
-  const bool far = kind == RG_KIND_FAR;
-  const int n = far ? min(cfg.grid_side_points, cap) : min(cfg.close_block_side_points, cap);
-  const int s = cfg.close_scale;
-  const int cw = w / s, ch = h / s;
-  double sx0 = 0, sy0 = 0, sw = 0, sh = 0;
-  if (!far) {
-    sx0 = __dadd_rn(box.x0, __ddiv_rn(__dmul_rn((double)c, bw), (double)cols));
-    sy0 = __dadd_rn(box.y0, __ddiv_rn(__dmul_rn((double)r, bh), (double)rows));
-    sw = __ddiv_rn(bw, (double)cols);
-    sh = __ddiv_rn(bh, (double)rows);
-  }
+  const SampleGeom g = dev_sample_geom(det, kind, r, c, rows, cols, cfg, w, h);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   int base = 0;
-  for (int c0 = 0; c0 < n * n; c0 += blockDim.x) {
+  for (int c0 = 0; c0 < g.n * g.n; c0 += blockDim.x) {
     const int idx = c0 + threadIdx.x;
-    bool keep = idx < n * n;
     int px = 0, py = 0;
-    double fx = 0, fy = 0;
-    if (keep) {
-      const int j = idx / n, i = idx - j * n;
-      if (far) {
-        fy = __dadd_rn(box.y0, __ddiv_rn(__dmul_rn(__dadd_rn((double)j, 0.5), bh), (double)n));
-        fx = __dadd_rn(box.x0, __ddiv_rn(__dmul_rn(__dadd_rn((double)i, 0.5), bw), (double)n));
-        px = (int)lround(fx);
-        py = (int)lround(fy);
-        keep = px >= 0 && px < w && py >= 0 && py < h;
-      } else {
-        fy = __dadd_rn(sy0, __ddiv_rn(__dmul_rn(__dadd_rn((double)j, 0.5), sh), (double)n));
-        fx = __dadd_rn(sx0, __ddiv_rn(__dmul_rn(__dadd_rn((double)i, 0.5), sw), (double)n));
-        keep = !(fx < 0 || fx >= w || fy < 0 || fy >= h);
-      }
-    }
-    if (keep) {  // occluded points drop (template_match.hpp:159-163, 181, 212)
-      bool hidden = false;
-      if (occ_all) {
-        for (int k = 0; k < n_all && !hidden; ++k) {
-          if (k == self || !dev_occludes(det, occ_all[k])) continue;
-          const PBox ob = pixel_box(occ_all[k], w, h);
-          hidden = box_contains(ob.x0, ob.y0, ob.x1, ob.y1, fx, fy);
-        }
-      } else {
-        for (int k = 0; k < n_occ && !hidden; ++k)
-          hidden = box_contains(occ[4 * k], occ[4 * k + 1], occ[4 * k + 2], occ[4 * k + 3], fx, fy);
-      }
-      keep = !hidden;
-    }
-    if (keep && !far) {  // map into the reduced raster (template_match.hpp:213-215)
-      px = (int)lround(__ddiv_rn(__dmul_rn(fx, (double)cw), (double)w));
-      py = (int)lround(__ddiv_rn(__dmul_rn(fy, (double)ch), (double)h));
-      keep = px >= 0 && px < cw && py >= 0 && py < ch;
-    }
+    const bool keep = idx < g.n * g.n &&
+                      dev_sample_point(g, idx, det, occ, n_occ, occ_all, n_all, self, w, h, &px, &py);
     const unsigned bal = __ballot_sync(0xffffffffu, keep);
     if (lane == 0) s_wtot[wid] = __popc(bal);
     __syncthreads();
@@ -164,6 +184,28 @@ __device__ __forceinline__ int dev_sample_block(const rg_detection& det, int kin
     base += total;
     __syncthreads();
   }
+  return base;
+}
+
+// Warp-wide sampler: same points, same order; returns the count (warp-uniform).
+__device__ __forceinline__ int dev_sample_block_warp(const rg_detection& det, int kind, int r, int c,
+                                                     int rows, int cols, const double* occ, int n_occ,
+                                                     const rg_detection* occ_all, int n_all, int self,
+                                                     const rg_ranger_config& cfg, int w, int h,
+                                                     int2* pts) {
+  const SampleGeom g = dev_sample_geom(det, kind, r, c, rows, cols, cfg, w, h);
+  const int lane = threadIdx.x & 31;
+  int base = 0;
+  for (int c0 = 0; c0 < g.n * g.n; c0 += 32) {
+    const int idx = c0 + lane;
+    int px = 0, py = 0;
+    const bool keep = idx < g.n * g.n &&
+                      dev_sample_point(g, idx, det, occ, n_occ, occ_all, n_all, self, w, h, &px, &py);
+    const unsigned bal = __ballot_sync(0xffffffffu, keep);
+    if (keep) pts[base + __popc(bal & ((1u << lane) - 1u))] = make_int2(px, py);
+    base += __popc(bal);
+  }
+  __syncwarp();
   return base;
 }
 
