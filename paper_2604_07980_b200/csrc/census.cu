@@ -88,8 +88,8 @@ __global__ void __launch_bounds__(TPB) census_frames_kernel(
 constexpr int C2_LANES_PAIRS = 4;                 // pixel pairs per lane
 constexpr int C2_TX = 32 * C2_LANES_PAIRS;        // 128 tile columns
 constexpr int C2_WARPS = 8;
-constexpr int C2_PR = 8;                          // pair rows per warp strip
-constexpr int C2_TY = C2_WARPS * C2_PR * 2;       // 128 tile rows
+constexpr int C2_PR = 4;                          // pair rows per warp strip
+constexpr int C2_TY = C2_WARPS * C2_PR * 2;       // 64 tile rows
 constexpr int C2_VW = C2_TX + 4;                  // V entries per row (x0-2 .. x0+TX+1)
 constexpr int C2_VR = C2_TY + 3;                  // V rows (y0-2 .. y0+TY)
 constexpr int C2_WORDS = C2_TX / 4 + 2;           // image words per row (x0-4 .. x0+TX+3)
@@ -101,11 +101,17 @@ __device__ __forceinline__ uint32_t c2_vpair(uint32_t a, uint32_t b, int j) {
   return __byte_perm(t, 0x64646464u, (j & 1) ? 0x4342 : 0x4140);
 }
 
-__device__ __forceinline__ uint32_t c2_assemble(uint32_t g0, uint32_t g1, uint32_t g2, int hi) {
-  const uint32_t a = (hi ? g0 >> 16 : g0) & 0x3FFu;   // w0..w9
-  const uint32_t b = (hi ? g1 >> 16 : g1) & 0x3FFu;   // w10..w19 (centre bit included)
-  const uint32_t c = ((hi ? g2 >> 16 : g2) >> 5) & 0x1Fu;  // w20..w24
-  return 0x2000000u | (a << 15) | (b << 5) | c;
+// The three fp16 accumulators are built so each group's compare bits sit in
+// the low bits of the half's mantissa (value 1024 + B, exponent fixed):
+// g0 = w0..w7 (init 4.0, 8 steps), g1 = w8..w16 (init 2.0, 9 bits incl. the
+// centre 0), g2 = w17..w24 (init 4.0).  code = 1<<25 | B0<<17 | B1<<8 | B2,
+// assembled with byte permutes for both lanes (lo = row y, hi = row y+1).
+__device__ __forceinline__ void c2_assemble(uint32_t g0, uint32_t g1, uint32_t g2, uint32_t& lo,
+                                            uint32_t& hi) {
+  const uint32_t xl = __byte_perm(g2, g1, 0x0540);  // [B2, B1 lo8, 0x64|B1b8, 0]
+  const uint32_t xh = __byte_perm(g2, g1, 0x0762);  // same from the high halves
+  lo = (((xl & 0x1FFFFu) | ((g0 << 17) & 0x1FE0000u)) & 0x1FFFFFFu) | 0x2000000u;
+  hi = (((xh & 0x1FFFFu) | ((g0 << 1) & 0x1FE0000u)) & 0x1FFFFFFu) | 0x2000000u;
 }
 
 __global__ void __launch_bounds__(C2_WARPS * 32) census_pairs_kernel(
@@ -132,14 +138,20 @@ __global__ void __launch_bounds__(C2_WARPS * 32) census_pairs_kernel(
     const int kw = min(max((x0 - 4) / 4 + wk, 0), wmax);
     const uint32_t* col = reinterpret_cast<const uint32_t*>(img) + kw;
     const int pw = pitch / 4;
-    const int r0 = run * RUN_LEN, r1 = min(C2_VR, r0 + RUN_LEN);
-    uint32_t a = __ldg(col + (int64_t)min(max(y0 - 2 + r0, 0), h - 1) * pw);
-    for (int r = r0; r < r1; ++r) {
-      const uint32_t b = __ldg(col + (int64_t)min(max(y0 - 1 + r, 0), h - 1) * pw);
-      uint32_t* vrow = V + r * C2_VW + 4 * wk - 2;  // entries 4wk-2 .. 4wk+1
-      if (wk > 0) *reinterpret_cast<uint2*>(vrow) = make_uint2(c2_vpair(a, b, 0), c2_vpair(a, b, 1));
-      if (wk < C2_WORDS - 1) *reinterpret_cast<uint2*>(vrow + 2) = make_uint2(c2_vpair(a, b, 2), c2_vpair(a, b, 3));
-      a = b;
+    const int r0 = run * RUN_LEN, n = min(RUN_LEN, C2_VR - r0);
+    uint32_t wv[RUN_LEN + 1];  // all loads of the run in flight at once
+#pragma unroll
+    for (int t = 0; t <= RUN_LEN; ++t)
+      if (t <= n) wv[t] = __ldg(col + (int64_t)min(max(y0 - 2 + r0 + t, 0), h - 1) * pw);
+#pragma unroll
+    for (int t = 0; t < RUN_LEN; ++t) {
+      if (t < n) {
+        const uint32_t a = wv[t], b = wv[t + 1];
+        uint32_t* vrow = V + (r0 + t) * C2_VW + 4 * wk - 2;  // entries 4wk-2 .. 4wk+1
+        if (wk > 0) *reinterpret_cast<uint2*>(vrow) = make_uint2(c2_vpair(a, b, 0), c2_vpair(a, b, 1));
+        if (wk < C2_WORDS - 1)
+          *reinterpret_cast<uint2*>(vrow + 2) = make_uint2(c2_vpair(a, b, 2), c2_vpair(a, b, 3));
+      }
     }
   }
   __syncthreads();
@@ -149,7 +161,6 @@ __global__ void __launch_bounds__(C2_WARPS * 32) census_pairs_kernel(
   const int xl = x0 + 4 * lane;  // first column of this lane
   if (xl >= w) return;
   const __half2 two = __float2half2_rn(2.0f), four = __float2half2_rn(4.0f);
-  const uint32_t one2 = 0x3C003C00u;  // half2(1.0, 1.0)
   uint32_t win[5][8];
   const int pr0 = wid * C2_PR;
   auto load_row = [&](int slot, int vr) {
@@ -162,7 +173,7 @@ __global__ void __launch_bounds__(C2_WARPS * 32) census_pairs_kernel(
 #pragma unroll
   for (int j = 0; j < 5; ++j) load_row(j, 2 * pr0 + j);
   const bool xedge = xl < 2 || xl + 3 > w - 3;
-#pragma unroll 1
+#pragma unroll
   for (int p = pr0; p < pr0 + C2_PR; ++p) {
     const int y = y0 + 2 * p;
     if (y >= h) break;
@@ -171,20 +182,18 @@ __global__ void __launch_bounds__(C2_WARPS * 32) census_pairs_kernel(
     for (int q = 0; q < 4; ++q) {
       const __half2 c = *reinterpret_cast<const __half2*>(&win[2][q + 2]);
       __half2 g[3];
-      g[0] = g[1] = g[2] = *reinterpret_cast<const __half2*>(&one2);
+      g[0] = g[2] = __float2half2_rn(4.0f);
+      g[1] = __float2half2_rn(2.0f);
 #pragma unroll
       for (int wi = 0; wi < 25; ++wi) {
         if (wi == 12) continue;  // centre: its 0 bit is folded into w13's x4
         const int j = wi / 5, i = wi % 5;
         const __half2 m = __hgt2(*reinterpret_cast<const __half2*>(&win[j][q + i]), c);
-        const int gi = wi < 10 ? 0 : (wi < 20 ? 1 : 2);
+        const int gi = wi < 8 ? 0 : (wi < 17 ? 1 : 2);
         g[gi] = __hfma2(g[gi], wi == 13 ? four : two, m);
       }
-      const uint32_t g0 = *reinterpret_cast<uint32_t*>(&g[0]);
-      const uint32_t g1 = *reinterpret_cast<uint32_t*>(&g[1]);
-      const uint32_t g2 = *reinterpret_cast<uint32_t*>(&g[2]);
-      lo[q] = c2_assemble(g0, g1, g2, 0);
-      hi[q] = c2_assemble(g0, g1, g2, 1);
+      c2_assemble(*reinterpret_cast<uint32_t*>(&g[0]), *reinterpret_cast<uint32_t*>(&g[1]),
+                  *reinterpret_cast<uint32_t*>(&g[2]), lo[q], hi[q]);
     }
     // border: codes are 0 where the window leaves the image (census.hpp:44)
     if (xedge || y < 2 || y + 1 > h - 3) {
