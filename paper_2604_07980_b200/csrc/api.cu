@@ -333,7 +333,7 @@ rg_status enqueue_pipeline(rg_ctx* ctx, const FrameJob& J, const rg_ranger_confi
   if (prof) RG_CUDA(ctx, cudaEventRecord(ctx->ev[3], s));
   // K4 aggregation + range
   RG_CUDA(ctx, launch_aggregate(objs, J.out_count, F, J.out_stride, res, capacity, cfg, J.focal,
-                                J.baseline, scratch, J.out, s));
+                                J.baseline, scratch, J.out, counters, s));
   count_launch(ctx, ST_AGG);
   if (prof) RG_CUDA(ctx, cudaEventRecord(ctx->ev[4], s));
   if (pb) *pb = {fl, fr, sl, sr, gf, gs, objs, slots, res, counters, scratch, capacity};

@@ -21,6 +21,7 @@
 //   * argmin of (sum/n, |dx|, dy, dx) by exact rational compare and warp
 //     shuffles; FP64 epilogue in the reference's operation order.
 #include <climits>
+#include <cstdlib>
 
 #include "rg_common.cuh"
 #include "rg_device.cuh"
@@ -28,9 +29,9 @@
 namespace rg {
 namespace {
 
-constexpr int WPB = 4;       // warps (slots) per CTA
 constexpr int kWarpOcc = 32; // occluder boxes per warp kept in smem
-constexpr int CMAX = 9;      // 32-wide dx chunks per sweep
+constexpr int CMAX = 9;      // 32-wide dx chunks per sweep (branch-free path)
+constexpr int CMAX_SLOW = 4; // chunks per sweep on the checked path
 
 struct Cand {
   int sum, n, dx, dy;  // n == 0: infinite cost
@@ -97,24 +98,35 @@ template <bool FAST>
 __device__ __forceinline__ void sweep_chunks(const int2* vp, int nv, const uint32_t* base, int lane,
                                              int c0, int k, int ndx, int dx_min, int dy, Cand& best,
                                              int& evals) {
-  switch (k) {
 #define RG_SWEEP_CASE(K) \
   case K:                \
     sweep<FAST, K>(vp, nv, base, lane, c0, ndx, dx_min, dy, best, evals); \
     break;
-    RG_SWEEP_CASE(1)
-    RG_SWEEP_CASE(2)
-    RG_SWEEP_CASE(3)
-    RG_SWEEP_CASE(4)
-    RG_SWEEP_CASE(5)
-    RG_SWEEP_CASE(6)
-    RG_SWEEP_CASE(7)
-    RG_SWEEP_CASE(8)
-    RG_SWEEP_CASE(9)
-#undef RG_SWEEP_CASE
-    default:
-      break;
+  if (FAST) {
+    switch (k) {
+      RG_SWEEP_CASE(1)
+      RG_SWEEP_CASE(2)
+      RG_SWEEP_CASE(3)
+      RG_SWEEP_CASE(4)
+      RG_SWEEP_CASE(5)
+      RG_SWEEP_CASE(6)
+      RG_SWEEP_CASE(7)
+      RG_SWEEP_CASE(8)
+      RG_SWEEP_CASE(9)
+      default:
+        break;
+    }
+  } else {
+    switch (k) {
+      RG_SWEEP_CASE(1)
+      RG_SWEEP_CASE(2)
+      RG_SWEEP_CASE(3)
+      RG_SWEEP_CASE(4)
+      default:
+        break;
+    }
   }
+#undef RG_SWEEP_CASE
 }
 
 // One block_match pass (census.hpp:178-272) by the calling warp.
@@ -159,10 +171,12 @@ __device__ Pass warp_pass(const int2* pts, int np, int sx, int sy, const uint32_
   const bool fast = trusted && xmin - rg.dx_max >= g.sx0 && xmax - rg.dx_min <= g.sx1 &&
                     ymin + rg.dy_min >= g.sy0 && ymax + rg.dy_max <= g.sy1;
   Cand best = {0, 0, 0, 0};
+  // the checked path keeps fewer chunks live (it also carries counts)
+  const int cmax = fast ? CMAX : CMAX_SLOW;
   for (int dy = rg.dy_min; dy <= rg.dy_max; ++dy) {
-    for (int c0 = 0; c0 < nch; c0 += CMAX) {
+    for (int c0 = 0; c0 < nch; c0 += cmax) {
       const uint32_t* base = R + (int64_t)dy * g.pitch - rg.dx_min - lane - 32 * c0;
-      const int k = min(CMAX, nch - c0);
+      const int k = min(cmax, nch - c0);
       if (fast)
         sweep_chunks<true>(vp, nv, base, lane, c0, k, ndx, rg.dx_min, dy, best, evals);
       else
@@ -227,19 +241,22 @@ __device__ __forceinline__ void finish(const Pass& p, rg_match_result& r) {  // 
   }
 }
 
-__global__ void __launch_bounds__(WPB * 32) match_slots_warp_kernel(
+template <int WPB, int MINB>
+__global__ void __launch_bounds__(WPB * 32, MINB) match_slots_warp_kernel(
     const Slot* __restrict__ slots, int32_t* __restrict__ counters, const ObjEntry* __restrict__ objs,
     const rg_detection* __restrict__ dets, const int32_t* __restrict__ det_off,
     const uint32_t* __restrict__ fl, const uint32_t* __restrict__ fr, PadGeom gf,
     const uint32_t* __restrict__ sl, const uint32_t* __restrict__ sr, PadGeom gs, int img_w,
     int img_h, int trusted, rg_ranger_config cfg, rg_match_result* __restrict__ res,
-    rg_ranger_stats* __restrict__ stats, int maxp) {
+    rg_ranger_stats* __restrict__ stats, int maxp, int capacity) {
   extern __shared__ __align__(16) int2 wsm[];
   __shared__ double occ[WPB][4 * kWarpOcc];
   __shared__ int nocc[WPB];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int slot = blockIdx.x * WPB + warp;
-  if (slot >= counters[0]) return;  // warp-uniform
+  // an overflowed plan (counters[1], set by K3) is re-run with a bigger list:
+  // skip it entirely; otherwise only planned slots inside the list exist
+  if (counters[1] || slot >= min(counters[0], capacity)) return;  // warp-uniform
   int2* pts = wsm + (size_t)warp * 2 * maxp;
   int2* vp = pts + maxp;
   const Slot s = slots[slot];
@@ -310,6 +327,25 @@ __global__ void __launch_bounds__(WPB * 32) match_slots_warp_kernel(
 
 }  // namespace
 
+template <int WPB, int MINB>
+static cudaError_t launch_variant(const Slot* slots, int32_t* counters, int slot_capacity,
+                                  const ObjEntry* objs, const rg_detection* dets, const int32_t* det_off,
+                                  const uint32_t* fl, const uint32_t* fr, const PadGeom& gf,
+                                  const uint32_t* sl, const uint32_t* sr, const PadGeom& gs, int img_w,
+                                  int img_h, int trusted, rg_ranger_config cfg, rg_match_result* res,
+                                  rg_ranger_stats* stats, int max_points, cudaStream_t s) {
+  auto kern = match_slots_warp_kernel<WPB, MINB>;
+  const size_t smem = sizeof(int2) * 2 * (size_t)max_points * WPB;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  const int grid = (slot_capacity + WPB - 1) / WPB;
+  kern<<<grid, WPB * 32, smem, s>>>(slots, counters, objs, dets, det_off, fl, fr, gf, sl, sr, gs, img_w, img_h,
+                                    trusted, cfg, res, stats, max_points, slot_capacity);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_match_slots(const Slot* slots, int32_t* counters, int slot_capacity,
                                const ObjEntry* objs, const rg_detection* dets, const int32_t* det_off,
                                const uint32_t* fl, const uint32_t* fr, const PadGeom& gf,
@@ -317,17 +353,20 @@ cudaError_t launch_match_slots(const Slot* slots, int32_t* counters, int slot_ca
                                int img_h, int trusted, rg_ranger_config cfg, rg_match_result* res,
                                rg_ranger_stats* stats, int max_points, cudaStream_t s) {
   if (slot_capacity <= 0) return cudaSuccess;
-  const size_t smem = sizeof(int2) * 2 * (size_t)max_points * WPB;
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(match_slots_warp_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
+  static int variant = [] {
+    const char* v = getenv("RG_MATCH_VARIANT");
+    return v ? atoi(v) : 0;
+  }();
+#define RG_ARGS slots, counters, slot_capacity, objs, dets, det_off, fl, fr, gf, sl, sr, gs, img_w, img_h, \
+                trusted, cfg, res, stats, max_points, s
+  switch (variant) {  // A/B knobs; default measured best (tools/variants.sh)
+    case 1: return launch_variant<4, 8>(RG_ARGS);
+    case 2: return launch_variant<16, 2>(RG_ARGS);
+    case 3: return launch_variant<8, 5>(RG_ARGS);
+    case 4: return launch_variant<4, 1>(RG_ARGS);
+    default: return launch_variant<8, 4>(RG_ARGS);
   }
-  const int grid = (slot_capacity + WPB - 1) / WPB;
-  match_slots_warp_kernel<<<grid, WPB * 32, smem, s>>>(slots, counters, objs, dets, det_off, fl, fr, gf,
-                                                       sl, sr, gs, img_w, img_h, trusted, cfg, res,
-                                                       stats, max_points);
-  return cudaGetLastError();
+#undef RG_ARGS
 }
 
 }  // namespace rg

@@ -129,12 +129,13 @@ __global__ void __launch_bounds__(128) aggregate_kernel(
     const ObjEntry* __restrict__ objs, const int32_t* __restrict__ out_count, int out_stride,
     const rg_match_result* __restrict__ res, int slot_capacity, rg_ranger_config cfg,
     double focal, double baseline, double* __restrict__ scratch,
-    rg_object_disparity* __restrict__ out) {
+    rg_object_disparity* __restrict__ out, const int32_t* __restrict__ counters) {
   __shared__ double vals[kAggCapacity];
   __shared__ int cnt;
   const int g = blockIdx.x;
   const int f = g / out_stride, k = g - f * out_stride;
   if (k >= out_count[f]) return;
+  if (counters[1]) return;  // overflowed plan: the host re-runs the batch
   const ObjEntry e = objs[g];
   if (e.slot_base + e.n_slots > slot_capacity) return;  // overflowed batch, re-run follows
   int valid = 0, used = 0;
@@ -257,11 +258,11 @@ cudaError_t launch_plan_frames(const rg_detection* dets, const int32_t* det_off,
 cudaError_t launch_aggregate(const ObjEntry* objs, const int32_t* out_count, int n_frames,
                              int out_stride, const rg_match_result* res, int slot_capacity,
                              rg_ranger_config cfg, double focal, double baseline, double* scratch,
-                             rg_object_disparity* out, cudaStream_t s) {
+                             rg_object_disparity* out, const int32_t* counters, cudaStream_t s) {
   if (n_frames <= 0 || out_stride <= 0) return cudaSuccess;
   aggregate_kernel<<<n_frames * out_stride, 128, 0, s>>>(objs, out_count, out_stride, res,
                                                          slot_capacity, cfg, focal, baseline,
-                                                         scratch, out);
+                                                         scratch, out, counters);
   return cudaGetLastError();
 }
 

@@ -155,7 +155,7 @@ cudaError_t launch_plan_frames(const rg_detection* dets, const int32_t* det_off,
 cudaError_t launch_aggregate(const ObjEntry* objs, const int32_t* out_count, int n_frames,
                              int out_stride, const rg_match_result* res, int slot_capacity,
                              rg_ranger_config cfg, double focal, double baseline, double* scratch,
-                             rg_object_disparity* out, cudaStream_t s);
+                             rg_object_disparity* out, const int32_t* counters, cudaStream_t s);
 cudaError_t launch_select_objects(const rg_detection* dets, int n, rg_ranger_config cfg,
                                   int32_t* out_idx, int32_t* n_out, cudaStream_t s);
 cudaError_t launch_find_occluders(const rg_detection* dets, int n, int32_t* counts,
