@@ -13,6 +13,8 @@
 // (via the prefix minimum lagging two indices behind) -- exactly the
 // reference's rules (bm.hpp:75-92).  Valid counts (raw > 16*d_min) are
 // reduced per CTA and added with one integer atomic (deterministic).
+#include <cstdlib>
+
 #include "rg_common.cuh"
 
 namespace rg {
@@ -200,6 +202,199 @@ __global__ void __launch_bounds__(BT) bm_kernel(const uint8_t* __restrict__ left
   }
 }
 
+// ---------------------------------------------------------------------------
+// Fast SAD matcher: disparities in lanes.  A warp owns a band of 32 output
+// columns and a strip of rows of one (frame, delta) crop; lane l owns the
+// disparities d_lo + l + 32k (k < DPL).  Per lane the column sums of |L - R|
+// over the 2HW+1 window rows live in registers for the band plus halo and
+// are updated by one row in / one row out per output row; the 9-wide row sum
+// slides along the band.  Per pixel the argmin over d is a warp reduction:
+// __reduce_min_sync on (SAD << 7 | d) gives the first minimum (ties -> the
+// smaller d, bm.hpp:75-82), a second reduction the best over |i - best| > 1
+// (bm.hpp:84-89), two shuffles the neighbours; the FP64 epilogue then runs
+// lane-parallel over the band's 32 pixels.  Texture gate (bm.hpp:50-56):
+// column sums of horizontal |diffs| per lane column, window sum by shuffles.
+constexpr int LBW = 32;   // band width (output columns)
+constexpr int LRS = 32;   // strip rows
+constexpr int LWPB = 4;   // warps (bands) per CTA
+
+__device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
+
+template <int HW, int DPL>
+__global__ void __launch_bounds__(LWPB * 32) bm_lanes_kernel(
+    const uint8_t* __restrict__ left, const uint8_t* __restrict__ right, int64_t stride, int pitch, int img_h,
+    int W, int H, int x0c, int y0c, int delta_min, int n_delta, int d_lo, int nd, double tex, double uniq,
+    int16_t* __restrict__ raw, int64_t* __restrict__ counts) {
+  constexpr int NC = LBW + 2 * HW;  // column sums per lane
+  // column sums in smem, lane-major so every access is conflict-free
+  __shared__ int css[LWPB][DPL][NC][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int band = blockIdx.x * LWPB + warp;
+  const int xb = band * LBW;
+  if (xb >= W) return;  // warp-uniform; no block-level sync below
+  const int yb = blockIdx.y * LRS;
+  const int frame = blockIdx.z / n_delta, kd = blockIdx.z - frame * n_delta;
+  const int delta = delta_min + kd;
+  const uint8_t* Limg = left + (int64_t)frame * stride + x0c;
+  const uint8_t* Rimg = right + (int64_t)frame * stride + x0c;
+  const int d_hi = d_lo + nd;
+  int(*cs)[NC][32] = css[warp];
+  // crop row -> image row (left shifted by delta with edge clamp, image.hpp:145-154)
+  auto lrow = [&](int yr) { return Limg + (int64_t)clampi(y0c + clampi(yr, 0, H - 1) - delta, 0, img_h - 1) * pitch; };
+  auto rrow = [&](int yr) { return Rimg + (int64_t)(y0c + clampi(yr, 0, H - 1)) * pitch; };
+  // this lane's disparity offsets into the right row (clamped: out-of-crop
+  // samples only reach non-evaluable (x, d) pairs)
+  int dd[DPL];
+#pragma unroll
+  for (int k = 0; k < DPL; ++k) dd[k] = d_lo + lane + 32 * k;
+  for (int c = 0; c < NC; ++c) {
+    const int xc = clampi(xb - HW + c, 0, W - 1);
+    int acc[DPL];
+#pragma unroll
+    for (int k = 0; k < DPL; ++k) acc[k] = 0;
+    for (int j = -HW; j <= HW; ++j) {
+      const uint8_t* lr = lrow(yb + j);
+      const uint8_t* rr = rrow(yb + j);
+      const int lv = lr[xc];
+#pragma unroll
+      for (int k = 0; k < DPL; ++k) acc[k] += abs(lv - (int)rr[clampi(xb - HW + c - dd[k], 0, W - 1)]);
+    }
+#pragma unroll
+    for (int k = 0; k < DPL; ++k) cs[k][c][lane] = acc[k];
+  }
+  // texture column sums: lane holds columns xb-HW+lane and xb-HW+32+lane
+  int tv0 = 0, tv1 = 0;
+  const int tc0 = xb - HW + lane, tc1 = tc0 + 32;
+  auto hd = [&](const uint8_t* lr, int c) {
+    return abs((int)lr[clampi(c + 1, 0, W - 1)] - (int)lr[clampi(c, 0, W - 1)]);
+  };
+  for (int j = -HW; j <= HW; ++j) {
+    const uint8_t* lr = lrow(yb + j);
+    tv0 += hd(lr, tc0);
+    tv1 += hd(lr, tc1);
+  }
+  int valid_count = 0;
+  const int lo_raw = d_lo * 16;
+  const int yend = min(yb + LRS, H);
+  for (int y = yb; y < yend; ++y) {
+    if (y > yb) {  // slide the column sums down one row
+      const uint8_t* ln = lrow(y + HW);
+      const uint8_t* rn = rrow(y + HW);
+      const uint8_t* lo = lrow(y - HW - 1);
+      const uint8_t* ro = rrow(y - HW - 1);
+#pragma unroll 4
+      for (int c = 0; c < NC; ++c) {
+        const int xc = clampi(xb - HW + c, 0, W - 1);
+        const int lnv = ln[xc], lov = lo[xc];
+#pragma unroll
+        for (int k = 0; k < DPL; ++k) {
+          const int xr = clampi(xb - HW + c - dd[k], 0, W - 1);
+          cs[k][c][lane] += abs(lnv - (int)rn[xr]) - abs(lov - (int)ro[xr]);
+        }
+      }
+      tv0 += hd(ln, tc0) - hd(lo, tc0);
+      tv1 += hd(ln, tc1) - hd(lo, tc1);
+    }
+    __syncwarp();
+    // texture gate of this lane's pixel x = xb + lane: columns x-HW .. x+HW-1
+    int grad = 0;
+#pragma unroll
+    for (int t = 0; t < 2 * HW; ++t) {
+      const int src = lane + t;
+      const int a = __shfl_sync(0xffffffffu, tv0, src & 31);
+      const int b = __shfl_sync(0xffffffffu, tv1, src & 31);
+      grad += src < 32 ? a : b;
+    }
+    // per-pixel argmin over d (results land in lane == pixel index)
+    int my_best = 0, my_bi = -1, my_second = 0x7fffffff, my_cm = -1, my_cp = -1;
+    int sad[DPL];
+#pragma unroll
+    for (int k = 0; k < DPL; ++k) {
+      sad[k] = 0;
+#pragma unroll
+      for (int c = 0; c < 2 * HW + 1; ++c) sad[k] += cs[k][c][lane];
+    }
+#pragma unroll 2
+    for (int xi = 0; xi < LBW; ++xi) {
+      if (xi > 0) {
+#pragma unroll
+        for (int k = 0; k < DPL; ++k) sad[k] += cs[k][xi + 2 * HW][lane] - cs[k][xi - 1][lane];
+      }
+      const int x = xb + xi;
+      int key = 0x7fffffff;
+      bool ev[DPL];
+#pragma unroll
+      for (int k = 0; k < DPL; ++k) {
+        ev[k] = (lane + 32 * k < nd) && (x - dd[k] - HW >= 0) && (x - dd[k] + HW < W);  // bm.hpp:61-64
+        if (ev[k]) key = min(key, (sad[k] << 7) | (lane + 32 * k));
+      }
+      const int bk = __reduce_min_sync(0xffffffffu, key);
+      if (bk != 0x7fffffff) {  // warp-uniform
+        const int bi = bk & 127;
+        int sec = 0x7fffffff, vm = -1, vp = -1;
+#pragma unroll
+        for (int k = 0; k < DPL; ++k) {
+          const int i = lane + 32 * k;
+          if (ev[k] && abs(i - bi) > 1) sec = min(sec, sad[k]);
+          if (bi >= 1 && k == ((bi - 1) >> 5)) vm = ev[k] ? sad[k] : -1;
+          if (k == ((bi + 1) >> 5)) vp = ev[k] ? sad[k] : -1;
+        }
+        sec = __reduce_min_sync(0xffffffffu, sec);
+        const int cm = __shfl_sync(0xffffffffu, vm, (bi - 1) & 31);
+        const int cp = __shfl_sync(0xffffffffu, vp, (bi + 1) & 31);
+        if (lane == xi) {
+          my_best = bk >> 7;
+          my_bi = bi;
+          my_second = sec;
+          my_cm = bi >= 1 ? cm : -1;
+          my_cp = bi + 1 < nd ? cp : -1;
+        }
+      }
+    }
+    // lane-parallel epilogue for pixel (xb + lane, y) (bm.hpp:47-100)
+    const int x = xb + lane;
+    if (x < W) {
+      int out = kInvalid;
+      const bool defined = x >= HW && x < W - HW && y >= HW && y < H - HW && !((double)grad < tex);
+      if (defined && my_bi >= 0) {
+        bool ok = true;
+        if (my_second != 0x7fffffff &&
+            __dmul_rn((double)my_best, __dadd_rn(1.0, __ddiv_rn(uniq, 100.0))) >= (double)my_second)
+          ok = false;
+        if (ok) {
+          double d_hat = (double)(d_lo + my_bi);
+          if (my_bi > 0 && my_bi + 1 < nd && my_cm >= 0 && my_cp >= 0)
+            d_hat = __dadd_rn(d_hat, subpix((double)my_cm, (double)my_best, (double)my_cp));
+          long long r = llround(__dmul_rn(d_hat, 16.0));
+          const long long rlo = (long long)d_lo * 16, rhi = (long long)d_hi * 16 - 1;
+          r = r < rlo ? rlo : (r > rhi ? rhi : r);
+          out = (int)r;
+        }
+      }
+      if (raw) raw[((int64_t)frame * n_delta + kd) * W * H + (int64_t)y * W + x] = (int16_t)out;
+      if (out != kInvalid && out > lo_raw) ++valid_count;
+    }
+    __syncwarp();
+  }
+  if (counts) {
+    valid_count = __reduce_add_sync(0xffffffffu, valid_count);
+    if (lane == 0 && valid_count)
+      atomicAdd((unsigned long long*)&counts[(int64_t)frame * n_delta + kd], (unsigned long long)valid_count);
+  }
+}
+
+template <int HW, int DPL>
+static cudaError_t launch_lanes(const uint8_t* left, const uint8_t* right, int n_frames, int64_t stride, int pitch,
+                                int img_h, int w, int h, int x0, int y0, int delta_min, int n_delta, rg_bm_params p,
+                                int16_t* raw, int64_t* counts, cudaStream_t s) {
+  const int bands = (w + LBW - 1) / LBW;
+  dim3 grid((bands + LWPB - 1) / LWPB, (h + LRS - 1) / LRS, n_frames * n_delta);
+  bm_lanes_kernel<HW, DPL><<<grid, LWPB * 32, 0, s>>>(left, right, stride, pitch, img_h, w, h, x0, y0, delta_min,
+                                                       n_delta, p.min_disparity, p.num_disparities,
+                                                       p.texture_threshold, p.uniqueness_ratio, raw, counts);
+  return cudaGetLastError();
+}
+
 __global__ void downscale_kernel(const uint8_t* __restrict__ in, int w, int h, int s,
                                  uint8_t* __restrict__ out) {  // image.hpp:98-116
   const int ow = w / s, oh = h / s;
@@ -254,6 +449,16 @@ cudaError_t launch_bm(const uint8_t* left, const uint8_t* right, int n_frames, i
                       int n_delta, rg_bm_params p, int16_t* raw, int64_t* counts, cudaStream_t s) {
   if (n_frames <= 0 || n_delta <= 0) return cudaSuccess;
   const int hw = p.block_size / 2;
+  const int dpl = (p.num_disparities + 31) / 32;
+  if (getenv("RG_BM_LEGACY") == nullptr && hw >= 1 && hw <= 4 && dpl <= 2) {
+#define RG_BM_CASE(HW, DPL)                                                                             \
+  if (hw == HW && dpl == DPL)                                                                            \
+    return launch_lanes<HW, DPL>(left, right, n_frames, stride, pitch, img_h, w, h, x0, y0, delta_min, n_delta, \
+                                 p, raw, counts, s);
+    RG_BM_CASE(1, 1) RG_BM_CASE(2, 1) RG_BM_CASE(3, 1) RG_BM_CASE(4, 1)
+    RG_BM_CASE(1, 2) RG_BM_CASE(2, 2) RG_BM_CASE(3, 2) RG_BM_CASE(4, 2)
+#undef RG_BM_CASE
+  }
   const int TR = TYB + 2 * hw, LW = TXB + 2 * hw, RW = TXB + 2 * hw + p.num_disparities - 1;
   const size_t smem = (((size_t)TR * (LW + RW)) + 15) / 16 * 16 + sizeof(int) * TYB * LW;
   cudaError_t e = cudaFuncSetAttribute(bm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
