@@ -132,7 +132,7 @@ __device__ __forceinline__ void c2_codes(const uint32_t (&w)[5][8], uint32_t lo[
       if (wi == 12) continue;  // centre: its 0 bit is folded into w13's x4
       const int j = wi / 5, i = wi % 5;
       const __half2 v = *reinterpret_cast<const __half2*>(&w[j][q + i]);
-      const __half2 m = (wi % 3 == 0) ? __hsub2_sat(v, c) : __hgt2(v, c);
+      const __half2 m = (wi % 6 == 0) ? __hsub2_sat(v, c) : __hgt2(v, c);
       const int gi = wi < 8 ? 0 : (wi < 17 ? 1 : 2);
       g[gi] = __hfma2(g[gi], wi == 13 ? four : two, m);
     }
@@ -204,12 +204,18 @@ __global__ void __launch_bounds__(C2_WARPS * 32) census_pairs_kernel(
   const int wk = threadIdx.x % C2_WORDS, run = threadIdx.x / C2_WORDS;
   if (run < C2_RUNS) {
     const int kw = min(max((x0 - 4) / 4 + wk, 0), (w + 3) / 4 - 1);
-    const uint32_t* col = reinterpret_cast<const uint32_t*>(img) + kw;
     const int pw = pitch / 4;
-    const int r0 = run * C2_RUN;
+    const int r0 = run * C2_RUN, ya = y0 - 2 + r0;
     uint32_t wv[C2_RUN + 1];
+    if (ya >= 0 && ya + C2_RUN <= h - 1) {  // interior run: plain strided loads
+      const uint32_t* col = reinterpret_cast<const uint32_t*>(img) + (int64_t)ya * pw + kw;
 #pragma unroll
-    for (int t = 0; t <= C2_RUN; ++t) wv[t] = __ldg(col + (int64_t)min(max(y0 - 2 + r0 + t, 0), h - 1) * pw);
+      for (int t = 0; t <= C2_RUN; ++t) wv[t] = __ldg(col + t * pw);
+    } else {
+      const uint32_t* col = reinterpret_cast<const uint32_t*>(img) + kw;
+#pragma unroll
+      for (int t = 0; t <= C2_RUN; ++t) wv[t] = __ldg(col + (int64_t)min(max(ya + t, 0), h - 1) * pw);
+    }
     uint32_t* vrow = V + r0 * C2_VW + C2_VOFF + 4 * wk - 2;  // entries of columns x0-4+4wk .. +3
 #pragma unroll
     for (int t = 0; t < C2_RUN; ++t) {
