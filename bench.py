@@ -184,7 +184,7 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--frames", type=int, default=256, help="frames per step per GPU")
     ap.add_argument("--distinct", type=int, default=32, help="distinct rendered frames in the HBM ring")
@@ -376,11 +376,11 @@ def main():
     except Exception:
         pass
     census_roof = {"bound": "hbm", "achieved": census_gbs, "peak": hbm_peak, "unit": "GB/s",
-                   "frac": census_gbs / hbm_peak, "traffic": traffic, "kernel": "census_frames_kernel",
+                   "frac": census_gbs / hbm_peak, "traffic": traffic, "kernel": "census_pairs_kernel",
                    "peak_source": peak_kind, "algorithmic_bytes_per_launch": CENSUS_BYTES_PER_FRAME * F,
                    "ms_per_launch": census_ms}
     match_roof = {"bound": "int/popc", "achieved": match_rate / 1e12, "peak": popc_peak / 1e12,
-                  "unit": "Tevals/s", "frac": match_rate / popc_peak, "kernel": "match_slots_kernel",
+                  "unit": "Tevals/s", "frac": match_rate / popc_peak, "kernel": "match_slots_warp_kernel",
                   "hamming_evals_per_launch": evals_per_launch, "ms_per_launch": match_ms,
                   "peak_source": f"nominal {POPC_PER_CLK_PER_SM} POPC/clk/SM x {N_SM} SMs x {clk_mhz:.0f} MHz"}
     dominant = census_roof if census_ms >= match_ms else match_roof
