@@ -63,6 +63,8 @@ inline rg_ranger_config to_c(const RangerConfig& c) {
   r.crop_y1 = c.frontal_crop.y1;
   r.dx_max_far = c.dx_max_far;
   r.dx_max_close = c.dx_max_close;
+  r.census_9x7 = 0;  // the reference has only the 5x5 transform
+  r.reserved = 0;
   return r;
 }
 inline const rg_detection* to_c(const std::vector<Detection>& d) {

@@ -117,6 +117,10 @@ typedef struct {
   double crop_x0, crop_y0, crop_x1, crop_y1;
   int32_t dx_max_far;
   int32_t dx_max_close;
+  /* extension (BASELINE config 1): 1 = 9x7 census, 64-bit
+   * descriptors (63 compares + sentinel bit 63); 0 = the reference's 5x5. */
+  int32_t census_9x7;
+  int32_t reserved;
 } rg_ranger_config;
 
 /* ObjectDisparity (template_match.hpp:18-24) plus the range z_cam
@@ -174,6 +178,14 @@ rg_status rg_census_transform_rois(rg_ctx* ctx, const uint8_t* img, int w, int h
                                    int out_w, int out_h, const rg_rect* rois,
                                    int n_rois, uint32_t* codes);
 
+/* 9x7 census extension: code = 1, then for window rows -3..3 and
+ * columns -4..4 (row-major) code = code << 1 | (I(x+i, y+j) > I(x, y)); the
+ * sentinel ends in bit 63; 0 when the window leaves the image (x < 4,
+ * y < 3, x >= W-4, y >= H-3).  Same reduced-raster mapping as census.hpp:59-64.
+ * No reference function exists (parity unpinned by the reference's tests). */
+rg_status rg_census_transform64(rg_ctx* ctx, const uint8_t* img, int w, int h, int out_w,
+                                int out_h, uint64_t* codes);
+
 /* ------------------------------------------------------ matcher (K2) */
 
 /* block_match (census.hpp:178-272), forward_backward_match (:281-303) and
@@ -185,6 +197,12 @@ rg_status rg_match_blocks(rg_ctx* ctx, const uint32_t* left, int lw, int lh,
                           const int32_t* points_xy, const int64_t* offsets,
                           const rg_search_range* ranges, int n_blocks, int mode,
                           double tau_v, rg_match_result* out);
+
+/* rg_match_blocks over 64-bit (9x7) descriptors */
+rg_status rg_match_blocks64(rg_ctx* ctx, const uint64_t* left, int lw, int lh,
+                            const uint64_t* right, int rw, int rh, const int32_t* points_xy,
+                            const int64_t* offsets, const rg_search_range* ranges, int n_blocks,
+                            int mode, double tau_v, rg_match_result* out);
 
 /* ------------------------------------------------------ object ranger */
 

@@ -58,6 +58,13 @@ extern "C" {
 ORC_DECL(orc_)
 ORC_DECL(ref_)
 
+/* 9x7 / uint64 extension (restatement only; no reference function) */
+int orc_census_transform64(const uint8_t* img, int w, int h, int ow, int oh, uint64_t* out);
+int orc_match_blocks64(const uint64_t* left, int lw, int lh, const uint64_t* right, int rw, int rh,
+                       const int32_t* points_xy, const int64_t* offsets,
+                       const rg_search_range* ranges, int n_blocks, int mode, double tau_v,
+                       rg_match_result* out);
+
 /* reference-only extras (ref_shim.cpp) */
 int ref_render_stereo_pair(const rg_scene_config* cfg, const rg_scene_object* objs,
                            int n_obj, uint8_t* left, uint8_t* right);

@@ -33,6 +33,19 @@ static uint32_t census_at(const uint8_t* img, int w, int h, int sx, int sy) {
   return code;
 }
 
+/* 9x7 extension: census.hpp:43-56 with rows -3..3, columns
+ * -4..4; 63 compares after the sentinel, which ends in bit 63. */
+static uint64_t census_at64(const uint8_t* img, int w, int h, int sx, int sy) {
+  if (sx < 4 || sy < 3 || sx >= w - 4 || sy >= h - 3) return 0u;
+  const uint8_t centre = img[(size_t)sy * w + sx];
+  uint64_t code = 1u;
+  for (int dy = -3; dy <= 3; ++dy) {
+    const uint8_t* row = img + (size_t)(sy + dy) * w + sx;
+    for (int dx = -4; dx <= 4; ++dx) code = (code << 1) | (uint64_t)(row[dx] > centre);
+  }
+  return code;
+}
+
 /* census.hpp:59-64 detail::scaled_coords */
 static void scaled_coords(int out, int src, int* m) {
   for (int i = 0; i < out; ++i)
@@ -49,6 +62,19 @@ int orc_census_transform(const uint8_t* img, int w, int h, int ow, int oh, uint3
   scaled_coords(oh, h, my);
   for (int y = 0; y < oh; ++y)
     for (int x = 0; x < ow; ++x) out[(size_t)y * ow + x] = census_at(img, w, h, mx[x], my[y]);
+  free(mx);
+  free(my);
+  return RG_OK;
+}
+
+int orc_census_transform64(const uint8_t* img, int w, int h, int ow, int oh, uint64_t* out) {
+  if (ow > w || oh > h || ow < 1 || oh < 1) return RG_EINVAL;
+  int* mx = (int*)malloc(sizeof(int) * (size_t)ow);
+  int* my = (int*)malloc(sizeof(int) * (size_t)oh);
+  scaled_coords(ow, w, mx);
+  scaled_coords(oh, h, my);
+  for (int y = 0; y < oh; ++y)
+    for (int x = 0; x < ow; ++x) out[(size_t)y * ow + x] = census_at64(img, w, h, mx[x], my[y]);
   free(mx);
   free(my);
   return RG_OK;
@@ -88,10 +114,13 @@ int orc_census_transform_rois(const uint8_t* img, int w, int h, int ow, int oh,
 typedef struct {
   const uint32_t* codes;
   int w, h;
+  const uint64_t* codes64; /* 9x7 extension: used when non-NULL */
 } raster;
 
 static int r_inside(const raster* r, int x, int y) { return x >= 0 && x < r->w && y >= 0 && y < r->h; }
-static uint32_t r_code(const raster* r, int x, int y) { return r->codes[(size_t)y * r->w + x]; }
+static uint64_t r_code(const raster* r, int x, int y) {
+  return r->codes64 ? r->codes64[(size_t)y * r->w + x] : r->codes[(size_t)y * r->w + x];
+}
 
 /* census.hpp:167-171 */
 static double subpixel(double cm, double c0, double cp) {
@@ -115,13 +144,13 @@ static int block_match(const int32_t* pts, int np, rg_search_range rg, const ras
   int* cnt = (int*)calloc(nc, sizeof(int));
   int* vx = (int*)malloc(sizeof(int) * (size_t)np);
   int* vy = (int*)malloc(sizeof(int) * (size_t)np);
-  uint32_t* lc = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)np);
+  uint64_t* lc = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)np);
   int nv = 0;
   /* :195-201 keep points whose left descriptor exists */
   for (int k = 0; k < np; ++k) {
     const int x = pts[2 * k], y = pts[2 * k + 1];
     if (!r_inside(L, x, y)) continue;
-    const uint32_t c = r_code(L, x, y);
+    const uint64_t c = r_code(L, x, y);
     if (c == 0u) continue;
     vx[nv] = x;
     vy[nv] = y;
@@ -138,9 +167,9 @@ static int block_match(const int32_t* pts, int np, rg_search_range rg, const ras
       for (int k = 0; k < nv; ++k) {
         const int rx = vx[k] - dx, ry = vy[k] + dy;
         if (!r_inside(R, rx, ry)) continue;
-        const uint32_t rc = r_code(R, rx, ry);
+        const uint64_t rc = r_code(R, rx, ry);
         if (rc == 0u) continue;
-        sum += __builtin_popcount(lc[k] ^ rc);
+        sum += __builtin_popcountll(lc[k] ^ rc);
         ++n;
       }
       mean[(size_t)iy * ndx + ix] = n > 0 ? (double)sum / n : INFINITY;
@@ -222,7 +251,21 @@ int orc_match_blocks(const uint32_t* left, int lw, int lh, const uint32_t* right
                      int rh, const int32_t* points_xy, const int64_t* offsets,
                      const rg_search_range* ranges, int n_blocks, int mode, double tau_v,
                      rg_match_result* out) {
-  const raster L = {left, lw, lh}, R = {right, rw, rh};
+  const raster L = {left, lw, lh, NULL}, R = {right, rw, rh, NULL};
+  for (int b = 0; b < n_blocks; ++b) {
+    const int np = (int)(offsets[b + 1] - offsets[b]);
+    const int32_t* p = points_xy + 2 * offsets[b];
+    const int st = mode == RG_MATCH_FWD_BWD ? fb_match(p, np, ranges[b], tau_v, &L, &R, &out[b])
+                                            : block_match(p, np, ranges[b], &L, &R, &out[b]);
+    if (st != RG_OK) return st;
+  }
+  return RG_OK;
+}
+
+int orc_match_blocks64(const uint64_t* left, int lw, int lh, const uint64_t* right, int rw, int rh,
+                       const int32_t* points_xy, const int64_t* offsets, const rg_search_range* ranges,
+                       int n_blocks, int mode, double tau_v, rg_match_result* out) {
+  const raster L = {NULL, lw, lh, left}, R = {NULL, rw, rh, right};
   for (int b = 0; b < n_blocks; ++b) {
     const int np = (int)(offsets[b + 1] - offsets[b]);
     const int32_t* p = points_xy + 2 * offsets[b];
@@ -486,6 +529,7 @@ int orc_estimate_object_disparities(const uint8_t* left, const uint8_t* right, i
                                     rg_census_cache* cache, double focal_px, double baseline_m,
                                     rg_object_disparity* out, int* n_out, rg_ranger_stats* stats) {
   if (validate_cfg(cfg) != RG_OK) return RG_EINVAL;
+  if (cfg->census_9x7 && cache) return RG_EINVAL; /* caches hold 5x5 codes */
   *n_out = 0;
   if (stats) {
     stats->query_points = 0;
@@ -565,7 +609,7 @@ int orc_estimate_object_disparities(const uint8_t* left, const uint8_t* right, i
   if (cache && cache->has_full) {
     fl = cache->full_left;
     fr = cache->full_right;
-  } else if (n_far_b > 0) {
+  } else if (n_far_b > 0 && !cfg->census_9x7) {
     fl = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)w * h);
     fr = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)w * h);
     orc_census_transform_rois(left, w, h, w, h, far_rois, n_far_roi, fl);
@@ -580,7 +624,7 @@ int orc_estimate_object_disparities(const uint8_t* left, const uint8_t* right, i
   if (cache && cache->has_scaled) {
     sl = cache->scaled_left;
     sr = cache->scaled_right;
-  } else if (n_close_b > 0) {
+  } else if (n_close_b > 0 && !cfg->census_9x7) {
     sl = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)cw * ch);
     sr = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)cw * ch);
     orc_census_transform_rois(left, w, h, cw, ch, sc_rois, n_sc_roi, sl);
@@ -593,7 +637,24 @@ int orc_estimate_object_disparities(const uint8_t* left, const uint8_t* right, i
     own_scaled = 1;
   }
   rg_match_result* res = (rg_match_result*)calloc((size_t)(nb + 1), sizeof(rg_match_result));
-  const raster FL = {fl, w, h}, FR = {fr, w, h}, SL = {sl, cw, ch}, SR = {sr, cw, ch};
+  raster FL = {fl, w, h, NULL}, FR = {fr, w, h, NULL}, SL = {sl, cw, ch, NULL}, SR = {sr, cw, ch, NULL};
+  uint64_t *f64l = NULL, *f64r = NULL, *s64l = NULL, *s64r = NULL;
+  if (cfg->census_9x7) { /* extension: full-frame 9x7 rasters (same results as ROI rasters) */
+    f64l = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)w * h);
+    f64r = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)w * h);
+    s64l = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)cw * ch + 8);
+    s64r = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)cw * ch + 8);
+    orc_census_transform64(left, w, h, w, h, f64l);
+    orc_census_transform64(right, w, h, w, h, f64r);
+    if (cw > 0 && ch > 0) {
+      orc_census_transform64(left, w, h, cw, ch, s64l);
+      orc_census_transform64(right, w, h, cw, ch, s64r);
+    }
+    FL.codes64 = f64l;
+    FR.codes64 = f64r;
+    SL.codes64 = s64l;
+    SR.codes64 = s64r;
+  }
   for (int b = 0; b < nb; ++b) {
     const int far = kind[owner[b]] == RG_KIND_FAR;
     fb_match(pts + 2 * boff[b], (int)(boff[b + 1] - boff[b]), rgs[b], cfg->tau_v,
@@ -634,6 +695,10 @@ int orc_estimate_object_disparities(const uint8_t* left, const uint8_t* right, i
   }
   free(disps);
   free(res);
+  free(f64l);
+  free(f64r);
+  free(s64l);
+  free(s64r);
   if (own_full) {
     free(fl);
     free(fr);

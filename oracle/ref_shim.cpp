@@ -252,6 +252,7 @@ int ref_estimate_object_disparities(const uint8_t* left, const uint8_t* right, i
                                     const rg_detection* dets, int n_dets, const rg_ranger_config* cfg,
                                     rg_census_cache* cache, double focal_px, double baseline_m,
                                     rg_object_disparity* out, int* n_out, rg_ranger_stats* stats) {
+  if (cfg->census_9x7) return RG_EINVAL;  // the reference has only the 5x5 census
   return guarded([&] {
     const GrayImage L = to_gray(left, w, h), R = to_gray(right, w, h);
     const RangerConfig rc = to_cfg(cfg);

@@ -41,6 +41,7 @@ class RangerConfig(C.Structure):
         ("n_min", C.c_int32), ("max_objects", C.c_int32), ("tau_v", C.c_double),
         ("crop_x0", C.c_double), ("crop_y0", C.c_double), ("crop_x1", C.c_double), ("crop_y1", C.c_double),
         ("dx_max_far", C.c_int32), ("dx_max_close", C.c_int32),
+        ("census_9x7", C.c_int32), ("reserved", C.c_int32),
     ]
 
 
@@ -112,6 +113,8 @@ SIGNATURES = {
     "rg_census_transform": (I, [P, P, I, I, I, I, P]),
     "rg_census_transform_rois": (I, [P, P, I, I, I, I, P, I, P]),
     "rg_match_blocks": (I, [P, P, I, I, P, I, I, P, P, P, I, I, D, P]),
+    "rg_census_transform64": (I, [P, P, I, I, I, I, P]),
+    "rg_match_blocks64": (I, [P, P, I, I, P, I, I, P, P, P, I, I, D, P]),
     "rg_validate_ranger_config": (I, [P, P]),
     "rg_select_objects": (I, [P, P, I, P, P, P]),
     "rg_find_occluders": (I, [P, P, I, P, P]),

@@ -196,9 +196,9 @@ int planner_max_points(const rg_ranger_config& c) {
   return std::max(nf * nf, nc * nc);
 }
 
-size_t match_smem_bytes(int maxp, bool with_pts) {
+size_t match_smem_bytes(int maxp, bool with_pts, size_t code_bytes = sizeof(uint32_t)) {
   const size_t mp = (size_t)((maxp + 3) & ~3);
-  return sizeof(uint32_t) * kWindowCodes + (with_pts ? 8 * mp : 0) + 16 * mp;
+  return code_bytes * (kWindowCodes + mp) + (with_pts ? 8 * mp : 0) + 12 * mp;
 }
 constexpr size_t kSmemLimit = 220 * 1024;
 
@@ -229,7 +229,7 @@ bool same_geom(const PadGeom& a, const PadGeom& b) {
 }
 
 struct PipelineBufs {
-  uint32_t *fl, *fr, *sl, *sr;
+  uint32_t *fl, *fr, *sl, *sr;  // 5x5 rasters (9x7 runs keep 64-bit codes here)
   PadGeom gf, gs;
   ObjEntry* objs;
   Slot* slots;
@@ -246,32 +246,39 @@ rg_status enqueue_pipeline(rg_ctx* ctx, const FrameJob& J, const rg_ranger_confi
   const int F = J.n_frames;
   if (cw < 1 || ch < 1) return set_err(ctx, RG_EINVAL, "estimate_object_disparities: close raster empty");
   const int maxp = planner_max_points(cfg);
-  if (sizeof(int2) * 2 * (size_t)maxp * 4 > kSmemLimit)
+  // 9x7 extension: 64-bit codes, window rows +-3 / cols +-4
+  const bool wide = cfg.census_9x7 != 0;
+  const size_t csz = wide ? sizeof(unsigned long long) : sizeof(uint32_t);
+  const int rx = wide ? 4 : 2, ry = wide ? 3 : 2;
+  if ((sizeof(int2) + 2 * csz) * (size_t)maxp * 8 > kSmemLimit)
     return set_err(ctx, RG_EINVAL, "RangerConfig: blocks too large for the device matcher");
+  if (wide && (J.full_l || J.scaled_l))
+    return set_err(ctx, RG_EINVAL, "RangerConfig: census_9x7 cannot use a CensusCache");
   // zero-padded census rasters: margins cover every sample the search reaches
   const int dxs = (cfg.dx_max_close + sc - 1) / sc;
   const int padf = 32 * ((cfg.dx_max_far + 1 + 31) / 32) + 4;
   const int pads = 32 * ((dxs + 1 + 31) / 32) + 4;
   PadGeom gf = make_geom(w, h, padf, 2), gs = make_geom(cw, ch, pads, 2);
-  // where a computed code is defined: full [2, W-3] (census.hpp:44); reduced
-  // x' with lround(x' * W / cw) in [2, W-3] (census.hpp:59-64)
+  // where a computed code is defined: full [rx, W-1-rx] (census.hpp:44); reduced
+  // x' with lround(x' * W / cw) in that range (census.hpp:59-64)
   {
     const auto mx = scaled_coords(cw, w), my = scaled_coords(ch, h);
-    gf.sx0 = 2, gf.sx1 = w - 3, gf.sy0 = 2, gf.sy1 = h - 3;
+    gf.sx0 = rx, gf.sx1 = w - 1 - rx, gf.sy0 = ry, gf.sy1 = h - 1 - ry;
     gs.sx0 = cw, gs.sx1 = -1, gs.sy0 = ch, gs.sy1 = -1;
     for (int i = 0; i < cw; ++i)
-      if (mx[i] >= 2 && mx[i] <= w - 3) gs.sx0 = std::min(gs.sx0, i), gs.sx1 = std::max(gs.sx1, i);
+      if (mx[i] >= rx && mx[i] <= w - 1 - rx) gs.sx0 = std::min(gs.sx0, i), gs.sx1 = std::max(gs.sx1, i);
     for (int i = 0; i < ch; ++i)
-      if (my[i] >= 2 && my[i] <= h - 3) gs.sy0 = std::min(gs.sy0, i), gs.sy1 = std::max(gs.sy1, i);
+      if (my[i] >= ry && my[i] <= h - 1 - ry) gs.sy0 = std::min(gs.sy0, i), gs.sy1 = std::max(gs.sy1, i);
   }
-  const size_t fbytes = sizeof(uint32_t) * (size_t)gf.fstride * F;
-  const size_t sbytes = sizeof(uint32_t) * (size_t)gs.fstride * F;
+  const size_t fbytes = csz * (size_t)gf.fstride * F;
+  const size_t sbytes = csz * (size_t)gs.fstride * F;
   const bool regeom = ctx->cap[B_CEN_FL] < fbytes || ctx->cap[B_CEN_SL] < sbytes ||
-                      !same_geom(ctx->pad_key, gf) || !same_geom(ctx->pad_key_s, gs);
-  uint32_t* fl = DBUF(uint32_t, ctx, B_CEN_FL, gf.fstride * F);
-  uint32_t* fr = DBUF(uint32_t, ctx, B_CEN_FR, gf.fstride * F);
-  uint32_t* sl = DBUF(uint32_t, ctx, B_CEN_SL, gs.fstride * F);
-  uint32_t* sr = DBUF(uint32_t, ctx, B_CEN_SR, gs.fstride * F);
+                      !same_geom(ctx->pad_key, gf) || !same_geom(ctx->pad_key_s, gs) ||
+                      ctx->pad_wide != (int)wide;
+  uint32_t* fl = static_cast<uint32_t*>(dev_buf(ctx, B_CEN_FL, fbytes));
+  uint32_t* fr = static_cast<uint32_t*>(dev_buf(ctx, B_CEN_FR, fbytes));
+  uint32_t* sl = static_cast<uint32_t*>(dev_buf(ctx, B_CEN_SL, sbytes));
+  uint32_t* sr = static_cast<uint32_t*>(dev_buf(ctx, B_CEN_SR, sbytes));
   NEED(fl);
   NEED(fr);
   NEED(sl);
@@ -283,6 +290,7 @@ rg_status enqueue_pipeline(rg_ctx* ctx, const FrameJob& J, const rg_ranger_confi
     RG_CUDA(ctx, cudaMemsetAsync(sr, 0, ctx->cap[B_CEN_SR], s));
     ctx->pad_key = gf;
     ctx->pad_key_s = gs;
+    ctx->pad_wide = (int)wide;
   }
   if (ctx->slot_capacity < F * 64) ctx->slot_capacity = F * 64;
   const int capacity = ctx->slot_capacity;
@@ -300,7 +308,12 @@ rg_status enqueue_pipeline(rg_ctx* ctx, const FrameJob& J, const rg_ranger_confi
   const bool prof = ctx->profiling;
   if (prof) RG_CUDA(ctx, cudaEventRecord(ctx->ev[0], s));
   // K1 census (full + fused reduced raster) of both images of every frame
-  if (!(J.full_l && J.scaled_l)) {
+  if (wide) {
+    using u64 = unsigned long long;
+    RG_CUDA(ctx, launch_census64_frames(J.left, J.right, F, J.frame_stride, J.pitch, w, h, (u64*)fl, (u64*)fr,
+                                        gf, (u64*)sl, (u64*)sr, gs, ix, iy, s));
+    count_launch(ctx, ST_CENSUS);
+  } else if (!(J.full_l && J.scaled_l)) {
     RG_CUDA(ctx, launch_census_frames(J.left, J.right, F, J.frame_stride, J.pitch, w, h, fl, fr, gf, sl,
                                       sr, gs, ix, iy, s));
     count_launch(ctx, ST_CENSUS);
@@ -328,7 +341,7 @@ rg_status enqueue_pipeline(rg_ctx* ctx, const FrameJob& J, const rg_ranger_confi
   // K2 fused sampler + forward/backward matcher, one warp per slot
   const int trusted = !(J.full_l || J.scaled_l);
   RG_CUDA(ctx, launch_match_slots(slots, counters, capacity, objs, J.dets, J.det_off, fl, fr, gf, sl, sr, gs,
-                                  w, h, trusted, cfg, res, J.stats, maxp, s));
+                                  w, h, trusted, (int)wide, cfg, res, J.stats, maxp, s));
   count_launch(ctx, ST_MATCH);
   if (prof) RG_CUDA(ctx, cudaEventRecord(ctx->ev[3], s));
   // K4 aggregation + range
@@ -546,7 +559,10 @@ rg_status rg_census_transform_rois(rg_ctx* ctx, const uint8_t* img, int w, int h
 }
 
 // =========================================================== matcher
-rg_status rg_match_blocks(rg_ctx* ctx, const uint32_t* left, int lw, int lh, const uint32_t* right,
+}  // extern "C"
+
+template <typename CT>
+static rg_status match_blocks_common(rg_ctx* ctx, const CT* left, int lw, int lh, const CT* right,
                           int rw, int rh, const int32_t* points_xy, const int64_t* offsets,
                           const rg_search_range* ranges, int n_blocks, int mode, double tau_v,
                           rg_match_result* out) {
@@ -563,12 +579,13 @@ rg_status rg_match_blocks(rg_ctx* ctx, const uint32_t* left, int lw, int lh, con
     if (np > 0 && (ranges[b].dx_min > ranges[b].dx_max || ranges[b].dy_min > ranges[b].dy_max))
       return set_err(ctx, RG_EINVAL, "block_match: empty search range");  // census.hpp:182-183
   }
-  if (match_smem_bytes((int)std::min<int64_t>(maxp, 1 << 20), false) > kSmemLimit)
+  if (match_smem_bytes((int)std::min<int64_t>(maxp, 1 << 20), false, sizeof(CT)) > kSmemLimit)
     return set_err(ctx, RG_EINVAL, "block_match: block has too many points for the device matcher");
   const int64_t total = offsets[n_blocks] - offsets[0];
   const size_t lsz = std::max<size_t>((size_t)lw * lh, 1), rsz = std::max<size_t>((size_t)rw * rh, 1);
-  uint32_t* dl = DBUF(uint32_t, ctx, B_CEN_FL, lsz);
-  uint32_t* dr = DBUF(uint32_t, ctx, B_CEN_FR, rsz);
+  CT* dl = DBUF(CT, ctx, B_CEN_FL, lsz);
+  CT* dr = DBUF(CT, ctx, B_CEN_FR, rsz);
+  ctx->pad_key = PadGeom{};  // the padded pipeline rasters are clobbered
   int32_t* dp = DBUF(int32_t, ctx, B_PTS, 2 * std::max<int64_t>(total, 1));
   int64_t* doff = DBUF(int64_t, ctx, B_OFFS, n_blocks + 1);
   rg_search_range* drg = DBUF(rg_search_range, ctx, B_RANGES, n_blocks);
@@ -580,8 +597,8 @@ rg_status rg_match_blocks(rg_ctx* ctx, const uint32_t* left, int lw, int lh, con
   NEED(drg);
   NEED(dres);
   cudaStream_t s = ctx->stream;
-  if ((size_t)lw * lh) RG_CUDA(ctx, cudaMemcpyAsync(dl, left, sizeof(uint32_t) * lw * lh, cudaMemcpyHostToDevice, s));
-  if ((size_t)rw * rh) RG_CUDA(ctx, cudaMemcpyAsync(dr, right, sizeof(uint32_t) * rw * rh, cudaMemcpyHostToDevice, s));
+  if ((size_t)lw * lh) RG_CUDA(ctx, cudaMemcpyAsync(dl, left, sizeof(CT) * lw * lh, cudaMemcpyHostToDevice, s));
+  if ((size_t)rw * rh) RG_CUDA(ctx, cudaMemcpyAsync(dr, right, sizeof(CT) * rw * rh, cudaMemcpyHostToDevice, s));
   if (total > 0)
     RG_CUDA(ctx, cudaMemcpyAsync(dp, points_xy + 2 * offsets[0], sizeof(int32_t) * 2 * total,
                                  cudaMemcpyHostToDevice, s));
@@ -589,12 +606,65 @@ rg_status rg_match_blocks(rg_ctx* ctx, const uint32_t* left, int lw, int lh, con
   for (int b = 0; b <= n_blocks; ++b) off0[b] = offsets[b] - offsets[0];
   RG_CUDA(ctx, cudaMemcpyAsync(doff, off0.data(), sizeof(int64_t) * (n_blocks + 1), cudaMemcpyHostToDevice, s));
   RG_CUDA(ctx, cudaMemcpyAsync(drg, ranges, sizeof(rg_search_range) * n_blocks, cudaMemcpyHostToDevice, s));
-  const Raster L = {dl, lw, lh, lw}, R = {dr, rw, rh, rw};
-  RG_CUDA(ctx, launch_match_blocks(L, R, dp, doff, drg, n_blocks, mode, tau_v, dres,
-                                   (int)std::max<int64_t>(maxp, 4), s));
+  const RasterT<CT> L = {dl, lw, lh, lw}, R = {dr, rw, rh, rw};
+  if constexpr (sizeof(CT) == 4)
+    RG_CUDA(ctx, launch_match_blocks(L, R, dp, doff, drg, n_blocks, mode, tau_v, dres,
+                                     (int)std::max<int64_t>(maxp, 4), s));
+  else
+    RG_CUDA(ctx, launch_match_blocks64(L, R, dp, doff, drg, n_blocks, mode, tau_v, dres,
+                                       (int)std::max<int64_t>(maxp, 4), s));
   count_launch(ctx, ST_MATCH);
   RG_CUDA(ctx, cudaMemcpyAsync(out, dres, sizeof(rg_match_result) * n_blocks, cudaMemcpyDeviceToHost, s));
   RG_CUDA(ctx, cudaStreamSynchronize(s));
+  return RG_OK;
+}
+
+extern "C" {
+
+rg_status rg_match_blocks(rg_ctx* ctx, const uint32_t* left, int lw, int lh, const uint32_t* right,
+                          int rw, int rh, const int32_t* points_xy, const int64_t* offsets,
+                          const rg_search_range* ranges, int n_blocks, int mode, double tau_v,
+                          rg_match_result* out) {
+  return match_blocks_common(ctx, left, lw, lh, right, rw, rh, points_xy, offsets, ranges, n_blocks, mode,
+                             tau_v, out);
+}
+
+// 9x7 extension: same matcher over 64-bit codes
+rg_status rg_match_blocks64(rg_ctx* ctx, const uint64_t* left, int lw, int lh, const uint64_t* right,
+                            int rw, int rh, const int32_t* points_xy, const int64_t* offsets,
+                            const rg_search_range* ranges, int n_blocks, int mode, double tau_v,
+                            rg_match_result* out) {
+  using u64 = unsigned long long;
+  return match_blocks_common(ctx, reinterpret_cast<const u64*>(left), lw, lh,
+                             reinterpret_cast<const u64*>(right), rw, rh, points_xy, offsets, ranges,
+                             n_blocks, mode, tau_v, out);
+}
+
+// 9x7 extension: full / nearest-downscaled 64-bit census of one image
+rg_status rg_census_transform64(rg_ctx* ctx, const uint8_t* img, int w, int h, int ow, int oh,
+                                uint64_t* codes) {
+  TRY(bind(ctx));
+  if (!img || !codes || w < 1 || h < 1) return set_err(ctx, RG_EINVAL, "census_transform64: bad image");
+  if (ow > w || oh > h) return set_err(ctx, RG_EINVAL, "census_transform64: output dims exceed source");
+  if (ow < 1 || oh < 1) return set_err(ctx, RG_EINVAL, "census_transform64: empty output");
+  using u64 = unsigned long long;
+  uint8_t* d = nullptr;
+  TRY(upload_image(ctx, B_IMG_L, img, w, h, &d));
+  u64* full = DBUF(u64, ctx, B_TMP0, (size_t)w * h);
+  NEED(full);
+  u64* red = nullptr;
+  if (ow != w || oh != h) {
+    red = DBUF(u64, ctx, B_TMP1, (size_t)ow * oh);
+    NEED(red);
+  }
+  int32_t *ix = nullptr, *iy = nullptr;
+  TRY(upload_inverse_maps(ctx, w, h, ow, oh, ctx->stream, &ix, &iy));
+  RG_CUDA(ctx, launch_census64_frames(d, nullptr, 1, 0, w, w, h, full, nullptr, make_geom(w, h, 0, 0), red,
+                                      nullptr, make_geom(ow, oh, 0, 0), ix, iy, ctx->stream));
+  count_launch(ctx, ST_CENSUS);
+  RG_CUDA(ctx, cudaMemcpyAsync(codes, red ? red : full, sizeof(u64) * (size_t)ow * oh, cudaMemcpyDeviceToHost,
+                               ctx->stream));
+  RG_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   return RG_OK;
 }
 
@@ -760,6 +830,8 @@ rg_status rg_estimate_object_disparities(rg_ctx* ctx, const uint8_t* left, const
                                          int* n_out, rg_ranger_stats* stats) {
   TRY(bind(ctx));
   TRY(check_cfg(ctx, cfg));
+  if (cfg->census_9x7 && cache)  // caches hold 5x5 codes
+    return set_err(ctx, RG_EINVAL, "estimate_object_disparities: census_9x7 cannot use a CensusCache");
   if (!left || !right || !n_out || w < 1 || h < 1 || n_dets < 0 || (n_dets > 0 && (!dets || !out)))
     return set_err(ctx, RG_EINVAL, "estimate_object_disparities: bad arguments");
   *n_out = 0;

@@ -236,6 +236,58 @@ __global__ void __launch_bounds__(C2_WARPS * 32) census_pairs_kernel(
     c2_strip<false>(V, full, red, gf, gs, x0, y0, w, h);
 }
 
+// ---------------------------------------------------------------------------
+// 9x7 census extension (BASELINE config 1): 64-bit descriptors, 63
+// compares after the sentinel (window rows -3..3, columns -4..4, row-major,
+// first compare in bit 62), 0 where the window leaves the image.  One output
+// per thread from a byte tile in shared memory; the same inverse maps write
+// the reduced raster.
+constexpr int X_TX = 128, X_TY = 16, X_TPB = 256;
+
+__global__ void __launch_bounds__(X_TPB) census64_kernel(
+    const uint8_t* __restrict__ left, const uint8_t* __restrict__ right, int64_t frame_stride, int pitch,
+    int w, int h, unsigned long long* __restrict__ fl, unsigned long long* __restrict__ fr, PadGeom gf,
+    unsigned long long* __restrict__ sl, unsigned long long* __restrict__ sr, PadGeom gs,
+    const int32_t* __restrict__ inv_x, const int32_t* __restrict__ inv_y) {
+  __shared__ uint8_t tile[X_TY + 6][X_TX + 8];
+  const int sides = right ? 2 : 1;
+  const int frame = blockIdx.z / sides, side = blockIdx.z - frame * sides;
+  const uint8_t* img = (side ? right : left) + (int64_t)frame * frame_stride;
+  unsigned long long* full = (side ? fr : fl) + (int64_t)frame * gf.fstride + gf.origin;
+  unsigned long long* red = side ? sr : sl;
+  if (red) red += (int64_t)frame * gs.fstride + gs.origin;
+  const int x0 = blockIdx.x * X_TX, y0 = blockIdx.y * X_TY;
+  for (int idx = threadIdx.x; idx < (X_TY + 6) * (X_TX + 8); idx += X_TPB) {
+    const int r = idx / (X_TX + 8), c = idx - r * (X_TX + 8);
+    const int gx = x0 + c - 4, gy = y0 + r - 3;
+    tile[r][c] = (gx >= 0 && gx < w && gy >= 0 && gy < h) ? img[(int64_t)gy * pitch + gx] : 0;
+  }
+  __syncthreads();
+  const int tx = threadIdx.x % X_TX, x = x0 + tx;
+  const int ix = (x < w) ? inv_x[x] : -1;
+  for (int ty = threadIdx.x / X_TX; ty < X_TY; ty += X_TPB / X_TX) {
+    const int y = y0 + ty;
+    if (x >= w || y >= h) continue;
+    unsigned long long code = 0ull;
+    if (x >= 4 && y >= 3 && x < w - 4 && y < h - 3) {
+      const uint32_t c = tile[ty + 3][tx + 4];
+      code = 1ull;
+#pragma unroll
+      for (int j = 0; j < 7; ++j) {
+        uint32_t bits = 0u;
+#pragma unroll
+        for (int i = 0; i < 9; ++i) bits = (bits << 1) | (uint32_t)(tile[ty + j][tx + i] > c);
+        code = (code << 9) | bits;
+      }
+    }
+    full[(int64_t)y * gf.pitch + x] = code;
+    if (red && ix >= 0) {
+      const int iy = inv_y[y];
+      if (iy >= 0) red[(int64_t)iy * gs.pitch + ix] = code;
+    }
+  }
+}
+
 // census_transform_rois mask (census.hpp:111-136): keep codes inside the
 // union of the clipped rectangles, zero elsewhere.
 __global__ void roi_mask_kernel(uint32_t* __restrict__ codes, int w, int h,
@@ -281,6 +333,18 @@ cudaError_t launch_census_frames(const uint8_t* left, const uint8_t* right, int 
   dim3 grid((w + TX - 1) / TX, (h + TY - 1) / TY, sides * n_frames);
   census_frames_kernel<<<grid, TPB, 0, s>>>(left, right, frame_stride, pitch, w, h, fl, fr, gf, sl,
                                             sr, gs, inv_x, inv_y);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_census64_frames(const uint8_t* left, const uint8_t* right, int n_frames, int64_t frame_stride,
+                                   int pitch, int w, int h, unsigned long long* fl, unsigned long long* fr,
+                                   const PadGeom& gf, unsigned long long* sl, unsigned long long* sr,
+                                   const PadGeom& gs, const int32_t* inv_x, const int32_t* inv_y,
+                                   cudaStream_t s) {
+  if (n_frames <= 0) return cudaSuccess;
+  dim3 grid((w + X_TX - 1) / X_TX, (h + X_TY - 1) / X_TY, (right ? 2 : 1) * n_frames);
+  census64_kernel<<<grid, X_TPB, 0, s>>>(left, right, frame_stride, pitch, w, h, fl, fr, gf, sl, sr, gs, inv_x,
+                                         inv_y);
   return cudaGetLastError();
 }
 

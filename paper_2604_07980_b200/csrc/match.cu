@@ -77,39 +77,45 @@ struct Scratch {
   PassOut pass;
 };
 
+__device__ __forceinline__ int popc(uint32_t x) { return __popc(x); }
+__device__ __forceinline__ int popc(unsigned long long x) { return __popcll(x); }
+
+template <typename CT>  // code type: uint32_t (5x5) or unsigned long long (9x7)
 struct Dyn {  // dynamic shared memory views
+  CT* win;      // right-census window
+  CT* lc;       // left codes of the valid points
   int2* pts;    // block points (planner path); unused by the CSR path
   int* px;      // valid points after the shift
   int* py;
-  uint32_t* lc; // their left codes
   int* off;     // their window offsets
-  uint32_t* win;
 };
 
-__device__ __forceinline__ Dyn carve(void* base, int maxp, bool with_pts) {
-  Dyn d;
+template <typename CT>
+__device__ __forceinline__ Dyn<CT> carve(void* base, int maxp, bool with_pts) {
+  Dyn<CT> d;
   char* p = reinterpret_cast<char*>(base);
-  d.win = reinterpret_cast<uint32_t*>(p);
-  p += sizeof(uint32_t) * kWindowCodes;
+  d.win = reinterpret_cast<CT*>(p);
+  p += sizeof(CT) * kWindowCodes;
+  d.lc = reinterpret_cast<CT*>(p);
+  p += sizeof(CT) * maxp;
   d.pts = reinterpret_cast<int2*>(p);
   if (with_pts) p += sizeof(int2) * maxp;
   d.px = reinterpret_cast<int*>(p);
   p += sizeof(int) * maxp;
   d.py = reinterpret_cast<int*>(p);
   p += sizeof(int) * maxp;
-  d.lc = reinterpret_cast<uint32_t*>(p);
-  p += sizeof(uint32_t) * maxp;
   d.off = reinterpret_cast<int*>(p);
   return d;
 }
 
-__device__ __forceinline__ uint32_t sample(const Raster& r, int x, int y) {
-  return (x >= 0 && x < r.w && y >= 0 && y < r.h) ? __ldg(r.p + (int64_t)y * r.pitch + x) : 0u;
+template <typename CT>
+__device__ __forceinline__ CT sample(const RasterT<CT>& r, int x, int y) {
+  return (x >= 0 && x < r.w && y >= 0 && y < r.h) ? __ldg(r.p + (int64_t)y * r.pitch + x) : CT(0);
 }
 
 // Candidate sweep over one chunk of CPT candidates per thread.
-template <int CPT, int MODE>  // MODE 0: window, no zeros; 1: window with zeros; 2: global
-__device__ __forceinline__ void sweep(const Dyn& S, int nv, const Raster& R, int c0, int nc,
+template <typename CT, int CPT, int MODE>  // MODE 0: window, no zeros; 1: window with zeros; 2: global
+__device__ __forceinline__ void sweep(const Dyn<CT>& S, int nv, const RasterT<CT>& R, int c0, int nc,
                                       int ndx, int WW, const rg_search_range& rg, Best& mine,
                                       int& evals) {
   const int tid = threadIdx.x;
@@ -130,7 +136,7 @@ __device__ __forceinline__ void sweep(const Dyn& S, int nv, const Raster& R, int
   }
   if (MODE == 0) {
     int k = 0;
-    for (; k + 4 <= nv; k += 4) {
+    if constexpr (sizeof(CT) == 4) for (; k + 4 <= nv; k += 4) {
       const int4 o4 = *reinterpret_cast<const int4*>(S.off + k);
       const uint4 l4 = *reinterpret_cast<const uint4*>(S.lc + k);
 #pragma unroll
@@ -141,21 +147,21 @@ __device__ __forceinline__ void sweep(const Dyn& S, int nv, const Raster& R, int
     }
     for (; k < nv; ++k) {
       const int o = S.off[k];
-      const uint32_t l = S.lc[k];
+      const CT l = S.lc[k];
 #pragma unroll
-      for (int j = 0; j < CPT; ++j) s[j] += __popc(l ^ S.win[o + base[j]]);
+      for (int j = 0; j < CPT; ++j) s[j] += popc(l ^ S.win[o + base[j]]);
     }
 #pragma unroll
     for (int j = 0; j < CPT; ++j) n[j] = nv;
   } else if (MODE == 1) {
     for (int k = 0; k < nv; ++k) {
       const int o = S.off[k];
-      const uint32_t l = S.lc[k];
+      const CT l = S.lc[k];
 #pragma unroll
       for (int j = 0; j < CPT; ++j) {
-        const uint32_t r = S.win[o + base[j]];
+        const CT r = S.win[o + base[j]];
         if (r != 0u) {
-          s[j] += __popc(l ^ r);
+          s[j] += popc(l ^ r);
           ++n[j];
         }
       }
@@ -163,12 +169,12 @@ __device__ __forceinline__ void sweep(const Dyn& S, int nv, const Raster& R, int
   } else {
     for (int k = 0; k < nv; ++k) {
       const int x = S.px[k], y = S.py[k];
-      const uint32_t l = S.lc[k];
+      const CT l = S.lc[k];
 #pragma unroll
       for (int j = 0; j < CPT; ++j) {
-        const uint32_t r = sample(R, x - cdx[j], y + cdy[j]);
+        const CT r = sample(R, x - cdx[j], y + cdy[j]);
         if (r != 0u) {
-          s[j] += __popc(l ^ r);
+          s[j] += popc(l ^ r);
           ++n[j];
         }
       }
@@ -183,15 +189,15 @@ __device__ __forceinline__ void sweep(const Dyn& S, int nv, const Raster& R, int
   }
 }
 
-template <int MODE>
-__device__ __forceinline__ void sweep_all(const Dyn& S, int nv, const Raster& R, int nc, int ndx,
+template <typename CT, int MODE>
+__device__ __forceinline__ void sweep_all(const Dyn<CT>& S, int nv, const RasterT<CT>& R, int nc, int ndx,
                                           int WW, const rg_search_range& rg, Best& mine, int& evals) {
   if (nc <= NT) {
-    sweep<1, MODE>(S, nv, R, 0, nc, ndx, WW, rg, mine, evals);
+    sweep<CT, 1, MODE>(S, nv, R, 0, nc, ndx, WW, rg, mine, evals);
   } else if (nc <= 2 * NT) {
-    sweep<2, MODE>(S, nv, R, 0, nc, ndx, WW, rg, mine, evals);
+    sweep<CT, 2, MODE>(S, nv, R, 0, nc, ndx, WW, rg, mine, evals);
   } else {
-    for (int c0 = 0; c0 < nc; c0 += 4 * NT) sweep<4, MODE>(S, nv, R, c0, nc, ndx, WW, rg, mine, evals);
+    for (int c0 = 0; c0 < nc; c0 += 4 * NT) sweep<CT, 4, MODE>(S, nv, R, c0, nc, ndx, WW, rg, mine, evals);
   }
 }
 
@@ -248,8 +254,9 @@ __device__ void block_sum4(int v[4], Scratch& sc) {
 
 // One block_match pass (census.hpp:178-272).  Points come from `pts`
 // (shared or global memory) shifted by (sx, sy).  Writes sc.pass.
-__device__ void match_pass(const int2* pts, int np, int sx, int sy, const Raster& L,
-                           const Raster& R, const rg_search_range& rg, const Dyn& S,
+template <typename CT>
+__device__ void match_pass(const int2* pts, int np, int sx, int sy, const RasterT<CT>& L,
+                           const RasterT<CT>& R, const rg_search_range& rg, const Dyn<CT>& S,
                            Scratch& sc, int& evals) {
   const int tid = threadIdx.x;
   if (tid == 0) {
@@ -265,7 +272,7 @@ __device__ void match_pass(const int2* pts, int np, int sx, int sy, const Raster
   for (int k = tid; k < np; k += NT) {
     const int2 p = pts[k];
     const int x = p.x + sx, y = p.y + sy;
-    const uint32_t c = sample(L, x, y);
+    const CT c = sample(L, x, y);
     if (c != 0u) {
       const int slot = atomicAdd(&sc.nv, 1);
       S.px[slot] = x;
@@ -297,7 +304,7 @@ __device__ void match_pass(const int2* pts, int np, int sx, int sy, const Raster
     int zero = 0;
     for (int idx = tid; idx < WW * WH; idx += NT) {
       const int wy = idx / WW, wx = idx - wy * WW;
-      const uint32_t v = sample(R, wx0 + wx, wy0 + wy);
+      const CT v = sample(R, wx0 + wx, wy0 + wy);
       S.win[idx] = v;
       zero |= (v == 0u);
     }
@@ -306,11 +313,11 @@ __device__ void match_pass(const int2* pts, int np, int sx, int sy, const Raster
   }
   Best mine = {0, 0, 0, 0};
   if (use_win && !any_zero)
-    sweep_all<0>(S, nv, R, nc, ndx, WW, rg, mine, evals);
+    sweep_all<CT, 0>(S, nv, R, nc, ndx, WW, rg, mine, evals);
   else if (use_win)
-    sweep_all<1>(S, nv, R, nc, ndx, WW, rg, mine, evals);
+    sweep_all<CT, 1>(S, nv, R, nc, ndx, WW, rg, mine, evals);
   else
-    sweep_all<2>(S, nv, R, nc, ndx, WW, rg, mine, evals);
+    sweep_all<CT, 2>(S, nv, R, nc, ndx, WW, rg, mine, evals);
   const Best b = block_best(mine, sc);
   if (b.n == 0) {  // no offset had a contributing point
     if (tid == 0) sc.pass.has = 0;
@@ -323,15 +330,15 @@ __device__ void match_pass(const int2* pts, int np, int sx, int sy, const Raster
   if (interior) {  // costs of (dx-1, dy) and (dx+1, dy)
     for (int k = tid; k < nv; k += NT) {
       const int x = S.px[k], y = S.py[k] + b.dy;
-      const uint32_t l = S.lc[k];
-      const uint32_t rm = sample(R, x - (b.dx - 1), y);
-      const uint32_t rp = sample(R, x - (b.dx + 1), y);
+      const CT l = S.lc[k];
+      const CT rm = sample(R, x - (b.dx - 1), y);
+      const CT rp = sample(R, x - (b.dx + 1), y);
       if (rm) {
-        v[0] += __popc(l ^ rm);
+        v[0] += popc(l ^ rm);
         v[1] += 1;
       }
       if (rp) {
-        v[2] += __popc(l ^ rp);
+        v[2] += popc(l ^ rp);
         v[3] += 1;
       }
     }
@@ -373,8 +380,9 @@ __device__ void finish_pass(const PassOut& p, rg_match_result& r) {
 }
 
 // block_match / forward_backward_match of one block; result written by tid 0.
-__device__ void match_block(const int2* pts, int np, const Raster& L, const Raster& R,
-                            const rg_search_range& rg, int mode, double tau_v, const Dyn& S,
+template <typename CT>
+__device__ void match_block(const int2* pts, int np, const RasterT<CT>& L, const RasterT<CT>& R,
+                            const rg_search_range& rg, int mode, double tau_v, const Dyn<CT>& S,
                             Scratch& sc, rg_match_result* out, unsigned long long* eval_counter) {
   int evals = 0;
   rg_match_result r;
@@ -411,7 +419,8 @@ __device__ void match_block(const int2* pts, int np, const Raster& L, const Rast
 }
 
 // ---------------------------------------------------------------- CSR path
-__global__ void __launch_bounds__(NT) match_blocks_kernel(Raster L, Raster R,
+template <typename CT>
+__global__ void __launch_bounds__(NT) match_blocks_kernel(RasterT<CT> L, RasterT<CT> R,
                                                           const int32_t* __restrict__ pts,
                                                           const int64_t* __restrict__ offs,
                                                           const rg_search_range* __restrict__ ranges,
@@ -420,16 +429,31 @@ __global__ void __launch_bounds__(NT) match_blocks_kernel(Raster L, Raster R,
   extern __shared__ __align__(16) unsigned char dyn[];
   __shared__ Scratch sc;
   const int b = blockIdx.x;
-  const Dyn S = carve(dyn, maxp, false);
+  const Dyn<CT> S = carve<CT>(dyn, maxp, false);
   const int64_t o0 = offs[b];
   const int np = (int)(offs[b + 1] - o0);
   match_block(reinterpret_cast<const int2*>(pts) + o0, np, L, R, ranges[b], mode, tau_v, S, sc,
               &out[b], nullptr);
 }
 
+template <typename CT>
 size_t dyn_bytes(int maxp, bool with_pts) {
-  return sizeof(uint32_t) * kWindowCodes + (with_pts ? sizeof(int2) * maxp : 0) +
-         4 * sizeof(int) * (size_t)maxp;
+  return sizeof(CT) * ((size_t)kWindowCodes + maxp) + (with_pts ? sizeof(int2) * maxp : 0) +
+         3 * sizeof(int) * (size_t)maxp;
+}
+
+template <typename CT>
+cudaError_t launch_csr(RasterT<CT> L, RasterT<CT> R, const int32_t* pts, const int64_t* offs,
+                       const rg_search_range* ranges, int n_blocks, int mode, double tau_v,
+                       rg_match_result* out, int max_points, cudaStream_t s) {
+  if (n_blocks <= 0) return cudaSuccess;
+  const int maxp = (max_points + 3) & ~3;
+  const size_t smem = dyn_bytes<CT>(maxp, false);
+  cudaError_t e = cudaFuncSetAttribute(match_blocks_kernel<CT>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  match_blocks_kernel<CT><<<n_blocks, NT, smem, s>>>(L, R, pts, offs, ranges, mode, tau_v, maxp, out);
+  return cudaGetLastError();
 }
 
 }  // namespace
@@ -438,14 +462,15 @@ cudaError_t launch_match_blocks(Raster L, Raster R, const int32_t* pts, const in
                                 const rg_search_range* ranges, int n_blocks, int mode,
                                 double tau_v, rg_match_result* out, int max_points,
                                 cudaStream_t s) {
-  if (n_blocks <= 0) return cudaSuccess;
-  const int maxp = (max_points + 3) & ~3;
-  const size_t smem = dyn_bytes(maxp, false);
-  cudaError_t e = cudaFuncSetAttribute(match_blocks_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  match_blocks_kernel<<<n_blocks, NT, smem, s>>>(L, R, pts, offs, ranges, mode, tau_v, maxp, out);
-  return cudaGetLastError();
+  return launch_csr<uint32_t>(L, R, pts, offs, ranges, n_blocks, mode, tau_v, out, max_points, s);
+}
+
+cudaError_t launch_match_blocks64(Raster64 L, Raster64 R, const int32_t* pts, const int64_t* offs,
+                                  const rg_search_range* ranges, int n_blocks, int mode,
+                                  double tau_v, rg_match_result* out, int max_points,
+                                  cudaStream_t s) {
+  return launch_csr<unsigned long long>(L, R, pts, offs, ranges, n_blocks, mode, tau_v, out, max_points,
+                                        s);
 }
 
 }  // namespace rg

@@ -58,26 +58,43 @@ struct Pass {
   int has, dx, dy, sum, n, interior, cm_sum, cm_n, cp_sum, cp_n;
 };
 
+// a valid point of a pass: raster offset + left code (32-bit 5x5 or 64-bit 9x7)
+template <typename CT>
+struct VPoint;
+template <>
+struct __align__(8) VPoint<uint32_t> {
+  int off;
+  uint32_t code;
+};
+template <>
+struct __align__(16) VPoint<unsigned long long> {
+  int off;
+  int pad;
+  unsigned long long code;
+};
+__device__ __forceinline__ int popc(uint32_t x) { return __popc(x); }
+__device__ __forceinline__ int popc(unsigned long long x) { return __popcll(x); }
+
 // One sweep over K dx-chunks for one dy: vp[k] = {raster offset of point k,
 // its left code}; `base` = this lane's sample pointer for chunk c0 at offset 0.
-template <bool FAST, int K>
-__device__ __forceinline__ void sweep(const int2* __restrict__ vp, int nv, const uint32_t* base,
+template <typename CT, bool FAST, int K>
+__device__ __forceinline__ void sweep(const VPoint<CT>* __restrict__ vp, int nv, const CT* base,
                                       int lane, int c0, int ndx, int dx_min, int dy, Cand& best,
                                       int& evals) {
   int s[K], n[K];
 #pragma unroll
   for (int c = 0; c < K; ++c) s[c] = n[c] = 0;
   for (int k = 0; k < nv; ++k) {
-    const int2 q = vp[k];
-    const uint32_t* a = base + q.x;
-    const uint32_t l = (uint32_t)q.y;
+    const VPoint<CT> q = vp[k];
+    const CT* a = base + q.off;
+    const CT l = q.code;
 #pragma unroll
     for (int c = 0; c < K; ++c) {
-      const uint32_t r = __ldg(a - 32 * c);
+      const CT r = __ldg(a - 32 * c);
       if (FAST) {
-        s[c] += __popc(l ^ r);
+        s[c] += popc(l ^ r);
       } else if (r != 0u) {
-        s[c] += __popc(l ^ r);
+        s[c] += popc(l ^ r);
         ++n[c];
       }
     }
@@ -94,13 +111,13 @@ __device__ __forceinline__ void sweep(const int2* __restrict__ vp, int nv, const
   }
 }
 
-template <bool FAST>
-__device__ __forceinline__ void sweep_chunks(const int2* vp, int nv, const uint32_t* base, int lane,
+template <typename CT, bool FAST>
+__device__ __forceinline__ void sweep_chunks(const VPoint<CT>* vp, int nv, const CT* base, int lane,
                                              int c0, int k, int ndx, int dx_min, int dy, Cand& best,
                                              int& evals) {
 #define RG_SWEEP_CASE(K) \
   case K:                \
-    sweep<FAST, K>(vp, nv, base, lane, c0, ndx, dx_min, dy, best, evals); \
+    sweep<CT, FAST, K>(vp, nv, base, lane, c0, ndx, dx_min, dy, best, evals); \
     break;
   if (FAST) {
     switch (k) {
@@ -132,16 +149,17 @@ __device__ __forceinline__ void sweep_chunks(const int2* vp, int nv, const uint3
 // One block_match pass (census.hpp:178-272) by the calling warp.
 // pts: the block's points (smem), shifted by (sx, sy); L: raster of the left
 // codes, R: raster sampled at (x - dx, y + dy).  Both share geometry g.
-__device__ Pass warp_pass(const int2* pts, int np, int sx, int sy, const uint32_t* L,
-                          const uint32_t* R, const PadGeom& g, bool trusted,
-                          const rg_search_range& rg, int2* vp, int lane, int& evals) {
+template <typename CT>
+__device__ Pass warp_pass(const int2* pts, int np, int sx, int sy, const CT* L, const CT* R,
+                          const PadGeom& g, bool trusted, const rg_search_range& rg, VPoint<CT>* vp,
+                          int lane, int& evals) {
   Pass o = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   int nv = 0;
   int xmin = INT_MAX, xmax = INT_MIN, ymin = INT_MAX, ymax = INT_MIN;
   for (int b = 0; b < np; b += 32) {  // keep points with a defined left code (:195-201)
     const int k = b + lane;
     int x = 0, y = 0;
-    uint32_t code = 0;
+    CT code = 0;
     if (k < np) {
       const int2 p = pts[k];
       x = p.x + sx;
@@ -151,7 +169,10 @@ __device__ Pass warp_pass(const int2* pts, int np, int sx, int sy, const uint32_
     const bool ok = code != 0u;
     const unsigned bal = __ballot_sync(0xffffffffu, ok);
     if (ok) {
-      vp[nv + __popc(bal & ((1u << lane) - 1u))] = make_int2(y * g.pitch + x, (int)code);
+      VPoint<CT> q;
+      q.off = y * g.pitch + x;
+      q.code = code;
+      vp[nv + __popc(bal & ((1u << lane) - 1u))] = q;
       xmin = min(xmin, x);
       xmax = max(xmax, x);
       ymin = min(ymin, y);
@@ -175,12 +196,12 @@ __device__ Pass warp_pass(const int2* pts, int np, int sx, int sy, const uint32_
   const int cmax = fast ? CMAX : CMAX_SLOW;
   for (int dy = rg.dy_min; dy <= rg.dy_max; ++dy) {
     for (int c0 = 0; c0 < nch; c0 += cmax) {
-      const uint32_t* base = R + (int64_t)dy * g.pitch - rg.dx_min - lane - 32 * c0;
+      const CT* base = R + (int64_t)dy * g.pitch - rg.dx_min - lane - 32 * c0;
       const int k = min(cmax, nch - c0);
       if (fast)
-        sweep_chunks<true>(vp, nv, base, lane, c0, k, ndx, rg.dx_min, dy, best, evals);
+        sweep_chunks<CT, true>(vp, nv, base, lane, c0, k, ndx, rg.dx_min, dy, best, evals);
       else
-        sweep_chunks<false>(vp, nv, base, lane, c0, k, ndx, rg.dx_min, dy, best, evals);
+        sweep_chunks<CT, false>(vp, nv, base, lane, c0, k, ndx, rg.dx_min, dy, best, evals);
     }
   }
 #pragma unroll
@@ -203,15 +224,15 @@ __device__ Pass warp_pass(const int2* pts, int np, int sx, int sy, const uint32_
   if (o.interior) {  // costs at (dx - 1, dy) and (dx + 1, dy) for the parabola
     int ms = 0, mn = 0, ps = 0, pn = 0;
     for (int k = lane; k < nv; k += 32) {
-      const int2 q = vp[k];
-      const uint32_t* a = R + q.x + (int64_t)best.dy * g.pitch - best.dx;
-      const uint32_t rm = a[1], rp = a[-1];
+      const VPoint<CT> q = vp[k];
+      const CT* a = R + q.off + (int64_t)best.dy * g.pitch - best.dx;
+      const CT rm = a[1], rp = a[-1];
       if (rm) {
-        ms += __popc((uint32_t)q.y ^ rm);
+        ms += popc(q.code ^ rm);
         ++mn;
       }
       if (rp) {
-        ps += __popc((uint32_t)q.y ^ rp);
+        ps += popc(q.code ^ rp);
         ++pn;
       }
     }
@@ -241,15 +262,15 @@ __device__ __forceinline__ void finish(const Pass& p, rg_match_result& r) {  // 
   }
 }
 
-template <int WPB, int MINB>
+template <typename CT, int WPB, int MINB>
 __global__ void __launch_bounds__(WPB * 32, MINB) match_slots_warp_kernel(
     const Slot* __restrict__ slots, int32_t* __restrict__ counters, const ObjEntry* __restrict__ objs,
     const rg_detection* __restrict__ dets, const int32_t* __restrict__ det_off,
-    const uint32_t* __restrict__ fl, const uint32_t* __restrict__ fr, PadGeom gf,
-    const uint32_t* __restrict__ sl, const uint32_t* __restrict__ sr, PadGeom gs, int img_w,
+    const CT* __restrict__ fl, const CT* __restrict__ fr, PadGeom gf,
+    const CT* __restrict__ sl, const CT* __restrict__ sr, PadGeom gs, int img_w,
     int img_h, int trusted, rg_ranger_config cfg, rg_match_result* __restrict__ res,
     rg_ranger_stats* __restrict__ stats, int maxp, int capacity) {
-  extern __shared__ __align__(16) int2 wsm[];
+  extern __shared__ __align__(16) unsigned char wsm_raw[];
   __shared__ double occ[WPB][4 * kWarpOcc];
   __shared__ int nocc[WPB];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -257,8 +278,10 @@ __global__ void __launch_bounds__(WPB * 32, MINB) match_slots_warp_kernel(
   // an overflowed plan (counters[1], set by K3) is re-run with a bigger list:
   // skip it entirely; otherwise only planned slots inside the list exist
   if (counters[1] || slot >= min(counters[0], capacity)) return;  // warp-uniform
-  int2* pts = wsm + (size_t)warp * 2 * maxp;
-  int2* vp = pts + maxp;
+  // per warp: maxp sampled points + maxp valid points
+  unsigned char* wbase = wsm_raw + (size_t)warp * maxp * (sizeof(int2) + sizeof(VPoint<CT>));
+  int2* pts = reinterpret_cast<int2*>(wbase);
+  VPoint<CT>* vp = reinterpret_cast<VPoint<CT>*>(wbase + sizeof(int2) * maxp);
   const Slot s = slots[slot];
   const ObjEntry e = objs[s.obj];
   const rg_detection det = dets[e.det];
@@ -299,16 +322,16 @@ __global__ void __launch_bounds__(WPB * 32, MINB) match_slots_warp_kernel(
     const bool far = e.kind == RG_KIND_FAR;
     const PadGeom& g = far ? gf : gs;
     const int64_t fo = (int64_t)s.frame * g.fstride + g.origin;
-    const uint32_t* L = (far ? fl : sl) + fo;
-    const uint32_t* R = (far ? fr : sr) + fo;
+    const CT* L = (far ? fl : sl) + fo;
+    const CT* R = (far ? fr : sr) + fo;
     const int sc = cfg.close_scale;
     const rg_search_range rg = far ? rg_search_range{0, cfg.dx_max_far, -1, 1}
                                    : rg_search_range{0, (cfg.dx_max_close + sc - 1) / sc, -1, 1};
-    const Pass f = warp_pass(pts, np, 0, 0, L, R, g, trusted != 0, rg, vp, lane, evals);
+    const Pass f = warp_pass<CT>(pts, np, 0, 0, L, R, g, trusted != 0, rg, vp, lane, evals);
     if (f.has) {
       finish(f, r);
       const rg_search_range brg = {-rg.dx_max, -rg.dx_min, -f.dy, -f.dy};
-      const Pass b = warp_pass(pts, np, -f.dx, f.dy, R, L, g, trusted != 0, brg, vp, lane, evals);
+      const Pass b = warp_pass<CT>(pts, np, -f.dx, f.dy, R, L, g, trusted != 0, brg, vp, lane, evals);
       if (b.has) {
         rg_match_result rb;
         finish(b, rb);
@@ -325,32 +348,34 @@ __global__ void __launch_bounds__(WPB * 32, MINB) match_slots_warp_kernel(
   }
 }
 
-}  // namespace
-
-template <int WPB, int MINB>
-static cudaError_t launch_variant(const Slot* slots, int32_t* counters, int slot_capacity,
+template <typename CT, int WPB, int MINB>
+cudaError_t launch_variant(const Slot* slots, int32_t* counters, int slot_capacity,
                                   const ObjEntry* objs, const rg_detection* dets, const int32_t* det_off,
-                                  const uint32_t* fl, const uint32_t* fr, const PadGeom& gf,
-                                  const uint32_t* sl, const uint32_t* sr, const PadGeom& gs, int img_w,
-                                  int img_h, int trusted, rg_ranger_config cfg, rg_match_result* res,
-                                  rg_ranger_stats* stats, int max_points, cudaStream_t s) {
-  auto kern = match_slots_warp_kernel<WPB, MINB>;
-  const size_t smem = sizeof(int2) * 2 * (size_t)max_points * WPB;
+                                  const void* fl, const void* fr, const PadGeom& gf, const void* sl,
+                                  const void* sr, const PadGeom& gs, int img_w, int img_h, int trusted,
+                                  rg_ranger_config cfg, rg_match_result* res, rg_ranger_stats* stats,
+                                  int max_points, cudaStream_t s) {
+  auto kern = match_slots_warp_kernel<CT, WPB, MINB>;
+  const size_t smem = (sizeof(int2) + sizeof(VPoint<CT>)) * (size_t)max_points * WPB;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
   const int grid = (slot_capacity + WPB - 1) / WPB;
-  kern<<<grid, WPB * 32, smem, s>>>(slots, counters, objs, dets, det_off, fl, fr, gf, sl, sr, gs, img_w, img_h,
-                                    trusted, cfg, res, stats, max_points, slot_capacity);
+  kern<<<grid, WPB * 32, smem, s>>>(slots, counters, objs, dets, det_off, static_cast<const CT*>(fl),
+                                    static_cast<const CT*>(fr), gf, static_cast<const CT*>(sl),
+                                    static_cast<const CT*>(sr), gs, img_w, img_h, trusted, cfg, res, stats,
+                                    max_points, slot_capacity);
   return cudaGetLastError();
 }
 
+}  // namespace
+
 cudaError_t launch_match_slots(const Slot* slots, int32_t* counters, int slot_capacity,
                                const ObjEntry* objs, const rg_detection* dets, const int32_t* det_off,
-                               const uint32_t* fl, const uint32_t* fr, const PadGeom& gf,
-                               const uint32_t* sl, const uint32_t* sr, const PadGeom& gs, int img_w,
-                               int img_h, int trusted, rg_ranger_config cfg, rg_match_result* res,
+                               const void* fl, const void* fr, const PadGeom& gf, const void* sl,
+                               const void* sr, const PadGeom& gs, int img_w, int img_h, int trusted,
+                               int wide, rg_ranger_config cfg, rg_match_result* res,
                                rg_ranger_stats* stats, int max_points, cudaStream_t s) {
   if (slot_capacity <= 0) return cudaSuccess;
   static int variant = [] {
@@ -359,12 +384,13 @@ cudaError_t launch_match_slots(const Slot* slots, int32_t* counters, int slot_ca
   }();
 #define RG_ARGS slots, counters, slot_capacity, objs, dets, det_off, fl, fr, gf, sl, sr, gs, img_w, img_h, \
                 trusted, cfg, res, stats, max_points, s
+  if (wide) return launch_variant<unsigned long long, 8, 2>(RG_ARGS);  // 9x7 extension
   switch (variant) {  // A/B knobs; default measured best (tools/variants.sh)
-    case 1: return launch_variant<4, 8>(RG_ARGS);
-    case 2: return launch_variant<16, 2>(RG_ARGS);
-    case 3: return launch_variant<8, 5>(RG_ARGS);
-    case 4: return launch_variant<4, 1>(RG_ARGS);
-    default: return launch_variant<8, 4>(RG_ARGS);
+    case 1: return launch_variant<uint32_t, 4, 8>(RG_ARGS);
+    case 2: return launch_variant<uint32_t, 16, 2>(RG_ARGS);
+    case 3: return launch_variant<uint32_t, 8, 5>(RG_ARGS);
+    case 4: return launch_variant<uint32_t, 4, 1>(RG_ARGS);
+    default: return launch_variant<uint32_t, 8, 4>(RG_ARGS);
   }
 #undef RG_ARGS
 }

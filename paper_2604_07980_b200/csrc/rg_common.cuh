@@ -22,11 +22,14 @@ constexpr int kMaxOccluders = 128;     // per-object occluder boxes kept in smem
 constexpr int kAggCapacity = 4096;     // CLOSE blocks aggregated in smem
 
 // ------------------------------------------------------------ device structs
-struct Raster {  // census raster in device memory
-  const uint32_t* p;
+template <typename CT>
+struct RasterT {  // census raster in device memory
+  const CT* p;
   int w, h;
   int pitch;  // elements
 };
+using Raster = RasterT<uint32_t>;              // 5x5 codes
+using Raster64 = RasterT<unsigned long long>;  // 9x7 codes (extension)
 
 // Layout of a census raster in device memory: `w x h` codes at `origin`
 // inside a zero margin of padx columns / pady rows, rows `pitch` apart, frames
@@ -83,6 +86,7 @@ struct rg_ctx {
   cudaStream_t copy_stream = nullptr;  // H2D staging of the host-fed batch API
   int map_key[4] = {-1, -1, -1, -1};  // geometry of the cached inverse maps
   rg::PadGeom pad_key{}, pad_key_s{};  // layout of the zeroed census rasters
+  int pad_wide = 0;                    // ... and their code width (1 = 64-bit)
   std::string err;
   bool profiling = false;
   double stage_ms[5] = {0, 0, 0, 0, 0};
@@ -130,6 +134,11 @@ cudaError_t launch_census_frames(const uint8_t* left, const uint8_t* right, int 
                                  uint32_t* fl, uint32_t* fr, const PadGeom& gf, uint32_t* sl,
                                  uint32_t* sr, const PadGeom& gs, const int32_t* inv_x,
                                  const int32_t* inv_y, cudaStream_t s);
+cudaError_t launch_census64_frames(const uint8_t* left, const uint8_t* right, int n_frames, int64_t frame_stride,
+                                   int pitch, int w, int h, unsigned long long* fl, unsigned long long* fr,
+                                   const PadGeom& gf, unsigned long long* sl, unsigned long long* sr,
+                                   const PadGeom& gs, const int32_t* inv_x, const int32_t* inv_y,
+                                   cudaStream_t s);
 cudaError_t launch_roi_mask(uint32_t* codes, int w, int h, const rg_rect* rois, int n_rois,
                             cudaStream_t s);
 
@@ -138,11 +147,15 @@ cudaError_t launch_match_blocks(Raster L, Raster R, const int32_t* pts, const in
                                 const rg_search_range* ranges, int n_blocks, int mode,
                                 double tau_v, rg_match_result* out, int max_points,
                                 cudaStream_t s);
+cudaError_t launch_match_blocks64(Raster64 L, Raster64 R, const int32_t* pts, const int64_t* offs,
+                                  const rg_search_range* ranges, int n_blocks, int mode,
+                                  double tau_v, rg_match_result* out, int max_points,
+                                  cudaStream_t s);
 cudaError_t launch_match_slots(const Slot* slots, int32_t* counters, int slot_capacity,
                                const ObjEntry* objs, const rg_detection* dets,
-                               const int32_t* det_off, const uint32_t* fl, const uint32_t* fr,
-                               const PadGeom& gf, const uint32_t* sl, const uint32_t* sr,
-                               const PadGeom& gs, int img_w, int img_h, int trusted,
+                               const int32_t* det_off, const void* fl, const void* fr,
+                               const PadGeom& gf, const void* sl, const void* sr,
+                               const PadGeom& gs, int img_w, int img_h, int trusted, int wide,
                                rg_ranger_config cfg, rg_match_result* res,
                                rg_ranger_stats* stats, int max_points, cudaStream_t s);
 

@@ -172,6 +172,21 @@ def census_transform(img, out_w: Optional[int] = None, out_h: Optional[int] = No
     return CensusImage(ow, oh, codes, ow / w, oh / h)
 
 
+def census_transform64(img, out_w: Optional[int] = None, out_h: Optional[int] = None,
+                       ctx: Optional[Context] = None) -> CensusImage:
+    """9x7 extension: 64-bit codes, window rows -3..3 x cols -4..4,
+    row-major compare order, sentinel bit 63; same nearest-downscale mapping as
+    census_transform.  No reference counterpart (parity unpinned)."""
+    ctx = ctx or default_context()
+    a = _gray(img)
+    h, w = a.shape
+    ow = w if out_w is None else int(out_w)
+    oh = h if out_h is None else int(out_h)
+    codes = np.zeros((max(oh, 0), max(ow, 0)), np.uint64)
+    ctx.check(lib().rg_census_transform64(ctx.handle, _ptr(a), w, h, ow, oh, _ptr(codes)))
+    return CensusImage(ow, oh, codes, ow / w, oh / h)
+
+
 @dataclass
 class CensusRoi:
     x0: int = 0
@@ -247,10 +262,13 @@ def _match(blocks, left: CensusImage, right: CensusImage, mode: int, tau_v: floa
     if not blocks:
         return []
     pts, offs, rg = _blocks_csr(blocks)
-    L = np.ascontiguousarray(left.codes, np.uint32)
-    R = np.ascontiguousarray(right.codes, np.uint32)
+    wide = left.codes.dtype == np.uint64  # 9x7 extension rasters
+    ct = np.uint64 if wide else np.uint32
+    L = np.ascontiguousarray(left.codes, ct)
+    R = np.ascontiguousarray(right.codes, ct)
     out = (_abi.MatchResult * len(blocks))()
-    ctx.check(lib().rg_match_blocks(ctx.handle, _ptr(L), left.width, left.height, _ptr(R), right.width,
+    fn = lib().rg_match_blocks64 if wide else lib().rg_match_blocks
+    ctx.check(fn(ctx.handle, _ptr(L), left.width, left.height, _ptr(R), right.width,
                                     right.height, _ptr(pts), _ptr(offs), rg, len(blocks), mode,
                                     float(tau_v), out))
     res = []
@@ -324,13 +342,14 @@ class RangerConfig:
     frontal_crop: FrontalCrop = field(default_factory=FrontalCrop)
     dx_max_far: int = 64
     dx_max_close: int = 192
+    census_9x7: bool = False  # extension: 64-bit 9x7 descriptors; no cache
 
     def to_c(self) -> _abi.RangerConfig:
         c = self.frontal_crop
         return _abi.RangerConfig(float(self.tau_s), self.close_scale, self.grid_side_points,
                                  self.max_total_points, self.close_block_side_points, float(self.tau_d),
                                  self.n_min, self.max_objects, float(self.tau_v), c.x0, c.y0, c.x1, c.y1,
-                                 self.dx_max_far, self.dx_max_close)
+                                 self.dx_max_far, self.dx_max_close, int(bool(self.census_9x7)), 0)
 
 
 @dataclass

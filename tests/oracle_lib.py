@@ -52,6 +52,12 @@ class Checker:
             self.lib.ref_bench_estimate.restype = D
             self.lib.ref_bench_estimate.argtypes = [P, P, I, I, I, P, P, P, I, P, I, P]
 
+        if prefix == "orc_":  # 9x7 extension (restatement only)
+            self.lib.orc_census_transform64.restype = I
+            self.lib.orc_census_transform64.argtypes = [P, I, I, I, I, P]
+            self.lib.orc_match_blocks64.restype = I
+            self.lib.orc_match_blocks64.argtypes = [P, I, I, P, I, I, P, P, P, I, I, D, P]
+
     def fn(self, name):
         return getattr(self.lib, self.prefix + name)
 
@@ -62,6 +68,15 @@ class Checker:
         oh = h if oh is None else oh
         out = np.zeros((oh, ow), np.uint32)
         st = self.fn("census_transform")(img.ctypes.data, w, h, ow, oh, out.ctypes.data)
+        assert st == 0, st
+        return out
+
+    def census64(self, img: np.ndarray, ow=None, oh=None) -> np.ndarray:
+        h, w = img.shape
+        ow = w if ow is None else ow
+        oh = h if oh is None else oh
+        out = np.zeros((oh, ow), np.uint64)
+        st = self.lib.orc_census_transform64(img.ctypes.data, w, h, ow, oh, out.ctypes.data)
         assert st == 0, st
         return out
 
@@ -84,9 +99,11 @@ class Checker:
         pa = np.ascontiguousarray(np.asarray(pts, np.int32).reshape(-1, 2))
         rg = (_abi.SearchRange * max(len(blocks), 1))(*[_abi.SearchRange(*r) for _, r in blocks])
         out = (_abi.MatchResult * max(len(blocks), 1))()
-        L = np.ascontiguousarray(L, np.uint32)
-        R = np.ascontiguousarray(R, np.uint32)
-        st = self.fn("match_blocks")(L.ctypes.data, L.shape[1], L.shape[0], R.ctypes.data, R.shape[1],
+        wide = np.asarray(L).dtype == np.uint64
+        L = np.ascontiguousarray(L, np.uint64 if wide else np.uint32)
+        R = np.ascontiguousarray(R, np.uint64 if wide else np.uint32)
+        fn = self.lib.orc_match_blocks64 if wide else self.fn("match_blocks")
+        st = fn(L.ctypes.data, L.shape[1], L.shape[0], R.ctypes.data, R.shape[1],
                                      R.shape[0], pa.ctypes.data, offs.ctypes.data, C.addressof(rg),
                                      len(blocks), mode, tau_v, C.addressof(out))
         return st, list(out)[:len(blocks)]
