@@ -106,16 +106,16 @@ __device__ __forceinline__ uint32_t c2_vpair(uint32_t a, uint32_t b, int j) {
 }
 
 // The three fp16 accumulators are built so each group's compare bits sit in
-// the low bits of the half's mantissa (value 1024 + B, exponent fixed):
-// g0 = w0..w7 (init 4.0, 8 steps), g1 = w8..w16 (init 2.0, 9 bits incl. the
-// centre 0), g2 = w17..w24 (init 4.0).  code = 1<<25 | B0<<17 | B1<<8 | B2,
-// assembled with byte permutes for both lanes (lo = row y, hi = row y+1).
+// the low mantissa bits of the half (exponent fixed, value in [1024, 2048)):
+// g0 = w0..w8 (init 3.0, 9 steps: mantissa = 1<<9 | B0, the sentinel rides in
+// mantissa bit 9), g1 = w9..w16 (init 4.0, 8 bits incl. the centre 0),
+// g2 = w17..w24 (init 4.0).  code = (1<<9 | B0) << 16 | B1 << 8 | B2 is then
+// three byte permutes and a mask for both lanes (lo = row y, hi = row y+1).
 __device__ __forceinline__ void c2_assemble(uint32_t g0, uint32_t g1, uint32_t g2, uint32_t& lo,
                                             uint32_t& hi) {
-  const uint32_t xl = __byte_perm(g2, g1, 0x0540);  // [B2, B1 lo8, 0x64|B1b8, 0]
-  const uint32_t xh = __byte_perm(g2, g1, 0x0762);  // same from the high halves
-  lo = (((xl & 0x1FFFFu) | ((g0 << 17) & 0x1FE0000u)) & 0x1FFFFFFu) | 0x2000000u;
-  hi = (((xh & 0x1FFFFu) | ((g0 << 1) & 0x1FE0000u)) & 0x1FFFFFFu) | 0x2000000u;
+  const uint32_t t = __byte_perm(g2, g1, 0x6240);      // [B2 lo, B1 lo, B2 hi, B1 hi]
+  lo = __byte_perm(t, g0, 0x5410) & 0x03FFFFFFu;       // g0 lo half: 0x66|b8 -> 0x2|b8
+  hi = __byte_perm(t, g0, 0x7632) & 0x03FFFFFFu;
 }
 
 // Descriptors of 4 pixel pairs from the 5 V rows w[0..4] (y-2 .. y+2).
@@ -125,15 +125,15 @@ __device__ __forceinline__ void c2_codes(const uint32_t (&w)[5][8], uint32_t lo[
   for (int q = 0; q < 4; ++q) {
     const __half2 c = *reinterpret_cast<const __half2*>(&w[2][q + 2]);
     __half2 g[3];
-    g[0] = g[2] = __float2half2_rn(4.0f);
-    g[1] = __float2half2_rn(2.0f);
+    g[0] = __float2half2_rn(3.0f);
+    g[1] = g[2] = __float2half2_rn(4.0f);
 #pragma unroll
     for (int wi = 0; wi < 25; ++wi) {
       if (wi == 12) continue;  // centre: its 0 bit is folded into w13's x4
       const int j = wi / 5, i = wi % 5;
       const __half2 v = *reinterpret_cast<const __half2*>(&w[j][q + i]);
       const __half2 m = (wi % 6 == 0) ? __hsub2_sat(v, c) : __hgt2(v, c);
-      const int gi = wi < 8 ? 0 : (wi < 17 ? 1 : 2);
+      const int gi = wi < 9 ? 0 : (wi < 17 ? 1 : 2);
       g[gi] = __hfma2(g[gi], wi == 13 ? four : two, m);
     }
     c2_assemble(*reinterpret_cast<uint32_t*>(&g[0]), *reinterpret_cast<uint32_t*>(&g[1]),
@@ -151,8 +151,12 @@ __device__ __forceinline__ void c2_strip(const uint32_t* __restrict__ V, uint32_
   const int xl = x0 + 4 * lane;  // first column of this lane
   const int pr0 = wid * C2_PR;
   const uint32_t* vbase = V + C2_VOFF + 4 * lane;  // V index of column xl - 2
+  // output pointers advance by whole pair rows (no per-row 64-bit index math)
+  uint32_t* o = full + (int64_t)(y0 + 2 * pr0) * gf.pitch + xl;
+  uint32_t* ro = red ? red + (int64_t)((y0 >> 1) + pr0) * gs.pitch + (xl >> 1) : full;  // full: never written
+  const int64_t ostep = 2 * (int64_t)gf.pitch;
 #pragma unroll
-  for (int p = pr0; p < pr0 + C2_PR; ++p) {
+  for (int p = pr0; p < pr0 + C2_PR; ++p, o += ostep, ro += gs.pitch) {
     const int y = y0 + 2 * p;
     if (EDGE && y >= h) break;
     uint32_t win[5][8];
@@ -174,13 +178,10 @@ __device__ __forceinline__ void c2_strip(const uint32_t* __restrict__ V, uint32_
         if (!(xin && y + 1 >= 2 && y + 1 <= h - 3)) hi[q] = 0u;
       }
     }
-    uint32_t* o = full + (int64_t)y * gf.pitch + xl;
     *reinterpret_cast<uint4*>(o) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
     if (!EDGE || y + 1 < h) *reinterpret_cast<uint4*>(o + gf.pitch) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-    if (red) {  // reduced raster = codes at even (x, y): (x/2, y/2)
-      uint32_t* ro = red + (int64_t)(y >> 1) * gs.pitch + (xl >> 1);
-      *reinterpret_cast<uint2*>(ro) = make_uint2(lo[0], lo[2]);
-    }
+    // reduced raster = codes at even (x, y): (x/2, y/2)
+    if (red) *reinterpret_cast<uint2*>(ro) = make_uint2(lo[0], lo[2]);
   }
 }
 
