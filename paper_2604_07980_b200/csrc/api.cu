@@ -160,7 +160,7 @@ rg_status census_one(rg_ctx* ctx, const uint8_t* d_img, int w, int h, int ow, in
   int32_t *ix = nullptr, *iy = nullptr;
   TRY(upload_inverse_maps(ctx, w, h, ow, oh, ctx->stream, &ix, &iy));
   RG_CUDA(ctx, launch_census_frames(d_img, nullptr, 1, 0, w, w, h, d_full, nullptr, make_geom(w, h, 0, 0),
-                                    d_red, nullptr, make_geom(ow, oh, 0, 0), ix, iy, ctx->stream));
+                                    d_red, nullptr, make_geom(ow, oh, 0, 0), ix, iy, false, ctx->stream));
   count_launch(ctx, ST_CENSUS);
   return RG_OK;
 }
@@ -315,7 +315,7 @@ rg_status enqueue_pipeline(rg_ctx* ctx, const FrameJob& J, const rg_ranger_confi
     count_launch(ctx, ST_CENSUS);
   } else if (!(J.full_l && J.scaled_l)) {
     RG_CUDA(ctx, launch_census_frames(J.left, J.right, F, J.frame_stride, J.pitch, w, h, fl, fr, gf, sl,
-                                      sr, gs, ix, iy, s));
+                                      sr, gs, ix, iy, true, s));
     count_launch(ctx, ST_CENSUS);
   }
   // caller-supplied codes (a pre-filled CensusCache) into the padded layout

@@ -37,7 +37,7 @@ __global__ void __launch_bounds__(TPB) census_frames_kernel(
     const uint8_t* __restrict__ left, const uint8_t* __restrict__ right, int64_t frame_stride,
     int pitch, int w, int h, uint32_t* __restrict__ fl, uint32_t* __restrict__ fr, PadGeom gf,
     uint32_t* __restrict__ sl, uint32_t* __restrict__ sr, PadGeom gs,
-    const int32_t* __restrict__ inv_x, const int32_t* __restrict__ inv_y) {
+    const int32_t* __restrict__ inv_x, const int32_t* __restrict__ inv_y, bool s31) {
   __shared__ __align__(16) uint8_t tile[TY + 4][TX + 8];
   const int sides = right ? 2 : 1;
   const int frame = blockIdx.z / sides, side = blockIdx.z - frame * sides;
@@ -64,6 +64,7 @@ __global__ void __launch_bounds__(TPB) census_frames_kernel(
     if (x >= w || y >= h) continue;
     uint32_t code = 0;
     if (x >= 2 && y >= 2 && x < w - 2 && y < h - 2) code = census_window(&tile[ty + 2][tx + 2], TX + 8);
+    if (s31 && code) code = (code & 0x01FFFFFFu) | 0x80000000u;  // internal layout
     full[(int64_t)y * gf.pitch + x] = code;
     if (red && ix >= 0) {
       const int iy = inv_y[y];
@@ -88,8 +89,14 @@ __global__ void __launch_bounds__(TPB) census_frames_kernel(
 // thread in flight at once); each warp then computes a 16-row strip reading
 // its 5-row window straight from V (2 LDS.128 per row).
 constexpr int C2_TX = 128;                        // tile columns: 32 lanes x 4 pixel pairs
-constexpr int C2_WARPS = 8;
-constexpr int C2_PR = 4;                          // pair rows per warp strip
+#ifndef RG_C2_WARPS
+#define RG_C2_WARPS 8
+#endif
+#ifndef RG_C2_PR
+#define RG_C2_PR 4
+#endif
+constexpr int C2_WARPS = RG_C2_WARPS;
+constexpr int C2_PR = RG_C2_PR;                          // pair rows per warp strip
 constexpr int C2_TY = C2_WARPS * C2_PR * 2;       // 64 tile rows
 constexpr int C2_VW = C2_TX + 12;                 // V row stride: 4 pad + x0-2 .. x0+TX+1 + pad
 constexpr int C2_VOFF = 4;                        // V index of column x0-2
@@ -111,21 +118,28 @@ __device__ __forceinline__ uint32_t c2_vpair(uint32_t a, uint32_t b, int j) {
 // mantissa bit 9), g1 = w9..w16 (init 4.0, 8 bits incl. the centre 0),
 // g2 = w17..w24 (init 4.0).  code = (1<<9 | B0) << 16 | B1 << 8 | B2 is then
 // three byte permutes and a mask for both lanes (lo = row y, hi = row y+1).
+template <bool S31>  // S31: internal layout, sentinel moved from bit 25 to bit 31
 __device__ __forceinline__ void c2_assemble(uint32_t g0, uint32_t g1, uint32_t g2, uint32_t& lo,
                                             uint32_t& hi) {
   const uint32_t t = __byte_perm(g2, g1, 0x6240);      // [B2 lo, B1 lo, B2 hi, B1 hi]
-  lo = __byte_perm(t, g0, 0x5410) & 0x03FFFFFFu;       // g0 lo half: 0x66|b8 -> 0x2|b8
-  hi = __byte_perm(t, g0, 0x7632) & 0x03FFFFFFu;
+  if (S31) {  // g0 negative: its high byte is 0xE6|b8 -> 0x80|b8
+    lo = __byte_perm(t, g0, 0x5410) & 0x81FFFFFFu;
+    hi = __byte_perm(t, g0, 0x7632) & 0x81FFFFFFu;
+  } else {
+    lo = __byte_perm(t, g0, 0x5410) & 0x03FFFFFFu;     // g0 lo half: 0x66|b8 -> 0x2|b8
+    hi = __byte_perm(t, g0, 0x7632) & 0x03FFFFFFu;
+  }
 }
 
 // Descriptors of 4 pixel pairs from the 5 V rows w[0..4] (y-2 .. y+2).
+template <bool S31>
 __device__ __forceinline__ void c2_codes(const uint32_t (&w)[5][8], uint32_t lo[4], uint32_t hi[4]) {
   const __half2 two = __float2half2_rn(2.0f), four = __float2half2_rn(4.0f);
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     const __half2 c = *reinterpret_cast<const __half2*>(&w[2][q + 2]);
     __half2 g[3];
-    g[0] = __float2half2_rn(3.0f);
+    g[0] = __float2half2_rn(S31 ? -3.0f : 3.0f);  // S31: negative, so the fp16 sign lands on bit 31
     g[1] = g[2] = __float2half2_rn(4.0f);
 #pragma unroll
     for (int wi = 0; wi < 25; ++wi) {
@@ -134,16 +148,16 @@ __device__ __forceinline__ void c2_codes(const uint32_t (&w)[5][8], uint32_t lo[
       const __half2 v = *reinterpret_cast<const __half2*>(&w[j][q + i]);
       const __half2 m = (wi % 6 == 0) ? __hsub2_sat(v, c) : __hgt2(v, c);
       const int gi = wi < 9 ? 0 : (wi < 17 ? 1 : 2);
-      g[gi] = __hfma2(g[gi], wi == 13 ? four : two, m);
+      g[gi] = __hfma2(g[gi], wi == 13 ? four : two, (S31 && gi == 0) ? __hneg2(m) : m);
     }
-    c2_assemble(*reinterpret_cast<uint32_t*>(&g[0]), *reinterpret_cast<uint32_t*>(&g[1]),
+    c2_assemble<S31>(*reinterpret_cast<uint32_t*>(&g[0]), *reinterpret_cast<uint32_t*>(&g[1]),
                 *reinterpret_cast<uint32_t*>(&g[2]), lo[q], hi[q]);
   }
 }
 
 // Phase 2 for one warp: its C2_PR pair rows of the tile whose V is in smem.
 // EDGE: the strip touches the image border (codes 0 where the window leaves).
-template <bool EDGE>
+template <bool EDGE, bool S31>
 __device__ __forceinline__ void c2_strip(const uint32_t* __restrict__ V, uint32_t* __restrict__ full,
                                          uint32_t* __restrict__ red, const PadGeom& gf, const PadGeom& gs,
                                          int x0, int y0, int w, int h) {
@@ -168,7 +182,7 @@ __device__ __forceinline__ void c2_strip(const uint32_t* __restrict__ V, uint32_
       win[j][4] = b.x; win[j][5] = b.y; win[j][6] = b.z; win[j][7] = b.w;
     }
     uint32_t lo[4], hi[4];
-    c2_codes(win, lo, hi);
+    c2_codes<S31>(win, lo, hi);
     if (EDGE) {
       if (xl >= w) continue;
 #pragma unroll
@@ -185,6 +199,7 @@ __device__ __forceinline__ void c2_strip(const uint32_t* __restrict__ V, uint32_
   }
 }
 
+template <bool S31>
 __global__ void __launch_bounds__(C2_WARPS * 32) census_pairs_kernel(
     const uint8_t* __restrict__ left, const uint8_t* __restrict__ right, int64_t frame_stride,
     int pitch, int w, int h, uint32_t* __restrict__ fl, uint32_t* __restrict__ fr, PadGeom gf,
@@ -232,9 +247,9 @@ __global__ void __launch_bounds__(C2_WARPS * 32) census_pairs_kernel(
   if (ys >= h) return;
   const bool edge = x0 < 2 || x0 + C2_TX + 3 > w - 3 || ys < 2 || ys + 2 * C2_PR + 1 > h - 3;
   if (__any_sync(0xffffffffu, edge || lane_x >= w))
-    c2_strip<true>(V, full, red, gf, gs, x0, y0, w, h);
+    c2_strip<true, S31>(V, full, red, gf, gs, x0, y0, w, h);
   else
-    c2_strip<false>(V, full, red, gf, gs, x0, y0, w, h);
+    c2_strip<false, S31>(V, full, red, gf, gs, x0, y0, w, h);
 }
 
 // ---------------------------------------------------------------------------
@@ -290,7 +305,8 @@ __global__ void __launch_bounds__(X_TPB) census64_kernel(
 }
 
 // census_transform_rois mask (census.hpp:111-136): keep codes inside the
-// union of the clipped rectangles, zero elsewhere.
+// union of the clipped rectangles, zero elsewhere.  Kept codes leave in the
+// reference layout (sentinel bit 25) whichever layout they were computed in.
 __global__ void roi_mask_kernel(uint32_t* __restrict__ codes, int w, int h,
                                 const rg_rect* __restrict__ rois, int n_rois) {
   const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y;
@@ -300,7 +316,11 @@ __global__ void roi_mask_kernel(uint32_t* __restrict__ codes, int w, int h,
     const rg_rect q = rois[r];
     in = x >= max(0, q.x0) && x < min(w, q.x1) && y >= max(0, q.y0) && y < min(h, q.y1);
   }
-  if (!in) codes[(int64_t)y * w + x] = 0u;
+  uint32_t& c = codes[(int64_t)y * w + x];
+  if (!in)
+    c = 0u;
+  else if (c)
+    c = (c & 0x01FFFFFFu) | 0x02000000u;
 }
 
 }  // namespace
@@ -310,7 +330,7 @@ cudaError_t launch_census_frames(const uint8_t* left, const uint8_t* right, int 
                                  int64_t frame_stride, int pitch, int w, int h, uint32_t* fl,
                                  uint32_t* fr, const PadGeom& gf, uint32_t* sl, uint32_t* sr,
                                  const PadGeom& gs, const int32_t* inv_x, const int32_t* inv_y,
-                                 cudaStream_t s) {
+                                 bool internal, cudaStream_t s) {
   if (n_frames <= 0) return cudaSuccess;
   const int sides = right ? 2 : 1;
   const bool aligned = (pitch % 4 == 0) && (w % 4 == 0) && (frame_stride % 4 == 0) &&
@@ -319,21 +339,20 @@ cudaError_t launch_census_frames(const uint8_t* left, const uint8_t* right, int 
                        gf.origin % 4 == 0 && w >= 8 && h >= 8;
   const bool half = !sl || (gs.w * 2 == w && gs.h * 2 == h && gs.pitch % 2 == 0 && gs.origin % 2 == 0);
   if (aligned && half) {
-    static bool attr = false;
-    if (!attr) {
-      cudaError_t e = cudaFuncSetAttribute(census_pairs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)C2_SMEM);
+    auto kern = internal ? census_pairs_kernel<true> : census_pairs_kernel<false>;
+    static bool attr[2] = {false, false};
+    if (!attr[internal]) {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C2_SMEM);
       if (e != cudaSuccess) return e;
-      attr = true;
+      attr[internal] = true;
     }
     dim3 grid((w + C2_TX - 1) / C2_TX, (h + C2_TY - 1) / C2_TY, sides * n_frames);
-    census_pairs_kernel<<<grid, C2_WARPS * 32, C2_SMEM, s>>>(left, right, frame_stride, pitch, w, h, fl, fr,
-                                                             gf, sl, sr, gs);
+    kern<<<grid, C2_WARPS * 32, C2_SMEM, s>>>(left, right, frame_stride, pitch, w, h, fl, fr, gf, sl, sr, gs);
     return cudaGetLastError();
   }
   dim3 grid((w + TX - 1) / TX, (h + TY - 1) / TY, sides * n_frames);
   census_frames_kernel<<<grid, TPB, 0, s>>>(left, right, frame_stride, pitch, w, h, fl, fr, gf, sl,
-                                            sr, gs, inv_x, inv_y);
+                                            sr, gs, inv_x, inv_y, internal);
   return cudaGetLastError();
 }
 

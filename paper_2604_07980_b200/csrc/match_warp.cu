@@ -29,9 +29,18 @@
 namespace rg {
 namespace {
 
-constexpr int kWarpOcc = 32; // occluder boxes per warp kept in smem
-constexpr int CMAX = 9;      // 32-wide dx chunks per sweep (branch-free path)
-constexpr int CMAX_SLOW = 4; // chunks per sweep on the checked path
+#ifndef RG_MW_CMAX
+#define RG_MW_CMAX 4
+#endif
+#ifndef RG_MW_TAIL
+#define RG_MW_TAIL 4
+#endif
+#ifndef RG_MW_NOINLINE
+#define RG_MW_NOINLINE 0
+#endif
+constexpr int kWarpOcc = 32;      // occluder boxes per warp kept in smem
+constexpr int CMAX = RG_MW_CMAX;  // 32-wide dx chunks per sweep (balanced groups)
+constexpr int TAIL = RG_MW_TAIL;  // a last chunk with <= TAIL candidates goes point-parallel
 
 struct Cand {
   int sum, n, dx, dy;  // n == 0: infinite cost
@@ -58,41 +67,69 @@ struct Pass {
   int has, dx, dy, sum, n, interior, cm_sum, cm_n, cp_sum, cp_n;
 };
 
-// a valid point of a pass: raster offset + left code (32-bit 5x5 or 64-bit 9x7)
+// a valid point of a pass: BYTE offset into the raster + left code (32-bit
+// 5x5 or 64-bit 9x7).  Byte offsets keep the per-point address a single
+// 64-bit add.
 template <typename CT>
 struct VPoint;
 template <>
 struct __align__(8) VPoint<uint32_t> {
-  int off;
+  uint32_t off;
   uint32_t code;
 };
 template <>
 struct __align__(16) VPoint<unsigned long long> {
-  int off;
-  int pad;
+  uint32_t off;
+  uint32_t pad;
   unsigned long long code;
 };
 __device__ __forceinline__ int popc(uint32_t x) { return __popc(x); }
 __device__ __forceinline__ int popc(unsigned long long x) { return __popcll(x); }
+// all ones for a defined code of the internal layout (sentinel = top bit), 0 for undefined
+__device__ __forceinline__ uint32_t defined_mask(uint32_t r) { return (uint32_t)((int32_t)r >> 31); }
+__device__ __forceinline__ unsigned long long defined_mask(unsigned long long r) {
+  return (unsigned long long)((long long)r >> 63);
+}
+template <typename CT>
+__device__ __forceinline__ CT ld_at(const CT* base, uint32_t byte_off) {
+  return __ldg(reinterpret_cast<const CT*>(reinterpret_cast<const char*>(base) + byte_off));
+}
 
-// One sweep over K dx-chunks for one dy: vp[k] = {raster offset of point k,
-// its left code}; `base` = this lane's sample pointer for chunk c0 at offset 0.
-template <typename CT, bool FAST, int K>
+// Sweep modes.  FAST: every sample is a defined code (n = #points).  SIGN:
+// samples may be undefined, rasters in the internal layout (sentinel in the
+// top bit): mask by the sign.  GENERIC: caller-supplied codes, test r != 0.
+enum { M_FAST = 0, M_SIGN = 1, M_GENERIC = 2 };
+
+// FAST-mode argmin key: all candidates of a FAST pass share n, so the
+// reference order (sum/n, |dx|, dy, dx) (census.hpp:225-252) is the order of
+// (sum, |dx|, dy, dx >= 0) packed into 64 bits (|dx| < 2^15, |dy| < 2^15).
+__device__ __forceinline__ unsigned long long fast_key(int sum, int dx, int dy) {
+  const uint32_t lo = ((uint32_t)abs(dx) << 17) | ((uint32_t)(dy + 0x8000) << 1) | (dx >= 0 ? 1u : 0u);
+  return ((unsigned long long)(uint32_t)sum << 32) | lo;
+}
+
+// One sweep over K dx-chunks for one dy: `base` = this lane's sample pointer
+// for chunk c0 at offset 0; chunk c reads 32*c codes to the left.
+template <typename CT, int MODE, int K>
 __device__ __forceinline__ void sweep(const VPoint<CT>* __restrict__ vp, int nv, const CT* base,
                                       int lane, int c0, int ndx, int dx_min, int dy, Cand& best,
-                                      int& evals) {
+                                      unsigned long long& bkey, int& evals) {
   int s[K], n[K];
 #pragma unroll
   for (int c = 0; c < K; ++c) s[c] = n[c] = 0;
   for (int k = 0; k < nv; ++k) {
     const VPoint<CT> q = vp[k];
-    const CT* a = base + q.off;
+    const CT* a = reinterpret_cast<const CT*>(reinterpret_cast<const char*>(base) + q.off);
     const CT l = q.code;
 #pragma unroll
     for (int c = 0; c < K; ++c) {
       const CT r = __ldg(a - 32 * c);
-      if (FAST) {
+      if (MODE == M_FAST) {
         s[c] += popc(l ^ r);
+      } else if (MODE == M_SIGN) {
+        const CT m = defined_mask(r);
+        s[c] += popc((l ^ r) & m);
+        n[c] -= (int)m;
       } else if (r != 0u) {
         s[c] += popc(l ^ r);
         ++n[c];
@@ -102,55 +139,121 @@ __device__ __forceinline__ void sweep(const VPoint<CT>* __restrict__ vp, int nv,
 #pragma unroll
   for (int c = 0; c < K; ++c) {
     const int ix = lane + 32 * (c0 + c);
-    const int nn = FAST ? nv : n[c];
-    if (ix < ndx && nn > 0) {
-      evals += nn;  // Hamming evaluations, census.hpp:209-221
-      const Cand cd = {s[c], nn, dx_min + ix, dy};
+    if (MODE == M_FAST) {
+      if (ix < ndx) {
+        evals += nv;  // Hamming evaluations, census.hpp:209-221
+        const unsigned long long key = fast_key(s[c], dx_min + ix, dy);
+        bkey = key < bkey ? key : bkey;
+      }
+    } else if (ix < ndx && n[c] > 0) {
+      evals += n[c];
+      const Cand cd = {s[c], n[c], dx_min + ix, dy};
       if (better(cd, best)) best = cd;
     }
   }
 }
 
-template <typename CT, bool FAST>
+template <typename CT, int MODE>
 __device__ __forceinline__ void sweep_chunks(const VPoint<CT>* vp, int nv, const CT* base, int lane,
                                              int c0, int k, int ndx, int dx_min, int dy, Cand& best,
-                                             int& evals) {
-#define RG_SWEEP_CASE(K) \
-  case K:                \
-    sweep<CT, FAST, K>(vp, nv, base, lane, c0, ndx, dx_min, dy, best, evals); \
+                                             unsigned long long& bkey, int& evals) {
+  static_assert(CMAX >= 1 && CMAX <= 9, "chunk cap");
+#define RG_SWEEP_CASE(K)                                                                                 \
+  case K:                                                                                                \
+    if (K <= CMAX)                                                                                       \
+      sweep<CT, MODE, (K <= CMAX ? K : 1)>(vp, nv, base, lane, c0, ndx, dx_min, dy, best, bkey, evals); \
     break;
-  if (FAST) {
-    switch (k) {
-      RG_SWEEP_CASE(1)
-      RG_SWEEP_CASE(2)
-      RG_SWEEP_CASE(3)
-      RG_SWEEP_CASE(4)
-      RG_SWEEP_CASE(5)
-      RG_SWEEP_CASE(6)
-      RG_SWEEP_CASE(7)
-      RG_SWEEP_CASE(8)
-      RG_SWEEP_CASE(9)
-      default:
-        break;
-    }
-  } else {
-    switch (k) {
-      RG_SWEEP_CASE(1)
-      RG_SWEEP_CASE(2)
-      RG_SWEEP_CASE(3)
-      RG_SWEEP_CASE(4)
-      default:
-        break;
-    }
+  switch (k) {
+    RG_SWEEP_CASE(1)
+    RG_SWEEP_CASE(2)
+    RG_SWEEP_CASE(3)
+    RG_SWEEP_CASE(4)
+    RG_SWEEP_CASE(5)
+    RG_SWEEP_CASE(6)
+    RG_SWEEP_CASE(7)
+    RG_SWEEP_CASE(8)
+    RG_SWEEP_CASE(9)
+    default:
+      break;
   }
 #undef RG_SWEEP_CASE
+}
+
+// The last m (<= TAIL) candidates of a range that is not a multiple of 32:
+// lanes split the points instead of the candidates, so the warp does not
+// evaluate 32 - m dead lanes for every point.
+template <typename CT, int MODE>
+__device__ __forceinline__ void sweep_tail(const VPoint<CT>* vp, int nv, const CT* rdy, int dx0, int m,
+                                           int dy, int lane, Cand& best, unsigned long long& bkey,
+                                           int& evals) {
+  for (int j = 0; j < m; ++j) {
+    const int dx = dx0 + j;
+    const CT* rd = rdy - dx;
+    int sum = 0, n = 0;
+    for (int k = lane; k < nv; k += 32) {
+      const VPoint<CT> q = vp[k];
+      const CT r = ld_at(rd, q.off);
+      if (MODE == M_FAST) {
+        sum += popc(q.code ^ r);
+      } else if (MODE == M_SIGN) {
+        const CT mk = defined_mask(r);
+        sum += popc((q.code ^ r) & mk);
+        n -= (int)mk;
+      } else if (r != 0u) {
+        sum += popc(q.code ^ r);
+        ++n;
+      }
+    }
+    sum = __reduce_add_sync(0xffffffffu, sum);
+    n = MODE == M_FAST ? nv : __reduce_add_sync(0xffffffffu, n);
+    if (lane == 0 && n > 0) {
+      evals += n;
+      if (MODE == M_FAST) {
+        const unsigned long long key = fast_key(sum, dx, dy);
+        bkey = key < bkey ? key : bkey;
+      } else {
+        const Cand cd = {sum, n, dx, dy};
+        if (better(cd, best)) best = cd;
+      }
+    }
+  }
+}
+
+template <typename CT, int MODE>
+__device__ __forceinline__ void sweep_range(const VPoint<CT>* vp, int nv, const CT* R, const PadGeom& g,
+                                            const rg_search_range& rg, int lane, Cand& best,
+                                            unsigned long long& bkey, int& evals) {
+  // lane-parallel chunks in balanced groups of <= CMAX; a short tail chunk
+  // goes point-parallel
+  const int ndx = rg.dx_max - rg.dx_min + 1;
+  const int nch = (ndx + 31) / 32;
+  const int mt = ndx & 31;
+  const bool ptail = mt != 0 && mt <= TAIL;
+  const int nfull = ptail ? ndx >> 5 : nch;
+  const int groups = (nfull + CMAX - 1) / CMAX;
+  for (int dy = rg.dy_min; dy <= rg.dy_max; ++dy) {
+    for (int gi = 0, c0 = 0; gi < groups; ++gi) {
+      const int k = (nfull - c0 + groups - gi - 1) / (groups - gi);
+      const CT* base = R + (int64_t)dy * g.pitch - rg.dx_min - lane - 32 * c0;
+      sweep_chunks<CT, MODE>(vp, nv, base, lane, c0, k, ndx, rg.dx_min, dy, best, bkey, evals);
+      c0 += k;
+    }
+    if (ptail)
+      sweep_tail<CT, MODE>(vp, nv, R + (int64_t)dy * g.pitch, rg.dx_min + 32 * nfull, mt, dy, lane, best, bkey,
+                           evals);
+  }
 }
 
 // One block_match pass (census.hpp:178-272) by the calling warp.
 // pts: the block's points (smem), shifted by (sx, sy); L: raster of the left
 // codes, R: raster sampled at (x - dx, y + dy).  Both share geometry g.
 template <typename CT>
-__device__ Pass warp_pass(const int2* pts, int np, int sx, int sy, const CT* L, const CT* R,
+#if RG_MW_NOINLINE
+__device__ __noinline__ Pass warp_pass(
+#else
+__device__ Pass warp_pass(
+#endif
+    const int2* pts, int np, int sx, int sy, const CT* L, const CT* R,
                           const PadGeom& g, bool trusted, const rg_search_range& rg, VPoint<CT>* vp,
                           int lane, int& evals) {
   Pass o = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
@@ -169,8 +272,8 @@ __device__ Pass warp_pass(const int2* pts, int np, int sx, int sy, const CT* L, 
     const bool ok = code != 0u;
     const unsigned bal = __ballot_sync(0xffffffffu, ok);
     if (ok) {
-      VPoint<CT> q;
-      q.off = y * g.pitch + x;
+      VPoint<CT> q{};
+      q.off = (uint32_t)(y * g.pitch + x) * (uint32_t)sizeof(CT);
       q.code = code;
       vp[nv + __popc(bal & ((1u << lane) - 1u))] = q;
       xmin = min(xmin, x);
@@ -187,31 +290,38 @@ __device__ Pass warp_pass(const int2* pts, int np, int sx, int sy, const CT* L, 
   xmax = __reduce_max_sync(0xffffffffu, xmax);
   ymax = __reduce_max_sync(0xffffffffu, ymax);
   const int ndx = rg.dx_max - rg.dx_min + 1;
-  const int nch = (ndx + 31) / 32;
   // every sample of every real candidate lies where a computed code is defined
+  // (and the candidate fits the packed FAST key)
   const bool fast = trusted && xmin - rg.dx_max >= g.sx0 && xmax - rg.dx_min <= g.sx1 &&
-                    ymin + rg.dy_min >= g.sy0 && ymax + rg.dy_max <= g.sy1;
+                    ymin + rg.dy_min >= g.sy0 && ymax + rg.dy_max <= g.sy1 && rg.dx_min > -32768 &&
+                    rg.dx_max < 32768 && rg.dy_min >= -32768 && rg.dy_max < 32768;
   Cand best = {0, 0, 0, 0};
-  // the checked path keeps fewer chunks live (it also carries counts)
-  const int cmax = fast ? CMAX : CMAX_SLOW;
-  for (int dy = rg.dy_min; dy <= rg.dy_max; ++dy) {
-    for (int c0 = 0; c0 < nch; c0 += cmax) {
-      const CT* base = R + (int64_t)dy * g.pitch - rg.dx_min - lane - 32 * c0;
-      const int k = min(cmax, nch - c0);
-      if (fast)
-        sweep_chunks<CT, true>(vp, nv, base, lane, c0, k, ndx, rg.dx_min, dy, best, evals);
-      else
-        sweep_chunks<CT, false>(vp, nv, base, lane, c0, k, ndx, rg.dx_min, dy, best, evals);
-    }
-  }
+  if (fast) {
+    unsigned long long bkey = ~0ull;
+    sweep_range<CT, M_FAST>(vp, nv, R, g, rg, lane, best, bkey, evals);
+    // warp argmin of the packed keys (64-bit: two 32-bit reductions)
+    const uint32_t hi = __reduce_min_sync(0xffffffffu, (uint32_t)(bkey >> 32));
+    const uint32_t lo = __reduce_min_sync(0xffffffffu, (uint32_t)(bkey >> 32) == hi ? (uint32_t)bkey : ~0u);
+    const int adx = (int)(lo >> 17);
+    best.sum = (int)hi;
+    best.n = nv;
+    best.dx = (lo & 1u) ? adx : -adx;
+    best.dy = (int)((lo >> 1) & 0xFFFFu) - 0x8000;
+  } else {
+    unsigned long long unused = 0;
+    if (trusted)
+      sweep_range<CT, M_SIGN>(vp, nv, R, g, rg, lane, best, unused, evals);
+    else
+      sweep_range<CT, M_GENERIC>(vp, nv, R, g, rg, lane, best, unused, evals);
 #pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {  // warp argmin
-    Cand u;
-    u.sum = __shfl_xor_sync(0xffffffffu, best.sum, off);
-    u.n = __shfl_xor_sync(0xffffffffu, best.n, off);
-    u.dx = __shfl_xor_sync(0xffffffffu, best.dx, off);
-    u.dy = __shfl_xor_sync(0xffffffffu, best.dy, off);
-    if (better(u, best)) best = u;
+    for (int off = 16; off > 0; off >>= 1) {  // warp argmin
+      Cand u;
+      u.sum = __shfl_xor_sync(0xffffffffu, best.sum, off);
+      u.n = __shfl_xor_sync(0xffffffffu, best.n, off);
+      u.dx = __shfl_xor_sync(0xffffffffu, best.dx, off);
+      u.dy = __shfl_xor_sync(0xffffffffu, best.dy, off);
+      if (better(u, best)) best = u;
+    }
   }
   if (best.n == 0) return o;
   const int bix = best.dx - rg.dx_min;
@@ -225,7 +335,8 @@ __device__ Pass warp_pass(const int2* pts, int np, int sx, int sy, const CT* L, 
     int ms = 0, mn = 0, ps = 0, pn = 0;
     for (int k = lane; k < nv; k += 32) {
       const VPoint<CT> q = vp[k];
-      const CT* a = R + q.off + (int64_t)best.dy * g.pitch - best.dx;
+      const CT* a = reinterpret_cast<const CT*>(reinterpret_cast<const char*>(R + (int64_t)best.dy * g.pitch - best.dx) +
+                                                q.off);
       const CT rm = a[1], rp = a[-1];
       if (rm) {
         ms += popc(q.code ^ rm);

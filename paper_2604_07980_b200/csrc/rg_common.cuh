@@ -129,11 +129,13 @@ void count_launch(rg_ctx* ctx, int stage, int n = 1);
 
 // ------------------------------------------------------------ launchers
 // census (census.cu)
+// internal: batched-pipeline layout, sentinel at bit 31 instead of 25 (Hamming
+// distances unchanged; lets the matcher mask undefined codes by the sign bit)
 cudaError_t launch_census_frames(const uint8_t* left, const uint8_t* right, int n_frames,
                                  int64_t frame_stride, int pitch, int w, int h,
                                  uint32_t* fl, uint32_t* fr, const PadGeom& gf, uint32_t* sl,
                                  uint32_t* sr, const PadGeom& gs, const int32_t* inv_x,
-                                 const int32_t* inv_y, cudaStream_t s);
+                                 const int32_t* inv_y, bool internal, cudaStream_t s);
 cudaError_t launch_census64_frames(const uint8_t* left, const uint8_t* right, int n_frames, int64_t frame_stride,
                                    int pitch, int w, int h, unsigned long long* fl, unsigned long long* fr,
                                    const PadGeom& gf, unsigned long long* sl, unsigned long long* sr,

@@ -24,7 +24,8 @@ import numpy as np
 from . import _abi
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "lib", "libranger_cuda.so")
+# RG_LIB_PATH: A/B builds of the same library (csrc/Makefile VAR=...)
+LIB_PATH = os.environ.get("RG_LIB_PATH") or os.path.join(_PKG, "lib", "libranger_cuda.so")
 
 SUB_LEVELS = 16          # DisparityMap::kSubLevels, image.hpp:53
 RAW_INVALID = -32768     # DisparityMap::kInvalid, image.hpp:54
