@@ -35,9 +35,16 @@ namespace {
 #ifndef RG_MW_TAIL
 #define RG_MW_TAIL 4
 #endif
+#ifndef RG_MW_PIPE
+#define RG_MW_PIPE 1
+#endif
+#ifndef RG_MW_PIPE_UNROLL
+#define RG_MW_PIPE_UNROLL 2
+#endif
 #ifndef RG_MW_NOINLINE
 #define RG_MW_NOINLINE 0
 #endif
+constexpr int kPipeUnroll = RG_MW_PIPE_UNROLL;
 constexpr int kWarpOcc = 32;      // occluder boxes per warp kept in smem
 constexpr int CMAX = RG_MW_CMAX;  // 32-wide dx chunks per sweep (balanced groups)
 constexpr int TAIL = RG_MW_TAIL;  // a last chunk with <= TAIL candidates goes point-parallel
@@ -117,6 +124,49 @@ __device__ __forceinline__ void sweep(const VPoint<CT>* __restrict__ vp, int nv,
   int s[K], n[K];
 #pragma unroll
   for (int c = 0; c < K; ++c) s[c] = n[c] = 0;
+#if RG_MW_PIPE
+  // software-pipelined: the samples of point k+1 are in flight while point k
+  // is consumed (the last prefetch re-reads point nv-1, harmless)
+  VPoint<CT> qn = vp[0];
+  CT rn[K];
+  {
+    const CT* a = reinterpret_cast<const CT*>(reinterpret_cast<const char*>(base) + qn.off);
+#pragma unroll
+    for (int c = 0; c < K; ++c) rn[c] = __ldg(a - 32 * c);
+  }
+#if RG_MW_PIPE == 2  // distance 2: points k+1 and k+2 in flight
+  VPoint<CT> qm = vp[min(1, nv - 1)];
+  CT rm[K];
+  {
+    const CT* a = reinterpret_cast<const CT*>(reinterpret_cast<const char*>(base) + qm.off);
+#pragma unroll
+    for (int c = 0; c < K; ++c) rm[c] = __ldg(a - 32 * c);
+  }
+#endif
+#pragma unroll kPipeUnroll
+  for (int k = 0; k < nv; ++k) {
+    const CT l = qn.code;
+    CT rc[K];
+#pragma unroll
+    for (int c = 0; c < K; ++c) rc[c] = rn[c];
+#if RG_MW_PIPE == 2
+    qn = qm;
+#pragma unroll
+    for (int c = 0; c < K; ++c) rn[c] = rm[c];
+    qm = vp[min(k + 2, nv - 1)];
+    const CT* a = reinterpret_cast<const CT*>(reinterpret_cast<const char*>(base) + qm.off);
+#pragma unroll
+    for (int c = 0; c < K; ++c) rm[c] = __ldg(a - 32 * c);
+#else
+    qn = vp[min(k + 1, nv - 1)];
+    const CT* a = reinterpret_cast<const CT*>(reinterpret_cast<const char*>(base) + qn.off);
+#pragma unroll
+    for (int c = 0; c < K; ++c) rn[c] = __ldg(a - 32 * c);
+#endif
+#pragma unroll
+    for (int c = 0; c < K; ++c) {
+      const CT r = rc[c];
+#else
   for (int k = 0; k < nv; ++k) {
     const VPoint<CT> q = vp[k];
     const CT* a = reinterpret_cast<const CT*>(reinterpret_cast<const char*>(base) + q.off);
@@ -124,6 +174,7 @@ __device__ __forceinline__ void sweep(const VPoint<CT>* __restrict__ vp, int nv,
 #pragma unroll
     for (int c = 0; c < K; ++c) {
       const CT r = __ldg(a - 32 * c);
+#endif
       if (MODE == M_FAST) {
         s[c] += popc(l ^ r);
       } else if (MODE == M_SIGN) {
@@ -219,8 +270,16 @@ __device__ __forceinline__ void sweep_tail(const VPoint<CT>* vp, int nv, const C
   }
 }
 
+#ifndef RG_MW_RANGE_NOINLINE
+#define RG_MW_RANGE_NOINLINE 0
+#endif
 template <typename CT, int MODE>
-__device__ __forceinline__ void sweep_range(const VPoint<CT>* vp, int nv, const CT* R, const PadGeom& g,
+#if RG_MW_RANGE_NOINLINE
+__device__ __noinline__ void sweep_range(
+#else
+__device__ __forceinline__ void sweep_range(
+#endif
+    const VPoint<CT>* vp, int nv, const CT* R, const PadGeom& g,
                                             const rg_search_range& rg, int lane, Cand& best,
                                             unsigned long long& bkey, int& evals) {
   // lane-parallel chunks in balanced groups of <= CMAX; a short tail chunk
