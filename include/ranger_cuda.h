@@ -268,6 +268,10 @@ typedef struct {
   int32_t* d_out_count;
   double focal_px;   /* <= 0: no range */
   double baseline_m;
+  /* nullable, n_frames entries: vertical shift applied to frame f's LEFT image
+   * before ranging, shift_vertical(left, s) (image.hpp:145-154; the rect
+   * correction of pipeline.hpp:135-138), folded into the census row addressing */
+  const int32_t* d_left_shift;
 } rg_frame_batch;
 
 rg_status rg_range_frames(rg_ctx* ctx, const rg_frame_batch* batch,

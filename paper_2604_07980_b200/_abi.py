@@ -71,7 +71,7 @@ class FrameBatch(C.Structure):
         ("frame_stride", C.c_int64), ("d_left", C.c_void_p), ("d_right", C.c_void_p),
         ("d_dets", C.c_void_p), ("d_det_offsets", C.c_void_p), ("max_dets_per_frame", C.c_int32),
         ("out_stride", C.c_int32), ("d_out", C.c_void_p), ("d_out_count", C.c_void_p),
-        ("focal_px", C.c_double), ("baseline_m", C.c_double),
+        ("focal_px", C.c_double), ("baseline_m", C.c_double), ("d_left_shift", C.c_void_p),
     ]
 
 

@@ -30,6 +30,8 @@ rg_status cuda_err(rg_ctx* ctx, cudaError_t e, const char* what) {
   return e == cudaErrorMemoryAllocation ? RG_ENOMEM : RG_ECUDA;
 }
 
+static_assert(B_COUNT <= 40, "rg_ctx::buf too small");
+
 void* dev_buf(rg_ctx* ctx, int id, size_t bytes) {
   if (bytes == 0) bytes = 16;
   if (ctx->cap[id] >= bytes) return ctx->buf[id];
@@ -160,7 +162,7 @@ rg_status census_one(rg_ctx* ctx, const uint8_t* d_img, int w, int h, int ow, in
   int32_t *ix = nullptr, *iy = nullptr;
   TRY(upload_inverse_maps(ctx, w, h, ow, oh, ctx->stream, &ix, &iy));
   RG_CUDA(ctx, launch_census_frames(d_img, nullptr, 1, 0, w, w, h, d_full, nullptr, make_geom(w, h, 0, 0),
-                                    d_red, nullptr, make_geom(ow, oh, 0, 0), ix, iy, false, ctx->stream));
+                                    d_red, nullptr, make_geom(ow, oh, 0, 0), ix, iy, nullptr, false, ctx->stream));
   count_launch(ctx, ST_CENSUS);
   return RG_OK;
 }
@@ -221,6 +223,7 @@ struct FrameJob {
   const uint32_t* full_r = nullptr;
   const uint32_t* scaled_l = nullptr;
   const uint32_t* scaled_r = nullptr;
+  const int32_t* left_shift = nullptr;  // device, n_frames entries (nullable)
 };
 
 bool same_geom(const PadGeom& a, const PadGeom& b) {
@@ -311,11 +314,11 @@ rg_status enqueue_pipeline(rg_ctx* ctx, const FrameJob& J, const rg_ranger_confi
   if (wide) {
     using u64 = unsigned long long;
     RG_CUDA(ctx, launch_census64_frames(J.left, J.right, F, J.frame_stride, J.pitch, w, h, (u64*)fl, (u64*)fr,
-                                        gf, (u64*)sl, (u64*)sr, gs, ix, iy, s));
+                                        gf, (u64*)sl, (u64*)sr, gs, ix, iy, J.left_shift, s));
     count_launch(ctx, ST_CENSUS);
   } else if (!(J.full_l && J.scaled_l)) {
     RG_CUDA(ctx, launch_census_frames(J.left, J.right, F, J.frame_stride, J.pitch, w, h, fl, fr, gf, sl,
-                                      sr, gs, ix, iy, true, s));
+                                      sr, gs, ix, iy, J.left_shift, true, s));
     count_launch(ctx, ST_CENSUS);
   }
   // caller-supplied codes (a pre-filled CensusCache) into the padded layout
@@ -660,7 +663,7 @@ rg_status rg_census_transform64(rg_ctx* ctx, const uint8_t* img, int w, int h, i
   int32_t *ix = nullptr, *iy = nullptr;
   TRY(upload_inverse_maps(ctx, w, h, ow, oh, ctx->stream, &ix, &iy));
   RG_CUDA(ctx, launch_census64_frames(d, nullptr, 1, 0, w, w, h, full, nullptr, make_geom(w, h, 0, 0), red,
-                                      nullptr, make_geom(ow, oh, 0, 0), ix, iy, ctx->stream));
+                                      nullptr, make_geom(ow, oh, 0, 0), ix, iy, nullptr, ctx->stream));
   count_launch(ctx, ST_CENSUS);
   RG_CUDA(ctx, cudaMemcpyAsync(codes, red ? red : full, sizeof(u64) * (size_t)ow * oh, cudaMemcpyDeviceToHost,
                                ctx->stream));
@@ -965,6 +968,7 @@ rg_status rg_range_frames(rg_ctx* ctx, const rg_frame_batch* b, const rg_ranger_
   FrameJob J = {b->d_left, b->d_right, b->n_frames, b->width, b->height, b->pitch, b->frame_stride,
                 b->d_dets, b->d_det_offsets, b->out_stride, b->d_out, b->d_out_count, nullptr,
                 b->focal_px, b->baseline_m};
+  J.left_shift = b->d_left_shift;
   cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
   return run_pipeline(ctx, J, *cfg, s, nullptr);
 }
@@ -1008,6 +1012,13 @@ rg_status rg_range_frames_host(rg_ctx* ctx, const rg_frame_batch* b, const rg_ra
   NEED(counters);
   NEED(hoffs);
   NEED(hc);
+  // per-frame left shifts (host array in this variant): one upload
+  int32_t* d_shift = nullptr;
+  if (b->d_left_shift) {
+    d_shift = DBUF(int32_t, ctx, B_SHIFT, F);
+    NEED(d_shift);
+    RG_CUDA(ctx, cudaMemcpyAsync(d_shift, b->d_left_shift, sizeof(int32_t) * F, cudaMemcpyHostToDevice, s));
+  }
   cudaEvent_t ready[2] = {ctx->ev[6], ctx->ev[7]}, done[2] = {ctx->ev[8], ctx->ev[9]};
   auto stage = [&](int c0, int k) -> rg_status {  // H2D of one chunk into slot k
     const int n = std::min(chunk, F - c0);
@@ -1040,6 +1051,7 @@ rg_status rg_range_frames_host(rg_ctx* ctx, const rg_frame_batch* b, const rg_ra
                   b->height, b->pitch, (int64_t)img_bytes, st_d + (size_t)k * max_chunk_dets,
                   st_o + k * (chunk + 1), b->out_stride, st_out + (size_t)k * chunk * b->out_stride,
                   st_cnt + (size_t)k * chunk, nullptr, b->focal_px, b->baseline_m};
+    if (d_shift) J.left_shift = d_shift + c0;
     TRY(enqueue_pipeline(ctx, J, *cfg, s, counters, nullptr));
     RG_CUDA(ctx, cudaEventRecord(done[k], s));
     // prefetch the next chunk into the other slot once its previous user is done

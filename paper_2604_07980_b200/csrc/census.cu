@@ -37,10 +37,12 @@ __global__ void __launch_bounds__(TPB) census_frames_kernel(
     const uint8_t* __restrict__ left, const uint8_t* __restrict__ right, int64_t frame_stride,
     int pitch, int w, int h, uint32_t* __restrict__ fl, uint32_t* __restrict__ fr, PadGeom gf,
     uint32_t* __restrict__ sl, uint32_t* __restrict__ sr, PadGeom gs,
-    const int32_t* __restrict__ inv_x, const int32_t* __restrict__ inv_y, bool s31) {
+    const int32_t* __restrict__ inv_x, const int32_t* __restrict__ inv_y,
+    const int32_t* __restrict__ lshift, bool s31) {
   __shared__ __align__(16) uint8_t tile[TY + 4][TX + 8];
   const int sides = right ? 2 : 1;
   const int frame = blockIdx.z / sides, side = blockIdx.z - frame * sides;
+  const int sh = (side == 0 && lshift) ? lshift[frame] : 0;  // shift_vertical of the left image
   const uint8_t* img = (side ? right : left) + (int64_t)frame * frame_stride;
   uint32_t* full = (side ? fr : fl) + (int64_t)frame * gf.fstride + gf.origin;
   uint32_t* red = (side ? sr : sl);
@@ -52,7 +54,9 @@ __global__ void __launch_bounds__(TPB) census_frames_kernel(
   for (int idx = threadIdx.x; idx < (TY + 4) * (TX + 4); idx += TPB) {
     const int r = idx / (TX + 4), c = idx - r * (TX + 4);
     const int gx = x0 + c - 2, gy = y0 + r - 2;
-    tile[r][c] = (gx >= 0 && gx < w && gy >= 0 && gy < h) ? img[(int64_t)gy * pitch + gx] : 0;
+    tile[r][c] = (gx >= 0 && gx < w && gy >= 0 && gy < h)
+                     ? img[(int64_t)min(max(gy - sh, 0), h - 1) * pitch + gx]  // image.hpp:145-154
+                     : 0;
   }
   __syncthreads();
 
@@ -203,10 +207,13 @@ template <bool S31>
 __global__ void __launch_bounds__(C2_WARPS * 32) census_pairs_kernel(
     const uint8_t* __restrict__ left, const uint8_t* __restrict__ right, int64_t frame_stride,
     int pitch, int w, int h, uint32_t* __restrict__ fl, uint32_t* __restrict__ fr, PadGeom gf,
-    uint32_t* __restrict__ sl, uint32_t* __restrict__ sr, PadGeom gs) {
+    uint32_t* __restrict__ sl, uint32_t* __restrict__ sr, PadGeom gs, const int32_t* __restrict__ lshift) {
   extern __shared__ __align__(16) uint32_t V[];  // [C2_VR][C2_VW]
   const int sides = right ? 2 : 1;
   const int frame = blockIdx.z / sides, side = blockIdx.z - frame * sides;
+  // shift_vertical (image.hpp:145-154) of the left image folded into the row
+  // addressing: image row y reads source row clamp(y - sh)
+  const int sh = (side == 0 && lshift) ? lshift[frame] : 0;
   const uint8_t* img = (side ? right : left) + (int64_t)frame * frame_stride;
   uint32_t* full = (side ? fr : fl) + (int64_t)frame * gf.fstride + gf.origin;
   uint32_t* red = side ? sr : sl;
@@ -221,7 +228,7 @@ __global__ void __launch_bounds__(C2_WARPS * 32) census_pairs_kernel(
   if (run < C2_RUNS) {
     const int kw = min(max((x0 - 4) / 4 + wk, 0), (w + 3) / 4 - 1);
     const int pw = pitch / 4;
-    const int r0 = run * C2_RUN, ya = y0 - 2 + r0;
+    const int r0 = run * C2_RUN, ya = y0 - 2 + r0 - sh;
     uint32_t wv[C2_RUN + 1];
     if (ya >= 0 && ya + C2_RUN <= h - 1) {  // interior run: plain strided loads
       const uint32_t* col = reinterpret_cast<const uint32_t*>(img) + (int64_t)ya * pw + kw;
@@ -264,10 +271,11 @@ __global__ void __launch_bounds__(X_TPB) census64_kernel(
     const uint8_t* __restrict__ left, const uint8_t* __restrict__ right, int64_t frame_stride, int pitch,
     int w, int h, unsigned long long* __restrict__ fl, unsigned long long* __restrict__ fr, PadGeom gf,
     unsigned long long* __restrict__ sl, unsigned long long* __restrict__ sr, PadGeom gs,
-    const int32_t* __restrict__ inv_x, const int32_t* __restrict__ inv_y) {
+    const int32_t* __restrict__ inv_x, const int32_t* __restrict__ inv_y, const int32_t* __restrict__ lshift) {
   __shared__ uint8_t tile[X_TY + 6][X_TX + 8];
   const int sides = right ? 2 : 1;
   const int frame = blockIdx.z / sides, side = blockIdx.z - frame * sides;
+  const int sh = (side == 0 && lshift) ? lshift[frame] : 0;
   const uint8_t* img = (side ? right : left) + (int64_t)frame * frame_stride;
   unsigned long long* full = (side ? fr : fl) + (int64_t)frame * gf.fstride + gf.origin;
   unsigned long long* red = side ? sr : sl;
@@ -276,7 +284,8 @@ __global__ void __launch_bounds__(X_TPB) census64_kernel(
   for (int idx = threadIdx.x; idx < (X_TY + 6) * (X_TX + 8); idx += X_TPB) {
     const int r = idx / (X_TX + 8), c = idx - r * (X_TX + 8);
     const int gx = x0 + c - 4, gy = y0 + r - 3;
-    tile[r][c] = (gx >= 0 && gx < w && gy >= 0 && gy < h) ? img[(int64_t)gy * pitch + gx] : 0;
+    tile[r][c] = (gx >= 0 && gx < w && gy >= 0 && gy < h) ? img[(int64_t)min(max(gy - sh, 0), h - 1) * pitch + gx]
+                                                          : 0;
   }
   __syncthreads();
   const int tx = threadIdx.x % X_TX, x = x0 + tx;
@@ -330,7 +339,7 @@ cudaError_t launch_census_frames(const uint8_t* left, const uint8_t* right, int 
                                  int64_t frame_stride, int pitch, int w, int h, uint32_t* fl,
                                  uint32_t* fr, const PadGeom& gf, uint32_t* sl, uint32_t* sr,
                                  const PadGeom& gs, const int32_t* inv_x, const int32_t* inv_y,
-                                 bool internal, cudaStream_t s) {
+                                 const int32_t* lshift, bool internal, cudaStream_t s) {
   if (n_frames <= 0) return cudaSuccess;
   const int sides = right ? 2 : 1;
   const bool aligned = (pitch % 4 == 0) && (w % 4 == 0) && (frame_stride % 4 == 0) &&
@@ -347,12 +356,13 @@ cudaError_t launch_census_frames(const uint8_t* left, const uint8_t* right, int 
       attr[internal] = true;
     }
     dim3 grid((w + C2_TX - 1) / C2_TX, (h + C2_TY - 1) / C2_TY, sides * n_frames);
-    kern<<<grid, C2_WARPS * 32, C2_SMEM, s>>>(left, right, frame_stride, pitch, w, h, fl, fr, gf, sl, sr, gs);
+    kern<<<grid, C2_WARPS * 32, C2_SMEM, s>>>(left, right, frame_stride, pitch, w, h, fl, fr, gf, sl, sr, gs,
+                                              lshift);
     return cudaGetLastError();
   }
   dim3 grid((w + TX - 1) / TX, (h + TY - 1) / TY, sides * n_frames);
   census_frames_kernel<<<grid, TPB, 0, s>>>(left, right, frame_stride, pitch, w, h, fl, fr, gf, sl,
-                                            sr, gs, inv_x, inv_y, internal);
+                                            sr, gs, inv_x, inv_y, lshift, internal);
   return cudaGetLastError();
 }
 
@@ -360,11 +370,11 @@ cudaError_t launch_census64_frames(const uint8_t* left, const uint8_t* right, in
                                    int pitch, int w, int h, unsigned long long* fl, unsigned long long* fr,
                                    const PadGeom& gf, unsigned long long* sl, unsigned long long* sr,
                                    const PadGeom& gs, const int32_t* inv_x, const int32_t* inv_y,
-                                   cudaStream_t s) {
+                                   const int32_t* lshift, cudaStream_t s) {
   if (n_frames <= 0) return cudaSuccess;
   dim3 grid((w + X_TX - 1) / X_TX, (h + X_TY - 1) / X_TY, (right ? 2 : 1) * n_frames);
   census64_kernel<<<grid, X_TPB, 0, s>>>(left, right, frame_stride, pitch, w, h, fl, fr, gf, sl, sr, gs, inv_x,
-                                         inv_y);
+                                         inv_y, lshift);
   return cudaGetLastError();
 }
 

@@ -98,8 +98,8 @@ struct rg_ctx {
   int slot_capacity = 0;    // grows on RG_EOVERFLOW
   int64_t last_slots = 0;   // slots used by the last batch
   // grow-only device scratch, keyed by role
-  void* buf[32] = {};
-  size_t cap[32] = {};
+  void* buf[40] = {};
+  size_t cap[40] = {};
   // pinned host scratch
   void* hbuf[8] = {};
   size_t hcap[8] = {};
@@ -111,7 +111,8 @@ enum BufId {
   B_IMG_L, B_IMG_R, B_CEN_FL, B_CEN_FR, B_CEN_SL, B_CEN_SR, B_DETS, B_DET_OFF,
   B_OBJ, B_SLOTS, B_SLOT_RES, B_OUT, B_OUT_CNT, B_COUNTERS, B_MAPX, B_MAPY,
   B_PTS, B_OFFS, B_RANGES, B_MRES, B_TMP0, B_TMP1, B_TMP2, B_TMP3, B_STATS,
-  B_BM_L, B_BM_R, B_BM_OUT, B_BM_CNT, B_ROIS, B_STAGE_L, B_STAGE_R,
+  B_BM_L, B_BM_R, B_BM_OUT, B_BM_CNT, B_ROIS, B_STAGE_L, B_STAGE_R, B_SHIFT,
+  B_COUNT
 };
 
 // error helpers (defined in api.cu)
@@ -135,12 +136,13 @@ cudaError_t launch_census_frames(const uint8_t* left, const uint8_t* right, int 
                                  int64_t frame_stride, int pitch, int w, int h,
                                  uint32_t* fl, uint32_t* fr, const PadGeom& gf, uint32_t* sl,
                                  uint32_t* sr, const PadGeom& gs, const int32_t* inv_x,
-                                 const int32_t* inv_y, bool internal, cudaStream_t s);
+                                 const int32_t* inv_y, const int32_t* lshift, bool internal,
+                                 cudaStream_t s);
 cudaError_t launch_census64_frames(const uint8_t* left, const uint8_t* right, int n_frames, int64_t frame_stride,
                                    int pitch, int w, int h, unsigned long long* fl, unsigned long long* fr,
                                    const PadGeom& gf, unsigned long long* sl, unsigned long long* sr,
                                    const PadGeom& gs, const int32_t* inv_x, const int32_t* inv_y,
-                                   cudaStream_t s);
+                                   const int32_t* lshift, cudaStream_t s);
 cudaError_t launch_roi_mask(uint32_t* codes, int w, int h, const rg_rect* rois, int n_rois,
                             cudaStream_t s);
 

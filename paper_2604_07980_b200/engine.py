@@ -49,28 +49,34 @@ class FrameEngine:
         self.out_stride = max(1, min(max_dets_per_frame, cfg.max_objects))
         self.focal, self.baseline = focal_px, baseline_m
 
-    def _batch(self, n_frames, pitch, stride, left, right, dets, offs, out, cnt) -> _abi.FrameBatch:
+    def _batch(self, n_frames, pitch, stride, left, right, dets, offs, out, cnt, shift=None) -> _abi.FrameBatch:
         return _abi.FrameBatch(n_frames, self.w, self.h, pitch, stride, left, right, dets, offs, self.max_dets,
-                               self.out_stride, out, cnt, self.focal, self.baseline)
+                               self.out_stride, out, cnt, self.focal, self.baseline, shift)
 
-    def range_device(self, left, right, dets, offsets, out, out_count, stream=None) -> None:
+    def range_device(self, left, right, dets, offsets, out, out_count, stream=None, left_shift=None) -> None:
         """All arguments are CUDA torch tensors: left/right uint8 (F, H, pitch);
         dets uint8 view of DET_DTYPE records; offsets int32 (F+1); out uint8
-        (F * out_stride * 32); out_count int32 (F)."""
+        (F * out_stride * 32); out_count int32 (F); left_shift int32 (F) or
+        None: per-frame shift_vertical of the left image (pipeline.hpp:135-138)."""
         F = left.shape[0]
         pitch = left.shape[2] if left.dim() == 3 else self.w
         b = self._batch(F, pitch, left.stride(0), left.data_ptr(), right.data_ptr(), dets.data_ptr(),
-                        offsets.data_ptr(), out.data_ptr(), out_count.data_ptr())
+                        offsets.data_ptr(), out.data_ptr(), out_count.data_ptr(),
+                        left_shift.data_ptr() if left_shift is not None else None)
         s = C.c_void_p(stream) if stream is not None else None
         self.ctx.check(lib().rg_range_frames(self.ctx.handle, C.byref(b), C.byref(self._c), s))
 
     def range_host(self, left: np.ndarray, right: np.ndarray, dets: np.ndarray, offsets: np.ndarray,
-                   out: np.ndarray, out_count: np.ndarray, chunk: int = 16, stream=None) -> None:
+                   out: np.ndarray, out_count: np.ndarray, chunk: int = 16, stream=None,
+                   left_shift: Optional[np.ndarray] = None) -> None:
         """Host (ideally pinned) numpy buffers; H2D / compute / D2H inside."""
         F = left.shape[0]
+        if left_shift is not None:
+            left_shift = np.ascontiguousarray(left_shift, np.int32)
+            assert left_shift.shape == (F,)
         b = self._batch(F, self.w, self.w * self.h, left.ctypes.data, right.ctypes.data,
                         dets.ctypes.data if dets.size else 0, offsets.ctypes.data, out.ctypes.data,
-                        out_count.ctypes.data)
+                        out_count.ctypes.data, left_shift.ctypes.data if left_shift is not None else None)
         s = C.c_void_p(stream) if stream is not None else None
         self.ctx.check(lib().rg_range_frames_host(self.ctx.handle, C.byref(b), C.byref(self._c), chunk, s))
 

@@ -64,6 +64,45 @@ def test_range_frames_device_and_host(ctx, orc, name):
         assert ho[f, :len(want)].tobytes() == want
 
 
+def shift_vertical(img, dy):
+    """image.hpp:145-154: out(x, y) = in(x, clamp(y - dy, 0, H - 1))."""
+    h = img.shape[0]
+    return img[np.clip(np.arange(h) - dy, 0, h - 1)]
+
+
+@pytest.mark.parametrize("name,wide", [("c1", False), ("c2", False), ("c1", True)])
+def test_range_frames_left_shift(ctx, orc, name, wide):
+    """Per-frame rect correction (pipeline.hpp:135-138) folded into the census
+    row addressing == ranging shift_vertical(left, s) with the oracle."""
+    import torch
+
+    fn = {"c1": S.scene_c1, "c2": S.scene_c2}[name]
+    shifts = np.array([-3, 0, 2, 5, -1], np.int32)
+    n = len(shifts)
+    L, R, D, cfg, sc = _frames(fn, n)
+    cfg.census_9x7 = wide
+    maxd = max(len(d) for d in D)
+    eng = FrameEngine(sc.width, sc.height, cfg, maxd, S.F_PX, S.BASELINE_M, ctx=ctx)
+    recs, offs = pack_detections(D)
+    dev = torch.device("cuda", 0)
+    out = torch.zeros(n * eng.out_stride * 32, dtype=torch.uint8, device=dev)
+    cnt = torch.zeros(n, dtype=torch.int32, device=dev)
+    eng.range_device(torch.from_numpy(L).to(dev), torch.from_numpy(R).to(dev),
+                     torch.from_numpy(recs.view(np.uint8)).to(dev), torch.from_numpy(offs).to(dev), out, cnt,
+                     left_shift=torch.from_numpy(shifts).to(dev))
+    torch.cuda.synchronize()
+    o = out.cpu().numpy().reshape(n, eng.out_stride * 32)
+    h_out = np.zeros(n * eng.out_stride, OUT_DTYPE)
+    h_cnt = np.zeros(n, np.int32)
+    eng.range_host(L, R, recs, offs, h_out, h_cnt, chunk=2, left_shift=shifts)
+    ho = h_out.view(np.uint8).reshape(n, eng.out_stride * 32)
+    for f in range(n):
+        want = _want(orc, np.ascontiguousarray(shift_vertical(L[f], int(shifts[f]))), R[f], D[f], cfg)
+        assert int(cnt[f]) * 32 == len(want) == int(h_cnt[f]) * 32
+        assert o[f, :len(want)].tobytes() == want
+        assert ho[f, :len(want)].tobytes() == want
+
+
 def test_auto_rect_frames_equals_single(ctx):
     import torch
 
