@@ -284,6 +284,50 @@ rg_status rg_range_frames(rg_ctx* ctx, const rg_frame_batch* batch,
 rg_status rg_range_frames_host(rg_ctx* ctx, const rg_frame_batch* batch,
                                const rg_ranger_config* cfg, int chunk, void* stream);
 
+/* ------------------------------------------------- sequence orchestration */
+
+/* RectSearchConfig (pipeline.hpp:52-62): the per-frame vertical-offset search
+ * and its filter, as Pipeline::process_frame runs them (pipeline.hpp:135-178). */
+typedef struct {
+  int32_t enabled;
+  int32_t delta_min, delta_max;
+  int32_t window;      /* median filter length, frames */
+  double rate_limit;   /* max applied-offset change, px per frame */
+  rg_bm_params bm;     /* reference default {32, 9, -4, 10, 10, 1} */
+} rg_rect_search_config;
+
+#define RG_RECT_MAX_WINDOW 64
+/* RectOffsetState (autorect.hpp:62-75), carried across calls by the caller. */
+typedef struct {
+  int32_t window;
+  int32_t n_hist;  /* history.size() */
+  int32_t next;
+  int32_t pad;
+  double delta_max;
+  double current;  /* applied offset */
+  int32_t history[RG_RECT_MAX_WINDOW];
+} rg_rect_state;
+
+/* RectOffsetState(k, rate) (autorect.hpp:69-72); k in [1, RG_RECT_MAX_WINDOW]. */
+rg_status rg_rect_state_init(rg_rect_state* st, int window, double rate);
+/* filter_offset (autorect.hpp:77-90): push delta*, return the applied offset. */
+rg_status rg_filter_offset(rg_rect_state* st, int delta_star, double* applied);
+
+/* The TEMPLATE_MATCHER frame loop of Pipeline::process_frame over a batch of
+ * consecutive frames (pipeline.hpp:124-178), as the two-pass schedule of
+ * pass A runs the offset search on every UNCORRECTED pair
+ * (rect_search_roi = central half, pipeline.hpp:268-275) on the device; the
+ * host then walks the frames in order -- shift_f = lround(st.current) before
+ * frame f's filter update (pipeline.hpp:135-138, 178); pass B ranges
+ * shift_vertical(left_f, shift_f) with the shift folded into the census row
+ * addressing.  `b` holds DEVICE pointers as for rg_range_frames (its
+ * d_left_shift is ignored); `st` is updated in place; out_shift / out_delta
+ * (HOST, n_frames entries, nullable) receive the applied shifts and the raw
+ * search results.  Asynchronous on `stream` after the host scan. */
+rg_status rg_range_sequence(rg_ctx* ctx, const rg_frame_batch* b, const rg_ranger_config* cfg,
+                            const rg_rect_search_config* rect, rg_rect_state* st,
+                            int32_t* out_shift, int32_t* out_delta, void* stream);
+
 /* ------------------------------------------------------ BM / autorect (K5) */
 
 /* validate(const BmParams&), bm.hpp:24-32 */

@@ -70,6 +70,11 @@ int ref_render_stereo_pair(const rg_scene_config* cfg, const rg_scene_object* ob
                            int n_obj, uint8_t* left, uint8_t* right);
 int ref_ground_truth_detections(const rg_scene_config* cfg, const rg_scene_object* objs,
                                 int n_obj, rg_detection* out, int* n_out);
+int ref_pipeline_sequence(const uint8_t* left, const uint8_t* right, int w, int h, int n_frames,
+                          const rg_detection* dets, const int32_t* det_offsets, const rg_ranger_config* cfg,
+                          const rg_rect_search_config* rect, double f, double b, double cx, double cy,
+                          double h_cam, rg_object_disparity* out, int out_stride, int32_t* out_count,
+                          double* rect_applied);
 /* CPU baseline: range n_frames frames (left/right packed w*h each, dets CSR)
  * with `threads` host threads, each thread ranging whole frames at workers=1
  * (SURVEY.md 8(d) mode iii); returns wall seconds, fills out like

@@ -16,6 +16,7 @@
 #include "ranger/autorect.hpp"
 #include "ranger/bm.hpp"
 #include "ranger/census.hpp"
+#include "ranger/pipeline.hpp"
 #include "ranger/synth.hpp"
 #include "ranger/template_match.hpp"
 
@@ -406,6 +407,56 @@ double ref_bench_estimate(const uint8_t* left, const uint8_t* right, int w, int 
     });
   for (auto& th : pool) th.join();
   return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+
+/* Pipeline::process_frame (pipeline.hpp:124-266), TEMPLATE_MATCHER method,
+ * over n_frames consecutive frames (packed w*h images, dets CSR); no radar.
+ * out[f*out_stride + k], out_count[f]: PipelineResult::objects of frame f;
+ * rect_applied[f]: RefinerLogRecord::rect_delta. */
+int ref_pipeline_sequence(const uint8_t* left, const uint8_t* right, int w, int h, int n_frames,
+                          const rg_detection* dets, const int32_t* det_offsets, const rg_ranger_config* cfg,
+                          const rg_rect_search_config* rect, double f, double b, double cx, double cy,
+                          double h_cam, rg_object_disparity* out, int out_stride, int32_t* out_count,
+                          double* rect_applied) {
+  return guarded([&] {
+    PipelineConfig pc;
+    pc.method = DepthMethod::kTemplateMatcher;
+    pc.calib = make_calibration(f, b, cx, cy, h_cam);
+    pc.ranger = to_cfg(cfg);
+    pc.rect.enabled = rect->enabled != 0;
+    pc.rect.delta_min = rect->delta_min;
+    pc.rect.delta_max = rect->delta_max;
+    pc.rect.window = rect->window;
+    pc.rect.rate_limit = rect->rate_limit;
+    pc.rect.bm = to_bm(&rect->bm);
+    pc.workers = 1;
+    Pipeline pipe(pc);
+    const std::size_t img = std::size_t(w) * h;
+    for (int t = 0; t < n_frames; ++t) {
+      FrameInput in;
+      in.frame_id = t;
+      in.left = to_gray(left + img * t, w, h);
+      in.right = to_gray(right + img * t, w, h);
+      in.detections = to_dets(dets + det_offsets[t], det_offsets[t + 1] - det_offsets[t]);
+      PipelineResult res;
+      pipe.process_frame(in, res);
+      int k = 0;
+      for (const auto& fo : res.objects) {
+        if (k >= out_stride) break;
+        rg_object_disparity& o = out[std::size_t(t) * out_stride + k++];
+        std::memset(&o, 0, sizeof(o));
+        o.det_id = fo.obj.det_id;
+        o.kind = fo.obj.kind == ObjectKind::kFar ? RG_KIND_FAR : RG_KIND_CLOSE;
+        o.n_blocks_used = fo.obj.n_blocks_used;
+        o.valid = fo.obj.valid;
+        o.disparity = fo.obj.disparity;
+      }
+      out_count[t] = k;
+      rect_applied[t] = res.refiner_log.empty() ? 0.0 : res.refiner_log.back().rect_delta;
+    }
+    return RG_OK;
+  });
 }
 
 }  // extern "C"

@@ -65,6 +65,19 @@ class BmParams(C.Structure):
                 ("downscale", C.c_int32), ("texture_threshold", C.c_double), ("uniqueness_ratio", C.c_double)]
 
 
+class RectSearchConfig(C.Structure):
+    _fields_ = [("enabled", C.c_int32), ("delta_min", C.c_int32), ("delta_max", C.c_int32), ("window", C.c_int32),
+                ("rate_limit", C.c_double), ("bm", BmParams)]
+
+
+RECT_MAX_WINDOW = 64
+
+
+class RectState(C.Structure):
+    _fields_ = [("window", C.c_int32), ("n_hist", C.c_int32), ("next", C.c_int32), ("pad", C.c_int32),
+                ("delta_max", C.c_double), ("current", C.c_double), ("history", C.c_int32 * RECT_MAX_WINDOW)]
+
+
 class FrameBatch(C.Structure):
     _fields_ = [
         ("n_frames", C.c_int32), ("width", C.c_int32), ("height", C.c_int32), ("pitch", C.c_int32),
@@ -123,6 +136,9 @@ SIGNATURES = {
     "rg_estimate_object_disparities": (I, [P, P, P, I, I, P, I, P, P, D, D, P, P, P]),
     "rg_range_frames": (I, [P, P, P, P]),
     "rg_range_frames_host": (I, [P, P, P, I, P]),
+    "rg_rect_state_init": (I, [P, I, D]),
+    "rg_filter_offset": (I, [P, I, P]),
+    "rg_range_sequence": (I, [P, P, P, P, P, P, P, P]),
     "rg_validate_bm_params": (I, [P, P]),
     "rg_bm_disparity": (I, [P, P, P, I, I, P, P]),
     "rg_auto_rect_search": (I, [P, P, P, I, I, P, I, I, P, P, P]),

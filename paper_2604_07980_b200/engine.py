@@ -80,6 +80,27 @@ class FrameEngine:
         s = C.c_void_p(stream) if stream is not None else None
         self.ctx.check(lib().rg_range_frames_host(self.ctx.handle, C.byref(b), C.byref(self._c), chunk, s))
 
+    def range_sequence(self, left, right, dets, offsets, out, out_count, rect=None, state=None, stream=None):
+        """Pipeline::process_frame's TEMPLATE_MATCHER loop over consecutive
+        device frames (rg_range_sequence): offset search on every uncorrected
+        pair, host filter scan, ranging of the rect-corrected pairs.  `state`
+        (RectOffsetState) is advanced in place; returns (shifts, delta_stars)."""
+        from .ranger import RectOffsetState, RectSearchConfig, rect_state_from_c, rect_state_to_c
+
+        rect = rect or RectSearchConfig()
+        state = state if state is not None else RectOffsetState(rect.window, rect.rate_limit)
+        F = left.shape[0]
+        pitch = left.shape[2] if left.dim() == 3 else self.w
+        b = self._batch(F, pitch, left.stride(0), left.data_ptr(), right.data_ptr(), dets.data_ptr(),
+                        offsets.data_ptr(), out.data_ptr(), out_count.data_ptr())
+        rc, sc = rect.to_c(), rect_state_to_c(state)
+        shifts, deltas = np.zeros(F, np.int32), np.zeros(F, np.int32)
+        s = C.c_void_p(stream) if stream is not None else None
+        self.ctx.check(lib().rg_range_sequence(self.ctx.handle, C.byref(b), C.byref(self._c), C.byref(rc),
+                                               C.byref(sc), shifts.ctypes.data, deltas.ctypes.data, s))
+        rect_state_from_c(sc, state)
+        return shifts, deltas
+
     def auto_rect_device(self, left, right, roi, delta_min: int, delta_max: int, bm, best, counts=None,
                          stream=None) -> None:
         """rg_auto_rect_frames over device frames (torch tensors)."""

@@ -615,6 +615,36 @@ class RectOffsetState:
         self.next = 0
 
 
+@dataclass
+class RectSearchConfig:
+    """pipeline.hpp:52-62 with the reference's defaults."""
+    enabled: bool = True
+    delta_min: int = -3
+    delta_max: int = 3
+    window: int = 5
+    rate_limit: float = 1.0
+    bm: BmParams = field(default_factory=lambda: BmParams(32, 9, -4, 10, 10, 1))
+
+    def to_c(self) -> _abi.RectSearchConfig:
+        return _abi.RectSearchConfig(int(bool(self.enabled)), self.delta_min, self.delta_max, self.window,
+                                     float(self.rate_limit), self.bm.to_c())
+
+
+def rect_state_to_c(st: RectOffsetState) -> _abi.RectState:
+    if not 1 <= st.window <= _abi.RECT_MAX_WINDOW:
+        raise InvalidArgument("RectOffsetState: window must be in [1, 64] for the device path")
+    c = _abi.RectState()
+    c.window, c.n_hist, c.next, c.delta_max, c.current = st.window, len(st.history), st.next, st.delta_max, st.current
+    for i, v in enumerate(st.history):
+        c.history[i] = int(v)
+    return c
+
+
+def rect_state_from_c(c: _abi.RectState, st: RectOffsetState) -> None:
+    st.window, st.next, st.delta_max, st.current = c.window, c.next, c.delta_max, c.current
+    st.history = [int(c.history[i]) for i in range(c.n_hist)]
+
+
 def filter_offset(st: RectOffsetState, delta_star: int) -> float:
     """autorect.hpp:77-90: lower median of the window, rate-limited."""
     if len(st.history) < st.window:

@@ -49,6 +49,8 @@ class Checker:
             self.lib.ref_render_stereo_pair.argtypes = [P, P, I, P, P]
             self.lib.ref_ground_truth_detections.restype = I
             self.lib.ref_ground_truth_detections.argtypes = [P, P, I, P, P]
+            self.lib.ref_pipeline_sequence.restype = I
+            self.lib.ref_pipeline_sequence.argtypes = [P, P, I, I, I, P, P, P, P, D, D, D, D, D, P, I, P, P]
             self.lib.ref_bench_estimate.restype = D
             self.lib.ref_bench_estimate.argtypes = [P, P, I, I, I, P, P, P, I, P, I, P]
 

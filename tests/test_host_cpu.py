@@ -44,7 +44,8 @@ def test_struct_layouts_match_the_c_header():
                "rg_detection": _abi.Detection, "rg_ranger_config": _abi.RangerConfig,
                "rg_object_disparity": _abi.ObjectDisparity, "rg_ranger_stats": _abi.RangerStats,
                "rg_census_cache": _abi.CensusCache, "rg_bm_params": _abi.BmParams,
-               "rg_frame_batch": _abi.FrameBatch, "rg_scene_object": _abi.SceneObject,
+               "rg_frame_batch": _abi.FrameBatch, "rg_rect_search_config": _abi.RectSearchConfig,
+               "rg_rect_state": _abi.RectState, "rg_scene_object": _abi.SceneObject,
                "rg_scene_config": _abi.SceneConfig}
     for cname, py in structs.items():
         for f, _ in py._fields_:
