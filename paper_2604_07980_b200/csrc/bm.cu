@@ -15,6 +15,9 @@
 // reduced per CTA and added with one integer atomic (deterministic).
 #include <cstdlib>
 
+#include <algorithm>
+#include <cstdlib>
+
 #include "rg_common.cuh"
 
 namespace rg {
@@ -224,14 +227,14 @@ template <int HW, int DPL>
 __global__ void __launch_bounds__(LWPB * 32) bm_lanes_kernel(
     const uint8_t* __restrict__ left, const uint8_t* __restrict__ right, int64_t stride, int pitch, int img_h,
     int W, int H, int x0c, int y0c, int delta_min, int n_delta, int d_lo, int nd, double tex, double uniq,
-    int16_t* __restrict__ raw, int64_t* __restrict__ counts) {
+    int16_t* __restrict__ raw, int64_t* __restrict__ counts, int skip0, int skip1) {
   constexpr int NC = LBW + 2 * HW;  // column sums per lane
   // column sums in smem, lane-major so every access is conflict-free
   __shared__ int css[LWPB][DPL][NC][32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int band = blockIdx.x * LWPB + warp;
   const int xb = band * LBW;
-  if (xb >= W) return;  // warp-uniform; no block-level sync below
+  if (xb >= W || (band >= skip0 && band < skip1)) return;  // warp-uniform; no block-level sync below
   const int yb = blockIdx.y * LRS;
   const int frame = blockIdx.z / n_delta, kd = blockIdx.z - frame * n_delta;
   const int delta = delta_min + kd;
@@ -386,12 +389,257 @@ __global__ void __launch_bounds__(LWPB * 32) bm_lanes_kernel(
 template <int HW, int DPL>
 static cudaError_t launch_lanes(const uint8_t* left, const uint8_t* right, int n_frames, int64_t stride, int pitch,
                                 int img_h, int w, int h, int x0, int y0, int delta_min, int n_delta, rg_bm_params p,
-                                int16_t* raw, int64_t* counts, cudaStream_t s) {
+                                int16_t* raw, int64_t* counts, cudaStream_t s, int skip0 = 0, int skip1 = 0) {
   const int bands = (w + LBW - 1) / LBW;
+  if (skip0 <= 0 && skip1 >= bands) return cudaSuccess;
   dim3 grid((bands + LWPB - 1) / LWPB, (h + LRS - 1) / LRS, n_frames * n_delta);
   bm_lanes_kernel<HW, DPL><<<grid, LWPB * 32, 0, s>>>(left, right, stride, pitch, img_h, w, h, x0, y0, delta_min,
                                                        n_delta, p.min_disparity, p.num_disparities,
-                                                       p.texture_threshold, p.uniqueness_ratio, raw, counts);
+                                                       p.texture_threshold, p.uniqueness_ratio, raw, counts,
+                                                       skip0, skip1);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Byte-SIMD SAD matcher for num_disparities <= 32, block_size <= 9 (the
+// autorect search and the common dense configs).  Same band/strip tiling as
+// bm_lanes_kernel (warp = 32 output columns x SB_RS rows of one (frame, delta)
+// crop, lane = disparity), but every stage runs packed:
+//   * |L - R| of 4 columns is one VABSDIFF4 (__vabsdiffu4) on 32-bit words:
+//     the lane's right-row bytes x - d are realigned by a funnel shift;
+//   * the 2HW+1-row column sums V are 16-bit pairs (c, c+1) updated by one
+//     IADD3 per pair (V + new - old is exact lane-wise: both lanes' results
+//     are window sums in [0, 2^16), so no borrow crosses the halves); the
+//     absolute differences of the last 2HW+1 rows live in a shared-memory ring;
+//   * the row-direction box sum slides over (x, x+16) pairs, one IADD3 per
+//     two output pixels;
+//   * the per-pixel argmin is transposed: lane d writes key = SAD << 5 | d for
+//     its 32 pixels into a [pixel][d] tile and lane x then reduces its own
+//     32 keys with 3-input mins (first minimum = smallest d, bm.hpp:75-82);
+//     the second best (|i - best| > 1, bm.hpp:84-89) is a second pass after
+//     masking the three neighbours in the tile.
+// Texture gate (bm.hpp:50-56): sum of 8 adjacent |diffs| per window row with
+// two VABSDIFF4.ACC (__vsadu4) per row, slid over rows.
+// Only bands whose byte reads stay inside the image rows are run here (the
+// launcher computes that range); the others run bm_lanes_kernel.
+constexpr int SB_W = 4;     // warps (bands) per CTA
+constexpr int SB_RS = 32;   // rows per warp strip
+constexpr int SB_NCW = 10;  // AD words per row: columns xb-4 .. xb+35
+constexpr int SB_TP = 36;   // transpose tile pitch (words)
+constexpr uint32_t SB_INF = 0xFFFFFFFFu;
+
+template <int HW>
+constexpr size_t sb_smem() {
+  return sizeof(uint32_t) * SB_W * ((2 * HW + 1) * SB_NCW * 32 + 32 * SB_TP);
+}
+
+template <int HW>
+__global__ void __launch_bounds__(SB_W * 32) bm_simd_kernel(
+    const uint8_t* __restrict__ left, const uint8_t* __restrict__ right, int64_t stride, int pitch, int img_h,
+    int W, int H, int x0c, int y0c, int delta_min, int n_delta, int d_lo, int nd, double tex, double uniq,
+    int16_t* __restrict__ raw, int64_t* __restrict__ counts, int band0, int band1) {
+  constexpr int NR = 2 * HW + 1;
+  extern __shared__ __align__(16) uint32_t sbm[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int band = band0 + blockIdx.x * SB_W + warp;
+  if (band >= band1) return;  // warp-uniform; warps never synchronise with each other
+  uint32_t* ring = sbm + warp * (NR * SB_NCW * 32 + 32 * SB_TP);  // [NR][NCW][32]
+  uint32_t* tile = ring + NR * SB_NCW * 32;                       // [32 pixels][SB_TP]
+  const int xb = band * 32;
+  const int yb = blockIdx.y * SB_RS;
+  if (yb >= H) return;
+  const int frame = blockIdx.z / n_delta, kd = blockIdx.z - frame * n_delta;
+  const int delta = delta_min + kd;
+  const uint8_t* Lf = left + (int64_t)frame * stride;
+  const uint8_t* Rf = right + (int64_t)frame * stride;
+  // crop row -> image row pointers (left shifted by delta with edge clamp,
+  // image.hpp:145-154; crop rows clamped like the reference's reads never need)
+  auto lrow = [&](int yr) {
+    return reinterpret_cast<const uint32_t*>(
+        Lf + (int64_t)clampi(y0c + clampi(yr, 0, H - 1) - delta, 0, img_h - 1) * pitch);
+  };
+  auto rrow = [&](int yr) {
+    return reinterpret_cast<const uint32_t*>(Rf + (int64_t)(y0c + clampi(yr, 0, H - 1)) * pitch);
+  };
+  const int k = lane;
+  const int dk = d_lo + min(k, nd - 1);      // idle lanes (k >= nd) read valid bytes
+  const int lcol = x0c + xb - 4;             // image column of AD column 0
+  const int lw0 = lcol >> 2, lsh = (lcol & 3) * 8;
+  const int rcol = lcol - dk;                // this lane's right column for AD column 0
+  const int rw0 = rcol >> 2, rsh = (rcol & 3) * 8;
+  // |L - R| words of one crop row: columns xb-4+4g .. +3 of this lane's d
+  auto ad_row = [&](int yr, uint32_t (&a)[SB_NCW]) {
+    const uint32_t* lp = lrow(yr) + lw0;
+    const uint32_t* rp = rrow(yr) + rw0;
+    uint32_t lv[SB_NCW + 1], rv[SB_NCW + 1];
+#pragma unroll
+    for (int g = 0; g <= SB_NCW; ++g) {
+      lv[g] = __ldg(lp + g);
+      rv[g] = __ldg(rp + g);
+    }
+#pragma unroll
+    for (int g = 0; g < SB_NCW; ++g)
+      a[g] = __vabsdiffu4(__funnelshift_r(lv[g], lv[g + 1], lsh), __funnelshift_r(rv[g], rv[g + 1], rsh));
+  };
+  // texture: 8 adjacent |diffs| of row yr around pixel x = xb + lane (columns
+  // x-4 .. x+4), window columns x-HW .. x+HW only
+  const int tcol = x0c + xb + lane - 4;
+  const int tw0 = tcol >> 2, tsh = (tcol & 3) * 8;
+  constexpr uint32_t TM0 = HW >= 4 ? 0xFFFFFFFFu : (0xFFFFFFFFu << (8 * (4 - HW)));   // i = -4..-1
+  constexpr uint32_t TM1 = HW >= 4 ? 0xFFFFFFFFu : (0xFFFFFFFFu >> (8 * (4 - HW)));   // i = 0..3
+  auto tex_row = [&](int yr) -> int {
+    const uint32_t* lp = lrow(yr) + tw0;
+    const uint32_t u0 = __ldg(lp), u1 = __ldg(lp + 1), u2 = __ldg(lp + 2);
+    const uint32_t a0 = __funnelshift_r(u0, u1, tsh), a1 = __funnelshift_r(u1, u2, tsh);  // x-4..x-1, x..x+3
+    const uint32_t b0 = __funnelshift_r(a0, a1, 8), b1 = __funnelshift_r(a1, __funnelshift_r(u2, u2, tsh), 8);
+    return (int)__vsadu4(a0 & TM0, b0 & TM0) + (int)__vsadu4(a1 & TM1, b1 & TM1);
+  };
+  // ---- initial window rows yb-HW .. yb+HW
+  uint32_t V[SB_NCW * 2];
+#pragma unroll
+  for (int i = 0; i < SB_NCW * 2; ++i) V[i] = 0u;
+  int grad = 0;
+  for (int r = 0; r < NR; ++r) {
+    uint32_t a[SB_NCW];
+    ad_row(yb - HW + r, a);
+#pragma unroll
+    for (int g = 0; g < SB_NCW; ++g) {
+      ring[(r * SB_NCW + g) * 32 + lane] = a[g];
+      V[2 * g] += __byte_perm(a[g], 0u, 0x4140);
+      V[2 * g + 1] += __byte_perm(a[g], 0u, 0x4342);
+    }
+    grad += tex_row(yb - HW + r);
+  }
+  // evaluable pixels of this lane's d: x - d - HW >= 0 && x - d + HW < W (bm.hpp:61-64)
+  const int xlo = dk + HW - xb, xhi = W - 1 - HW + dk - xb;  // band-relative
+  const bool all_ev = __all_sync(0xffffffffu, k >= nd || (xlo <= 0 && xhi >= 31));
+  const int x = xb + lane;
+  const int lo_raw = d_lo * 16;
+  int valid_count = 0;
+  const int yend = min(yb + SB_RS, H);
+  for (int y = yb; y < yend; ++y) {
+    if (y > yb) {  // slide the window down one row: + row y+HW, - row y-HW-1
+      const int slot = (y - yb - 1) % NR;
+      uint32_t a[SB_NCW];
+      ad_row(y + HW, a);
+#pragma unroll
+      for (int g = 0; g < SB_NCW; ++g) {
+        uint32_t* rs = ring + (slot * SB_NCW + g) * 32 + lane;
+        const uint32_t o = *rs;
+        *rs = a[g];
+        V[2 * g] = V[2 * g] + __byte_perm(a[g], 0u, 0x4140) - __byte_perm(o, 0u, 0x4140);
+        V[2 * g + 1] = V[2 * g + 1] + __byte_perm(a[g], 0u, 0x4342) - __byte_perm(o, 0u, 0x4342);
+      }
+      grad += tex_row(y + HW) - tex_row(y - HW - 1);
+    }
+    // ---- row box sums over (x, x+16) pairs; AD column c = x + 4 (+16)
+    uint32_t Vh[16 + 2 * HW];  // Vh[j] = (V(j - HW + 4), V(j - HW + 20))
+#pragma unroll
+    for (int j = 0; j < 16 + 2 * HW; ++j) {
+      const int c = j - HW + 4;
+      Vh[j] = __byte_perm(V[c >> 1], V[(c >> 1) + 8], (c & 1) ? 0x7632 : 0x5410);
+    }
+    uint32_t S = 0;
+#pragma unroll
+    for (int j = 0; j < 2 * HW + 1; ++j) S += Vh[j];
+    const uint32_t kbits = (k < nd) ? (uint32_t)k : SB_INF;
+#pragma unroll
+    for (int xi = 0; xi < 16; ++xi) {
+      if (xi > 0) S = S + Vh[xi + 2 * HW] - Vh[xi - 1];
+      uint32_t k0 = ((S << 5) & 0x1FFFE0u) | kbits;  // pixel xi
+      uint32_t k1 = ((S >> 11) & 0x1FFFE0u) | kbits;  // pixel xi + 16
+      if (!all_ev) {
+        if (xi < xlo || xi > xhi) k0 = SB_INF;
+        if (xi + 16 < xlo || xi + 16 > xhi) k1 = SB_INF;
+      }
+      tile[xi * SB_TP + k] = k0;
+      tile[(xi + 16) * SB_TP + k] = k1;
+    }
+    __syncwarp();
+    // ---- per-pixel argmin: lane = pixel xb + lane
+    uint32_t* row = tile + lane * SB_TP;
+    uint32_t bk = SB_INF;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const uint4 v = *reinterpret_cast<const uint4*>(row + 4 * q);
+      bk = min(min(bk, v.x), min(v.y, min(v.z, v.w)));
+    }
+    int out = kInvalid;
+    const bool defined = x < W && x >= HW && x < W - HW && y >= HW && y < H - HW && !((double)grad < tex);
+    if (bk != SB_INF) {
+      const int bi = (int)(bk & 31u);
+      const uint32_t vm = bi >= 1 ? row[bi - 1] : SB_INF;
+      const uint32_t vp = bi + 1 < 32 ? row[bi + 1] : SB_INF;
+      // second best over |i - bi| > 1
+      if (bi >= 1) row[bi - 1] = SB_INF;
+      row[bi] = SB_INF;
+      if (bi + 1 < 32) row[bi + 1] = SB_INF;
+      uint32_t sk = SB_INF;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const uint4 v = *reinterpret_cast<const uint4*>(row + 4 * q);
+        sk = min(min(sk, v.x), min(v.y, min(v.z, v.w)));
+      }
+      if (defined) {
+        const int best = (int)(bk >> 5);
+        bool ok = true;
+        if (sk != SB_INF && __dmul_rn((double)best, __dadd_rn(1.0, __ddiv_rn(uniq, 100.0))) >= (double)(sk >> 5))
+          ok = false;
+        if (ok) {
+          double d_hat = (double)(d_lo + bi);
+          if (bi > 0 && bi + 1 < nd && vm != SB_INF && vp != SB_INF)
+            d_hat = __dadd_rn(d_hat, subpix((double)(vm >> 5), (double)best, (double)(vp >> 5)));
+          long long r = llround(__dmul_rn(d_hat, 16.0));
+          const long long rlo = (long long)d_lo * 16, rhi = (long long)(d_lo + nd) * 16 - 1;
+          r = r < rlo ? rlo : (r > rhi ? rhi : r);
+          out = (int)r;
+        }
+      }
+    }
+    if (x < W) {
+      if (raw) raw[((int64_t)frame * n_delta + kd) * W * H + (int64_t)y * W + x] = (int16_t)out;
+      if (out != kInvalid && out > lo_raw) ++valid_count;
+    }
+    __syncwarp();
+  }
+  if (counts) {
+    valid_count = __reduce_add_sync(0xffffffffu, valid_count);
+    if (lane == 0 && valid_count)
+      atomicAdd((unsigned long long*)&counts[(int64_t)frame * n_delta + kd], (unsigned long long)valid_count);
+  }
+}
+
+template <int HW>
+static cudaError_t launch_simd(const uint8_t* left, const uint8_t* right, int n_frames, int64_t stride, int pitch,
+                               int img_h, int w, int h, int x0, int y0, int delta_min, int n_delta, rg_bm_params p,
+                               int16_t* raw, int64_t* counts, cudaStream_t s) {
+  // bands whose reads stay in [row start, row start + pitch): left edge of the
+  // widest disparity, right edge of the smallest one (+ realignment slack)
+  const int bands = (w + 31) / 32;
+  const int d_lo = p.min_disparity, d_max = p.min_disparity + p.num_disparities - 1;
+  auto in_row = [&](int b) {
+    const int lcol = x0 + 32 * b - 4;
+    const int lo = std::min(lcol, lcol - d_max), hi = std::max(lcol, lcol - d_lo);
+    return lo >= 0 && ((hi >> 2) + SB_NCW) * 4 + 3 <= pitch - 1;
+  };
+  int b0 = 0;
+  while (b0 < bands && !in_row(b0)) ++b0;
+  int b1 = b0;
+  while (b1 < bands && in_row(b1)) ++b1;
+  cudaError_t e = launch_lanes<HW, 1>(left, right, n_frames, stride, pitch, img_h, w, h, x0, y0, delta_min, n_delta,
+                                      p, raw, counts, s, b0, b1);
+  if (e != cudaSuccess || b1 <= b0) return e;
+  static bool attr = false;
+  if (!attr) {
+    e = cudaFuncSetAttribute(bm_simd_kernel<HW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb_smem<HW>());
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  dim3 grid((b1 - b0 + SB_W - 1) / SB_W, (h + SB_RS - 1) / SB_RS, n_frames * n_delta);
+  bm_simd_kernel<HW><<<grid, SB_W * 32, sb_smem<HW>(), s>>>(left, right, stride, pitch, img_h, w, h, x0, y0,
+                                                             delta_min, n_delta, d_lo, p.num_disparities,
+                                                             p.texture_threshold, p.uniqueness_ratio, raw, counts,
+                                                             b0, b1);
   return cudaGetLastError();
 }
 
@@ -450,6 +698,15 @@ cudaError_t launch_bm(const uint8_t* left, const uint8_t* right, int n_frames, i
   if (n_frames <= 0 || n_delta <= 0) return cudaSuccess;
   const int hw = p.block_size / 2;
   const int dpl = (p.num_disparities + 31) / 32;
+  const bool aligned = pitch % 4 == 0 && stride % 4 == 0 && reinterpret_cast<uintptr_t>(left) % 4 == 0 &&
+                       reinterpret_cast<uintptr_t>(right) % 4 == 0;
+  if (getenv("RG_BM_LEGACY") == nullptr && getenv("RG_BM_NOSIMD") == nullptr && aligned && hw >= 1 && hw <= 4 &&
+      p.num_disparities <= 32) {
+#define RG_BM_SIMD(HW) \
+  if (hw == HW) return launch_simd<HW>(left, right, n_frames, stride, pitch, img_h, w, h, x0, y0, delta_min, n_delta, p, raw, counts, s);
+    RG_BM_SIMD(1) RG_BM_SIMD(2) RG_BM_SIMD(3) RG_BM_SIMD(4)
+#undef RG_BM_SIMD
+  }
   if (getenv("RG_BM_LEGACY") == nullptr && hw >= 1 && hw <= 4 && dpl <= 2) {
 #define RG_BM_CASE(HW, DPL)                                                                             \
   if (hw == HW && dpl == DPL)                                                                            \

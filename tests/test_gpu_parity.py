@@ -226,6 +226,22 @@ def test_bm_disparity_matches_oracle(ctx, orc, nd, bs, dmin, ds, tex, uniq):
         assert st == 0 and np.array_equal(got, want)
 
 
+@pytest.mark.parametrize("nd,bs,dmin,tex,uniq", [(32, 3, -8, 5, 5), (32, 7, 4, 20, 25), (31, 9, 0, 10, 10),
+                                                 (8, 3, 0, 0, 0), (17, 5, -20, 40, 15), (32, 9, -4, 10, 10)])
+def test_bm_simd_path_matches_oracle(ctx, orc, nd, bs, dmin, tex, uniq):
+    """Wide frames so most bands take the byte-SIMD kernel (nd <= 32, bs <= 9)."""
+    rng = np.random.default_rng(nd * 7 + bs + dmin)
+    sc = S.SceneConfig(width=320, height=90, background_contrast=90, seed=nd + bs)
+    L, _ = S.render_stereo_pair(sc)
+    R = np.ascontiguousarray(np.roll(L, -7, axis=1))
+    R[::7] = rand_img(rng, R[::7].shape[0], 320)  # some rows unmatched
+    for a, b in ((L, R), (rand_img(rng, 70, 300), rand_img(rng, 70, 300))):
+        p = rg.BmParams(nd, bs, dmin, tex, uniq, 1)
+        got = rg.bm_disparity(a, b, p, ctx=ctx)
+        st, want = orc.bm(a, b, p.to_c())
+        assert st == 0 and np.array_equal(got, want)
+
+
 @pytest.mark.parametrize("voff", [-3, 0, 2])
 def test_auto_rect_search_matches_oracle(ctx, orc, voff):  # test_autorect.cpp:36-42
     sc = S.SceneConfig(objects=[S.SceneObject(id=1, position=(30.0, 0.0, 1.5), texture_seed=11)],
