@@ -423,18 +423,29 @@ static cudaError_t launch_lanes(const uint8_t* left, const uint8_t* right, int n
 // Only bands whose byte reads stay inside the image rows are run here (the
 // launcher computes that range); the others run bm_lanes_kernel.
 constexpr int SB_W = 4;     // warps (bands) per CTA
-constexpr int SB_RS = 32;   // rows per warp strip
+#ifndef RG_BM_RS
+#define RG_BM_RS 32
+#endif
+constexpr int SB_RS = RG_BM_RS;  // rows per warp strip
 constexpr int SB_NCW = 10;  // AD words per row: columns xb-4 .. xb+35
 constexpr int SB_TP = 36;   // transpose tile pitch (words)
 constexpr uint32_t SB_INF = 0xFFFFFFFFu;
 
-template <int HW>
-constexpr size_t sb_smem() {
-  return sizeof(uint32_t) * SB_W * ((2 * HW + 1) * SB_NCW * 32 + 32 * SB_TP);
-}
+#ifndef RG_BM_RING
+#define RG_BM_RING 0  // 1: |L-R| of the window rows kept in a smem ring; 0: recompute the leaving row
+#endif
+constexpr int SB_RINGW = RG_BM_RING ? SB_NCW : 0;
 
 template <int HW>
-__global__ void __launch_bounds__(SB_W * 32) bm_simd_kernel(
+constexpr size_t sb_smem() {
+  return sizeof(uint32_t) * SB_W * ((2 * HW + 1) * (SB_RINGW + 1) * 32 + 32 * SB_TP);
+}
+
+#ifndef RG_BM_MINB
+#define RG_BM_MINB 8
+#endif
+template <int HW, bool LA>  // LA: the band's left columns are word-aligned (x0 % 4 == 0)
+__global__ void __launch_bounds__(SB_W * 32, RG_BM_MINB) bm_simd_kernel(
     const uint8_t* __restrict__ left, const uint8_t* __restrict__ right, int64_t stride, int pitch, int img_h,
     int W, int H, int x0c, int y0c, int delta_min, int n_delta, int d_lo, int nd, double tex, double uniq,
     int16_t* __restrict__ raw, int64_t* __restrict__ counts, int band0, int band1) {
@@ -443,8 +454,9 @@ __global__ void __launch_bounds__(SB_W * 32) bm_simd_kernel(
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int band = band0 + blockIdx.x * SB_W + warp;
   if (band >= band1) return;  // warp-uniform; warps never synchronise with each other
-  uint32_t* ring = sbm + warp * (NR * SB_NCW * 32 + 32 * SB_TP);  // [NR][NCW][32]
-  uint32_t* tile = ring + NR * SB_NCW * 32;                       // [32 pixels][SB_TP]
+  uint32_t* ring = sbm + warp * (NR * (SB_RINGW + 1) * 32 + 32 * SB_TP);  // [NR][NCW][32]
+  int* tring = reinterpret_cast<int*>(ring + NR * SB_RINGW * 32);           // [NR][32] texture rows
+  uint32_t* tile = ring + NR * (SB_RINGW + 1) * 32;                        // [32 pixels][SB_TP]
   const int xb = band * 32;
   const int yb = blockIdx.y * SB_RS;
   if (yb >= H) return;
@@ -474,12 +486,13 @@ __global__ void __launch_bounds__(SB_W * 32) bm_simd_kernel(
     uint32_t lv[SB_NCW + 1], rv[SB_NCW + 1];
 #pragma unroll
     for (int g = 0; g <= SB_NCW; ++g) {
-      lv[g] = __ldg(lp + g);
+      if (!LA || g < SB_NCW) lv[g] = __ldg(lp + g);
       rv[g] = __ldg(rp + g);
     }
 #pragma unroll
     for (int g = 0; g < SB_NCW; ++g)
-      a[g] = __vabsdiffu4(__funnelshift_r(lv[g], lv[g + 1], lsh), __funnelshift_r(rv[g], rv[g + 1], rsh));
+      a[g] = __vabsdiffu4(LA ? lv[g] : __funnelshift_r(lv[g], lv[g + 1], lsh),
+                          __funnelshift_r(rv[g], rv[g + 1], rsh));
   };
   // texture: 8 adjacent |diffs| of row yr around pixel x = xb + lane (columns
   // x-4 .. x+4), window columns x-HW .. x+HW only
@@ -504,11 +517,13 @@ __global__ void __launch_bounds__(SB_W * 32) bm_simd_kernel(
     ad_row(yb - HW + r, a);
 #pragma unroll
     for (int g = 0; g < SB_NCW; ++g) {
-      ring[(r * SB_NCW + g) * 32 + lane] = a[g];
+      if (RG_BM_RING) ring[(r * SB_RINGW + g) * 32 + lane] = a[g];
       V[2 * g] += __byte_perm(a[g], 0u, 0x4140);
       V[2 * g + 1] += __byte_perm(a[g], 0u, 0x4342);
     }
-    grad += tex_row(yb - HW + r);
+    const int tr = tex_row(yb - HW + r);
+    tring[r * 32 + lane] = tr;
+    grad += tr;
   }
   // evaluable pixels of this lane's d: x - d - HW >= 0 && x - d + HW < W (bm.hpp:61-64)
   const int xlo = dk + HW - xb, xhi = W - 1 - HW + dk - xb;  // band-relative
@@ -520,17 +535,25 @@ __global__ void __launch_bounds__(SB_W * 32) bm_simd_kernel(
   for (int y = yb; y < yend; ++y) {
     if (y > yb) {  // slide the window down one row: + row y+HW, - row y-HW-1
       const int slot = (y - yb - 1) % NR;
-      uint32_t a[SB_NCW];
+      uint32_t a[SB_NCW], ao[SB_NCW];
       ad_row(y + HW, a);
+      if (!RG_BM_RING) ad_row(y - HW - 1, ao);
 #pragma unroll
       for (int g = 0; g < SB_NCW; ++g) {
-        uint32_t* rs = ring + (slot * SB_NCW + g) * 32 + lane;
-        const uint32_t o = *rs;
-        *rs = a[g];
+        uint32_t o;
+        if (RG_BM_RING) {
+          uint32_t* rs = ring + (slot * SB_RINGW + g) * 32 + lane;
+          o = *rs;
+          *rs = a[g];
+        } else {
+          o = ao[g];
+        }
         V[2 * g] = V[2 * g] + __byte_perm(a[g], 0u, 0x4140) - __byte_perm(o, 0u, 0x4140);
         V[2 * g + 1] = V[2 * g + 1] + __byte_perm(a[g], 0u, 0x4342) - __byte_perm(o, 0u, 0x4342);
       }
-      grad += tex_row(y + HW) - tex_row(y - HW - 1);
+      const int tr = tex_row(y + HW);
+      grad += tr - tring[slot * 32 + lane];
+      tring[slot * 32 + lane] = tr;
     }
     // ---- row box sums over (x, x+16) pairs; AD column c = x + 4 (+16)
     uint32_t Vh[16 + 2 * HW];  // Vh[j] = (V(j - HW + 4), V(j - HW + 20))
@@ -543,17 +566,24 @@ __global__ void __launch_bounds__(SB_W * 32) bm_simd_kernel(
 #pragma unroll
     for (int j = 0; j < 2 * HW + 1; ++j) S += Vh[j];
     const uint32_t kbits = (k < nd) ? (uint32_t)k : SB_INF;
+    if (all_ev) {  // every (pixel, d) of the band is evaluable: no masks
 #pragma unroll
-    for (int xi = 0; xi < 16; ++xi) {
-      if (xi > 0) S = S + Vh[xi + 2 * HW] - Vh[xi - 1];
-      uint32_t k0 = ((S << 5) & 0x1FFFE0u) | kbits;  // pixel xi
-      uint32_t k1 = ((S >> 11) & 0x1FFFE0u) | kbits;  // pixel xi + 16
-      if (!all_ev) {
+      for (int xi = 0; xi < 16; ++xi) {
+        if (xi > 0) S = S + Vh[xi + 2 * HW] - Vh[xi - 1];
+        tile[xi * SB_TP + k] = ((S << 5) & 0x1FFFE0u) | kbits;           // pixel xi
+        tile[(xi + 16) * SB_TP + k] = ((S >> 11) & 0x1FFFE0u) | kbits;   // pixel xi + 16
+      }
+    } else {
+#pragma unroll
+      for (int xi = 0; xi < 16; ++xi) {
+        if (xi > 0) S = S + Vh[xi + 2 * HW] - Vh[xi - 1];
+        uint32_t k0 = ((S << 5) & 0x1FFFE0u) | kbits;
+        uint32_t k1 = ((S >> 11) & 0x1FFFE0u) | kbits;
         if (xi < xlo || xi > xhi) k0 = SB_INF;
         if (xi + 16 < xlo || xi + 16 > xhi) k1 = SB_INF;
+        tile[xi * SB_TP + k] = k0;
+        tile[(xi + 16) * SB_TP + k] = k1;
       }
-      tile[xi * SB_TP + k] = k0;
-      tile[(xi + 16) * SB_TP + k] = k1;
     }
     __syncwarp();
     // ---- per-pixel argmin: lane = pixel xb + lane
@@ -609,7 +639,7 @@ __global__ void __launch_bounds__(SB_W * 32) bm_simd_kernel(
   }
 }
 
-template <int HW>
+template <int HW, bool LA>
 static cudaError_t launch_simd(const uint8_t* left, const uint8_t* right, int n_frames, int64_t stride, int pitch,
                                int img_h, int w, int h, int x0, int y0, int delta_min, int n_delta, rg_bm_params p,
                                int16_t* raw, int64_t* counts, cudaStream_t s) {
@@ -631,12 +661,13 @@ static cudaError_t launch_simd(const uint8_t* left, const uint8_t* right, int n_
   if (e != cudaSuccess || b1 <= b0) return e;
   static bool attr = false;
   if (!attr) {
-    e = cudaFuncSetAttribute(bm_simd_kernel<HW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb_smem<HW>());
+    e = cudaFuncSetAttribute(bm_simd_kernel<HW, LA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sb_smem<HW>());
     if (e != cudaSuccess) return e;
     attr = true;
   }
   dim3 grid((b1 - b0 + SB_W - 1) / SB_W, (h + SB_RS - 1) / SB_RS, n_frames * n_delta);
-  bm_simd_kernel<HW><<<grid, SB_W * 32, sb_smem<HW>(), s>>>(left, right, stride, pitch, img_h, w, h, x0, y0,
+  bm_simd_kernel<HW, LA><<<grid, SB_W * 32, sb_smem<HW>(), s>>>(left, right, stride, pitch, img_h, w, h, x0, y0,
                                                              delta_min, n_delta, d_lo, p.num_disparities,
                                                              p.texture_threshold, p.uniqueness_ratio, raw, counts,
                                                              b0, b1);
@@ -702,8 +733,12 @@ cudaError_t launch_bm(const uint8_t* left, const uint8_t* right, int n_frames, i
                        reinterpret_cast<uintptr_t>(right) % 4 == 0;
   if (getenv("RG_BM_LEGACY") == nullptr && getenv("RG_BM_NOSIMD") == nullptr && aligned && hw >= 1 && hw <= 4 &&
       p.num_disparities <= 32) {
-#define RG_BM_SIMD(HW) \
-  if (hw == HW) return launch_simd<HW>(left, right, n_frames, stride, pitch, img_h, w, h, x0, y0, delta_min, n_delta, p, raw, counts, s);
+#define RG_BM_SIMD(HW)                                                                                          \
+  if (hw == HW)                                                                                                 \
+    return x0 % 4 == 0 ? launch_simd<HW, true>(left, right, n_frames, stride, pitch, img_h, w, h, x0, y0,       \
+                                               delta_min, n_delta, p, raw, counts, s)                           \
+                       : launch_simd<HW, false>(left, right, n_frames, stride, pitch, img_h, w, h, x0, y0,      \
+                                                delta_min, n_delta, p, raw, counts, s);
     RG_BM_SIMD(1) RG_BM_SIMD(2) RG_BM_SIMD(3) RG_BM_SIMD(4)
 #undef RG_BM_SIMD
   }
