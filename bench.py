@@ -374,6 +374,34 @@ def main():
     except Exception as e:  # pragma: no cover
         rect = {"error": str(e)}
 
+    # ---- the full TEMPLATE_MATCHER frame loop (rg_range_sequence): offset
+    # search on every uncorrected pair (RectSearchConfig defaults: delta -3..3,
+    # central half, 32 disparities) + filter scan + corrected ranging
+    seq = None
+    try:
+        nsf = min(F, 64)
+        rect_cfg = rg.RectSearchConfig()
+        seq_out = torch.zeros(nsf * eng.out_stride * OUT_DTYPE.itemsize, dtype=torch.uint8, device=dev)
+        seq_cnt = torch.zeros(nsf, dtype=torch.int32, device=dev)
+        seq_offs = torch.from_numpy(pack_detections([dets] * nsf)[1]).to(dev)
+        for _ in range(2):
+            eng.range_sequence(dL[:nsf], dR[:nsf], d_dets, seq_offs, seq_out, seq_cnt, rect=rect_cfg,
+                               stream=stream.cuda_stream)
+        torch.cuda.synchronize()
+        reps = 3
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            eng.range_sequence(dL[:nsf], dR[:nsf], d_dets, seq_offs, seq_out, seq_cnt, rect=rect_cfg,
+                               stream=stream.cuda_stream)
+        torch.cuda.synchronize()
+        sdt = (time.perf_counter() - t0) / reps
+        seq = {"config": f"C2 frames, {nsf} per call: offset search delta -3..3 on the central half (BM 32 disp, "
+                         "9x9) + filter_offset scan + ranging of the rect-corrected pairs (rg_range_sequence)",
+               "frames_per_sec": nsf / sdt, "boxes_per_sec": int(seq_cnt.sum().item()) / sdt,
+               "ms_per_frame": 1000.0 * sdt / nsf}
+    except Exception as e:  # pragma: no cover
+        seq = {"error": str(e)}
+
     # ---- roofline of the dominant kernel (stage times from CUDA events on our stream)
     hbm_peak, sm_max, peak_kind = peaks()
     census_ms = stage_ms[0] / max(stage_launches[0], 1)
@@ -432,6 +460,7 @@ def main():
                                               zip(["census", "plan", "match", "aggregate"], stage_ms[:4])}},
             "hamming_evals_per_frame": evals / max(F * args.steps, 1),
             "autorect": rect,
+            "sequence": seq,
             "clocks": clk,
             "parity_spot_check_vs_oracle": spot,
             "cpu_baseline": cpu,
