@@ -68,7 +68,7 @@ __global__ void __launch_bounds__(TPB) census_frames_kernel(
     if (x >= w || y >= h) continue;
     uint32_t code = 0;
     if (x >= 2 && y >= 2 && x < w - 2 && y < h - 2) code = census_window(&tile[ty + 2][tx + 2], TX + 8);
-    if (s31 && code) code = (code & 0x01FFFFFFu) | 0x80000000u;  // internal layout
+    if (s31 && code) code = (code & 0x01FFFFFFu) | kInternalHigh;  // internal layout
     full[(int64_t)y * gf.pitch + x] = code;
     if (red && ix >= 0) {
       const int iy = inv_y[y];
@@ -92,7 +92,15 @@ __global__ void __launch_bounds__(TPB) census_frames_kernel(
 // memory (6 byte permutes per 4 entries from raw image words, all loads of a
 // thread in flight at once); each warp then computes a 16-row strip reading
 // its 5-row window straight from V (2 LDS.128 per row).
-constexpr int C2_TX = 128;                        // tile columns: 32 lanes x 4 pixel pairs
+#ifndef RG_C2_MASK
+#define RG_C2_MASK 0xFFFFFFFFu
+#endif
+#ifndef RG_C2_TX
+#define RG_C2_TX 128
+#endif
+constexpr int C2_TX = RG_C2_TX;                   // tile columns: groups of 32 lanes x 4 pixel pairs
+constexpr int C2_G = C2_TX / 128;                 // 128-column groups per warp row
+static_assert(C2_TX % 128 == 0, "tile width");
 #ifndef RG_C2_WARPS
 #define RG_C2_WARPS 8
 #endif
@@ -126,9 +134,9 @@ template <bool S31>  // S31: internal layout, sentinel moved from bit 25 to bit 
 __device__ __forceinline__ void c2_assemble(uint32_t g0, uint32_t g1, uint32_t g2, uint32_t& lo,
                                             uint32_t& hi) {
   const uint32_t t = __byte_perm(g2, g1, 0x6240);      // [B2 lo, B1 lo, B2 hi, B1 hi]
-  if (S31) {  // g0 negative: its high byte is 0xE6|b8 -> 0x80|b8
-    lo = __byte_perm(t, g0, 0x5410) & 0x81FFFFFFu;
-    hi = __byte_perm(t, g0, 0x7632) & 0x81FFFFFFu;
+  if (S31) {  // g0 negative: its high byte is already 0xE6|b8 (kInternalHigh | bit 24)
+    lo = __byte_perm(t, g0, 0x5410) & RG_C2_MASK;
+    hi = __byte_perm(t, g0, 0x7632) & RG_C2_MASK;
   } else {
     lo = __byte_perm(t, g0, 0x5410) & 0x03FFFFFFu;     // g0 lo half: 0x66|b8 -> 0x2|b8
     hi = __byte_perm(t, g0, 0x7632) & 0x03FFFFFFu;
@@ -166,40 +174,43 @@ __device__ __forceinline__ void c2_strip(const uint32_t* __restrict__ V, uint32_
                                          uint32_t* __restrict__ red, const PadGeom& gf, const PadGeom& gs,
                                          int x0, int y0, int w, int h) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int xl = x0 + 4 * lane;  // first column of this lane
   const int pr0 = wid * C2_PR;
-  const uint32_t* vbase = V + C2_VOFF + 4 * lane;  // V index of column xl - 2
-  // output pointers advance by whole pair rows (no per-row 64-bit index math)
-  uint32_t* o = full + (int64_t)(y0 + 2 * pr0) * gf.pitch + xl;
-  uint32_t* ro = red ? red + (int64_t)((y0 >> 1) + pr0) * gs.pitch + (xl >> 1) : full;  // full: never written
   const int64_t ostep = 2 * (int64_t)gf.pitch;
 #pragma unroll
-  for (int p = pr0; p < pr0 + C2_PR; ++p, o += ostep, ro += gs.pitch) {
-    const int y = y0 + 2 * p;
-    if (EDGE && y >= h) break;
-    uint32_t win[5][8];
+  for (int g = 0; g < C2_G; ++g) {
+    const int xl = x0 + 128 * g + 4 * lane;  // first column of this lane in group g
+    const uint32_t* vbase = V + C2_VOFF + 128 * g + 4 * lane;  // V index of column xl - 2
+    // output pointers advance by whole pair rows (no per-row 64-bit index math)
+    uint32_t* o = full + (int64_t)(y0 + 2 * pr0) * gf.pitch + xl;
+    uint32_t* ro = red ? red + (int64_t)((y0 >> 1) + pr0) * gs.pitch + (xl >> 1) : full;  // full: never written
 #pragma unroll
-    for (int j = 0; j < 5; ++j) {
-      const uint4* src = reinterpret_cast<const uint4*>(vbase + (2 * p + j) * C2_VW);
-      const uint4 a = src[0], b = src[1];
-      win[j][0] = a.x; win[j][1] = a.y; win[j][2] = a.z; win[j][3] = a.w;
-      win[j][4] = b.x; win[j][5] = b.y; win[j][6] = b.z; win[j][7] = b.w;
-    }
-    uint32_t lo[4], hi[4];
-    c2_codes<S31>(win, lo, hi);
-    if (EDGE) {
-      if (xl >= w) continue;
+    for (int p = pr0; p < pr0 + C2_PR; ++p, o += ostep, ro += gs.pitch) {
+      const int y = y0 + 2 * p;
+      if (EDGE && y >= h) break;
+      uint32_t win[5][8];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const bool xin = xl + q >= 2 && xl + q <= w - 3;
-        if (!(xin && y >= 2 && y <= h - 3)) lo[q] = 0u;
-        if (!(xin && y + 1 >= 2 && y + 1 <= h - 3)) hi[q] = 0u;
+      for (int j = 0; j < 5; ++j) {
+        const uint4* src = reinterpret_cast<const uint4*>(vbase + (2 * p + j) * C2_VW);
+        const uint4 a = src[0], b = src[1];
+        win[j][0] = a.x; win[j][1] = a.y; win[j][2] = a.z; win[j][3] = a.w;
+        win[j][4] = b.x; win[j][5] = b.y; win[j][6] = b.z; win[j][7] = b.w;
       }
+      uint32_t lo[4], hi[4];
+      c2_codes<S31>(win, lo, hi);
+      if (EDGE) {
+        if (xl >= w) continue;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const bool xin = xl + q >= 2 && xl + q <= w - 3;
+          if (!(xin && y >= 2 && y <= h - 3)) lo[q] = 0u;
+          if (!(xin && y + 1 >= 2 && y + 1 <= h - 3)) hi[q] = 0u;
+        }
+      }
+      *reinterpret_cast<uint4*>(o) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+      if (!EDGE || y + 1 < h) *reinterpret_cast<uint4*>(o + gf.pitch) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+      // reduced raster = codes at even (x, y): (x/2, y/2)
+      if (red) *reinterpret_cast<uint2*>(ro) = make_uint2(lo[0], lo[2]);
     }
-    *reinterpret_cast<uint4*>(o) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
-    if (!EDGE || y + 1 < h) *reinterpret_cast<uint4*>(o + gf.pitch) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-    // reduced raster = codes at even (x, y): (x/2, y/2)
-    if (red) *reinterpret_cast<uint2*>(ro) = make_uint2(lo[0], lo[2]);
   }
 }
 
@@ -249,11 +260,10 @@ __global__ void __launch_bounds__(C2_WARPS * 32) census_pairs_kernel(
   }
   __syncthreads();
   // ---- phase 2
-  const int lane_x = x0 + 4 * (threadIdx.x & 31);
   const int ys = y0 + 2 * (threadIdx.x >> 5) * C2_PR;
   if (ys >= h) return;
   const bool edge = x0 < 2 || x0 + C2_TX + 3 > w - 3 || ys < 2 || ys + 2 * C2_PR + 1 > h - 3;
-  if (__any_sync(0xffffffffu, edge || lane_x >= w))
+  if (__any_sync(0xffffffffu, edge))  // warp-uniform (the vote lets the compiler keep one branch)
     c2_strip<true, S31>(V, full, red, gf, gs, x0, y0, w, h);
   else
     c2_strip<false, S31>(V, full, red, gf, gs, x0, y0, w, h);

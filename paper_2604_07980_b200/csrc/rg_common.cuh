@@ -21,6 +21,13 @@ constexpr int kWindowCodes = 12288;    // smem census window (48 KB)
 constexpr int kMaxOccluders = 128;     // per-object occluder boxes kept in smem
 constexpr int kAggCapacity = 4096;     // CLOSE blocks aggregated in smem
 
+// Internal census layout of the batched pipeline: reference bits 0..24, bits
+// 25..31 = 0x73 (sign set).  A constant high part cancels in l ^ r, so Hamming
+// distances equal the reference's; the sign bit marks a defined code (0 =
+// undefined).  0xE6 is the high byte of the fp16 accumulator -(1536 + B) that
+// the fast census produces directly (census.cu).
+constexpr uint32_t kInternalHigh = 0xE6000000u;
+
 // ------------------------------------------------------------ device structs
 template <typename CT>
 struct RasterT {  // census raster in device memory
@@ -130,7 +137,7 @@ void count_launch(rg_ctx* ctx, int stage, int n = 1);
 
 // ------------------------------------------------------------ launchers
 // census (census.cu)
-// internal: batched-pipeline layout, sentinel at bit 31 instead of 25 (Hamming
+// internal: batched-pipeline layout (kInternalHigh; Hamming distances unchanged,
 // distances unchanged; lets the matcher mask undefined codes by the sign bit)
 cudaError_t launch_census_frames(const uint8_t* left, const uint8_t* right, int n_frames,
                                  int64_t frame_stride, int pitch, int w, int h,

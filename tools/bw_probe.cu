@@ -1,0 +1,89 @@
+// HBM bandwidth probe (measurement tool, not part of the library): achievable
+// B200 bandwidth for the access mixes of the census kernel.  Streams 128-bit
+// accesses over buffers far larger than L2, CUDA-event timed, best of 10.
+//   write  : stores only                     (census is ~81 % writes)
+//   read   : loads only
+//   copy   : 1 load : 1 store                (the MEASURED_PEAKS "hbm_gbs" mix)
+//   census : 1 load : 5 stores  (per pixel 1 B read, 4 B full + 1 B reduced written)
+// Build: nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o tools/bw_probe tools/bw_probe.cu
+#include <cstdint>
+#include <cstdio>
+#include <cuda_runtime.h>
+
+__global__ void k_write(uint4* __restrict__ o, size_t n, uint32_t v) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    o[i] = make_uint4(v, v ^ (uint32_t)i, v, (uint32_t)i);
+}
+__global__ void k_read(const uint4* __restrict__ a, size_t n, uint32_t* sink) {
+  uint32_t acc = 0;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const uint4 x = __ldg(a + i);
+    acc ^= x.x ^ x.y ^ x.z ^ x.w;
+  }
+  if (acc == 0x12345678u) *sink = acc;
+}
+__global__ void k_copy(const uint4* __restrict__ a, uint4* __restrict__ o, size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    o[i] = __ldg(a + i);
+}
+// one 16-B read feeds five 16-B writes (the census byte ratio)
+__global__ void k_mix(const uint4* __restrict__ a, uint4* __restrict__ o, size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const uint4 x = __ldg(a + i);
+#pragma unroll
+    for (int k = 0; k < 5; ++k) o[(size_t)k * n + i] = make_uint4(x.x + k, x.y, x.z, x.w);
+  }
+}
+
+// the census pattern: one read stream, a 4x contiguous write stream (full
+// raster) and a 1x write stream (reduced raster)
+__global__ void k_mix2(const uint4* __restrict__ a, uint4* __restrict__ o1, uint4* __restrict__ o2, size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const uint4 x = __ldg(a + i);
+    const size_t base = (i / 32) * 128 + (i % 32);  // warp-contiguous 4 x 512 B
+#pragma unroll
+    for (int k = 0; k < 4; ++k) o1[base + 32 * k] = make_uint4(x.x + k, x.y, x.z, x.w);
+    o2[i] = x;
+  }
+}
+
+int main() {
+  const size_t n = (size_t)1 << 28;  // 4 GiB of uint4 per buffer
+  uint4 *a, *o;
+  uint32_t* sink;
+  if (cudaMalloc(&a, n * 16) != cudaSuccess || cudaMalloc(&o, 5 * n * 16) != cudaSuccess ||
+      cudaMalloc(&sink, 4) != cudaSuccess) {
+    printf("{\"error\": \"alloc\"}\n");
+    return 1;
+  }
+  cudaMemset(a, 1, n * 16);
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const int grid = sms * 8, block = 256;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  auto best = [&](auto launch, double bytes) {
+    float b = 1e30f;
+    for (int r = 0; r < 12; ++r) {
+      cudaEventRecord(e0);
+      launch();
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms = 0;
+      cudaEventElapsedTime(&ms, e0, e1);
+      if (r >= 2 && ms < b) b = ms;
+    }
+    return bytes / (b / 1e3) / 1e9;
+  };
+  const double B = (double)n * 16;
+  const double w = best([&] { k_write<<<grid, block>>>(o, n, 7u); }, B);
+  const double r = best([&] { k_read<<<grid, block>>>(a, n, sink); }, B);
+  const double c = best([&] { k_copy<<<grid, block>>>(a, o, n); }, 2 * B);
+  const double m = best([&] { k_mix<<<grid, block>>>(a, o, n / 5); }, 6 * B / 5);
+  const double m2 = best([&] { k_mix2<<<grid, block>>>(a, o, o + 4 * (n / 5), n / 5); }, 6 * B / 5);
+  printf("{\"write_gbs\": %.1f, \"read_gbs\": %.1f, \"copy_gbs\": %.1f, \"census_mix_1r5w_gbs\": %.1f, "
+         "\"census_mix_1r_4w_1w_gbs\": %.1f, \"buffer_gib\": 4, \"access\": \"uint4 grid-stride, %d CTAs x %d\"}\n",
+         w, r, c, m, m2, grid, block);
+  return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}
