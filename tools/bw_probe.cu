@@ -8,6 +8,7 @@
 // Build: nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o tools/bw_probe tools/bw_probe.cu
 #include <cstdint>
 #include <cstdio>
+#include <algorithm>
 #include <cuda_runtime.h>
 
 __global__ void k_write(uint4* __restrict__ o, size_t n, uint32_t v) {
@@ -47,6 +48,24 @@ __global__ void k_mix2(const uint4* __restrict__ a, uint4* __restrict__ o1, uint
   }
 }
 
+// writes in the census tile pattern: CTA = 128-px x 64-row tile of a row-major
+// raster (pitch 2440 codes), warp = 8 rows x 512 B, plus a half-res raster
+// (4 rows x 256 B per warp); tiles in x fastest, then y, then images
+__global__ void k_tilewrite(uint4* __restrict__ o, int pitch_u4, int tiles_x, int tiles_y, size_t img_u4,
+                            uint2* __restrict__ r, int rpitch_u2, size_t rimg_u2) {
+  const int t = blockIdx.x, img = t / (tiles_x * tiles_y), rem = t % (tiles_x * tiles_y);
+  const int ty = rem / tiles_x, tx = rem % tiles_x;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint4* base = o + img * img_u4 + (size_t)(ty * 64 + w * 8) * pitch_u4 + tx * 32 + lane;
+  uint2* rb = r + img * rimg_u2 + (size_t)(ty * 32 + w * 4) * rpitch_u2 + tx * 32 + lane;
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    base[(2 * p) * (size_t)pitch_u4] = make_uint4(p, lane, w, t);
+    base[(2 * p + 1) * (size_t)pitch_u4] = make_uint4(p, lane, w, t);
+    rb[p * (size_t)rpitch_u2] = make_uint2(p, t);
+  }
+}
+
 int main() {
   const size_t n = (size_t)1 << 28;  // 4 GiB of uint4 per buffer
   uint4 *a, *o;
@@ -82,6 +101,15 @@ int main() {
   const double c = best([&] { k_copy<<<grid, block>>>(a, o, n); }, 2 * B);
   const double m = best([&] { k_mix<<<grid, block>>>(a, o, n / 5); }, 6 * B / 5);
   const double m2 = best([&] { k_mix2<<<grid, block>>>(a, o, o + 4 * (n / 5), n / 5); }, 6 * B / 5);
+  // 2 x 256 images of 1920x1080 codes in a 2440-wide padded raster
+  const int pitch_u4 = 2440 / 4, tiles_x = 15, tiles_y = 17, rows = 1088 + 4;
+  const size_t img_u4 = (size_t)pitch_u4 * rows, rimg_u2 = (size_t)(1220 / 2) * 548;
+  const int imgs = (int)std::min<size_t>(512, (5 * n) / (img_u4 + rimg_u2 / 2 + 1));
+  const double tw = best([&] { k_tilewrite<<<imgs * tiles_x * tiles_y, 256>>>(o, pitch_u4, tiles_x, tiles_y, img_u4,
+                                                                              reinterpret_cast<uint2*>(o + imgs * img_u4),
+                                                                              1220 / 2, rimg_u2); },
+                         (double)imgs * (1920.0 * 1088 * 4 + 960.0 * 544 * 4));
+  printf("{\"census_tile_write_pattern_gbs\": %.1f, \"images\": %d}\n", tw, imgs);
   printf("{\"write_gbs\": %.1f, \"read_gbs\": %.1f, \"copy_gbs\": %.1f, \"census_mix_1r5w_gbs\": %.1f, "
          "\"census_mix_1r_4w_1w_gbs\": %.1f, \"buffer_gib\": 4, \"access\": \"uint4 grid-stride, %d CTAs x %d\"}\n",
          w, r, c, m, m2, grid, block);
