@@ -253,7 +253,7 @@ rg_status enqueue_pipeline(rg_ctx* ctx, const FrameJob& J, const rg_ranger_confi
   const bool wide = cfg.census_9x7 != 0;
   const size_t csz = wide ? sizeof(unsigned long long) : sizeof(uint32_t);
   const int rx = wide ? 4 : 2, ry = wide ? 3 : 2;
-  if ((sizeof(int2) + 2 * csz) * (size_t)maxp * 8 > kSmemLimit)
+  if ((sizeof(int2) + 2 * csz) * (size_t)(maxp + 1) * 8 > kSmemLimit)
     return set_err(ctx, RG_EINVAL, "RangerConfig: blocks too large for the device matcher");
   if (wide && (J.full_l || J.scaled_l))
     return set_err(ctx, RG_EINVAL, "RangerConfig: census_9x7 cannot use a CensusCache");

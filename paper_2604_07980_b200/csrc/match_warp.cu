@@ -158,7 +158,7 @@ __device__ __forceinline__ void sweep(const VPoint<CT>* __restrict__ vp, int nv,
 #pragma unroll
     for (int c = 0; c < K; ++c) rm[c] = __ldg(a - 32 * c);
 #else
-    qn = vp[min(k + 1, nv - 1)];
+    qn = vp[k + 1];  // vp[nv] duplicates vp[nv - 1] (warp_pass), so no clamp
     const CT* a = reinterpret_cast<const CT*>(reinterpret_cast<const char*>(base) + qn.off);
 #pragma unroll
     for (int c = 0; c < K; ++c) rn[c] = __ldg(a - 32 * c);
@@ -290,9 +290,10 @@ __device__ __forceinline__ void sweep_range(
   const bool ptail = mt != 0 && mt <= TAIL;
   const int nfull = ptail ? ndx >> 5 : nch;
   const int groups = (nfull + CMAX - 1) / CMAX;
+  const int gq = groups ? nfull / groups : 0, gr = groups ? nfull - gq * groups : 0;  // balanced group sizes
   for (int dy = rg.dy_min; dy <= rg.dy_max; ++dy) {
     for (int gi = 0, c0 = 0; gi < groups; ++gi) {
-      const int k = (nfull - c0 + groups - gi - 1) / (groups - gi);
+      const int k = gq + (gi < gr ? 1 : 0);
       const CT* base = R + (int64_t)dy * g.pitch - rg.dx_min - lane - 32 * c0;
       sweep_chunks<CT, MODE>(vp, nv, base, lane, c0, k, ndx, rg.dx_min, dy, best, bkey, evals);
       c0 += k;
@@ -344,6 +345,8 @@ __device__ Pass warp_pass(
   }
   __syncwarp();
   if (nv == 0) return o;  // no contributing point anywhere: nullopt
+  if (lane == 0) vp[nv] = vp[nv - 1];  // padding read by the sweeps' one-ahead prefetch
+  __syncwarp();
   xmin = __reduce_min_sync(0xffffffffu, xmin);
   ymin = __reduce_min_sync(0xffffffffu, ymin);
   xmax = __reduce_max_sync(0xffffffffu, xmax);
@@ -449,7 +452,7 @@ __global__ void __launch_bounds__(WPB * 32, MINB) match_slots_warp_kernel(
   // skip it entirely; otherwise only planned slots inside the list exist
   if (counters[1] || slot >= min(counters[0], capacity)) return;  // warp-uniform
   // per warp: maxp sampled points + maxp valid points
-  unsigned char* wbase = wsm_raw + (size_t)warp * maxp * (sizeof(int2) + sizeof(VPoint<CT>));
+  unsigned char* wbase = wsm_raw + (size_t)warp * (maxp * sizeof(int2) + (maxp + 1) * sizeof(VPoint<CT>));
   int2* pts = reinterpret_cast<int2*>(wbase);
   VPoint<CT>* vp = reinterpret_cast<VPoint<CT>*>(wbase + sizeof(int2) * maxp);
   const Slot s = slots[slot];
@@ -526,7 +529,8 @@ cudaError_t launch_variant(const Slot* slots, int32_t* counters, int slot_capaci
                                   rg_ranger_config cfg, rg_match_result* res, rg_ranger_stats* stats,
                                   int max_points, cudaStream_t s) {
   auto kern = match_slots_warp_kernel<CT, WPB, MINB>;
-  const size_t smem = (sizeof(int2) + sizeof(VPoint<CT>)) * (size_t)max_points * WPB;
+  max_points = (max_points + 1) & ~1;  // keeps every warp's VPoint array 16-B aligned
+  const size_t smem = (sizeof(int2) * (size_t)max_points + sizeof(VPoint<CT>) * (size_t)(max_points + 1)) * WPB;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;

@@ -24,4 +24,4 @@ ctx.reset_counters(); ctx.set_profiling(True)
 for _ in range(20): eng.range_device(dL, dR, d_dets, d_offs, out, cnt, stream=st.cuda_stream)
 torch.cuda.synchronize(); ctx.set_profiling(False)
 ms, n, _ = ctx.counters()
-print(os.environ.get("RG_LIB_PATH", "base").split("/")[-2], "census ms/launch", round(ms[0] / n[0], 4), "match", round(ms[2] / n[2], 4))
+print((os.environ.get("RG_LIB_PATH") or "x/base/x").split("/")[-2], "census ms/launch", round(ms[0] / n[0], 4), "match", round(ms[2] / n[2], 4))
