@@ -139,3 +139,72 @@ def test_reference_tests_pass_on_the_gpu_path(binary):
     if binary == "acceptance_tests":
         for c in (1, 3, 4, 5, 6, 7, 13, 14):
             assert f"criterion {c:2d}: PASS" in r.stdout
+
+
+def _batch_vs_oracle(ctx, orc, L, R, D, cfg, focal=0.0, base=0.0):
+    import torch
+
+    n, h, w = L.shape
+    maxd = max(1, max(len(d) for d in D))
+    eng = FrameEngine(w, h, cfg, maxd, focal, base, ctx=ctx)
+    recs, offs = pack_detections(D)
+    dev = torch.device("cuda", 0)
+    out = torch.zeros(n * eng.out_stride * 32, dtype=torch.uint8, device=dev)
+    cnt = torch.zeros(n, dtype=torch.int32, device=dev)
+    eng.range_device(torch.from_numpy(np.ascontiguousarray(L)).to(dev), torch.from_numpy(np.ascontiguousarray(R)).to(dev),
+                     torch.from_numpy(recs.view(np.uint8)).to(dev), torch.from_numpy(offs).to(dev), out, cnt)
+    torch.cuda.synchronize()
+    o = out.cpu().numpy().reshape(n, eng.out_stride * 32)
+    for f in range(n):
+        got_n = int(cnt[f])
+        if D[f]:
+            want, _ = orc.estimate(np.ascontiguousarray(L[f]), np.ascontiguousarray(R[f]),
+                                   [_abi.Detection(d.cx, d.cy, d.w, d.h, d.class_id, d.id) for d in D[f]],
+                                   cfg.to_c(), focal, base)
+            want = b"".join(bytes(x) for x in want)
+        else:
+            want = b""
+        assert got_n * 32 == len(want), (f, got_n, len(want))
+        assert o[f, :len(want)].tobytes() == want, f
+
+
+@pytest.mark.parametrize("case", ["odd_width", "empty_frames", "degenerate_boxes", "selection_overflow",
+                                  "zero_range", "wide_range", "close_only_scale3"])
+def test_range_frames_edge_cases(ctx, orc, case):
+    """Batched path vs the oracle on the shapes the planner/census/matcher
+    special-case: non-multiple-of-4 widths (general census kernel), frames
+    without detections, boxes leaving or degenerate in the image, more boxes
+    than max_objects, one-candidate and >256-candidate search ranges, a
+    non-half close scale (gather-mapped reduced raster)."""
+    rng = np.random.default_rng(hash(case) % 1000)
+    sc, cfg = S.scene_c1(seed=81, noise=2.0)
+    L, R = S.render_stereo_pair(sc)
+    dets = S.ground_truth_detections(sc)
+    if case == "odd_width":
+        L, R = L[:, :637], R[:, :637]
+        frames = [(L, R, dets), (L, R, dets[::2])]
+    elif case == "empty_frames":
+        frames = [(L, R, []), (L, R, dets), (L, R, [])]
+    elif case == "degenerate_boxes":
+        bad = [rg.Detection(1.02, 0.5, 0.2, 0.2, 0, 900), rg.Detection(0.5, 0.5, 0.0, 0.3, 0, 901),
+               rg.Detection(-0.05, 0.1, 0.2, 0.25, 1, 902), rg.Detection(0.5, 0.999, 0.3, 0.05, 0, 903),
+               rg.Detection(0.5, 0.5, 1e-4, 1e-4, 0, 904)]
+        frames = [(L, R, dets + bad), (L, R, bad)]
+    elif case == "selection_overflow":
+        cfg.max_objects = 3
+        frames = [(L, R, dets), (L, R, list(reversed(dets)))]
+    elif case == "zero_range":
+        cfg.dx_max_far = 0
+        cfg.dx_max_close = 0
+        frames = [(L, R, dets)]
+    elif case == "wide_range":
+        cfg.dx_max_far = 300
+        cfg.dx_max_close = 600
+        frames = [(L, R, dets)]
+    else:  # close_only_scale3
+        cfg.close_scale = 3
+        cfg.tau_s = 1e9  # everything CLOSE
+        frames = [(L, R, dets)]
+    Ls = np.stack([f[0] for f in frames])
+    Rs = np.stack([f[1] for f in frames])
+    _batch_vs_oracle(ctx, orc, Ls, Rs, [f[2] for f in frames], cfg, S.F_PX, S.BASELINE_M)
