@@ -349,6 +349,36 @@ rg_status rg_auto_rect_frames(rg_ctx* ctx, const uint8_t* d_left,
                               int delta_max, const rg_bm_params* p, int32_t* d_best,
                               int64_t* d_counts, void* stream);
 
+/* ------------------------------------------------------ SGM (8f row 2) */
+
+/* SgmParams, sgm.hpp:14-19 */
+typedef struct {
+  int32_t num_disparities; /* <= 256 on the device path */
+  int32_t min_disparity;
+  int32_t p1;
+  int32_t p2;
+} rg_sgm_params;
+
+/* validate(const SgmParams&), sgm.hpp:21-28 */
+rg_status rg_validate_sgm_params(rg_ctx* ctx, const rg_sgm_params* p);
+/* sgm_disparity, sgm.hpp:118-155: census cost, 4 directional passes
+ * ({1,0},{0,1},{1,1},{-1,1}), winner-take-all + sub-pixel; raw int16 map
+ * (DisparityMap::raw, kInvalid = -32768). */
+rg_status rg_sgm_disparity(rg_ctx* ctx, const uint8_t* left, const uint8_t* right, int w, int h,
+                           const rg_sgm_params* p, int16_t* out_raw);
+/* Batched device variant: frames as in rg_frame_batch; d_raw[n_frames * w * h]. */
+rg_status rg_sgm_frames(rg_ctx* ctx, const uint8_t* d_left, const uint8_t* d_right, int n_frames,
+                        int64_t frame_stride, int pitch, int w, int h, const rg_sgm_params* p,
+                        int16_t* d_raw, void* stream);
+/* detail::sgm_cost_volume, sgm.hpp:37-56 (codes: w*h reference-layout census;
+ * cost: w*h*num_disparities bytes, [y][x][i]) */
+rg_status rg_sgm_cost_volume(rg_ctx* ctx, const uint32_t* left_codes, const uint32_t* right_codes,
+                             int w, int h, const rg_sgm_params* p, uint8_t* cost);
+/* detail::sgm_direction_pass, sgm.hpp:60-110: adds L_r of direction (sx, sy)
+ * into acc (w*h*nd int32, [y][x][d]) */
+rg_status rg_sgm_direction_pass(rg_ctx* ctx, const uint8_t* cost, int w, int h, int nd, int p1,
+                                int p2, int sx, int sy, int32_t* acc);
+
 /* ------------------------------------------------------ synthetic frames */
 
 /* SceneObject (synth.hpp:25-34) and SceneConfig (synth.hpp:36-52) with the

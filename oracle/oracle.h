@@ -65,6 +65,16 @@ int orc_match_blocks64(const uint64_t* left, int lw, int lh, const uint64_t* rig
                        const rg_search_range* ranges, int n_blocks, int mode, double tau_v,
                        rg_match_result* out);
 
+/* SGM (8f row 2): sgm.hpp:37-155 */
+int orc_sgm_direction_pass(const uint8_t* cost, int w, int h, int nd, int p1, int p2, int sx, int sy,
+                           int32_t* acc);
+int orc_sgm_disparity(const uint8_t* left, const uint8_t* right, int w, int h, int nd, int d_lo, int p1, int p2,
+                      int16_t* out);
+int ref_sgm_direction_pass(const uint8_t* cost, int w, int h, int nd, int p1, int p2, int sx, int sy,
+                           int32_t* acc);
+int ref_sgm_disparity(const uint8_t* left, const uint8_t* right, int w, int h, int nd, int d_lo, int p1, int p2,
+                      int16_t* out);
+
 /* reference-only extras (ref_shim.cpp) */
 int ref_render_stereo_pair(const rg_scene_config* cfg, const rg_scene_object* objs,
                            int n_obj, uint8_t* left, uint8_t* right);

@@ -884,3 +884,105 @@ int orc_auto_rect_search(const uint8_t* left, const uint8_t* right, int w, int h
   free(d);
   return RG_OK;
 }
+
+/* ======================================================== SGM (8f row 2) */
+
+/* sgm.hpp:37-56 sgm_cost_volume: popcount of the census XOR, 27 where the
+ * right column leaves the frame */
+static void sgm_cost(const uint32_t* cl, const uint32_t* cr, int w, int h, int nd, int d_lo, uint8_t* cost) {
+  for (int y = 0; y < h; ++y)
+    for (int x = 0; x < w; ++x) {
+      uint8_t* c = cost + ((size_t)y * w + x) * nd;
+      for (int i = 0; i < nd; ++i) {
+        const int rx = x - (d_lo + i);
+        c[i] = (rx < 0 || rx >= w) ? 27 : (uint8_t)__builtin_popcount(cl[(size_t)y * w + x] ^ cr[(size_t)y * w + rx]);
+      }
+    }
+}
+
+/* sgm.hpp:60-110 one directional pass, restated path by path (each path is
+ * walked from the pixel whose predecessor leaves the image) */
+int orc_sgm_direction_pass(const uint8_t* cost, int w, int h, int nd, int p1, int p2, int sx, int sy,
+                           int32_t* acc) {
+  const int big = 0x7fffffff / 4;
+  int32_t* L = (int32_t*)malloc(sizeof(int32_t) * (size_t)nd);
+  int32_t* Ln = (int32_t*)malloc(sizeof(int32_t) * (size_t)nd);
+  for (int y0 = 0; y0 < h; ++y0)
+    for (int x0 = 0; x0 < w; ++x0) {
+      const int px = x0 - sx, py = y0 - sy;
+      if (px >= 0 && px < w && py >= 0 && py < h) continue; /* not a path start */
+      int x = x0, y = y0, first = 1, pmin = 0;
+      while (x >= 0 && x < w && y >= 0 && y < h) {
+        const uint8_t* c = cost + ((size_t)y * w + x) * nd;
+        int mn = big;
+        for (int d = 0; d < nd; ++d) {
+          if (first) {
+            Ln[d] = c[d];
+          } else {
+            int best = L[d];
+            if (d > 0 && L[d - 1] + p1 < best) best = L[d - 1] + p1;
+            if (d + 1 < nd && L[d + 1] + p1 < best) best = L[d + 1] + p1;
+            if (pmin + p2 < best) best = pmin + p2;
+            Ln[d] = c[d] + best - pmin;
+          }
+          if (Ln[d] < mn) mn = Ln[d];
+        }
+        int32_t* a = acc + ((size_t)y * w + x) * nd;
+        for (int d = 0; d < nd; ++d) {
+          a[d] += Ln[d];
+          L[d] = Ln[d];
+        }
+        pmin = mn;
+        first = 0;
+        x += sx;
+        y += sy;
+      }
+    }
+  free(L);
+  free(Ln);
+  return RG_OK;
+}
+
+/* sgm.hpp:118-155 */
+int orc_sgm_disparity(const uint8_t* left, const uint8_t* right, int w, int h, int nd, int d_lo, int p1, int p2,
+                      int16_t* out) {
+  if (nd < 1 || p1 < 0 || p2 < p1) return RG_EINVAL;
+  uint32_t* cl = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)w * h);
+  uint32_t* cr = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)w * h);
+  orc_census_transform(left, w, h, w, h, cl);
+  orc_census_transform(right, w, h, w, h, cr);
+  uint8_t* cost = (uint8_t*)malloc((size_t)w * h * nd);
+  sgm_cost(cl, cr, w, h, nd, d_lo, cost);
+  int32_t* acc = (int32_t*)calloc((size_t)w * h * nd, sizeof(int32_t));
+  const int dirs[4][2] = {{1, 0}, {0, 1}, {1, 1}, {-1, 1}};
+  for (int k = 0; k < 4; ++k) orc_sgm_direction_pass(cost, w, h, nd, p1, p2, dirs[k][0], dirs[k][1], acc);
+  for (int y = 0; y < h; ++y)
+    for (int x = 0; x < w; ++x) {
+      const int32_t* a = acc + ((size_t)y * w + x) * nd;
+      int bi = -1;
+      int32_t best = 0x7fffffff;
+      for (int i = 0; i < nd; ++i) {
+        const int rx = x - (d_lo + i);
+        if (rx < 0 || rx >= w) continue;
+        if (a[i] < best) {
+          best = a[i];
+          bi = i;
+        }
+      }
+      int16_t r = (int16_t)-32768;
+      if (bi >= 0) {
+        double d_hat = d_lo + bi;
+        if (bi > 0 && bi + 1 < nd && x - (d_lo + bi + 1) >= 0) d_hat += subpixel((double)a[bi - 1], (double)best, (double)a[bi + 1]);
+        long v = lround(d_hat * 16.0);
+        const long lo = (long)d_lo * 16, hi = (long)(d_lo + nd) * 16 - 1;
+        v = v < lo ? lo : (v > hi ? hi : v);
+        r = (int16_t)v;
+      }
+      out[(size_t)y * w + x] = r;
+    }
+  free(cl);
+  free(cr);
+  free(cost);
+  free(acc);
+  return RG_OK;
+}

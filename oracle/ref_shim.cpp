@@ -459,4 +459,30 @@ int ref_pipeline_sequence(const uint8_t* left, const uint8_t* right, int w, int 
   });
 }
 
+
+int ref_sgm_direction_pass(const uint8_t* cost, int w, int h, int nd, int p1, int p2, int sx, int sy,
+                           int32_t* acc) {
+  return guarded([&] {
+    const std::vector<std::uint8_t> c(cost, cost + std::size_t(w) * h * nd);
+    std::vector<std::int32_t> a(acc, acc + std::size_t(w) * h * nd);
+    detail::sgm_direction_pass(c, w, h, nd, p1, p2, sx, sy, a);
+    std::memcpy(acc, a.data(), sizeof(int32_t) * a.size());
+    return RG_OK;
+  });
+}
+
+int ref_sgm_disparity(const uint8_t* left, const uint8_t* right, int w, int h, int nd, int d_lo, int p1, int p2,
+                      int16_t* out) {
+  return guarded([&] {
+    SgmParams p;
+    p.num_disparities = nd;
+    p.min_disparity = d_lo;
+    p.p1 = p1;
+    p.p2 = p2;
+    const DisparityMap m = sgm_disparity(to_gray(left, w, h), to_gray(right, w, h), p, 1);
+    std::memcpy(out, m.raw.data(), sizeof(int16_t) * m.raw.size());
+    return RG_OK;
+  });
+}
+
 }  // extern "C"

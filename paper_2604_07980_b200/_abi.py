@@ -65,6 +65,10 @@ class BmParams(C.Structure):
                 ("downscale", C.c_int32), ("texture_threshold", C.c_double), ("uniqueness_ratio", C.c_double)]
 
 
+class SgmParams(C.Structure):
+    _fields_ = [("num_disparities", C.c_int32), ("min_disparity", C.c_int32), ("p1", C.c_int32), ("p2", C.c_int32)]
+
+
 class RectSearchConfig(C.Structure):
     _fields_ = [("enabled", C.c_int32), ("delta_min", C.c_int32), ("delta_max", C.c_int32), ("window", C.c_int32),
                 ("rate_limit", C.c_double), ("bm", BmParams)]
@@ -143,6 +147,11 @@ SIGNATURES = {
     "rg_bm_disparity": (I, [P, P, P, I, I, P, P]),
     "rg_auto_rect_search": (I, [P, P, P, I, I, P, I, I, P, P, P]),
     "rg_auto_rect_frames": (I, [P, P, P, I, I64, I, I, I, P, I, I, P, P, P, P]),
+    "rg_validate_sgm_params": (I, [P, P]),
+    "rg_sgm_disparity": (I, [P, P, P, I, I, P, P]),
+    "rg_sgm_frames": (I, [P, P, P, I, I64, I, I, I, P, P, P]),
+    "rg_sgm_cost_volume": (I, [P, P, P, I, I, P, P]),
+    "rg_sgm_direction_pass": (I, [P, P, I, I, I, I, I, I, I, P]),
     "rg_render_stereo_pair": (I, [P, P, I, P, P, P, P]),
     "rg_ground_truth_detections": (I, [P, P, I, P, P]),
 }

@@ -62,7 +62,7 @@ __global__ void __launch_bounds__(TPB) census_frames_kernel(
 
   const int tx = threadIdx.x & (TX - 1);
   const int x = x0 + tx;
-  const int ix = (x < w) ? inv_x[x] : -1;
+  const int ix = (red && x < w) ? inv_x[x] : -1;  // maps are only passed with a reduced raster
   for (int ty = threadIdx.x / TX; ty < TY; ty += TPB / TX) {
     const int y = y0 + ty;
     if (x >= w || y >= h) continue;
@@ -299,7 +299,7 @@ __global__ void __launch_bounds__(X_TPB) census64_kernel(
   }
   __syncthreads();
   const int tx = threadIdx.x % X_TX, x = x0 + tx;
-  const int ix = (x < w) ? inv_x[x] : -1;
+  const int ix = (red && x < w) ? inv_x[x] : -1;  // maps are only passed with a reduced raster
   for (int ty = threadIdx.x / X_TX; ty < X_TY; ty += X_TPB / X_TX) {
     const int y = y0 + ty;
     if (x >= w || y >= h) continue;

@@ -616,6 +616,33 @@ class RectOffsetState:
 
 
 @dataclass
+class SgmParams:
+    """sgm.hpp:14-19 with the reference's defaults."""
+    num_disparities: int = 64
+    min_disparity: int = 0
+    p1: int = 8
+    p2: int = 32
+
+    def to_c(self) -> _abi.SgmParams:
+        return _abi.SgmParams(self.num_disparities, self.min_disparity, self.p1, self.p2)
+
+
+def sgm_disparity(left, right, p: SgmParams, workers: int = 1, ctx: Optional[Context] = None) -> np.ndarray:
+    """sgm.hpp:118-155 (census SGM, 4 paths, WTA + sub-pixel): raw int16 map."""
+    ctx = ctx or default_context()
+    L, R = _gray(left), _gray(right)
+    if L.shape != R.shape:
+        c = p.to_c()
+        ctx.check(lib().rg_validate_sgm_params(ctx.handle, C.byref(c)))
+        raise InvalidArgument("sgm_disparity: image dims differ")
+    h, w = L.shape
+    out = np.empty((h, w), np.int16)
+    c = p.to_c()
+    ctx.check(lib().rg_sgm_disparity(ctx.handle, _ptr(L), _ptr(R), w, h, C.byref(c), _ptr(out)))
+    return out
+
+
+@dataclass
 class RectSearchConfig:
     """pipeline.hpp:52-62 with the reference's defaults."""
     enabled: bool = True

@@ -132,10 +132,35 @@ def main():
         ar.append({"voff": voff, "sha_left": sha(L), "sha_right": sha(R), "best": best,
                    "counts": [int(c) for c in counts]})
     g["autorect"] = ar
+    g["sgm"] = sgm_section(ref)
     with open(os.path.join(HERE, "golden.json"), "w") as f:
         json.dump(g, f, indent=0)
     print("wrote", os.path.join(HERE, "golden.json"))
 
 
+SGM_CASES = [(200, 40, 24, 16, 0, 8, 32), (201, 33, 17, 8, -3, 0, 0), (202, 64, 20, 24, 2, 3, 50),
+             (203, 16, 12, 40, 0, 10, 10), (204, 90, 7, 32, -8, 8, 32)]
+
+
+def sgm_section(ref):
+    """sgm_disparity of the reference on seeded random pairs: raw-map hashes."""
+    out = []
+    for (seed, w, h, nd, d_lo, p1, p2) in SGM_CASES:
+        a, b = rand_img(seed, h, w), rand_img(seed + 1000, h, w)
+        raw = np.zeros((h, w), np.int16)
+        assert ref.lib.ref_sgm_disparity(a.ctypes.data, b.ctypes.data, w, h, nd, d_lo, p1, p2, raw.ctypes.data) == 0
+        out.append({"seed": seed, "w": w, "h": h, "params": [nd, d_lo, p1, p2], "sha": sha(raw),
+                    "n_valid": int((raw != -32768).sum())})
+    return out
+
+
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["--only", "sgm"]:  # add/refresh just the SGM section
+        path = os.path.join(HERE, "golden.json")
+        g = json.load(open(path))
+        g["sgm"] = sgm_section(oracle_lib.reference())
+        with open(path, "w") as f:
+            json.dump(g, f, indent=0)
+        print("updated sgm in", path)
+    else:
+        main()

@@ -54,6 +54,10 @@ class Checker:
             self.lib.ref_bench_estimate.restype = D
             self.lib.ref_bench_estimate.argtypes = [P, P, I, I, I, P, P, P, I, P, I, P]
 
+        for nm, args in (("sgm_direction_pass", [P, I, I, I, I, I, I, I, P]),
+                         ("sgm_disparity", [P, P, I, I, I, I, I, I, P])):
+            f = getattr(self.lib, prefix + nm)
+            f.restype, f.argtypes = I, args
         if prefix == "orc_":  # 9x7 extension (restatement only)
             self.lib.orc_census_transform64.restype = I
             self.lib.orc_census_transform64.argtypes = [P, I, I, I, I, P]
@@ -79,6 +83,13 @@ class Checker:
         oh = h if oh is None else oh
         out = np.zeros((oh, ow), np.uint64)
         st = self.lib.orc_census_transform64(img.ctypes.data, w, h, ow, oh, out.ctypes.data)
+        assert st == 0, st
+        return out
+
+    def sgm(self, left, right, nd, d_lo, p1, p2) -> np.ndarray:
+        h, w = left.shape
+        out = np.zeros((h, w), np.int16)
+        st = self.fn("sgm_disparity")(left.ctypes.data, right.ctypes.data, w, h, nd, d_lo, p1, p2, out.ctypes.data)
         assert st == 0, st
         return out
 

@@ -141,3 +141,26 @@ def test_oracle_equals_reference_fresh_inputs(orc):
         b, sb = ref.estimate(L, R, dets, cfg.to_c())
         assert [bytes(x) for x in a] == [bytes(y) for y in b]
         assert bytes(sa) == bytes(sb)
+
+
+@pytest.mark.parametrize("rec", GOLDEN["sgm"], ids=lambda r: f"sgm{r['params']}")
+def test_oracle_sgm_golden(orc, rec):  # sgm.hpp:118-155 pinned to the reference's outputs
+    a, b = rand_img(rec["seed"], rec["h"], rec["w"]), rand_img(rec["seed"] + 1000, rec["h"], rec["w"])
+    nd, d_lo, p1, p2 = rec["params"]
+    raw = orc.sgm(a, b, nd, d_lo, p1, p2)
+    assert sha(raw) == rec["sha"] and int((raw != -32768).sum()) == rec["n_valid"]
+
+
+def test_oracle_sgm_pass_equals_reference_fresh(orc):
+    if not oracle_lib.have_reference():
+        pytest.skip("oracle/_ref not built here")
+    ref = oracle_lib.reference()
+    rng = np.random.default_rng(7)
+    for (w, h, nd, p1, p2) in [(17, 9, 12, 3, 20), (8, 23, 40, 0, 5), (31, 5, 33, 7, 7)]:
+        cost = rng.integers(0, 28, (h, w, nd), dtype=np.uint8)
+        for sx, sy in [(1, 0), (0, 1), (1, 1), (-1, 1), (-1, 0), (0, -1), (1, -1), (-1, -1)]:
+            acc0 = rng.integers(-5, 5, (h, w, nd)).astype(np.int32)
+            a1, a2 = acc0.copy(), acc0.copy()
+            assert orc.lib.orc_sgm_direction_pass(cost.ctypes.data, w, h, nd, p1, p2, sx, sy, a1.ctypes.data) == 0
+            assert ref.lib.ref_sgm_direction_pass(cost.ctypes.data, w, h, nd, p1, p2, sx, sy, a2.ctypes.data) == 0
+            assert np.array_equal(a1, a2), (w, h, nd, sx, sy)
