@@ -402,6 +402,30 @@ def main():
     except Exception as e:  # pragma: no cover
         seq = {"error": str(e)}
 
+    # ---- SGM dense baseline on the same frames: 64
+    # disparities, P1 8 / P2 32 (sgm.hpp defaults), rg_sgm_frames
+    sgm = None
+    try:
+        nsg = min(F, 8)
+        sp = rg.SgmParams(64, 0, 8, 32).to_c()
+        sgm_out = torch.zeros(nsg * W * H, dtype=torch.int16, device=dev)
+
+        def sgm_run():
+            ctx.check(rg.lib().rg_sgm_frames(ctx.handle, dL.data_ptr(), dR.data_ptr(), nsg, dL.stride(0), W, W, H,
+                                             C.byref(sp), sgm_out.data_ptr(), C.c_void_p(stream.cuda_stream)))
+        sgm_run()
+        torch.cuda.synchronize()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        sgm_run()
+        g1.record(stream)
+        torch.cuda.synchronize()
+        sms = g0.elapsed_time(g1) / nsg
+        sgm = {"config": "1920x1080 C2 frames, census SGM, 64 disparities, P1 8, P2 32, 4 paths (rg_sgm_frames)",
+               "ms_per_frame": sms, "frames_per_sec": 1000.0 / sms}
+    except Exception as e:  # pragma: no cover
+        sgm = {"error": str(e)}
+
     # ---- roofline of the dominant kernel (stage times from CUDA events on our stream)
     hbm_peak, sm_max, peak_kind = peaks()
     census_ms = stage_ms[0] / max(stage_launches[0], 1)
@@ -461,6 +485,7 @@ def main():
             "hamming_evals_per_frame": evals / max(F * args.steps, 1),
             "autorect": rect,
             "sequence": seq,
+            "sgm": sgm,
             "clocks": clk,
             "parity_spot_check_vs_oracle": spot,
             "cpu_baseline": cpu,

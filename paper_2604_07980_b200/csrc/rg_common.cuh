@@ -176,6 +176,9 @@ cudaError_t launch_sgm_cost(const uint32_t* cl, const uint32_t* cr, int w, int h
 cudaError_t launch_sgm_pass(const uint8_t* cost, int w, int h, int nd, int p1, int p2, int sx, int sy,
                             int32_t* acc, cudaStream_t s);
 cudaError_t launch_sgm_wta(const int32_t* acc, int w, int h, int nd, int d_lo, int16_t* out, cudaStream_t s);
+int sgm_l_bytes(int p2);
+cudaError_t launch_sgm_fast(const uint32_t* cl, const uint32_t* cr, int w, int h, int nd, int d_lo, int p1, int p2,
+                            void* Lbuf, int16_t* out, cudaStream_t s);
 
 // planner / aggregation / helpers (plan.cu)
 cudaError_t launch_plan_frames(const rg_detection* dets, const int32_t* det_off, int n_frames,

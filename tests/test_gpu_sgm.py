@@ -17,7 +17,9 @@ def rand_img(rng, h, w):
 
 @pytest.mark.parametrize("w,h,nd,d_lo,p1,p2", [(40, 24, 16, 0, 8, 32), (33, 17, 8, -3, 0, 0), (64, 20, 24, 2, 3, 50),
                                                (90, 7, 32, -8, 8, 32), (70, 30, 40, 0, 8, 32),
-                                               (50, 12, 96, -20, 5, 60), (1, 9, 4, 0, 8, 32)])
+                                               (50, 12, 96, -20, 5, 60), (1, 9, 4, 0, 8, 32),
+                                               (80, 16, 48, -5, 4, 20), (120, 10, 64, -10, 8, 32),
+                                               (70, 9, 64, 3, 100, 300)])
 def test_sgm_random_matches_oracle(ctx, orc, w, h, nd, d_lo, p1, p2):
     rng = np.random.default_rng(w * 31 + nd)
     a, b = rand_img(rng, h, w), rand_img(rng, h, w)
