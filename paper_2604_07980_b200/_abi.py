@@ -123,6 +123,7 @@ SIGNATURES = {
     "rg_create_error": (C.c_char_p, []),
     "rg_build_info": (C.c_char_p, []),
     "rg_set_profiling": (I, [P, I]),
+    "rg_set_overlap": (I, [P, I]),
     "rg_get_counters": (I, [P, P, P, P]),
     "rg_reset_counters": (I, [P]),
     "rg_get_work": (I, [P, P, P]),

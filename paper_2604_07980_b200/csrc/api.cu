@@ -242,11 +242,19 @@ struct PipelineBufs {
   int capacity;
 };
 
-rg_status enqueue_pipeline(rg_ctx* ctx, const FrameJob& J, const rg_ranger_config& cfg,
-                           cudaStream_t s, int32_t* counters, PipelineBufs* pb) {
+// Geometry and device buffers of the padded census rasters for `frames`
+// frames (the margins are zeroed on `s` whenever the layout changes).
+struct Rasters {
+  uint32_t *fl, *fr, *sl, *sr;
+  PadGeom gf, gs;
+  bool wide;
+  int32_t *ix, *iy;
+};
+
+rg_status prepare_rasters(rg_ctx* ctx, const FrameJob& J, const rg_ranger_config& cfg, int frames, cudaStream_t s,
+                          Rasters* R) {
   const int w = J.w, h = J.h, sc = cfg.close_scale;
   const int cw = w / sc, ch = h / sc;
-  const int F = J.n_frames;
   if (cw < 1 || ch < 1) return set_err(ctx, RG_EINVAL, "estimate_object_disparities: close raster empty");
   const int maxp = planner_max_points(cfg);
   // 9x7 extension: 64-bit codes, window rows +-3 / cols +-4
@@ -273,8 +281,8 @@ rg_status enqueue_pipeline(rg_ctx* ctx, const FrameJob& J, const rg_ranger_confi
     for (int i = 0; i < ch; ++i)
       if (my[i] >= ry && my[i] <= h - 1 - ry) gs.sy0 = std::min(gs.sy0, i), gs.sy1 = std::max(gs.sy1, i);
   }
-  const size_t fbytes = csz * (size_t)gf.fstride * F;
-  const size_t sbytes = csz * (size_t)gs.fstride * F;
+  const size_t fbytes = csz * (size_t)gf.fstride * frames;
+  const size_t sbytes = csz * (size_t)gs.fstride * frames;
   const bool regeom = ctx->cap[B_CEN_FL] < fbytes || ctx->cap[B_CEN_SL] < sbytes ||
                       !same_geom(ctx->pad_key, gf) || !same_geom(ctx->pad_key_s, gs) ||
                       ctx->pad_wide != (int)wide;
@@ -295,6 +303,58 @@ rg_status enqueue_pipeline(rg_ctx* ctx, const FrameJob& J, const rg_ranger_confi
     ctx->pad_key_s = gs;
     ctx->pad_wide = (int)wide;
   }
+  int32_t *ix = nullptr, *iy = nullptr;
+  TRY(upload_inverse_maps(ctx, w, h, cw, ch, s, &ix, &iy));
+  *R = {fl, fr, sl, sr, gf, gs, wide, ix, iy};
+  return RG_OK;
+}
+
+// K1 of job J into the rasters starting at raster frame `slot0`
+rg_status enqueue_census(rg_ctx* ctx, const FrameJob& J, const Rasters& R, int slot0, cudaStream_t s) {
+  const int w = J.w, h = J.h, F = J.n_frames;
+  const size_t csz = R.wide ? sizeof(unsigned long long) : sizeof(uint32_t);
+  auto at = [&](uint32_t* p, const PadGeom& g) {
+    return reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(p) + csz * (size_t)g.fstride * slot0);
+  };
+  uint32_t *fl = at(R.fl, R.gf), *fr = at(R.fr, R.gf), *sl = at(R.sl, R.gs), *sr = at(R.sr, R.gs);
+  if (R.wide) {
+    using u64 = unsigned long long;
+    RG_CUDA(ctx, launch_census64_frames(J.left, J.right, F, J.frame_stride, J.pitch, w, h, (u64*)fl, (u64*)fr,
+                                        R.gf, (u64*)sl, (u64*)sr, R.gs, R.ix, R.iy, J.left_shift, s));
+    count_launch(ctx, ST_CENSUS);
+  } else if (!(J.full_l && J.scaled_l)) {
+    RG_CUDA(ctx, launch_census_frames(J.left, J.right, F, J.frame_stride, J.pitch, w, h, fl, fr, R.gf, sl, sr,
+                                      R.gs, R.ix, R.iy, J.left_shift, true, s));
+    count_launch(ctx, ST_CENSUS);
+  }
+  // caller-supplied codes (a pre-filled CensusCache) into the padded layout
+  auto put = [&](uint32_t* dst, const uint32_t* src, const PadGeom& g) -> rg_status {
+    RG_CUDA(ctx, cudaMemcpy2DAsync(dst + g.origin, sizeof(uint32_t) * g.pitch, src, sizeof(uint32_t) * g.w,
+                                   sizeof(uint32_t) * g.w, g.h, cudaMemcpyDefault, s));
+    return RG_OK;
+  };
+  if (J.full_l) {
+    TRY(put(fl, J.full_l, R.gf));
+    TRY(put(fr, J.full_r, R.gf));
+  }
+  if (J.scaled_l) {
+    TRY(put(sl, J.scaled_l, R.gs));
+    TRY(put(sr, J.scaled_r, R.gs));
+  }
+  return RG_OK;
+}
+
+// K3 planner, K2 matcher, K4 aggregation of job J over the rasters at `slot0`.
+// ev (nullable): 4 timing events recorded before K3, K2, K4 and after K4.
+rg_status enqueue_match(rg_ctx* ctx, const FrameJob& J, const rg_ranger_config& cfg, const Rasters& R, int slot0,
+                        cudaStream_t s, int32_t* counters, const cudaEvent_t* ev, PipelineBufs* pb) {
+  const int w = J.w, h = J.h, F = J.n_frames;
+  const size_t csz = R.wide ? sizeof(unsigned long long) : sizeof(uint32_t);
+  auto at = [&](uint32_t* p, const PadGeom& g) {
+    return reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(p) + csz * (size_t)g.fstride * slot0);
+  };
+  uint32_t *fl = at(R.fl, R.gf), *fr = at(R.fr, R.gf), *sl = at(R.sl, R.gs), *sr = at(R.sr, R.gs);
+  const int maxp = planner_max_points(cfg);
   if (ctx->slot_capacity < F * 64) ctx->slot_capacity = F * 64;
   const int capacity = ctx->slot_capacity;
   ObjEntry* objs = DBUF(ObjEntry, ctx, B_OBJ, (size_t)F * std::max(J.out_stride, 1));
@@ -305,55 +365,37 @@ rg_status enqueue_pipeline(rg_ctx* ctx, const FrameJob& J, const rg_ranger_confi
   NEED(slots);
   NEED(res);
   NEED(scratch);
-  int32_t *ix = nullptr, *iy = nullptr;
-  TRY(upload_inverse_maps(ctx, w, h, cw, ch, s, &ix, &iy));
   RG_CUDA(ctx, cudaMemsetAsync(counters, 0, 4 * sizeof(int32_t), s));
-  const bool prof = ctx->profiling;
-  if (prof) RG_CUDA(ctx, cudaEventRecord(ctx->ev[0], s));
-  // K1 census (full + fused reduced raster) of both images of every frame
-  if (wide) {
-    using u64 = unsigned long long;
-    RG_CUDA(ctx, launch_census64_frames(J.left, J.right, F, J.frame_stride, J.pitch, w, h, (u64*)fl, (u64*)fr,
-                                        gf, (u64*)sl, (u64*)sr, gs, ix, iy, J.left_shift, s));
-    count_launch(ctx, ST_CENSUS);
-  } else if (!(J.full_l && J.scaled_l)) {
-    RG_CUDA(ctx, launch_census_frames(J.left, J.right, F, J.frame_stride, J.pitch, w, h, fl, fr, gf, sl,
-                                      sr, gs, ix, iy, J.left_shift, true, s));
-    count_launch(ctx, ST_CENSUS);
-  }
-  // caller-supplied codes (a pre-filled CensusCache) into the padded layout
-  auto put = [&](uint32_t* dst, const uint32_t* src, const PadGeom& g) -> rg_status {
-    RG_CUDA(ctx, cudaMemcpy2DAsync(dst + g.origin, sizeof(uint32_t) * g.pitch, src, sizeof(uint32_t) * g.w,
-                                   sizeof(uint32_t) * g.w, g.h, cudaMemcpyDefault, s));
-    return RG_OK;
-  };
-  if (J.full_l) {
-    TRY(put(fl, J.full_l, gf));
-    TRY(put(fr, J.full_r, gf));
-  }
-  if (J.scaled_l) {
-    TRY(put(sl, J.scaled_l, gs));
-    TRY(put(sr, J.scaled_r, gs));
-  }
-  if (prof) RG_CUDA(ctx, cudaEventRecord(ctx->ev[1], s));
+  if (ev) RG_CUDA(ctx, cudaEventRecord(ev[0], s));
   // K3 planner
   RG_CUDA(ctx, launch_plan_frames(J.dets, J.det_off, F, w, h, cfg, J.out_stride, objs, J.out,
                                   J.out_count, slots, capacity, counters, J.stats, s));
   count_launch(ctx, ST_PLAN);
-  if (prof) RG_CUDA(ctx, cudaEventRecord(ctx->ev[2], s));
+  if (ev) RG_CUDA(ctx, cudaEventRecord(ev[1], s));
   // K2 fused sampler + forward/backward matcher, one warp per slot
   const int trusted = !(J.full_l || J.scaled_l);
-  RG_CUDA(ctx, launch_match_slots(slots, counters, capacity, objs, J.dets, J.det_off, fl, fr, gf, sl, sr, gs,
-                                  w, h, trusted, (int)wide, cfg, res, J.stats, maxp, s));
+  RG_CUDA(ctx, launch_match_slots(slots, counters, capacity, objs, J.dets, J.det_off, fl, fr, R.gf, sl, sr, R.gs,
+                                  w, h, trusted, (int)R.wide, cfg, res, J.stats, maxp, s));
   count_launch(ctx, ST_MATCH);
-  if (prof) RG_CUDA(ctx, cudaEventRecord(ctx->ev[3], s));
+  if (ev) RG_CUDA(ctx, cudaEventRecord(ev[2], s));
   // K4 aggregation + range
   RG_CUDA(ctx, launch_aggregate(objs, J.out_count, F, J.out_stride, res, capacity, cfg, J.focal,
                                 J.baseline, scratch, J.out, counters, s));
   count_launch(ctx, ST_AGG);
-  if (prof) RG_CUDA(ctx, cudaEventRecord(ctx->ev[4], s));
-  if (pb) *pb = {fl, fr, sl, sr, gf, gs, objs, slots, res, counters, scratch, capacity};
+  if (ev) RG_CUDA(ctx, cudaEventRecord(ev[3], s));
+  if (pb) *pb = {fl, fr, sl, sr, R.gf, R.gs, objs, slots, res, counters, scratch, capacity};
   return RG_OK;
+}
+
+// census + match of J on one stream (timing events ev[0..4] when profiling)
+rg_status enqueue_pipeline(rg_ctx* ctx, const FrameJob& J, const rg_ranger_config& cfg,
+                           cudaStream_t s, int32_t* counters, PipelineBufs* pb) {
+  Rasters R;
+  TRY(prepare_rasters(ctx, J, cfg, J.n_frames, s, &R));
+  const bool prof = ctx->profiling;
+  if (prof) RG_CUDA(ctx, cudaEventRecord(ctx->ev[0], s));
+  TRY(enqueue_census(ctx, J, R, 0, s));
+  return enqueue_match(ctx, J, cfg, R, 0, s, counters, prof ? ctx->ev + 1 : nullptr, pb);
 }
 
 void accumulate_profile(rg_ctx* ctx) {
@@ -398,6 +440,109 @@ rg_status run_pipeline(rg_ctx* ctx, const FrameJob& J, const rg_ranger_config& c
   return finish_pipeline(ctx, J, cfg, s, counters, hc, pb);
 }
 
+int census_stream_priority() {  // lowest priority: census CTAs fill what the matcher leaves
+  int lo = 0, hi = 0;
+  cudaDeviceGetStreamPriorityRange(&lo, &hi);
+  const char* v = getenv("RG_CENSUS_PRIO");
+  return v ? atoi(v) : lo;
+}
+
+int match_stream_priority() {  // greatest priority: the latency-bound matcher is scheduled first
+  int lo = 0, hi = 0;
+  cudaDeviceGetStreamPriorityRange(&lo, &hi);
+  const char* v = getenv("RG_MATCH_PRIO");
+  return v ? atoi(v) : hi;
+}
+
+// rg_range_frames schedule: the batch is cut into chunks; K1 of chunk k+1 runs
+// on the context's census stream while K3/K2/K4 of chunk k run on the caller's
+// stream, so the HBM-bound census overlaps the latency-bound matcher.  The
+// rasters are double-buffered by chunk parity (census k+2 waits for match k).
+rg_status run_pipeline_overlapped(rg_ctx* ctx, const FrameJob& J, const rg_ranger_config& cfg, cudaStream_t s) {
+  const int F = J.n_frames;
+  constexpr int kMinChunk = 16;
+  if (!ctx->overlap || F < 2 * kMinChunk || J.full_l || J.scaled_l) return run_pipeline(ctx, J, cfg, s, nullptr);
+  static const int n_chunks = [] {
+    const char* v = getenv("RG_CHUNKS");
+    return v ? std::max(2, atoi(v)) : 4;
+  }();
+  const int chunk = std::max(kMinChunk, (F + n_chunks - 1) / n_chunks);
+  const int nch = (F + chunk - 1) / chunk;
+  if (nch > 6) return run_pipeline(ctx, J, cfg, s, nullptr);  // ev_prof holds 6 chunks
+  Rasters R;
+  TRY(prepare_rasters(ctx, J, cfg, 2 * chunk, s, &R));
+  int32_t* counters = DBUF(int32_t, ctx, B_COUNTERS, 4 * (size_t)nch);
+  int32_t* hc = static_cast<int32_t*>(host_buf(ctx, 0, 4 * sizeof(int32_t) * nch));
+  NEED(counters);
+  NEED(hc);
+  cudaStream_t cs = ctx->census_stream, ms = ctx->match_stream;
+  const bool prof = ctx->profiling;
+  // both internal streams start after everything already queued on s
+  RG_CUDA(ctx, cudaEventRecord(ctx->ev_sync[0], s));
+  RG_CUDA(ctx, cudaStreamWaitEvent(cs, ctx->ev_sync[0], 0));
+  RG_CUDA(ctx, cudaStreamWaitEvent(ms, ctx->ev_sync[0], 0));
+  auto sub = [&](int k) {
+    FrameJob Jk = J;
+    const int f0 = k * chunk;
+    Jk.n_frames = std::min(F, f0 + chunk) - f0;
+    Jk.left = J.left + (int64_t)f0 * J.frame_stride;
+    Jk.right = J.right + (int64_t)f0 * J.frame_stride;
+    Jk.det_off = J.det_off + f0;
+    Jk.out = J.out + (int64_t)f0 * J.out_stride;
+    Jk.out_count = J.out_count + f0;
+    Jk.stats = J.stats ? J.stats + f0 : nullptr;
+    Jk.left_shift = J.left_shift ? J.left_shift + f0 : nullptr;
+    return Jk;
+  };
+  for (int k = 0; k < nch; ++k) {
+    const int slot = k & 1;
+    const FrameJob Jk = sub(k);
+    if (k >= 2) RG_CUDA(ctx, cudaStreamWaitEvent(cs, ctx->ev_sync[2 + slot], 0));  // match k-2 released the slot
+    if (prof) RG_CUDA(ctx, cudaEventRecord(ctx->ev_prof[6 * k], cs));
+    TRY(enqueue_census(ctx, Jk, R, slot * chunk, cs));
+    if (prof) RG_CUDA(ctx, cudaEventRecord(ctx->ev_prof[6 * k + 1], cs));
+    RG_CUDA(ctx, cudaEventRecord(ctx->ev_sync[4 + slot], cs));
+    RG_CUDA(ctx, cudaStreamWaitEvent(ms, ctx->ev_sync[4 + slot], 0));
+    TRY(enqueue_match(ctx, Jk, cfg, R, slot * chunk, ms, counters + 4 * k, prof ? ctx->ev_prof + 6 * k + 2 : nullptr,
+                      nullptr));
+    RG_CUDA(ctx, cudaEventRecord(ctx->ev_sync[2 + slot], ms));
+  }
+  // join: the caller's stream continues after the last matcher chunk (which
+  // itself follows every census chunk)
+  RG_CUDA(ctx, cudaEventRecord(ctx->ev_sync[1], ms));
+  RG_CUDA(ctx, cudaStreamWaitEvent(s, ctx->ev_sync[1], 0));
+  RG_CUDA(ctx, cudaMemcpyAsync(hc, counters, 4 * sizeof(int32_t) * nch, cudaMemcpyDeviceToHost, s));
+  RG_CUDA(ctx, cudaStreamSynchronize(s));
+  if (prof) {
+    for (int k = 0; k < nch; ++k) {
+      float ms = 0;
+      if (cudaEventElapsedTime(&ms, ctx->ev_prof[6 * k], ctx->ev_prof[6 * k + 1]) == cudaSuccess)
+        ctx->stage_ms[ST_CENSUS] += ms;
+      for (int i = 0; i < 3; ++i)
+        if (cudaEventElapsedTime(&ms, ctx->ev_prof[6 * k + 2 + i], ctx->ev_prof[6 * k + 3 + i]) == cudaSuccess)
+          ctx->stage_ms[1 + i] += ms;
+    }
+    cudaGetLastError();
+  }
+  int64_t slots = 0;
+  for (int k = 0; k < nch; ++k) {
+    const int32_t* c = hc + 4 * k;
+    if (c[1]) {  // this chunk overflowed its slot list: grow and re-run it alone
+      ctx->slot_capacity = std::max(ctx->slot_capacity * 2, c[0] + c[0] / 4 + 64);
+      const FrameJob Jk = sub(k);
+      TRY(run_pipeline(ctx, Jk, cfg, s, nullptr));
+      continue;
+    }
+    int64_t ev;
+    std::memcpy(&ev, c + 2, sizeof(ev));
+    ctx->hamming_evals += ev;
+    ctx->slots_total += c[0];
+    slots += c[0];
+  }
+  ctx->last_slots = slots;
+  return RG_OK;
+}
+
 }  // namespace
 
 // =========================================================== C ABI: context
@@ -430,12 +575,17 @@ rg_status rg_ctx_create(int device, rg_ctx** out) {
   rg_ctx* c = new rg_ctx();
   c->device = device;
   if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
-      cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) != cudaSuccess) {
+      cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithPriority(&c->census_stream, cudaStreamNonBlocking, census_stream_priority()) !=
+          cudaSuccess ||
+      cudaStreamCreateWithPriority(&c->match_stream, cudaStreamNonBlocking, match_stream_priority()) != cudaSuccess) {
     g_create_err = "cudaStreamCreate failed";
     delete c;
     return RG_ECUDA;
   }
   for (auto& ev : c->ev) cudaEventCreate(&ev);
+  for (auto& ev : c->ev_sync) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+  for (auto& ev : c->ev_prof) cudaEventCreate(&ev);
   *out = c;
   return RG_OK;
 }
@@ -450,8 +600,14 @@ void rg_ctx_destroy(rg_ctx* ctx) {
     if (ctx->hbuf[i]) cudaFreeHost(ctx->hbuf[i]);
   for (auto& ev : ctx->ev)
     if (ev) cudaEventDestroy(ev);
+  for (auto ev : ctx->ev_sync)
+    if (ev) cudaEventDestroy(ev);
+  for (auto ev : ctx->ev_prof)
+    if (ev) cudaEventDestroy(ev);
   cudaStreamDestroy(ctx->stream);
   cudaStreamDestroy(ctx->copy_stream);
+  cudaStreamDestroy(ctx->census_stream);
+  cudaStreamDestroy(ctx->match_stream);
   delete ctx;
 }
 
@@ -462,6 +618,12 @@ const char* rg_build_info(void) { return RG_BUILD_INFO; }
 rg_status rg_set_profiling(rg_ctx* ctx, int on) {
   if (!ctx) return RG_EINVAL;
   ctx->profiling = on != 0;
+  return RG_OK;
+}
+
+rg_status rg_set_overlap(rg_ctx* ctx, int on) {
+  if (!ctx) return RG_EINVAL;
+  ctx->overlap = on != 0;
   return RG_OK;
 }
 
@@ -970,7 +1132,7 @@ rg_status rg_range_frames(rg_ctx* ctx, const rg_frame_batch* b, const rg_ranger_
                 b->focal_px, b->baseline_m};
   J.left_shift = b->d_left_shift;
   cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
-  return run_pipeline(ctx, J, *cfg, s, nullptr);
+  return run_pipeline_overlapped(ctx, J, *cfg, s);
 }
 
 rg_status rg_range_frames_host(rg_ctx* ctx, const rg_frame_batch* b, const rg_ranger_config* cfg,

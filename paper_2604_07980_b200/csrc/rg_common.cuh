@@ -91,6 +91,11 @@ struct rg_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;  // stream of the synchronous compat API
   cudaStream_t copy_stream = nullptr;  // H2D staging of the host-fed batch API
+  cudaStream_t census_stream = nullptr;  // K1 of chunk k+1 while K2 of chunk k runs (rg_range_frames)
+  cudaStream_t match_stream = nullptr;   // K3/K2/K4 chunks (highest priority), joined back to the caller
+  bool overlap = false;                  // chunked census/matcher overlap in rg_range_frames (opt-in)
+  cudaEvent_t ev_sync[6] = {};           // cross-stream ordering events (no timing)
+  cudaEvent_t ev_prof[40] = {};          // per-chunk stage timing when profiling
   int map_key[4] = {-1, -1, -1, -1};  // geometry of the cached inverse maps
   rg::PadGeom pad_key{}, pad_key_s{};  // layout of the zeroed census rasters
   int pad_wide = 0;                    // ... and their code width (1 = 64-bit)

@@ -92,6 +92,10 @@ class Context:
     def set_profiling(self, on: bool) -> None:
         self.check(lib().rg_set_profiling(self._h, 1 if on else 0))
 
+    def set_overlap(self, on: bool) -> None:
+        """rg_range_frames schedule: chunked census/matcher overlap (default) or one stream."""
+        self.check(lib().rg_set_overlap(self._h, 1 if on else 0))
+
     def counters(self) -> Tuple[List[float], List[int], int]:
         t = (C.c_double * 5)()
         n = (C.c_int64 * 5)()

@@ -208,3 +208,23 @@ def test_range_frames_edge_cases(ctx, orc, case):
     Ls = np.stack([f[0] for f in frames])
     Rs = np.stack([f[1] for f in frames])
     _batch_vs_oracle(ctx, orc, Ls, Rs, [f[2] for f in frames], cfg, S.F_PX, S.BASELINE_M)
+
+
+@pytest.mark.parametrize("overlap", [True, False])
+def test_range_frames_chunked_overlap_schedule(ctx, orc, overlap):
+    """>= 32 frames take the chunked census/matcher overlap schedule (chunk
+    rasters double-buffered across two streams); it must equal the oracle and
+    the single-stream schedule frame by frame."""
+    rng = np.random.default_rng(5)
+    n = 37  # 4 chunks, the last one partial
+    sc, cfg = S.scene_c1(seed=91, noise=2.0)
+    L0, R0 = S.render_stereo_pair(sc)
+    dets0 = S.ground_truth_detections(sc)
+    L = np.stack([np.roll(L0, 3 * i, axis=1) for i in range(n)])
+    R = np.stack([np.roll(R0, 3 * i, axis=1) for i in range(n)])
+    D = [list(rng.permutation(dets0))[: 1 + (i % len(dets0))] for i in range(n)]
+    ctx.set_overlap(overlap)
+    try:
+        _batch_vs_oracle(ctx, orc, L, R, D, cfg, S.F_PX, S.BASELINE_M)
+    finally:
+        ctx.set_overlap(False)
