@@ -365,7 +365,7 @@ rg_status enqueue_match(rg_ctx* ctx, const FrameJob& J, const rg_ranger_config& 
   NEED(slots);
   NEED(res);
   NEED(scratch);
-  RG_CUDA(ctx, cudaMemsetAsync(counters, 0, 4 * sizeof(int32_t), s));
+  RG_CUDA(ctx, cudaMemsetAsync(counters, 0, kCounterInts * sizeof(int32_t), s));
   if (ev) RG_CUDA(ctx, cudaEventRecord(ev[0], s));
   // K3 planner
   RG_CUDA(ctx, launch_plan_frames(J.dets, J.det_off, F, w, h, cfg, J.out_stride, objs, J.out,
@@ -432,8 +432,8 @@ rg_status finish_pipeline(rg_ctx* ctx, const FrameJob& J, const rg_ranger_config
 // run + overflow check (synchronous)
 rg_status run_pipeline(rg_ctx* ctx, const FrameJob& J, const rg_ranger_config& cfg, cudaStream_t s,
                        PipelineBufs* pb) {
-  int32_t* counters = DBUF(int32_t, ctx, B_COUNTERS, 4);
-  int32_t* hc = static_cast<int32_t*>(host_buf(ctx, 0, 4 * sizeof(int32_t)));
+  int32_t* counters = DBUF(int32_t, ctx, B_COUNTERS, kCounterInts);
+  int32_t* hc = static_cast<int32_t*>(host_buf(ctx, 0, kCounterInts * sizeof(int32_t)));
   NEED(counters);
   NEED(hc);
   TRY(enqueue_pipeline(ctx, J, cfg, s, counters, pb));
@@ -471,8 +471,8 @@ rg_status run_pipeline_overlapped(rg_ctx* ctx, const FrameJob& J, const rg_range
   if (nch > 6) return run_pipeline(ctx, J, cfg, s, nullptr);  // ev_prof holds 6 chunks
   Rasters R;
   TRY(prepare_rasters(ctx, J, cfg, 2 * chunk, s, &R));
-  int32_t* counters = DBUF(int32_t, ctx, B_COUNTERS, 4 * (size_t)nch);
-  int32_t* hc = static_cast<int32_t*>(host_buf(ctx, 0, 4 * sizeof(int32_t) * nch));
+  int32_t* counters = DBUF(int32_t, ctx, B_COUNTERS, kCounterInts * (size_t)nch);
+  int32_t* hc = static_cast<int32_t*>(host_buf(ctx, 0, kCounterInts * sizeof(int32_t) * nch));
   NEED(counters);
   NEED(hc);
   cudaStream_t cs = ctx->census_stream, ms = ctx->match_stream;
@@ -503,15 +503,15 @@ rg_status run_pipeline_overlapped(rg_ctx* ctx, const FrameJob& J, const rg_range
     if (prof) RG_CUDA(ctx, cudaEventRecord(ctx->ev_prof[6 * k + 1], cs));
     RG_CUDA(ctx, cudaEventRecord(ctx->ev_sync[4 + slot], cs));
     RG_CUDA(ctx, cudaStreamWaitEvent(ms, ctx->ev_sync[4 + slot], 0));
-    TRY(enqueue_match(ctx, Jk, cfg, R, slot * chunk, ms, counters + 4 * k, prof ? ctx->ev_prof + 6 * k + 2 : nullptr,
-                      nullptr));
+    TRY(enqueue_match(ctx, Jk, cfg, R, slot * chunk, ms, counters + kCounterInts * k,
+                      prof ? ctx->ev_prof + 6 * k + 2 : nullptr, nullptr));
     RG_CUDA(ctx, cudaEventRecord(ctx->ev_sync[2 + slot], ms));
   }
   // join: the caller's stream continues after the last matcher chunk (which
   // itself follows every census chunk)
   RG_CUDA(ctx, cudaEventRecord(ctx->ev_sync[1], ms));
   RG_CUDA(ctx, cudaStreamWaitEvent(s, ctx->ev_sync[1], 0));
-  RG_CUDA(ctx, cudaMemcpyAsync(hc, counters, 4 * sizeof(int32_t) * nch, cudaMemcpyDeviceToHost, s));
+  RG_CUDA(ctx, cudaMemcpyAsync(hc, counters, kCounterInts * sizeof(int32_t) * nch, cudaMemcpyDeviceToHost, s));
   RG_CUDA(ctx, cudaStreamSynchronize(s));
   if (prof) {
     for (int k = 0; k < nch; ++k) {
@@ -526,7 +526,7 @@ rg_status run_pipeline_overlapped(rg_ctx* ctx, const FrameJob& J, const rg_range
   }
   int64_t slots = 0;
   for (int k = 0; k < nch; ++k) {
-    const int32_t* c = hc + 4 * k;
+    const int32_t* c = hc + kCounterInts * k;
     if (c[1]) {  // this chunk overflowed its slot list: grow and re-run it alone
       ctx->slot_capacity = std::max(ctx->slot_capacity * 2, c[0] + c[0] / 4 + 64);
       const FrameJob Jk = sub(k);
@@ -1162,7 +1162,7 @@ rg_status rg_range_frames_host(rg_ctx* ctx, const rg_frame_batch* b, const rg_ra
   int32_t* st_o = DBUF(int32_t, ctx, B_DET_OFF, 2 * (size_t)(chunk + 1));
   rg_object_disparity* st_out = DBUF(rg_object_disparity, ctx, B_OUT, 2 * (size_t)chunk * b->out_stride);
   int32_t* st_cnt = DBUF(int32_t, ctx, B_OUT_CNT, 2 * (size_t)chunk);
-  int32_t* counters = DBUF(int32_t, ctx, B_COUNTERS, 4);
+  int32_t* counters = DBUF(int32_t, ctx, B_COUNTERS, kCounterInts);
   int32_t* hoffs = static_cast<int32_t*>(host_buf(ctx, 1, sizeof(int32_t) * 2 * (chunk + 1)));
   int32_t* hc = static_cast<int32_t*>(host_buf(ctx, 0, 4 * sizeof(int32_t)));
   NEED(st_l);

@@ -20,6 +20,9 @@ constexpr int kMatchThreads = 256;     // CTA size of the matcher
 constexpr int kWindowCodes = 12288;    // smem census window (48 KB)
 constexpr int kMaxOccluders = 128;     // per-object occluder boxes kept in smem
 constexpr int kAggCapacity = 4096;     // CLOSE blocks aggregated in smem
+// per-launch device counters of the batched pipeline: [0] slots planned,
+// [1] overflow flag, [2..3] Hamming evaluations (int64), [4] matcher work index
+constexpr int kCounterInts = 8;
 
 // Internal census layout of the batched pipeline: reference bits 0..24, bits
 // 25..31 = 0x73 (sign set).  A constant high part cancels in l ^ r, so Hamming
