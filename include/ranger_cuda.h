@@ -355,6 +355,37 @@ rg_status rg_auto_rect_frames(rg_ctx* ctx, const uint8_t* d_left,
                               int delta_max, const rg_bm_params* p, int32_t* d_best,
                               int64_t* d_counts, void* stream);
 
+/* ------------------------------------------------------ dense BM objects (8f row 3) */
+
+/* Pipeline::box_disparity (pipeline.hpp:304-328): median of the box's valid
+ * dense disparities, their count, and dynamic_disparity_variance
+ * (geometry.hpp:162-178) of the top-quartile "near" subset.  valid = 0: no
+ * valid pixel (std::nullopt); -1: a raw value outside [raw_lo, raw_hi]. */
+typedef struct {
+  int32_t valid;
+  int32_t count;
+  double median;
+  double variance;
+} rg_box_stats;
+
+/* box_disparity for n boxes of one raw map (HOST pointers; DisparityMap::raw,
+ * 1/16 px, kInvalid = -32768); every valid raw value must lie in
+ * [raw_lo, raw_hi] (the BM output range), raw_hi - raw_lo < 49152. */
+rg_status rg_box_disparity(rg_ctx* ctx, const int16_t* raw, int w, int h, const rg_detection* dets,
+                           int n, int raw_lo, int raw_hi, double sigma_obs2, double gamma,
+                           double sigma_sys2, rg_box_stats* out);
+/* The STEREO_BM branch of Pipeline::process_frame for one frame
+ * (pipeline.hpp:140-141, 207-224): bm_disparity on the device, select_objects
+ * (sorted, template_match.hpp:63-94), box_disparity per selected box;
+ * out[k] = {det_id, kind = classify_far_close, n_blocks_used = count,
+ * valid = has_value, disparity = median or 0, z_cam = 0}.  box_out and
+ * raw_out (w*h) are optional. */
+rg_status rg_dense_objects(rg_ctx* ctx, const uint8_t* left, const uint8_t* right, int w, int h,
+                           const rg_detection* dets, int n, const rg_ranger_config* cfg,
+                           const rg_bm_params* bm, double sigma_obs2, double gamma,
+                           double sigma_sys2, rg_object_disparity* out, rg_box_stats* box_out,
+                           int* n_out, int16_t* raw_out);
+
 /* ------------------------------------------------------ SGM (8f row 2) */
 
 /* SgmParams, sgm.hpp:14-19 */

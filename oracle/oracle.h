@@ -75,6 +75,13 @@ int ref_sgm_direction_pass(const uint8_t* cost, int w, int h, int nd, int p1, in
 int ref_sgm_disparity(const uint8_t* left, const uint8_t* right, int w, int h, int nd, int d_lo, int p1, int p2,
                       int16_t* out);
 
+/* dense BM objects (8f row 3): pipeline.hpp:304-328 */
+int orc_box_disparity(const int16_t* raw, int w, int h, const rg_detection* dets, int n, double sigma_obs2,
+                      double gamma, double sigma_sys2, rg_box_stats* out);
+/* geometry.hpp:162-178 on explicit samples (pins the restatement's variance) */
+int ref_dynamic_disparity_variance(const double* near_s, int n_near, const double* all_s, int n_all,
+                                   double sigma_obs2, double gamma, double sigma_sys2, double* out);
+
 /* reference-only extras (ref_shim.cpp) */
 int ref_render_stereo_pair(const rg_scene_config* cfg, const rg_scene_object* objs,
                            int n_obj, uint8_t* left, uint8_t* right);
@@ -83,8 +90,8 @@ int ref_ground_truth_detections(const rg_scene_config* cfg, const rg_scene_objec
 int ref_pipeline_sequence(const uint8_t* left, const uint8_t* right, int w, int h, int n_frames,
                           const rg_detection* dets, const int32_t* det_offsets, const rg_ranger_config* cfg,
                           const rg_rect_search_config* rect, double f, double b, double cx, double cy,
-                          double h_cam, rg_object_disparity* out, int out_stride, int32_t* out_count,
-                          double* rect_applied);
+                          double h_cam, int method, const rg_bm_params* bm, rg_object_disparity* out,
+                          int out_stride, int32_t* out_count, double* rect_applied);
 /* CPU baseline: range n_frames frames (left/right packed w*h each, dets CSR)
  * with `threads` host threads, each thread ranging whole frames at workers=1
  * (SURVEY.md 8(d) mode iii); returns wall seconds, fills out like

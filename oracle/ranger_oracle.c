@@ -986,3 +986,45 @@ int orc_sgm_disparity(const uint8_t* left, const uint8_t* right, int w, int h, i
   free(acc);
   return RG_OK;
 }
+
+/* ======================================================== dense BM objects (8f row 3) */
+
+/* pipeline.hpp:304-328 box_disparity + geometry.hpp:162-178 dynamic_disparity_variance */
+int orc_box_disparity(const int16_t* raw, int w, int h, const rg_detection* dets, int n, double sigma_obs2,
+                      double gamma, double sigma_sys2, rg_box_stats* out) {
+  for (int b = 0; b < n; ++b) {
+    const rg_detection* d = &dets[b];
+    const double bx0 = (d->cx - d->w / 2) * w, bx1 = (d->cx + d->w / 2) * w;
+    const double by0 = (d->cy - d->h / 2) * h, by1 = (d->cy + d->h / 2) * h;
+    int y0 = (int)floor(by0), y1 = (int)ceil(by1), x0 = (int)floor(bx0), x1 = (int)ceil(bx1);
+    if (y0 < 0) y0 = 0;
+    if (x0 < 0) x0 = 0;
+    if (y1 > h) y1 = h;
+    if (x1 > w) x1 = w;
+    const int bw = x1 > x0 ? x1 - x0 : 0, bh = y1 > y0 ? y1 - y0 : 0;
+    double* v = (double*)malloc(sizeof(double) * ((size_t)bw * bh + 1));
+    size_t m = 0;
+    for (int y = y0; y < y1; ++y)
+      for (int x = x0; x < x1; ++x) {
+        const int16_t r = raw[(size_t)y * w + x];
+        if (r != -32768) v[m++] = r / 16.0;
+      }
+    rg_box_stats o = {0, 0, 0.0, 0.0};
+    if (m > 0) {
+      qsort(v, m, sizeof(double), cmp_double);
+      const size_t near_from = (3 * (m - 1)) / 4;
+      double sn = 0, sa = 0;
+      for (size_t i = near_from; i < m; ++i) sn += v[i];
+      for (size_t i = 0; i < m; ++i) sa += v[i];
+      const double mean_near = sn / (double)(m - near_from), mean_all = sa / (double)m;
+      const double diff = mean_near - mean_all;
+      o.valid = 1;
+      o.count = (int32_t)m;
+      o.median = v[(m - 1) / 2];
+      o.variance = sigma_obs2 / (double)(m - near_from) + gamma * diff * diff + sigma_sys2;
+    }
+    out[b] = o;
+    free(v);
+  }
+  return RG_OK;
+}

@@ -410,18 +410,19 @@ double ref_bench_estimate(const uint8_t* left, const uint8_t* right, int w, int 
 }
 
 
-/* Pipeline::process_frame (pipeline.hpp:124-266), TEMPLATE_MATCHER method,
+/* Pipeline::process_frame (pipeline.hpp:124-266), TEMPLATE_MATCHER (method 0) or STEREO_BM (1),
  * over n_frames consecutive frames (packed w*h images, dets CSR); no radar.
  * out[f*out_stride + k], out_count[f]: PipelineResult::objects of frame f;
  * rect_applied[f]: RefinerLogRecord::rect_delta. */
 int ref_pipeline_sequence(const uint8_t* left, const uint8_t* right, int w, int h, int n_frames,
                           const rg_detection* dets, const int32_t* det_offsets, const rg_ranger_config* cfg,
                           const rg_rect_search_config* rect, double f, double b, double cx, double cy,
-                          double h_cam, rg_object_disparity* out, int out_stride, int32_t* out_count,
-                          double* rect_applied) {
+                          double h_cam, int method, const rg_bm_params* bm, rg_object_disparity* out,
+                          int out_stride, int32_t* out_count, double* rect_applied) {
   return guarded([&] {
     PipelineConfig pc;
-    pc.method = DepthMethod::kTemplateMatcher;
+    pc.method = method == 1 ? DepthMethod::kStereoBm : DepthMethod::kTemplateMatcher;
+    if (bm) pc.bm = to_bm(bm);
     pc.calib = make_calibration(f, b, cx, cy, h_cam);
     pc.ranger = to_cfg(cfg);
     pc.rect.enabled = rect->enabled != 0;
@@ -459,6 +460,15 @@ int ref_pipeline_sequence(const uint8_t* left, const uint8_t* right, int w, int 
   });
 }
 
+
+int ref_dynamic_disparity_variance(const double* near_s, int n_near, const double* all_s, int n_all,
+                                   double sigma_obs2, double gamma, double sigma_sys2, double* out) {
+  return guarded([&] {
+    const std::vector<double> a(near_s, near_s + n_near), b(all_s, all_s + n_all);
+    *out = dynamic_disparity_variance(a, b, sigma_obs2, gamma, sigma_sys2);
+    return RG_OK;
+  });
+}
 
 int ref_sgm_direction_pass(const uint8_t* cost, int w, int h, int nd, int p1, int p2, int sx, int sy,
                            int32_t* acc) {

@@ -65,6 +65,10 @@ class BmParams(C.Structure):
                 ("downscale", C.c_int32), ("texture_threshold", C.c_double), ("uniqueness_ratio", C.c_double)]
 
 
+class BoxStats(C.Structure):
+    _fields_ = [("valid", C.c_int32), ("count", C.c_int32), ("median", C.c_double), ("variance", C.c_double)]
+
+
 class SgmParams(C.Structure):
     _fields_ = [("num_disparities", C.c_int32), ("min_disparity", C.c_int32), ("p1", C.c_int32), ("p2", C.c_int32)]
 
@@ -148,6 +152,8 @@ SIGNATURES = {
     "rg_bm_disparity": (I, [P, P, P, I, I, P, P]),
     "rg_auto_rect_search": (I, [P, P, P, I, I, P, I, I, P, P, P]),
     "rg_auto_rect_frames": (I, [P, P, P, I, I64, I, I, I, P, I, I, P, P, P, P]),
+    "rg_box_disparity": (I, [P, P, I, I, P, I, I, I, D, D, D, P]),
+    "rg_dense_objects": (I, [P, P, P, I, I, P, I, P, P, D, D, D, P, P, P, P]),
     "rg_validate_sgm_params": (I, [P, P]),
     "rg_sgm_disparity": (I, [P, P, P, I, I, P, P]),
     "rg_sgm_frames": (I, [P, P, P, I, I64, I, I, I, P, P, P]),

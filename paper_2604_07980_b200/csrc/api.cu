@@ -1282,6 +1282,114 @@ rg_status rg_bm_disparity(rg_ctx* ctx, const uint8_t* left, const uint8_t* right
   return RG_OK;
 }
 
+// raw value range of bm_disparity's output (bm.hpp:113-135: the downscale
+// path matches over q and upscales raw by s)
+static void bm_raw_range(const rg_bm_params& p, int* lo, int* hi) {
+  const int s = p.downscale;
+  if (s <= 1) {
+    *lo = p.min_disparity * 16;
+    *hi = (p.min_disparity + p.num_disparities) * 16 - 1;
+    return;
+  }
+  const int qlo = (p.min_disparity + s - 1) / s;
+  const int qnd = std::max(1, (p.min_disparity + p.num_disparities) / s - qlo);
+  const int a = qlo * 16 * s, b = ((qlo + qnd) * 16 - 1) * s;
+  *lo = std::min(a, b);
+  *hi = std::max(a, b);
+}
+
+static rg_status box_stats_device(rg_ctx* ctx, const int16_t* draw, int w, int h, const rg_detection* ddets,
+                                  const std::vector<int32_t>& idx, int raw_lo, int raw_hi, double sigma_obs2,
+                                  double gamma, double sigma_sys2, std::vector<rg_box_stats>& res) {
+  const int nb = (int)idx.size();
+  res.assign(static_cast<size_t>(nb), rg_box_stats{});
+  if (nb == 0) return RG_OK;
+  const int nbins = raw_hi - raw_lo + 1;
+  if (nbins < 1 || nbins > 49152) return set_err(ctx, RG_EINVAL, "box_disparity: raw range too wide");
+  int32_t* didx = DBUF(int32_t, ctx, B_BOX_IDX, nb);
+  rg_box_stats* dout = DBUF(rg_box_stats, ctx, B_BOX_OUT, nb);
+  NEED(didx);
+  NEED(dout);
+  cudaStream_t st = ctx->stream;
+  RG_CUDA(ctx, cudaMemcpyAsync(didx, idx.data(), sizeof(int32_t) * nb, cudaMemcpyHostToDevice, st));
+  RG_CUDA(ctx, launch_box_disparity(draw, w, h, 0, ddets, didx, nullptr, nb, raw_lo, nbins, sigma_obs2, gamma,
+                                    sigma_sys2, dout, st));
+  count_launch(ctx, ST_AGG);
+  RG_CUDA(ctx, cudaMemcpyAsync(res.data(), dout, sizeof(rg_box_stats) * nb, cudaMemcpyDeviceToHost, st));
+  RG_CUDA(ctx, cudaStreamSynchronize(st));
+  for (const auto& r : res)
+    if (r.valid < 0) return set_err(ctx, RG_EINVAL, "box_disparity: raw value outside [raw_lo, raw_hi]");
+  return RG_OK;
+}
+
+rg_status rg_box_disparity(rg_ctx* ctx, const int16_t* raw, int w, int h, const rg_detection* dets, int n,
+                           int raw_lo, int raw_hi, double sigma_obs2, double gamma, double sigma_sys2,
+                           rg_box_stats* out) {
+  TRY(bind(ctx));
+  if (!raw || w < 1 || h < 1 || n < 0 || (n > 0 && (!dets || !out)))
+    return set_err(ctx, RG_EINVAL, "box_disparity: bad arguments");
+  if (n == 0) return RG_OK;
+  int16_t* draw = DBUF(int16_t, ctx, B_BM_OUT, (size_t)w * h);
+  NEED(draw);
+  RG_CUDA(ctx, cudaMemcpyAsync(draw, raw, sizeof(int16_t) * w * h, cudaMemcpyHostToDevice, ctx->stream));
+  rg_detection* dd = nullptr;
+  TRY(upload_dets(ctx, dets, n, &dd));
+  std::vector<int32_t> idx(static_cast<size_t>(n));
+  for (int i = 0; i < n; ++i) idx[i] = i;
+  std::vector<rg_box_stats> res;
+  TRY(box_stats_device(ctx, draw, w, h, dd, idx, raw_lo, raw_hi, sigma_obs2, gamma, sigma_sys2, res));
+  std::copy(res.begin(), res.end(), out);
+  return RG_OK;
+}
+
+rg_status rg_dense_objects(rg_ctx* ctx, const uint8_t* left, const uint8_t* right, int w, int h,
+                           const rg_detection* dets, int n, const rg_ranger_config* cfg, const rg_bm_params* bm,
+                           double sigma_obs2, double gamma, double sigma_sys2, rg_object_disparity* out,
+                           rg_box_stats* box_out, int* n_out, int16_t* raw_out) {
+  TRY(bind(ctx));
+  TRY(check_cfg(ctx, cfg));
+  TRY(check_bm(ctx, bm));
+  if (!left || !right || !n_out || w < 1 || h < 1 || n < 0 || (n > 0 && (!dets || !out)))
+    return set_err(ctx, RG_EINVAL, "dense_objects: bad arguments");
+  *n_out = 0;
+  // pipeline.hpp:140-141: the selected detections in input order
+  std::vector<int32_t> sel(static_cast<size_t>(std::max(n, 1)));
+  int ns = 0;
+  if (n > 0) TRY(rg_select_objects(ctx, dets, n, cfg, sel.data(), &ns));
+  sel.resize(static_cast<size_t>(ns));
+  std::sort(sel.begin(), sel.end());
+  // primary depth: the dense BM map on the device (pipeline.hpp:284-286)
+  uint8_t *dl = nullptr, *dr = nullptr;
+  TRY(upload_image(ctx, B_BM_L, left, w, h, &dl));
+  TRY(upload_image(ctx, B_BM_R, right, w, h, &dr));
+  int16_t* draw = DBUF(int16_t, ctx, B_BM_OUT, (size_t)w * h);
+  NEED(draw);
+  TRY(bm_device(ctx, dl, dr, w, h, *bm, draw, ctx->stream));
+  if (raw_out)
+    RG_CUDA(ctx, cudaMemcpyAsync(raw_out, draw, sizeof(int16_t) * w * h, cudaMemcpyDeviceToHost, ctx->stream));
+  rg_detection* dd = nullptr;
+  if (n > 0) TRY(upload_dets(ctx, dets, n, &dd));
+  int lo = 0, hi = 0;
+  bm_raw_range(*bm, &lo, &hi);
+  std::vector<rg_box_stats> res;
+  TRY(box_stats_device(ctx, draw, w, h, dd, sel, lo, hi, sigma_obs2, gamma, sigma_sys2, res));
+  // pipeline.hpp:218-224
+  for (int k = 0; k < ns; ++k) {
+    const rg_detection& d = dets[sel[k]];
+    rg_object_disparity o{};
+    o.det_id = d.id;
+    const double side = std::max(d.w * w, d.h * h);  // classify_far_close, template_match.hpp:63-67
+    o.kind = side < cfg->tau_s ? RG_KIND_FAR : RG_KIND_CLOSE;
+    o.valid = res[k].valid > 0;
+    o.disparity = o.valid ? res[k].median : 0.0;
+    o.n_blocks_used = o.valid ? res[k].count : 0;
+    out[k] = o;
+    if (box_out) box_out[k] = res[k];
+  }
+  *n_out = ns;
+  return RG_OK;
+}
+
 static rg_status check_rect(rg_ctx* ctx, int w, int h, const rg_rect* roi, int dmin, int dmax,
                             const rg_bm_params* p) {  // autorect.hpp:25-32
   if (!roi || !p) return set_err(ctx, RG_EINVAL, "auto_rect_search: null argument");

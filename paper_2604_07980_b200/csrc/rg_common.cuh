@@ -127,7 +127,7 @@ enum BufId {
   B_OBJ, B_SLOTS, B_SLOT_RES, B_OUT, B_OUT_CNT, B_COUNTERS, B_MAPX, B_MAPY,
   B_PTS, B_OFFS, B_RANGES, B_MRES, B_TMP0, B_TMP1, B_TMP2, B_TMP3, B_STATS,
   B_BM_L, B_BM_R, B_BM_OUT, B_BM_CNT, B_ROIS, B_STAGE_L, B_STAGE_R, B_SHIFT,
-  B_SEQ, B_SGM_COST, B_SGM_ACC, B_COUNT
+  B_SEQ, B_SGM_COST, B_SGM_ACC, B_BOX_IDX, B_BOX_OUT, B_COUNT
 };
 
 // error helpers (defined in api.cu)
@@ -177,6 +177,12 @@ cudaError_t launch_match_slots(const Slot* slots, int32_t* counters, int slot_ca
                                const PadGeom& gs, int img_w, int img_h, int trusted, int wide,
                                rg_ranger_config cfg, rg_match_result* res,
                                rg_ranger_stats* stats, int max_points, cudaStream_t s);
+
+// box statistics of dense maps (dense.cu)
+cudaError_t launch_box_disparity(const int16_t* raw, int w, int h, int64_t frame_stride, const rg_detection* dets,
+                                 const int32_t* box_det, const int32_t* box_frame, int n_boxes, int raw_lo,
+                                 int nbins, double sigma_obs2, double gamma, double sigma_sys2,
+                                 rg_box_stats* out, cudaStream_t s);
 
 // SGM (sgm.cu)
 cudaError_t launch_sgm_cost(const uint32_t* cl, const uint32_t* cr, int w, int h, int nd, int d_lo, uint8_t* cost,

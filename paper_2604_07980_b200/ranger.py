@@ -620,6 +620,47 @@ class RectOffsetState:
 
 
 @dataclass
+class BoxDisparity:
+    """Pipeline::BoxDisparity (pipeline.hpp:298-302)."""
+    median: float = 0.0
+    variance: float = 0.0
+    count: int = 0
+
+
+@dataclass
+class DenseVarianceParams:
+    """PipelineConfig sigma_obs2 / var_gamma / sigma_sys2 (pipeline.hpp:78-80 defaults)."""
+    sigma_obs2: float = 0.3
+    gamma: float = 1.0
+    sigma_sys2: float = 0.01
+
+
+def dense_objects(left, right, dets: Sequence[Detection], cfg: RangerConfig, bm: "BmParams",
+                  var: Optional[DenseVarianceParams] = None, ctx: Optional[Context] = None):
+    """The STEREO_BM branch of Pipeline::process_frame (pipeline.hpp:140-141,
+    207-224): dense BM on the device, select_objects, box_disparity per
+    selected box.  Returns ([ObjectDisparity], [Optional[BoxDisparity]], raw map)."""
+    ctx = ctx or default_context()
+    var = var or DenseVarianceParams()
+    L, R = _gray(left), _gray(right)
+    h, w = L.shape
+    arr = dets_array(dets)
+    n = len(dets)
+    out = (_abi.ObjectDisparity * max(n, 1))()
+    box = (_abi.BoxStats * max(n, 1))()
+    n_out = C.c_int()
+    raw = np.empty((h, w), np.int16)
+    c, b = cfg.to_c(), bm.to_c()
+    ctx.check(lib().rg_dense_objects(ctx.handle, _ptr(L), _ptr(R), w, h, arr, n, C.byref(c), C.byref(b),
+                                     float(var.sigma_obs2), float(var.gamma), float(var.sigma_sys2), out, box,
+                                     C.byref(n_out), _ptr(raw)))
+    objs = [ObjectDisparity(o.det_id, o.disparity, o.kind, o.n_blocks_used, bool(o.valid), o.z_cam)
+            for o in list(out)[:n_out.value]]
+    boxes = [BoxDisparity(x.median, x.variance, x.count) if x.valid > 0 else None for x in list(box)[:n_out.value]]
+    return objs, boxes, raw
+
+
+@dataclass
 class SgmParams:
     """sgm.hpp:14-19 with the reference's defaults."""
     num_disparities: int = 64

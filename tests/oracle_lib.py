@@ -50,7 +50,9 @@ class Checker:
             self.lib.ref_ground_truth_detections.restype = I
             self.lib.ref_ground_truth_detections.argtypes = [P, P, I, P, P]
             self.lib.ref_pipeline_sequence.restype = I
-            self.lib.ref_pipeline_sequence.argtypes = [P, P, I, I, I, P, P, P, P, D, D, D, D, D, P, I, P, P]
+            self.lib.ref_pipeline_sequence.argtypes = [P, P, I, I, I, P, P, P, P, D, D, D, D, D, I, P, P, I, P, P]
+            self.lib.ref_dynamic_disparity_variance.restype = I
+            self.lib.ref_dynamic_disparity_variance.argtypes = [P, I, P, I, D, D, D, P]
             self.lib.ref_bench_estimate.restype = D
             self.lib.ref_bench_estimate.argtypes = [P, P, I, I, I, P, P, P, I, P, I, P]
 
@@ -58,7 +60,9 @@ class Checker:
                          ("sgm_disparity", [P, P, I, I, I, I, I, I, P])):
             f = getattr(self.lib, prefix + nm)
             f.restype, f.argtypes = I, args
-        if prefix == "orc_":  # 9x7 extension (restatement only)
+        if prefix == "orc_":  # restatement-only entry points
+            self.lib.orc_box_disparity.restype = I
+            self.lib.orc_box_disparity.argtypes = [P, I, I, P, I, D, D, D, P]
             self.lib.orc_census_transform64.restype = I
             self.lib.orc_census_transform64.argtypes = [P, I, I, I, I, P]
             self.lib.orc_match_blocks64.restype = I

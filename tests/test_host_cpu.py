@@ -45,7 +45,7 @@ def test_struct_layouts_match_the_c_header():
                "rg_object_disparity": _abi.ObjectDisparity, "rg_ranger_stats": _abi.RangerStats,
                "rg_census_cache": _abi.CensusCache, "rg_bm_params": _abi.BmParams,
                "rg_frame_batch": _abi.FrameBatch, "rg_rect_search_config": _abi.RectSearchConfig,
-               "rg_rect_state": _abi.RectState, "rg_sgm_params": _abi.SgmParams, "rg_scene_object": _abi.SceneObject,
+               "rg_rect_state": _abi.RectState, "rg_sgm_params": _abi.SgmParams, "rg_box_stats": _abi.BoxStats, "rg_scene_object": _abi.SceneObject,
                "rg_scene_config": _abi.SceneConfig}
     for cname, py in structs.items():
         for f, _ in py._fields_:

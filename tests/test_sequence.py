@@ -102,7 +102,7 @@ def test_oracle_schedule_equals_reference_pipeline(orc):
     rc = rect.to_c()
     st = ref.lib.ref_pipeline_sequence(L.ctypes.data, R.ctypes.data, w, h, n, C.addressof(arr), offs.ctypes.data,
                                        C.byref(cfg.to_c()), C.byref(rc), sc.f, sc.b, sc.cx, sc.cy, sc.h_cam,
-                                       C.addressof(out), stride, cnt.ctypes.data, applied.ctypes.data)
+                                       0, None, C.addressof(out), stride, cnt.ctypes.data, applied.ctypes.data)
     assert st == 0
     # shifts actually move, and match the reference's applied rect offset
     assert any(s != 0 for s in shifts)
@@ -146,3 +146,96 @@ def test_range_sequence_matches_oracle(ctx, orc, enabled):
         want = b"".join(bytes(x) for x in objs[t])
         assert int(cnt[t]) * 32 == len(want)
         assert o[t, :len(want)].tobytes() == want, t
+
+
+# ------------------------------------------------------------ dense STEREO_BM branch (8f row 3)
+def test_oracle_box_variance_equals_reference(orc):
+    if not oracle_lib.have_reference():
+        pytest.skip("oracle/_ref not built here")
+    ref = oracle_lib.reference()
+    rng = np.random.default_rng(4)
+    for n in (1, 2, 7, 100):
+        raw = rng.integers(-40, 900, (1, n)).astype(np.int16)
+        d = _abi.Detection(0.5, 0.5, 1.0, 1.0, 0, 1)
+        got = _abi.BoxStats()
+        assert orc.lib.orc_box_disparity(raw.ctypes.data, n, 1, C.byref(d), 1, 0.3, 1.0, 0.01, C.byref(got)) == 0
+        v = np.sort(raw.ravel() / 16.0)
+        near = np.ascontiguousarray(v[(3 * (n - 1)) // 4:])
+        want = C.c_double()
+        assert ref.lib.ref_dynamic_disparity_variance(near.ctypes.data, len(near), v.ctypes.data, n, 0.3, 1.0, 0.01,
+                                                      C.byref(want)) == 0
+        assert got.variance == want.value and got.median == v[(n - 1) // 2] and got.count == n
+
+
+def test_oracle_dense_objects_equal_reference_pipeline(orc):
+    """The reference Pipeline with method STEREO_BM (no radar): its objects are
+    ObjectDisparity {det id, kind, box median, count} from box_disparity of
+    the dense BM map of the rect-corrected pair."""
+    if not oracle_lib.have_reference():
+        pytest.skip("oracle/_ref not built here")
+    ref = oracle_lib.reference()
+    L, R, D, cfg, sc = seq_frames([0, 0, 0])
+    n, h, w = L.shape
+    bm = rg.BmParams(32, 9, 0, 10, 10, 1)  # PipelineConfig::bm defaults (pipeline.hpp:67)
+    rect = rg.RectSearchConfig(enabled=False)
+    recs, offs = [], [0]
+    for d in D:
+        recs.extend(cdet(x) for x in d)
+        offs.append(len(recs))
+    arr = (_abi.Detection * len(recs))(*recs)
+    offs = np.asarray(offs, np.int32)
+    stride = max(len(d) for d in D)
+    out = (_abi.ObjectDisparity * (n * stride))()
+    cnt = np.zeros(n, np.int32)
+    applied = np.zeros(n)
+    assert ref.lib.ref_pipeline_sequence(L.ctypes.data, R.ctypes.data, w, h, n, C.addressof(arr), offs.ctypes.data,
+                                         C.byref(cfg.to_c()), C.byref(rect.to_c()), sc.f, sc.b, sc.cx, sc.cy,
+                                         sc.h_cam, 1, C.byref(bm.to_c()), C.addressof(out), stride, cnt.ctypes.data,
+                                         applied.ctypes.data) == 0
+    for t in range(n):
+        _, raw = orc.bm(L[t], R[t], bm.to_c())
+        sel = np.zeros(len(D[t]), np.int32)
+        ns = C.c_int()
+        dets = (_abi.Detection * len(D[t]))(*[cdet(x) for x in D[t]])
+        orc.fn("select_objects")(C.addressof(dets), len(D[t]), C.byref(cfg.to_c()), sel.ctypes.data, C.byref(ns))
+        idx = sorted(sel[:ns.value].tolist())
+        boxes = (_abi.Detection * max(len(idx), 1))(*[cdet(D[t][i]) for i in idx])
+        st = (_abi.BoxStats * max(len(idx), 1))()
+        assert orc.lib.orc_box_disparity(raw.ctypes.data, w, h, C.addressof(boxes), len(idx), 0.3, 1.0, 0.01,
+                                         C.addressof(st)) == 0
+        got = [(o.det_id, o.kind, o.n_blocks_used, o.valid, o.disparity) for o in list(out)[t * stride:t * stride + cnt[t]]]
+        want = []
+        for k, i in enumerate(idx):
+            d = D[t][i]
+            kind = 0 if max(d.w * w, d.h * h) < cfg.tau_s else 1
+            want.append((d.id, kind, st[k].count if st[k].valid else 0, int(st[k].valid > 0),
+                         st[k].median if st[k].valid else 0.0))
+        assert got == want, t
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("bs,nd,dmin,ds", [(9, 32, 0, 1), (7, 48, -4, 1), (9, 64, 0, 2)])
+def test_dense_objects_match_oracle(ctx, orc, bs, nd, dmin, ds):
+    L, R, D, cfg, sc = seq_frames([0, 1])
+    bm = rg.BmParams(nd, bs, dmin, 10, 10, ds)
+    for t in range(len(L)):
+        objs, boxes, raw = rg.dense_objects(L[t], R[t], D[t], cfg, bm, ctx=ctx)
+        st, want_raw = orc.bm(L[t], R[t], bm.to_c())
+        assert np.array_equal(raw, want_raw)
+        sel = np.zeros(len(D[t]), np.int32)
+        ns = C.c_int()
+        dets = (_abi.Detection * len(D[t]))(*[cdet(x) for x in D[t]])
+        orc.fn("select_objects")(C.addressof(dets), len(D[t]), C.byref(cfg.to_c()), sel.ctypes.data, C.byref(ns))
+        idx = sorted(sel[:ns.value].tolist())
+        bx = (_abi.Detection * max(len(idx), 1))(*[cdet(D[t][i]) for i in idx])
+        stt = (_abi.BoxStats * max(len(idx), 1))()
+        orc.lib.orc_box_disparity(want_raw.ctypes.data, sc.width, sc.height, C.addressof(bx), len(idx), 0.3, 1.0,
+                                  0.01, C.addressof(stt))
+        assert len(objs) == len(idx)
+        for k, i in enumerate(idx):
+            assert objs[k].det_id == D[t][i].id
+            assert objs[k].valid == (stt[k].valid > 0)
+            if objs[k].valid:
+                assert np.float64(objs[k].disparity).tobytes() == np.float64(stt[k].median).tobytes()
+                assert np.float64(boxes[k].variance).tobytes() == np.float64(stt[k].variance).tobytes()
+                assert boxes[k].count == stt[k].count == objs[k].n_blocks_used
