@@ -615,7 +615,11 @@ __global__ void __launch_bounds__(SB_W * 32, RG_BM_MINB) bm_simd_kernel(
         bool ok = true;
         if (sk != SB_INF && __dmul_rn((double)best, __dadd_rn(1.0, __ddiv_rn(uniq, 100.0))) >= (double)(sk >> 5))
           ok = false;
-        if (ok) {
+        if (ok && !raw) {
+          // count-only (autorect): raw > d_lo*16 <=> bi >= 1, since the
+          // parabolic offset of a minimum lies in [-1/2, 1/2] (no FP64 needed)
+          if (bi >= 1) ++valid_count;
+        } else if (ok) {
           double d_hat = (double)(d_lo + bi);
           if (bi > 0 && bi + 1 < nd && vm != SB_INF && vp != SB_INF)
             d_hat = __dadd_rn(d_hat, subpix((double)(vm >> 5), (double)best, (double)(vp >> 5)));
@@ -626,8 +630,8 @@ __global__ void __launch_bounds__(SB_W * 32, RG_BM_MINB) bm_simd_kernel(
         }
       }
     }
-    if (x < W) {
-      if (raw) raw[((int64_t)frame * n_delta + kd) * W * H + (int64_t)y * W + x] = (int16_t)out;
+    if (x < W && raw) {
+      raw[((int64_t)frame * n_delta + kd) * W * H + (int64_t)y * W + x] = (int16_t)out;
       if (out != kInvalid && out > lo_raw) ++valid_count;
     }
     __syncwarp();
