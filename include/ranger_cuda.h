@@ -278,6 +278,11 @@ typedef struct {
    * before ranging, shift_vertical(left, s) (image.hpp:145-154; the rect
    * correction of pipeline.hpp:135-138), folded into the census row addressing */
   const int32_t* d_left_shift;
+  /* nullable, n_frames*out_stride entries: receives the frame-local index of
+   * the detection behind d_out[f*out_stride + k] (the sorted `sel` of
+   * pipeline.hpp:140-141).  Device batches only: rg_range_frames_host rejects
+   * a non-null value. */
+  int32_t* d_out_index;
 } rg_frame_batch;
 
 rg_status rg_range_frames(rg_ctx* ctx, const rg_frame_batch* batch,
@@ -329,10 +334,92 @@ rg_status rg_filter_offset(rg_rect_state* st, int delta_star, double* applied);
  * addressing.  `b` holds DEVICE pointers as for rg_range_frames (its
  * d_left_shift is ignored); `st` is updated in place; out_shift / out_delta
  * (HOST, n_frames entries, nullable) receive the applied shifts and the raw
- * search results.  Asynchronous on `stream` after the host scan. */
+ * search results; out_rect_applied (HOST, nullable) the filtered offset in
+ * force for each frame (RefinerLogRecord::rect_delta).  Asynchronous on
+ * `stream` after the host scan. */
 rg_status rg_range_sequence(rg_ctx* ctx, const rg_frame_batch* b, const rg_ranger_config* cfg,
                             const rg_rect_search_config* rect, rg_rect_state* st,
-                            int32_t* out_shift, int32_t* out_delta, void* stream);
+                            int32_t* out_shift, int32_t* out_delta, double* out_rect_applied,
+                            void* stream);
+
+/* ------------------------------------------ per-frame records (host side) */
+
+/* The sequential tail of Pipeline::process_frame (pipeline.hpp:180-265 minus
+ * the tracker): object refiner, the stereo / ground-point / size cues,
+ * fuse_depth -> DepthRecord, RefinerLogRecord.  Host code (a few hundred
+ * flops per object), run after the device results of a batch are back. */
+
+/* StereoCalibration (geometry.hpp:101-110); R row-major camera -> vehicle.
+ * Q is derived as make_calibration does (geometry.hpp:118-127). */
+typedef struct {
+  double f, b, cx, cy, h_cam;
+  double R[9];
+  double t[3];
+} rg_calibration;
+
+typedef struct {
+  double x, y, z;
+} rg_vec3;
+
+/* ObjRefinerState (object_refiner.hpp:14-21) */
+typedef struct {
+  double prev_offset, beta, r_max, w_p, tau, rate_limit;
+} rg_obj_refiner_state;
+
+/* one entry of PipelineConfig::class_width_m (pipeline.hpp:78) */
+typedef struct {
+  int32_t class_id;
+  int32_t pad;
+  double width_m;
+} rg_class_width;
+
+typedef struct {
+  rg_calibration calib;
+  const rg_class_width* class_widths; /* host, n_class_widths entries, distinct ids */
+  int32_t n_class_widths;
+  int32_t object_refiner;   /* PipelineConfig::object_refiner (pipeline.hpp:66) */
+  double obj_cand_half_px;  /* pipeline.hpp:72 */
+  double obj_cand_step_px;
+  double fuse_sanity_ratio; /* TrackerConfig::fuse_sanity_ratio (tracker.hpp:18) */
+} rg_record_params;
+
+/* DepthSource (geometry.hpp:187) */
+enum { RG_SRC_STEREO = 0, RG_SRC_GPT = 1, RG_SRC_SIZE = 2 };
+
+/* DepthRecord (io.hpp:264-274); absent candidates are NaN */
+typedef struct {
+  int32_t frame_id;
+  int32_t det_id;
+  double disparity;
+  int32_t valid;
+  int32_t source;
+  double clp_by_stereo, clp_by_gpt, clp_by_size, z_fused;
+} rg_depth_record;
+
+/* RefinerLogRecord (io.hpp:225-230) */
+typedef struct {
+  int32_t frame_id;
+  int32_t pad;
+  double rect_delta, radar_offset, obj_offset;
+} rg_refiner_log;
+
+/* ObjRefinerState defaults (object_refiner.hpp:15-20) */
+rg_status rg_obj_refiner_state_init(rg_obj_refiner_state* st);
+/* make_calibration(f, b, cx, cy, h_cam) with the canonical rotation and
+ * t = (0, 0, h_cam) (geometry.hpp:130-133) */
+rg_status rg_make_calibration(double f, double b, double cx, double cy, double h_cam, rg_calibration* out);
+
+/* One frame of pipeline.hpp:180-249 for the TEMPLATE_MATCHER method
+ * (dense = 0) or a dense method (dense = 1, objects[k] = box medians, the
+ * radar refiner off).  dets: the frame's detections (HOST); sel[k]: the
+ * frame-local index of objects[k] (rg_frame_batch.d_out_index); objects is
+ * updated in place (object refiner offset); radar: the frame's radar
+ * positions (vehicle frame).  Writes n_obj records and one log entry. */
+rg_status rg_frame_records(const rg_record_params* p, int frame_id, int img_w, int img_h, int dense,
+                           const rg_detection* dets, int n_dets, const int32_t* sel,
+                           rg_object_disparity* objects, int n_obj, const rg_vec3* radar, int n_radar,
+                           rg_obj_refiner_state* st, double rect_applied, rg_depth_record* records,
+                           rg_refiner_log* log);
 
 /* ------------------------------------------------------ BM / autorect (K5) */
 

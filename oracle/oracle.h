@@ -92,6 +92,12 @@ int ref_pipeline_sequence(const uint8_t* left, const uint8_t* right, int w, int 
                           const rg_rect_search_config* rect, double f, double b, double cx, double cy,
                           double h_cam, int method, const rg_bm_params* bm, rg_object_disparity* out,
                           int out_stride, int32_t* out_count, double* rect_applied);
+int ref_pipeline_records(const uint8_t* left, const uint8_t* right, int w, int h, int n_frames,
+                         const rg_detection* dets, const int32_t* det_offsets, const double* radar_xyz,
+                         const int32_t* radar_offsets, const rg_ranger_config* cfg,
+                         const rg_rect_search_config* rect, const rg_record_params* rp, int method,
+                         const rg_bm_params* bm, rg_object_disparity* out, int out_stride, int32_t* out_count,
+                         rg_depth_record* recs, rg_refiner_log* logs);
 /* CPU baseline: range n_frames frames (left/right packed w*h each, dets CSR)
  * with `threads` host threads, each thread ranging whole frames at workers=1
  * (SURVEY.md 8(d) mode iii); returns wall seconds, fills out like

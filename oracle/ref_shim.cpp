@@ -461,6 +461,84 @@ int ref_pipeline_sequence(const uint8_t* left, const uint8_t* right, int w, int 
 }
 
 
+/* Pipeline::process_frame with radar and the per-frame records: objects,
+ * DepthRecord and RefinerLogRecord per frame (pipeline.hpp:124-265).
+ * radar_xyz: CSR (radar_offsets, n_frames + 1) of vehicle-frame positions. */
+int ref_pipeline_records(const uint8_t* left, const uint8_t* right, int w, int h, int n_frames,
+                         const rg_detection* dets, const int32_t* det_offsets, const double* radar_xyz,
+                         const int32_t* radar_offsets, const rg_ranger_config* cfg,
+                         const rg_rect_search_config* rect, const rg_record_params* rp, int method,
+                         const rg_bm_params* bm, rg_object_disparity* out, int out_stride, int32_t* out_count,
+                         rg_depth_record* recs, rg_refiner_log* logs) {
+  return guarded([&] {
+    PipelineConfig pc;
+    pc.method = method == 1 ? DepthMethod::kStereoBm : DepthMethod::kTemplateMatcher;
+    if (bm) pc.bm = to_bm(bm);
+    Mat3 R;
+    for (int i = 0; i < 9; ++i) R.m[i] = rp->calib.R[i];
+    pc.calib = make_calibration(rp->calib.f, rp->calib.b, rp->calib.cx, rp->calib.cy, rp->calib.h_cam, R,
+                                Vec3{rp->calib.t[0], rp->calib.t[1], rp->calib.t[2]});
+    pc.ranger = to_cfg(cfg);
+    pc.rect.enabled = rect->enabled != 0;
+    pc.rect.delta_min = rect->delta_min;
+    pc.rect.delta_max = rect->delta_max;
+    pc.rect.window = rect->window;
+    pc.rect.rate_limit = rect->rate_limit;
+    pc.rect.bm = to_bm(&rect->bm);
+    pc.object_refiner = rp->object_refiner != 0;
+    pc.radar_refiner = false;
+    pc.obj_cand_half_px = rp->obj_cand_half_px;
+    pc.obj_cand_step_px = rp->obj_cand_step_px;
+    pc.tracker.fuse_sanity_ratio = rp->fuse_sanity_ratio;
+    pc.class_width_m.clear();
+    for (int i = 0; i < rp->n_class_widths; ++i) pc.class_width_m[rp->class_widths[i].class_id] = rp->class_widths[i].width_m;
+    pc.workers = 1;
+    Pipeline pipe(pc);
+    const std::size_t img = std::size_t(w) * h;
+    for (int t = 0; t < n_frames; ++t) {
+      FrameInput in;
+      in.frame_id = t;
+      in.left = to_gray(left + img * t, w, h);
+      in.right = to_gray(right + img * t, w, h);
+      in.detections = to_dets(dets + det_offsets[t], det_offsets[t + 1] - det_offsets[t]);
+      for (int j = radar_offsets[t]; j < radar_offsets[t + 1]; ++j) {
+        RadarDetection r;
+        r.position = Vec3{radar_xyz[3 * j], radar_xyz[3 * j + 1], radar_xyz[3 * j + 2]};
+        in.radar.push_back(r);
+      }
+      PipelineResult res;
+      pipe.process_frame(in, res);
+      int k = 0;
+      for (const auto& fo : res.objects) {
+        if (k >= out_stride) break;
+        rg_object_disparity& o = out[std::size_t(t) * out_stride + k];
+        std::memset(&o, 0, sizeof(o));
+        o.det_id = fo.obj.det_id;
+        o.kind = fo.obj.kind == ObjectKind::kFar ? RG_KIND_FAR : RG_KIND_CLOSE;
+        o.n_blocks_used = fo.obj.n_blocks_used;
+        o.valid = fo.obj.valid;
+        o.disparity = fo.obj.disparity;
+        const DepthRecord& d = res.depth[std::size_t(k)];
+        rg_depth_record& r = recs[std::size_t(t) * out_stride + k];
+        r.frame_id = d.frame_id;
+        r.det_id = d.det_id;
+        r.disparity = d.disparity;
+        r.valid = d.valid;
+        r.source = d.source == DepthSource::kStereo ? RG_SRC_STEREO : d.source == DepthSource::kGpt ? RG_SRC_GPT : RG_SRC_SIZE;
+        r.clp_by_stereo = d.clp_by_stereo;
+        r.clp_by_gpt = d.clp_by_gpt;
+        r.clp_by_size = d.clp_by_size;
+        r.z_fused = d.z_fused;
+        ++k;
+      }
+      out_count[t] = k;
+      const RefinerLogRecord& lg = res.refiner_log.back();
+      logs[t] = rg_refiner_log{lg.frame_id, 0, lg.rect_delta, lg.radar_offset, lg.obj_offset};
+    }
+    return RG_OK;
+  });
+}
+
 int ref_dynamic_disparity_variance(const double* near_s, int n_near, const double* all_s, int n_all,
                                    double sigma_obs2, double gamma, double sigma_sys2, double* out) {
   return guarded([&] {

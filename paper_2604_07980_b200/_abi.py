@@ -93,7 +93,43 @@ class FrameBatch(C.Structure):
         ("d_dets", C.c_void_p), ("d_det_offsets", C.c_void_p), ("max_dets_per_frame", C.c_int32),
         ("out_stride", C.c_int32), ("d_out", C.c_void_p), ("d_out_count", C.c_void_p),
         ("focal_px", C.c_double), ("baseline_m", C.c_double), ("d_left_shift", C.c_void_p),
+        ("d_out_index", C.c_void_p),
     ]
+
+
+class Calibration(C.Structure):
+    _fields_ = [("f", C.c_double), ("b", C.c_double), ("cx", C.c_double), ("cy", C.c_double),
+                ("h_cam", C.c_double), ("R", C.c_double * 9), ("t", C.c_double * 3)]
+
+
+class Vec3(C.Structure):
+    _fields_ = [("x", C.c_double), ("y", C.c_double), ("z", C.c_double)]
+
+
+class ObjRefinerState(C.Structure):
+    _fields_ = [("prev_offset", C.c_double), ("beta", C.c_double), ("r_max", C.c_double), ("w_p", C.c_double),
+                ("tau", C.c_double), ("rate_limit", C.c_double)]
+
+
+class ClassWidth(C.Structure):
+    _fields_ = [("class_id", C.c_int32), ("pad", C.c_int32), ("width_m", C.c_double)]
+
+
+class RecordParams(C.Structure):
+    _fields_ = [("calib", Calibration), ("class_widths", C.c_void_p), ("n_class_widths", C.c_int32),
+                ("object_refiner", C.c_int32), ("obj_cand_half_px", C.c_double), ("obj_cand_step_px", C.c_double),
+                ("fuse_sanity_ratio", C.c_double)]
+
+
+class DepthRecord(C.Structure):
+    _fields_ = [("frame_id", C.c_int32), ("det_id", C.c_int32), ("disparity", C.c_double), ("valid", C.c_int32),
+                ("source", C.c_int32), ("clp_by_stereo", C.c_double), ("clp_by_gpt", C.c_double),
+                ("clp_by_size", C.c_double), ("z_fused", C.c_double)]
+
+
+class RefinerLog(C.Structure):
+    _fields_ = [("frame_id", C.c_int32), ("pad", C.c_int32), ("rect_delta", C.c_double),
+                ("radar_offset", C.c_double), ("obj_offset", C.c_double)]
 
 
 class SceneObject(C.Structure):
@@ -147,7 +183,10 @@ SIGNATURES = {
     "rg_range_frames_host": (I, [P, P, P, I, P]),
     "rg_rect_state_init": (I, [P, I, D]),
     "rg_filter_offset": (I, [P, I, P]),
-    "rg_range_sequence": (I, [P, P, P, P, P, P, P, P]),
+    "rg_range_sequence": (I, [P, P, P, P, P, P, P, P, P]),
+    "rg_obj_refiner_state_init": (I, [P]),
+    "rg_make_calibration": (I, [D, D, D, D, D, P]),
+    "rg_frame_records": (I, [P, I, I, I, I, P, I, P, P, I, P, I, P, D, P, P]),
     "rg_validate_bm_params": (I, [P, P]),
     "rg_bm_disparity": (I, [P, P, P, I, I, P, P]),
     "rg_auto_rect_search": (I, [P, P, P, I, I, P, I, I, P, P, P]),

@@ -224,6 +224,7 @@ struct FrameJob {
   const uint32_t* scaled_l = nullptr;
   const uint32_t* scaled_r = nullptr;
   const int32_t* left_shift = nullptr;  // device, n_frames entries (nullable)
+  int32_t* out_index = nullptr;         // device, like out (nullable)
 };
 
 bool same_geom(const PadGeom& a, const PadGeom& b) {
@@ -369,7 +370,7 @@ rg_status enqueue_match(rg_ctx* ctx, const FrameJob& J, const rg_ranger_config& 
   if (ev) RG_CUDA(ctx, cudaEventRecord(ev[0], s));
   // K3 planner
   RG_CUDA(ctx, launch_plan_frames(J.dets, J.det_off, F, w, h, cfg, J.out_stride, objs, J.out,
-                                  J.out_count, slots, capacity, counters, J.stats, s));
+                                  J.out_count, slots, capacity, counters, J.stats, J.out_index, s));
   count_launch(ctx, ST_PLAN);
   if (ev) RG_CUDA(ctx, cudaEventRecord(ev[1], s));
   // K2 fused sampler + forward/backward matcher, one warp per slot
@@ -492,6 +493,7 @@ rg_status run_pipeline_overlapped(rg_ctx* ctx, const FrameJob& J, const rg_range
     Jk.out_count = J.out_count + f0;
     Jk.stats = J.stats ? J.stats + f0 : nullptr;
     Jk.left_shift = J.left_shift ? J.left_shift + f0 : nullptr;
+    Jk.out_index = J.out_index ? J.out_index + (int64_t)f0 * J.out_stride : nullptr;
     return Jk;
   };
   for (int k = 0; k < nch; ++k) {
@@ -1131,6 +1133,7 @@ rg_status rg_range_frames(rg_ctx* ctx, const rg_frame_batch* b, const rg_ranger_
                 b->d_dets, b->d_det_offsets, b->out_stride, b->d_out, b->d_out_count, nullptr,
                 b->focal_px, b->baseline_m};
   J.left_shift = b->d_left_shift;
+  J.out_index = b->d_out_index;
   cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
   return run_pipeline_overlapped(ctx, J, *cfg, s);
 }
@@ -1145,6 +1148,7 @@ rg_status rg_range_frames_host(rg_ctx* ctx, const rg_frame_batch* b, const rg_ra
   if (b->max_dets_per_frame > 4096) return set_err(ctx, RG_EINVAL, "range_frames_host: > 4096 detections per frame");
   if (b->out_stride < std::min(b->max_dets_per_frame, cfg->max_objects))
     return set_err(ctx, RG_EINVAL, "range_frames_host: out_stride too small");
+  if (b->d_out_index) return set_err(ctx, RG_EINVAL, "range_frames_host: d_out_index is a device-batch output");
   if (chunk < 1) chunk = 16;
   const int F = b->n_frames;
   // compute on `stream` (or the context stream), H2D staging on copy_stream

@@ -29,7 +29,7 @@ __global__ void __launch_bounds__(PT) plan_frames_kernel(
     rg_ranger_config cfg, int out_stride, ObjEntry* __restrict__ objs,
     rg_object_disparity* __restrict__ out, int32_t* __restrict__ out_count,
     Slot* __restrict__ slots, int slot_capacity, int32_t* __restrict__ counters,
-    rg_ranger_stats* __restrict__ stats) {
+    rg_ranger_stats* __restrict__ stats, int32_t* __restrict__ out_index) {
   __shared__ unsigned char sel[kMaxDetsPerFrame];
   __shared__ int warp_tot[PT / 32];
   const int f = blockIdx.x;
@@ -85,6 +85,7 @@ __global__ void __launch_bounds__(PT) plan_frames_kernel(
       od.disparity = 0.0;
       od.z_cam = 0.0;
       out[g] = od;
+      if (out_index) out_index[g] = i;
       if (sb + ns > slot_capacity) {
         counters[1] = 1;  // overflow: the host grows the list and re-runs
       } else {
@@ -248,10 +249,10 @@ cudaError_t launch_plan_frames(const rg_detection* dets, const int32_t* det_off,
                                int h, rg_ranger_config cfg, int out_stride, ObjEntry* objs,
                                rg_object_disparity* out, int32_t* out_count, Slot* slots,
                                int slot_capacity, int32_t* counters, rg_ranger_stats* stats,
-                               cudaStream_t s) {
+                               int32_t* out_index, cudaStream_t s) {
   if (n_frames <= 0) return cudaSuccess;
   plan_frames_kernel<<<n_frames, PT, 0, s>>>(dets, det_off, w, h, cfg, out_stride, objs, out,
-                                             out_count, slots, slot_capacity, counters, stats);
+                                             out_count, slots, slot_capacity, counters, stats, out_index);
   return cudaGetLastError();
 }
 

@@ -56,7 +56,7 @@ rg_status rg_filter_offset(rg_rect_state* st, int delta_star, double* applied) {
 
 rg_status rg_range_sequence(rg_ctx* ctx, const rg_frame_batch* b, const rg_ranger_config* cfg,
                             const rg_rect_search_config* rect, rg_rect_state* st, int32_t* out_shift,
-                            int32_t* out_delta, void* stream) {
+                            int32_t* out_delta, double* out_rect_applied, void* stream) {
   if (!ctx) return RG_EINVAL;
   if (!b || !cfg || !rect || !st) return fail(ctx, RG_EINVAL, "range_sequence: null argument");
   if (b->n_frames < 0 || b->width < 1 || b->height < 1)
@@ -65,6 +65,7 @@ rg_status rg_range_sequence(rg_ctx* ctx, const rg_frame_batch* b, const rg_range
   if (F == 0) return RG_OK;
   cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
   std::vector<int32_t> delta(F, 0), shift(F, 0);
+  std::vector<double> applied(F, 0.0);
   if (rect->enabled) {
     if (rect->delta_min > rect->delta_max) return fail(ctx, RG_EINVAL, "range_sequence: empty offset range");
     if (st->window < 1 || st->window > RG_RECT_MAX_WINDOW)
@@ -85,6 +86,7 @@ rg_status rg_range_sequence(rg_ctx* ctx, const rg_frame_batch* b, const rg_range
     // host scan in frame order: the shift applied to frame t is the filter
     // state before frame t's own search result is pushed
     for (int t = 0; t < F; ++t) {
+      applied[t] = st->current;  // RefinerLogRecord::rect_delta (pipeline.hpp:134, 264)
       shift[t] = (int32_t)std::lround(st->current);
       if ((e = rg_filter_offset(st, delta[t], nullptr)) != RG_OK)
         return fail(ctx, e, "range_sequence: filter_offset");
@@ -103,6 +105,7 @@ rg_status rg_range_sequence(rg_ctx* ctx, const rg_frame_batch* b, const rg_range
   if (e != RG_OK) return e;
   if (out_shift) std::copy(shift.begin(), shift.end(), out_shift);
   if (out_delta) std::copy(delta.begin(), delta.end(), out_delta);
+  if (out_rect_applied) std::copy(applied.begin(), applied.end(), out_rect_applied);
   // (the pageable shift upload is staged before cudaMemcpyAsync returns, so
   // the host vector may go; pass B stays asynchronous on s)
   return RG_OK;

@@ -49,9 +49,10 @@ class FrameEngine:
         self.out_stride = max(1, min(max_dets_per_frame, cfg.max_objects))
         self.focal, self.baseline = focal_px, baseline_m
 
-    def _batch(self, n_frames, pitch, stride, left, right, dets, offs, out, cnt, shift=None) -> _abi.FrameBatch:
+    def _batch(self, n_frames, pitch, stride, left, right, dets, offs, out, cnt, shift=None,
+               out_index=None) -> _abi.FrameBatch:
         return _abi.FrameBatch(n_frames, self.w, self.h, pitch, stride, left, right, dets, offs, self.max_dets,
-                               self.out_stride, out, cnt, self.focal, self.baseline, shift)
+                               self.out_stride, out, cnt, self.focal, self.baseline, shift, out_index)
 
     def range_device(self, left, right, dets, offsets, out, out_count, stream=None, left_shift=None) -> None:
         """All arguments are CUDA torch tensors: left/right uint8 (F, H, pitch);
@@ -80,11 +81,15 @@ class FrameEngine:
         s = C.c_void_p(stream) if stream is not None else None
         self.ctx.check(lib().rg_range_frames_host(self.ctx.handle, C.byref(b), C.byref(self._c), chunk, s))
 
-    def range_sequence(self, left, right, dets, offsets, out, out_count, rect=None, state=None, stream=None):
+    def range_sequence(self, left, right, dets, offsets, out, out_count, rect=None, state=None, stream=None,
+                       out_index=None, applied=None):
         """Pipeline::process_frame's TEMPLATE_MATCHER loop over consecutive
         device frames (rg_range_sequence): offset search on every uncorrected
         pair, host filter scan, ranging of the rect-corrected pairs.  `state`
-        (RectOffsetState) is advanced in place; returns (shifts, delta_stars)."""
+        (RectOffsetState) is advanced in place; returns (shifts, delta_stars).
+        out_index (device int32, F*out_stride) receives the frame-local
+        detection index per output; applied (host float64, F) the rect offset
+        in force per frame."""
         from .ranger import RectOffsetState, RectSearchConfig, rect_state_from_c, rect_state_to_c
 
         rect = rect or RectSearchConfig()
@@ -92,14 +97,62 @@ class FrameEngine:
         F = left.shape[0]
         pitch = left.shape[2] if left.dim() == 3 else self.w
         b = self._batch(F, pitch, left.stride(0), left.data_ptr(), right.data_ptr(), dets.data_ptr(),
-                        offsets.data_ptr(), out.data_ptr(), out_count.data_ptr())
+                        offsets.data_ptr(), out.data_ptr(), out_count.data_ptr(),
+                        out_index=out_index.data_ptr() if out_index is not None else None)
         rc, sc = rect.to_c(), rect_state_to_c(state)
         shifts, deltas = np.zeros(F, np.int32), np.zeros(F, np.int32)
+        if applied is not None:
+            assert applied.dtype == np.float64 and applied.shape == (F,) and applied.flags.c_contiguous
         s = C.c_void_p(stream) if stream is not None else None
         self.ctx.check(lib().rg_range_sequence(self.ctx.handle, C.byref(b), C.byref(self._c), C.byref(rc),
-                                               C.byref(sc), shifts.ctypes.data, deltas.ctypes.data, s))
+                                               C.byref(sc), shifts.ctypes.data, deltas.ctypes.data,
+                                               applied.ctypes.data if applied is not None else None, s))
         rect_state_from_c(sc, state)
         return shifts, deltas
+
+    def pipeline_frames(self, left, right, frames_dets, params, radar=None, frame_ids=None, rect=None,
+                        rect_state=None, obj_state=None, stream=None):
+        """Pipeline::process_frame, TEMPLATE_MATCHER method, over consecutive
+        device frames minus the tracker (pipeline.hpp:124-265): the device
+        two-pass frame loop (rg_range_sequence) then, per frame in order on
+        the host, the object refiner, the depth cues and fusion
+        (rg_frame_records).  frames_dets: per-frame lists of Detection;
+        radar: per-frame (n, 3) vehicle-frame positions (or None).
+        Returns (objects per frame, DepthRecords per frame, RefinerLog per frame)."""
+        import torch
+
+        from .ranger import ObjRefinerState, RectOffsetState, RectSearchConfig, frame_records
+
+        F = left.shape[0]
+        dev = left.device
+        rect = rect or RectSearchConfig()
+        rect_state = rect_state if rect_state is not None else RectOffsetState(rect.window, rect.rate_limit)
+        obj_state = obj_state if obj_state is not None else ObjRefinerState()
+        recs, offs = pack_detections(frames_dets)
+        d_dets = torch.from_numpy(recs.view(np.uint8).copy() if len(recs) else np.zeros(1, np.uint8)).to(dev)
+        d_offs = torch.from_numpy(offs).to(dev)
+        out = torch.zeros(F * self.out_stride * OUT_DTYPE.itemsize, dtype=torch.uint8, device=dev)
+        cnt = torch.zeros(F, dtype=torch.int32, device=dev)
+        idx = torch.zeros(F * self.out_stride, dtype=torch.int32, device=dev)
+        applied = np.zeros(F, np.float64)
+        self.range_sequence(left, right, d_dets, d_offs, out, cnt, rect=rect, state=rect_state, stream=stream,
+                            out_index=idx, applied=applied)
+        if stream is not None:
+            torch.cuda.ExternalStream(stream).synchronize()
+        else:
+            torch.cuda.synchronize(dev)
+        objs = unpack_results(out.cpu().numpy(), cnt.cpu().numpy(), self.out_stride)
+        sel = idx.cpu().numpy().reshape(F, self.out_stride)
+        all_objs, all_recs, logs = [], [], []
+        for f in range(F):
+            n = len(objs[f])
+            fid = int(frame_ids[f]) if frame_ids is not None else f
+            o, r, lg = frame_records(params, fid, self.w, self.h, recs[offs[f]:offs[f + 1]], sel[f, :n], objs[f],
+                                     radar[f] if radar is not None else None, obj_state, float(applied[f]))
+            all_objs.append(o)
+            all_recs.append(r)
+            logs.append(lg)
+        return all_objs, all_recs, logs
 
     def auto_rect_device(self, left, right, roi, delta_min: int, delta_max: int, bm, best, counts=None,
                          stream=None) -> None:

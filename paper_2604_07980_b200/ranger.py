@@ -731,6 +731,89 @@ def filter_offset(st: RectOffsetState, delta_star: int) -> float:
     return st.current
 
 
+class Calibration:
+    """StereoCalibration built by make_calibration(f, b, cx, cy, h_cam)
+    (geometry.hpp:101-133): canonical camera->vehicle rotation, t = (0, 0, h_cam)."""
+
+    def __init__(self, f: float, b: float, cx: float, cy: float, h_cam: float):
+        self._c = _abi.Calibration()
+        if lib().rg_make_calibration(f, b, cx, cy, h_cam, C.byref(self._c)) != _abi.RG_OK:
+            raise InvalidArgument("make_calibration: f and b must be positive")
+
+    def to_c(self) -> _abi.Calibration:
+        return self._c
+
+
+@dataclass
+class ObjRefinerState:
+    """object_refiner.hpp:14-21 (defaults)."""
+    prev_offset: float = 0.0
+    beta: float = 0.1
+    r_max: float = 5.0
+    w_p: float = 1.0
+    tau: float = 0.5
+    rate_limit: float = 0.5
+
+    def to_c(self) -> _abi.ObjRefinerState:
+        return _abi.ObjRefinerState(self.prev_offset, self.beta, self.r_max, self.w_p, self.tau, self.rate_limit)
+
+    def update(self, c: _abi.ObjRefinerState) -> None:
+        self.prev_offset = c.prev_offset
+
+
+@dataclass
+class RecordParams:
+    """The PipelineConfig fields the per-frame records use (pipeline.hpp:64-79,
+    tracker.hpp:18): calibration, class widths, object refiner switches and
+    the fusion sanity ratio."""
+    calib: Calibration
+    class_width_m: dict = field(default_factory=lambda: {0: 1.9, 1: 2.5})
+    object_refiner: bool = True
+    obj_cand_half_px: float = 2.0
+    obj_cand_step_px: float = 0.25
+    fuse_sanity_ratio: float = 0.5
+
+    def to_c(self):
+        cw = (_abi.ClassWidth * max(1, len(self.class_width_m)))()
+        for i, (k, v) in enumerate(sorted(self.class_width_m.items())):
+            cw[i] = _abi.ClassWidth(int(k), 0, float(v))
+        p = _abi.RecordParams(self.calib.to_c(), C.cast(cw, C.c_void_p), len(self.class_width_m),
+                              int(self.object_refiner), self.obj_cand_half_px, self.obj_cand_step_px,
+                              self.fuse_sanity_ratio)
+        return p, cw  # keep cw alive while p is in use
+
+
+DEPTH_SOURCES = ("STEREO", "GPT", "SIZE")  # DepthSource (geometry.hpp:187), io.hpp:76-82 spelling
+
+
+def frame_records(params: RecordParams, frame_id: int, img_w: int, img_h: int, dets: np.ndarray,
+                  sel: np.ndarray, objects: np.ndarray, radar: Optional[np.ndarray], state: ObjRefinerState,
+                  rect_applied: float = 0.0, dense: bool = False):
+    """rg_frame_records: pipeline.hpp:180-249 for one frame (host code in the
+    library).  dets: the frame's DET_DTYPE records; sel: int32 frame-local
+    index per object; objects: OUT_DTYPE records (not modified); radar: (n, 3)
+    float64 vehicle-frame positions.  Returns (objects after the object
+    refiner offset, list of _abi.DepthRecord, _abi.RefinerLog)."""
+    objects = np.array(objects, copy=True)
+    dets = np.ascontiguousarray(dets)
+    n = len(objects)
+    sel = np.ascontiguousarray(sel, np.int32)
+    radar = np.ascontiguousarray(radar if radar is not None else np.zeros((0, 3)), np.float64).reshape(-1, 3)
+    recs = (_abi.DepthRecord * max(1, n))()
+    log = _abi.RefinerLog()
+    p, keep = params.to_c()
+    st = state.to_c()
+    rc = lib().rg_frame_records(C.byref(p), frame_id, img_w, img_h, int(dense), dets.ctypes.data if len(dets) else None,
+                                len(dets), sel.ctypes.data, objects.ctypes.data if n else None, n,
+                                radar.ctypes.data if len(radar) else None, len(radar), C.byref(st), rect_applied,
+                                recs, C.byref(log))
+    del keep
+    if rc != _abi.RG_OK:
+        raise InvalidArgument("frame_records: invalid input (reproject / radar behind camera / indices)")
+    state.update(st)
+    return objects, list(recs)[:n], log
+
+
 def range_z(disparity: float, focal_px: float, baseline_m: float) -> float:
     """geometry.hpp:142-146 with the canonical Q (:124-127): z = f / ((1/b) d)."""
     return focal_px / ((1.0 / baseline_m) * disparity)

@@ -51,6 +51,8 @@ class Checker:
             self.lib.ref_ground_truth_detections.argtypes = [P, P, I, P, P]
             self.lib.ref_pipeline_sequence.restype = I
             self.lib.ref_pipeline_sequence.argtypes = [P, P, I, I, I, P, P, P, P, D, D, D, D, D, I, P, P, I, P, P]
+            self.lib.ref_pipeline_records.restype = I
+            self.lib.ref_pipeline_records.argtypes = [P, P, I, I, I, P, P, P, P, P, P, P, I, P, P, I, P, P, P]
             self.lib.ref_dynamic_disparity_variance.restype = I
             self.lib.ref_dynamic_disparity_variance.argtypes = [P, I, P, I, D, D, D, P]
             self.lib.ref_bench_estimate.restype = D

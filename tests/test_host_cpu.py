@@ -46,7 +46,10 @@ def test_struct_layouts_match_the_c_header():
                "rg_census_cache": _abi.CensusCache, "rg_bm_params": _abi.BmParams,
                "rg_frame_batch": _abi.FrameBatch, "rg_rect_search_config": _abi.RectSearchConfig,
                "rg_rect_state": _abi.RectState, "rg_sgm_params": _abi.SgmParams, "rg_box_stats": _abi.BoxStats, "rg_scene_object": _abi.SceneObject,
-               "rg_scene_config": _abi.SceneConfig}
+               "rg_scene_config": _abi.SceneConfig, "rg_calibration": _abi.Calibration, "rg_vec3": _abi.Vec3,
+               "rg_obj_refiner_state": _abi.ObjRefinerState, "rg_class_width": _abi.ClassWidth,
+               "rg_record_params": _abi.RecordParams, "rg_depth_record": _abi.DepthRecord,
+               "rg_refiner_log": _abi.RefinerLog}
     for cname, py in structs.items():
         for f, _ in py._fields_:
             src += f'printf("{cname}.{f} %zu\\n", offsetof({cname}, {f}));\n'
