@@ -413,19 +413,20 @@ void accumulate_profile(rg_ctx* ctx) {
 rg_status finish_pipeline(rg_ctx* ctx, const FrameJob& J, const rg_ranger_config& cfg,
                           cudaStream_t s, int32_t* counters, int32_t* hc, PipelineBufs* pb) {
   for (int attempt = 0;; ++attempt) {
-    RG_CUDA(ctx, cudaMemcpyAsync(hc, counters, 4 * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    RG_CUDA(ctx, cudaMemcpyAsync(hc, counters, kCounterInts * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     RG_CUDA(ctx, cudaStreamSynchronize(s));
     accumulate_profile(ctx);
-    ctx->last_slots = hc[0];
+    const int used = hc[0] + hc[4];  // FAR slots from the bottom, CLOSE slots from the top
+    ctx->last_slots = used;
     if (!hc[1]) {
       int64_t ev;
       std::memcpy(&ev, hc + 2, sizeof(ev));
       ctx->hamming_evals += ev;
-      ctx->slots_total += hc[0];
+      ctx->slots_total += used;
       return RG_OK;
     }
     if (attempt >= 3) return set_err(ctx, RG_EOVERFLOW, "device block list overflow");
-    ctx->slot_capacity = std::max(ctx->slot_capacity * 2, hc[0] + hc[0] / 4 + 64);
+    ctx->slot_capacity = std::max(ctx->slot_capacity * 2, used + used / 4 + 64);
     TRY(enqueue_pipeline(ctx, J, cfg, s, counters, pb));
   }
 }
@@ -530,7 +531,7 @@ rg_status run_pipeline_overlapped(rg_ctx* ctx, const FrameJob& J, const rg_range
   for (int k = 0; k < nch; ++k) {
     const int32_t* c = hc + kCounterInts * k;
     if (c[1]) {  // this chunk overflowed its slot list: grow and re-run it alone
-      ctx->slot_capacity = std::max(ctx->slot_capacity * 2, c[0] + c[0] / 4 + 64);
+      ctx->slot_capacity = std::max(ctx->slot_capacity * 2, c[0] + c[4] + (c[0] + c[4]) / 4 + 64);
       const FrameJob Jk = sub(k);
       TRY(run_pipeline(ctx, Jk, cfg, s, nullptr));
       continue;
@@ -538,8 +539,8 @@ rg_status run_pipeline_overlapped(rg_ctx* ctx, const FrameJob& J, const rg_range
     int64_t ev;
     std::memcpy(&ev, c + 2, sizeof(ev));
     ctx->hamming_evals += ev;
-    ctx->slots_total += c[0];
-    slots += c[0];
+    ctx->slots_total += c[0] + c[4];
+    slots += c[0] + c[4];
   }
   ctx->last_slots = slots;
   return RG_OK;
@@ -1053,7 +1054,7 @@ rg_status rg_estimate_object_disparities(rg_ctx* ctx, const uint8_t* left, const
 
   // fill an empty cache with ROI-masked codes (template_match.hpp:304-321)
   if (cache && (!cache->has_full || !cache->has_scaled)) {
-    const int nslots = (int)ctx->last_slots;
+    const int nslots = pb.capacity;  // CLOSE slots sit at the top of the list
     std::vector<ObjEntry> objs(static_cast<size_t>(hcnt));
     std::vector<rg_match_result> res(static_cast<size_t>(std::max(nslots, 1)));
     if (hcnt > 0)

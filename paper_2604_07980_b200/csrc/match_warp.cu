@@ -450,7 +450,14 @@ __global__ void __launch_bounds__(WPB * 32, MINB) match_slots_warp_kernel(
   const int slot = blockIdx.x * WPB + warp;
   // an overflowed plan (counters[1], set by K3) is re-run with a bigger list:
   // skip it entirely; otherwise only planned slots inside the list exist
-  if (counters[1] || slot >= min(counters[0], capacity)) return;  // warp-uniform
+  // (FAR slots [0, counters[0]), CLOSE slots [capacity - counters[4], capacity);
+  // the two regions meeting is an overflow too)
+  const int n_lo = counters[0], n_hi = counters[4];
+  if (n_lo + n_hi > capacity) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) counters[1] = 1;
+    return;
+  }
+  if (counters[1] || (slot >= n_lo && slot < capacity - n_hi) || slot >= capacity) return;  // warp-uniform
   // per warp: maxp sampled points + maxp valid points
   unsigned char* wbase = wsm_raw + (size_t)warp * (maxp * sizeof(int2) + (maxp + 1) * sizeof(VPoint<CT>));
   int2* pts = reinterpret_cast<int2*>(wbase);
@@ -559,12 +566,11 @@ cudaError_t launch_match_slots(const Slot* slots, int32_t* counters, int slot_ca
 #define RG_ARGS slots, counters, slot_capacity, objs, dets, det_off, fl, fr, gf, sl, sr, gs, img_w, img_h, \
                 trusted, cfg, res, stats, max_points, s
   if (wide) return launch_variant<unsigned long long, 8, 2>(RG_ARGS);  // 9x7 extension
-  switch (variant) {  // A/B knobs; default measured best (tools/variants.sh)
-    case 1: return launch_variant<uint32_t, 4, 8>(RG_ARGS);
-    case 2: return launch_variant<uint32_t, 16, 2>(RG_ARGS);
-    case 3: return launch_variant<uint32_t, 8, 5>(RG_ARGS);
-    case 4: return launch_variant<uint32_t, 4, 1>(RG_ARGS);
-    default: return launch_variant<uint32_t, 8, 4>(RG_ARGS);
+  switch (variant) {  // A/B knobs; default measured best (tools/census_time.py with RG_MATCH_VARIANT)
+    case 1: return launch_variant<uint32_t, 8, 4>(RG_ARGS);
+    case 2: return launch_variant<uint32_t, 8, 5>(RG_ARGS);
+    case 3: return launch_variant<uint32_t, 16, 4>(RG_ARGS);
+    default: return launch_variant<uint32_t, 16, 3>(RG_ARGS);
   }
 #undef RG_ARGS
 }

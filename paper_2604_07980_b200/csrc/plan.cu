@@ -65,7 +65,13 @@ __global__ void __launch_bounds__(PT) plan_frames_kernel(
       int rows = 1, cols = 1;
       if (kind == RG_KIND_CLOSE) dev_close_grid(pixel_box(di, w, h), cfg, &rows, &cols);
       const int ns = rows * cols;
-      const int sb = atomicAdd(&counters[0], ns);
+      // FAR blocks fill the slot list from the bottom, CLOSE sub-blocks from
+      // the top: the matcher's CTAs then hold slots of one kind, whose costs
+      // are alike (a FAR block is ~5x a CLOSE sub-block at C2), instead of a
+      // few FAR warps holding a whole CTA of finished CLOSE warps; the
+      // heavier FAR CTAs are also dispatched first (shorter tail)
+      const int sb = kind == RG_KIND_FAR ? atomicAdd(&counters[0], ns)
+                                         : slot_capacity - atomicAdd(&counters[4], ns) - ns;
       ObjEntry e;
       e.det = d0 + i;
       e.kind = kind;
@@ -86,7 +92,7 @@ __global__ void __launch_bounds__(PT) plan_frames_kernel(
       od.z_cam = 0.0;
       out[g] = od;
       if (out_index) out_index[g] = i;
-      if (sb + ns > slot_capacity) {
+      if (sb < 0 || sb + ns > slot_capacity) {
         counters[1] = 1;  // overflow: the host grows the list and re-runs
       } else {
         for (int t = 0; t < ns; ++t) slots[sb + t] = Slot{f, g, t, 0};
