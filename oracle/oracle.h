@@ -98,6 +98,10 @@ int ref_pipeline_records(const uint8_t* left, const uint8_t* right, int w, int h
                          const rg_rect_search_config* rect, const rg_record_params* rp, int method,
                          const rg_bm_params* bm, rg_object_disparity* out, int out_stride, int32_t* out_count,
                          rg_depth_record* recs, rg_refiner_log* logs);
+int ref_save_synthetic_run(const rg_scene_config* sc, const rg_scene_object* objs, int n_obj, int n_frames,
+                           double dt, const char* dir);
+int ref_run_directory(const char* dir, const char* out_dir, const rg_ranger_config* cfg,
+                      const rg_rect_search_config* rect, int object_refiner, double fuse_ratio);
 /* CPU baseline: range n_frames frames (left/right packed w*h each, dets CSR)
  * with `threads` host threads, each thread ranging whole frames at workers=1
  * (SURVEY.md 8(d) mode iii); returns wall seconds, fills out like

@@ -539,6 +539,41 @@ int ref_pipeline_records(const uint8_t* left, const uint8_t* right, int w, int h
   });
 }
 
+/* make_synthetic_frames + save_synthetic_run (pipeline.hpp:415-471): a
+ * reference-written run directory. */
+int ref_save_synthetic_run(const rg_scene_config* sc, const rg_scene_object* objs, int n_obj, int n_frames,
+                           double dt, const char* dir) {
+  return guarded([&] {
+    const SceneConfig scene = to_scene(sc, objs, n_obj);
+    save_synthetic_run(make_synthetic_frames(scene, n_frames, dt), scene, dir);
+    return RG_OK;
+  });
+}
+
+/* load_run_directory -> Pipeline (TEMPLATE_MATCHER, calib.txt of the run,
+ * radar refiner off) -> save_pipeline_outputs (pipeline.hpp:354-406). */
+int ref_run_directory(const char* dir, const char* out_dir, const rg_ranger_config* cfg,
+                      const rg_rect_search_config* rect, int object_refiner, double fuse_ratio) {
+  return guarded([&] {
+    PipelineConfig pc;
+    pc.method = DepthMethod::kTemplateMatcher;
+    pc.calib = load_calibration(std::string(dir) + "/calib.txt");
+    pc.ranger = to_cfg(cfg);
+    pc.rect.enabled = rect->enabled != 0;
+    pc.rect.delta_min = rect->delta_min;
+    pc.rect.delta_max = rect->delta_max;
+    pc.rect.window = rect->window;
+    pc.rect.rate_limit = rect->rate_limit;
+    pc.rect.bm = to_bm(&rect->bm);
+    pc.object_refiner = object_refiner != 0;
+    pc.radar_refiner = false;
+    pc.tracker.fuse_sanity_ratio = fuse_ratio;
+    pc.workers = 1;
+    save_pipeline_outputs(run_pipeline(pc, load_run_directory(dir)), out_dir);
+    return RG_OK;
+  });
+}
+
 int ref_dynamic_disparity_variance(const double* near_s, int n_near, const double* all_s, int n_all,
                                    double sigma_obs2, double gamma, double sigma_sys2, double* out) {
   return guarded([&] {

@@ -732,13 +732,24 @@ def filter_offset(st: RectOffsetState, delta_star: int) -> float:
 
 
 class Calibration:
-    """StereoCalibration built by make_calibration(f, b, cx, cy, h_cam)
-    (geometry.hpp:101-133): canonical camera->vehicle rotation, t = (0, 0, h_cam)."""
+    """StereoCalibration built by make_calibration (geometry.hpp:101-133):
+    the canonical camera->vehicle rotation and t = (0, 0, h_cam) unless R
+    (row-major, 9 values) / t are given."""
 
-    def __init__(self, f: float, b: float, cx: float, cy: float, h_cam: float):
+    def __init__(self, f: float, b: float, cx: float, cy: float, h_cam: float, R=None, t=None):
         self._c = _abi.Calibration()
         if lib().rg_make_calibration(f, b, cx, cy, h_cam, C.byref(self._c)) != _abi.RG_OK:
             raise InvalidArgument("make_calibration: f and b must be positive")
+        if R is not None:
+            r = np.asarray(R, np.float64).reshape(9)
+            m = r.reshape(3, 3)  # is_rotation(R, 1e-6), geometry.hpp:65-72, 110-111
+            if np.abs(m.T @ m - np.eye(3)).max() > 1e-6 or abs(np.linalg.det(m) - 1.0) > 1e-6:
+                raise InvalidArgument("make_calibration: R is not a rotation")
+            for i in range(9):
+                self._c.R[i] = float(r[i])
+        if t is not None:
+            for i in range(3):
+                self._c.t[i] = float(t[i])
 
     def to_c(self) -> _abi.Calibration:
         return self._c

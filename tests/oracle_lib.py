@@ -53,6 +53,10 @@ class Checker:
             self.lib.ref_pipeline_sequence.argtypes = [P, P, I, I, I, P, P, P, P, D, D, D, D, D, I, P, P, I, P, P]
             self.lib.ref_pipeline_records.restype = I
             self.lib.ref_pipeline_records.argtypes = [P, P, I, I, I, P, P, P, P, P, P, P, I, P, P, I, P, P, P]
+            self.lib.ref_save_synthetic_run.restype = I
+            self.lib.ref_save_synthetic_run.argtypes = [P, P, I, I, D, C.c_char_p]
+            self.lib.ref_run_directory.restype = I
+            self.lib.ref_run_directory.argtypes = [C.c_char_p, C.c_char_p, P, P, I, D]
             self.lib.ref_dynamic_disparity_variance.restype = I
             self.lib.ref_dynamic_disparity_variance.argtypes = [P, I, P, I, D, D, D, P]
             self.lib.ref_bench_estimate.restype = D
