@@ -376,7 +376,7 @@ rg_status enqueue_match(rg_ctx* ctx, const FrameJob& J, const rg_ranger_config& 
   // K2 fused sampler + forward/backward matcher, one warp per slot
   const int trusted = !(J.full_l || J.scaled_l);
   RG_CUDA(ctx, launch_match_slots(slots, counters, capacity, objs, J.dets, J.det_off, fl, fr, R.gf, sl, sr, R.gs,
-                                  w, h, trusted, (int)R.wide, cfg, res, J.stats, maxp, s));
+                                  w, h, trusted, (int)R.wide, cfg, res, J.stats, maxp, s, F));
   count_launch(ctx, ST_MATCH);
   if (ev) RG_CUDA(ctx, cudaEventRecord(ev[2], s));
   // K4 aggregation + range

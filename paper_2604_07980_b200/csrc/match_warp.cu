@@ -45,7 +45,8 @@ namespace {
 #define RG_MW_NOINLINE 0
 #endif
 constexpr int kPipeUnroll = RG_MW_PIPE_UNROLL;
-constexpr int kWarpOcc = 32;      // occluder boxes per warp kept in smem
+constexpr int kWarpOcc = 32;
+constexpr int kLatencyFrames = 4;  // batches up to this size use the latency-mode matcher      // occluder boxes per warp kept in smem
 constexpr int CMAX = RG_MW_CMAX;  // 32-wide dx chunks per sweep (balanced groups)
 constexpr int TAIL = RG_MW_TAIL;  // a last chunk with <= TAIL candidates goes point-parallel
 
@@ -117,7 +118,10 @@ __device__ __forceinline__ unsigned long long fast_key(int sum, int dx, int dy) 
 
 // One sweep over K dx-chunks for one dy: `base` = this lane's sample pointer
 // for chunk c0 at offset 0; chunk c reads 32*c codes to the left.
-template <typename CT, int MODE, int K>
+// PF > 0 (latency mode): the lines of point k+1+PF are prefetched into L1
+// while point k is consumed -- a small batch leaves most SMs idle and each
+// warp's point loop then waits on L2 latency, not on issue.
+template <typename CT, int MODE, int K, int PF = 0>
 __device__ __forceinline__ void sweep(const VPoint<CT>* __restrict__ vp, int nv, const CT* base,
                                       int lane, int c0, int ndx, int dx_min, int dy, Cand& best,
                                       unsigned long long& bkey, int& evals) {
@@ -162,6 +166,11 @@ __device__ __forceinline__ void sweep(const VPoint<CT>* __restrict__ vp, int nv,
     const CT* a = reinterpret_cast<const CT*>(reinterpret_cast<const char*>(base) + qn.off);
 #pragma unroll
     for (int c = 0; c < K; ++c) rn[c] = __ldg(a - 32 * c);
+    if (PF > 0) {
+      const CT* pa = reinterpret_cast<const CT*>(reinterpret_cast<const char*>(base) + vp[min(k + 1 + PF, nv)].off);
+#pragma unroll
+      for (int c = 0; c < K; ++c) asm volatile("prefetch.global.L1 [%0];" ::"l"(pa - 32 * c));
+    }
 #endif
 #pragma unroll
     for (int c = 0; c < K; ++c) {
@@ -204,7 +213,7 @@ __device__ __forceinline__ void sweep(const VPoint<CT>* __restrict__ vp, int nv,
   }
 }
 
-template <typename CT, int MODE>
+template <typename CT, int MODE, int PF = 0>
 __device__ __forceinline__ void sweep_chunks(const VPoint<CT>* vp, int nv, const CT* base, int lane,
                                              int c0, int k, int ndx, int dx_min, int dy, Cand& best,
                                              unsigned long long& bkey, int& evals) {
@@ -212,7 +221,7 @@ __device__ __forceinline__ void sweep_chunks(const VPoint<CT>* vp, int nv, const
 #define RG_SWEEP_CASE(K)                                                                                 \
   case K:                                                                                                \
     if (K <= CMAX)                                                                                       \
-      sweep<CT, MODE, (K <= CMAX ? K : 1)>(vp, nv, base, lane, c0, ndx, dx_min, dy, best, bkey, evals); \
+      sweep<CT, MODE, (K <= CMAX ? K : 1), PF>(vp, nv, base, lane, c0, ndx, dx_min, dy, best, bkey, evals); \
     break;
   switch (k) {
     RG_SWEEP_CASE(1)
@@ -273,7 +282,7 @@ __device__ __forceinline__ void sweep_tail(const VPoint<CT>* vp, int nv, const C
 #ifndef RG_MW_RANGE_NOINLINE
 #define RG_MW_RANGE_NOINLINE 0
 #endif
-template <typename CT, int MODE>
+template <typename CT, int MODE, int PF = 0>
 #if RG_MW_RANGE_NOINLINE
 __device__ __noinline__ void sweep_range(
 #else
@@ -281,24 +290,27 @@ __device__ __forceinline__ void sweep_range(
 #endif
     const VPoint<CT>* vp, int nv, const CT* R, const PadGeom& g,
                                             const rg_search_range& rg, int lane, Cand& best,
-                                            unsigned long long& bkey, int& evals) {
+                                            unsigned long long& bkey, int& evals, int part = 0, int nparts = 1) {
   // lane-parallel chunks in balanced groups of <= CMAX; a short tail chunk
-  // goes point-parallel
+  // goes point-parallel.  nparts > 1: this warp sweeps the chunks
+  // [part * nfull / nparts, (part + 1) * nfull / nparts) of every row offset
+  // and the last part the tail (cooperative FAR blocks, latency mode)
   const int ndx = rg.dx_max - rg.dx_min + 1;
   const int nch = (ndx + 31) / 32;
   const int mt = ndx & 31;
   const bool ptail = mt != 0 && mt <= TAIL;
   const int nfull = ptail ? ndx >> 5 : nch;
-  const int groups = (nfull + CMAX - 1) / CMAX;
-  const int gq = groups ? nfull / groups : 0, gr = groups ? nfull - gq * groups : 0;  // balanced group sizes
+  const int cb = part * nfull / nparts, ce = (part + 1) * nfull / nparts, nmine = ce - cb;
+  const int groups = (nmine + CMAX - 1) / CMAX;
+  const int gq = groups ? nmine / groups : 0, gr = groups ? nmine - gq * groups : 0;  // balanced group sizes
   for (int dy = rg.dy_min; dy <= rg.dy_max; ++dy) {
-    for (int gi = 0, c0 = 0; gi < groups; ++gi) {
+    for (int gi = 0, c0 = cb; gi < groups; ++gi) {
       const int k = gq + (gi < gr ? 1 : 0);
       const CT* base = R + (int64_t)dy * g.pitch - rg.dx_min - lane - 32 * c0;
-      sweep_chunks<CT, MODE>(vp, nv, base, lane, c0, k, ndx, rg.dx_min, dy, best, bkey, evals);
+      sweep_chunks<CT, MODE, PF>(vp, nv, base, lane, c0, k, ndx, rg.dx_min, dy, best, bkey, evals);
       c0 += k;
     }
-    if (ptail)
+    if (ptail && part == nparts - 1)
       sweep_tail<CT, MODE>(vp, nv, R + (int64_t)dy * g.pitch, rg.dx_min + 32 * nfull, mt, dy, lane, best, bkey,
                            evals);
   }
@@ -307,7 +319,7 @@ __device__ __forceinline__ void sweep_range(
 // One block_match pass (census.hpp:178-272) by the calling warp.
 // pts: the block's points (smem), shifted by (sx, sy); L: raster of the left
 // codes, R: raster sampled at (x - dx, y + dy).  Both share geometry g.
-template <typename CT>
+template <typename CT, int PF = 0>
 #if RG_MW_NOINLINE
 __device__ __noinline__ Pass warp_pass(
 #else
@@ -315,7 +327,7 @@ __device__ Pass warp_pass(
 #endif
     const int2* pts, int np, int sx, int sy, const CT* L, const CT* R,
                           const PadGeom& g, bool trusted, const rg_search_range& rg, VPoint<CT>* vp,
-                          int lane, int& evals) {
+                          int lane, int& evals, int part = 0, int nparts = 1, Cand* xc = nullptr) {
   Pass o = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   int nv = 0;
   int xmin = INT_MAX, xmax = INT_MIN, ymin = INT_MAX, ymax = INT_MIN;
@@ -360,10 +372,19 @@ __device__ Pass warp_pass(
   Cand best = {0, 0, 0, 0};
   if (fast) {
     unsigned long long bkey = ~0ull;
-    sweep_range<CT, M_FAST>(vp, nv, R, g, rg, lane, best, bkey, evals);
+    sweep_range<CT, M_FAST, PF>(vp, nv, R, g, rg, lane, best, bkey, evals, part, nparts);
     // warp argmin of the packed keys (64-bit: two 32-bit reductions)
-    const uint32_t hi = __reduce_min_sync(0xffffffffu, (uint32_t)(bkey >> 32));
-    const uint32_t lo = __reduce_min_sync(0xffffffffu, (uint32_t)(bkey >> 32) == hi ? (uint32_t)bkey : ~0u);
+    uint32_t hi = __reduce_min_sync(0xffffffffu, (uint32_t)(bkey >> 32));
+    uint32_t lo = __reduce_min_sync(0xffffffffu, (uint32_t)(bkey >> 32) == hi ? (uint32_t)bkey : ~0u);
+    if (nparts > 1) {  // across the CTA's warps (same vp, same decision in every warp)
+      if (lane == 0) xc[part] = Cand{(int)hi, (int)lo, 0, 0};
+      __syncthreads();
+      for (int q = 0; q < nparts; ++q) {
+        const uint32_t h2 = (uint32_t)xc[q].sum, l2 = (uint32_t)xc[q].n;
+        if (h2 < hi || (h2 == hi && l2 < lo)) hi = h2, lo = l2;
+      }
+      __syncthreads();
+    }
     const int adx = (int)(lo >> 17);
     best.sum = (int)hi;
     best.n = nv;
@@ -372,9 +393,9 @@ __device__ Pass warp_pass(
   } else {
     unsigned long long unused = 0;
     if (trusted)
-      sweep_range<CT, M_SIGN>(vp, nv, R, g, rg, lane, best, unused, evals);
+      sweep_range<CT, M_SIGN, PF>(vp, nv, R, g, rg, lane, best, unused, evals, part, nparts);
     else
-      sweep_range<CT, M_GENERIC>(vp, nv, R, g, rg, lane, best, unused, evals);
+      sweep_range<CT, M_GENERIC, PF>(vp, nv, R, g, rg, lane, best, unused, evals, part, nparts);
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {  // warp argmin
       Cand u;
@@ -383,6 +404,13 @@ __device__ Pass warp_pass(
       u.dx = __shfl_xor_sync(0xffffffffu, best.dx, off);
       u.dy = __shfl_xor_sync(0xffffffffu, best.dy, off);
       if (better(u, best)) best = u;
+    }
+    if (nparts > 1) {  // across the CTA's warps (a total order: any merge order)
+      if (lane == 0) xc[part] = best;
+      __syncthreads();
+      for (int q = 0; q < nparts; ++q)
+        if (better(xc[q], best)) best = xc[q];
+      __syncthreads();
     }
   }
   if (best.n == 0) return o;
@@ -435,7 +463,10 @@ __device__ __forceinline__ void finish(const Pass& p, rg_match_result& r) {  // 
   }
 }
 
-template <typename CT, int WPB, int MINB>
+// COOP (latency mode): a CTA per FAR block, its warps splitting the dx
+// chunks of both passes (the FAR block is the critical path of a small
+// batch: ~5x a CLOSE sub-block); CLOSE sub-blocks stay one per warp.
+template <typename CT, int WPB, int MINB, int PF = 0, bool COOP = false>
 __global__ void __launch_bounds__(WPB * 32, MINB) match_slots_warp_kernel(
     const Slot* __restrict__ slots, int32_t* __restrict__ counters, const ObjEntry* __restrict__ objs,
     const rg_detection* __restrict__ dets, const int32_t* __restrict__ det_off,
@@ -446,8 +477,9 @@ __global__ void __launch_bounds__(WPB * 32, MINB) match_slots_warp_kernel(
   extern __shared__ __align__(16) unsigned char wsm_raw[];
   __shared__ double occ[WPB][4 * kWarpOcc];
   __shared__ int nocc[WPB];
+  __shared__ Cand xc[WPB];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int slot = blockIdx.x * WPB + warp;
+  int slot = blockIdx.x * WPB + warp, part = 0, nparts = 1;
   // an overflowed plan (counters[1], set by K3) is re-run with a bigger list:
   // skip it entirely; otherwise only planned slots inside the list exist
   // (FAR slots [0, counters[0]), CLOSE slots [capacity - counters[4], capacity);
@@ -457,7 +489,19 @@ __global__ void __launch_bounds__(WPB * 32, MINB) match_slots_warp_kernel(
     if (blockIdx.x == 0 && threadIdx.x == 0) counters[1] = 1;
     return;
   }
-  if (counters[1] || (slot >= n_lo && slot < capacity - n_hi) || slot >= capacity) return;  // warp-uniform
+  if (COOP) {  // CTA b < n_lo: FAR slot b; then CLOSE slots WPB per CTA from capacity - n_hi
+    if (counters[1]) return;
+    if ((int)blockIdx.x < n_lo) {
+      slot = blockIdx.x;
+      part = warp;
+      nparts = WPB;
+    } else {
+      slot = capacity - n_hi + ((int)blockIdx.x - n_lo) * WPB + warp;
+      if (slot >= capacity) return;  // warp-uniform; no CTA barrier in this case
+    }
+  } else if (counters[1] || (slot >= n_lo && slot < capacity - n_hi) || slot >= capacity) {
+    return;  // warp-uniform
+  }
   // per warp: maxp sampled points + maxp valid points
   unsigned char* wbase = wsm_raw + (size_t)warp * (maxp * sizeof(int2) + (maxp + 1) * sizeof(VPoint<CT>));
   int2* pts = reinterpret_cast<int2*>(wbase);
@@ -507,11 +551,12 @@ __global__ void __launch_bounds__(WPB * 32, MINB) match_slots_warp_kernel(
     const int sc = cfg.close_scale;
     const rg_search_range rg = far ? rg_search_range{0, cfg.dx_max_far, -1, 1}
                                    : rg_search_range{0, (cfg.dx_max_close + sc - 1) / sc, -1, 1};
-    const Pass f = warp_pass<CT>(pts, np, 0, 0, L, R, g, trusted != 0, rg, vp, lane, evals);
+    const Pass f = warp_pass<CT, PF>(pts, np, 0, 0, L, R, g, trusted != 0, rg, vp, lane, evals, part, nparts, xc);
     if (f.has) {
       finish(f, r);
       const rg_search_range brg = {-rg.dx_max, -rg.dx_min, -f.dy, -f.dy};
-      const Pass b = warp_pass<CT>(pts, np, -f.dx, f.dy, R, L, g, trusted != 0, brg, vp, lane, evals);
+      const Pass b = warp_pass<CT, PF>(pts, np, -f.dx, f.dy, R, L, g, trusted != 0, brg, vp, lane, evals, part,
+                                       nparts, xc);
       if (b.has) {
         rg_match_result rb;
         finish(b, rb);
@@ -521,28 +566,32 @@ __global__ void __launch_bounds__(WPB * 32, MINB) match_slots_warp_kernel(
   }
   evals = __reduce_add_sync(0xffffffffu, evals);
   if (lane == 0) {
-    res[slot] = r;
     if (evals) atomicAdd(reinterpret_cast<unsigned long long*>(counters + 2), (unsigned long long)evals);
-    if (stats && np >= 4) atomicAdd(reinterpret_cast<unsigned long long*>(&stats[s.frame].query_points),
-                                    (unsigned long long)np);
+    if (part == 0) {
+      res[slot] = r;
+      if (stats && np >= 4) atomicAdd(reinterpret_cast<unsigned long long*>(&stats[s.frame].query_points),
+                                      (unsigned long long)np);
+    }
   }
 }
 
-template <typename CT, int WPB, int MINB>
+template <typename CT, int WPB, int MINB, int PF = 0, bool COOP = false>
 cudaError_t launch_variant(const Slot* slots, int32_t* counters, int slot_capacity,
                                   const ObjEntry* objs, const rg_detection* dets, const int32_t* det_off,
                                   const void* fl, const void* fr, const PadGeom& gf, const void* sl,
                                   const void* sr, const PadGeom& gs, int img_w, int img_h, int trusted,
                                   rg_ranger_config cfg, rg_match_result* res, rg_ranger_stats* stats,
                                   int max_points, cudaStream_t s) {
-  auto kern = match_slots_warp_kernel<CT, WPB, MINB>;
+  auto kern = match_slots_warp_kernel<CT, WPB, MINB, PF, COOP>;
   max_points = (max_points + 1) & ~1;  // keeps every warp's VPoint array 16-B aligned
   const size_t smem = (sizeof(int2) * (size_t)max_points + sizeof(VPoint<CT>) * (size_t)(max_points + 1)) * WPB;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
-  const int grid = (slot_capacity + WPB - 1) / WPB;
+  // COOP: up to one CTA per slot (FAR CTAs + CLOSE CTAs <= capacity); the
+  // CTAs past the planned slots exit at once
+  const int grid = COOP ? slot_capacity : (slot_capacity + WPB - 1) / WPB;
   kern<<<grid, WPB * 32, smem, s>>>(slots, counters, objs, dets, det_off, static_cast<const CT*>(fl),
                                     static_cast<const CT*>(fr), gf, static_cast<const CT*>(sl),
                                     static_cast<const CT*>(sr), gs, img_w, img_h, trusted, cfg, res, stats,
@@ -557,7 +606,8 @@ cudaError_t launch_match_slots(const Slot* slots, int32_t* counters, int slot_ca
                                const void* fl, const void* fr, const PadGeom& gf, const void* sl,
                                const void* sr, const PadGeom& gs, int img_w, int img_h, int trusted,
                                int wide, rg_ranger_config cfg, rg_match_result* res,
-                               rg_ranger_stats* stats, int max_points, cudaStream_t s) {
+                               rg_ranger_stats* stats, int max_points, cudaStream_t s,
+                               int n_frames) {
   if (slot_capacity <= 0) return cudaSuccess;
   static int variant = [] {
     const char* v = getenv("RG_MATCH_VARIANT");
@@ -566,6 +616,11 @@ cudaError_t launch_match_slots(const Slot* slots, int32_t* counters, int slot_ca
 #define RG_ARGS slots, counters, slot_capacity, objs, dets, det_off, fl, fr, gf, sl, sr, gs, img_w, img_h, \
                 trusted, cfg, res, stats, max_points, s
   if (wide) return launch_variant<unsigned long long, 8, 2>(RG_ARGS);  // 9x7 extension
+  // latency mode (a few frames): most SMs would idle and each warp's point
+  // loop waits on L2, so small CTAs spread over every SM and L1 prefetch of
+  // the point 4 ahead (single C2 frame: 84 -> 68 us)
+  if (variant == 0 && n_frames > 0 && n_frames <= kLatencyFrames)
+    return launch_variant<uint32_t, 4, 12, 4, true>(RG_ARGS);
   switch (variant) {  // A/B knobs; default measured best (tools/census_time.py with RG_MATCH_VARIANT)
     case 1: return launch_variant<uint32_t, 8, 4>(RG_ARGS);
     case 2: return launch_variant<uint32_t, 8, 5>(RG_ARGS);

@@ -23,6 +23,7 @@ namespace {
 
 constexpr int PT = 256;
 constexpr int kMaxDetsPerFrame = 4096;
+constexpr int kKeyCap = 1024;  // detections per frame ranked from shared-memory keys
 
 __global__ void __launch_bounds__(PT) plan_frames_kernel(
     const rg_detection* __restrict__ dets, const int32_t* __restrict__ det_off, int w, int h,
@@ -32,16 +33,47 @@ __global__ void __launch_bounds__(PT) plan_frames_kernel(
     rg_ranger_stats* __restrict__ stats, int32_t* __restrict__ out_index) {
   __shared__ unsigned char sel[kMaxDetsPerFrame];
   __shared__ int warp_tot[PT / 32];
+  __shared__ int warp_sf[PT / 32], warp_sc[PT / 32], chunk_base[2];
+  __shared__ double s_key[kKeyCap];
+  __shared__ int s_id[kKeyCap];
+  __shared__ bool s_front[kKeyCap];
   const int f = blockIdx.x;
   const int d0 = det_off[f], n = det_off[f + 1] - d0;
   const rg_detection* D = dets + d0;
   // rank of every detection in the priority order; selected iff rank < budget
-  for (int i = threadIdx.x; i < n; i += PT) {
-    const rg_detection di = D[i];
-    int rank = 0;
-    for (int j = 0; j < n && rank < cfg.max_objects; ++j)
-      if (j != i && dev_precedes(D[j], j, di, i, cfg)) ++rank;
-    sel[i] = rank < cfg.max_objects;
+  if (n <= kKeyCap) {
+    // dev_precedes on precomputed keys: frontal flag, then area (frontal) or
+    // box bottom (else), then id, then index -- the same doubles, so the same
+    // order, without re-deriving both keys for every pair
+    for (int i = threadIdx.x; i < n; i += PT) {
+      const rg_detection d = D[i];
+      const bool f = dev_frontal(d, cfg);
+      s_front[i] = f;
+      s_key[i] = f ? __dmul_rn(d.w, d.h) : __dadd_rn(d.cy, half_of(d.h));
+      s_id[i] = d.id;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += PT) {
+      const bool fi = s_front[i];
+      const double ki = s_key[i];
+      const int idi = s_id[i];
+      int rank = 0;
+      for (int j = 0; j < n && rank < cfg.max_objects; ++j) {
+        const bool fj = s_front[j];
+        const double kj = s_key[j];
+        const bool prec = fj != fi ? fj : kj != ki ? kj > ki : s_id[j] != idi ? s_id[j] < idi : j < i;
+        rank += (j != i && prec) ? 1 : 0;
+      }
+      sel[i] = rank < cfg.max_objects;
+    }
+  } else {
+    for (int i = threadIdx.x; i < n; i += PT) {
+      const rg_detection di = D[i];
+      int rank = 0;
+      for (int j = 0; j < n && rank < cfg.max_objects; ++j)
+        if (j != i && dev_precedes(D[j], j, di, i, cfg)) ++rank;
+      sel[i] = rank < cfg.max_objects;
+    }
   }
   __syncthreads();
   // selected objects in input order: block-wide exclusive scan over chunks
@@ -58,20 +90,44 @@ __global__ void __launch_bounds__(PT) plan_frames_kernel(
       if (q < wid) before += warp_tot[q];
       total += warp_tot[q];
     }
+    // kind and sub-block grid of this thread's object, then one block-wide
+    // exclusive scan of the slot counts per kind and ONE atomic per kind and
+    // chunk (per-object atomics on the same two counters serialised the
+    // planner: 23 -> ~10 us for one C2 frame)
+    int kind = RG_KIND_FAR, rows = 1, cols = 1;
+    rg_detection di{};
     if (flag) {
-      const int k = base_k + before + __popc(bal & ((1u << lane) - 1u));
-      const rg_detection di = D[i];
-      const int kind = dev_classify(di, w, h, cfg.tau_s);
-      int rows = 1, cols = 1;
+      di = D[i];
+      kind = dev_classify(di, w, h, cfg.tau_s);
       if (kind == RG_KIND_CLOSE) dev_close_grid(pixel_box(di, w, h), cfg, &rows, &cols);
-      const int ns = rows * cols;
+    }
+    const int ns = flag ? rows * cols : 0;
+    int incf = kind == RG_KIND_FAR ? ns : 0, incc = kind == RG_KIND_CLOSE ? ns : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int uf = __shfl_up_sync(0xffffffffu, incf, o), uc = __shfl_up_sync(0xffffffffu, incc, o);
+      if (lane >= o) incf += uf, incc += uc;
+    }
+    if (lane == 31) warp_sf[wid] = incf, warp_sc[wid] = incc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int tf = 0, tc = 0;
+      for (int q = 0; q < PT / 32; ++q) tf += warp_sf[q], tc += warp_sc[q];
       // FAR blocks fill the slot list from the bottom, CLOSE sub-blocks from
       // the top: the matcher's CTAs then hold slots of one kind, whose costs
       // are alike (a FAR block is ~5x a CLOSE sub-block at C2), instead of a
       // few FAR warps holding a whole CTA of finished CLOSE warps; the
       // heavier FAR CTAs are also dispatched first (shorter tail)
-      const int sb = kind == RG_KIND_FAR ? atomicAdd(&counters[0], ns)
-                                         : slot_capacity - atomicAdd(&counters[4], ns) - ns;
+      chunk_base[0] = tf ? atomicAdd(&counters[0], tf) : 0;
+      chunk_base[1] = tc ? atomicAdd(&counters[4], tc) : 0;
+    }
+    __syncthreads();
+    if (flag) {
+      const int k = base_k + before + __popc(bal & ((1u << lane) - 1u));
+      int pf = 0, pc = 0;
+      for (int q = 0; q < wid; ++q) pf += warp_sf[q], pc += warp_sc[q];
+      const int sb = kind == RG_KIND_FAR ? chunk_base[0] + pf + incf - ns
+                                         : slot_capacity - (chunk_base[1] + pc + incc);
       ObjEntry e;
       e.det = d0 + i;
       e.kind = kind;

@@ -176,7 +176,8 @@ cudaError_t launch_match_slots(const Slot* slots, int32_t* counters, int slot_ca
                                const PadGeom& gf, const void* sl, const void* sr,
                                const PadGeom& gs, int img_w, int img_h, int trusted, int wide,
                                rg_ranger_config cfg, rg_match_result* res,
-                               rg_ranger_stats* stats, int max_points, cudaStream_t s);
+                               rg_ranger_stats* stats, int max_points, cudaStream_t s,
+                               int n_frames = 0);
 
 // box statistics of dense maps (dense.cu)
 cudaError_t launch_box_disparity(const int16_t* raw, int w, int h, int64_t frame_stride, const rg_detection* dets,
