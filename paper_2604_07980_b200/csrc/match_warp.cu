@@ -616,15 +616,17 @@ cudaError_t launch_match_slots(const Slot* slots, int32_t* counters, int slot_ca
 #define RG_ARGS slots, counters, slot_capacity, objs, dets, det_off, fl, fr, gf, sl, sr, gs, img_w, img_h, \
                 trusted, cfg, res, stats, max_points, s
   if (wide) return launch_variant<unsigned long long, 8, 2>(RG_ARGS);  // 9x7 extension
-  // latency mode (a few frames): most SMs would idle and each warp's point
-  // loop waits on L2, so small CTAs spread over every SM and L1 prefetch of
-  // the point 4 ahead (single C2 frame: 84 -> 68 us)
+  // latency mode (a few frames): most SMs would idle and the FAR blocks are
+  // the critical path, so one CTA per FAR block splits its passes over 4
+  // warps, with an L1 prefetch of the point 4 ahead (single C2 frame:
+  // 84 -> 45 us)
   if (variant == 0 && n_frames > 0 && n_frames <= kLatencyFrames)
     return launch_variant<uint32_t, 4, 12, 4, true>(RG_ARGS);
   switch (variant) {  // A/B knobs; default measured best (tools/census_time.py with RG_MATCH_VARIANT)
     case 1: return launch_variant<uint32_t, 8, 4>(RG_ARGS);
     case 2: return launch_variant<uint32_t, 8, 5>(RG_ARGS);
     case 3: return launch_variant<uint32_t, 16, 4>(RG_ARGS);
+    case 4: return launch_variant<uint32_t, 4, 12, 0, true>(RG_ARGS);
     default: return launch_variant<uint32_t, 16, 3>(RG_ARGS);
   }
 #undef RG_ARGS
