@@ -479,7 +479,7 @@ __global__ void __launch_bounds__(WPB * 32, MINB) match_slots_warp_kernel(
   __shared__ int nocc[WPB];
   __shared__ Cand xc[WPB];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  int slot = blockIdx.x * WPB + warp, part = 0, nparts = 1;
+  const int slot0 = blockIdx.x * WPB + warp;
   // an overflowed plan (counters[1], set by K3) is re-run with a bigger list:
   // skip it entirely; otherwise only planned slots inside the list exist
   // (FAR slots [0, counters[0]), CLOSE slots [capacity - counters[4], capacity);
@@ -489,89 +489,94 @@ __global__ void __launch_bounds__(WPB * 32, MINB) match_slots_warp_kernel(
     if (blockIdx.x == 0 && threadIdx.x == 0) counters[1] = 1;
     return;
   }
-  if (COOP) {  // CTA b < n_lo: FAR slot b; then CLOSE slots WPB per CTA from capacity - n_hi
-    if (counters[1]) return;
-    if ((int)blockIdx.x < n_lo) {
-      slot = blockIdx.x;
-      part = warp;
-      nparts = WPB;
-    } else {
-      slot = capacity - n_hi + ((int)blockIdx.x - n_lo) * WPB + warp;
-      if (slot >= capacity) return;  // warp-uniform; no CTA barrier in this case
-    }
-  } else if (counters[1] || (slot >= n_lo && slot < capacity - n_hi) || slot >= capacity) {
-    return;  // warp-uniform
-  }
-  // per warp: maxp sampled points + maxp valid points
-  unsigned char* wbase = wsm_raw + (size_t)warp * (maxp * sizeof(int2) + (maxp + 1) * sizeof(VPoint<CT>));
-  int2* pts = reinterpret_cast<int2*>(wbase);
-  VPoint<CT>* vp = reinterpret_cast<VPoint<CT>*>(wbase + sizeof(int2) * maxp);
-  const Slot s = slots[slot];
-  const ObjEntry e = objs[s.obj];
-  const rg_detection det = dets[e.det];
-  const int d0 = det_off[s.frame], d1 = det_off[s.frame + 1];
-  // occluders of this detection among the frame's detections (:71-89)
-  if (lane == 0) nocc[warp] = 0;
-  __syncwarp();
-  bool overflow = false;
-  for (int j = d0 + lane; j < d1; j += 32) {
-    if (j == e.det) continue;
-    const rg_detection dj = dets[j];
-    if (!dev_occludes(det, dj)) continue;
-    const int k = atomicAdd(&nocc[warp], 1);
-    if (k < kWarpOcc) {
-      const PBox b = pixel_box(dj, img_w, img_h);
-      occ[warp][4 * k] = b.x0;
-      occ[warp][4 * k + 1] = b.y0;
-      occ[warp][4 * k + 2] = b.x1;
-      occ[warp][4 * k + 3] = b.y1;
-    } else {
-      overflow = true;
-    }
-  }
-  __syncwarp();
-  const bool all = __any_sync(0xffffffffu, overflow);
-  const int cols = max(e.cols, 1);
-  const int np = dev_sample_block_warp(det, e.kind, s.sub / cols, s.sub % cols, e.rows, e.cols,
-                                       occ[warp], min(nocc[warp], kWarpOcc), all ? dets + d0 : nullptr,
-                                       d1 - d0, e.det - d0, cfg, img_w, img_h, pts);
-  rg_match_result r;
-  r.dx_int = r.dy_int = 0;
-  r.dx_subpix = r.cost = 0.0;
-  r.cost_minus = r.cost_plus = -1.0;
-  r.valid_points = r.verified = r.has_value = 0;
-  r.n_points = np;
-  int evals = 0;
-  if (np >= 4) {  // blocks with < 4 points are dropped (:185, :219)
-    const bool far = e.kind == RG_KIND_FAR;
-    const PadGeom& g = far ? gf : gs;
-    const int64_t fo = (int64_t)s.frame * g.fstride + g.origin;
-    const CT* L = (far ? fl : sl) + fo;
-    const CT* R = (far ? fr : sr) + fo;
-    const int sc = cfg.close_scale;
-    const rg_search_range rg = far ? rg_search_range{0, cfg.dx_max_far, -1, 1}
-                                   : rg_search_range{0, (cfg.dx_max_close + sc - 1) / sc, -1, 1};
-    const Pass f = warp_pass<CT, PF>(pts, np, 0, 0, L, R, g, trusted != 0, rg, vp, lane, evals, part, nparts, xc);
-    if (f.has) {
-      finish(f, r);
-      const rg_search_range brg = {-rg.dx_max, -rg.dx_min, -f.dy, -f.dy};
-      const Pass b = warp_pass<CT, PF>(pts, np, -f.dx, f.dy, R, L, g, trusted != 0, brg, vp, lane, evals, part,
-                                       nparts, xc);
-      if (b.has) {
-        rg_match_result rb;
-        finish(b, rb);
-        r.verified = fabs(__dadd_rn(r.dx_subpix, rb.dx_subpix)) < cfg.tau_v;
+  if (counters[1]) return;
+  auto run_slot = [&](const int slot, const int part, const int nparts) {
+    // per warp: maxp sampled points + maxp valid points
+    unsigned char* wbase = wsm_raw + (size_t)warp * (maxp * sizeof(int2) + (maxp + 1) * sizeof(VPoint<CT>));
+    int2* pts = reinterpret_cast<int2*>(wbase);
+    VPoint<CT>* vp = reinterpret_cast<VPoint<CT>*>(wbase + sizeof(int2) * maxp);
+    const Slot s = slots[slot];
+    const ObjEntry e = objs[s.obj];
+    const rg_detection det = dets[e.det];
+    const int d0 = det_off[s.frame], d1 = det_off[s.frame + 1];
+    // occluders of this detection among the frame's detections (:71-89)
+    if (lane == 0) nocc[warp] = 0;
+    __syncwarp();
+    bool overflow = false;
+    for (int j = d0 + lane; j < d1; j += 32) {
+      if (j == e.det) continue;
+      const rg_detection dj = dets[j];
+      if (!dev_occludes(det, dj)) continue;
+      const int k = atomicAdd(&nocc[warp], 1);
+      if (k < kWarpOcc) {
+        const PBox b = pixel_box(dj, img_w, img_h);
+        occ[warp][4 * k] = b.x0;
+        occ[warp][4 * k + 1] = b.y0;
+        occ[warp][4 * k + 2] = b.x1;
+        occ[warp][4 * k + 3] = b.y1;
+      } else {
+        overflow = true;
       }
     }
-  }
-  evals = __reduce_add_sync(0xffffffffu, evals);
-  if (lane == 0) {
-    if (evals) atomicAdd(reinterpret_cast<unsigned long long*>(counters + 2), (unsigned long long)evals);
-    if (part == 0) {
-      res[slot] = r;
-      if (stats && np >= 4) atomicAdd(reinterpret_cast<unsigned long long*>(&stats[s.frame].query_points),
-                                      (unsigned long long)np);
+    __syncwarp();
+    const bool all = __any_sync(0xffffffffu, overflow);
+    const int cols = max(e.cols, 1);
+    const int np = dev_sample_block_warp(det, e.kind, s.sub / cols, s.sub % cols, e.rows, e.cols,
+                                         occ[warp], min(nocc[warp], kWarpOcc), all ? dets + d0 : nullptr,
+                                         d1 - d0, e.det - d0, cfg, img_w, img_h, pts);
+    rg_match_result r;
+    r.dx_int = r.dy_int = 0;
+    r.dx_subpix = r.cost = 0.0;
+    r.cost_minus = r.cost_plus = -1.0;
+    r.valid_points = r.verified = r.has_value = 0;
+    r.n_points = np;
+    int evals = 0;
+    if (np >= 4) {  // blocks with < 4 points are dropped (:185, :219)
+      const bool far = e.kind == RG_KIND_FAR;
+      const PadGeom& g = far ? gf : gs;
+      const int64_t fo = (int64_t)s.frame * g.fstride + g.origin;
+      const CT* L = (far ? fl : sl) + fo;
+      const CT* R = (far ? fr : sr) + fo;
+      const int sc = cfg.close_scale;
+      const rg_search_range rg = far ? rg_search_range{0, cfg.dx_max_far, -1, 1}
+                                     : rg_search_range{0, (cfg.dx_max_close + sc - 1) / sc, -1, 1};
+      const Pass f = warp_pass<CT, PF>(pts, np, 0, 0, L, R, g, trusted != 0, rg, vp, lane, evals, part, nparts, xc);
+      if (f.has) {
+        finish(f, r);
+        const rg_search_range brg = {-rg.dx_max, -rg.dx_min, -f.dy, -f.dy};
+        const Pass b = warp_pass<CT, PF>(pts, np, -f.dx, f.dy, R, L, g, trusted != 0, brg, vp, lane, evals, part,
+                                         nparts, xc);
+        if (b.has) {
+          rg_match_result rb;
+          finish(b, rb);
+          r.verified = fabs(__dadd_rn(r.dx_subpix, rb.dx_subpix)) < cfg.tau_v;
+        }
+      }
     }
+    evals = __reduce_add_sync(0xffffffffu, evals);
+    if (lane == 0) {
+      if (evals) atomicAdd(reinterpret_cast<unsigned long long*>(counters + 2), (unsigned long long)evals);
+      if (part == 0) {
+        res[slot] = r;
+        if (stats && np >= 4) atomicAdd(reinterpret_cast<unsigned long long*>(&stats[s.frame].query_points),
+                                        (unsigned long long)np);
+      }
+    }
+  };
+  if (COOP) {
+    // items: FAR slot b (b < n_lo, the whole CTA) or WPB CLOSE slots from
+    // capacity - n_hi; a grid of about one wave walks them
+    const int n_items = n_lo + (n_hi + WPB - 1) / WPB;
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+      if (it < n_lo) {
+        run_slot(it, warp, WPB);
+      } else {
+        const int sl = capacity - n_hi + (it - n_lo) * WPB + warp;
+        if (sl < capacity) run_slot(sl, 0, 1);  // no CTA barrier on this path
+      }
+    }
+  } else if (!((slot0 >= n_lo && slot0 < capacity - n_hi) || slot0 >= capacity)) {  // warp-uniform
+    run_slot(slot0, 0, 1);
   }
 }
 
@@ -589,9 +594,9 @@ cudaError_t launch_variant(const Slot* slots, int32_t* counters, int slot_capaci
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
-  // COOP: up to one CTA per slot (FAR CTAs + CLOSE CTAs <= capacity); the
-  // CTAs past the planned slots exit at once
-  const int grid = COOP ? slot_capacity : (slot_capacity + WPB - 1) / WPB;
+  // COOP: about one wave of CTAs walks the work items (their count is only
+  // known on the device)
+  const int grid = COOP ? std::min(slot_capacity, 148 * MINB) : (slot_capacity + WPB - 1) / WPB;
   kern<<<grid, WPB * 32, smem, s>>>(slots, counters, objs, dets, det_off, static_cast<const CT*>(fl),
                                     static_cast<const CT*>(fr), gf, static_cast<const CT*>(sl),
                                     static_cast<const CT*>(sr), gs, img_w, img_h, trusted, cfg, res, stats,

@@ -58,7 +58,8 @@ __global__ void __launch_bounds__(PT) plan_frames_kernel(
       const double ki = s_key[i];
       const int idi = s_id[i];
       int rank = 0;
-      for (int j = 0; j < n && rank < cfg.max_objects; ++j) {
+#pragma unroll 8
+      for (int j = 0; j < n; ++j) {  // no early exit: independent iterations overlap their smem loads
         const bool fj = s_front[j];
         const double kj = s_key[j];
         const bool prec = fj != fi ? fj : kj != ki ? kj > ki : s_id[j] != idi ? s_id[j] < idi : j < i;
