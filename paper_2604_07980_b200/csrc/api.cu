@@ -347,8 +347,12 @@ rg_status enqueue_census(rg_ctx* ctx, const FrameJob& J, const Rasters& R, int s
 
 // K3 planner, K2 matcher, K4 aggregation of job J over the rasters at `slot0`.
 // ev (nullable): 4 timing events recorded before K3, K2, K4 and after K4.
+// plan_stream (nullable): run the counter reset and K3 there (the caller has
+// made it wait for everything earlier on s), so K3 overlaps whatever s runs
+// before this call (K1); s then waits for K3 before K2.
 rg_status enqueue_match(rg_ctx* ctx, const FrameJob& J, const rg_ranger_config& cfg, const Rasters& R, int slot0,
-                        cudaStream_t s, int32_t* counters, const cudaEvent_t* ev, PipelineBufs* pb) {
+                        cudaStream_t s, int32_t* counters, const cudaEvent_t* ev, PipelineBufs* pb,
+                        cudaStream_t plan_stream = nullptr) {
   const int w = J.w, h = J.h, F = J.n_frames;
   const size_t csz = R.wide ? sizeof(unsigned long long) : sizeof(uint32_t);
   auto at = [&](uint32_t* p, const PadGeom& g) {
@@ -366,12 +370,17 @@ rg_status enqueue_match(rg_ctx* ctx, const FrameJob& J, const rg_ranger_config& 
   NEED(slots);
   NEED(res);
   NEED(scratch);
-  RG_CUDA(ctx, cudaMemsetAsync(counters, 0, kCounterInts * sizeof(int32_t), s));
-  if (ev) RG_CUDA(ctx, cudaEventRecord(ev[0], s));
+  const cudaStream_t ps = plan_stream ? plan_stream : s;
+  RG_CUDA(ctx, cudaMemsetAsync(counters, 0, kCounterInts * sizeof(int32_t), ps));
+  if (ev) RG_CUDA(ctx, cudaEventRecord(ev[0], ps));
   // K3 planner
   RG_CUDA(ctx, launch_plan_frames(J.dets, J.det_off, F, w, h, cfg, J.out_stride, objs, J.out,
-                                  J.out_count, slots, capacity, counters, J.stats, J.out_index, s));
+                                  J.out_count, slots, capacity, counters, J.stats, J.out_index, ps));
   count_launch(ctx, ST_PLAN);
+  if (plan_stream) {
+    RG_CUDA(ctx, cudaEventRecord(ctx->ev_sync[1], plan_stream));
+    RG_CUDA(ctx, cudaStreamWaitEvent(s, ctx->ev_sync[1], 0));
+  }
   if (ev) RG_CUDA(ctx, cudaEventRecord(ev[1], s));
   // K2 fused sampler + forward/backward matcher, one warp per slot
   const int trusted = !(J.full_l || J.scaled_l);
@@ -394,9 +403,17 @@ rg_status enqueue_pipeline(rg_ctx* ctx, const FrameJob& J, const rg_ranger_confi
   Rasters R;
   TRY(prepare_rasters(ctx, J, cfg, J.n_frames, s, &R));
   const bool prof = ctx->profiling;
+  // latency mode (a few frames, not profiling): K3 on the auxiliary stream
+  // alongside K1 -- both are a few microseconds for one frame
+  cudaStream_t aux = nullptr;
+  if (!prof && J.n_frames <= 4 && ctx->match_stream) {
+    aux = ctx->match_stream;  // high priority: the one planner CTA is dispatched ahead of K1's
+    RG_CUDA(ctx, cudaEventRecord(ctx->ev_sync[0], s));
+    RG_CUDA(ctx, cudaStreamWaitEvent(aux, ctx->ev_sync[0], 0));
+  }
   if (prof) RG_CUDA(ctx, cudaEventRecord(ctx->ev[0], s));
   TRY(enqueue_census(ctx, J, R, 0, s));
-  return enqueue_match(ctx, J, cfg, R, 0, s, counters, prof ? ctx->ev + 1 : nullptr, pb);
+  return enqueue_match(ctx, J, cfg, R, 0, s, counters, prof ? ctx->ev + 1 : nullptr, pb, aux);
 }
 
 void accumulate_profile(rg_ctx* ctx) {
