@@ -663,13 +663,8 @@ static cudaError_t launch_simd(const uint8_t* left, const uint8_t* right, int n_
   cudaError_t e = launch_lanes<HW, 1>(left, right, n_frames, stride, pitch, img_h, w, h, x0, y0, delta_min, n_delta,
                                       p, raw, counts, s, b0, b1);
   if (e != cudaSuccess || b1 <= b0) return e;
-  static bool attr = false;
-  if (!attr) {
-    e = cudaFuncSetAttribute(bm_simd_kernel<HW, LA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)sb_smem<HW>());
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  static SmemAttr attr;
+  if ((e = attr.ensure((const void*)bm_simd_kernel<HW, LA>, sb_smem<HW>())) != cudaSuccess) return e;
   dim3 grid((b1 - b0 + SB_W - 1) / SB_W, (h + SB_RS - 1) / SB_RS, n_frames * n_delta);
   bm_simd_kernel<HW, LA><<<grid, SB_W * 32, sb_smem<HW>(), s>>>(left, right, stride, pitch, img_h, w, h, x0, y0,
                                                              delta_min, n_delta, d_lo, p.num_disparities,

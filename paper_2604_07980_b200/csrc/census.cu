@@ -359,12 +359,9 @@ cudaError_t launch_census_frames(const uint8_t* left, const uint8_t* right, int 
   const bool half = !sl || (gs.w * 2 == w && gs.h * 2 == h && gs.pitch % 2 == 0 && gs.origin % 2 == 0);
   if (aligned && half) {
     auto kern = internal ? census_pairs_kernel<true> : census_pairs_kernel<false>;
-    static bool attr[2] = {false, false};
-    if (!attr[internal]) {
-      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C2_SMEM);
-      if (e != cudaSuccess) return e;
-      attr[internal] = true;
-    }
+    static SmemAttr attr[2];
+    const cudaError_t e = attr[internal].ensure((const void*)kern, C2_SMEM);
+    if (e != cudaSuccess) return e;
     dim3 grid((w + C2_TX - 1) / C2_TX, (h + C2_TY - 1) / C2_TY, sides * n_frames);
     kern<<<grid, C2_WARPS * 32, C2_SMEM, s>>>(left, right, frame_stride, pitch, w, h, fl, fr, gf, sl, sr, gs,
                                               lshift);

@@ -124,11 +124,10 @@ cudaError_t launch_box_disparity(const int16_t* raw, int w, int h, int64_t frame
                                  rg_box_stats* out, cudaStream_t s) {
   if (n_boxes <= 0) return cudaSuccess;
   const size_t smem = sizeof(int) * (size_t)nbins;
-  static size_t attr = 0;
-  if (smem > 48 * 1024 && smem > attr) {
-    cudaError_t e = cudaFuncSetAttribute(box_disparity_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  static SmemAttr attr;
+  if (smem > 48 * 1024) {
+    const cudaError_t e = attr.ensure((const void*)box_disparity_kernel, smem);
     if (e != cudaSuccess) return e;
-    attr = smem;
   }
   box_disparity_kernel<<<n_boxes, kBoxThreads, smem, s>>>(raw, w, h, frame_stride, dets, box_det, box_frame, raw_lo,
                                                          nbins, sigma_obs2, gamma, sigma_sys2, out);

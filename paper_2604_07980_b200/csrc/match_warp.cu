@@ -590,8 +590,9 @@ cudaError_t launch_variant(const Slot* slots, int32_t* counters, int slot_capaci
   auto kern = match_slots_warp_kernel<CT, WPB, MINB, PF, COOP>;
   max_points = (max_points + 1) & ~1;  // keeps every warp's VPoint array 16-B aligned
   const size_t smem = (sizeof(int2) * (size_t)max_points + sizeof(VPoint<CT>) * (size_t)(max_points + 1)) * WPB;
+  static SmemAttr attr;  // one per instantiation
   if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const cudaError_t e = attr.ensure((const void*)kern, smem);
     if (e != cudaSuccess) return e;
   }
   // COOP: about one wave of CTAs walks the work items (their count is only

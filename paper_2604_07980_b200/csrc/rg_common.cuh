@@ -9,11 +9,33 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <string>
 
 #include "../../include/ranger_cuda.h"
 
 namespace rg {
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) is per DEVICE: one cache
+// per kernel (a static of the call site) remembers the size raised on each
+// device, so a process driving several GPUs raises it on every one.
+struct SmemAttr {
+  static constexpr int kDevices = 64;
+  std::atomic<int> raised[kDevices] = {};
+  cudaError_t ensure(const void* fn, size_t bytes) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kDevices)
+      return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (raised[dev].load(std::memory_order_relaxed) >= (int)bytes) return cudaSuccess;
+    const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e == cudaSuccess) {
+      int cur = raised[dev].load(std::memory_order_relaxed);
+      while (cur < (int)bytes && !raised[dev].compare_exchange_weak(cur, (int)bytes)) {
+      }
+    }
+    return e;
+  }
+};
 
 // ------------------------------------------------------------ limits
 constexpr int kMatchThreads = 256;     // CTA size of the matcher
