@@ -312,6 +312,7 @@ rg_status prepare_rasters(rg_ctx* ctx, const FrameJob& J, const rg_ranger_config
 
 // K1 of job J into the rasters starting at raster frame `slot0`
 rg_status enqueue_census(rg_ctx* ctx, const FrameJob& J, const Rasters& R, int slot0, cudaStream_t s) {
+  RG_NVTX("K1 census");
   const int w = J.w, h = J.h, F = J.n_frames;
   const size_t csz = R.wide ? sizeof(unsigned long long) : sizeof(uint32_t);
   auto at = [&](uint32_t* p, const PadGeom& g) {
@@ -353,6 +354,7 @@ rg_status enqueue_census(rg_ctx* ctx, const FrameJob& J, const Rasters& R, int s
 rg_status enqueue_match(rg_ctx* ctx, const FrameJob& J, const rg_ranger_config& cfg, const Rasters& R, int slot0,
                         cudaStream_t s, int32_t* counters, const cudaEvent_t* ev, PipelineBufs* pb,
                         cudaStream_t plan_stream = nullptr) {
+  RG_NVTX("K3 plan + K2 match + K4 aggregate");
   const int w = J.w, h = J.h, F = J.n_frames;
   const size_t csz = R.wide ? sizeof(unsigned long long) : sizeof(uint32_t);
   auto at = [&](uint32_t* p, const PadGeom& g) {
@@ -730,6 +732,7 @@ static rg_status census_common(rg_ctx* ctx, const uint8_t* img, int w, int h, in
 
 rg_status rg_census_transform(rg_ctx* ctx, const uint8_t* img, int w, int h, int ow, int oh,
                               uint32_t* codes) {
+  RG_NVTX("rg_census_transform");
   return census_common(ctx, img, w, h, ow, oh, nullptr, 0, false, codes, "census_transform");
 }
 
@@ -810,6 +813,7 @@ rg_status rg_match_blocks(rg_ctx* ctx, const uint32_t* left, int lw, int lh, con
                           int rw, int rh, const int32_t* points_xy, const int64_t* offsets,
                           const rg_search_range* ranges, int n_blocks, int mode, double tau_v,
                           rg_match_result* out) {
+  RG_NVTX("rg_match_blocks");
   return match_blocks_common(ctx, left, lw, lh, right, rw, rh, points_xy, offsets, ranges, n_blocks, mode,
                              tau_v, out);
 }
@@ -1013,6 +1017,7 @@ rg_status rg_estimate_object_disparities(rg_ctx* ctx, const uint8_t* left, const
                                          const rg_ranger_config* cfg, rg_census_cache* cache,
                                          double focal_px, double baseline_m, rg_object_disparity* out,
                                          int* n_out, rg_ranger_stats* stats) {
+  RG_NVTX("rg_estimate_object_disparities");
   TRY(bind(ctx));
   TRY(check_cfg(ctx, cfg));
   if (cfg->census_9x7 && cache)  // caches hold 5x5 codes
@@ -1139,6 +1144,7 @@ rg_status rg_estimate_object_disparities(rg_ctx* ctx, const uint8_t* left, const
 // =========================================================== batched frames
 rg_status rg_range_frames(rg_ctx* ctx, const rg_frame_batch* b, const rg_ranger_config* cfg,
                           void* stream) {
+  RG_NVTX("rg_range_frames");
   TRY(bind(ctx));
   TRY(check_cfg(ctx, cfg));
   if (!b || b->n_frames < 0 || b->width < 1 || b->height < 1 || b->pitch < b->width)
@@ -1158,6 +1164,7 @@ rg_status rg_range_frames(rg_ctx* ctx, const rg_frame_batch* b, const rg_ranger_
 
 rg_status rg_range_frames_host(rg_ctx* ctx, const rg_frame_batch* b, const rg_ranger_config* cfg,
                                int chunk, void* stream) {
+  RG_NVTX("rg_range_frames_host");
   TRY(bind(ctx));
   TRY(check_cfg(ctx, cfg));
   if (!b || b->n_frames < 0 || b->width < 1 || b->height < 1 || b->pitch < b->width)
@@ -1368,6 +1375,7 @@ rg_status rg_dense_objects(rg_ctx* ctx, const uint8_t* left, const uint8_t* righ
                            const rg_detection* dets, int n, const rg_ranger_config* cfg, const rg_bm_params* bm,
                            double sigma_obs2, double gamma, double sigma_sys2, rg_object_disparity* out,
                            rg_box_stats* box_out, int* n_out, int16_t* raw_out) {
+  RG_NVTX("rg_dense_objects");
   TRY(bind(ctx));
   TRY(check_cfg(ctx, cfg));
   TRY(check_bm(ctx, bm));
@@ -1483,6 +1491,7 @@ rg_status rg_auto_rect_frames(rg_ctx* ctx, const uint8_t* d_left, const uint8_t*
                               int64_t frame_stride, int pitch, int w, int h, const rg_rect* roi,
                               int delta_min, int delta_max, const rg_bm_params* p, int32_t* d_best,
                               int64_t* d_counts, void* stream) {
+  RG_NVTX("rg_auto_rect_frames");
   TRY(bind(ctx));
   if (!d_left || !d_right || !d_best || n_frames < 0 || w < 1 || h < 1 || pitch < w)
     return set_err(ctx, RG_EINVAL, "auto_rect_frames: bad arguments");

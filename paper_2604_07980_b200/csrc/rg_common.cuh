@@ -12,9 +12,22 @@
 #include <atomic>
 #include <string>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/ranger_cuda.h"
 
 namespace rg {
+
+// NVTX ranges around the public entry points and the stages they enqueue
+// (host-side ranges: visible to nsys / ncu --nvtx; header-only NVTX v3, a
+// no-op unless a tool injects itself)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+#define RG_NVTX(name) ::rg::NvtxRange rg_nvtx_range_(name)
 
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) is per DEVICE: one cache
 // per kernel (a static of the call site) remembers the size raised on each

@@ -57,6 +57,7 @@ rg_status rg_filter_offset(rg_rect_state* st, int delta_star, double* applied) {
 rg_status rg_range_sequence(rg_ctx* ctx, const rg_frame_batch* b, const rg_ranger_config* cfg,
                             const rg_rect_search_config* rect, rg_rect_state* st, int32_t* out_shift,
                             int32_t* out_delta, double* out_rect_applied, void* stream) {
+  RG_NVTX("rg_range_sequence");
   if (!ctx) return RG_EINVAL;
   if (!b || !cfg || !rect || !st) return fail(ctx, RG_EINVAL, "range_sequence: null argument");
   if (b->n_frames < 0 || b->width < 1 || b->height < 1)

@@ -547,6 +547,7 @@ rg_status rg_validate_sgm_params(rg_ctx* ctx, const rg_sgm_params* p) {
 
 rg_status rg_sgm_disparity(rg_ctx* ctx, const uint8_t* left, const uint8_t* right, int w, int h,
                            const rg_sgm_params* p, int16_t* out_raw) {
+  RG_NVTX("rg_sgm_disparity");
   SG_TRY(sgm_bind(ctx));
   SG_TRY(sgm_check(ctx, p));
   if (!left || !right || !out_raw || w < 1 || h < 1) return set_err(ctx, RG_EINVAL, "sgm_disparity: bad image");
@@ -569,6 +570,7 @@ rg_status rg_sgm_disparity(rg_ctx* ctx, const uint8_t* left, const uint8_t* righ
 rg_status rg_sgm_frames(rg_ctx* ctx, const uint8_t* d_left, const uint8_t* d_right, int n_frames,
                         int64_t frame_stride, int pitch, int w, int h, const rg_sgm_params* p, int16_t* d_raw,
                         void* stream) {
+  RG_NVTX("rg_sgm_frames");
   SG_TRY(sgm_bind(ctx));
   SG_TRY(sgm_check(ctx, p));
   if (!d_left || !d_right || !d_raw || n_frames < 0 || w < 1 || h < 1 || pitch < w)
