@@ -260,3 +260,51 @@ def test_latency_and_throughput_matchers_agree(ctx, name):
     assert run(0, 6) == big  # repeat: bit-identical
     small = run(0, 1) + run(1, 3) + run(3, 6)  # latency matcher (1, 2, 3 frames)
     assert small == big
+
+
+def _random_cfgs(n, seed=11):
+    rng = np.random.default_rng(seed)
+    out = []
+    for _ in range(n):
+        cfg = rg.RangerConfig(
+            tau_s=float(rng.choice([20.0, 48.0, 100.0])), close_scale=int(rng.choice([1, 2, 3])),
+            grid_side_points=int(rng.choice([2, 5, 8, 11])), max_total_points=int(rng.choice([4, 25, 64, 100])),
+            close_block_side_points=int(rng.choice([2, 3, 5])), tau_d=float(rng.choice([0.5, 1.0, 3.0])),
+            n_min=int(rng.choice([1, 3, 5])), tau_v=float(rng.choice([0.5, 1.0, 2.0])),
+            max_objects=int(rng.choice([3, 8, 16])), dx_max_far=int(rng.choice([7, 33, 64, 100, 130])),
+            dx_max_close=int(rng.choice([5, 64, 129, 192])))
+        out.append(cfg)
+    return out
+
+
+@pytest.mark.parametrize("k", range(8))
+def test_random_configs_both_matchers_match_oracle(ctx, orc, k):
+    """Randomised RangerConfigs (ranges that are / are not multiples of 32,
+    tails, tiny grids, close scales 1-3, selection budgets) on C1 frames:
+    the latency (cooperative) matcher on a 1-frame batch and the throughput
+    matcher on a 5-frame batch both equal the oracle frame by frame."""
+    import torch
+
+    cfg = _random_cfgs(8)[k]
+    L, R, D, _, sc = _frames(S.scene_c1, 5)
+    eng = FrameEngine(sc.width, sc.height, cfg, max(len(d) for d in D), S.F_PX, S.BASELINE_M, ctx=ctx)
+    dev = torch.device("cuda", 0)
+
+    def run(lo, hi):
+        recs, offs = pack_detections(D[lo:hi])
+        n = hi - lo
+        out = torch.zeros(n * eng.out_stride * 32, dtype=torch.uint8, device=dev)
+        cnt = torch.zeros(n, dtype=torch.int32, device=dev)
+        eng.range_device(torch.from_numpy(L[lo:hi]).to(dev), torch.from_numpy(R[lo:hi]).to(dev),
+                         torch.from_numpy(recs.view(np.uint8)).to(dev), torch.from_numpy(offs).to(dev), out, cnt)
+        torch.cuda.synchronize()
+        c = cnt.cpu().numpy()
+        o = out.cpu().numpy().reshape(n, -1)
+        return [o[f, :c[f] * 32].tobytes() for f in range(n)]
+
+    big = run(0, 5)
+    small = [run(f, f + 1)[0] for f in range(5)]
+    for f in range(5):
+        want = _want(orc, L[f], R[f], D[f], cfg)
+        assert big[f] == want, (f, cfg)
+        assert small[f] == want, (f, cfg)
