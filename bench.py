@@ -384,6 +384,27 @@ def main():
     e2e_value = int(h_cnt.sum()) * e2e_steps * world / float(te.item())
     h2d = int(hL.nbytes + hR.nbytes + h_recs.nbytes + h_offs.nbytes)
     d2h = int(h_out.nbytes + h_cnt.nbytes)
+    # the e2e bound: this box's pinned host -> device copy bandwidth (one
+    # 256 MiB copy stream, CUDA events, best of 3 x 8 copies)
+    pcie_gbs = None
+    try:
+        ph = torch.empty(256 << 20, dtype=torch.uint8).pin_memory()
+        pd = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+        best = 0.0
+        for _ in range(3):
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+            with torch.cuda.stream(stream):
+                for _ in range(8):
+                    pd.copy_(ph, non_blocking=True)
+            a1.record(stream)
+            torch.cuda.synchronize()
+            best = max(best, 8 * ph.nbytes / (a0.elapsed_time(a1) * 1e-3) / 1e9)
+        pcie_gbs = best
+        del ph, pd
+    except Exception:  # pragma: no cover
+        pass
+    e2e_h2d_gbs = h2d * e2e_steps / float(te.item()) / 1e9
 
     # ---- p50 latency: one frame, host in -> per-box results on host
     lat = []
@@ -526,7 +547,10 @@ def main():
                              f"per step > 126 MB L2 (no flush needed)",
                        "parallelism": f"frame-sharded dp{world}, NCCL all_gather of per-box results"},
             "e2e": {"value": e2e_value, "unit": "boxes/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "api": "rg_range_frames_host (pinned host frames, chunked H2D/compute/D2H)"},
+                    "api": "rg_range_frames_host (pinned host frames, chunked H2D/compute/D2H)",
+                    "bound": {"kind": "pcie_h2d", "achieved_gbs": e2e_h2d_gbs, "peak_gbs": pcie_gbs,
+                              "frac": (e2e_h2d_gbs / pcie_gbs) if pcie_gbs else None,
+                              "peak_source": "measured here: pinned 256 MiB host->device copies, best of 3"}},
             "gpu_launches": int(total_launches),
             "roofline": dominant,
             "kernels": {"census": census_roof, "matcher": match_roof,
