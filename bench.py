@@ -182,10 +182,32 @@ def cpu_reference_run(L, R, dets, cfg, seconds: float, threads: int):
         wall += t
         frames += n
         boxes += int(cnt.sum())
-    return {"value": boxes / wall, "unit": "boxes/s", "frames_per_sec": frames / wall, "cores": threads,
-            "kind": kind, "sample": f"{frames} C2 frames ({n} distinct, noise 2.0) ranged by the reference's "
-                                    f"estimate_object_disparities, {threads} threads x whole frames at workers=1, "
-                                    f"{wall:.1f} s"}
+    res = {"value": boxes / wall, "unit": "boxes/s", "frames_per_sec": frames / wall, "cores": threads,
+           "kind": kind, "sample": f"{frames} C2 frames ({n} distinct, noise 2.0) ranged by the reference's "
+                                   f"estimate_object_disparities, {threads} threads x whole frames at workers=1, "
+                                   f"{wall:.1f} s"}
+    # the reference's stages on one frame at workers = 1 and
+    # workers = nproc (median of reps): estimate_object_disparities (ROI
+    # census path), census_transform x 2, and the C4 offset search
+    try:
+        from paper_2604_07980_b200 import synth as S
+        d = (_abi.Detection * len(dets))(*[_abi.Detection(x.cx, x.cy, x.w, x.h, x.class_id, x.id) for x in dets])
+        roi = _abi.Rect(*S.C4_ROI)
+        bm = S.c4_bm().to_c()
+        detail = {}
+        for wk, reps, rr in ((1, 3, 1), (threads, 5, 2)):
+            t = (C.c_double * 3)()
+            chk.lib.ref_bench_stages.restype = C.c_int
+            st = chk.lib.ref_bench_stages(C.c_void_p(Lc[0].ctypes.data), C.c_void_p(Rc[0].ctypes.data), W, H,
+                                          C.byref(d), len(dets), C.byref(c), wk, reps, C.byref(roi), -8, 8,
+                                          C.byref(bm), rr, t)
+            if st == 0:
+                detail[f"workers_{wk}"] = {"estimate_ms_per_frame": 1e3 * t[0], "census_x2_ms": 1e3 * t[1],
+                                           "autorect_c4_ms": 1e3 * t[2]}
+        res["stages_one_frame"] = detail
+    except Exception as e:  # pragma: no cover
+        res["stages_one_frame"] = f"error: {e}"
+    return res
 
 
 # ------------------------------------------------------------------ reference arm

@@ -111,6 +111,9 @@ double ref_bench_estimate(const uint8_t* left, const uint8_t* right, int w, int 
                           const int32_t* det_offsets, const rg_ranger_config* cfg,
                           int threads, rg_object_disparity* out, int out_stride,
                           int32_t* out_count);
+int ref_bench_stages(const uint8_t* left, const uint8_t* right, int w, int h, const rg_detection* dets, int n_dets,
+                     const rg_ranger_config* cfg, int workers, int reps, const rg_rect* roi, int delta_min,
+                     int delta_max, const rg_bm_params* bm, int reps_rect, double* out_s);
 
 #ifdef __cplusplus
 }

@@ -410,6 +410,46 @@ double ref_bench_estimate(const uint8_t* left, const uint8_t* right, int w, int 
 }
 
 
+/* SURVEY 8(d) CPU baseline detail: median seconds of `reps` runs of one
+ * frame through the reference at `workers`: [0] estimate_object_disparities
+ * (the production ROI-census path), [1] census_transform of both images,
+ * [2] auto_rect_search over `roi` / [delta_min, delta_max] with `bm`
+ * (skipped when reps_rect == 0). */
+int ref_bench_stages(const uint8_t* left, const uint8_t* right, int w, int h, const rg_detection* dets, int n_dets,
+                     const rg_ranger_config* cfg, int workers, int reps, const rg_rect* roi, int delta_min,
+                     int delta_max, const rg_bm_params* bm, int reps_rect, double* out_s) {
+  return guarded([&] {
+    const GrayImage L = to_gray(left, w, h), R = to_gray(right, w, h);
+    const std::vector<Detection> D = to_dets(dets, n_dets);
+    const RangerConfig rc = to_cfg(cfg);
+    auto median_of = [](std::vector<double> v) {
+      std::sort(v.begin(), v.end());
+      return v.empty() ? 0.0 : v[v.size() / 2];
+    };
+    auto timed = [&](int n, auto&& fn) {
+      std::vector<double> t;
+      for (int r = 0; r < n; ++r) {
+        const auto t0 = std::chrono::steady_clock::now();
+        fn();
+        t.push_back(std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
+      }
+      return median_of(t);
+    };
+    out_s[0] = timed(reps, [&] { (void)estimate_object_disparities(L, R, D, rc, nullptr, workers, nullptr); });
+    out_s[1] = timed(reps, [&] {
+      (void)census_transform(L, workers);
+      (void)census_transform(R, workers);
+    });
+    out_s[2] = 0.0;
+    if (reps_rect > 0) {
+      const ImageRoi r{roi->x0, roi->y0, roi->x1, roi->y1};
+      const BmParams p = to_bm(bm);
+      out_s[2] = timed(reps_rect, [&] { (void)auto_rect_search(L, R, r, delta_min, delta_max, p, workers); });
+    }
+    return RG_OK;
+  });
+}
+
 /* Pipeline::process_frame (pipeline.hpp:124-266), TEMPLATE_MATCHER (method 0) or STEREO_BM (1),
  * over n_frames consecutive frames (packed w*h images, dets CSR); no radar.
  * out[f*out_stride + k], out_count[f]: PipelineResult::objects of frame f;
