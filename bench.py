@@ -33,6 +33,16 @@ METRIC = "boxes ranged/sec & stereo frames/sec at 1920x1080, 64 boxes; p50 frame
 W, H = 1920, 1080
 CENSUS_BYTES_PER_FRAME = 2 * (W * H + 4 * W * H + 4 * (W // 2) * (H // 2))  # 24,883,200
 POPC_PER_CLK_PER_SM = 16  # CUDA programming guide throughput table (cc 8.x-9.0)
+
+
+def popc_peak_per_clk():
+    """Measured XOR+POPC+IADD evaluations per clock per SM on this GPU model
+    (tools/popc_probe.cu -> profiles/r1_popc_probe.json), else the nominal 16."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1_popc_probe.json")) as f:
+            return float(json.load(f)["evals_per_clk_per_sm"]), "measured (tools/popc_probe.cu)"
+    except Exception:
+        return float(POPC_PER_CLK_PER_SM), "nominal"
 N_SM = 148
 
 
@@ -526,7 +536,8 @@ def main():
     census_gbs = CENSUS_BYTES_PER_FRAME * F / (census_ms / 1000.0) / 1e9
     evals_per_launch = r_evals / max(stage_launches[2], 1)
     clk_mhz = clk["sm_mhz"] or sm_max
-    popc_peak = POPC_PER_CLK_PER_SM * N_SM * clk_mhz * 1e6
+    popc_clk, popc_src = popc_peak_per_clk()
+    popc_peak = popc_clk * N_SM * clk_mhz * 1e6
     match_rate = evals_per_launch / (match_ms / 1000.0)
     traffic = None
     try:
@@ -539,11 +550,11 @@ def main():
     census_roof = {"bound": "hbm", "achieved": census_gbs, "peak": hbm_peak, "unit": "GB/s",
                    "frac": census_gbs / hbm_peak, "traffic": traffic, "kernel": "census_pairs_kernel",
                    "peak_source": peak_kind, "algorithmic_bytes_per_launch": CENSUS_BYTES_PER_FRAME * F,
-                   "ms_per_launch": census_ms}
+                   "ms_per_launch": census_ms, "frac_of_nominal_8000_gbs": census_gbs / 8000.0}
     match_roof = {"bound": "int/popc", "achieved": match_rate / 1e12, "peak": popc_peak / 1e12,
                   "unit": "Tevals/s", "frac": match_rate / popc_peak, "kernel": "match_slots_warp_kernel",
                   "hamming_evals_per_launch": evals_per_launch, "ms_per_launch": match_ms,
-                  "peak_source": f"nominal {POPC_PER_CLK_PER_SM} POPC/clk/SM x {N_SM} SMs x {clk_mhz:.0f} MHz"}
+                  "peak_source": f"{popc_src} {popc_clk:.2f} evals/clk/SM x {N_SM} SMs x {clk_mhz:.0f} MHz"}
     dominant = census_roof if census_ms >= match_ms else match_roof
     step_ms = ms_max / args.steps
 
