@@ -1193,7 +1193,7 @@ rg_status rg_range_frames_host(rg_ctx* ctx, const rg_frame_batch* b, const rg_ra
   int32_t* st_cnt = DBUF(int32_t, ctx, B_OUT_CNT, 2 * (size_t)chunk);
   int32_t* counters = DBUF(int32_t, ctx, B_COUNTERS, kCounterInts);
   int32_t* hoffs = static_cast<int32_t*>(host_buf(ctx, 1, sizeof(int32_t) * 2 * (chunk + 1)));
-  int32_t* hc = static_cast<int32_t*>(host_buf(ctx, 0, 4 * sizeof(int32_t)));
+  int32_t* hc = static_cast<int32_t*>(host_buf(ctx, 0, kCounterInts * sizeof(int32_t)));
   NEED(st_l);
   NEED(st_r);
   NEED(st_d);
