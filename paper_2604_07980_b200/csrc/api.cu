@@ -615,11 +615,12 @@ rg_status rg_ctx_create(int device, rg_ctx** out) {
 void rg_ctx_destroy(rg_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
-  cudaStreamSynchronize(ctx->stream);
-  for (int i = 0; i < 32; ++i)
-    if (ctx->buf[i]) cudaFree(ctx->buf[i]);
-  for (int i = 0; i < 8; ++i)
-    if (ctx->hbuf[i]) cudaFreeHost(ctx->hbuf[i]);
+  for (cudaStream_t st : {ctx->stream, ctx->copy_stream, ctx->census_stream, ctx->match_stream})
+    if (st) cudaStreamSynchronize(st);
+  for (void* p : ctx->buf)
+    if (p) cudaFree(p);
+  for (void* p : ctx->hbuf)
+    if (p) cudaFreeHost(p);
   for (auto& ev : ctx->ev)
     if (ev) cudaEventDestroy(ev);
   for (auto ev : ctx->ev_sync)
