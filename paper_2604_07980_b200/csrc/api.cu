@@ -35,13 +35,14 @@ static_assert(B_COUNT <= 40, "rg_ctx::buf too small");
 void* dev_buf(rg_ctx* ctx, int id, size_t bytes) {
   if (bytes == 0) bytes = 16;
   if (ctx->cap[id] >= bytes) return ctx->buf[id];
+  const size_t old_cap = ctx->cap[id];
   if (ctx->buf[id]) {
     cudaStreamSynchronize(ctx->stream);
     cudaFree(ctx->buf[id]);
     ctx->buf[id] = nullptr;
     ctx->cap[id] = 0;
   }
-  const size_t want = std::max(bytes, ctx->cap[id] + ctx->cap[id] / 4);
+  const size_t want = std::max(bytes, old_cap + old_cap / 4);  // grow geometrically
   void* p = nullptr;
   if (cudaMalloc(&p, want) != cudaSuccess) {
     cudaGetLastError();

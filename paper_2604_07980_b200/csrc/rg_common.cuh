@@ -164,7 +164,6 @@ enum BufId {
   B_BM_L, B_BM_R, B_BM_OUT, B_BM_CNT, B_ROIS, B_STAGE_L, B_STAGE_R, B_SHIFT,
   B_SEQ, B_SGM_COST, B_SGM_ACC, B_BOX_IDX, B_BOX_OUT, B_COUNT
 };
-static_assert(B_COUNT <= (int)(sizeof(rg_ctx::buf) / sizeof(rg_ctx::buf[0])), "rg_ctx::buf too small");
 
 // error helpers (defined in api.cu)
 rg_status set_err(rg_ctx* ctx, rg_status st, const std::string& msg);
