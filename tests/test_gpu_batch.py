@@ -141,6 +141,20 @@ def test_reference_tests_pass_on_the_gpu_path(binary):
             assert f"criterion {c:2d}: PASS" in r.stdout
 
 
+def test_integration_example_program():
+    """INTEGRATION.md's C-ABI binding as a standalone C++ program
+    (tests/dropin/integration_example.cpp): device frame loop + host records."""
+    exe = os.path.join(ROOT, "tests", "dropin", "_bin", "integration_example")
+    if not os.path.exists(exe):
+        pytest.skip("integration example not built")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("frame ")]
+    assert len(lines) == 6
+    # the offset injected from frame 2 on is found and applied to later frames
+    assert any("delta* 2" in l for l in lines) and "shift 0" in lines[0]
+
+
 def _batch_vs_oracle(ctx, orc, L, R, D, cfg, focal=0.0, base=0.0):
     import torch
 
