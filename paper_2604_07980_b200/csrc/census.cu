@@ -88,9 +88,9 @@ __global__ void __launch_bounds__(TPB) census_frames_kernel(
 // two descriptors by one bit.  The 24 compare bits go into three fp16
 // accumulators initialised so each group's bits land in the low mantissa bits
 // (value 1024 + B), and four byte-permute/logic ops assemble the reference's
-// descriptor for both rows.  V is built once per 128 x 64 tile in shared
+// descriptor for both rows.  V is built once per 128 x 60 tile in shared
 // memory (6 byte permutes per 4 entries from raw image words, all loads of a
-// thread in flight at once); each warp then computes a 16-row strip reading
+// thread in flight at once); each warp then computes a 10-row strip reading
 // its 5-row window straight from V (2 LDS.128 per row).
 #ifndef RG_C2_MASK
 #define RG_C2_MASK 0xFFFFFFFFu
@@ -102,19 +102,19 @@ constexpr int C2_TX = RG_C2_TX;                   // tile columns: groups of 32 
 constexpr int C2_G = C2_TX / 128;                 // 128-column groups per warp row
 static_assert(C2_TX % 128 == 0, "tile width");
 #ifndef RG_C2_WARPS
-#define RG_C2_WARPS 8
+#define RG_C2_WARPS 6
 #endif
 #ifndef RG_C2_PR
-#define RG_C2_PR 4
+#define RG_C2_PR 5
 #endif
 constexpr int C2_WARPS = RG_C2_WARPS;
 constexpr int C2_PR = RG_C2_PR;                          // pair rows per warp strip
-constexpr int C2_TY = C2_WARPS * C2_PR * 2;       // 64 tile rows
+constexpr int C2_TY = C2_WARPS * C2_PR * 2;       // 60 tile rows (1080, 1860 and 480 split evenly)
 constexpr int C2_VW = C2_TX + 12;                 // V row stride: 4 pad + x0-2 .. x0+TX+1 + pad
 constexpr int C2_VOFF = 4;                        // V index of column x0-2
 constexpr int C2_WORDS = C2_TX / 4 + 2;           // image words per row (x0-4 .. x0+TX+3)
-constexpr int C2_RUNS = (C2_WARPS * 32) / C2_WORDS;          // 7 runs of rows in the V build
-constexpr int C2_RUN = (C2_TY + 3 + C2_RUNS - 1) / C2_RUNS;  // 10 V rows per run
+constexpr int C2_RUNS = (C2_WARPS * 32) / C2_WORDS;          // 5 runs of rows in the V build
+constexpr int C2_RUN = (C2_TY + 3 + C2_RUNS - 1) / C2_RUNS;  // 13 V rows per run
 constexpr int C2_VR = C2_RUNS * C2_RUN;           // V rows y0-2 .. (padded: every run is full)
 constexpr size_t C2_SMEM = sizeof(uint32_t) * C2_VR * C2_VW;
 
