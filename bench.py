@@ -138,6 +138,76 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows), "source": "nvml" if self.nvml else "nvidia-smi"}
 
 
+# ------------------------------------------------------------------ C5 stream
+def c5_stream(args, eng, ctx, dev, stream, rank, world, dets, ring_out0):
+    """BASELINE config 4 (C5): a stream of N distinct C2 frames (seeds 1..N)
+    sharded contiguously over the ranks (shard.shard_bounds),
+    each shard rendered in HBM by the device frame source, ranged in chunks of
+    --frames, and the per-box results all_gathered to every rank (NCCL).
+    Strong scaling: the stream is fixed as the rank count grows.  Timed with
+    CUDA events from the first chunk to the gathered results, max over ranks."""
+    import torch
+    import torch.distributed as dist
+    from paper_2604_07980_b200 import synth as S
+    from paper_2604_07980_b200.engine import OUT_DTYPE, pack_detections
+    from paper_2604_07980_b200.shard import shard_bounds
+
+    N, chunk = args.stream_frames, args.frames
+    lo, hi = shard_bounds(N, rank, world)
+    n, per = hi - lo, -(-N // world)
+    rec = eng.out_stride * OUT_DTYPE.itemsize
+    dL = torch.empty((max(n, 1), H, W), dtype=torch.uint8, device=dev)
+    dR = torch.empty_like(dL)
+    r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    r0.record(stream)
+    for c0 in range(0, n, 512):
+        c1 = min(n, c0 + 512)
+        S.render_frames_device(ctx, [S.scene_c2(seed=1 + f, noise=2.0)[0] for f in range(lo + c0, lo + c1)],
+                               dL[c0:], dR[c0:], stream=stream.cuda_stream)
+    r1.record(stream)
+    recs, offs = pack_detections([dets] * chunk)
+    d_dets = torch.from_numpy(recs.view(np.uint8)).to(dev)
+    d_offs = torch.from_numpy(offs).to(dev)
+    out = torch.zeros(per * rec, dtype=torch.uint8, device=dev)
+    cnt = torch.zeros(per, dtype=torch.int32, device=dev)
+    g_out = torch.zeros(world * out.numel(), dtype=torch.uint8, device=dev) if world > 1 else out
+    g_cnt = torch.zeros(world * per, dtype=torch.int32, device=dev) if world > 1 else cnt
+
+    def run():
+        for c0 in range(0, n, chunk):
+            c1 = min(n, c0 + chunk)
+            eng.range_device(dL[c0:c1], dR[c0:c1], d_dets, d_offs[:c1 - c0 + 1], out[c0 * rec:c1 * rec], cnt[c0:c1],
+                             stream=stream.cuda_stream)
+        if world > 1:
+            dist.all_gather_into_tensor(g_out, out)
+            dist.all_gather_into_tensor(g_cnt, cnt)
+
+    run()  # warm-up pass (allocations for the tail chunk)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    run()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1), r0.elapsed_time(r1)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms, render_ms = float(t[0]), float(t[1])
+    counts = g_cnt.view(world, per).cpu().numpy()
+    boxes = int(sum(counts[r][:shard_bounds(N, r, world)[1] - shard_bounds(N, r, world)[0]].sum()
+                    for r in range(world)))
+    # global frame 0 (seed 1) is also frame 0 of rank 0's bench ring
+    f0 = bytes(g_out[:rec].cpu().numpy()) == ring_out0 if ring_out0 is not None else None
+    del dL, dR
+    return {"config": f"C5: {N} distinct C2 frames (device-rendered, seeds 1..{N}, noise 2.0) sharded contiguously "
+                      f"over {world} rank(s), ranged in chunks of {chunk}, per-box results all_gathered (NCCL)",
+            "frames": N, "ms": ms, "frames_per_sec": N / (ms / 1e3), "boxes": boxes,
+            "boxes_per_sec": boxes / (ms / 1e3), "scaling": "strong", "render_ms_per_rank": render_ms,
+            "frame0_matches_ring": f0}
+
+
 # ------------------------------------------------------------------ frames
 def make_frames(n_distinct: int, seed0: int, noise: float = 2.0):
     """C2 frames: fixed 64-box layout, per-frame noise seed."""
@@ -277,7 +347,13 @@ def main():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--frames", type=int, default=256, help="frames per step per GPU")
-    ap.add_argument("--distinct", type=int, default=32, help="distinct rendered frames in the HBM ring")
+    ap.add_argument("--distinct", type=int, default=32, help="distinct host-rendered frames in the HBM ring "
+                    "(--frame-source host)")
+    ap.add_argument("--stream-frames", type=int, default=4096,
+                    help="C5: frames in the sharded stream measurement (0: skip)")
+    ap.add_argument("--frame-source", choices=["device", "host"], default="device",
+                    help="device: every ring frame rendered on the GPU (rg_render_frames_device); "
+                    "host: --distinct host renders tiled")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -303,15 +379,29 @@ def main():
     from paper_2604_07980_b200 import synth as S
 
     F = args.frames
-    L, R, dets, cfg = make_frames(args.distinct, 1 + rank * 100003)
-    n_boxes = len(dets)
     ctx = rg.Context(local)
-    eng = FrameEngine(W, H, cfg, n_boxes, S.F_PX, S.BASELINE_M, ctx=ctx)
     dev = torch.device("cuda", local)
-    # HBM ring: F frames (> L2 in bytes), tiled from the distinct renders
-    idx = np.arange(F) % args.distinct
-    dL = torch.from_numpy(L[idx]).to(dev)
-    dR = torch.from_numpy(R[idx]).to(dev)
+    seed0 = 1 + rank * 100003
+    if args.frame_source == "device":
+        # every frame of the HBM ring distinct, rendered in place by the device
+        # frame source (byte-identical to the host renderer, tests/test_gpu_render.py)
+        args.distinct = F
+        scenes = [S.scene_c2(seed=seed0 + i, noise=2.0)[0] for i in range(F)]
+        dets, cfg = S.ground_truth_detections(scenes[0]), S.scene_c2(seed=seed0)[1]
+        dL = torch.empty((F, H, W), dtype=torch.uint8, device=dev)
+        dR = torch.empty_like(dL)
+        S.render_frames_device(ctx, scenes, dL, dR)
+        torch.cuda.synchronize()
+        L, R = dL.cpu().numpy(), dR.cpu().numpy()  # host copies: e2e feed, CPU baseline, spot check
+        idx = np.arange(F)
+    else:
+        L, R, dets, cfg = make_frames(args.distinct, seed0)
+        # HBM ring: F frames (> L2 in bytes), tiled from the distinct renders
+        idx = np.arange(F) % args.distinct
+        dL = torch.from_numpy(L[idx]).to(dev)
+        dR = torch.from_numpy(R[idx]).to(dev)
+    n_boxes = len(dets)
+    eng = FrameEngine(W, H, cfg, n_boxes, S.F_PX, S.BASELINE_M, ctx=ctx)
     recs, offs = pack_detections([dets] * F)
     d_dets = torch.from_numpy(recs.view(np.uint8)).to(dev)
     d_offs = torch.from_numpy(offs).to(dev)
@@ -529,6 +619,20 @@ def main():
     except Exception as e:  # pragma: no cover
         sgm = {"error": str(e)}
 
+    # ---- C5: the sharded 4096-frame stream (BASELINE config 4)
+    stream_c5 = None
+    if args.stream_frames > 0:
+        try:
+            rec0 = eng.out_stride * OUT_DTYPE.itemsize
+            # ring frame 0 again (the latency runs reused the first output slot)
+            eng.range_device(dL[0:1], dR[0:1], d_dets, d_offs[:2], d_out, d_cnt, stream=stream.cuda_stream)
+            torch.cuda.synchronize()
+            stream_c5 = c5_stream(args, eng, ctx, dev, stream, rank, world, dets,
+                                  bytes(d_out[:rec0].cpu().numpy()) if rank == 0 else None)
+        except Exception as e:  # pragma: no cover
+            stream_c5 = {"error": str(e)}
+        torch.cuda.empty_cache()
+
     # ---- roofline of the dominant kernel (stage times from CUDA events on our stream)
     hbm_peak, sm_max, peak_kind = peaks()
     census_ms = stage_ms[0] / max(stage_launches[0], 1)
@@ -575,7 +679,8 @@ def main():
             "p50_latency_ms": 1000 * statistics.median(lat), "p50_latency_device_ms": 1000 * statistics.median(lat_dev),
             "config": {"workload": "C2: 1920x1080 rendered stereo pairs, 64 boxes (48 FAR + 16 CLOSE), "
                                    "dx_max_far = dx_max_close = 256, tau_v 1.0, fwd-bwd + sub-pixel, range z",
-                       "frames_per_step_per_gpu": F, "distinct_frames": args.distinct, "noise_sigma": 2.0,
+                       "frames_per_step_per_gpu": F, "distinct_frames": args.distinct, "frame_source": args.frame_source,
+                       "noise_sigma": 2.0,
                        "l2": f"inputs {2 * F * W * H / 1e6:.0f} MB + census {F * CENSUS_BYTES_PER_FRAME / 1e6:.0f} MB "
                              f"per step > 126 MB L2 (no flush needed)",
                        "parallelism": f"frame-sharded dp{world}, NCCL all_gather of per-box results"},
@@ -594,6 +699,7 @@ def main():
             "autorect": rect,
             "sequence": seq,
             "sgm": sgm,
+            "stream_c5": stream_c5,
             "clocks": clk,
             "parity_spot_check_vs_oracle": spot,
             "cpu_baseline": cpu,

@@ -536,6 +536,18 @@ typedef struct {
 rg_status rg_render_stereo_pair(const rg_scene_config* cfg, const rg_scene_object* objs,
                                 int n_obj, uint8_t* left, uint8_t* right,
                                 double* true_disparity, int32_t* object_id);
+/* Device frame source: render_stereo_pair (synth.hpp:142-230) for n_frames
+ * scenes rendered straight into device memory, byte-identical to
+ * rg_render_stereo_pair (feeds device-resident streams without PCIe, SURVEY
+ * 8(f) row 4).  cfgs[f] and objs[obj_offsets[f] .. obj_offsets[f+1]) are HOST
+ * arrays; every frame must share width and height.  d_left / d_right receive
+ * frame f at f * frame_stride as dense rows of `width` bytes.  Enqueued on
+ * `stream` (NULL: the context's stream); returns once the scene tables are
+ * uploaded (the kernels may still run).  RG_EINVAL for any scene
+ * rg_render_stereo_pair rejects. */
+rg_status rg_render_frames_device(rg_ctx* ctx, const rg_scene_config* cfgs, const rg_scene_object* objs,
+                                  const int32_t* obj_offsets, int n_frames, uint8_t* d_left,
+                                  uint8_t* d_right, int64_t frame_stride, void* stream);
 /* ground_truth_detections, synth.hpp:253-274 (capacity n_obj). */
 rg_status rg_ground_truth_detections(const rg_scene_config* cfg,
                                      const rg_scene_object* objs, int n_obj,

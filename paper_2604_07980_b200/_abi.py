@@ -200,6 +200,7 @@ SIGNATURES = {
     "rg_sgm_direction_pass": (I, [P, P, I, I, I, I, I, I, I, P]),
     "rg_render_stereo_pair": (I, [P, P, I, P, P, P, P]),
     "rg_ground_truth_detections": (I, [P, P, I, P, P]),
+    "rg_render_frames_device": (I, [P, P, P, P, I, P, P, I64, P]),
 }
 
 

@@ -162,7 +162,7 @@ enum BufId {
   B_OBJ, B_SLOTS, B_SLOT_RES, B_OUT, B_OUT_CNT, B_COUNTERS, B_MAPX, B_MAPY,
   B_PTS, B_OFFS, B_RANGES, B_MRES, B_TMP0, B_TMP1, B_TMP2, B_TMP3, B_STATS,
   B_BM_L, B_BM_R, B_BM_OUT, B_BM_CNT, B_ROIS, B_STAGE_L, B_STAGE_R, B_SHIFT,
-  B_SEQ, B_SGM_COST, B_SGM_ACC, B_BOX_IDX, B_BOX_OUT, B_COUNT
+  B_SEQ, B_SGM_COST, B_SGM_ACC, B_BOX_IDX, B_BOX_OUT, B_SYNTH, B_COUNT
 };
 
 // error helpers (defined in api.cu)

@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "../../include/ranger_cuda.h"
+#include "synth_scene.h"
 
 namespace {
 
@@ -99,14 +100,14 @@ void rows_parallel(int n, Fn&& fn) {
 
 }  // namespace
 
-extern "C" rg_status rg_render_stereo_pair(const rg_scene_config* cfg, const rg_scene_object* objs,
-                                           int n_obj, uint8_t* left, uint8_t* right,
-                                           double* true_disp, int32_t* object_id) {
-  if (!cfg || !left || !right || n_obj < 0 || (n_obj > 0 && !objs)) return RG_EINVAL;
-  const rg_scene_config& c = *cfg;
+namespace rg_synth {
+
+rg_status prepare_scene(const rg_scene_config& c, const rg_scene_object* objs, int n_obj,
+                        std::vector<RenderObj>& out) {
+  out.clear();
+  if (n_obj < 0 || (n_obj > 0 && !objs)) return RG_EINVAL;
   if (c.width < 8 || c.height < 8 || c.gamma <= 0) return RG_EINVAL;
   const int w = c.width, h = c.height;
-
   std::vector<Proj> pr(static_cast<size_t>(n_obj));
   for (int i = 0; i < n_obj; ++i) {
     const Cam p = to_camera(objs[i], c);
@@ -115,25 +116,16 @@ extern "C" rg_status rg_render_stereo_pair(const rg_scene_config* cfg, const rg_
   }
   std::vector<int> order(static_cast<size_t>(n_obj));
   for (int i = 0; i < n_obj; ++i) order[i] = i;
-  std::sort(order.begin(), order.end(), [&](int a, int b) {  // far to near
+  std::sort(order.begin(), order.end(), [&](int a, int b) {  // far to near, synth.hpp:168
     if (pr[a].z != pr[b].z) return pr[a].z > pr[b].z;
     return objs[a].id < objs[b].id;
   });
   for (int i : order)
     if (std::abs(objs[i].disparity_ramp) >= 1) return RG_EINVAL;
-
-  const NoiseField bg{c.background_seed, c.texture_cell_px, c.background_contrast, c.texture_quant};
-  std::vector<NoiseField> tex;
-  struct Span {
-    int ly0, ly1, lx0, lx1, rx0, rx1;
-    double k, c0;
-  };
-  std::vector<Span> sp;
   for (int i : order) {
     const rg_scene_object& o = objs[i];
     const Proj& p = pr[i];
-    tex.push_back({o.texture_seed, c.texture_cell_px, o.contrast, c.texture_quant});
-    Span s;
+    RenderObj s{};
     s.ly0 = std::max(0, int(std::ceil(p.v0)));
     s.ly1 = std::min(h - 1, int(std::floor(p.v1)));
     s.lx0 = std::max(0, int(std::ceil(p.u0)));
@@ -143,8 +135,46 @@ extern "C" rg_status rg_render_stereo_pair(const rg_scene_config* cfg, const rg_
     const double ru0 = p.u0 * s.k - s.c0, ru1 = p.u1 * s.k - s.c0;
     s.rx0 = std::max(0, int(std::ceil(std::min(ru0, ru1))));
     s.rx1 = std::min(w - 1, int(std::floor(std::max(ru0, ru1))));
-    sp.push_back(s);
+    s.id = o.id;
+    s.u0 = p.u0;
+    s.u1 = p.u1;
+    s.v0 = p.v0;
+    s.uc = p.uc;
+    s.disp = p.disp;
+    s.ramp = o.disparity_ramp;
+    s.tex_seed = o.texture_seed;
+    s.contrast = o.contrast;
+    out.push_back(s);
   }
+  return RG_OK;
+}
+
+void radiometric_lut(const rg_scene_config& c, uint8_t lut[256]) {  // synth.hpp:212-217
+  const bool apply = c.gain != 1 || c.rad_bias != 0 || c.gamma != 1;
+  for (int v = 0; v < 256; ++v) {
+    if (!apply) {
+      lut[v] = uint8_t(v);
+      continue;
+    }
+    const double m = c.gain * std::pow(v / 255.0, c.gamma) * 255.0 + c.rad_bias;
+    const long r = std::lround(m);
+    lut[v] = uint8_t(r < 0 ? 0 : (r > 255 ? 255 : r));
+  }
+}
+
+}  // namespace rg_synth
+
+extern "C" rg_status rg_render_stereo_pair(const rg_scene_config* cfg, const rg_scene_object* objs,
+                                           int n_obj, uint8_t* left, uint8_t* right,
+                                           double* true_disp, int32_t* object_id) {
+  if (!cfg || !left || !right) return RG_EINVAL;
+  const rg_scene_config& c = *cfg;
+  std::vector<rg_synth::RenderObj> sp;
+  if (rg_synth::prepare_scene(c, objs, n_obj, sp) != RG_OK) return RG_EINVAL;
+  const int w = c.width, h = c.height;
+  const NoiseField bg{c.background_seed, c.texture_cell_px, c.background_contrast, c.texture_quant};
+  std::vector<NoiseField> tex;
+  for (const auto& s : sp) tex.push_back({s.tex_seed, c.texture_cell_px, s.contrast, c.texture_quant});
   const bool shift = c.vertical_offset_px != 0;
   std::vector<uint8_t> rtmp;
   uint8_t* rbody = right;
@@ -162,30 +192,26 @@ extern "C" rg_status rg_render_stereo_pair(const rg_scene_config* cfg, const rg_
     }
     if (true_disp) std::fill(true_disp + size_t(y) * w, true_disp + size_t(y + 1) * w, 0.0);
     if (object_id) std::fill(object_id + size_t(y) * w, object_id + size_t(y + 1) * w, -1);
-    for (size_t t = 0; t < order.size(); ++t) {
-      const Span& s = sp[t];
+    for (size_t t = 0; t < sp.size(); ++t) {
+      const rg_synth::RenderObj& s = sp[t];
       if (y < s.ly0 || y > s.ly1) continue;
-      const rg_scene_object& o = objs[order[t]];
-      const Proj& p = pr[order[t]];
       for (int x = s.lx0; x <= s.lx1; ++x) {
-        lrow[x] = to_byte(tex[t].at(x - p.u0, y - p.v0));
-        if (true_disp) true_disp[size_t(y) * w + x] = p.disp + o.disparity_ramp * (x - p.uc);
-        if (object_id) object_id[size_t(y) * w + x] = o.id;
+        lrow[x] = to_byte(tex[t].at(x - s.u0, y - s.v0));
+        if (true_disp) true_disp[size_t(y) * w + x] = s.disp + s.ramp * (x - s.uc);
+        if (object_id) object_id[size_t(y) * w + x] = s.id;
       }
       for (int xr = s.rx0; xr <= s.rx1; ++xr) {
         const double u = (xr + s.c0) / s.k;
-        if (u < p.u0 || u > p.u1) continue;
-        rrow[xr] = to_byte(tex[t].at(u - p.u0, y - p.v0));
+        if (u < s.u0 || u > s.u1) continue;
+        rrow[xr] = to_byte(tex[t].at(u - s.u0, y - s.v0));
       }
     }
   });
 
   if (c.gain != 1 || c.rad_bias != 0 || c.gamma != 1) {
-    for (size_t i = 0; i < size_t(w) * h; ++i) {
-      const double m = c.gain * std::pow(rbody[i] / 255.0, c.gamma) * 255.0 + c.rad_bias;
-      const long v = std::lround(m);
-      rbody[i] = uint8_t(v < 0 ? 0 : (v > 255 ? 255 : v));
-    }
+    uint8_t lut[256];
+    rg_synth::radiometric_lut(c, lut);
+    for (size_t i = 0; i < size_t(w) * h; ++i) rbody[i] = lut[rbody[i]];
   }
   if (shift) {  // image.hpp:145-154: out(y) = in(clamp(y - dy))
     for (int y = 0; y < h; ++y) {

@@ -81,6 +81,36 @@ def render_stereo_pair(cfg: SceneConfig) -> Tuple[np.ndarray, np.ndarray]:
     return left, right
 
 
+def render_frames_device(ctx, cfgs: List[SceneConfig], left, right, frame_stride: int = 0, stream=None) -> None:
+    """Device frame source (synth.hpp:142-230 for a batch of scenes, rendered
+    in HBM): frame f of `cfgs` lands at byte f * frame_stride of the uint8 CUDA
+    tensors `left` / `right` (dense rows; frame_stride defaults to W*H).
+    Byte-identical to render_stereo_pair; `stream` is a CUDA stream handle
+    (int) or None for the context's stream."""
+    if not cfgs:
+        raise InvalidArgument("render_frames_device: no scenes")
+    w, h = cfgs[0].width, cfgs[0].height
+    stride = frame_stride or w * h
+    need = (len(cfgs) - 1) * stride + w * h
+    for t in (left, right):
+        if not t.is_cuda or t.dtype.itemsize != 1 or not t.is_contiguous() or t.numel() < need:
+            raise InvalidArgument("render_frames_device: outputs must be contiguous uint8 CUDA tensors "
+                                  f"of at least {need} bytes")
+    cs, objs, offs = [], [], [0]
+    for cfg in cfgs:
+        c, o = cfg.to_c()
+        cs.append(c)
+        objs.extend(o[:len(cfg.objects)])
+        offs.append(len(objs))
+    carr = (_abi.SceneConfig * len(cs))(*cs)
+    oarr = (_abi.SceneObject * max(len(objs), 1))(*objs)
+    off = (C.c_int32 * len(offs))(*offs)
+    st = lib().rg_render_frames_device(ctx.handle, carr, oarr, off, len(cfgs), C.c_void_p(left.data_ptr()),
+                                       C.c_void_p(right.data_ptr()), stride,
+                                       C.c_void_p(stream) if stream else None)
+    ctx.check(st)
+
+
 def ground_truth_detections(cfg: SceneConfig) -> List[Detection]:
     """synth.hpp:253-274."""
     c, objs = cfg.to_c()
