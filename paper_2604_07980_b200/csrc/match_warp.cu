@@ -624,15 +624,20 @@ cudaError_t launch_match_slots(const Slot* slots, int32_t* counters, int slot_ca
   if (wide) return launch_variant<unsigned long long, 8, 2>(RG_ARGS);  // 9x7 extension
   // latency mode (a few frames): most SMs would idle and the FAR blocks are
   // the critical path, so one CTA per FAR block splits its passes over 4
-  // warps, with an L1 prefetch of the point 4 ahead (single C2 frame:
-  // 84 -> 45 us)
+  // warps (single C2 frame: 84 -> 43 us).  The L1 prefetch of the point 4
+  // ahead paid 2 us until the padded rasters got 128-B aligned rows; now it
+  // costs 2 us (variant 7 keeps it); 8 or 16 warps per FAR block measured
+  // 47 / 80 us (variants 5, 6).
   if (variant == 0 && n_frames > 0 && n_frames <= kLatencyFrames)
-    return launch_variant<uint32_t, 4, 12, 4, true>(RG_ARGS);
+    return launch_variant<uint32_t, 4, 12, 0, true>(RG_ARGS);
   switch (variant) {  // A/B knobs; default measured best (tools/census_time.py with RG_MATCH_VARIANT)
     case 1: return launch_variant<uint32_t, 8, 4>(RG_ARGS);
     case 2: return launch_variant<uint32_t, 8, 5>(RG_ARGS);
     case 3: return launch_variant<uint32_t, 16, 4>(RG_ARGS);
     case 4: return launch_variant<uint32_t, 4, 12, 0, true>(RG_ARGS);
+    case 5: return launch_variant<uint32_t, 8, 6, 4, true>(RG_ARGS);
+    case 6: return launch_variant<uint32_t, 16, 3, 4, true>(RG_ARGS);
+    case 7: return launch_variant<uint32_t, 4, 12, 4, true>(RG_ARGS);
     default: return launch_variant<uint32_t, 16, 3>(RG_ARGS);
   }
 #undef RG_ARGS
