@@ -214,11 +214,16 @@ __device__ __forceinline__ void c2_strip(const uint32_t* __restrict__ V, uint32_
   }
 }
 
-#ifndef RG_C2_MINB
-#define RG_C2_MINB 1
+// RG_C2_MINB: A/B knob only.  Any explicit minimum (even 1) changes ptxas's
+// register heuristic: 1 gives 88 registers and 1.54 ms per 256 C2 frames, 6
+// gives 56 and 1.53 ms, the bare bound 62 registers and 1.353 ms.
+#ifdef RG_C2_MINB
+#define RG_C2_BOUNDS __launch_bounds__(C2_WARPS * 32, RG_C2_MINB)
+#else
+#define RG_C2_BOUNDS __launch_bounds__(C2_WARPS * 32)
 #endif
 template <bool S31>
-__global__ void __launch_bounds__(C2_WARPS * 32, RG_C2_MINB) census_pairs_kernel(
+__global__ void RG_C2_BOUNDS census_pairs_kernel(
     const uint8_t* __restrict__ left, const uint8_t* __restrict__ right, int64_t frame_stride,
     int pitch, int w, int h, uint32_t* __restrict__ fl, uint32_t* __restrict__ fr, PadGeom gf,
     uint32_t* __restrict__ sl, uint32_t* __restrict__ sr, PadGeom gs, const int32_t* __restrict__ lshift) {
