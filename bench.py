@@ -15,7 +15,6 @@ Prints one JSON line (rank 0).  Needs the CUDA library (build() first).
 from __future__ import annotations
 
 import argparse
-import ctypes as C
 import json
 import os
 import statistics
@@ -138,23 +137,84 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows), "source": "nvml" if self.nvml else "nvidia-smi"}
 
 
+# ------------------------------------------------------------------ shared
+def workload_config(F: int, world: int) -> dict:
+    """The `config` both arms print (same_config): the C2 workload, frames per
+    step per GPU and how the frames are seeded."""
+    return {"workload": "C2: 1920x1080 rendered stereo pairs (render_stereo_pair), 64 boxes (48 FAR + 16 CLOSE), "
+                        "dx_max_far = dx_max_close = 256, tau_v 1.0, fwd-bwd + sub-pixel, range z",
+            "frames_per_step_per_gpu": F, "noise_sigma": 2.0,
+            "frame_seeds": "global frame g = rank * frames_per_step + i has seed 1 + g (all distinct)",
+            "l2": f"inputs {2 * F * W * H / 1e6:.0f} MB + census {F * CENSUS_BYTES_PER_FRAME / 1e6:.0f} MB "
+                  f"per step per GPU > 126 MB L2 (no flush needed)",
+            "parallelism": f"frame-sharded dp{world}, per-box results all_gathered"}
+
+
+def ref_arm():
+    """oracle/ref_arm.py: the reference compiled in place, no product import."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import ref_arm as ra
+    return ra
+
+
+def free_port() -> int:
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def spawn_ranks(n: int) -> int:
+    """--gpus N without WORLD_SIZE: re-exec this command under
+    torch.distributed.run with N ranks (one per GPU) on 127.0.0.1."""
+    import torch
+    have = torch.cuda.device_count()
+    if n > have:
+        print(json.dumps({"metric": METRIC, "error": f"--gpus {n} but only {have} CUDA device(s) visible"}))
+        return 1
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def compare_records(got_recs, got_cnt, want_recs, want_cnt):
+    """Per-frame bytewise comparison of rg_object_disparity rows -> (frame
+    mismatches, box mismatches)."""
+    bad_f = bad_b = 0
+    for f in range(len(want_cnt)):
+        n = int(want_cnt[f])
+        if int(got_cnt[f]) != n:
+            bad_f += 1
+            bad_b += max(n, int(got_cnt[f]))
+            continue
+        g = np.frombuffer(bytes(got_recs[f][:32 * n]), np.uint8).reshape(n, 32)
+        w = np.frombuffer(want_recs[f][:n].tobytes(), np.uint8).reshape(n, 32)
+        d = int((g != w).any(axis=1).sum())
+        bad_b += d
+        bad_f += int(d > 0)
+    return bad_f, bad_b
+
+
 # ------------------------------------------------------------------ C5 stream
-def c5_stream(args, eng, ctx, dev, stream, rank, world, dets, ring_out0):
+def c5_stream(args, eng, ctx, dev, stream, rank, world, dets, recs_np, offs_np):
     """BASELINE config 4 (C5): a stream of N distinct C2 frames (seeds 1..N)
-    sharded contiguously over the ranks (shard.shard_bounds),
-    each shard rendered in HBM by the device frame source, ranged in chunks of
-    --frames, and the per-box results all_gathered to every rank (NCCL).
-    Strong scaling: the stream is fixed as the rank count grows.  Timed with
-    CUDA events from the first chunk to the gathered results, max over ranks."""
+    sharded contiguously over the ranks, each shard rendered in HBM by the
+    device frame source (untimed), ranged in chunks of --frames and the
+    per-box results all_gathered -- shard.run_stream / gather_slabs /
+    frame_order / gathered_boxes, the functions tests/test_dist_cpu.py runs at
+    world 2.  Strong scaling.  Timed with CUDA events, max over ranks.  Then
+    every (N/256)-th frame is re-ranged by the reference on the host cores
+    and compared with the gathered records."""
     import torch
     import torch.distributed as dist
-    from paper_2604_07980_b200 import synth as S
-    from paper_2604_07980_b200.engine import OUT_DTYPE, pack_detections
-    from paper_2604_07980_b200.shard import shard_bounds
+    from paper_2604_07980_b200 import shard, synth as S
+    from paper_2604_07980_b200.engine import OUT_DTYPE
 
     N, chunk = args.stream_frames, args.frames
-    lo, hi = shard_bounds(N, rank, world)
-    n, per = hi - lo, -(-N // world)
+    lo, hi = shard.shard_bounds(N, rank, world)
+    n = hi - lo
     rec = eng.out_stride * OUT_DTYPE.itemsize
     dL = torch.empty((max(n, 1), H, W), dtype=torch.uint8, device=dev)
     dR = torch.empty_like(dL)
@@ -165,22 +225,18 @@ def c5_stream(args, eng, ctx, dev, stream, rank, world, dets, ring_out0):
         S.render_frames_device(ctx, [S.scene_c2(seed=1 + f, noise=2.0)[0] for f in range(lo + c0, lo + c1)],
                                dL[c0:], dR[c0:], stream=stream.cuda_stream)
     r1.record(stream)
-    recs, offs = pack_detections([dets] * chunk)
-    d_dets = torch.from_numpy(recs.view(np.uint8)).to(dev)
-    d_offs = torch.from_numpy(offs).to(dev)
-    out = torch.zeros(per * rec, dtype=torch.uint8, device=dev)
-    cnt = torch.zeros(per, dtype=torch.int32, device=dev)
-    g_out = torch.zeros(world * out.numel(), dtype=torch.uint8, device=dev) if world > 1 else out
-    g_cnt = torch.zeros(world * per, dtype=torch.int32, device=dev) if world > 1 else cnt
+    d_dets = torch.from_numpy(np.tile(recs_np[offs_np[0]:offs_np[1]], chunk).view(np.uint8)).to(dev)
+    d_offs = torch.from_numpy((np.arange(chunk + 1) * len(dets)).astype(np.int32)).to(dev)
+    out, cnt, g_out, g_cnt = shard.alloc_slabs(N, world, rec, device=dev)
+
+    def range_chunk(glo, ghi, o, c):
+        a = glo - lo
+        eng.range_device(dL[a:a + ghi - glo], dR[a:a + ghi - glo], d_dets, d_offs[:ghi - glo + 1], o, c,
+                         stream=stream.cuda_stream)
 
     def run():
-        for c0 in range(0, n, chunk):
-            c1 = min(n, c0 + chunk)
-            eng.range_device(dL[c0:c1], dR[c0:c1], d_dets, d_offs[:c1 - c0 + 1], out[c0 * rec:c1 * rec], cnt[c0:c1],
-                             stream=stream.cuda_stream)
-        if world > 1:
-            dist.all_gather_into_tensor(g_out, out)
-            dist.all_gather_into_tensor(g_cnt, cnt)
+        shard.run_stream(range_chunk, N, rank, world, chunk, out, cnt, rec)
+        shard.gather_slabs(out, cnt, g_out, g_cnt, world)
 
     run()  # warm-up pass (allocations for the tail chunk)
     torch.cuda.synchronize()
@@ -195,92 +251,251 @@ def c5_stream(args, eng, ctx, dev, stream, rank, world, dets, ring_out0):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms, render_ms = float(t[0]), float(t[1])
-    counts = g_cnt.view(world, per).cpu().numpy()
-    boxes = int(sum(counts[r][:shard_bounds(N, r, world)[1] - shard_bounds(N, r, world)[0]].sum()
-                    for r in range(world)))
-    # global frame 0 (seed 1) is also frame 0 of rank 0's bench ring
-    f0 = bytes(g_out[:rec].cpu().numpy()) == ring_out0 if ring_out0 is not None else None
+    boxes = shard.gathered_boxes(g_cnt, N, world)
+    # parity sample: every (N/256)-th global frame, checked by its owner rank
+    parity = {"checked_frames": 0, "frame_mismatches": 0, "box_mismatches": 0}
+    if not args.no_parity:
+        ra = ref_arm()
+        step_s = max(1, N // args.parity_c5_frames)
+        mine = [g for g in range(0, N, step_s) if lo <= g < hi]
+        recs_all, cnt_all = shard.frame_order(g_out, g_cnt, N, world, rec)
+        if mine and ra.have_reference():
+            idx = torch.tensor([g - lo for g in mine], device=dev)
+            hL, hR = dL[idx].cpu().numpy(), dR[idx].cpu().numpy()
+            pr, po = np.tile(recs_np[offs_np[0]:offs_np[1]], len(mine)), \
+                (np.arange(len(mine) + 1) * len(dets)).astype(np.int32)
+            _, want, wcnt = ra.range_frames(hL, hR, pr, po, ra.ranger_config_c2(), ra.cpu_threads(), eng.out_stride)
+            bf, bb = compare_records(recs_all[mine], cnt_all[mine], want, wcnt)
+            parity = {"checked_frames": len(mine), "frame_mismatches": bf, "box_mismatches": bb}
+        pt = torch.tensor([parity["checked_frames"], parity["frame_mismatches"], parity["box_mismatches"]],
+                          dtype=torch.int64, device=dev)
+        if world > 1:
+            dist.all_reduce(pt)
+        parity = {"checked_frames": int(pt[0]), "frame_mismatches": int(pt[1]), "box_mismatches": int(pt[2]),
+                  "sample": f"every {step_s}-th frame of the stream, re-ranged by oracle/_ref (the reference "
+                            "compiled in place) on the owner rank's host cores, vs the gathered records",
+                  "checker": "reference" if ra.have_reference() else "unavailable"}
     del dL, dR
     return {"config": f"C5: {N} distinct C2 frames (device-rendered, seeds 1..{N}, noise 2.0) sharded contiguously "
-                      f"over {world} rank(s), ranged in chunks of {chunk}, per-box results all_gathered (NCCL)",
+                      f"over {world} rank(s), ranged in chunks of {chunk}, per-box results all_gathered",
             "frames": N, "ms": ms, "frames_per_sec": N / (ms / 1e3), "boxes": boxes,
             "boxes_per_sec": boxes / (ms / 1e3), "scaling": "strong", "render_ms_per_rank": render_ms,
-            "frame0_matches_ring": f0}
+            "parity": parity}
 
 
-# ------------------------------------------------------------------ frames
-def make_frames(n_distinct: int, seed0: int, noise: float = 2.0):
-    """C2 frames: fixed 64-box layout, per-frame noise seed."""
+# ------------------------------------------------------------------ other BASELINE configs
+def config_c3(args, ctx, dev, stream):
+    """C3 (BASELINE config 2): 2880x1860, 256 boxes (192 FAR in 96 occluded
+    pairs + 64 CLOSE), occlusion-aware sampling, CLOSE median aggregation;
+    device-rendered distinct frames, one rg_range_frames per step; the first
+    frames re-ranged by the reference for parity."""
+    import torch
     from paper_2604_07980_b200 import synth as S
-    from concurrent.futures import ThreadPoolExecutor
+    from paper_2604_07980_b200.engine import OUT_DTYPE, FrameEngine, pack_detections
 
-    sc0, cfg = S.scene_c2(seed=seed0, noise=noise)
-    dets = S.ground_truth_detections(sc0)
+    F3 = args.c3_frames
+    sc0, cfg = S.scene_c3(seed=1, noise=2.0)
+    w, h = sc0.width, sc0.height
+    scenes = [S.scene_c3(seed=1 + i, noise=2.0)[0] for i in range(F3)]
+    dets = S.ground_truth_detections(scenes[0])
+    dL = torch.empty((F3, h, w), dtype=torch.uint8, device=dev)
+    dR = torch.empty_like(dL)
+    S.render_frames_device(ctx, scenes, dL, dR, stream=stream.cuda_stream)
+    eng = FrameEngine(w, h, cfg, len(dets), S.F_PX, S.BASELINE_M, ctx=ctx)
+    recs, offs = pack_detections([dets] * F3)
+    d_dets = torch.from_numpy(recs.view(np.uint8)).to(dev)
+    d_offs = torch.from_numpy(offs).to(dev)
+    out = torch.zeros(F3 * eng.out_stride * OUT_DTYPE.itemsize, dtype=torch.uint8, device=dev)
+    cnt = torch.zeros(F3, dtype=torch.int32, device=dev)
+    step = lambda: eng.range_device(dL, dR, d_dets, d_offs, out, cnt, stream=stream.cuda_stream)  # noqa: E731
+    for _ in range(3):
+        step()
+    torch.cuda.synchronize()
+    ctx.reset_counters()
+    reps = max(3, min(args.steps, 10))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(reps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    evals, _ = ctx.work()
+    boxes = int(cnt.sum().item())
+    res = {"config": f"C3: {w}x{h}, {len(dets)} boxes (192 FAR incl. 96 occluded + 64 CLOSE), dx_max 256, "
+                     f"{F3} device-rendered distinct frames (noise 2.0) per rg_range_frames call",
+           "ms_per_step": ms, "boxes_per_sec": boxes / (ms / 1e3), "frames_per_sec": F3 / (ms / 1e3),
+           "valid_boxes_per_frame": None, "hamming_evals_per_frame": evals / (reps * F3)}
+    o = np.frombuffer(out.cpu().numpy().tobytes(), OUT_DTYPE).reshape(F3, eng.out_stride)
+    c = cnt.cpu().numpy()
+    res["valid_boxes_per_frame"] = float(np.mean([o[f, :c[f]]["valid"].sum() for f in range(F3)]))
+    if not args.no_parity:
+        ra = ref_arm()
+        if ra.have_reference():
+            k = min(F3, args.c3_parity_frames)
+            hL, hR = dL[:k].cpu().numpy(), dR[:k].cpu().numpy()
+            _, want, wcnt = ra.range_frames(hL, hR, recs[:offs[k]], offs[:k + 1], cfg.to_c(), ra.cpu_threads(),
+                                            eng.out_stride)
+            got = out.cpu().numpy().reshape(F3, -1)
+            bf, bb = compare_records(got[:k], c[:k], want, wcnt)
+            res["parity"] = {"checked_frames": k, "frame_mismatches": bf, "box_mismatches": bb,
+                             "checker": "reference (oracle/_ref)"}
+    del dL, dR
+    return res
 
-    def render(i):
-        sc, _ = S.scene_c2(seed=seed0 + i, noise=noise)
-        return S.render_stereo_pair(sc)
 
-    with ThreadPoolExecutor(max_workers=2) as ex:  # renderer is itself row-parallel
-        pairs = list(ex.map(render, range(n_distinct)))
-    L = np.stack([p[0] for p in pairs])
-    R = np.stack([p[1] for p in pairs])
-    return L, R, dets, cfg
+def config_c1_9x7(args, ctx, dev, stream):
+    """C1 (BASELINE config 0) with the 9x7 / uint64 census extension: 640x480,
+    8 boxes at integer disparities, dx_max 64; parity against the C
+    restatement (the reference has no 9x7 window: parity unpinned)."""
+    import torch
+    from paper_2604_07980_b200 import _abi, synth as S
+    from paper_2604_07980_b200.engine import OUT_DTYPE, FrameEngine, pack_detections
+
+    F1 = args.c1_frames
+    sc0, cfg = S.scene_c1(seed=1, noise=2.0)
+    cfg.census_9x7 = True
+    w, h = sc0.width, sc0.height
+    scenes = [S.scene_c1(seed=1 + i, noise=2.0)[0] for i in range(F1)]
+    dets = S.ground_truth_detections(scenes[0])
+    dL = torch.empty((F1, h, w), dtype=torch.uint8, device=dev)
+    dR = torch.empty_like(dL)
+    S.render_frames_device(ctx, scenes, dL, dR, stream=stream.cuda_stream)
+    eng = FrameEngine(w, h, cfg, len(dets), S.F_PX, S.BASELINE_M, ctx=ctx)
+    recs, offs = pack_detections([dets] * F1)
+    d_dets = torch.from_numpy(recs.view(np.uint8)).to(dev)
+    d_offs = torch.from_numpy(offs).to(dev)
+    out = torch.zeros(F1 * eng.out_stride * OUT_DTYPE.itemsize, dtype=torch.uint8, device=dev)
+    cnt = torch.zeros(F1, dtype=torch.int32, device=dev)
+    step = lambda: eng.range_device(dL, dR, d_dets, d_offs, out, cnt, stream=stream.cuda_stream)  # noqa: E731
+    for _ in range(3):
+        step()
+    torch.cuda.synchronize()
+    ctx.reset_counters()
+    ctx.set_profiling(True)
+    reps = max(3, min(args.steps, 10))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(reps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ctx.set_profiling(False)
+    stage_ms, stage_launches, _ = ctx.counters()
+    ms = e0.elapsed_time(e1) / reps
+    boxes = int(cnt.sum().item())
+    cen_bytes = 2 * (w * h + 8 * w * h + 8 * (w // 2) * (h // 2))  # SURVEY 8(d): B = 8 for 9x7
+    cen_ms = stage_ms[0] / max(stage_launches[0], 1)
+    res = {"config": f"C1 9x7: {w}x{h}, {len(dets)} boxes (5 FAR + 3 CLOSE) at integer disparities, dx_max 64, "
+                     f"9x7 census / uint64 descriptors, {F1} device-rendered distinct frames (noise 2.0) per call",
+           "ms_per_step": ms, "boxes_per_sec": boxes / (ms / 1e3), "frames_per_sec": F1 / (ms / 1e3),
+           "census64": {"ms_per_launch": cen_ms, "achieved_gbs": cen_bytes * F1 / (cen_ms / 1e3) / 1e9,
+                        "algorithmic_bytes_per_frame": cen_bytes}}
+    if not args.no_parity:
+        sys.path.insert(0, os.path.join(ROOT, "tests"))
+        import oracle_lib
+        k = min(F1, 8)
+        hL, hR = dL[:k].cpu().numpy(), dR[:k].cpu().numpy()
+        got = out.cpu().numpy().reshape(F1, -1)
+        c = cnt.cpu().numpy()
+        bad_f = 0
+        for f in range(k):
+            want, _ = oracle_lib.oracle().estimate(hL[f], hR[f], [_abi.Detection(d.cx, d.cy, d.w, d.h, d.class_id,
+                                                                                 d.id) for d in dets],
+                                                   cfg.to_c(), S.F_PX, S.BASELINE_M)
+            wb = b"".join(bytes(x) for x in want)
+            bad_f += int(int(c[f]) != len(want) or bytes(got[f][:len(wb)]) != wb)
+        res["parity"] = {"checked_frames": k, "frame_mismatches": bad_f,
+                         "checker": "oracle restatement (9x7 parity unpinned: no reference 9x7 window)"}
+    del dL, dR
+    return res
 
 
-def cpu_threads():
-    try:
-        return len(os.sched_getaffinity(0))
-    except Exception:
-        return os.cpu_count() or 1
+# ------------------------------------------------------------------ reference arm
+def run_reference(args):
+    """Reference arm: the reference's own render_stereo_pair and
+    estimate_object_disparities (compiled in place into oracle/_ref; no
+    product library loaded), all host threads, frame-parallel (one whole frame
+    per thread at workers = 1), on the GPU arm's rank-0 step: the same
+    --frames C2 frames (seeds 1..F), K timed steps after W warm-up steps."""
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    if rank != 0:
+        return 0
+    ra = ref_arm()
+    if not ra.have_reference():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libranger_ref.so not built"}))
+        return 0
+    threads = ra.cpu_threads()
+    F = args.frames
+    L, R, dets, offs = ra.render([ra.scene_c2(1 + i, 2.0) for i in range(F)], threads)
+    cfg = ra.ranger_config_c2()
+    out_stride = 64
+    secs, boxes = [], 0
+    for i in range(args.warmup + args.steps):
+        t, _, cnt = ra.range_frames(L, R, dets, offs, cfg, threads, out_stride)
+        if i >= args.warmup:
+            secs.append(t)
+            boxes += int(cnt.sum())
+    total = sum(secs)
+    val = boxes / total
+    sample = (f"{F} C2 frames per step (seeds 1..{F}, noise 2.0) rendered by the reference's render_stereo_pair, "
+              f"ranged one per host thread at workers=1 (frame-parallel) by the reference's "
+              f"estimate_object_disparities from oracle/_ref, {len(secs)} steps, {total:.1f} s")
+    line = {
+        "metric": METRIC, "impl": "reference", "value": val, "unit": "boxes/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * total / len(secs),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8/u32/f64",
+        "data": "synthetic", "frames_per_sec": F * len(secs) / total,
+        "config": workload_config(F, world),
+        "cpu_baseline": {"value": val, "unit": "boxes/s", "cores": threads, "kind": "reference", "sample": sample,
+                         "cpu_model": ra.cpu_model()},
+        "e2e": {"value": val, "unit": "boxes/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
 
 
-def cpu_reference_run(L, R, dets, cfg, seconds: float, threads: int):
-    """Time the reference (oracle/_ref, compiled from the reference headers) on
-    the host cores, frame-parallel (SURVEY 8(d) mode iii), bounded in time."""
-    sys.path.insert(0, os.path.join(ROOT, "tests"))
-    import oracle_lib
-    from paper_2604_07980_b200 import _abi
-    from paper_2604_07980_b200.engine import OUT_DTYPE, pack_detections
-
-    if oracle_lib.have_reference():
-        chk, kind = oracle_lib.reference(), "reference"
-    else:
+def cpu_reference_run(L, R, dets_np, offs_np, seconds: float):
+    """cpu_baseline: the reference (oracle/_ref) on the host cores,
+    frame-parallel (SURVEY 8(d) mode iii), bounded in time, plus the
+    reference's per-stage times on one frame at workers = 1 and = nproc."""
+    import ctypes as C
+    ra = ref_arm()
+    if not ra.have_reference():
         return None
+    threads = ra.cpu_threads()
+    cfg = ra.ranger_config_c2()
     n = L.shape[0]
-    recs, offs = pack_detections([dets] * n)
-    c = cfg.to_c()
-    out_stride = min(len(dets), cfg.max_objects)
-    out = np.zeros(n * out_stride, OUT_DTYPE)
-    cnt = np.zeros(n, np.int32)
-    Lc, Rc = np.ascontiguousarray(L), np.ascontiguousarray(R)
-    frames, wall = 0, 0.0
-    boxes = 0
+    frames, wall, boxes = 0, 0.0, 0
     while wall < seconds:
-        t = chk.lib.ref_bench_estimate(Lc.ctypes.data, Rc.ctypes.data, W, H, n, recs.ctypes.data, offs.ctypes.data,
-                                       C.byref(c), threads, out.ctypes.data, out_stride, cnt.ctypes.data)
+        t, _, cnt = ra.range_frames(L, R, dets_np, offs_np, cfg, threads, 64)
         wall += t
         frames += n
         boxes += int(cnt.sum())
     res = {"value": boxes / wall, "unit": "boxes/s", "frames_per_sec": frames / wall, "cores": threads,
-           "kind": kind, "sample": f"{frames} C2 frames ({n} distinct, noise 2.0) ranged by the reference's "
-                                   f"estimate_object_disparities, {threads} threads x whole frames at workers=1, "
-                                   f"{wall:.1f} s"}
-    # SURVEY 8(d): the reference's stages on one frame at workers = 1 and
-    # workers = nproc (median of reps): estimate_object_disparities (ROI
-    # census path), census_transform x 2, and the C4 offset search
+           "cpu_model": ra.cpu_model(), "kind": "reference",
+           "sample": f"{frames} C2 frames ({n} distinct, noise 2.0) ranged by the reference's "
+                     f"estimate_object_disparities, {threads} threads x whole frames at workers=1, {wall:.1f} s"}
     try:
-        from paper_2604_07980_b200 import synth as S
-        d = (_abi.Detection * len(dets))(*[_abi.Detection(x.cx, x.cy, x.w, x.h, x.class_id, x.id) for x in dets])
-        roi = _abi.Rect(*S.C4_ROI)
-        bm = S.c4_bm().to_c()
+        lib = ra.lib()
+        d0 = np.ascontiguousarray(dets_np[offs_np[0]:offs_np[1]])
+
+        class Rect(C.Structure):
+            _fields_ = [("x0", C.c_int32), ("y0", C.c_int32), ("x1", C.c_int32), ("y1", C.c_int32)]
+
+        class Bm(C.Structure):
+            _fields_ = [("num_disparities", C.c_int32), ("block_size", C.c_int32), ("min_disparity", C.c_int32),
+                        ("downscale", C.c_int32), ("texture_threshold", C.c_double),
+                        ("uniqueness_ratio", C.c_double)]
+        roi, bm = Rect(480, 270, 1440, 810), Bm(32, 9, -4, 1, 10.0, 10.0)
         detail = {}
+        lib.ref_bench_stages.restype = C.c_int
         for wk, reps, rr in ((1, 3, 1), (threads, 5, 2)):
             t = (C.c_double * 3)()
-            chk.lib.ref_bench_stages.restype = C.c_int
-            st = chk.lib.ref_bench_stages(C.c_void_p(Lc[0].ctypes.data), C.c_void_p(Rc[0].ctypes.data), W, H,
-                                          C.byref(d), len(dets), C.byref(c), wk, reps, C.byref(roi), -8, 8,
-                                          C.byref(bm), rr, t)
+            st = lib.ref_bench_stages(C.c_void_p(L[0].ctypes.data), C.c_void_p(R[0].ctypes.data), W, H,
+                                      C.c_void_p(d0.ctypes.data), len(d0), C.byref(cfg), wk, reps, C.byref(roi),
+                                      -8, 8, C.byref(bm), rr, t)
             if st == 0:
                 detail[f"workers_{wk}"] = {"estimate_ms_per_frame": 1e3 * t[0], "census_x2_ms": 1e3 * t[1],
                                            "autorect_c4_ms": 1e3 * t[2]}
@@ -290,56 +505,6 @@ def cpu_reference_run(L, R, dets, cfg, seconds: float, threads: int):
     return res
 
 
-# ------------------------------------------------------------------ reference arm
-def run_reference(args):
-    """Reference arm: the reference's own estimate_object_disparities (compiled
-    in place into oracle/_ref) on all host threads, one whole C2 frame per
-    thread per step (frame-parallel), K timed steps after W warm-up steps."""
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
-        return 0
-    sys.path.insert(0, os.path.join(ROOT, "tests"))
-    import oracle_lib
-    from paper_2604_07980_b200.engine import OUT_DTYPE, pack_detections
-
-    if not oracle_lib.have_reference():
-        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libranger_ref.so not built"}))
-        return 0
-    threads = cpu_threads()
-    L, R, dets, cfg = make_frames(threads, 1)
-    chk = oracle_lib.reference()
-    recs, offs = pack_detections([dets] * threads)
-    c = cfg.to_c()
-    out_stride = min(len(dets), cfg.max_objects)
-    out = np.zeros(threads * out_stride, OUT_DTYPE)
-    cnt = np.zeros(threads, np.int32)
-    Lc, Rc = np.ascontiguousarray(L), np.ascontiguousarray(R)
-    secs = []
-    for i in range(args.warmup + args.steps):
-        t = chk.lib.ref_bench_estimate(Lc.ctypes.data, Rc.ctypes.data, W, H, threads, recs.ctypes.data,
-                                       offs.ctypes.data, C.byref(c), threads, out.ctypes.data, out_stride,
-                                       cnt.ctypes.data)
-        if i >= args.warmup:
-            secs.append(t)
-    boxes = int(cnt.sum())
-    total = sum(secs)
-    val = boxes * len(secs) / total
-    sample = (f"{threads} C2 frames per step (noise 2.0), one per host thread at workers=1 (frame-parallel), "
-              f"reference estimate_object_disparities from oracle/_ref, {len(secs)} steps, {total:.1f} s")
-    line = {
-        "metric": METRIC, "impl": "reference", "value": val, "unit": "boxes/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * total / len(secs),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8/u32/f64",
-        "data": "synthetic", "frames_per_sec": threads * len(secs) / total,
-        "config": {"workload": "C2: 1920x1080 stereo, 64 boxes (48 FAR + 16 CLOSE), dx_max 256, "
-                               "fwd-bwd + sub-pixel, noise 2.0", "frames_per_step": threads},
-        "cpu_baseline": {"value": val, "unit": "boxes/s", "cores": threads, "kind": "reference", "sample": sample},
-        "e2e": {"value": val, "unit": "boxes/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }
-    print(json.dumps(line))
-    return 0
-
-
 # ------------------------------------------------------------------ our arm
 def main():
     ap = argparse.ArgumentParser()
@@ -347,21 +512,23 @@ def main():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--frames", type=int, default=256, help="frames per step per GPU")
-    ap.add_argument("--distinct", type=int, default=32, help="distinct host-rendered frames in the HBM ring "
-                    "(--frame-source host)")
     ap.add_argument("--stream-frames", type=int, default=4096,
                     help="C5: frames in the sharded stream measurement (0: skip)")
-    ap.add_argument("--frame-source", choices=["device", "host"], default="device",
-                    help="device: every ring frame rendered on the GPU (rg_render_frames_device); "
-                    "host: --distinct host renders tiled")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--latency-runs", type=int, default=300)
+    ap.add_argument("--no-parity", action="store_true", help="skip the parity sweeps against oracle/_ref")
+    ap.add_argument("--parity-c5-frames", type=int, default=256)
+    ap.add_argument("--latency-runs", type=int, default=1000)
+    ap.add_argument("--c3-frames", type=int, default=32, help="C3 frames per call (0: skip the C3 line)")
+    ap.add_argument("--c3-parity-frames", type=int, default=16)
+    ap.add_argument("--c1-frames", type=int, default=1024, help="9x7 C1 frames per call (0: skip)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
         return run_reference(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args.gpus)
 
     import torch
     import torch.distributed as dist
@@ -369,72 +536,55 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    assert world == args.gpus, f"WORLD_SIZE {world} != --gpus {args.gpus}"
+    assert world <= torch.cuda.device_count(), f"{world} ranks but {torch.cuda.device_count()} CUDA devices"
     torch.cuda.set_device(local)
     os.environ["RG_DEVICE"] = str(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
-    from paper_2604_07980_b200 import ranger as rg
-    from paper_2604_07980_b200.engine import DET_DTYPE, OUT_DTYPE, FrameEngine, pack_detections
+    from paper_2604_07980_b200 import ranger as rg, shard
+    from paper_2604_07980_b200.engine import OUT_DTYPE, FrameEngine, pack_detections
     from paper_2604_07980_b200 import synth as S
 
     F = args.frames
     ctx = rg.Context(local)
     dev = torch.device("cuda", local)
-    seed0 = 1 + rank * 100003
-    if args.frame_source == "device":
-        # every frame of the HBM ring distinct, rendered in place by the device
-        # frame source (byte-identical to the host renderer, tests/test_gpu_render.py)
-        args.distinct = F
-        scenes = [S.scene_c2(seed=seed0 + i, noise=2.0)[0] for i in range(F)]
-        dets, cfg = S.ground_truth_detections(scenes[0]), S.scene_c2(seed=seed0)[1]
-        dL = torch.empty((F, H, W), dtype=torch.uint8, device=dev)
-        dR = torch.empty_like(dL)
-        S.render_frames_device(ctx, scenes, dL, dR)
-        torch.cuda.synchronize()
-        L, R = dL.cpu().numpy(), dR.cpu().numpy()  # host copies: e2e feed, CPU baseline, spot check
-        idx = np.arange(F)
-    else:
-        L, R, dets, cfg = make_frames(args.distinct, seed0)
-        # HBM ring: F frames (> L2 in bytes), tiled from the distinct renders
-        idx = np.arange(F) % args.distinct
-        dL = torch.from_numpy(L[idx]).to(dev)
-        dR = torch.from_numpy(R[idx]).to(dev)
+    # the ring is this rank's shard of a (world x F)-frame stream: global frame
+    # g = rank * F + i, seed 1 + g, every frame distinct, rendered in HBM by the
+    # device frame source (byte-identical to the reference renderer,
+    # tests/test_gpu_render.py, tests/test_ref_arm.py)
+    lo, hi = shard.shard_bounds(F * world, rank, world)
+    scenes = [S.scene_c2(seed=1 + g, noise=2.0)[0] for g in range(lo, hi)]
+    dets, cfg = S.ground_truth_detections(scenes[0]), S.scene_c2(seed=1)[1]
+    dL = torch.empty((F, H, W), dtype=torch.uint8, device=dev)
+    dR = torch.empty_like(dL)
+    S.render_frames_device(ctx, scenes, dL, dR)
+    torch.cuda.synchronize()
+    L, R = dL.cpu().numpy(), dR.cpu().numpy()  # host copies: e2e feed, CPU baseline, parity sweep
     n_boxes = len(dets)
     eng = FrameEngine(W, H, cfg, n_boxes, S.F_PX, S.BASELINE_M, ctx=ctx)
+    rec = eng.out_stride * OUT_DTYPE.itemsize
     recs, offs = pack_detections([dets] * F)
     d_dets = torch.from_numpy(recs.view(np.uint8)).to(dev)
     d_offs = torch.from_numpy(offs).to(dev)
-    d_out = torch.zeros(F * eng.out_stride * OUT_DTYPE.itemsize, dtype=torch.uint8, device=dev)
-    d_cnt = torch.zeros(F, dtype=torch.int32, device=dev)
-    gather = torch.zeros(world * d_out.numel(), dtype=torch.uint8, device=dev) if world > 1 else None
+    d_out, d_cnt, g_out, g_cnt = shard.alloc_slabs(F * world, world, rec, device=dev)
     # a real (non-legacy-default) stream: the library launches on it and the
     # CUDA events below are recorded on it
     stream = torch.cuda.Stream(dev)
     torch.cuda.set_stream(stream)
 
-    def step():
-        eng.range_device(dL, dR, d_dets, d_offs, d_out, d_cnt, stream=stream.cuda_stream)
-        if world > 1:  # per-box results -> every rank's slab on rank 0 (NCCL over NVLink)
-            dist.all_gather_into_tensor(gather, d_out)
+    def range_chunk(glo, ghi, o, c):
+        eng.range_device(dL, dR, d_dets, d_offs, o, c, stream=stream.cuda_stream)
+
+    def step():  # the shard's F frames, then the per-box results to every rank
+        shard.run_stream(range_chunk, F * world, rank, world, F, d_out, d_cnt, rec)
+        shard.gather_slabs(d_out, d_cnt, g_out, g_cnt, world)
 
     # ---- warmup
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    # parity spot check of the bench frames against the C oracle (frame 0)
-    spot = None
-    if rank == 0:
-        try:
-            sys.path.insert(0, os.path.join(ROOT, "tests"))
-            import oracle_lib
-            from paper_2604_07980_b200 import _abi
-            want, _ = oracle_lib.oracle().estimate(L[0], R[0], [_abi.Detection(d.cx, d.cy, d.w, d.h, d.class_id, d.id)
-                                                                for d in dets], cfg.to_c(), S.F_PX, S.BASELINE_M)
-            got = np.frombuffer(d_out.cpu().numpy().tobytes(), OUT_DTYPE)[:int(d_cnt[0])]
-            spot = bool(len(got) == len(want) and all(bytes(w) == got[i].tobytes() for i, w in enumerate(want)))
-        except Exception as e:  # pragma: no cover
-            spot = f"error: {e}"
 
     # ---- timed region (device-resident feed, default one-stream schedule)
     ctx.reset_counters()
@@ -455,26 +605,41 @@ def main():
     clk = clocks.stop()
     _, _, total_launches = ctx.counters()
     evals, blocks = ctx.work()
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    boxes_step = shard.gathered_boxes(g_cnt, F * world, world)
+    value = boxes_step * args.steps / (ms_max / 1000.0)
+    fps = F * args.steps * world / (ms_max / 1000.0)
+
+    # ---- parity sweep: every ring frame of every rank, re-ranged by the
+    # reference (oracle/_ref) on the host cores, vs the gathered records
+    parity = None
+    if not args.no_parity:
+        ra = ref_arm()
+        bf = bb = 0
+        if ra.have_reference():
+            recs_all, cnt_all = shard.frame_order(g_out, g_cnt, F * world, world, rec)
+            _, want, wcnt = ra.range_frames(L, R, recs, offs, cfg.to_c(), ra.cpu_threads(), eng.out_stride)
+            bf, bb = compare_records(recs_all[lo:hi], cnt_all[lo:hi], want, wcnt)
+        pt = torch.tensor([hi - lo if ra.have_reference() else 0, bf, bb], dtype=torch.int64, device=dev)
+        if world > 1:
+            dist.all_reduce(pt)
+        parity = {"checked_frames": int(pt[0]), "frame_mismatches": int(pt[1]), "box_mismatches": int(pt[2]),
+                  "sample": "every ring frame of every rank (the timed step's output, after the gather)",
+                  "checker": "reference (oracle/_ref, compiled in place)" if ra.have_reference() else "unavailable"}
+
     # ---- kernel rooflines: the same steps with per-stage CUDA events
     ctx.reset_counters()
-    ctx.set_overlap(False)
     ctx.set_profiling(True)
     roof_steps = max(3, min(args.steps, 10))
     for _ in range(roof_steps):
         step()
     torch.cuda.synchronize()
     ctx.set_profiling(False)
-    ctx.set_overlap(True)
     stage_ms, stage_launches, _ = ctx.counters()
     r_evals, _ = ctx.work()
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
-    boxes_step = int(d_cnt.sum().item())
-    total_boxes = boxes_step * args.steps * world
-    value = total_boxes / (ms_max / 1000.0)
-    fps = F * args.steps * world / (ms_max / 1000.0)
 
     # ---- end-to-end through the public host API (pinned host frames, H2D/D2H inside)
     keep = []
@@ -485,7 +650,7 @@ def main():
         v = t.numpy().view(a.dtype).reshape(a.shape)
         v[...] = a
         return v
-    hL, hR = pin(L[idx]), pin(R[idx])
+    hL, hR = pin(L), pin(R)
     h_recs, h_offs = pin(recs), pin(offs)
     h_out = pin(np.zeros(F * eng.out_stride, OUT_DTYPE))
     h_cnt = pin(np.zeros(F, np.int32))
@@ -504,6 +669,7 @@ def main():
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_value = int(h_cnt.sum()) * e2e_steps * world / float(te.item())
+    e2e_parity = bool(h_out.tobytes() == d_out.cpu().numpy().tobytes()[:h_out.nbytes])
     h2d = int(hL.nbytes + hR.nbytes + h_recs.nbytes + h_offs.nbytes)
     d2h = int(h_out.nbytes + h_cnt.nbytes)
     # the e2e bound: this box's pinned host -> device copy bandwidth (one
@@ -532,11 +698,11 @@ def main():
     lat = []
     for i in range(args.latency_runs):
         a = time.perf_counter()
-        eng.range_host(hL[i % F:i % F + 1], hR[i % F:i % F + 1], h_recs[:n_boxes], h_offs[:2] - 0, h_out[:eng.out_stride],
+        eng.range_host(hL[i % F:i % F + 1], hR[i % F:i % F + 1], h_recs[:n_boxes], h_offs[:2], h_out[:eng.out_stride],
                        h_cnt[:1], chunk=1, stream=stream.cuda_stream)
         lat.append(time.perf_counter() - a)
     lat_dev = []
-    for i in range(max(50, args.latency_runs // 3)):
+    for i in range(args.latency_runs):
         a = time.perf_counter()
         eng.range_device(dL[i % F:i % F + 1], dR[i % F:i % F + 1], d_dets, d_offs[:2], d_out, d_cnt,
                          stream=stream.cuda_stream)
@@ -599,6 +765,7 @@ def main():
     # disparities, P1 8 / P2 32 (sgm.hpp defaults), rg_sgm_frames
     sgm = None
     try:
+        import ctypes as C
         nsg = min(F, 8)
         sp = rg.SgmParams(64, 0, 8, 32).to_c()
         sgm_out = torch.zeros(nsg * W * H, dtype=torch.int16, device=dev)
@@ -623,14 +790,24 @@ def main():
     stream_c5 = None
     if args.stream_frames > 0:
         try:
-            rec0 = eng.out_stride * OUT_DTYPE.itemsize
-            # ring frame 0 again (the latency runs reused the first output slot)
-            eng.range_device(dL[0:1], dR[0:1], d_dets, d_offs[:2], d_out, d_cnt, stream=stream.cuda_stream)
-            torch.cuda.synchronize()
-            stream_c5 = c5_stream(args, eng, ctx, dev, stream, rank, world, dets,
-                                  bytes(d_out[:rec0].cpu().numpy()) if rank == 0 else None)
+            stream_c5 = c5_stream(args, eng, ctx, dev, stream, rank, world, dets, recs, offs)
         except Exception as e:  # pragma: no cover
             stream_c5 = {"error": str(e)}
+        torch.cuda.empty_cache()
+
+    # ---- C3 and 9x7 C1 (BASELINE configs 2 and 0), rank 0 only
+    c3 = c1w = None
+    if rank == 0 and args.c3_frames > 0:
+        try:
+            c3 = config_c3(args, ctx, dev, stream)
+        except Exception as e:  # pragma: no cover
+            c3 = {"error": str(e)}
+        torch.cuda.empty_cache()
+    if rank == 0 and args.c1_frames > 0:
+        try:
+            c1w = config_c1_9x7(args, ctx, dev, stream)
+        except Exception as e:  # pragma: no cover
+            c1w = {"error": str(e)}
         torch.cuda.empty_cache()
 
     # ---- roofline of the dominant kernel (stage times from CUDA events on our stream)
@@ -665,27 +842,26 @@ def main():
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
         try:
-            cpu = cpu_reference_run(L[:min(args.distinct, cpu_threads() * 2)], R[:min(args.distinct, cpu_threads() * 2)],
-                                    dets, cfg, seconds=args.cpu_seconds, threads=cpu_threads())
+            k = min(F, ref_arm().cpu_threads() * 2)
+            cpu = cpu_reference_run(L[:k], R[:k], recs[:offs[k]], offs[:k + 1], seconds=args.cpu_seconds)
         except Exception as e:  # pragma: no cover
             cpu = {"error": str(e)}
 
+    mism = [p["frame_mismatches"] for p in (parity, (stream_c5 or {}).get("parity"), (c3 or {}).get("parity"),
+                                            (c1w or {}).get("parity")) if isinstance(p, dict)]
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "boxes/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u8/u32/f64", "data": "synthetic",
-            "frames_per_sec": fps, "boxes_per_frame": boxes_step / F,
+            "frames_per_sec": fps, "boxes_per_frame": boxes_step / (F * world),
             "p50_latency_ms": 1000 * statistics.median(lat), "p50_latency_device_ms": 1000 * statistics.median(lat_dev),
-            "config": {"workload": "C2: 1920x1080 rendered stereo pairs, 64 boxes (48 FAR + 16 CLOSE), "
-                                   "dx_max_far = dx_max_close = 256, tau_v 1.0, fwd-bwd + sub-pixel, range z",
-                       "frames_per_step_per_gpu": F, "distinct_frames": args.distinct, "frame_source": args.frame_source,
-                       "noise_sigma": 2.0,
-                       "l2": f"inputs {2 * F * W * H / 1e6:.0f} MB + census {F * CENSUS_BYTES_PER_FRAME / 1e6:.0f} MB "
-                             f"per step > 126 MB L2 (no flush needed)",
-                       "parallelism": f"frame-sharded dp{world}, NCCL all_gather of per-box results"},
+            "latency_runs": args.latency_runs,
+            "config": workload_config(F, world),
+            "feed": "device-resident HBM ring, every frame rendered on the GPU by rg_render_frames_device",
             "e2e": {"value": e2e_value, "unit": "boxes/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "api": "rg_range_frames_host (pinned host frames, chunked H2D/compute/D2H)",
+                    "records_equal_device_path": e2e_parity,
                     "bound": {"kind": "pcie_h2d", "achieved_gbs": e2e_h2d_gbs, "peak_gbs": pcie_gbs,
                               "frac": (e2e_h2d_gbs / pcie_gbs) if pcie_gbs else None,
                               "peak_source": "measured here: pinned 256 MiB host->device copies, best of 6 x 16"}},
@@ -696,12 +872,15 @@ def main():
                         "stage_ms_per_step": {k: v / roof_steps for k, v in
                                               zip(["census", "plan", "match", "aggregate"], stage_ms[:4])}},
             "hamming_evals_per_frame": evals / max(F * args.steps, 1),
+            "parity_mismatches": int(sum(mism)) if mism else None,
+            "parity": {"ring": parity},
             "autorect": rect,
             "sequence": seq,
             "sgm": sgm,
             "stream_c5": stream_c5,
+            "c3": c3,
+            "c1_9x7": c1w,
             "clocks": clk,
-            "parity_spot_check_vs_oracle": spot,
             "cpu_baseline": cpu,
         }
         print(json.dumps(line))

@@ -111,6 +111,18 @@ double ref_bench_estimate(const uint8_t* left, const uint8_t* right, int w, int 
                           const int32_t* det_offsets, const rg_ranger_config* cfg,
                           int threads, rg_object_disparity* out, int out_stride,
                           int32_t* out_count);
+/* ref_bench_estimate with z_cam (reference reproject) when focal_px,
+ * baseline_m > 0 -- the checker for the bench's parity sweep. */
+double ref_range_frames(const uint8_t* left, const uint8_t* right, int w, int h, int n_frames,
+                        const rg_detection* dets, const int32_t* det_offsets, const rg_ranger_config* cfg,
+                        int threads, double focal_px, double baseline_m, rg_object_disparity* out,
+                        int out_stride, int32_t* out_count);
+/* The reference's render_stereo_pair + ground_truth_detections for a batch of
+ * scenes on `threads` host threads (frame f at byte f*W*H; dets at
+ * dets[obj_offsets[f]..], n_dets[f] of them; dets may be NULL). */
+int ref_render_frames(const rg_scene_config* cfgs, const rg_scene_object* objs, const int32_t* obj_offsets,
+                      int n_frames, int threads, uint8_t* left, uint8_t* right, rg_detection* dets,
+                      int32_t* n_dets);
 int ref_bench_stages(const uint8_t* left, const uint8_t* right, int w, int h, const rg_detection* dets, int n_dets,
                      const rg_ranger_config* cfg, int workers, int reps, const rg_rect* roi, int delta_min,
                      int delta_max, const rg_bm_params* bm, int reps_rect, double* out_s);

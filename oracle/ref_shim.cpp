@@ -372,10 +372,16 @@ int ref_ground_truth_detections(const rg_scene_config* cfg, const rg_scene_objec
   });
 }
 
-double ref_bench_estimate(const uint8_t* left, const uint8_t* right, int w, int h, int n_frames,
-                          const rg_detection* dets, const int32_t* det_offsets,
-                          const rg_ranger_config* cfg, int threads, rg_object_disparity* out,
-                          int out_stride, int32_t* out_count) {
+/* Frame-parallel ranging by the reference (SURVEY 8(d) mode iii): `threads`
+ * host threads, each ranging whole frames with estimate_object_disparities
+ * at workers = 1.  Records as rg_object_disparity (z_cam through the
+ * reference's reproject when focal_px, baseline_m > 0, as
+ * ref_estimate_object_disparities).  Returns the wall seconds of the ranging
+ * (frame/detection marshalling excluded). */
+double ref_range_frames(const uint8_t* left, const uint8_t* right, int w, int h, int n_frames,
+                        const rg_detection* dets, const int32_t* det_offsets, const rg_ranger_config* cfg,
+                        int threads, double focal_px, double baseline_m, rg_object_disparity* out,
+                        int out_stride, int32_t* out_count) {
   const RangerConfig rc = to_cfg(cfg);
   std::vector<GrayImage> Ls, Rs;
   std::vector<std::vector<Detection>> D;
@@ -384,6 +390,9 @@ double ref_bench_estimate(const uint8_t* left, const uint8_t* right, int w, int 
     Rs.push_back(to_gray(right + std::size_t(f) * w * h, w, h));
     D.push_back(to_dets(dets + det_offsets[f], det_offsets[f + 1] - det_offsets[f]));
   }
+  const bool range_z = focal_px > 0 && baseline_m > 0;
+  const StereoCalibration cal =
+      range_z ? make_calibration(focal_px, baseline_m, w / 2.0, h / 2.0, 1.5) : StereoCalibration{};
   if (threads < 1) threads = 1;
   const auto t0 = std::chrono::steady_clock::now();
   std::vector<std::thread> pool;
@@ -400,6 +409,7 @@ double ref_bench_estimate(const uint8_t* left, const uint8_t* right, int w, int 
             o.n_blocks_used = res[i].n_blocks_used;
             o.valid = res[i].valid;
             o.disparity = res[i].disparity;
+            if (range_z && res[i].valid && res[i].disparity > 0) o.z_cam = reproject(0.0, 0.0, res[i].disparity, cal).z;
           }
           out_count[f] = int32_t(res.size());
         }
@@ -409,6 +419,58 @@ double ref_bench_estimate(const uint8_t* left, const uint8_t* right, int w, int 
   return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }
 
+double ref_bench_estimate(const uint8_t* left, const uint8_t* right, int w, int h, int n_frames,
+                          const rg_detection* dets, const int32_t* det_offsets,
+                          const rg_ranger_config* cfg, int threads, rg_object_disparity* out,
+                          int out_stride, int32_t* out_count) {
+  return ref_range_frames(left, right, w, h, n_frames, dets, det_offsets, cfg, threads, 0.0, 0.0, out, out_stride,
+                          out_count);
+}
+
+/* The reference's render_stereo_pair + ground_truth_detections over a batch of
+ * scenes on `threads` host threads (scene f = cfgs[f] with objects
+ * objs[obj_offsets[f] .. obj_offsets[f+1])); frame f at byte f*W*H of left /
+ * right, its detections at dets[obj_offsets[f] ..] (n_dets[f] of them). */
+int ref_render_frames(const rg_scene_config* cfgs, const rg_scene_object* objs, const int32_t* obj_offsets,
+                      int n_frames, int threads, uint8_t* left, uint8_t* right, rg_detection* dets,
+                      int32_t* n_dets) {
+  return guarded([&] {
+    if (threads < 1) threads = 1;
+    std::vector<std::thread> pool;
+    std::vector<int> st(std::size_t(threads), RG_OK);
+    for (int t = 0; t < threads; ++t)
+      pool.emplace_back([&, t] {
+        st[t] = guarded([&] {
+          for (int f = t; f < n_frames; f += threads) {
+            const std::size_t px = std::size_t(cfgs[f].width) * cfgs[f].height;
+            const int o0 = obj_offsets[f], no = obj_offsets[f + 1] - obj_offsets[f];
+            const SceneConfig sc = to_scene(&cfgs[f], objs + o0, no);
+            const RenderResult r = render_stereo_pair(sc);
+            std::memcpy(left + std::size_t(f) * px, r.left.data.data(), px);
+            std::memcpy(right + std::size_t(f) * px, r.right.data.data(), px);
+            if (dets) {
+              const auto d = ground_truth_detections(sc);
+              for (std::size_t i = 0; i < d.size(); ++i) {
+                rg_detection& o = dets[o0 + i];
+                o.cx = d[i].cx;
+                o.cy = d[i].cy;
+                o.w = d[i].w;
+                o.h = d[i].h;
+                o.class_id = d[i].class_id;
+                o.id = d[i].id;
+              }
+              n_dets[f] = int32_t(d.size());
+            }
+          }
+          return RG_OK;
+        });
+      });
+    for (auto& th : pool) th.join();
+    for (int v : st)
+      if (v != RG_OK) return v;
+    return RG_OK;
+  });
+}
 
 /* SURVEY 8(d) CPU baseline detail: median seconds of `reps` runs of one
  * frame through the reference at `workers`: [0] estimate_object_disparities

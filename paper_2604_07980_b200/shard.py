@@ -65,6 +65,85 @@ def gather_results(out: np.ndarray, counts: np.ndarray, n_frames: int, group=Non
     return full, cnt
 
 
+# ---------------------------------------------------------------- stream plumbing
+# The bench's C5 stream and its ring steps run exactly these functions (with
+# rg_range_frames as `range_chunk`); tests/test_dist_cpu.py runs them at world
+# size 2 over gloo with the C oracle as `range_chunk`.
+
+def stream_chunks(n_frames: int, rank: int, world: int, chunk: int) -> List[Tuple[int, int]]:
+    """This rank's shard of an n_frames stream cut into chunks of <= chunk
+    frames: [(global_lo, global_hi)], in frame order."""
+    if chunk < 1:
+        raise ValueError("chunk must be >= 1")
+    lo, hi = shard_bounds(n_frames, rank, world)
+    return [(c, min(hi, c + chunk)) for c in range(lo, hi, chunk)]
+
+
+def slab_frames(n_frames: int, world: int) -> int:
+    """Frames per rank slab of the padded gather (the largest shard)."""
+    return -(-n_frames // world)
+
+
+def alloc_slabs(n_frames: int, world: int, rec_bytes: int, device=None):
+    """Per-rank result slab (uint8, slab_frames * rec_bytes) and counts
+    (int32, slab_frames), plus the gathered buffers (world x the slab) --
+    the shard's frames occupy the head of the slab in frame order."""
+    import torch
+
+    per = slab_frames(n_frames, world)
+    out = torch.zeros(per * rec_bytes, dtype=torch.uint8, device=device)
+    cnt = torch.zeros(per, dtype=torch.int32, device=device)
+    g_out = torch.zeros(world * out.numel(), dtype=torch.uint8, device=device) if world > 1 else out
+    g_cnt = torch.zeros(world * per, dtype=torch.int32, device=device) if world > 1 else cnt
+    return out, cnt, g_out, g_cnt
+
+
+def run_stream(range_chunk, n_frames: int, rank: int, world: int, chunk: int, out, cnt, rec_bytes: int) -> int:
+    """Range this rank's shard chunk by chunk: range_chunk(glo, ghi, out_view,
+    cnt_view) writes frames [glo, ghi)'s records and counts into the views of
+    the slab.  No collective.  Returns the frames ranged."""
+    lo, _ = shard_bounds(n_frames, rank, world)
+    done = 0
+    for glo, ghi in stream_chunks(n_frames, rank, world, chunk):
+        a, b = glo - lo, ghi - lo
+        range_chunk(glo, ghi, out[a * rec_bytes:b * rec_bytes], cnt[a:b])
+        done += ghi - glo
+    return done
+
+
+def gather_slabs(out, cnt, g_out, g_cnt, world: int, group=None) -> None:
+    """The only exchange: every rank's slab of records and counts to every
+    rank (one all_gather each; NCCL over NVLink on GPUs, gloo on CPU)."""
+    if world > 1:
+        import torch.distributed as dist
+        dist.all_gather_into_tensor(g_out, out, group=group)
+        dist.all_gather_into_tensor(g_cnt, cnt, group=group)
+
+
+def frame_order(g_out, g_cnt, n_frames: int, world: int, rec_bytes: int):
+    """Gathered slabs -> (records uint8 (n_frames, rec_bytes), counts int32
+    (n_frames)) in global frame order (the reference's sequential order,
+    pipeline.hpp:338-344)."""
+    per = slab_frames(n_frames, world)
+    ob = g_out.cpu().numpy().reshape(world, per, rec_bytes)
+    cb = g_cnt.cpu().numpy().reshape(world, per)
+    recs = np.zeros((n_frames, rec_bytes), np.uint8)
+    cnt = np.zeros(n_frames, np.int32)
+    for r in range(world):
+        a, b = shard_bounds(n_frames, r, world)
+        recs[a:b] = ob[r, :b - a]
+        cnt[a:b] = cb[r, :b - a]
+    return recs, cnt
+
+
+def gathered_boxes(g_cnt, n_frames: int, world: int) -> int:
+    """Boxes ranged over the whole stream (padding rows of short shards excluded)."""
+    per = slab_frames(n_frames, world)
+    cb = g_cnt.cpu().numpy().reshape(world, per)
+    return int(sum(int(cb[r, :shard_bounds(n_frames, r, world)[1] - shard_bounds(n_frames, r, world)[0]].sum())
+                   for r in range(world)))
+
+
 def rect_shift_schedule(delta_stars: Sequence[int], window: int = 5, rate: float = 1.0) -> List[int]:
     """Two-pass rect schedule: from the per-frame search
     results delta*_t (pass A, computed sharded on the uncorrected pairs,
