@@ -123,6 +123,10 @@ double ref_range_frames(const uint8_t* left, const uint8_t* right, int w, int h,
 int ref_render_frames(const rg_scene_config* cfgs, const rg_scene_object* objs, const int32_t* obj_offsets,
                       int n_frames, int threads, uint8_t* left, uint8_t* right, rg_detection* dets,
                       int32_t* n_dets);
+/* auto_rect_search at `workers` + per-delta counts over `workers` threads */
+int ref_auto_rect_search_mt(const uint8_t* left, const uint8_t* right, int w, int h, const rg_rect* roi,
+                            int delta_min, int delta_max, const rg_bm_params* p, int workers,
+                            int32_t* best_delta, int64_t* counts);
 int ref_bench_stages(const uint8_t* left, const uint8_t* right, int w, int h, const rg_detection* dets, int n_dets,
                      const rg_ranger_config* cfg, int workers, int reps, const rg_rect* roi, int delta_min,
                      int delta_max, const rg_bm_params* bm, int reps_rect, double* out_s);

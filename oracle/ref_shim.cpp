@@ -345,6 +345,43 @@ int ref_auto_rect_search(const uint8_t* left, const uint8_t* right, int w, int h
   });
 }
 
+/* auto_rect_search at `workers` (autorect.hpp:22-58: bm_disparity's rows in
+ * `workers` threads per delta) plus the per-delta counts as the search body
+ * computes them, the deltas spread over `workers` threads (each
+ * bm_disparity at workers = 1; results are worker-count invariant,
+ * test_bm.cpp / image.hpp:158-178). */
+int ref_auto_rect_search_mt(const uint8_t* left, const uint8_t* right, int w, int h, const rg_rect* roi,
+                            int delta_min, int delta_max, const rg_bm_params* p, int workers,
+                            int32_t* best_delta, int64_t* counts) {
+  return guarded([&] {
+    const GrayImage L = to_gray(left, w, h), R = to_gray(right, w, h);
+    const BmParams bm = to_bm(p);
+    const ImageRoi r{roi->x0, roi->y0, roi->x1, roi->y1};
+    if (workers < 1) workers = 1;
+    *best_delta = auto_rect_search(L, R, r, delta_min, delta_max, bm, workers);
+    if (counts) {
+      const GrayImage rcrop = crop(R, r.x0, r.y0, r.width(), r.height());
+      const int n = delta_max - delta_min + 1;
+      std::vector<std::thread> pool;
+      for (int t = 0; t < workers; ++t)
+        pool.emplace_back([&, t] {
+          for (int k = t; k < n; k += workers) {
+            const int d = delta_min + k;
+            const GrayImage lcrop = crop(shift_vertical(L, d), r.x0, r.y0, r.width(), r.height());
+            const DisparityMap dm = bm_disparity(lcrop, rcrop, bm, 1);
+            int64_t c = 0;
+            const int lo = bm.min_disparity * DisparityMap::kSubLevels;
+            for (std::int16_t v : dm.raw)
+              if (v != DisparityMap::kInvalid && v > lo) ++c;
+            counts[k] = c;
+          }
+        });
+      for (auto& th : pool) th.join();
+    }
+    return RG_OK;
+  });
+}
+
 int ref_render_stereo_pair(const rg_scene_config* cfg, const rg_scene_object* objs, int n_obj,
                            uint8_t* left, uint8_t* right) {
   return guarded([&] {

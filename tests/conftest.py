@@ -26,3 +26,11 @@ def ctx():
 def orc():
     import oracle_lib
     return oracle_lib.oracle()
+
+
+@pytest.fixture(scope="session")
+def chk():
+    """GPU parity checker: the reference itself (oracle/_ref) when present,
+    the C restatement otherwise and for the 9x7 extension."""
+    import oracle_lib
+    return oracle_lib.checker()

@@ -172,3 +172,44 @@ def reference() -> Checker:
 
 def have_reference() -> bool:
     return os.path.exists(REF_SO)
+
+
+class RefFirst:
+    """The GPU parity tests' checker: the reference itself (oracle/_ref) for
+    everything it implements, the C restatement for the 9x7 / uint64
+    extension (the reference has no 9x7 window) and restatement-only entry
+    points."""
+    kind = "reference"
+
+    def __init__(self):
+        self.ref, self.orc = reference(), oracle()
+
+    def __getattr__(self, name):
+        return getattr(self.ref, name)
+
+    def estimate(self, left, right, dets, cfg, *a, **k):
+        return (self.orc if cfg.census_9x7 else self.ref).estimate(left, right, dets, cfg, *a, **k)
+
+    def match(self, L, R, blocks, mode=1, tau_v=1.0):
+        wide = np.asarray(L).dtype == np.uint64
+        return (self.orc if wide else self.ref).match(L, R, blocks, mode, tau_v)
+
+    def census64(self, *a, **k):
+        return self.orc.census64(*a, **k)
+
+    def autorect_mt(self, left, right, roi, dmin, dmax, p: _abi.BmParams, workers: int):
+        """auto_rect_search + per-delta counts at `workers` host threads."""
+        h, w = left.shape
+        r = _abi.Rect(*roi)
+        best = C.c_int32()
+        counts = np.zeros(dmax - dmin + 1, np.int64)
+        fn = self.ref.lib.ref_auto_rect_search_mt
+        fn.restype, fn.argtypes = I, [P, P, I, I, P, I, I, P, I, P, P]
+        st = fn(left.ctypes.data, right.ctypes.data, w, h, C.byref(r), dmin, dmax, C.byref(p), workers,
+                C.byref(best), counts.ctypes.data)
+        return st, best.value, counts
+
+
+def checker():
+    """oracle/_ref where it was built (the reference compiled in place), else the restatement."""
+    return RefFirst() if have_reference() else oracle()

@@ -27,14 +27,14 @@ def _frames(fn, n, **kw):
     return np.stack(Ls), np.stack(Rs), D, cfg, sc
 
 
-def _want(orc, L, R, dets, cfg):
-    out, _ = orc.estimate(L, R, [_abi.Detection(d.cx, d.cy, d.w, d.h, d.class_id, d.id) for d in dets],
+def _want(chk, L, R, dets, cfg):
+    out, _ = chk.estimate(L, R, [_abi.Detection(d.cx, d.cy, d.w, d.h, d.class_id, d.id) for d in dets],
                           cfg.to_c(), S.F_PX, S.BASELINE_M)
     return b"".join(bytes(o) for o in out)
 
 
 @pytest.mark.parametrize("name", ["c1", "c2", "c3"])
-def test_range_frames_device_and_host(ctx, orc, name):
+def test_range_frames_device_and_host(ctx, chk, name):
     import torch
 
     fn = {"c1": S.scene_c1, "c2": S.scene_c2, "c3": S.scene_c3}[name]
@@ -58,7 +58,7 @@ def test_range_frames_device_and_host(ctx, orc, name):
     eng.range_host(L, R, recs, offs, h_out, h_cnt, chunk=2)
     ho = h_out.view(np.uint8).reshape(n, eng.out_stride * 32)
     for f in range(n):
-        want = _want(orc, L[f], R[f], D[f], cfg)
+        want = _want(chk, L[f], R[f], D[f], cfg)
         assert int(c[f]) * 32 == len(want) and int(h_cnt[f]) == c[f]
         assert o[f, :len(want)].tobytes() == want
         assert ho[f, :len(want)].tobytes() == want
@@ -71,7 +71,7 @@ def shift_vertical(img, dy):
 
 
 @pytest.mark.parametrize("name,wide", [("c1", False), ("c2", False), ("c1", True)])
-def test_range_frames_left_shift(ctx, orc, name, wide):
+def test_range_frames_left_shift(ctx, chk, name, wide):
     """Per-frame rect correction (pipeline.hpp:135-138) folded into the census
     row addressing == ranging shift_vertical(left, s) with the oracle."""
     import torch
@@ -97,7 +97,7 @@ def test_range_frames_left_shift(ctx, orc, name, wide):
     eng.range_host(L, R, recs, offs, h_out, h_cnt, chunk=2, left_shift=shifts)
     ho = h_out.view(np.uint8).reshape(n, eng.out_stride * 32)
     for f in range(n):
-        want = _want(orc, np.ascontiguousarray(shift_vertical(L[f], int(shifts[f]))), R[f], D[f], cfg)
+        want = _want(chk, np.ascontiguousarray(shift_vertical(L[f], int(shifts[f]))), R[f], D[f], cfg)
         assert int(cnt[f]) * 32 == len(want) == int(h_cnt[f]) * 32
         assert o[f, :len(want)].tobytes() == want
         assert ho[f, :len(want)].tobytes() == want
@@ -155,7 +155,7 @@ def test_integration_example_program():
     assert any("delta* 2" in l for l in lines) and "shift 0" in lines[0]
 
 
-def _batch_vs_oracle(ctx, orc, L, R, D, cfg, focal=0.0, base=0.0):
+def _batch_vs_oracle(ctx, chk, L, R, D, cfg, focal=0.0, base=0.0):
     import torch
 
     n, h, w = L.shape
@@ -172,7 +172,7 @@ def _batch_vs_oracle(ctx, orc, L, R, D, cfg, focal=0.0, base=0.0):
     for f in range(n):
         got_n = int(cnt[f])
         if D[f]:
-            want, _ = orc.estimate(np.ascontiguousarray(L[f]), np.ascontiguousarray(R[f]),
+            want, _ = chk.estimate(np.ascontiguousarray(L[f]), np.ascontiguousarray(R[f]),
                                    [_abi.Detection(d.cx, d.cy, d.w, d.h, d.class_id, d.id) for d in D[f]],
                                    cfg.to_c(), focal, base)
             want = b"".join(bytes(x) for x in want)
@@ -184,7 +184,7 @@ def _batch_vs_oracle(ctx, orc, L, R, D, cfg, focal=0.0, base=0.0):
 
 @pytest.mark.parametrize("case", ["odd_width", "empty_frames", "degenerate_boxes", "selection_overflow",
                                   "zero_range", "wide_range", "close_only_scale3"])
-def test_range_frames_edge_cases(ctx, orc, case):
+def test_range_frames_edge_cases(ctx, chk, case):
     """Batched path vs the oracle on the shapes the planner/census/matcher
     special-case: non-multiple-of-4 widths (general census kernel), frames
     without detections, boxes leaving or degenerate in the image, more boxes
@@ -221,11 +221,11 @@ def test_range_frames_edge_cases(ctx, orc, case):
         frames = [(L, R, dets)]
     Ls = np.stack([f[0] for f in frames])
     Rs = np.stack([f[1] for f in frames])
-    _batch_vs_oracle(ctx, orc, Ls, Rs, [f[2] for f in frames], cfg, S.F_PX, S.BASELINE_M)
+    _batch_vs_oracle(ctx, chk, Ls, Rs, [f[2] for f in frames], cfg, S.F_PX, S.BASELINE_M)
 
 
 @pytest.mark.parametrize("overlap", [True, False])
-def test_range_frames_chunked_overlap_schedule(ctx, orc, overlap):
+def test_range_frames_chunked_overlap_schedule(ctx, chk, overlap):
     """>= 32 frames take the chunked census/matcher overlap schedule (chunk
     rasters double-buffered across two streams); it must equal the oracle and
     the single-stream schedule frame by frame."""
@@ -239,7 +239,7 @@ def test_range_frames_chunked_overlap_schedule(ctx, orc, overlap):
     D = [list(rng.permutation(dets0))[: 1 + (i % len(dets0))] for i in range(n)]
     ctx.set_overlap(overlap)
     try:
-        _batch_vs_oracle(ctx, orc, L, R, D, cfg, S.F_PX, S.BASELINE_M)
+        _batch_vs_oracle(ctx, chk, L, R, D, cfg, S.F_PX, S.BASELINE_M)
     finally:
         ctx.set_overlap(False)
 
@@ -292,7 +292,7 @@ def _random_cfgs(n, seed=11):
 
 
 @pytest.mark.parametrize("k", range(8))
-def test_random_configs_both_matchers_match_oracle(ctx, orc, k):
+def test_random_configs_both_matchers_match_oracle(ctx, chk, k):
     """Randomised RangerConfigs (ranges that are / are not multiples of 32,
     tails, tiny grids, close scales 1-3, selection budgets) on C1 frames:
     the latency (cooperative) matcher on a 1-frame batch and the throughput
@@ -319,6 +319,6 @@ def test_random_configs_both_matchers_match_oracle(ctx, orc, k):
     big = run(0, 5)
     small = [run(f, f + 1)[0] for f in range(5)]
     for f in range(5):
-        want = _want(orc, L[f], R[f], D[f], cfg)
+        want = _want(chk, L[f], R[f], D[f], cfg)
         assert big[f] == want, (f, cfg)
         assert small[f] == want, (f, cfg)

@@ -164,3 +164,22 @@ def test_oracle_sgm_pass_equals_reference_fresh(orc):
             assert orc.lib.orc_sgm_direction_pass(cost.ctypes.data, w, h, nd, p1, p2, sx, sy, a1.ctypes.data) == 0
             assert ref.lib.ref_sgm_direction_pass(cost.ctypes.data, w, h, nd, p1, p2, sx, sy, a2.ctypes.data) == 0
             assert np.array_equal(a1, a2), (w, h, nd, sx, sy)
+
+
+@pytest.mark.skipif(not oracle_lib.have_reference(), reason="oracle/_ref not built (no /root/reference)")
+def test_reference_autorect_mt_equals_single_worker(orc):
+    """The multi-threaded reference checker of the full-ROI C4 GPU test equals
+    the reference at workers = 1 and the restatement (autorect.hpp:22-58)."""
+    from paper_2604_07980_b200 import synth as S
+    from paper_2604_07980_b200.ranger import BmParams
+    sc = S.SceneConfig(objects=[S.SceneObject(id=1, position=(30.0, 0.0, 1.5), texture_seed=11)],
+                       vertical_offset_px=2)
+    L, R = S.render_stereo_pair(sc)
+    p = BmParams(24, 9, 0, 10, 10, 1).to_c()
+    roi = (240, 160, 400, 240)
+    ref = oracle_lib.checker()
+    a = ref.autorect_mt(L, R, roi, -3, 3, p, 4)
+    b = ref.ref.autorect(L, R, roi, -3, 3, p)
+    c = orc.autorect(L, R, roi, -3, 3, p)
+    assert a[0] == b[0] == c[0] == 0 and a[1] == b[1] == c[1] == 2
+    assert list(a[2]) == list(b[2]) == list(c[2])
