@@ -316,6 +316,188 @@ __device__ __forceinline__ void sweep_range(
   }
 }
 
+// ---------------------------------------------------------------------------
+// Vectorised sweep (throughput matcher: 32-bit codes in the padded internal
+// layout).  Lanes own dx PAIRS: lane l of chunk c holds dx e and e + 1, e =
+// E + 64 c + 2 l, and reads both samples with ONE 8-byte load at column
+// x - e - 1 -- aligned iff x - E - 1 is even (raster rows start 128-B
+// aligned).  So a pass's points split by the parity of x - D (D = dx_min):
+// class A sweeps with E = D, class B with E = D - 1, and B's pair sums are
+// realigned into A's layout by one lane shuffle per chunk.  Against one
+// 4-byte load per evaluation this halves the load instructions and the L1
+// wavefronts (a misaligned 128-B warp load touches two lines).
+// FAST blocks (every sample defined) add groups of three points through a
+// carry-save adder: popc(a) + popc(b) + popc(c) = popc(a ^ b ^ c) +
+// 2 popc(maj(a, b, c)) -- 2 POPC per 3 evaluations; POPC issues at a quarter
+// of the LOP3 rate (tools/hamming_probe.cu: 15.4 -> 21.5 evaluations/clk/SM).
+// Per chunk group, the candidate at its last A position (lane 31, last
+// chunk, dx e + 1), whose B part sits in the next group, and the final tail
+// beyond the last full chunk are evaluated point-parallel (v2_fixup).
+template <int NC, int MODE>
+__device__ __forceinline__ void v2_class(const VPoint<uint32_t>* __restrict__ vp, int nv, const char* rb,
+                                         int (&s)[NC][2], int (&n)[NC][2]) {
+  int k = 0;
+  if (MODE == M_FAST) {
+    for (; k + 3 <= nv; k += 3) {
+      const VPoint<uint32_t> a = vp[k], b = vp[k + 1], c = vp[k + 2];
+      const uint2* pa = reinterpret_cast<const uint2*>(rb + a.off);
+      const uint2* pb = reinterpret_cast<const uint2*>(rb + b.off);
+      const uint2* pc = reinterpret_cast<const uint2*>(rb + c.off);
+#pragma unroll
+      for (int ch = 0; ch < NC; ++ch) {
+        const uint2 va = __ldg(pa - 32 * ch), vb = __ldg(pb - 32 * ch), vc = __ldg(pc - 32 * ch);
+        // element 0 (dx e) is the upper word, element 1 (dx e + 1) the lower
+        const uint32_t x0 = a.code ^ va.y, y0 = b.code ^ vb.y, z0 = c.code ^ vc.y;
+        const uint32_t x1 = a.code ^ va.x, y1 = b.code ^ vb.x, z1 = c.code ^ vc.x;
+        const int t0 = __popc((x0 & y0) | (z0 & (x0 | y0))), t1 = __popc((x1 & y1) | (z1 & (x1 | y1)));
+        s[ch][0] += __popc(x0 ^ y0 ^ z0) + 2 * t0;
+        s[ch][1] += __popc(x1 ^ y1 ^ z1) + 2 * t1;
+      }
+    }
+  }
+  for (; k < nv; ++k) {
+    const VPoint<uint32_t> a = vp[k];
+    const uint2* pa = reinterpret_cast<const uint2*>(rb + a.off);
+#pragma unroll
+    for (int ch = 0; ch < NC; ++ch) {
+      const uint2 v = __ldg(pa - 32 * ch);
+      if (MODE == M_FAST) {
+        s[ch][0] += __popc(a.code ^ v.y);
+        s[ch][1] += __popc(a.code ^ v.x);
+      } else {  // M_SIGN: an undefined sample (code 0 in the padded layout) drops out
+        const uint32_t m0 = defined_mask(v.y), m1 = defined_mask(v.x);
+        s[ch][0] += __popc((a.code ^ v.y) & m0);
+        s[ch][1] += __popc((a.code ^ v.x) & m1);
+        n[ch][0] -= (int)m0;
+        n[ch][1] -= (int)m1;
+      }
+    }
+  }
+}
+
+// One chunk group [c0, c0 + NC) for one dy: both classes, B realigned into A,
+// then this lane's argmin over its candidates below dx_lim (the rest are fixups).
+template <int NC, int MODE>
+__device__ __forceinline__ void v2_group(const VPoint<uint32_t>* vpa, int na, const VPoint<uint32_t>* vpb, int nb,
+                                         const char* rdy, int D, int c0, int dx_lim, int dy, int lane, int nv,
+                                         Cand& best, unsigned long long& bkey, int& evals) {
+  int as[NC][2], bs[NC][2], an[NC][2], bn[NC][2];
+#pragma unroll
+  for (int c = 0; c < NC; ++c)
+#pragma unroll
+    for (int k = 0; k < 2; ++k) as[c][k] = bs[c][k] = an[c][k] = bn[c][k] = 0;
+  // lane base: element column x - e - 1 with e = E + 64 c0 + 2 lane (x enters via VPoint::off)
+  const int EA = D + 64 * c0, EB = EA - 1;
+  v2_class<NC, MODE>(vpa, na, rdy - 4 * (EA + 1 + 2 * lane), as, an);
+  v2_class<NC, MODE>(vpb, nb, rdy - 4 * (EB + 1 + 2 * lane), bs, bn);
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    // B element 1 (dx EB + 2l + 1 = EA + 2l) -> A element 0 of the same lane;
+    // B element 0 of lane l + 1 (dx EA + 2l + 1) -> A element 1 of lane l; lane
+    // 31 takes lane 0 of the next chunk (in the last chunk it is a fixup)
+    const int nxt = __shfl_sync(0xffffffffu, bs[c][0], (lane + 1) & 31);
+    int s0 = as[c][0] + bs[c][1], s1 = as[c][1] + (lane < 31 ? nxt : 0);
+    int n0 = 0, n1 = 0;
+    if (MODE == M_SIGN) {
+      const int nnx = __shfl_sync(0xffffffffu, bn[c][0], (lane + 1) & 31);
+      n0 = an[c][0] + bn[c][1];
+      n1 = an[c][1] + (lane < 31 ? nnx : 0);
+    }
+    if (c + 1 < NC) {
+      const int w = __shfl_sync(0xffffffffu, bs[c + 1][0], 0);
+      if (lane == 31) s1 += w;
+      if (MODE == M_SIGN) {
+        const int wn = __shfl_sync(0xffffffffu, bn[c + 1][0], 0);
+        if (lane == 31) n1 += wn;
+      }
+    }
+    const int dx0 = EA + 64 * c + 2 * lane;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int dx = dx0 + k;
+      if (dx >= dx_lim) continue;
+      const int sum = k ? s1 : s0;
+      if (MODE == M_FAST) {
+        evals += nv;
+        const unsigned long long key = fast_key(sum, dx, dy);
+        bkey = key < bkey ? key : bkey;
+      } else {
+        const int nn = k ? n1 : n0;
+        if (nn > 0) {
+          evals += nn;
+          const Cand cd = {sum, nn, dx, dy};
+          if (better(cd, best)) best = cd;
+        }
+      }
+    }
+  }
+}
+
+// Fixup candidates dx in [t0, t1] (group ends and the final tail), every point
+// of both classes, lanes over points.
+template <int MODE>
+__device__ __forceinline__ void v2_fixup(const VPoint<uint32_t>* vpa, int na, const VPoint<uint32_t>* vpb, int nb,
+                                         const char* rdy, int t0, int t1, int dy, int lane, Cand& best,
+                                         unsigned long long& bkey, int& evals) {
+  for (int t = t0; t <= t1; ++t) {
+    const char* rd = rdy - 4 * t;
+    int sum = 0, n = 0;
+    for (int k = lane; k < na + nb; k += 32) {
+      const VPoint<uint32_t> q = k < na ? vpa[k] : vpb[k - na];
+      const uint32_t r = __ldg(reinterpret_cast<const uint32_t*>(rd + q.off));
+      if (MODE == M_FAST) {
+        sum += __popc(q.code ^ r);
+      } else {
+        const uint32_t m = defined_mask(r);
+        sum += __popc((q.code ^ r) & m);
+        n -= (int)m;
+      }
+    }
+    sum = __reduce_add_sync(0xffffffffu, sum);
+    n = MODE == M_FAST ? na + nb : __reduce_add_sync(0xffffffffu, n);
+    if (lane == 0 && n > 0) {
+      evals += n;
+      if (MODE == M_FAST) {
+        const unsigned long long key = fast_key(sum, t, dy);
+        bkey = key < bkey ? key : bkey;
+      } else {
+        const Cand cd = {sum, n, t, dy};
+        if (better(cd, best)) best = cd;
+      }
+    }
+  }
+}
+
+// The whole search range of one pass: chunk groups of <= 4 (balanced) per dy,
+// each followed by its end fixup; the final tail after the last group.
+template <int MODE>
+__device__ __forceinline__ void v2_range(const VPoint<uint32_t>* vpa, int na, const VPoint<uint32_t>* vpb, int nb,
+                                         const uint32_t* R, const PadGeom& g, const rg_search_range& rg, int lane,
+                                         Cand& best, unsigned long long& bkey, int& evals) {
+  const int D = rg.dx_min, ndx = rg.dx_max - rg.dx_min + 1;
+  const int nfull = ndx >> 6, rem = ndx & 63;
+  const int nch = (nfull >= 1 && rem <= 3) ? nfull : nfull + 1;
+  const int groups = (nch + 3) / 4;
+  const int gq = nch / groups, gr = nch - gq * groups;
+  const int nv = na + nb;
+  for (int dy = rg.dy_min; dy <= rg.dy_max; ++dy) {
+    const char* rdy = reinterpret_cast<const char*>(R + (int64_t)dy * g.pitch);
+    for (int gi = 0, c0 = 0; gi < groups; ++gi) {
+      const int k = gq + (gi < gr ? 1 : 0);
+      const int end = D + 64 * (c0 + k) - 1;  // this group's last A position: a fixup
+      const int lim = min(end, rg.dx_max + 1);
+      if (k <= 2)  // 1 or 2 chunks: the 2-chunk body (a 1-chunk group's second chunk lies past lim)
+        v2_group<2, MODE>(vpa, na, vpb, nb, rdy, D, c0, lim, dy, lane, nv, best, bkey, evals);
+      else
+        v2_group<4, MODE>(vpa, na, vpb, nb, rdy, D, c0, lim, dy, lane, nv, best, bkey, evals);
+      c0 += k;
+      // the group end (and, after the last group, the tail up to dx_max)
+      const int t1 = gi + 1 < groups ? end : rg.dx_max;
+      if (end <= rg.dx_max) v2_fixup<MODE>(vpa, na, vpb, nb, rdy, end, t1, dy, lane, best, bkey, evals);
+    }
+  }
+}
+
 // One block_match pass (census.hpp:178-272) by the calling warp.
 // pts: the block's points (smem), shifted by (sx, sy); L: raster of the left
 // codes, R: raster sampled at (x - dx, y + dy).  Both share geometry g.
@@ -445,18 +627,127 @@ __device__ Pass warp_pass(
   return o;
 }
 
+// One block_match pass with the vectorised sweep (32-bit codes, trusted
+// padded rasters, one warp per block): the left-code filter writes class A
+// points from the front of vp and class B points from the back (cap entries).
+__device__ Pass warp_pass_v2(const int2* pts, int np, int sx, int sy, const uint32_t* L, const uint32_t* R,
+                             const PadGeom& g, const rg_search_range& rg, VPoint<uint32_t>* vp, int cap, int lane,
+                             int& evals) {
+  Pass o = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  const int D = rg.dx_min;
+  int na = 0, nb = 0;
+  int xmin = INT_MAX, xmax = INT_MIN, ymin = INT_MAX, ymax = INT_MIN;
+  const unsigned below = (1u << lane) - 1u;
+  for (int b = 0; b < np; b += 32) {  // keep points with a defined left code (census.hpp:195-201)
+    const int k = b + lane;
+    int x = 0, y = 0;
+    uint32_t code = 0;
+    if (k < np) {
+      const int2 p = pts[k];
+      x = p.x + sx;
+      y = p.y + sy;
+      if (x >= 0 && x < g.w && y >= 0 && y < g.h) code = L[(int64_t)y * g.pitch + x];
+    }
+    const bool ok = code != 0u;
+    const bool ca = ok && ((x - D) & 1);
+    const unsigned ba = __ballot_sync(0xffffffffu, ca), bbm = __ballot_sync(0xffffffffu, ok && !ca);
+    if (ok) {
+      VPoint<uint32_t> q;
+      q.off = (uint32_t)(y * g.pitch + x) * 4u;
+      q.code = code;
+      if (ca)
+        vp[na + __popc(ba & below)] = q;
+      else
+        vp[cap - 1 - nb - __popc(bbm & below)] = q;
+      xmin = min(xmin, x);
+      xmax = max(xmax, x);
+      ymin = min(ymin, y);
+      ymax = max(ymax, y);
+    }
+    na += __popc(ba);
+    nb += __popc(bbm);
+  }
+  __syncwarp();
+  const int nv = na + nb;
+  if (nv == 0) return o;  // no contributing point anywhere: nullopt
+  xmin = __reduce_min_sync(0xffffffffu, xmin);
+  ymin = __reduce_min_sync(0xffffffffu, ymin);
+  xmax = __reduce_max_sync(0xffffffffu, xmax);
+  ymax = __reduce_max_sync(0xffffffffu, ymax);
+  const VPoint<uint32_t>* vpa = vp;
+  const VPoint<uint32_t>* vpb = vp + cap - nb;
+  const int ndx = rg.dx_max - rg.dx_min + 1;
+  const bool fast = xmin - rg.dx_max >= g.sx0 && xmax - rg.dx_min <= g.sx1 && ymin + rg.dy_min >= g.sy0 &&
+                    ymax + rg.dy_max <= g.sy1 && rg.dx_min > -32768 && rg.dx_max < 32768 &&
+                    rg.dy_min >= -32768 && rg.dy_max < 32768;
+  Cand best = {0, 0, 0, 0};
+  if (fast) {
+    unsigned long long bkey = ~0ull;
+    v2_range<M_FAST>(vpa, na, vpb, nb, R, g, rg, lane, best, bkey, evals);
+    const uint32_t hi = __reduce_min_sync(0xffffffffu, (uint32_t)(bkey >> 32));
+    const uint32_t lo = __reduce_min_sync(0xffffffffu, (uint32_t)(bkey >> 32) == hi ? (uint32_t)bkey : ~0u);
+    const int adx = (int)(lo >> 17);
+    best.sum = (int)hi;
+    best.n = nv;
+    best.dx = (lo & 1u) ? adx : -adx;
+    best.dy = (int)((lo >> 1) & 0xFFFFu) - 0x8000;
+  } else {
+    unsigned long long unused = 0;
+    v2_range<M_SIGN>(vpa, na, vpb, nb, R, g, rg, lane, best, unused, evals);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {  // warp argmin (a total order)
+      Cand u;
+      u.sum = __shfl_xor_sync(0xffffffffu, best.sum, off);
+      u.n = __shfl_xor_sync(0xffffffffu, best.n, off);
+      u.dx = __shfl_xor_sync(0xffffffffu, best.dx, off);
+      u.dy = __shfl_xor_sync(0xffffffffu, best.dy, off);
+      if (better(u, best)) best = u;
+    }
+  }
+  if (best.n == 0) return o;
+  const int bix = best.dx - rg.dx_min;
+  o.has = 1;
+  o.dx = best.dx;
+  o.dy = best.dy;
+  o.sum = best.sum;
+  o.n = best.n;
+  o.interior = bix > 0 && bix + 1 < ndx;
+  if (o.interior) {  // costs at (dx - 1, dy) and (dx + 1, dy) for the parabola
+    int ms = 0, mn = 0, ps = 0, pn = 0;
+    const char* rb = reinterpret_cast<const char*>(R + (int64_t)best.dy * g.pitch - best.dx);
+    for (int k = lane; k < nv; k += 32) {
+      const VPoint<uint32_t> q = k < na ? vpa[k] : vpb[k - na];
+      const uint32_t* a = reinterpret_cast<const uint32_t*>(rb + q.off);
+      const uint32_t rm = a[1], rp = a[-1];
+      if (rm) {
+        ms += __popc(q.code ^ rm);
+        ++mn;
+      }
+      if (rp) {
+        ps += __popc(q.code ^ rp);
+        ++pn;
+      }
+    }
+    o.cm_sum = __reduce_add_sync(0xffffffffu, ms);
+    o.cm_n = __reduce_add_sync(0xffffffffu, mn);
+    o.cp_sum = __reduce_add_sync(0xffffffffu, ps);
+    o.cp_n = __reduce_add_sync(0xffffffffu, pn);
+  }
+  return o;
+}
+
 __device__ __forceinline__ void finish(const Pass& p, rg_match_result& r) {  // census.hpp:255-270
   r.has_value = 1;
   r.dx_int = p.dx;
   r.dy_int = p.dy;
-  r.cost = __ddiv_rn((double)p.sum, (double)p.n);
+  r.cost = div_n((double)p.sum, p.n);
   r.valid_points = p.n;
   r.dx_subpix = (double)p.dx;
   r.cost_minus = -1.0;
   r.cost_plus = -1.0;
   if (p.interior && p.cm_n > 0 && p.cp_n > 0) {
-    const double cm = __ddiv_rn((double)p.cm_sum, (double)p.cm_n);
-    const double cp = __ddiv_rn((double)p.cp_sum, (double)p.cp_n);
+    const double cm = div_n((double)p.cm_sum, p.cm_n);
+    const double cp = div_n((double)p.cp_sum, p.cp_n);
     r.cost_minus = cm;
     r.cost_plus = cp;
     r.dx_subpix = __dadd_rn((double)p.dx, subpixel(cm, r.cost, cp));
@@ -466,7 +757,7 @@ __device__ __forceinline__ void finish(const Pass& p, rg_match_result& r) {  // 
 // COOP (latency mode): a CTA per FAR block, its warps splitting the dx
 // chunks of both passes (the FAR block is the critical path of a small
 // batch: ~5x a CLOSE sub-block); CLOSE sub-blocks stay one per warp.
-template <typename CT, int WPB, int MINB, int PF = 0, bool COOP = false>
+template <typename CT, int WPB, int MINB, int PF = 0, bool COOP = false, bool V2 = false>
 __global__ void __launch_bounds__(WPB * 32, MINB) match_slots_warp_kernel(
     const Slot* __restrict__ slots, int32_t* __restrict__ counters, const ObjEntry* __restrict__ objs,
     const rg_detection* __restrict__ dets, const int32_t* __restrict__ det_off,
@@ -540,12 +831,18 @@ __global__ void __launch_bounds__(WPB * 32, MINB) match_slots_warp_kernel(
       const int sc = cfg.close_scale;
       const rg_search_range rg = far ? rg_search_range{0, cfg.dx_max_far, -1, 1}
                                      : rg_search_range{0, (cfg.dx_max_close + sc - 1) / sc, -1, 1};
-      const Pass f = warp_pass<CT, PF>(pts, np, 0, 0, L, R, g, trusted != 0, rg, vp, lane, evals, part, nparts, xc);
+      auto pass = [&](int sx, int sy, const CT* A, const CT* B, const rg_search_range& q) -> Pass {
+        if constexpr (V2 && sizeof(CT) == 4) {
+          if (trusted && nparts == 1)
+            return warp_pass_v2(pts, np, sx, sy, A, B, g, q, vp, maxp + 1, lane, evals);
+        }
+        return warp_pass<CT, PF>(pts, np, sx, sy, A, B, g, trusted != 0, q, vp, lane, evals, part, nparts, xc);
+      };
+      const Pass f = pass(0, 0, L, R, rg);
       if (f.has) {
         finish(f, r);
         const rg_search_range brg = {-rg.dx_max, -rg.dx_min, -f.dy, -f.dy};
-        const Pass b = warp_pass<CT, PF>(pts, np, -f.dx, f.dy, R, L, g, trusted != 0, brg, vp, lane, evals, part,
-                                         nparts, xc);
+        const Pass b = pass(-f.dx, f.dy, R, L, brg);
         if (b.has) {
           rg_match_result rb;
           finish(b, rb);
@@ -580,14 +877,14 @@ __global__ void __launch_bounds__(WPB * 32, MINB) match_slots_warp_kernel(
   }
 }
 
-template <typename CT, int WPB, int MINB, int PF = 0, bool COOP = false>
+template <typename CT, int WPB, int MINB, int PF = 0, bool COOP = false, bool V2 = false>
 cudaError_t launch_variant(const Slot* slots, int32_t* counters, int slot_capacity,
                                   const ObjEntry* objs, const rg_detection* dets, const int32_t* det_off,
                                   const void* fl, const void* fr, const PadGeom& gf, const void* sl,
                                   const void* sr, const PadGeom& gs, int img_w, int img_h, int trusted,
                                   rg_ranger_config cfg, rg_match_result* res, rg_ranger_stats* stats,
                                   int max_points, cudaStream_t s) {
-  auto kern = match_slots_warp_kernel<CT, WPB, MINB, PF, COOP>;
+  auto kern = match_slots_warp_kernel<CT, WPB, MINB, PF, COOP, V2>;
   max_points = (max_points + 1) & ~1;  // keeps every warp's VPoint array 16-B aligned
   const size_t smem = (sizeof(int2) * (size_t)max_points + sizeof(VPoint<CT>) * (size_t)(max_points + 1)) * WPB;
   static SmemAttr attr;  // one per instantiation
@@ -638,6 +935,12 @@ cudaError_t launch_match_slots(const Slot* slots, int32_t* counters, int slot_ca
     case 5: return launch_variant<uint32_t, 8, 6, 4, true>(RG_ARGS);
     case 6: return launch_variant<uint32_t, 16, 3, 4, true>(RG_ARGS);
     case 7: return launch_variant<uint32_t, 4, 12, 4, true>(RG_ARGS);
+    // 8-10: the vectorised carry-save sweep (warp_pass_v2), measured slower
+    // (1.26-1.75 vs 0.90 ms per 256 C2 frames: long-scoreboard stalls at
+    // 64 registers / 50 % occupancy, spills at 40)
+    case 8: return launch_variant<uint32_t, 16, 3, 0, false, true>(RG_ARGS);
+    case 9: return launch_variant<uint32_t, 8, 4, 0, false, true>(RG_ARGS);
+    case 10: return launch_variant<uint32_t, 16, 2, 0, false, true>(RG_ARGS);
     default: return launch_variant<uint32_t, 16, 3>(RG_ARGS);
   }
 #undef RG_ARGS

@@ -14,7 +14,14 @@ struct PBox {
   double x0, y0, x1, y1;
 };
 
-__device__ __forceinline__ double half_of(double v) { return __ddiv_rn(v, 2.0); }
+// v / 2.0 of the reference, as the exactly equal multiply by 0.5 (a power-of-
+// two scaling rounds the same real number: identical bits for every double)
+__device__ __forceinline__ double half_of(double v) { return __dmul_rn(v, 0.5); }
+// x / (double)n with the same bits: a multiply by 1/n when n is a power of two
+// (1/n exact), else the IEEE division
+__device__ __forceinline__ double div_n(double x, int n) {
+  return (n & (n - 1)) == 0 ? __dmul_rn(x, 1.0 / (double)n) : __ddiv_rn(x, (double)n);
+}
 __device__ __forceinline__ double dmin(double a, double b) { return b < a ? b : a; }  // std::min
 __device__ __forceinline__ double dmax(double a, double b) { return a < b ? b : a; }  // std::max
 
@@ -79,7 +86,7 @@ __device__ __forceinline__ int dev_cap(const rg_ranger_config& c) {
 }
 __device__ __forceinline__ void dev_close_grid(const PBox& b, const rg_ranger_config& c, int* rows,
                                                int* cols) {
-  const double half_tau = __ddiv_rn(c.tau_s, 2.0);
+  const double half_tau = half_of(c.tau_s);
   const int cc = (int)__ddiv_rn(__dsub_rn(b.x1, b.x0), half_tau);
   const int rr = (int)__ddiv_rn(__dsub_rn(b.y1, b.y0), half_tau);
   *cols = cc > 2 ? cc : 2;
@@ -127,14 +134,14 @@ __device__ __forceinline__ bool dev_sample_point(const SampleGeom& g, int idx, c
   const int j = idx / g.n, i = idx - j * g.n;
   double fx, fy;
   if (g.far) {
-    fy = __dadd_rn(g.box.y0, __ddiv_rn(__dmul_rn(__dadd_rn((double)j, 0.5), g.bh), (double)g.n));
-    fx = __dadd_rn(g.box.x0, __ddiv_rn(__dmul_rn(__dadd_rn((double)i, 0.5), g.bw), (double)g.n));
+    fy = __dadd_rn(g.box.y0, div_n(__dmul_rn(__dadd_rn((double)j, 0.5), g.bh), g.n));
+    fx = __dadd_rn(g.box.x0, div_n(__dmul_rn(__dadd_rn((double)i, 0.5), g.bw), g.n));
     *px = (int)lround(fx);
     *py = (int)lround(fy);
     if (*px < 0 || *px >= w || *py < 0 || *py >= h) return false;
   } else {
-    fy = __dadd_rn(g.sy0, __ddiv_rn(__dmul_rn(__dadd_rn((double)j, 0.5), g.sh), (double)g.n));
-    fx = __dadd_rn(g.sx0, __ddiv_rn(__dmul_rn(__dadd_rn((double)i, 0.5), g.sw), (double)g.n));
+    fy = __dadd_rn(g.sy0, div_n(__dmul_rn(__dadd_rn((double)j, 0.5), g.sh), g.n));
+    fx = __dadd_rn(g.sx0, div_n(__dmul_rn(__dadd_rn((double)i, 0.5), g.sw), g.n));
     if (fx < 0 || fx >= w || fy < 0 || fy >= h) return false;
   }
   // occluded points drop (template_match.hpp:159-163, 181, 212)
