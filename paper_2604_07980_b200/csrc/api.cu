@@ -325,7 +325,8 @@ rg_status prepare_rasters(rg_ctx* ctx, const FrameJob& J, const rg_ranger_config
 }
 
 // K1 of job J into the rasters starting at raster frame `slot0`
-rg_status enqueue_census(rg_ctx* ctx, const FrameJob& J, const Rasters& R, int slot0, cudaStream_t s) {
+rg_status enqueue_census(rg_ctx* ctx, const FrameJob& J, const rg_ranger_config& cfg, const Rasters& R, int slot0,
+                         cudaStream_t s) {
   RG_NVTX("K1 census");
   const int w = J.w, h = J.h, F = J.n_frames;
   const size_t csz = R.wide ? sizeof(unsigned long long) : sizeof(uint32_t);
@@ -339,8 +340,21 @@ rg_status enqueue_census(rg_ctx* ctx, const FrameJob& J, const Rasters& R, int s
                                         R.gf, (u64*)sl, (u64*)sr, R.gs, R.ix, R.iy, J.left_shift, s));
     count_launch(ctx, ST_CENSUS);
   } else if (!(J.full_l && J.scaled_l)) {
-    RG_CUDA(ctx, launch_census_frames(J.left, J.right, F, J.frame_stride, J.pitch, w, h, fl, fr, R.gf, sl, sr,
-                                      R.gs, R.ix, R.iy, J.left_shift, true, s));
+    // ROI rows only (census_transform_rois, template_match.hpp:300-321) when
+    // no caller codes are mixed in and the fast layout applies
+    static const bool rois_off = getenv("RG_CENSUS_FULL") != nullptr;  // A/B knob: full-frame K1
+    cudaError_t e = cudaErrorNotSupported;
+    if (!rois_off && !J.full_l && !J.scaled_l && J.dets) {
+      const size_t words = (size_t)F * ((h + 31) / 32 + (R.gs.h + 31) / 32);
+      uint32_t* masks = DBUF(uint32_t, ctx, B_ROWMASK, std::max<size_t>(words, 1));
+      NEED(masks);
+      e = launch_census_rois(J.left, J.right, F, J.frame_stride, J.pitch, w, h, fl, fr, R.gf, sl, sr, R.gs,
+                             J.left_shift, true, J.dets, J.det_off, cfg.tau_s, masks, s);
+      if (e != cudaSuccess && e != cudaErrorNotSupported) RG_CUDA(ctx, e);
+    }
+    if (e == cudaErrorNotSupported)
+      RG_CUDA(ctx, launch_census_frames(J.left, J.right, F, J.frame_stride, J.pitch, w, h, fl, fr, R.gf, sl, sr,
+                                        R.gs, R.ix, R.iy, J.left_shift, true, s));
     count_launch(ctx, ST_CENSUS);
   }
   // caller-supplied codes (a pre-filled CensusCache) into the padded layout
@@ -428,7 +442,7 @@ rg_status enqueue_pipeline(rg_ctx* ctx, const FrameJob& J, const rg_ranger_confi
     RG_CUDA(ctx, cudaStreamWaitEvent(aux, ctx->ev_sync[0], 0));
   }
   if (prof) RG_CUDA(ctx, cudaEventRecord(ctx->ev[0], s));
-  TRY(enqueue_census(ctx, J, R, 0, s));
+  TRY(enqueue_census(ctx, J, cfg, R, 0, s));
   return enqueue_match(ctx, J, cfg, R, 0, s, counters, prof ? ctx->ev + 1 : nullptr, pb, aux);
 }
 
@@ -535,7 +549,7 @@ rg_status run_pipeline_overlapped(rg_ctx* ctx, const FrameJob& J, const rg_range
     const FrameJob Jk = sub(k);
     if (k >= 2) RG_CUDA(ctx, cudaStreamWaitEvent(cs, ctx->ev_sync[2 + slot], 0));  // match k-2 released the slot
     if (prof) RG_CUDA(ctx, cudaEventRecord(ctx->ev_prof[6 * k], cs));
-    TRY(enqueue_census(ctx, Jk, R, slot * chunk, cs));
+    TRY(enqueue_census(ctx, Jk, cfg, R, slot * chunk, cs));
     if (prof) RG_CUDA(ctx, cudaEventRecord(ctx->ev_prof[6 * k + 1], cs));
     RG_CUDA(ctx, cudaEventRecord(ctx->ev_sync[4 + slot], cs));
     RG_CUDA(ctx, cudaStreamWaitEvent(ms, ctx->ev_sync[4 + slot], 0));

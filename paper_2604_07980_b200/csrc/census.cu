@@ -10,6 +10,7 @@
 #include <cuda_fp16.h>
 
 #include "rg_common.cuh"
+#include "rg_device.cuh"
 
 namespace rg {
 namespace {
@@ -75,6 +76,17 @@ __global__ void __launch_bounds__(TPB) census_frames_kernel(
       if (iy >= 0) red[(int64_t)iy * gs.pitch + ix] = code;
     }
   }
+}
+
+// any bit of rows [y0, y1) set in the row mask m (one bit per row)
+__device__ __forceinline__ bool rows_any(const uint32_t* __restrict__ m, int y0, int y1) {
+  for (int y = y0; y < y1;) {
+    const int wd = y >> 5, b0 = y & 31, nb = min(32 - b0, y1 - y);
+    const uint32_t bits = (nb == 32 ? 0xFFFFFFFFu : ((1u << nb) - 1u)) << b0;
+    if (__ldg(m + wd) & bits) return true;
+    y += nb;
+  }
+  return false;
 }
 
 // ---------------------------------------------------------------------------
@@ -143,12 +155,15 @@ __device__ __forceinline__ void c2_assemble(uint32_t g0, uint32_t g1, uint32_t g
   }
 }
 
-// Descriptors of 4 pixel pairs from the 5 V rows w[0..4] (y-2 .. y+2).
-template <bool S31>
-__device__ __forceinline__ void c2_codes(const uint32_t (&w)[5][8], uint32_t lo[4], uint32_t hi[4]) {
+// Descriptors of NQ pixel pairs from the 5 V rows w[0..4] (y-2 .. y+2): the
+// pair q sits at window column q * QS + 2 (QS = 1: four adjacent columns;
+// QS = 2: the even columns of the stride-2 reduced census).
+template <bool S31, int NQ = 4, int QS = 1>
+__device__ __forceinline__ void c2_codes(const uint32_t (&w)[5][8], uint32_t lo[NQ], uint32_t hi[NQ]) {
   const __half2 two = __float2half2_rn(2.0f), four = __float2half2_rn(4.0f);
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
+  for (int qq = 0; qq < NQ; ++qq) {
+    const int q = qq * QS;
     const __half2 c = *reinterpret_cast<const __half2*>(&w[2][q + 2]);
     __half2 g[3];
     g[0] = __float2half2_rn(S31 ? -3.0f : 3.0f);  // S31: negative, so the fp16 sign lands on bit 31
@@ -163,16 +178,19 @@ __device__ __forceinline__ void c2_codes(const uint32_t (&w)[5][8], uint32_t lo[
       g[gi] = __hfma2(g[gi], wi == 13 ? four : two, (S31 && gi == 0) ? __hneg2(m) : m);
     }
     c2_assemble<S31>(*reinterpret_cast<uint32_t*>(&g[0]), *reinterpret_cast<uint32_t*>(&g[1]),
-                *reinterpret_cast<uint32_t*>(&g[2]), lo[q], hi[q]);
+                *reinterpret_cast<uint32_t*>(&g[2]), lo[qq], hi[qq]);
   }
 }
 
 // Phase 2 for one warp: its C2_PR pair rows of the tile whose V is in smem.
 // EDGE: the strip touches the image border (codes 0 where the window leaves).
-template <bool EDGE, bool S31>
+// ROI: fm / rm are the frame's full / reduced row masks; a pair row is
+// computed when either raster needs it and each raster stores only its rows.
+template <bool EDGE, bool S31, bool ROI = false>
 __device__ __forceinline__ void c2_strip(const uint32_t* __restrict__ V, uint32_t* __restrict__ full,
                                          uint32_t* __restrict__ red, const PadGeom& gf, const PadGeom& gs,
-                                         int x0, int y0, int w, int h) {
+                                         int x0, int y0, int w, int h, const uint32_t* __restrict__ fm = nullptr,
+                                         const uint32_t* __restrict__ rm = nullptr) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int pr0 = wid * C2_PR;
   const int64_t ostep = 2 * (int64_t)gf.pitch;
@@ -187,6 +205,12 @@ __device__ __forceinline__ void c2_strip(const uint32_t* __restrict__ V, uint32_
     for (int p = pr0; p < pr0 + C2_PR; ++p, o += ostep, ro += gs.pitch) {
       const int y = y0 + 2 * p;
       if (EDGE && y >= h) break;
+      bool wf = true, wr = true;
+      if (ROI) {
+        wf = (__ldg(fm + (y >> 5)) >> (y & 31)) & 3u;  // y even: y, y + 1 share a word
+        wr = red && ((__ldg(rm + (y >> 6)) >> ((y >> 1) & 31)) & 1u);
+        if (!wf && !wr) continue;
+      }
       uint32_t win[5][8];
 #pragma unroll
       for (int j = 0; j < 5; ++j) {
@@ -206,10 +230,12 @@ __device__ __forceinline__ void c2_strip(const uint32_t* __restrict__ V, uint32_
           if (!(xin && y + 1 >= 2 && y + 1 <= h - 3)) hi[q] = 0u;
         }
       }
-      *reinterpret_cast<uint4*>(o) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
-      if (!EDGE || y + 1 < h) *reinterpret_cast<uint4*>(o + gf.pitch) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+      if (wf) {
+        *reinterpret_cast<uint4*>(o) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+        if (!EDGE || y + 1 < h) *reinterpret_cast<uint4*>(o + gf.pitch) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+      }
       // reduced raster = codes at even (x, y): (x/2, y/2)
-      if (red) *reinterpret_cast<uint2*>(ro) = make_uint2(lo[0], lo[2]);
+      if (red && wr) *reinterpret_cast<uint2*>(ro) = make_uint2(lo[0], lo[2]);
     }
   }
 }
@@ -226,10 +252,18 @@ template <bool S31>
 __global__ void RG_C2_BOUNDS census_pairs_kernel(
     const uint8_t* __restrict__ left, const uint8_t* __restrict__ right, int64_t frame_stride,
     int pitch, int w, int h, uint32_t* __restrict__ fl, uint32_t* __restrict__ fr, PadGeom gf,
-    uint32_t* __restrict__ sl, uint32_t* __restrict__ sr, PadGeom gs, const int32_t* __restrict__ lshift) {
+    uint32_t* __restrict__ sl, uint32_t* __restrict__ sr, PadGeom gs, const int32_t* __restrict__ lshift,
+    const uint32_t* __restrict__ rmask, int mstride) {
   extern __shared__ __align__(16) uint32_t V[];  // [C2_VR][C2_VW]
   const int sides = right ? 2 : 1;
   const int frame = blockIdx.z / sides, side = blockIdx.z - frame * sides;
+  // ROI rows (rmask: one bit per raster row of this frame): a tile without a
+  // needed row leaves before its V build, a warp strip without one after it
+  const uint32_t* fm = rmask ? rmask + (int64_t)frame * mstride : nullptr;
+  const uint32_t* rm = rmask ? fm + (h + 31) / 32 : nullptr;  // reduced rows follow the full rows
+  if (fm && !rows_any(fm, blockIdx.y * C2_TY, min(blockIdx.y * C2_TY + C2_TY, h)) &&
+      !(sl && rows_any(rm, blockIdx.y * C2_TY / 2, min(blockIdx.y * C2_TY / 2 + C2_TY / 2, gs.h))))
+    return;
   // shift_vertical (image.hpp:145-154) of the left image folded into the row
   // addressing: image row y reads source row clamp(y - sh)
   const int sh = (side == 0 && lshift) ? lshift[frame] : 0;
@@ -270,11 +304,203 @@ __global__ void RG_C2_BOUNDS census_pairs_kernel(
   // ---- phase 2
   const int ys = y0 + 2 * (threadIdx.x >> 5) * C2_PR;
   if (ys >= h) return;
+  if (fm && !rows_any(fm, ys, min(ys + 2 * C2_PR, h)) && !(sl && rows_any(rm, ys / 2, min(ys / 2 + C2_PR, gs.h))))
+    return;
   const bool edge = x0 < 2 || x0 + C2_TX + 3 > w - 3 || ys < 2 || ys + 2 * C2_PR + 1 > h - 3;
-  if (__any_sync(0xffffffffu, edge))  // warp-uniform (the vote lets the compiler keep one branch)
+  const bool e = __any_sync(0xffffffffu, edge);  // warp-uniform (the vote lets the compiler keep one branch)
+  if (fm) {
+    if (e)
+      c2_strip<true, S31, true>(V, full, red, gf, gs, x0, y0, w, h, fm, rm);
+    else
+      c2_strip<false, S31, true>(V, full, red, gf, gs, x0, y0, w, h, fm, rm);
+  } else if (e) {
     c2_strip<true, S31>(V, full, red, gf, gs, x0, y0, w, h);
-  else
+  } else {
     c2_strip<false, S31>(V, full, red, gf, gs, x0, y0, w, h);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// ROI-row census (the reference's census_transform_rois, census.hpp:100-138,
+// as estimate_object_disparities calls it, template_match.hpp:300-321): the
+// full-resolution raster only on rows of FAR census ROIs (box dilated by 3
+// rows, detail::add_roi :245-253) and the reduced raster only on rows of
+// CLOSE ROIs, computed by a stride-2 kernel instead of being gathered from a
+// full-frame transform.  Codes on those rows are bit-identical to the full
+// transform; the matcher never reads another row (its
+// samples lie within the box rows +-1).  At C2 this is 27 % of the full rows
+// and 87 % of the reduced rows: about half the bytes and compares of K1.
+
+// Row masks per frame: bit y of words [0, wf) = full raster row y needed
+// (FAR ROI), bit y' of words [wf, wf + wr) = reduced row y' (CLOSE ROI).
+// Every detection of the frame contributes (a superset of the selected ones:
+// the planner runs after the census).
+constexpr int RM_T = 128;
+__global__ void __launch_bounds__(RM_T) census_rows_kernel(const rg_detection* __restrict__ dets,
+                                                          const int32_t* __restrict__ det_off, int w, int h,
+                                                          double tau_s, int cw, int ch, int wf, int wr,
+                                                          uint32_t* __restrict__ mask) {
+  extern __shared__ uint32_t sm_rows[];
+  const int f = blockIdx.x;
+  for (int i = threadIdx.x; i < wf + wr; i += RM_T) sm_rows[i] = 0u;
+  __syncthreads();
+  const int d0 = det_off[f], n = det_off[f + 1] - d0;
+  const double sy = __ddiv_rn((double)ch, (double)h);  // template_match.hpp:305 double(ch) / h
+  auto clampi = [](double v) { return (int)fmin(fmax(v, -1.0e9), 1.0e9); };
+  for (int i = threadIdx.x; i < n; i += RM_T) {
+    const rg_detection d = dets[d0 + i];
+    const PBox b = pixel_box(d, w, h);
+    int a, e;
+    uint32_t* m;
+    if (dev_classify(d, w, h, tau_s) == RG_KIND_FAR) {  // add_roi(far_rois, box, 1, 1, .., 3, w, h)
+      a = max(0, clampi(floor(b.y0)) - 3);
+      e = min(h, clampi(ceil(b.y1)) + 3 + 1);
+      m = sm_rows;
+    } else {  // add_roi(scaled_rois, box, cw / w, ch / h, .., 3, cw, ch)
+      a = max(0, clampi(floor(__dmul_rn(b.y0, sy))) - 3);
+      e = min(ch, clampi(ceil(__dmul_rn(b.y1, sy))) + 3 + 1);
+      m = sm_rows + wf;
+    }
+    for (int y = a; y < e;) {
+      const int wd = y >> 5, b0 = y & 31, nb = min(32 - b0, e - y);
+      atomicOr(&m[wd], (nb == 32 ? 0xFFFFFFFFu : ((1u << nb) - 1u)) << b0);
+      y += nb;
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < wf + wr; i += RM_T) mask[(int64_t)f * (wf + wr) + i] = sm_rows[i];
+}
+
+// Warp-tile "vertical pair" census for ROI rows: every warp owns a tile of
+// 120 source columns x 10 output rows (5 row pairs; 120 columns + the 2-px
+// halo = 32 image words, one per lane) with its own V rows in
+// shared memory (no CTA barrier), so work follows the row masks at 10-row
+// granularity.  STRIDE 1 writes the full raster (4 codes per lane per row);
+// STRIDE 2 writes the reduced raster of an exact-half CLOSE scale (reduced
+// (x', y') = full (2x', 2y'), census.hpp:59-64 with lround(2i) = 2i): the V
+// entry of source row s pairs rows s and s + 2, so reduced rows y', y' + 1
+// (source rows 2y', 2y' + 2) advance together, and each lane emits the even
+// source columns c, c + 2 of the same 8-entry window rows.
+#ifndef RG_RW_WPB1
+#define RG_RW_WPB1 1
+#endif
+#ifndef RG_RW_WPB2
+#define RG_RW_WPB2 1
+#endif
+// warps (independent tiles) per CTA: the FAR row tiles are sparse (most warps
+// leave at once), so single-warp CTAs release their slot immediately
+template <int STRIDE>
+__host__ __device__ constexpr int rw_wpb() { return STRIDE == 1 ? RG_RW_WPB1 : RG_RW_WPB2; }
+template <int STRIDE>
+#ifndef RG_RW_PR2
+#define RG_RW_PR2 3
+#endif
+__host__ __device__ constexpr int rw_pr() { return STRIDE == 1 ? 5 : RG_RW_PR2; }  // row pairs per warp tile
+constexpr int RW_TX = 120;  // source columns per warp tile (lanes 0..29 emit codes)
+constexpr int RW_VW = 136;  // V row stride: index 4 = source column x0 - 2
+template <int STRIDE>
+__host__ __device__ constexpr int rw_nv() { return 2 * STRIDE * (rw_pr<STRIDE>() - 1) + 5; }  // V rows (13 / 13)
+template <int STRIDE>
+__host__ __device__ constexpr size_t rw_smem() { return sizeof(uint32_t) * rw_wpb<STRIDE>() * rw_nv<STRIDE>() * RW_VW; }
+
+template <bool S31, int STRIDE>
+__global__ void __launch_bounds__(rw_wpb<STRIDE>() * 32) census_rowtile_kernel(
+    const uint8_t* __restrict__ left, const uint8_t* __restrict__ right, int64_t frame_stride, int pitch, int w,
+    int h, uint32_t* __restrict__ ol, uint32_t* __restrict__ orr, PadGeom g, const int32_t* __restrict__ lshift,
+    const uint32_t* __restrict__ rmask, int mstride) {
+  constexpr int NV = rw_nv<STRIDE>(), NI = NV + STRIDE;  // V rows, image rows
+  constexpr int RW_PR = rw_pr<STRIDE>();
+  extern __shared__ __align__(16) uint32_t Vall[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int sides = right ? 2 : 1;
+  const int frame = blockIdx.z / sides, side = blockIdx.z - frame * sides;
+  const int Y0 = (blockIdx.y * rw_wpb<STRIDE>() + wid) * 2 * RW_PR;  // first output row of this warp's tile
+  if (Y0 >= g.h) return;
+  const uint32_t* fm = rmask + (int64_t)frame * mstride;
+  if (!rows_any(fm, Y0, min(Y0 + 2 * RW_PR, g.h))) return;
+  uint32_t* V = Vall + wid * NV * RW_VW;
+  const int sh = (side == 0 && lshift) ? lshift[frame] : 0;  // shift_vertical of the left image
+  const uint8_t* img = (side ? right : left) + (int64_t)frame * frame_stride;
+  uint32_t* out = (side ? orr : ol) + (int64_t)frame * g.fstride + g.origin;
+  const int x0 = blockIdx.x * RW_TX;  // source column origin
+  const int S0 = STRIDE * Y0 - 2;   // source row of V row 0
+  // ---- V rows: word column k of image rows S0 .. S0 + NI - 1 (clamped);
+  // entry (s, c) = half2(1024 + I(c, s), 1024 + I(c, s + STRIDE))
+  const int pw = pitch / 4;
+  {
+    const int k = lane;
+    const int kw = min(max((x0 - 4) / 4 + k, 0), (w + 3) / 4 - 1);
+    const int ya = S0 - sh;
+    uint32_t wv[NI];
+    if (ya >= 0 && ya + NI - 1 <= h - 1) {
+      const uint32_t* col = reinterpret_cast<const uint32_t*>(img) + (int64_t)ya * pw + kw;
+#pragma unroll
+      for (int t = 0; t < NI; ++t, col += pw) wv[t] = __ldg(col);
+    } else {
+      const uint32_t* col = reinterpret_cast<const uint32_t*>(img) + kw;
+#pragma unroll
+      for (int t = 0; t < NI; ++t) wv[t] = __ldg(col + (int64_t)min(max(ya + t, 0), h - 1) * pw);
+    }
+    uint32_t* vrow = V + 4 + 4 * k - 2;  // entries of source columns x0 - 4 + 4k .. + 3
+#pragma unroll
+    for (int t = 0; t < NV; ++t) {
+      const uint32_t a = wv[t], b = wv[t + STRIDE];
+      *reinterpret_cast<uint2*>(vrow + t * RW_VW) = make_uint2(c2_vpair(a, b, 0), c2_vpair(a, b, 1));
+      *reinterpret_cast<uint2*>(vrow + t * RW_VW + 2) = make_uint2(c2_vpair(a, b, 2), c2_vpair(a, b, 3));
+    }
+  }
+  __syncwarp();
+  // ---- codes: 5 row pairs (output rows y, y + 1 = source rows STRIDE y, STRIDE y + STRIDE)
+  constexpr int NQ = 4 / STRIDE;
+  const int xs = x0 + 4 * lane;     // source column of this lane's first output
+  const int xo = xs / STRIDE;       // its output column
+  if (lane >= RW_TX / 4 || xo >= g.w) return;
+  const bool edge = x0 < 2 || x0 + RW_TX + 2 > w - 3 || STRIDE * Y0 < 2 || STRIDE * (Y0 + 2 * RW_PR) > h - 3;
+  const uint32_t* vbase = V + 4 + 4 * lane;  // V index of source column xs - 2
+#pragma unroll
+  for (int p = 0; p < RW_PR; ++p) {
+    const int y = Y0 + 2 * p;
+    if (y >= g.h) break;
+    if (!((__ldg(fm + (y >> 5)) >> (y & 31)) & 3u)) continue;  // y even: y, y + 1 share a mask word
+    uint32_t win[5][8];
+#pragma unroll
+    for (int j = 0; j < 5; ++j) {
+      const uint4* src = reinterpret_cast<const uint4*>(vbase + (2 * STRIDE * p + j) * RW_VW);
+      const uint4 a = src[0], b = src[1];
+      win[j][0] = a.x; win[j][1] = a.y; win[j][2] = a.z; win[j][3] = a.w;
+      win[j][4] = b.x; win[j][5] = b.y; win[j][6] = b.z; win[j][7] = b.w;
+    }
+    uint32_t lo[NQ], hi[NQ];
+    c2_codes<S31, NQ, STRIDE>(win, lo, hi);
+    if (edge) {
+      const int sy0 = STRIDE * y, sy1 = STRIDE * y + STRIDE;
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        const int sx = xs + STRIDE * q;
+        const bool xin = sx >= 2 && sx <= w - 3;
+        if (!(xin && sy0 >= 2 && sy0 <= h - 3)) lo[q] = 0u;
+        if (!(xin && sy1 >= 2 && sy1 <= h - 3)) hi[q] = 0u;
+      }
+    }
+    uint32_t* o = out + (int64_t)y * g.pitch + xo;
+    const bool two = y + 1 < g.h;
+    if (xo + NQ <= g.w) {
+      if (STRIDE == 1) {
+        *reinterpret_cast<uint4*>(o) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+        if (two) *reinterpret_cast<uint4*>(o + g.pitch) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+      } else {
+        *reinterpret_cast<uint2*>(o) = make_uint2(lo[0], lo[NQ - 1]);
+        if (two) *reinterpret_cast<uint2*>(o + g.pitch) = make_uint2(hi[0], hi[NQ - 1]);
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        if (xo + q >= g.w) break;
+        o[q] = lo[q];
+        if (two) o[g.pitch + q] = hi[q];
+      }
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -372,13 +598,75 @@ cudaError_t launch_census_frames(const uint8_t* left, const uint8_t* right, int 
     if (e != cudaSuccess) return e;
     dim3 grid((w + C2_TX - 1) / C2_TX, (h + C2_TY - 1) / C2_TY, sides * n_frames);
     kern<<<grid, C2_WARPS * 32, C2_SMEM, s>>>(left, right, frame_stride, pitch, w, h, fl, fr, gf, sl, sr, gs,
-                                              lshift);
+                                              lshift, nullptr, 0);
     return cudaGetLastError();
   }
   dim3 grid((w + TX - 1) / TX, (h + TY - 1) / TY, sides * n_frames);
   census_frames_kernel<<<grid, TPB, 0, s>>>(left, right, frame_stride, pitch, w, h, fl, fr, gf, sl,
                                             sr, gs, inv_x, inv_y, lshift, internal);
   return cudaGetLastError();
+}
+
+// ROI-row census of a batch (see census_rows_kernel): the row masks, the
+// full raster on FAR ROI rows and the reduced raster on CLOSE ROI rows.
+// cudaErrorNotSupported when the fast layout does not apply (the caller then
+// runs the full-frame launch_census_frames).
+cudaError_t launch_census_rois(const uint8_t* left, const uint8_t* right, int n_frames, int64_t frame_stride,
+                               int pitch, int w, int h, uint32_t* fl, uint32_t* fr, const PadGeom& gf, uint32_t* sl,
+                               uint32_t* sr, const PadGeom& gs, const int32_t* lshift, bool internal,
+                               const rg_detection* dets, const int32_t* det_off, double tau_s, uint32_t* masks,
+                               cudaStream_t s) {
+  if (n_frames <= 0) return cudaSuccess;
+  const int sides = right ? 2 : 1;
+  const bool aligned = (pitch % 4 == 0) && (w % 4 == 0) && (frame_stride % 4 == 0) &&
+                       (reinterpret_cast<uintptr_t>(left) % 4 == 0) &&
+                       (!right || reinterpret_cast<uintptr_t>(right) % 4 == 0) && gf.pitch % 4 == 0 &&
+                       gf.origin % 4 == 0 && w >= 8 && h >= 8;
+  const bool half = sl && gs.w * 2 == w && gs.h * 2 == h && gs.pitch % 2 == 0 && gs.origin % 2 == 0 &&
+                    gs.w >= 4 && gs.h >= 4;
+  if (!aligned || !half || !masks || !dets) return cudaErrorNotSupported;
+  const int wf = (h + 31) / 32, wr = (gs.h + 31) / 32;
+  census_rows_kernel<<<n_frames, RM_T, sizeof(uint32_t) * (wf + wr), s>>>(dets, det_off, w, h, tau_s, gs.w, gs.h,
+                                                                         wf, wr, masks);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  static const int mode = [] {
+    // A/B knob: 1 warp row tiles (default), 0 the full-frame pair tiles storing
+    // only ROI rows (measured: no faster than storing every row -- K1 is
+    // bound by its compares and V builds, not by its stores)
+    const char* v = getenv("RG_CENSUS_MODE");
+    return v ? atoi(v) : 1;
+  }();
+  if (mode == 0) {
+    auto kern = internal ? census_pairs_kernel<true> : census_pairs_kernel<false>;
+    static SmemAttr pattr[2];
+    e = pattr[internal].ensure((const void*)kern, C2_SMEM);
+    if (e != cudaSuccess) return e;
+    dim3 grid((w + C2_TX - 1) / C2_TX, (h + C2_TY - 1) / C2_TY, sides * n_frames);
+    kern<<<grid, C2_WARPS * 32, C2_SMEM, s>>>(left, right, frame_stride, pitch, w, h, fl, fr, gf, sl, sr, gs, lshift,
+                                              masks, wf + wr);
+    return cudaGetLastError();
+  }
+  auto rowtile = [&](auto kern, size_t smem, SmemAttr& attr, uint32_t* a, uint32_t* b, const PadGeom& g,
+                     const uint32_t* m, int pr, int wpb) -> cudaError_t {
+    cudaError_t e2 = attr.ensure((const void*)kern, smem);
+    if (e2 != cudaSuccess) return e2;
+    const int ty = 2 * pr * wpb;  // output rows per CTA
+    dim3 grid((w + RW_TX - 1) / RW_TX, (g.h + ty - 1) / ty, sides * n_frames);
+    kern<<<grid, wpb * 32, smem, s>>>(left, right, frame_stride, pitch, w, h, a, b, g, lshift, m, wf + wr);
+    return cudaGetLastError();
+  };
+  static SmemAttr attr[4];
+  e = internal ? rowtile(census_rowtile_kernel<true, 1>, rw_smem<1>(), attr[0], fl, fr, gf, masks, rw_pr<1>(),
+                         rw_wpb<1>())
+               : rowtile(census_rowtile_kernel<false, 1>, rw_smem<1>(), attr[1], fl, fr, gf, masks, rw_pr<1>(),
+                         rw_wpb<1>());
+  if (e != cudaSuccess) return e;
+  e = internal ? rowtile(census_rowtile_kernel<true, 2>, rw_smem<2>(), attr[2], sl, sr, gs, masks + wf, rw_pr<2>(),
+                         rw_wpb<2>())
+               : rowtile(census_rowtile_kernel<false, 2>, rw_smem<2>(), attr[3], sl, sr, gs, masks + wf, rw_pr<2>(),
+                         rw_wpb<2>());
+  return e;
 }
 
 cudaError_t launch_census64_frames(const uint8_t* left, const uint8_t* right, int n_frames, int64_t frame_stride,

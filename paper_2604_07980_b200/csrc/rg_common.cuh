@@ -162,7 +162,7 @@ enum BufId {
   B_OBJ, B_SLOTS, B_SLOT_RES, B_OUT, B_OUT_CNT, B_COUNTERS, B_MAPX, B_MAPY,
   B_PTS, B_OFFS, B_RANGES, B_MRES, B_TMP0, B_TMP1, B_TMP2, B_TMP3, B_STATS,
   B_BM_L, B_BM_R, B_BM_OUT, B_BM_CNT, B_ROIS, B_STAGE_L, B_STAGE_R, B_SHIFT,
-  B_SEQ, B_SGM_COST, B_SGM_ACC, B_BOX_IDX, B_BOX_OUT, B_SYNTH, B_COUNT
+  B_SEQ, B_SGM_COST, B_SGM_ACC, B_BOX_IDX, B_BOX_OUT, B_SYNTH, B_ROWMASK, B_COUNT
 };
 
 // error helpers (defined in api.cu)
@@ -188,6 +188,11 @@ cudaError_t launch_census_frames(const uint8_t* left, const uint8_t* right, int 
                                  uint32_t* sr, const PadGeom& gs, const int32_t* inv_x,
                                  const int32_t* inv_y, const int32_t* lshift, bool internal,
                                  cudaStream_t s);
+cudaError_t launch_census_rois(const uint8_t* left, const uint8_t* right, int n_frames, int64_t frame_stride,
+                               int pitch, int w, int h, uint32_t* fl, uint32_t* fr, const PadGeom& gf, uint32_t* sl,
+                               uint32_t* sr, const PadGeom& gs, const int32_t* lshift, bool internal,
+                               const rg_detection* dets, const int32_t* det_off, double tau_s, uint32_t* masks,
+                               cudaStream_t s);
 cudaError_t launch_census64_frames(const uint8_t* left, const uint8_t* right, int n_frames, int64_t frame_stride,
                                    int pitch, int w, int h, unsigned long long* fl, unsigned long long* fr,
                                    const PadGeom& gf, unsigned long long* sl, unsigned long long* sr,
