@@ -253,11 +253,12 @@ def c5_stream(args, eng, ctx, dev, stream, rank, world, dets, recs_np, offs_np):
     def range_chunk(glo, ghi, o, c):
         a = glo - lo
         eng.range_device(dL[a:a + ghi - glo], dR[a:a + ghi - glo], d_dets, d_offs[:ghi - glo + 1], o, c,
-                         stream=stream.cuda_stream)
+                         stream=stream.cuda_stream, sync=False)
 
     def run():
         shard.run_stream(range_chunk, N, rank, world, chunk, out, cnt, rec)
         shard.gather_slabs(out, cnt, g_out, g_cnt, world)
+        assert ctx.sync() == 0, "C5: a batch overflowed the block list"
 
     run()  # warm-up pass (allocations for the tail chunk)
     torch.cuda.synchronize()
@@ -328,9 +329,13 @@ def config_c3(args, ctx, dev, stream):
     d_offs = torch.from_numpy(offs).to(dev)
     out = torch.zeros(F3 * eng.out_stride * OUT_DTYPE.itemsize, dtype=torch.uint8, device=dev)
     cnt = torch.zeros(F3, dtype=torch.int32, device=dev)
-    step = lambda: eng.range_device(dL, dR, d_dets, d_offs, out, cnt, stream=stream.cuda_stream)  # noqa: E731
+    step = lambda: eng.range_device(dL, dR, d_dets, d_offs, out, cnt, stream=stream.cuda_stream,  # noqa: E731
+                                    sync=False)
     for _ in range(3):
         step()
+        ctx.sync()
+    step()
+    assert ctx.sync() == 0
     torch.cuda.synchronize()
     ctx.reset_counters()
     reps = max(3, min(args.steps, 10))
@@ -339,6 +344,7 @@ def config_c3(args, ctx, dev, stream):
     for _ in range(reps):
         step()
     e1.record(stream)
+    assert ctx.sync() == 0
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / reps
     evals, _ = ctx.work()
@@ -390,10 +396,10 @@ def config_c1_9x7(args, ctx, dev, stream):
     cnt = torch.zeros(F1, dtype=torch.int32, device=dev)
     step = lambda: eng.range_device(dL, dR, d_dets, d_offs, out, cnt, stream=stream.cuda_stream)  # noqa: E731
     for _ in range(3):
-        step()
+        step()  # sync=True: resubmits a batch that overflowed
     torch.cuda.synchronize()
     ctx.reset_counters()
-    ctx.set_profiling(True)
+    ctx.set_profiling(True)  # profiling: every batch blocks
     reps = max(3, min(args.steps, 10))
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
@@ -595,16 +601,19 @@ def main():
     stream = torch.cuda.Stream(dev)
     torch.cuda.set_stream(stream)
 
-    def range_chunk(glo, ghi, o, c):
-        eng.range_device(dL, dR, d_dets, d_offs, o, c, stream=stream.cuda_stream)
+    def range_chunk(glo, ghi, o, c):  # asynchronous; ctx.sync() after the timed loop
+        eng.range_device(dL, dR, d_dets, d_offs, o, c, stream=stream.cuda_stream, sync=False)
 
     def step():  # the shard's F frames, then the per-box results to every rank
         shard.run_stream(range_chunk, F * world, rank, world, F, d_out, d_cnt, rec)
         shard.gather_slabs(d_out, d_cnt, g_out, g_cnt, world)
 
-    # ---- warmup
+    # ---- warmup (a first batch that overflows grows the device block list)
     for _ in range(args.warmup):
         step()
+        ctx.sync()
+    step()
+    assert ctx.sync() == 0, "the block list still overflows after the warm-up"
     torch.cuda.synchronize()
 
     # ---- timed region (device-resident feed, default one-stream schedule)
@@ -620,6 +629,7 @@ def main():
         step()
     e1.record(stream)
     torch.cuda.synchronize()
+    overflow_in_timed = ctx.sync()  # 0: every timed batch produced its results
     if world > 1:
         dist.barrier()
     ms = e0.elapsed_time(e1)
@@ -633,6 +643,17 @@ def main():
     boxes_step = shard.gathered_boxes(g_cnt, F * world, world)
     value = boxes_step * args.steps / (ms_max / 1000.0)
     fps = F * args.steps * world / (ms_max / 1000.0)
+
+    # ---- kernel rooflines: the same steps with per-stage CUDA events
+    ctx.reset_counters()
+    ctx.set_profiling(True)
+    roof_steps = max(3, min(args.steps, 10))
+    for _ in range(roof_steps):
+        step()
+    torch.cuda.synchronize()
+    ctx.set_profiling(False)
+    stage_ms, stage_launches, _ = ctx.counters()
+    r_evals, _ = ctx.work()
 
     # ---- parity sweep: every ring frame of every rank, re-ranged by the
     # reference (oracle/_ref) on the host cores, vs the gathered records
@@ -650,17 +671,6 @@ def main():
         parity = {"checked_frames": int(pt[0]), "frame_mismatches": int(pt[1]), "box_mismatches": int(pt[2]),
                   "sample": "every ring frame of every rank (the timed step's output, after the gather)",
                   "checker": "reference (oracle/_ref, compiled in place)" if ra.have_reference() else "unavailable"}
-
-    # ---- kernel rooflines: the same steps with per-stage CUDA events
-    ctx.reset_counters()
-    ctx.set_profiling(True)
-    roof_steps = max(3, min(args.steps, 10))
-    for _ in range(roof_steps):
-        step()
-    torch.cuda.synchronize()
-    ctx.set_profiling(False)
-    stage_ms, stage_launches, _ = ctx.counters()
-    r_evals, _ = ctx.work()
 
     # ---- end-to-end through the public host API (pinned host frames, H2D/D2H inside)
     keep = []
@@ -897,6 +907,7 @@ def main():
                               "frac": (e2e_h2d_gbs / pcie_gbs) if pcie_gbs else None,
                               "peak_source": "measured here: pinned 256 MiB host->device copies, best of 6 x 16"}},
             "gpu_launches": int(total_launches),
+            "timed_batches_overflowed": bool(overflow_in_timed),
             "roofline": dominant,
             "kernels": {"census": census_roof, "matcher": match_roof,
                         "timing": f"per-stage CUDA events over {roof_steps} extra steps (one stream)",

@@ -254,10 +254,19 @@ rg_status rg_estimate_object_disparities(rg_ctx* ctx, const uint8_t* left,
  * census path).  Detections of frame f: dets[det_offsets[f] .. det_offsets[f+1]).
  * Results: out[f*out_stride + k] for k < out_count[f] (selected objects in
  * input order); out_stride >= min(max_dets_per_frame, cfg.max_objects).
- * All pointers are device pointers; the call is asynchronous on `stream`
- * except that it returns RG_EOVERFLOW when the previous call on this context
- * found its internal block list too small (the call is then re-run
- * synchronously with a grown list). */
+ * All pointers are device pointers.  The call is ASYNCHRONOUS on `stream`: it
+ * returns once the batch is enqueued (no host synchronisation); the batch's
+ * buffers must stay valid until the stream has run it.  Its planner counters
+ * come back asynchronously and are inspected by later calls and by rg_sync:
+ * a batch whose internal block list overflowed produced no results (its
+ * out_count entries are not written), the list grows for later batches, and
+ * the next rg_sync returns RG_EOVERFLOW -- resubmit that batch.  The list
+ * starts at 512 blocks per frame (C2 plans 496), so a steady workload
+ * overflows at most once.  Consecutive batches may use different streams
+ * (the library orders them); every other entry point waits for the
+ * context's pending batches first.  With rg_set_sync_mode(ctx, 1), or while
+ * profiling / the overlap schedule is on, the call blocks and re-runs an
+ * overflowed batch itself. */
 typedef struct {
   int32_t n_frames;
   int32_t width;
@@ -288,12 +297,46 @@ typedef struct {
 rg_status rg_range_frames(rg_ctx* ctx, const rg_frame_batch* batch,
                           const rg_ranger_config* cfg, void* stream);
 
+/* Wait for every asynchronous rg_range_frames batch of the context; returns
+ * RG_EOVERFLOW if any of them overflowed since the last rg_sync (those
+ * batches must be submitted again), else RG_OK. */
+rg_status rg_sync(rg_ctx* ctx);
+/* 1: rg_range_frames blocks until its batch is done and re-runs it itself on
+ * overflow (the behaviour before asynchronous batches); 0 (default): async. */
+rg_status rg_set_sync_mode(rg_ctx* ctx, int on);
+
 /* Host-buffer variant of rg_range_frames: left/right/dets/offsets/out/count are
  * HOST pointers (pinned memory recommended).  The library streams frames
  * through device staging in chunks of `chunk` frames with copy/compute
  * overlap and returns after the results are on the host. */
 rg_status rg_range_frames_host(rg_ctx* ctx, const rg_frame_batch* batch,
                                const rg_ranger_config* cfg, int chunk, void* stream);
+
+/* ------------------------------------------------- multi-GPU */
+/* Frames shard contiguously over devices: frame f of n runs on rank
+ * floor(f * world / n), i.e. [lo, hi) = [ceil(rank n / world), ceil((rank+1) n / world)). */
+rg_status rg_shard_bounds(int n_frames, int rank, int world, int* lo, int* hi);
+
+/* One context, stream pair and host thread per device, NCCL communicators over
+ * them (system libnccl.so.2, opened at create).  Devices must be distinct. */
+typedef struct rg_multi rg_multi;
+rg_status rg_multi_create(const int* devices, int n_devices, rg_multi** out);
+void rg_multi_destroy(rg_multi* m);
+const char* rg_multi_last_error(const rg_multi* m);
+
+/* A HOST batch (pointers as rg_range_frames_host; no left shift or out index)
+ * ranged with its frames sharded over the handle's devices: each device
+ * stages its shard (pinned host -> device copies overlapping its asynchronous
+ * batches of `chunk` frames) and ranges it; the per-box records are then
+ * gathered IN FRAME ORDER to d_out0 / d_count0 (DEVICE pointers on the first
+ * device, n_frames * out_stride records and n_frames counts; nullable) by
+ * NCCL send/recv, and/or copied to h_out / h_count (HOST, nullable) by each
+ * device over its own link.  Blocks until done.  Replaces the frame loop of
+ * Pipeline::run (pipeline.hpp:338-344) for the ranging stage; the sequential
+ * per-frame state stays with the caller. */
+rg_status rg_multi_range_host(rg_multi* m, const rg_frame_batch* batch, const rg_ranger_config* cfg, int chunk,
+                              rg_object_disparity* d_out0, int32_t* d_count0, rg_object_disparity* h_out,
+                              int32_t* h_count);
 
 /* ------------------------------------------------- sequence orchestration */
 

@@ -164,6 +164,8 @@ SIGNATURES = {
     "rg_build_info": (C.c_char_p, []),
     "rg_set_profiling": (I, [P, I]),
     "rg_set_overlap": (I, [P, I]),
+    "rg_sync": (I, [P]),
+    "rg_set_sync_mode": (I, [P, I]),
     "rg_get_counters": (I, [P, P, P, P]),
     "rg_reset_counters": (I, [P]),
     "rg_get_work": (I, [P, P, P]),
@@ -181,6 +183,11 @@ SIGNATURES = {
     "rg_estimate_object_disparities": (I, [P, P, P, I, I, P, I, P, P, D, D, P, P, P]),
     "rg_range_frames": (I, [P, P, P, P]),
     "rg_range_frames_host": (I, [P, P, P, I, P]),
+    "rg_shard_bounds": (I, [I, I, I, P, P]),
+    "rg_multi_create": (I, [P, I, P]),
+    "rg_multi_destroy": (None, [P]),
+    "rg_multi_last_error": (C.c_char_p, [P]),
+    "rg_multi_range_host": (I, [P, P, P, I, P, P, P, P]),
     "rg_rect_state_init": (I, [P, I, D]),
     "rg_filter_offset": (I, [P, I, P]),
     "rg_range_sequence": (I, [P, P, P, P, P, P, P, P, P]),

@@ -113,10 +113,19 @@ thread_local std::string g_create_err;
 
 enum Stage { ST_CENSUS = 0, ST_PLAN = 1, ST_MATCH = 2, ST_AGG = 3, ST_RECT = 4 };
 
-rg_status bind(rg_ctx* ctx) {
+rg_status retire_pending(rg_ctx* ctx, bool block);
+
+// Every entry point binds the context's device; all but rg_range_frames also
+// wait for its asynchronous batches (they share the internal buffers).
+rg_status bind(rg_ctx* ctx, bool wait_async = true) {
   if (!ctx) return RG_EINVAL;
   cudaError_t e = cudaSetDevice(ctx->device);
   if (e != cudaSuccess) return cuda_err(ctx, e, "cudaSetDevice");
+  if (wait_async && ctx->pend_n) {
+    const rg_status st = retire_pending(ctx, true);
+    if (st != RG_OK) return st;
+    ctx->last_stream = nullptr;
+  }
   return RG_OK;
 }
 
@@ -390,7 +399,8 @@ rg_status enqueue_match(rg_ctx* ctx, const FrameJob& J, const rg_ranger_config& 
   };
   uint32_t *fl = at(R.fl, R.gf), *fr = at(R.fr, R.gf), *sl = at(R.sl, R.gs), *sr = at(R.sr, R.gs);
   const int maxp = planner_max_points(cfg);
-  if (ctx->slot_capacity < F * 64) ctx->slot_capacity = F * 64;
+  // initial list: 512 potential blocks per frame (C2 plans 496); grows on overflow
+  if (ctx->slot_capacity < F * 512) ctx->slot_capacity = F * 512;
   const int capacity = ctx->slot_capacity;
   ObjEntry* objs = DBUF(ObjEntry, ctx, B_OBJ, (size_t)F * std::max(J.out_stride, 1));
   Slot* slots = DBUF(Slot, ctx, B_SLOTS, capacity);
@@ -487,6 +497,66 @@ rg_status run_pipeline(rg_ctx* ctx, const FrameJob& J, const rg_ranger_config& c
   NEED(hc);
   TRY(enqueue_pipeline(ctx, J, cfg, s, counters, pb));
   return finish_pipeline(ctx, J, cfg, s, counters, hc, pb);
+}
+
+// ---- asynchronous batches (rg_range_frames without host synchronisation)
+// Planner counters of an enqueued batch: retire them (stats, overflow ->
+// grown list for the following batches).  block = false stops at the first
+// batch still running.
+rg_status retire_pending(rg_ctx* ctx, bool block) {
+  while (ctx->pend_n > 0) {
+    rg_ctx::Pending& p = ctx->pend[ctx->pend_head];
+    if (block) {
+      RG_CUDA(ctx, cudaEventSynchronize(p.ev));
+    } else {
+      const cudaError_t q = cudaEventQuery(p.ev);
+      if (q == cudaErrorNotReady) break;
+      RG_CUDA(ctx, q);
+    }
+    const int32_t* hc = p.hc;
+    const int used = hc[0] + hc[4];
+    ctx->last_slots = used;
+    if (hc[1]) {
+      ++ctx->overflowed;
+      ctx->slot_capacity = std::max(ctx->slot_capacity * 2, used + used / 4 + 64);
+    } else {
+      int64_t ev;
+      std::memcpy(&ev, hc + 2, sizeof(ev));
+      ctx->hamming_evals += ev;
+      ctx->slots_total += used;
+    }
+    ctx->pend_head = (ctx->pend_head + 1) % rg_ctx::kPending;
+    --ctx->pend_n;
+  }
+  return RG_OK;
+}
+
+// Enqueue J on s without waiting: the counters go to a pinned slot of the
+// pending ring with an event; a batch on another stream than the previous
+// one is ordered after it (the internal rasters and lists are shared).
+rg_status run_pipeline_async(rg_ctx* ctx, const FrameJob& J, const rg_ranger_config& cfg, cudaStream_t s) {
+  if (ctx->pend_n == rg_ctx::kPending) {  // ring full: wait for the oldest batch
+    rg_ctx::Pending& p = ctx->pend[ctx->pend_head];
+    RG_CUDA(ctx, cudaEventSynchronize(p.ev));
+  }
+  TRY(retire_pending(ctx, false));  // grows the list early when a finished batch overflowed
+  if (!ctx->ev_last) RG_CUDA(ctx, cudaEventCreateWithFlags(&ctx->ev_last, cudaEventDisableTiming));
+  if (ctx->last_stream && ctx->last_stream != s) {
+    RG_CUDA(ctx, cudaEventRecord(ctx->ev_last, ctx->last_stream));
+    RG_CUDA(ctx, cudaStreamWaitEvent(s, ctx->ev_last, 0));
+  }
+  const int slot = (ctx->pend_head + ctx->pend_n) % rg_ctx::kPending;
+  rg_ctx::Pending& p = ctx->pend[slot];
+  if (!p.ev) RG_CUDA(ctx, cudaEventCreateWithFlags(&p.ev, cudaEventDisableTiming));
+  if (!p.hc) RG_CUDA(ctx, cudaMallocHost(&p.hc, kCounterInts * sizeof(int32_t)));
+  int32_t* counters = DBUF(int32_t, ctx, B_COUNTERS, kCounterInts);
+  NEED(counters);
+  TRY(enqueue_pipeline(ctx, J, cfg, s, counters, nullptr));
+  RG_CUDA(ctx, cudaMemcpyAsync(p.hc, counters, kCounterInts * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  RG_CUDA(ctx, cudaEventRecord(p.ev, s));
+  ++ctx->pend_n;
+  ctx->last_stream = s;
+  return RG_OK;
 }
 
 int census_stream_priority() {  // lowest priority: census CTAs fill what the matcher leaves
@@ -643,8 +713,14 @@ rg_status rg_ctx_create(int device, rg_ctx** out) {
 void rg_ctx_destroy(rg_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
+  retire_pending(ctx, true);
   for (cudaStream_t st : {ctx->stream, ctx->copy_stream, ctx->census_stream, ctx->match_stream})
     if (st) cudaStreamSynchronize(st);
+  for (auto& p : ctx->pend) {
+    if (p.ev) cudaEventDestroy(p.ev);
+    if (p.hc) cudaFreeHost(p.hc);
+  }
+  if (ctx->ev_last) cudaEventDestroy(ctx->ev_last);
   for (void* p : ctx->buf)
     if (p) cudaFree(p);
   for (void* p : ctx->hbuf)
@@ -1174,7 +1250,7 @@ rg_status rg_estimate_object_disparities(rg_ctx* ctx, const uint8_t* left, const
 rg_status rg_range_frames(rg_ctx* ctx, const rg_frame_batch* b, const rg_ranger_config* cfg,
                           void* stream) {
   RG_NVTX("rg_range_frames");
-  TRY(bind(ctx));
+  TRY(bind(ctx, false));
   TRY(check_cfg(ctx, cfg));
   if (!b || b->n_frames < 0 || b->width < 1 || b->height < 1 || b->pitch < b->width)
     return set_err(ctx, RG_EINVAL, "range_frames: bad batch");
@@ -1188,7 +1264,32 @@ rg_status rg_range_frames(rg_ctx* ctx, const rg_frame_batch* b, const rg_ranger_
   J.left_shift = b->d_left_shift;
   J.out_index = b->d_out_index;
   cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
-  return run_pipeline_overlapped(ctx, J, *cfg, s);
+  if (ctx->sync_mode || ctx->profiling || ctx->overlap) {  // blocking schedules (per-stage events, chunk joins)
+    TRY(rg_sync(ctx));
+    return run_pipeline_overlapped(ctx, J, *cfg, s);
+  }
+  return run_pipeline_async(ctx, J, *cfg, s);
+}
+
+rg_status rg_sync(rg_ctx* ctx) {  // (see also rg::wait_async)
+  TRY(bind(ctx));
+  TRY(retire_pending(ctx, true));
+  ctx->last_stream = nullptr;
+  if (ctx->overflowed) {
+    const int n = ctx->overflowed;
+    ctx->overflowed = 0;
+    return set_err(ctx, RG_EOVERFLOW,
+                   std::to_string(n) + " batch(es) overflowed the device block list and produced no results; "
+                   "the list has grown: submit them again");
+  }
+  return RG_OK;
+}
+
+rg_status rg_set_sync_mode(rg_ctx* ctx, int on) {
+  if (!ctx) return RG_EINVAL;
+  TRY(rg_sync(ctx));
+  ctx->sync_mode = on != 0;
+  return RG_OK;
 }
 
 rg_status rg_range_frames_host(rg_ctx* ctx, const rg_frame_batch* b, const rg_ranger_config* cfg,
@@ -1550,3 +1651,13 @@ rg_status rg_auto_rect_frames(rg_ctx* ctx, const uint8_t* d_left, const uint8_t*
 }
 
 }  // extern "C"
+
+namespace rg {
+// for entry points outside api.cu: wait for the context's asynchronous batches
+rg_status wait_async(rg_ctx* ctx) {
+  if (!ctx || !ctx->pend_n) return RG_OK;
+  const rg_status st = retire_pending(ctx, true);
+  ctx->last_stream = nullptr;
+  return st;
+}
+}  // namespace rg

@@ -271,6 +271,7 @@ extern "C" rg_status rg_render_frames_device(rg_ctx* ctx, const rg_scene_config*
     return set_err(ctx, RG_EINVAL, "render_frames_device: bad arguments");
   const cudaError_t e = cudaSetDevice(ctx->device);
   if (e != cudaSuccess) return cuda_err(ctx, e, "cudaSetDevice");
+  if (const rg_status w = wait_async(ctx)) return w;
   for (int f = 0; f < n_frames; ++f)
     if (obj_offsets[f + 1] < obj_offsets[f] || (obj_offsets[f + 1] > obj_offsets[f] && !objs))
       return set_err(ctx, RG_EINVAL, "render_frames_device: bad object offsets");

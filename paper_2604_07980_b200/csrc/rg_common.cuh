@@ -153,6 +153,19 @@ struct rg_ctx {
   // pinned host scratch
   void* hbuf[8] = {};
   size_t hcap[8] = {};
+  // asynchronous rg_range_frames: planner counters of batches still in
+  // flight, retired (stats, overflow, capacity growth) by the next calls or
+  // rg_sync; oldest first in a ring of kPending
+  static constexpr int kPending = 8;
+  struct Pending {
+    cudaEvent_t ev = nullptr;
+    int32_t* hc = nullptr;  // pinned copy of the batch's counters
+  } pend[kPending];
+  int pend_head = 0, pend_n = 0;
+  int overflowed = 0;            // retired batches that overflowed since the last rg_sync
+  int sync_mode = 0;             // 1: rg_range_frames blocks and re-runs on overflow (legacy)
+  cudaStream_t last_stream = nullptr;  // stream of the last asynchronous batch
+  cudaEvent_t ev_last = nullptr;       // orders a batch on another stream after it
 };
 
 namespace rg {
@@ -171,6 +184,7 @@ rg_status cuda_err(rg_ctx* ctx, cudaError_t e, const char* what);
 void* dev_buf(rg_ctx* ctx, int id, size_t bytes);  // nullptr on failure
 void* host_buf(rg_ctx* ctx, int id, size_t bytes);
 void count_launch(rg_ctx* ctx, int stage, int n = 1);
+rg_status wait_async(rg_ctx* ctx);  // blocks until the context's asynchronous batches are done
 
 #define RG_CUDA(ctx, expr)                                  \
   do {                                                      \

@@ -59,6 +59,7 @@ rg_status rg_range_sequence(rg_ctx* ctx, const rg_frame_batch* b, const rg_range
                             int32_t* out_delta, double* out_rect_applied, void* stream) {
   RG_NVTX("rg_range_sequence");
   if (!ctx) return RG_EINVAL;
+  if (cudaSetDevice(ctx->device) != cudaSuccess || wait_async(ctx) != RG_OK) return RG_ECUDA;
   if (!b || !cfg || !rect || !st) return fail(ctx, RG_EINVAL, "range_sequence: null argument");
   if (b->n_frames < 0 || b->width < 1 || b->height < 1)
     return fail(ctx, RG_EINVAL, "range_sequence: bad batch");

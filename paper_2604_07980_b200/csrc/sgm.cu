@@ -494,7 +494,7 @@ namespace {
 rg_status sgm_bind(rg_ctx* ctx) {
   if (!ctx) return RG_EINVAL;
   cudaError_t e = cudaSetDevice(ctx->device);
-  return e == cudaSuccess ? RG_OK : cuda_err(ctx, e, "cudaSetDevice");
+  return e == cudaSuccess ? wait_async(ctx) : cuda_err(ctx, e, "cudaSetDevice");
 }
 
 rg_status sgm_check(rg_ctx* ctx, const rg_sgm_params* p) {  // sgm.hpp:21-28

@@ -54,24 +54,44 @@ class FrameEngine:
         return _abi.FrameBatch(n_frames, self.w, self.h, pitch, stride, left, right, dets, offs, self.max_dets,
                                self.out_stride, out, cnt, self.focal, self.baseline, shift, out_index)
 
-    def range_device(self, left, right, dets, offsets, out, out_count, stream=None, left_shift=None) -> None:
-        """All arguments are CUDA torch tensors: left/right uint8 (F, H, pitch);
-        dets uint8 view of DET_DTYPE records; offsets int32 (F+1); out uint8
+    def range_device(self, left, right, dets, offsets, out, out_count, stream=None, left_shift=None,
+                     sync: bool = True) -> None:
+        """All arguments are CUDA torch tensors: left/right uint8 (F, H, pitch)
+        with unit column stride and the same strides on both sides; dets uint8
+        view of DET_DTYPE records; offsets int32 (F+1); out uint8
         (F * out_stride * 32); out_count int32 (F); left_shift int32 (F) or
-        None: per-frame shift_vertical of the left image (pipeline.hpp:135-138)."""
+        None: per-frame shift_vertical of the left image (pipeline.hpp:135-138).
+        rg_range_frames is asynchronous: sync=True waits (rg_sync) and
+        resubmits the batch once if its block list overflowed; sync=False
+        returns at once (call ctx.sync() before reading the results)."""
         F = left.shape[0]
-        pitch = left.shape[2] if left.dim() == 3 else self.w
+        if left.dim() == 3:
+            if left.stride(2) != 1 or tuple(right.stride()) != tuple(left.stride()) or right.shape != left.shape:
+                raise ValueError("range_device: left/right must have unit column stride and identical layouts")
+            pitch = left.stride(1)
+        else:
+            pitch = self.w
         b = self._batch(F, pitch, left.stride(0), left.data_ptr(), right.data_ptr(), dets.data_ptr(),
                         offsets.data_ptr(), out.data_ptr(), out_count.data_ptr(),
                         left_shift.data_ptr() if left_shift is not None else None)
         s = C.c_void_p(stream) if stream is not None else None
-        self.ctx.check(lib().rg_range_frames(self.ctx.handle, C.byref(b), C.byref(self._c), s))
+        for attempt in range(2):
+            self.ctx.check(lib().rg_range_frames(self.ctx.handle, C.byref(b), C.byref(self._c), s))
+            if not sync or self.ctx.sync() == _abi.RG_OK:
+                return
+        raise RuntimeError("rg_range_frames: block list overflow persisted after a resubmit")
 
     def range_host(self, left: np.ndarray, right: np.ndarray, dets: np.ndarray, offsets: np.ndarray,
                    out: np.ndarray, out_count: np.ndarray, chunk: int = 16, stream=None,
                    left_shift: Optional[np.ndarray] = None) -> None:
-        """Host (ideally pinned) numpy buffers; H2D / compute / D2H inside."""
+        """Host (ideally pinned) numpy buffers, C-contiguous (F, H, W) images;
+        H2D / compute / D2H inside."""
         F = left.shape[0]
+        for a in (left, right):
+            if a.shape != (F, self.h, self.w) or not a.flags.c_contiguous or a.dtype != np.uint8:
+                raise ValueError("range_host: images must be C-contiguous uint8 (F, H, W)")
+        if offsets.dtype != np.int32 or offsets.shape != (F + 1,) or not offsets.flags.c_contiguous:
+            raise ValueError("range_host: offsets must be contiguous int32 (F + 1)")
         if left_shift is not None:
             left_shift = np.ascontiguousarray(left_shift, np.int32)
             assert left_shift.shape == (F,)
@@ -170,3 +190,55 @@ class FrameEngine:
 def unpack_results(out: np.ndarray, counts: np.ndarray, out_stride: int) -> List[np.ndarray]:
     recs = np.frombuffer(out.tobytes(), dtype=OUT_DTYPE).reshape(-1, out_stride)
     return [recs[f, :int(counts[f])] for f in range(len(counts))]
+
+
+class MultiRanger:
+    """rg_multi_*: host frame batches sharded over several devices (one
+    context + host thread each); per-box records gathered in
+    frame order to the first device (NCCL send/recv) and/or the host."""
+
+    def __init__(self, devices: Sequence[int], width: int, height: int, cfg: RangerConfig, max_dets_per_frame: int,
+                 focal_px: float = 0.0, baseline_m: float = 0.0):
+        arr = (C.c_int * len(devices))(*devices)
+        h = C.c_void_p()
+        st = lib().rg_multi_create(arr, len(devices), C.byref(h))
+        if st != _abi.RG_OK:
+            raise RuntimeError(f"rg_multi_create failed ({st}): "
+                               f"{(lib().rg_multi_last_error(h) or b'').decode() if h.value else ''}")
+        self._h, self.devices = h, list(devices)
+        self.w, self.h, self.cfg, self._c = width, height, cfg, cfg.to_c()
+        self.max_dets = max_dets_per_frame
+        self.out_stride = max(1, min(max_dets_per_frame, cfg.max_objects))
+        self.focal, self.baseline = focal_px, baseline_m
+
+    def range_host(self, left: np.ndarray, right: np.ndarray, dets: np.ndarray, offsets: np.ndarray,
+                   out: Optional[np.ndarray] = None, out_count: Optional[np.ndarray] = None, d_out0=None,
+                   d_count0=None, chunk: int = 64) -> None:
+        """left/right C-contiguous uint8 (F, H, W) host arrays (pinned for full
+        PCIe rate); out/out_count host arrays and/or d_out0/d_count0 uint8 /
+        int32 CUDA tensors on the first device."""
+        F = left.shape[0]
+        for a in (left, right):
+            if a.shape != (F, self.h, self.w) or not a.flags.c_contiguous or a.dtype != np.uint8:
+                raise ValueError("MultiRanger.range_host: images must be C-contiguous uint8 (F, H, W)")
+        b = _abi.FrameBatch(F, self.w, self.h, self.w, self.w * self.h, left.ctypes.data, right.ctypes.data,
+                            dets.ctypes.data if dets.size else 0, offsets.ctypes.data, self.max_dets,
+                            self.out_stride, None, None, self.focal, self.baseline, None, None)
+        st = lib().rg_multi_range_host(self._h, C.byref(b), C.byref(self._c), chunk,
+                                       d_out0.data_ptr() if d_out0 is not None else None,
+                                       d_count0.data_ptr() if d_count0 is not None else None,
+                                       out.ctypes.data if out is not None else None,
+                                       out_count.ctypes.data if out_count is not None else None)
+        if st != _abi.RG_OK:
+            raise RuntimeError(f"rg_multi_range_host failed ({st}): {lib().rg_multi_last_error(self._h).decode()}")
+
+    def close(self) -> None:
+        if self._h:
+            lib().rg_multi_destroy(self._h)
+            self._h = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -93,8 +93,20 @@ class Context:
         self.check(lib().rg_set_profiling(self._h, 1 if on else 0))
 
     def set_overlap(self, on: bool) -> None:
-        """rg_range_frames schedule: chunked census/matcher overlap (default) or one stream."""
+        """rg_range_frames schedule: chunked census/matcher overlap (opt-in) or one stream (default)."""
         self.check(lib().rg_set_overlap(self._h, 1 if on else 0))
+
+    def sync(self) -> int:
+        """rg_sync: wait for the asynchronous rg_range_frames batches; returns
+        RG_OK or RG_EOVERFLOW (a batch produced no results: resubmit it)."""
+        st = lib().rg_sync(self._h)
+        if st not in (_abi.RG_OK, _abi.RG_EOVERFLOW):
+            self.check(st)
+        return st
+
+    def set_sync_mode(self, on: bool) -> None:
+        """rg_set_sync_mode: blocking rg_range_frames that re-runs overflowed batches itself."""
+        self.check(lib().rg_set_sync_mode(self._h, 1 if on else 0))
 
     def counters(self) -> Tuple[List[float], List[int], int]:
         t = (C.c_double * 5)()

@@ -322,3 +322,50 @@ def test_random_configs_both_matchers_match_oracle(ctx, chk, k):
         want = _want(chk, L[f], R[f], D[f], cfg)
         assert big[f] == want, (f, cfg)
         assert small[f] == want, (f, cfg)
+
+
+def test_multi_example_program():
+    """The multi-GPU entry as a C++ program (tests/dropin/multi_example.cpp):
+    frames sharded over every visible device, NCCL gather to device 0 and
+    host copies, byte-equal to one context's rg_range_frames_host."""
+    exe = os.path.join(ROOT, "tests", "dropin", "_bin", "multi_example")
+    if not os.path.exists(exe):
+        pytest.skip("multi example not built")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert "multi ok" in r.stdout and "mismatches 0" in r.stdout
+
+
+@pytest.mark.parametrize("name", ["c1", "c2"])
+def test_multi_ranger_matches_single_context_and_reference(ctx, chk, name):
+    """MultiRanger on device 0 (one-rank NCCL communicator): host records and
+    the device-0 gather equal FrameEngine.range_host and the reference."""
+    import torch
+    from paper_2604_07980_b200.engine import MultiRanger
+
+    mk = S.scene_c1 if name == "c1" else S.scene_c2
+    n = 9 if name == "c1" else 3
+    scenes = [mk(seed=40 + f, noise=2.0) for f in range(n)]
+    pairs = [S.render_stereo_pair(sc) for sc, _ in scenes]
+    L = np.ascontiguousarray(np.stack([p[0] for p in pairs]))
+    R = np.ascontiguousarray(np.stack([p[1] for p in pairs]))
+    D = [S.ground_truth_detections(sc) for sc, _ in scenes]
+    cfg = scenes[0][1]
+    recs, offs = pack_detections(D)
+    w, h = L.shape[2], L.shape[1]
+    mr = MultiRanger([0], w, h, cfg, max(len(d) for d in D), S.F_PX, S.BASELINE_M)
+    out = np.zeros(n * mr.out_stride, OUT_DTYPE)
+    cnt = np.zeros(n, np.int32)
+    d_out = torch.zeros(n * mr.out_stride * 32, dtype=torch.uint8, device="cuda:0")
+    d_cnt = torch.zeros(n, dtype=torch.int32, device="cuda:0")
+    mr.range_host(L, R, recs, offs, out, cnt, d_out, d_cnt, chunk=2)
+    mr.close()
+    eng = FrameEngine(w, h, cfg, max(len(d) for d in D), S.F_PX, S.BASELINE_M, ctx=ctx)
+    out1 = np.zeros(n * eng.out_stride, OUT_DTYPE)
+    cnt1 = np.zeros(n, np.int32)
+    eng.range_host(L, R, recs, offs, out1, cnt1, chunk=2)
+    assert cnt.tolist() == cnt1.tolist() == d_cnt.cpu().tolist()
+    assert out.tobytes() == out1.tobytes() == d_out.cpu().numpy().tobytes()
+    for f in range(n):
+        got = out.reshape(n, -1)[f][:cnt[f]]
+        assert got.tobytes() == _want(chk, L[f], R[f], D[f], cfg)

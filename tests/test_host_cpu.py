@@ -110,6 +110,18 @@ def test_shard_bounds_partition(n, world):
     assert seen == list(range(n))
 
 
+@pytest.mark.parametrize("n,world", [(1, 1), (7, 2), (4096, 8), (5, 8), (256, 3), (37, 4), (0, 3)])
+def test_c_abi_shard_bounds_equal_python(n, world):
+    """rg_shard_bounds (the library's multi-GPU split, csrc/multi.cu) is the
+    same contiguous partition as shard.shard_bounds."""
+    import ctypes as C
+    for r in range(world):
+        lo, hi = C.c_int(), C.c_int()
+        assert rg.lib().rg_shard_bounds(n, r, world, C.byref(lo), C.byref(hi)) == 0
+        assert (lo.value, hi.value) == shard.shard_bounds(n, r, world)
+    assert rg.lib().rg_shard_bounds(n, world, world, C.byref(C.c_int()), C.byref(C.c_int())) != 0
+
+
 def test_pack_detections_roundtrip():
     sc, cfg = S.scene_c1()
     dets = S.ground_truth_detections(sc)
