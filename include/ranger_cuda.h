@@ -516,6 +516,66 @@ rg_status rg_dense_objects(rg_ctx* ctx, const uint8_t* left, const uint8_t* righ
                            double sigma_sys2, rg_object_disparity* out, rg_box_stats* box_out,
                            int* n_out, int16_t* raw_out);
 
+/* ------------------------------------- radar (dense-map) refiner (8f row 3) */
+
+/* RadarDetection, synth.hpp:19-23 */
+typedef struct {
+  rg_vec3 position; /* vehicle frame, m */
+  rg_vec3 extent;   /* m */
+  int32_t id;
+  int32_t pad;
+} rg_radar_detection;
+
+/* VoteState, radar_refiner.hpp:30-47: bins cover [-K, K] px at 1/16 px
+ * (2K*16 + 1 bins, K <= 32 here). */
+#define RG_VOTE_MAX_BINS 1025
+typedef struct {
+  int32_t k_px;
+  int32_t n_bins;
+  double lambda;
+  double smooth_sigma_px;
+  double smoothed_offset;
+  double memory[RG_VOTE_MAX_BINS];
+} rg_vote_state;
+
+/* VoteState(k, lambda, sigma_px) (defaults 4, 0.3, 1.0); RG_EINVAL as the
+ * reference's constructor throws (K < 1, lambda outside (0, 1]) or K > 32. */
+rg_status rg_vote_state_init(rg_vote_state* st, int k_px, double lambda, double smooth_sigma_px);
+
+/* radar_refine_step (radar_refiner.hpp:111-167) on a DEVICE disparity map
+ * d_raw (w*h int16, DisparityMap::raw): radar_extent_box per detection on the
+ * host, the closest-offset search over each box on the device, the vote
+ * smoothing / EMA of `st` on the host (sequential state), then the clamped
+ * offset added to every valid raw value on the device.  *applied receives
+ * the offset the reference returns.  Radar detections behind the camera or
+ * without a projectable corner are skipped as in the reference. */
+rg_status rg_radar_refine_step(rg_ctx* ctx, int16_t* d_raw, int w, int h, const rg_radar_detection* radar, int n,
+                               rg_vote_state* st, const rg_calibration* calib, double* applied);
+
+/* Host halves of rg_radar_refine_step (used by it; exposed for tests):
+ * rg_radar_boxes -- per detection p_cam = imu_to_cam(position), skipped when
+ * p_cam.z <= 0 or radar_extent_box fails, else box (x0, y0, x1, y1 inclusive)
+ * and d_radar = f b / p_cam.z; *n_boxes of them.  rg_radar_vote_update --
+ * the votes of the boxes' closest offsets (found[i] != 0) into `st`
+ * (radar_refiner.hpp:129-155); *applied = clamp(smoothed offset, -3, 3),
+ * *raw_off = lround(applied * 16). */
+rg_status rg_radar_boxes(const rg_radar_detection* radar, int n, const rg_calibration* calib, int w, int h,
+                         int32_t* boxes, double* d_radar, int* n_boxes);
+rg_status rg_radar_vote_update(rg_vote_state* st, const double* best_off, const int32_t* found, int n_boxes,
+                               double* applied, int* raw_off);
+
+/* rg_dense_objects with the radar refiner between the dense map and the box
+ * statistics (pipeline.hpp:182-183, 207-224; the PipelineConfig default
+ * radar_refiner = true): radar (HOST, n_radar entries) of this frame, vote
+ * state carried by the caller from frame to frame, *radar_applied receives
+ * the refiner log's radar offset.  raw_out (optional) is the refined map. */
+rg_status rg_dense_objects_refined(rg_ctx* ctx, const uint8_t* left, const uint8_t* right, int w, int h,
+                                   const rg_detection* dets, int n, const rg_ranger_config* cfg,
+                                   const rg_bm_params* bm, double sigma_obs2, double gamma, double sigma_sys2,
+                                   const rg_radar_detection* radar, int n_radar, rg_vote_state* st,
+                                   const rg_calibration* calib, rg_object_disparity* out, rg_box_stats* box_out,
+                                   int* n_out, int16_t* raw_out, double* radar_applied);
+
 /* ------------------------------------------------------ SGM (8f row 2) */
 
 /* SgmParams, sgm.hpp:14-19 */

@@ -98,6 +98,11 @@ int ref_pipeline_records(const uint8_t* left, const uint8_t* right, int w, int h
                          const rg_rect_search_config* rect, const rg_record_params* rp, int method,
                          const rg_bm_params* bm, rg_object_disparity* out, int out_stride, int32_t* out_count,
                          rg_depth_record* recs, rg_refiner_log* logs);
+int ref_pipeline_dense_radar(const uint8_t* left, const uint8_t* right, int w, int h, int n_frames,
+                             const rg_detection* dets, const int32_t* det_offsets, const rg_radar_detection* radar,
+                             const int32_t* radar_offsets, const rg_ranger_config* cfg, const rg_calibration* cal,
+                             const rg_bm_params* bm, int k_px, double lambda, double sigma_px,
+                             rg_object_disparity* out, int out_stride, int32_t* out_count, double* radar_applied);
 int ref_save_synthetic_run(const rg_scene_config* sc, const rg_scene_object* objs, int n_obj, int n_frames,
                            double dt, const char* dir);
 int ref_run_directory(const char* dir, const char* out_dir, const rg_ranger_config* cfg,

@@ -678,6 +678,66 @@ int ref_pipeline_records(const uint8_t* left, const uint8_t* right, int w, int h
   });
 }
 
+/* Pipeline::process_frame with DepthMethod::kStereoBm and the radar
+ * (dense-map) refiner on (pipeline.hpp:69, 182-183, 207-224), rect search
+ * off: per frame the objects (box medians of the refined map) and the
+ * refiner log's radar offset.  radar: CSR (radar_offsets) of position +
+ * extent records. */
+int ref_pipeline_dense_radar(const uint8_t* left, const uint8_t* right, int w, int h, int n_frames,
+                             const rg_detection* dets, const int32_t* det_offsets, const rg_radar_detection* radar,
+                             const int32_t* radar_offsets, const rg_ranger_config* cfg, const rg_calibration* cal,
+                             const rg_bm_params* bm, int k_px, double lambda, double sigma_px,
+                             rg_object_disparity* out, int out_stride, int32_t* out_count, double* radar_applied) {
+  return guarded([&] {
+    PipelineConfig pc;
+    pc.method = DepthMethod::kStereoBm;
+    pc.bm = to_bm(bm);
+    Mat3 R;
+    for (int i = 0; i < 9; ++i) R.m[i] = cal->R[i];
+    pc.calib = make_calibration(cal->f, cal->b, cal->cx, cal->cy, cal->h_cam, R, Vec3{cal->t[0], cal->t[1], cal->t[2]});
+    pc.ranger = to_cfg(cfg);
+    pc.rect.enabled = false;
+    pc.radar_refiner = true;
+    pc.vote_half_range_px = k_px;
+    pc.vote_lambda = lambda;
+    pc.vote_smooth_sigma_px = sigma_px;
+    pc.workers = 1;
+    Pipeline pipe(pc);
+    const std::size_t img = std::size_t(w) * h;
+    for (int t = 0; t < n_frames; ++t) {
+      FrameInput in;
+      in.frame_id = t;
+      in.left = to_gray(left + img * t, w, h);
+      in.right = to_gray(right + img * t, w, h);
+      in.detections = to_dets(dets + det_offsets[t], det_offsets[t + 1] - det_offsets[t]);
+      for (int j = radar_offsets[t]; j < radar_offsets[t + 1]; ++j) {
+        RadarDetection r;
+        r.position = Vec3{radar[j].position.x, radar[j].position.y, radar[j].position.z};
+        r.extent = Vec3{radar[j].extent.x, radar[j].extent.y, radar[j].extent.z};
+        r.id = radar[j].id;
+        in.radar.push_back(r);
+      }
+      PipelineResult res;
+      pipe.process_frame(in, res);
+      int k = 0;
+      for (const auto& fo : res.objects) {
+        if (k >= out_stride) break;
+        rg_object_disparity& o = out[std::size_t(t) * out_stride + k];
+        std::memset(&o, 0, sizeof(o));
+        o.det_id = fo.obj.det_id;
+        o.kind = fo.obj.kind == ObjectKind::kFar ? RG_KIND_FAR : RG_KIND_CLOSE;
+        o.n_blocks_used = fo.obj.n_blocks_used;
+        o.valid = fo.obj.valid;
+        o.disparity = fo.obj.disparity;
+        ++k;
+      }
+      out_count[t] = k;
+      radar_applied[t] = res.refiner_log.back().radar_offset;
+    }
+    return RG_OK;
+  });
+}
+
 /* make_synthetic_frames + save_synthetic_run (pipeline.hpp:415-471): a
  * reference-written run directory. */
 int ref_save_synthetic_run(const rg_scene_config* sc, const rg_scene_object* objs, int n_obj, int n_frames,

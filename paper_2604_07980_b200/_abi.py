@@ -106,6 +106,19 @@ class Vec3(C.Structure):
     _fields_ = [("x", C.c_double), ("y", C.c_double), ("z", C.c_double)]
 
 
+class RadarDetection(C.Structure):
+    _fields_ = [("position", Vec3), ("extent", Vec3), ("id", C.c_int32), ("pad", C.c_int32)]
+
+
+RG_VOTE_MAX_BINS = 1025
+
+
+class VoteState(C.Structure):
+    _fields_ = [("k_px", C.c_int32), ("n_bins", C.c_int32), ("lambda_", C.c_double),
+                ("smooth_sigma_px", C.c_double), ("smoothed_offset", C.c_double),
+                ("memory", C.c_double * RG_VOTE_MAX_BINS)]
+
+
 class ObjRefinerState(C.Structure):
     _fields_ = [("prev_offset", C.c_double), ("beta", C.c_double), ("r_max", C.c_double), ("w_p", C.c_double),
                 ("tau", C.c_double), ("rate_limit", C.c_double)]
@@ -184,6 +197,11 @@ SIGNATURES = {
     "rg_range_frames": (I, [P, P, P, P]),
     "rg_range_frames_host": (I, [P, P, P, I, P]),
     "rg_shard_bounds": (I, [I, I, I, P, P]),
+    "rg_vote_state_init": (I, [P, I, D, D]),
+    "rg_radar_refine_step": (I, [P, P, I, I, P, I, P, P, P]),
+    "rg_radar_boxes": (I, [P, I, P, I, I, P, P, P]),
+    "rg_radar_vote_update": (I, [P, P, P, I, P, P]),
+    "rg_dense_objects_refined": (I, [P, P, P, I, I, P, I, P, P, D, D, D, P, I, P, P, P, P, P, P, P]),
     "rg_multi_create": (I, [P, I, P]),
     "rg_multi_destroy": (None, [P]),
     "rg_multi_last_error": (C.c_char_p, [P]),

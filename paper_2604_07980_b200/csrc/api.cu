@@ -1501,17 +1501,62 @@ rg_status rg_box_disparity(rg_ctx* ctx, const int16_t* raw, int w, int h, const 
   return RG_OK;
 }
 
-rg_status rg_dense_objects(rg_ctx* ctx, const uint8_t* left, const uint8_t* right, int w, int h,
-                           const rg_detection* dets, int n, const rg_ranger_config* cfg, const rg_bm_params* bm,
-                           double sigma_obs2, double gamma, double sigma_sys2, rg_object_disparity* out,
-                           rg_box_stats* box_out, int* n_out, int16_t* raw_out) {
+rg_status rg_radar_refine_step(rg_ctx* ctx, int16_t* d_raw, int w, int h, const rg_radar_detection* radar, int n,
+                               rg_vote_state* st, const rg_calibration* calib, double* applied) {
+  RG_NVTX("rg_radar_refine_step");
+  TRY(bind(ctx));
+  if (!d_raw || !st || !calib || w < 1 || h < 1 || n < 0 || (n > 0 && !radar))
+    return set_err(ctx, RG_EINVAL, "radar_refine_step: bad arguments");
+  std::vector<int32_t> boxes(4 * (size_t)std::max(n, 1));
+  std::vector<double> dr(std::max(n, 1));
+  int nb = 0;
+  if (rg_radar_boxes(radar, n, calib, w, h, boxes.data(), dr.data(), &nb) != RG_OK)
+    return set_err(ctx, RG_EINVAL, "radar_refine_step: bad radar detections");
+  std::vector<double> best(std::max(nb, 1), 0.0);
+  std::vector<int32_t> found(std::max(nb, 1), 0);
+  if (nb > 0) {  // the closest-offset search of every box on the device
+    int32_t* db = DBUF(int32_t, ctx, B_TMP0, 4 * (size_t)nb);
+    double* dd = DBUF(double, ctx, B_TMP1, 2 * (size_t)nb);
+    int32_t* df = DBUF(int32_t, ctx, B_TMP2, (size_t)nb);
+    NEED(db);
+    NEED(dd);
+    NEED(df);
+    RG_CUDA(ctx, cudaMemcpyAsync(db, boxes.data(), sizeof(int32_t) * 4 * nb, cudaMemcpyHostToDevice, ctx->stream));
+    RG_CUDA(ctx, cudaMemcpyAsync(dd, dr.data(), sizeof(double) * nb, cudaMemcpyHostToDevice, ctx->stream));
+    RG_CUDA(ctx, launch_radar_votes(d_raw, w, db, dd, nb, dd + nb, df, ctx->stream));
+    count_launch(ctx, ST_RECT);
+    RG_CUDA(ctx, cudaMemcpyAsync(best.data(), dd + nb, sizeof(double) * nb, cudaMemcpyDeviceToHost, ctx->stream));
+    RG_CUDA(ctx, cudaMemcpyAsync(found.data(), df, sizeof(int32_t) * nb, cudaMemcpyDeviceToHost, ctx->stream));
+    RG_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  }
+  double a = 0.0;
+  int raw_off = 0;
+  if (rg_radar_vote_update(st, best.data(), found.data(), nb, &a, &raw_off) != RG_OK)
+    return set_err(ctx, RG_EINVAL, "radar_refine_step: vote state not initialised");
+  if (raw_off != 0) {
+    RG_CUDA(ctx, launch_raw_offset(d_raw, (int64_t)w * h, raw_off, ctx->stream));
+    count_launch(ctx, ST_RECT);
+  }
+  if (applied) *applied = a;
+  return RG_OK;
+}
+
+rg_status rg_dense_objects_refined(rg_ctx* ctx, const uint8_t* left, const uint8_t* right, int w, int h,
+                                   const rg_detection* dets, int n, const rg_ranger_config* cfg,
+                                   const rg_bm_params* bm, double sigma_obs2, double gamma, double sigma_sys2,
+                                   const rg_radar_detection* radar, int n_radar, rg_vote_state* st,
+                                   const rg_calibration* calib, rg_object_disparity* out, rg_box_stats* box_out,
+                                   int* n_out, int16_t* raw_out, double* radar_applied) {
   RG_NVTX("rg_dense_objects");
   TRY(bind(ctx));
   TRY(check_cfg(ctx, cfg));
   TRY(check_bm(ctx, bm));
   if (!left || !right || !n_out || w < 1 || h < 1 || n < 0 || (n > 0 && (!dets || !out)))
     return set_err(ctx, RG_EINVAL, "dense_objects: bad arguments");
+  if (st && (!calib || n_radar < 0 || (n_radar > 0 && !radar)))
+    return set_err(ctx, RG_EINVAL, "dense_objects: radar refiner needs a calibration and the radar list");
   *n_out = 0;
+  if (radar_applied) *radar_applied = 0.0;
   // pipeline.hpp:140-141: the selected detections in input order
   std::vector<int32_t> sel(static_cast<size_t>(std::max(n, 1)));
   int ns = 0;
@@ -1525,12 +1570,15 @@ rg_status rg_dense_objects(rg_ctx* ctx, const uint8_t* left, const uint8_t* righ
   int16_t* draw = DBUF(int16_t, ctx, B_BM_OUT, (size_t)w * h);
   NEED(draw);
   TRY(bm_device(ctx, dl, dr, w, h, *bm, draw, ctx->stream));
+  // the radar refiner on the dense map (pipeline.hpp:182-183)
+  if (st) TRY(rg_radar_refine_step(ctx, draw, w, h, radar, n_radar, st, calib, radar_applied));
   if (raw_out)
     RG_CUDA(ctx, cudaMemcpyAsync(raw_out, draw, sizeof(int16_t) * w * h, cudaMemcpyDeviceToHost, ctx->stream));
   rg_detection* dd = nullptr;
   if (n > 0) TRY(upload_dets(ctx, dets, n, &dd));
   int lo = 0, hi = 0;
   bm_raw_range(*bm, &lo, &hi);
+  if (st) lo = std::max(-32767, lo - 48), hi = std::min(32767, hi + 48);  // the refiner's offset is within +-3 px
   std::vector<rg_box_stats> res;
   TRY(box_stats_device(ctx, draw, w, h, dd, sel, lo, hi, sigma_obs2, gamma, sigma_sys2, res));
   // pipeline.hpp:218-224
@@ -1548,6 +1596,14 @@ rg_status rg_dense_objects(rg_ctx* ctx, const uint8_t* left, const uint8_t* righ
   }
   *n_out = ns;
   return RG_OK;
+}
+
+rg_status rg_dense_objects(rg_ctx* ctx, const uint8_t* left, const uint8_t* right, int w, int h,
+                           const rg_detection* dets, int n, const rg_ranger_config* cfg, const rg_bm_params* bm,
+                           double sigma_obs2, double gamma, double sigma_sys2, rg_object_disparity* out,
+                           rg_box_stats* box_out, int* n_out, int16_t* raw_out) {
+  return rg_dense_objects_refined(ctx, left, right, w, h, dets, n, cfg, bm, sigma_obs2, gamma, sigma_sys2, nullptr,
+                                  0, nullptr, nullptr, out, box_out, n_out, raw_out, nullptr);
 }
 
 static rg_status check_rect(rg_ctx* ctx, int w, int h, const rg_rect* roi, int dmin, int dmax,

@@ -116,7 +116,76 @@ __global__ void __launch_bounds__(kBoxThreads) box_disparity_kernel(
   }
 }
 
+// radar_refine_step's vote search (radar_refiner.hpp:117-131): per radar
+// detection, the valid map pixel of its projected extent box whose offset
+// d_radar - disparity is closest to zero (ties: the smaller offset).  The key
+// (|off|, off) is a total order, so the block reduction is order-free; the
+// offsets are exact FP64 (raw / 16 is exact).
+constexpr int kVoteThreads = 256;
+__global__ void __launch_bounds__(kVoteThreads) radar_vote_kernel(const int16_t* __restrict__ raw, int w,
+                                                                 const int32_t* __restrict__ boxes,
+                                                                 const double* __restrict__ d_radar,
+                                                                 double* __restrict__ best_off,
+                                                                 int32_t* __restrict__ found) {
+  __shared__ double s_off[kVoteThreads];
+  __shared__ int s_ok[kVoteThreads];
+  const int b = blockIdx.x;
+  const int x0 = boxes[4 * b], y0 = boxes[4 * b + 1], x1 = boxes[4 * b + 2], y1 = boxes[4 * b + 3];
+  const double dr = d_radar[b];
+  const int bw = x1 - x0 + 1, n = bw * (y1 - y0 + 1);
+  double best = 0.0;
+  int ok = 0;
+  for (int i = threadIdx.x; i < n; i += kVoteThreads) {
+    const int y = y0 + i / bw, x = x0 + i % bw;
+    const int r = raw[(int64_t)y * w + x];
+    if (r == kInvalidRaw) continue;
+    const double off = __dsub_rn(dr, __dmul_rn((double)r, 0.0625));  // raw / 16.0 (DisparityMap::disparity)
+    if (!ok || fabs(off) < fabs(best) || (fabs(off) == fabs(best) && off < best)) best = off, ok = 1;
+  }
+  s_off[threadIdx.x] = best;
+  s_ok[threadIdx.x] = ok;
+  __syncthreads();
+  for (int st = kVoteThreads / 2; st > 0; st >>= 1) {
+    if (threadIdx.x < st) {
+      const double a = s_off[threadIdx.x], c = s_off[threadIdx.x + st];
+      const int oa = s_ok[threadIdx.x], oc = s_ok[threadIdx.x + st];
+      if (oc && (!oa || fabs(c) < fabs(a) || (fabs(c) == fabs(a) && c < a))) {
+        s_off[threadIdx.x] = c;
+        s_ok[threadIdx.x] = 1;
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    best_off[b] = s_off[0];
+    found[b] = s_ok[0];
+  }
+}
+
+// radar_refine_step's map update (radar_refiner.hpp:157-165): every valid raw
+// value + raw_off, clamped to [INT16_MIN + 1, INT16_MAX].
+__global__ void raw_offset_kernel(int16_t* __restrict__ raw, int64_t n, int raw_off) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int r = raw[i];
+    if (r == kInvalidRaw) continue;
+    raw[i] = (int16_t)min(max(r + raw_off, -32767), 32767);
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_radar_votes(const int16_t* raw, int w, const int32_t* boxes, const double* d_radar, int n,
+                               double* best_off, int32_t* found, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  radar_vote_kernel<<<n, kVoteThreads, 0, s>>>(raw, w, boxes, d_radar, best_off, found);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_raw_offset(int16_t* raw, int64_t n, int raw_off, cudaStream_t s) {
+  if (n <= 0 || raw_off == 0) return cudaSuccess;
+  raw_offset_kernel<<<592, 256, 0, s>>>(raw, n, raw_off);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_box_disparity(const int16_t* raw, int w, int h, int64_t frame_stride, const rg_detection* dets,
                                  const int32_t* box_det, const int32_t* box_frame, int n_boxes, int raw_lo,

@@ -9,6 +9,7 @@
 // -ffp-contract=off), so the records are bit-identical.
 #include <algorithm>
 #include <cmath>
+#include <cstring>
 #include <limits>
 #include <stdexcept>
 #include <tuple>
@@ -245,6 +246,115 @@ rg_status rg_frame_records(const rg_record_params* p, int frame_id, int img_w, i
   } catch (const std::exception&) {
     return RG_EINVAL;
   }
+  return RG_OK;
+}
+
+// ---------------------------------------------------------------- radar refiner
+// Host halves of radar_refine_step (radar_refiner.hpp:49-167); the pixel
+// search and the map update run on the device (dense.cu).
+
+rg_status rg_vote_state_init(rg_vote_state* st, int k_px, double lambda, double smooth_sigma_px) {
+  if (!st) return RG_EINVAL;
+  if (k_px < 1 || lambda <= 0 || lambda > 1) return RG_EINVAL;  // VoteState ctor throws
+  if (2 * k_px * 16 + 1 > RG_VOTE_MAX_BINS) return RG_EINVAL;
+  std::memset(st, 0, sizeof(*st));
+  st->k_px = k_px;
+  st->n_bins = 2 * k_px * 16 + 1;
+  st->lambda = lambda;
+  st->smooth_sigma_px = smooth_sigma_px;
+  return RG_OK;
+}
+
+rg_status rg_radar_boxes(const rg_radar_detection* radar, int n, const rg_calibration* calib, int w, int h,
+                         int32_t* boxes, double* d_radar, int* n_boxes) {
+  if (!calib || !n_boxes || n < 0 || (n > 0 && (!radar || !boxes || !d_radar))) return RG_EINVAL;
+  const rg_calibration& c = *calib;
+  int m = 0;
+  for (int i = 0; i < n; ++i) {
+    const rg_radar_detection& det = radar[i];
+    const V3 pc = imu_to_cam(V3{det.position.x, det.position.y, det.position.z}, c);
+    if (pc.z <= 0) continue;
+    const double dr = c.f * c.b / pc.z;
+    // detail::radar_extent_box (radar_refiner.hpp:71-100)
+    double u_min = std::numeric_limits<double>::infinity(), u_max = -u_min, v_min = u_min, v_max = -u_min;
+    int np = 0;
+    for (int k = 0; k < 8; ++k) {
+      const V3 corner{det.position.x + (k & 1 ? 0.5 : -0.5) * det.extent.x,
+                      det.position.y + (k & 2 ? 0.5 : -0.5) * det.extent.y,
+                      det.position.z + (k & 4 ? 0.5 : -0.5) * det.extent.z};
+      const V3 p = imu_to_cam(corner, c);
+      if (p.z <= 0) continue;
+      const double u = c.cx + c.f * p.x / p.z, v = c.cy + c.f * p.y / p.z;
+      u_min = std::min(u_min, u);
+      u_max = std::max(u_max, u);
+      v_min = std::min(v_min, v);
+      v_max = std::max(v_max, v);
+      ++np;
+    }
+    if (np == 0) continue;
+    const int x0 = std::max(0, int(std::floor(u_min))), x1 = std::min(w - 1, int(std::ceil(u_max)));
+    const int y0 = std::max(0, int(std::floor(v_min))), y1 = std::min(h - 1, int(std::ceil(v_max)));
+    if (!(x0 <= x1 && y0 <= y1)) continue;
+    boxes[4 * m] = x0, boxes[4 * m + 1] = y0, boxes[4 * m + 2] = x1, boxes[4 * m + 3] = y1;
+    d_radar[m] = dr;
+    ++m;
+  }
+  *n_boxes = m;
+  return RG_OK;
+}
+
+rg_status rg_radar_vote_update(rg_vote_state* st, const double* best_off, const int32_t* found, int n_boxes,
+                               double* applied, int* raw_off) {
+  if (!st || st->n_bins != 2 * st->k_px * 16 + 1 || n_boxes < 0 || (n_boxes > 0 && (!best_off || !found)))
+    return RG_EINVAL;
+  const int bins = st->n_bins;
+  std::vector<double> votes(bins, 0.0);
+  int n_votes = 0;
+  for (int i = 0; i < n_boxes; ++i) {
+    const double best = best_off[i];
+    if (!found[i] || std::abs(best) > st->k_px) continue;
+    const int bin = std::clamp(int(std::lround((best + st->k_px) * 16)), 0, bins - 1);
+    votes[bin] += 1.0;  // one vote per detection
+    ++n_votes;
+  }
+  if (n_votes > 0) {
+    // detail::gaussian_smooth_bins (radar_refiner.hpp:51-69)
+    std::vector<double> sm;
+    const double sigma_bins = st->smooth_sigma_px * 16;
+    if (sigma_bins <= 0) {
+      sm = votes;
+    } else {
+      const int radius = std::max(1, int(std::ceil(3 * sigma_bins)));
+      std::vector<double> kernel(2 * radius + 1);
+      double sum = 0;
+      for (int i = -radius; i <= radius; ++i) {
+        kernel[i + radius] = std::exp(-0.5 * (i / sigma_bins) * (i / sigma_bins));
+        sum += kernel[i + radius];
+      }
+      for (auto& k : kernel) k /= sum;
+      sm.assign(bins, 0.0);
+      for (int i = 0; i < bins; ++i) {
+        if (votes[i] == 0) continue;
+        for (int j = -radius; j <= radius; ++j) {
+          const int t = i + j;
+          if (t >= 0 && t < bins) sm[t] += votes[i] * kernel[j + radius];
+        }
+      }
+    }
+    double l1 = 0;
+    for (double v : sm) l1 += v;
+    if (l1 > 0)
+      for (auto& v : sm) v /= l1;
+    for (int i = 0; i < bins; ++i) st->memory[i] = (1 - st->lambda) * st->memory[i] + st->lambda * sm[i];
+    int best_bin = 0;
+    for (int i = 1; i < bins; ++i)
+      if (st->memory[i] > st->memory[best_bin]) best_bin = i;
+    const double d_star = best_bin / 16.0 - st->k_px;  // VoteState::bin_center
+    st->smoothed_offset = (1 - st->lambda) * st->smoothed_offset + st->lambda * d_star;
+  }
+  const double a = std::clamp(st->smoothed_offset, -3.0, 3.0);
+  if (applied) *applied = a;
+  if (raw_off) *raw_off = int(std::lround(a * 16));  // DisparityMap::kSubLevels
   return RG_OK;
 }
 

@@ -234,6 +234,9 @@ cudaError_t launch_match_slots(const Slot* slots, int32_t* counters, int slot_ca
                                int n_frames = 0);
 
 // box statistics of dense maps (dense.cu)
+cudaError_t launch_radar_votes(const int16_t* raw, int w, const int32_t* boxes, const double* d_radar, int n,
+                               double* best_off, int32_t* found, cudaStream_t s);
+cudaError_t launch_raw_offset(int16_t* raw, int64_t n, int raw_off, cudaStream_t s);
 cudaError_t launch_box_disparity(const int16_t* raw, int w, int h, int64_t frame_stride, const rg_detection* dets,
                                  const int32_t* box_det, const int32_t* box_frame, int n_boxes, int raw_lo,
                                  int nbins, double sigma_obs2, double gamma, double sigma_sys2,

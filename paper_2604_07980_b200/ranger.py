@@ -672,6 +672,65 @@ def dense_objects(left, right, dets: Sequence[Detection], cfg: RangerConfig, bm:
     return objs, boxes, raw
 
 
+class VoteState:
+    """VoteState (radar_refiner.hpp:30-47): the radar refiner's vote memory,
+    carried from frame to frame by the caller (defaults K 4, lambda 0.3,
+    sigma 1 px)."""
+
+    def __init__(self, k_px: int = 4, lam: float = 0.3, smooth_sigma_px: float = 1.0):
+        self._c = _abi.VoteState()
+        if lib().rg_vote_state_init(C.byref(self._c), k_px, lam, smooth_sigma_px) != _abi.RG_OK:
+            raise InvalidArgument("VoteState: K must be >= 1 (<= 32 here) and lambda in (0, 1]")
+
+    @property
+    def smoothed_offset(self) -> float:
+        return self._c.smoothed_offset
+
+    @property
+    def memory(self) -> np.ndarray:
+        return np.array(self._c.memory[:self._c.n_bins])
+
+    def to_c(self) -> _abi.VoteState:
+        return self._c
+
+
+def radar_array(radar):
+    """[(position (x, y, z), extent (x, y, z), id)] -> rg_radar_detection array."""
+    return (_abi.RadarDetection * max(len(radar), 1))(
+        *[_abi.RadarDetection(_abi.Vec3(*p), _abi.Vec3(*e), int(i), 0) for p, e, i in radar])
+
+
+def dense_objects_refined(left, right, dets: Sequence[Detection], cfg: RangerConfig, bm: "BmParams", radar,
+                          vote: VoteState, calib: "Calibration", var: Optional["DenseVarianceParams"] = None,
+                          ctx: Optional[Context] = None):
+    """dense_objects with the radar (dense-map) refiner between the BM map and
+    the box statistics (pipeline.hpp:182-183; PipelineConfig::radar_refiner
+    defaults to true).  radar: [(position, extent, id)] of this frame (vehicle
+    frame); vote: the VoteState carried across frames.  Returns ([ObjectDisparity],
+    [Optional[BoxDisparity]], refined raw map, radar offset applied)."""
+    ctx = ctx or default_context()
+    var = var or DenseVarianceParams()
+    L, R = _gray(left), _gray(right)
+    h, w = L.shape
+    arr = dets_array(dets)
+    n = len(dets)
+    out = (_abi.ObjectDisparity * max(n, 1))()
+    box = (_abi.BoxStats * max(n, 1))()
+    n_out = C.c_int()
+    raw = np.empty((h, w), np.int16)
+    applied = C.c_double()
+    c, b = cfg.to_c(), bm.to_c()
+    ra = radar_array(radar)
+    ctx.check(lib().rg_dense_objects_refined(ctx.handle, _ptr(L), _ptr(R), w, h, arr, n, C.byref(c), C.byref(b),
+                                             float(var.sigma_obs2), float(var.gamma), float(var.sigma_sys2), ra,
+                                             len(radar), C.byref(vote.to_c()), C.byref(calib.to_c()), out, box,
+                                             C.byref(n_out), _ptr(raw), C.byref(applied)))
+    objs = [ObjectDisparity(o.det_id, o.disparity, o.kind, o.n_blocks_used, bool(o.valid), o.z_cam)
+            for o in list(out)[:n_out.value]]
+    boxes = [BoxDisparity(x.median, x.variance, x.count) if x.valid > 0 else None for x in list(box)[:n_out.value]]
+    return objs, boxes, raw, applied.value
+
+
 @dataclass
 class SgmParams:
     """sgm.hpp:14-19 with the reference's defaults."""

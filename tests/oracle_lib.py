@@ -59,6 +59,8 @@ class Checker:
             self.lib.ref_run_directory.argtypes = [C.c_char_p, C.c_char_p, P, P, I, D]
             self.lib.ref_dynamic_disparity_variance.restype = I
             self.lib.ref_dynamic_disparity_variance.argtypes = [P, I, P, I, D, D, D, P]
+            self.lib.ref_pipeline_dense_radar.restype = I
+            self.lib.ref_pipeline_dense_radar.argtypes = [P, P, I, I, I, P, P, P, P, P, P, P, I, D, D, P, I, P, P]
             self.lib.ref_bench_estimate.restype = D
             self.lib.ref_bench_estimate.argtypes = [P, P, I, I, I, P, P, P, I, P, I, P]
 

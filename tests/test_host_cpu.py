@@ -138,3 +138,27 @@ def test_scene_configs_shapes():
         assert len(dets) == n
         kinds = [rg.classify_far_close(d, sc.width, sc.height, cfg.tau_s) for d in dets]
         assert kinds.count(rg.KIND_FAR) == far
+
+
+def test_vote_state_init_validates_like_the_reference():  # radar_refiner.hpp:37-43
+    v = rg.VoteState(4, 0.3, 1.0)
+    assert v.to_c().n_bins == 129 and v.smoothed_offset == 0.0 and not v.memory.any()
+    for bad in ((0, 0.3, 1.0), (4, 0.0, 1.0), (4, 1.5, 1.0), (33, 0.3, 1.0)):
+        with pytest.raises(rg.InvalidArgument):
+            rg.VoteState(*bad)
+
+
+def test_radar_vote_update_host_half():
+    """rg_radar_vote_update: one vote at offset +1 px -> the EMA moves toward
+    +1 (radar_refiner.hpp:129-155); no votes leave the state untouched."""
+    import ctypes as C
+    v = rg.VoteState()
+    a, off = C.c_double(), C.c_int()
+    best = (C.c_double * 1)(1.0)
+    found = (C.c_int32 * 1)(1)
+    assert rg.lib().rg_radar_vote_update(C.byref(v.to_c()), best, found, 1, C.byref(a), C.byref(off)) == 0
+    assert a.value == 0.3 * 1.0 and off.value == round(0.3 * 16)
+    before = v.smoothed_offset
+    found[0] = 0
+    assert rg.lib().rg_radar_vote_update(C.byref(v.to_c()), best, found, 1, C.byref(a), C.byref(off)) == 0
+    assert v.smoothed_offset == before

@@ -239,3 +239,65 @@ def test_dense_objects_match_oracle(ctx, orc, bs, nd, dmin, ds):
                 assert np.float64(objs[k].disparity).tobytes() == np.float64(stt[k].median).tobytes()
                 assert np.float64(boxes[k].variance).tobytes() == np.float64(stt[k].variance).tobytes()
                 assert boxes[k].count == stt[k].count == objs[k].n_blocks_used
+
+
+def _radar_frames(n, bias):
+    Ls, Rs, D, RA, scs = [], [], [], [], []
+    for t in range(n):
+        sc, cfg = S.scene_c1(seed=90 + t, noise=2.0)
+        sc.disparity_bias_px = bias
+        L, R = S.render_stereo_pair(sc)
+        Ls.append(L)
+        Rs.append(R)
+        D.append(S.ground_truth_detections(sc))
+        # simulate_radar without noise (synth.hpp:234-249): extent = (depth, width, height)
+        RA.append([(o.position, (o.depth_m, o.width_m, o.height_m), o.id) for o in sc.objects])
+        scs.append(sc)
+    return np.stack(Ls), np.stack(Rs), D, RA, cfg, scs[0]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("bias", [0.0, 1.5, -2.25])
+def test_dense_radar_refiner_matches_reference_pipeline(ctx, bias):
+    """STEREO_BM with the radar refiner on (PipelineConfig::radar_refiner
+    default, pipeline.hpp:69, 182-183): per frame the box medians of the
+    refined map and the refiner's radar offset equal the reference Pipeline's,
+    the vote state carried across frames (radar_refiner.hpp:111-167)."""
+    if not oracle_lib.have_reference():
+        pytest.skip("oracle/_ref not built")
+    ref = oracle_lib.reference()
+    n = 6
+    L, R, D, RA, cfg, sc = _radar_frames(n, bias)
+    h, w = L.shape[1:]
+    bm = rg.BmParams(32, 9, 0, 10, 10, 1)  # PipelineConfig::bm defaults
+    calib = rg.Calibration(sc.f, sc.b, w / 2.0, h / 2.0, sc.h_cam)
+    vote = rg.VoteState()
+    got, got_applied = [], []
+    for t in range(n):
+        objs, _, _, a = rg.dense_objects_refined(L[t], R[t], D[t], cfg, bm, RA[t], vote, calib, ctx=ctx)
+        got.append([(o.det_id, o.kind, o.n_blocks_used, int(o.valid), o.disparity) for o in objs])
+        got_applied.append(a)
+    recs, offs = [], [0]
+    for d in D:
+        recs.extend(cdet(x) for x in d)
+        offs.append(len(recs))
+    arr = (_abi.Detection * len(recs))(*recs)
+    offs = np.asarray(offs, np.int32)
+    flat = [r for fr in RA for r in fr]
+    rarr = rg.radar_array(flat)
+    roffs = np.cumsum([0] + [len(fr) for fr in RA]).astype(np.int32)
+    stride = max(len(d) for d in D)
+    out = (_abi.ObjectDisparity * (n * stride))()
+    cnt = np.zeros(n, np.int32)
+    applied = np.zeros(n)
+    assert ref.lib.ref_pipeline_dense_radar(L.ctypes.data, R.ctypes.data, w, h, n, C.addressof(arr), offs.ctypes.data,
+                                            C.addressof(rarr), roffs.ctypes.data, C.byref(cfg.to_c()),
+                                            C.byref(calib.to_c()), C.byref(bm.to_c()), 4, 0.3, 1.0, C.addressof(out),
+                                            stride, cnt.ctypes.data, applied.ctypes.data) == 0
+    for t in range(n):
+        want = [(o.det_id, o.kind, o.n_blocks_used, o.valid, o.disparity)
+                for o in list(out)[t * stride:t * stride + cnt[t]]]
+        assert got[t] == want, t
+    assert np.array(got_applied).tobytes() == applied.tobytes()
+    if bias != 0.0:
+        assert abs(applied[-1]) > 0.1  # the refiner acted
