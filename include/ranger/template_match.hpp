@@ -167,6 +167,24 @@ struct RangerStats {
   int n_close = 0;
 };
 
+namespace detail {
+
+/// template_match.hpp:243-255: the census ROI of a box in a raster scaled by
+/// (sx, sy) -- floor/ceil of the scaled edges, dilated, clipped to w x h (the
+/// right/bottom edges half-open, hence the + 1).  The device path computes
+/// the same rows (census_rows_kernel); this helper keeps the API surface.
+inline void add_roi(std::vector<CensusRoi>& rois, const PixelBox& b, double sx, double sy, int dilate_x,
+                    int dilate_y, int w, int h) {
+  CensusRoi r;
+  r.x0 = std::max(0, int(std::floor(b.x0 * sx)) - dilate_x);
+  r.y0 = std::max(0, int(std::floor(b.y0 * sy)) - dilate_y);
+  r.x1 = std::min(w, int(std::ceil(b.x1 * sx)) + dilate_x + 1);
+  r.y1 = std::min(h, int(std::ceil(b.y1 * sy)) + dilate_y + 1);
+  rois.push_back(r);
+}
+
+}  // namespace detail
+
 /// template_match.hpp:260-363 -> rg_estimate_object_disparities (whole frame on device)
 inline std::vector<ObjectDisparity> estimate_object_disparities(const GrayImage& left, const GrayImage& right,
                                                                 const std::vector<Detection>& dets,
@@ -185,12 +203,28 @@ inline std::vector<ObjectDisparity> estimate_object_disparities(const GrayImage&
   rg_census_cache cc{};
   const int cw = w / cfg.close_scale, ch = h / cfg.close_scale;
   std::vector<std::uint32_t> fl, fr, sl, sr;
+  // A pre-filled cache whose images are not w x h (or the CLOSE scale) is
+  // laid out on the frame's raster with zeros outside its extent: the
+  // reference drops samples that are not inside() the cached image exactly
+  // like undefined (0) codes (census.hpp:195-216), and the device path reads
+  // w*h (cw*ch) codes.
+  std::vector<std::uint32_t> rl[4];
+  // (rg_census_cache points are writable for the fill case; pre-filled codes are only read)
+  auto fit = [](const CensusImage& img, int ww, int hh, std::vector<std::uint32_t>& buf) -> std::uint32_t* {
+    if (img.width == ww && img.height == hh && img.codes.size() == std::size_t(ww) * hh)
+      return const_cast<std::uint32_t*>(img.codes.data());
+    buf.assign(std::size_t(std::max(ww, 0)) * std::max(hh, 0), 0u);
+    for (int y = 0; y < std::min(hh, img.height); ++y)
+      for (int x = 0; x < std::min(ww, img.width); ++x)
+        if (std::size_t(y) * img.width + x < img.codes.size()) buf[std::size_t(y) * ww + x] = img.code(x, y);
+    return buf.data();
+  };
   if (cache) {
     cc.has_full = cache->has_full;
     cc.has_scaled = cache->has_scaled;
     if (cache->has_full) {
-      cc.full_left = cache->full_left.codes.data();
-      cc.full_right = cache->full_right.codes.data();
+      cc.full_left = fit(cache->full_left, w, h, rl[0]);
+      cc.full_right = fit(cache->full_right, w, h, rl[1]);
     } else {
       fl.assign(std::size_t(w) * h, 0);
       fr.assign(std::size_t(w) * h, 0);
@@ -198,8 +232,8 @@ inline std::vector<ObjectDisparity> estimate_object_disparities(const GrayImage&
       cc.full_right = fr.data();
     }
     if (cache->has_scaled) {
-      cc.scaled_left = cache->scaled_left.codes.data();
-      cc.scaled_right = cache->scaled_right.codes.data();
+      cc.scaled_left = fit(cache->scaled_left, cw, ch, rl[2]);
+      cc.scaled_right = fit(cache->scaled_right, cw, ch, rl[3]);
     } else {
       sl.assign(std::size_t(std::max(cw, 0)) * std::max(ch, 0), 0);
       sr.assign(sl.size(), 0);

@@ -645,9 +645,11 @@ rg_status rg_render_stereo_pair(const rg_scene_config* cfg, const rg_scene_objec
  * 8(f) row 4).  cfgs[f] and objs[obj_offsets[f] .. obj_offsets[f+1]) are HOST
  * arrays; every frame must share width and height.  d_left / d_right receive
  * frame f at f * frame_stride as dense rows of `width` bytes.  Enqueued on
- * `stream` (NULL: the context's stream); returns once the scene tables are
- * uploaded (the kernels may still run).  RG_EINVAL for any scene
- * rg_render_stereo_pair rejects. */
+ * `stream`: returns with the upload of the scene tables (through a pinned
+ * staging buffer) and the kernels enqueued -- order later work on that
+ * stream or synchronise it before reading the frames.  stream NULL: the
+ * context's stream, and the call blocks until the frames are rendered.
+ * RG_EINVAL for any scene rg_render_stereo_pair rejects. */
 rg_status rg_render_frames_device(rg_ctx* ctx, const rg_scene_config* cfgs, const rg_scene_object* objs,
                                   const int32_t* obj_offsets, int n_frames, uint8_t* d_left,
                                   uint8_t* d_right, int64_t frame_stride, void* stream);

@@ -720,6 +720,27 @@ __global__ void autorect_pick_kernel(const int64_t* __restrict__ counts, int n_f
   best[f] = bd;
 }
 
+// autorect with downscale > 1 (autorect.hpp:36-44): crop(shift_vertical(img,
+// delta), roi) as one gather (image.hpp:75-82, 145-154) ...
+__global__ void crop_shift_kernel(const uint8_t* __restrict__ src, int w, int h, int x0, int y0, int rw, int rh,
+                                  int delta, uint8_t* __restrict__ dst) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x, y = blockIdx.y;
+  if (x >= rw || y >= rh) return;
+  const int sy = min(max(y0 + y - delta, 0), h - 1);
+  dst[(int64_t)y * rw + x] = src[(int64_t)sy * w + x0 + x];
+}
+
+// ... and the count of raw values that are valid and above 16 d_min
+__global__ void count_above_kernel(const int16_t* __restrict__ raw, int64_t n, int lo, int64_t* __restrict__ count) {
+  int c = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int v = raw[i];
+    c += (v != -32768 && v > lo) ? 1 : 0;
+  }
+  c = __reduce_add_sync(0xffffffffu, c);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(reinterpret_cast<unsigned long long*>(count), (unsigned long long)c);
+}
+
 }  // namespace
 
 cudaError_t launch_bm(const uint8_t* left, const uint8_t* right, int n_frames, int64_t stride,
@@ -772,6 +793,18 @@ cudaError_t launch_upscale(const int16_t* in, int w, int h, int s, int lo, int16
                            int oh, cudaStream_t st) {
   dim3 grid((ow + 127) / 128, oh);
   upscale_kernel<<<grid, 128, 0, st>>>(in, w, h, s, lo, out, ow, oh);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_crop_shift(const uint8_t* src, int w, int h, int x0, int y0, int rw, int rh, int delta,
+                              uint8_t* dst, cudaStream_t st) {
+  dim3 grid((rw + 255) / 256, rh);
+  crop_shift_kernel<<<grid, 256, 0, st>>>(src, w, h, x0, y0, rw, rh, delta, dst);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_count_above(const int16_t* raw, int64_t n, int lo, int64_t* count, cudaStream_t st) {
+  count_above_kernel<<<148, 256, 0, st>>>(raw, n, lo, count);
   return cudaGetLastError();
 }
 

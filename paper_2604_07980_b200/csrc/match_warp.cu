@@ -887,8 +887,14 @@ cudaError_t launch_variant(const Slot* slots, int32_t* counters, int slot_capaci
   auto kern = match_slots_warp_kernel<CT, WPB, MINB, PF, COOP, V2>;
   max_points = (max_points + 1) & ~1;  // keeps every warp's VPoint array 16-B aligned
   const size_t smem = (sizeof(int2) * (size_t)max_points + sizeof(VPoint<CT>) * (size_t)(max_points + 1)) * WPB;
+  // the opt-in covers static + dynamic shared memory (occluder boxes etc. are static)
+  static const size_t static_smem = [&] {
+    cudaFuncAttributes fa{};
+    return cudaFuncGetAttributes(&fa, (const void*)kern) == cudaSuccess ? fa.sharedSizeBytes : (size_t)0;
+  }();
+  if (static_smem + smem > kSmemPerBlockOptIn) return cudaErrorInvalidConfiguration;  // caller: fewer warps
   static SmemAttr attr;  // one per instantiation
-  if (smem > 48 * 1024) {
+  if (static_smem + smem > 48 * 1024) {
     const cudaError_t e = attr.ensure((const void*)kern, smem);
     if (e != cudaSuccess) return e;
   }
@@ -918,7 +924,21 @@ cudaError_t launch_match_slots(const Slot* slots, int32_t* counters, int slot_ca
   }();
 #define RG_ARGS slots, counters, slot_capacity, objs, dets, det_off, fl, fr, gf, sl, sr, gs, img_w, img_h, \
                 trusted, cfg, res, stats, max_points, s
-  if (wide) return launch_variant<unsigned long long, 8, 2>(RG_ARGS);  // 9x7 extension
+  // blocks too large for the default warps per CTA fall back to fewer
+  // (shared memory holds every warp's points: 16 or 24 B per point)
+  auto fallback = [&](cudaError_t e, auto... launchers) {
+    ((e = (e == cudaErrorInvalidConfiguration ? launchers() : e)), ...);
+    return e;
+  };
+  if (wide)  // 9x7 extension
+    return fallback(launch_variant<unsigned long long, 8, 2>(RG_ARGS),
+                    [&] { return launch_variant<unsigned long long, 2, 8>(RG_ARGS); },
+                    [&] { return launch_variant<unsigned long long, 1, 16>(RG_ARGS); });
+  auto small = [&](cudaError_t e) {
+    return fallback(e, [&] { return launch_variant<uint32_t, 8, 4>(RG_ARGS); },
+                    [&] { return launch_variant<uint32_t, 2, 8>(RG_ARGS); },
+                    [&] { return launch_variant<uint32_t, 1, 16>(RG_ARGS); });
+  };
   // latency mode (a few frames): most SMs would idle and the FAR blocks are
   // the critical path, so one CTA per FAR block splits its passes over 4
   // warps (single C2 frame: 84 -> 43 us).  The L1 prefetch of the point 4
@@ -926,7 +946,7 @@ cudaError_t launch_match_slots(const Slot* slots, int32_t* counters, int slot_ca
   // costs 2 us (variant 7 keeps it); 8 or 16 warps per FAR block measured
   // 47 / 80 us (variants 5, 6).
   if (variant == 0 && n_frames > 0 && n_frames <= kLatencyFrames)
-    return launch_variant<uint32_t, 4, 12, 0, true>(RG_ARGS);
+    return small(launch_variant<uint32_t, 4, 12, 0, true>(RG_ARGS));
   switch (variant) {  // A/B knobs; default measured best (tools/census_time.py with RG_MATCH_VARIANT)
     case 1: return launch_variant<uint32_t, 8, 4>(RG_ARGS);
     case 2: return launch_variant<uint32_t, 8, 5>(RG_ARGS);
@@ -941,7 +961,7 @@ cudaError_t launch_match_slots(const Slot* slots, int32_t* counters, int slot_ca
     case 8: return launch_variant<uint32_t, 16, 3, 0, false, true>(RG_ARGS);
     case 9: return launch_variant<uint32_t, 8, 4, 0, false, true>(RG_ARGS);
     case 10: return launch_variant<uint32_t, 16, 2, 0, false, true>(RG_ARGS);
-    default: return launch_variant<uint32_t, 16, 3>(RG_ARGS);
+    default: return small(launch_variant<uint32_t, 16, 3>(RG_ARGS));
   }
 #undef RG_ARGS
 }

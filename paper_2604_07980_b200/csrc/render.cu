@@ -241,10 +241,16 @@ rg_status render_frames_device(rg_ctx* ctx, const rg_scene_config* cfgs, const r
   const size_t sb = sizeof(FrameScene) * fs.size(), ob = sizeof(RenderObj) * std::max<size_t>(all.size(), 1);
   uint8_t* d = static_cast<uint8_t*>(dev_buf(ctx, B_SYNTH, sb + ob));
   if (!d) return set_err(ctx, RG_ENOMEM, "render_frames_device: scratch");
-  std::vector<uint8_t> hb(sb + ob);
-  memcpy(hb.data(), fs.data(), sb);
-  if (!all.empty()) memcpy(hb.data() + sb, all.data(), sizeof(RenderObj) * all.size());
-  RG_CUDA(ctx, cudaMemcpyAsync(d, hb.data(), sb + ob, cudaMemcpyHostToDevice, s));
+  // scene tables staged through a pinned buffer (the previous call's copy
+  // must have left it): the call returns with the kernels enqueued
+  if (!ctx->ev_stage) RG_CUDA(ctx, cudaEventCreateWithFlags(&ctx->ev_stage, cudaEventDisableTiming));
+  RG_CUDA(ctx, cudaEventSynchronize(ctx->ev_stage));
+  uint8_t* hb = static_cast<uint8_t*>(host_buf(ctx, 2, sb + ob));
+  if (!hb) return set_err(ctx, RG_ENOMEM, "render_frames_device: pinned staging");
+  memcpy(hb, fs.data(), sb);
+  if (!all.empty()) memcpy(hb + sb, all.data(), sizeof(RenderObj) * all.size());
+  RG_CUDA(ctx, cudaMemcpyAsync(d, hb, sb + ob, cudaMemcpyHostToDevice, s));
+  RG_CUDA(ctx, cudaEventRecord(ctx->ev_stage, s));
   const FrameScene* dfs = reinterpret_cast<const FrameScene*>(d);
   const RenderObj* dob = reinterpret_cast<const RenderObj*>(d + sb);
   dim3 grid((w + kBodyTx - 1) / kBodyTx, h, n_frames);
@@ -253,8 +259,6 @@ rg_status render_frames_device(rg_ctx* ctx, const rg_scene_config* cfgs, const r
   noise_kernel<<<n_frames, kNoiseThreads, 0, s>>>(dfs, w, h, d_left, d_right, frame_stride);
   RG_CUDA(ctx, cudaGetLastError());
   count_launch(ctx, 4, 2);
-  // the staging copy must finish before the host buffer is reused
-  RG_CUDA(ctx, cudaStreamSynchronize(s));
   return RG_OK;
 }
 
@@ -275,6 +279,8 @@ extern "C" rg_status rg_render_frames_device(rg_ctx* ctx, const rg_scene_config*
   for (int f = 0; f < n_frames; ++f)
     if (obj_offsets[f + 1] < obj_offsets[f] || (obj_offsets[f + 1] > obj_offsets[f] && !objs))
       return set_err(ctx, RG_EINVAL, "render_frames_device: bad object offsets");
-  return render_frames_device(ctx, cfgs, objs, obj_offsets, n_frames, d_left, d_right, frame_stride,
-                              stream ? static_cast<cudaStream_t>(stream) : ctx->stream);
+  const rg_status st = render_frames_device(ctx, cfgs, objs, obj_offsets, n_frames, d_left, d_right, frame_stride,
+                                            stream ? static_cast<cudaStream_t>(stream) : ctx->stream);
+  if (st == RG_OK && !stream) RG_CUDA(ctx, cudaStreamSynchronize(ctx->stream));  // NULL stream: blocking call
+  return st;
 }

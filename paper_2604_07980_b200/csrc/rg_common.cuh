@@ -32,6 +32,8 @@ struct NvtxRange {
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) is per DEVICE: one cache
 // per kernel (a static of the call site) remembers the size raised on each
 // device, so a process driving several GPUs raises it on every one.
+constexpr size_t kSmemPerBlockOptIn = 227 * 1024;  // sm_100 opt-in limit per CTA (static + dynamic)
+
 struct SmemAttr {
   static constexpr int kDevices = 64;
   std::atomic<int> raised[kDevices] = {};
@@ -166,6 +168,7 @@ struct rg_ctx {
   int sync_mode = 0;             // 1: rg_range_frames blocks and re-runs on overflow (legacy)
   cudaStream_t last_stream = nullptr;  // stream of the last asynchronous batch
   cudaEvent_t ev_last = nullptr;       // orders a batch on another stream after it
+  cudaEvent_t ev_stage = nullptr;      // pinned scene-table staging of rg_render_frames_device
 };
 
 namespace rg {
@@ -281,6 +284,9 @@ cudaError_t launch_bm(const uint8_t* left, const uint8_t* right, int n_frames, i
 cudaError_t launch_downscale(const uint8_t* in, int w, int h, int s, uint8_t* out, cudaStream_t st);
 cudaError_t launch_upscale(const int16_t* in, int w, int h, int s, int lo, int16_t* out, int ow,
                            int oh, cudaStream_t st);
+cudaError_t launch_crop_shift(const uint8_t* src, int w, int h, int x0, int y0, int rw, int rh, int delta,
+                              uint8_t* dst, cudaStream_t st);
+cudaError_t launch_count_above(const int16_t* raw, int64_t n, int lo, int64_t* count, cudaStream_t st);
 cudaError_t launch_autorect_pick(const int64_t* counts, int n_frames, int delta_min, int n_delta,
                                  int32_t* best, cudaStream_t s);
 

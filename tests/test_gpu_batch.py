@@ -369,3 +369,27 @@ def test_multi_ranger_matches_single_context_and_reference(ctx, chk, name):
     for f in range(n):
         got = out.reshape(n, -1)[f][:cnt[f]]
         assert got.tobytes() == _want(chk, L[f], R[f], D[f], cfg)
+
+
+@pytest.mark.parametrize("grid,maxp,frames", [(12, 144, 6), (12, 144, 2), (32, 1024, 6), (32, 1024, 1)])
+def test_large_blocks_fit_the_device_matcher(ctx, chk, grid, maxp, frames):
+    """Blocks of 144 and 1024 points (grid_side_points 12 / 32) through the
+    batched matcher (throughput variant > 4 frames, latency variant <= 4):
+    shared memory opts in for static + dynamic bytes and falls back to fewer
+    warps per CTA when 16 warps' points do not fit."""
+    import torch
+
+    L, R, D, cfg, sc = _frames(S.scene_c1, frames)
+    cfg.grid_side_points = grid
+    cfg.max_total_points = maxp
+    eng = FrameEngine(sc.width, sc.height, cfg, 8, S.F_PX, S.BASELINE_M, ctx=ctx)
+    recs, offs = pack_detections(D)
+    dev = torch.device("cuda", 0)
+    out = torch.zeros(frames * eng.out_stride * 32, dtype=torch.uint8, device=dev)
+    cnt = torch.zeros(frames, dtype=torch.int32, device=dev)
+    eng.range_device(torch.from_numpy(L).to(dev), torch.from_numpy(R).to(dev),
+                     torch.from_numpy(recs.view(np.uint8)).to(dev), torch.from_numpy(offs).to(dev), out, cnt)
+    o = out.cpu().numpy().reshape(frames, -1)
+    for f in range(frames):
+        want = _want(chk, L[f], R[f], D[f], cfg)
+        assert int(cnt[f]) * 32 == len(want) and o[f, :len(want)].tobytes() == want

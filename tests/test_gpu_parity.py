@@ -297,3 +297,19 @@ def test_auto_rect_c4_full_roi_counts_vs_reference(ctx, chk, voff):
     st, want, wc = chk.autorect_mt(L, R, S.C4_ROI, -8, 8, p.to_c(), len(os.sched_getaffinity(0)))
     assert st == 0 and got == want == voff
     assert counts == list(wc)
+
+
+@pytest.mark.parametrize("voff,ds", [(-2, 2), (1, 2), (0, 3)])
+def test_auto_rect_search_downscale_on_device(ctx, chk, voff, ds):
+    """autorect.hpp:36-44 with BmParams.downscale > 1: the shifted crops, the
+    downscaled BM and the counts all on the device; delta* and every count
+    equal the reference's."""
+    sc = S.SceneConfig(objects=[S.SceneObject(id=1, position=(30.0, 0.0, 1.5), texture_seed=11)],
+                       vertical_offset_px=voff)
+    L, R = S.render_stereo_pair(sc)
+    p = rg.BmParams(24, 9, 0, 10, 10, ds)
+    counts = []
+    got = rg.auto_rect_search(L, R, rg.ImageRoi(200, 120, 440, 280), -3, 3, p, ctx=ctx, counts_out=counts)
+    st, want, wc = chk.autorect(L, R, (200, 120, 440, 280), -3, 3, p.to_c())
+    assert st == 0 and got == want
+    assert counts == list(wc)
