@@ -2,8 +2,9 @@
 """Summarise ncu captures for profiles/: key metrics per kernel (from an
 --set full .ncu-rep) and launch shares (from a --metrics gpu__time_duration
 csv launch list).  Usage:
-  python tools/ncu_summary.py REP.ncu-rep LAUNCHES.csv OUT.md [frames_per_launch]
-Also writes profiles/traffic.json (census DRAM bytes per frame) for bench.py."""
+  python tools/ncu_summary.py REP.ncu-rep LAUNCHES.csv OUT.md [frames_per_launch] [captured command]
+Also writes profiles/r2_traffic.json (DRAM bytes of the census kernels of one
+launch, summed) for bench.py's roofline.traffic."""
 import collections
 import csv
 import io
@@ -49,6 +50,8 @@ def stalls(rep, kernel_regex):
     cols = [c for c in h if c.startswith("stall_") and "Not Issued" not in c]
     tot = collections.Counter()
     for r in rows[2:]:
+        if len(r) != len(h):
+            continue
         for c in cols:
             try:
                 tot[c[6:]] += float(r[h.index(c)] or 0)
@@ -76,11 +79,12 @@ def launches(path):
 def main():
     rep, lcsv, out = sys.argv[1:4]
     fpl = int(sys.argv[4]) if len(sys.argv) > 4 else 32
+    cmd = sys.argv[5] if len(sys.argv) > 5 else f"bench.py --frames {fpl}"
     data, units = raw(rep)
     lines = [f"# ncu summary: {os.path.basename(rep)}", "",
              f"Capture: `ncu --set full --clock-control none --import-source on` of "
-             f"`bench.py --frames {fpl}` (one launch per kernel shown; one launch = {fpl} C2 frames).", ""]
-    traffic = {}
+             f"`{cmd}` (one launch per kernel shown; one launch = {fpl} C2 frames).", ""]
+    traffic = {"census_dram_bytes_per_launch": 0.0, "frames_per_launch": fpl, "per_kernel": {}}
     for d in data:
         name = d["Kernel Name"].split("(")[0].split("::")[-1]
         lines.append(f"## {name}")
@@ -95,12 +99,12 @@ def main():
             lines.append(f"| top stall reasons (% of samples) | {', '.join(f'{k} {v}' for k, v in st.items())} |")
         lines.append("")
         if "census" in name:
-            mb = float(d["dram__bytes_read.sum"]) + float(d["dram__bytes_write.sum"])
-            scale = 1e6 if units.get("dram__bytes_read.sum", "") == "Mbyte" else 1e9 if units.get(
-                "dram__bytes_read.sum", "") == "Gbyte" else 1.0
-            traffic["census_bytes_per_frame"] = mb * scale / fpl
-            traffic["census_algorithmic_bytes_per_frame"] = 2 * (1920 * 1080 * 5 + 4 * 960 * 540)
-            traffic["source"] = os.path.basename(rep)
+            sc = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+            b = sum(float(d[m].replace(",", "")) * sc.get(units.get(m, "byte"), 1.0)
+                    for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+            traffic["census_dram_bytes_per_launch"] += b
+            traffic["per_kernel"][name + " " + d.get("Grid Size", d.get("launch__grid_size", ""))] = b
+            traffic["source"] = f"{os.path.basename(rep)}: {cmd}"
     if lcsv and os.path.exists(lcsv):
         agg = launches(lcsv)
         tot = sum(sum(v) for v in agg.values())
@@ -110,8 +114,8 @@ def main():
             lines.append(f"| {k} | {len(v)} | {sum(v) / 1e3:.1f} | {100 * sum(v) / tot:.1f}% |")
         lines.append("")
     open(out, "w").write("\n".join(lines) + "\n")
-    if traffic:
-        json.dump(traffic, open(os.path.join(os.path.dirname(out), "traffic.json"), "w"), indent=1)
+    if traffic["census_dram_bytes_per_launch"]:
+        json.dump(traffic, open(os.path.join(os.path.dirname(out), "r2_traffic.json"), "w"), indent=1)
     print("\n".join(lines))
 
 
