@@ -552,6 +552,11 @@ rg_status rg_vote_state_init(rg_vote_state* st, int k_px, double lambda, double 
 rg_status rg_radar_refine_step(rg_ctx* ctx, int16_t* d_raw, int w, int h, const rg_radar_detection* radar, int n,
                                rg_vote_state* st, const rg_calibration* calib, double* applied);
 
+/* rg_radar_refine_step on a HOST map (uploaded, refined on the device,
+ * copied back): the drop-in radar_refine_step of include/ranger/radar_refiner.hpp. */
+rg_status rg_radar_refine_step_host(rg_ctx* ctx, int16_t* raw, int w, int h, const rg_radar_detection* radar, int n,
+                                    rg_vote_state* st, const rg_calibration* calib, double* applied);
+
 /* Host halves of rg_radar_refine_step (used by it; exposed for tests):
  * rg_radar_boxes -- per detection p_cam = imu_to_cam(position), skipped when
  * p_cam.z <= 0 or radar_extent_box fails, else box (x0, y0, x1, y1 inclusive)

@@ -199,6 +199,7 @@ SIGNATURES = {
     "rg_shard_bounds": (I, [I, I, I, P, P]),
     "rg_vote_state_init": (I, [P, I, D, D]),
     "rg_radar_refine_step": (I, [P, P, I, I, P, I, P, P, P]),
+    "rg_radar_refine_step_host": (I, [P, P, I, I, P, I, P, P, P]),
     "rg_radar_boxes": (I, [P, I, P, I, I, P, P, P]),
     "rg_radar_vote_update": (I, [P, P, P, I, P, P]),
     "rg_dense_objects_refined": (I, [P, P, P, I, I, P, I, P, P, D, D, D, P, I, P, P, P, P, P, P, P]),
