@@ -441,12 +441,18 @@ __global__ void __launch_bounds__(rw_wpb<STRIDE>() * 32) census_rowtile_kernel(
 #pragma unroll
       for (int t = 0; t < NI; ++t) wv[t] = __ldg(col + (int64_t)min(max(ya + t, 0), h - 1) * pw);
     }
-    uint32_t* vrow = V + 4 + 4 * k - 2;  // entries of source columns x0 - 4 + 4k .. + 3
+    // word k holds source columns x0 - 4 + 4k .. + 3 = V indices 4k + 2 .. 4k + 5;
+    // the 16-B group k (indices 4k .. 4k + 3) takes the last two entries of
+    // word k - 1 (one lane down) and the first two of word k: one aligned
+    // STS.128 per row instead of two 8-B stores at a 16-B stride (half the
+    // shared-memory wavefronts of the V build; the windows read groups 1..31)
+    uint4* vrow = reinterpret_cast<uint4*>(V) + k;
 #pragma unroll
     for (int t = 0; t < NV; ++t) {
       const uint32_t a = wv[t], b = wv[t + STRIDE];
-      *reinterpret_cast<uint2*>(vrow + t * RW_VW) = make_uint2(c2_vpair(a, b, 0), c2_vpair(a, b, 1));
-      *reinterpret_cast<uint2*>(vrow + t * RW_VW + 2) = make_uint2(c2_vpair(a, b, 2), c2_vpair(a, b, 3));
+      const uint32_t e2 = c2_vpair(a, b, 2), e3 = c2_vpair(a, b, 3);
+      const uint32_t p2 = __shfl_up_sync(0xffffffffu, e2, 1), p3 = __shfl_up_sync(0xffffffffu, e3, 1);
+      vrow[t * (RW_VW / 4)] = make_uint4(p2, p3, c2_vpair(a, b, 0), c2_vpair(a, b, 1));
     }
   }
   __syncwarp();
