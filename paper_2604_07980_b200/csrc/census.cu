@@ -463,14 +463,23 @@ __global__ void __launch_bounds__(rw_wpb<STRIDE>() * 32) census_rowtile_kernel(
   if (lane >= RW_TX / 4 || xo >= g.w) return;
   const bool edge = x0 < 2 || x0 + RW_TX + 2 > w - 3 || STRIDE * Y0 < 2 || STRIDE * (Y0 + 2 * RW_PR) > h - 3;
   const uint32_t* vbase = V + 4 + 4 * lane;  // V index of source column xs - 2
+  // consecutive pairs' windows overlap by 5 - 2 STRIDE V rows (3 full, 1
+  // reduced): they stay in registers, only the new rows are loaded
+  // (every pair of a needed tile is computed, so the rotation is static and
+  // costs no register moves)
+  constexpr int KEEP = 5 - 2 * STRIDE;
+  uint32_t win[5][8];
 #pragma unroll
   for (int p = 0; p < RW_PR; ++p) {
     const int y = Y0 + 2 * p;
     if (y >= g.h) break;
-    if (!((__ldg(fm + (y >> 5)) >> (y & 31)) & 3u)) continue;  // y even: y, y + 1 share a mask word
-    uint32_t win[5][8];
 #pragma unroll
     for (int j = 0; j < 5; ++j) {
+      if (p > 0 && j < KEEP) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) win[j][q] = win[j + 2 * STRIDE][q];
+        continue;
+      }
       const uint4* src = reinterpret_cast<const uint4*>(vbase + (2 * STRIDE * p + j) * RW_VW);
       const uint4 a = src[0], b = src[1];
       win[j][0] = a.x; win[j][1] = a.y; win[j][2] = a.z; win[j][3] = a.w;
