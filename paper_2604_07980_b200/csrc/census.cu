@@ -9,6 +9,8 @@
 // batched kernel writes it from the same registers (inverse index maps).
 #include <cuda_fp16.h>
 
+#include <cstdlib>
+
 #include "rg_common.cuh"
 #include "rg_device.cuh"
 
@@ -572,6 +574,155 @@ __global__ void __launch_bounds__(X_TPB) census64_kernel(
   }
 }
 
+// 9x7 "vertical pair" census (the fast path of the 64-bit extension): the
+// same half2 formulation as census_pairs_kernel -- rows y, y+1 in the two
+// fp16 lanes, one compare + one HFMA2 per window tap for both rows -- with
+// one fp16 accumulator per WINDOW ROW: init 2.0, 9 steps, so the row's 9
+// compare bits are the low mantissa bits (1024 + B).  The window is walked
+// row by row (12 V entries per lane per row: columns x-4 .. x+7 for the
+// lane's 4 outputs), so registers hold one row of the window, not seven.
+// Code = sentinel bit 63 | B_r << (54 - 9 r) (rows r = 0..6 = window rows
+// -3..3, MSB-first; the centre compare is always 0: folded into a x4 step).
+constexpr int X2_WARPS = 6, X2_PR = 5;
+constexpr int X2_TX = 128, X2_TY = X2_WARPS * X2_PR * 2;       // 60 rows
+constexpr int X2_VW = X2_TX + 12;                             // index 4 = column x0 - 4
+constexpr int X2_WORDS = X2_TX / 4 + 2;                       // image words per row (x0-4 .. x0+TX+3)
+constexpr int X2_RUNS = (X2_WARPS * 32) / X2_WORDS;            // 5
+constexpr int X2_RUN = (X2_TY + 6 + X2_RUNS - 1) / X2_RUNS;    // V rows y0-3 .. y0+TY+2
+constexpr int X2_VR = X2_RUNS * X2_RUN;
+constexpr size_t X2_SMEM = sizeof(uint32_t) * X2_VR * X2_VW;
+
+template <bool EDGE>
+__device__ __forceinline__ void c64_strip(const uint32_t* __restrict__ V, unsigned long long* __restrict__ full,
+                                          unsigned long long* __restrict__ red, const PadGeom& gf,
+                                          const PadGeom& gs, int x0, int y0, int w, int h) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int xl = x0 + 4 * lane;
+  const uint32_t* vbase = V + 4 + 4 * lane;  // V index of column xl - 4
+  const __half2 two = __float2half2_rn(2.0f), four = __float2half2_rn(4.0f);
+#pragma unroll 1
+  for (int p = wid * X2_PR; p < wid * X2_PR + X2_PR; ++p) {
+    const int y = y0 + 2 * p;
+    if (EDGE && y >= h) break;
+    uint32_t clo[4], chi[4];  // 64-bit codes of rows y (lo) and y + 1 (hi), as two 32-bit halves
+    uint32_t dlo[4], dhi[4];
+    __half2 cen[4];
+    {
+      const uint4 c4 = *reinterpret_cast<const uint4*>(vbase + (2 * p + 3) * X2_VW + 4);  // columns xl .. xl+3
+      cen[0] = *reinterpret_cast<const __half2*>(&c4.x);
+      cen[1] = *reinterpret_cast<const __half2*>(&c4.y);
+      cen[2] = *reinterpret_cast<const __half2*>(&c4.z);
+      cen[3] = *reinterpret_cast<const __half2*>(&c4.w);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) clo[q] = dlo[q] = 0u, chi[q] = dhi[q] = 0x80000000u;  // sentinel bit 63
+#pragma unroll
+    for (int r = 0; r < 7; ++r) {
+      uint32_t e[12];
+      const uint4* src = reinterpret_cast<const uint4*>(vbase + (2 * p + r) * X2_VW);
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const uint4 a = src[k];
+        e[4 * k] = a.x, e[4 * k + 1] = a.y, e[4 * k + 2] = a.z, e[4 * k + 3] = a.w;
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        __half2 acc = two;
+#pragma unroll
+        for (int c = 0; c < 9; ++c) {
+          if (r == 3 && c == 4) continue;  // centre: its 0 bit is folded into the next step's x4
+          const __half2 v = *reinterpret_cast<const __half2*>(&e[q + c]);
+          const __half2 m = ((r * 9 + c) % 6 == 0) ? __hsub2_sat(v, cen[q]) : __hgt2(v, cen[q]);
+          acc = __hfma2(acc, (r == 3 && c == 5) ? four : two, m);
+        }
+        const uint32_t u = *reinterpret_cast<const uint32_t*>(&acc);
+        const uint32_t bl = u & 0x1FFu, bh = (u >> 16) & 0x1FFu;
+        // bit 54 - 9r of the 64-bit code: rows 0..2 in the high word, row 3
+        // straddles (bits 27..35), rows 4..6 in the low word
+        const int pos = 54 - 9 * r;
+        if (pos >= 32) {
+          chi[q] |= bl << (pos - 32);
+          dhi[q] |= bh << (pos - 32);
+        } else if (pos + 9 > 32) {
+          clo[q] |= bl << pos, chi[q] |= bl >> (32 - pos);
+          dlo[q] |= bh << pos, dhi[q] |= bh >> (32 - pos);
+        } else {
+          clo[q] |= bl << pos;
+          dlo[q] |= bh << pos;
+        }
+      }
+    }
+    unsigned long long lo[4], hi[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      lo[q] = ((unsigned long long)chi[q] << 32) | clo[q];
+      hi[q] = ((unsigned long long)dhi[q] << 32) | dlo[q];
+      if (EDGE) {  // 0 where the 9x7 window leaves the image
+        const bool xin = xl + q >= 4 && xl + q <= w - 5;
+        if (!(xin && y >= 3 && y <= h - 4)) lo[q] = 0ull;
+        if (!(xin && y + 1 >= 3 && y + 1 <= h - 4)) hi[q] = 0ull;
+      }
+    }
+    if (EDGE && xl >= w) continue;
+    unsigned long long* o = full + (int64_t)y * gf.pitch + xl;
+    reinterpret_cast<ulonglong2*>(o)[0] = make_ulonglong2(lo[0], lo[1]);
+    reinterpret_cast<ulonglong2*>(o)[1] = make_ulonglong2(lo[2], lo[3]);
+    if (!EDGE || y + 1 < h) {
+      reinterpret_cast<ulonglong2*>(o + gf.pitch)[0] = make_ulonglong2(hi[0], hi[1]);
+      reinterpret_cast<ulonglong2*>(o + gf.pitch)[1] = make_ulonglong2(hi[2], hi[3]);
+    }
+    if (red)  // reduced raster = codes at even (x, y)
+      *reinterpret_cast<ulonglong2*>(red + (int64_t)(y >> 1) * gs.pitch + (xl >> 1)) = make_ulonglong2(lo[0], lo[2]);
+  }
+}
+
+__global__ void __launch_bounds__(X2_WARPS * 32) census64_pairs_kernel(
+    const uint8_t* __restrict__ left, const uint8_t* __restrict__ right, int64_t frame_stride, int pitch, int w,
+    int h, unsigned long long* __restrict__ fl, unsigned long long* __restrict__ fr, PadGeom gf,
+    unsigned long long* __restrict__ sl, unsigned long long* __restrict__ sr, PadGeom gs,
+    const int32_t* __restrict__ lshift) {
+  extern __shared__ __align__(16) uint32_t V[];  // [X2_VR][X2_VW]
+  const int sides = right ? 2 : 1;
+  const int frame = blockIdx.z / sides, side = blockIdx.z - frame * sides;
+  const int sh = (side == 0 && lshift) ? lshift[frame] : 0;
+  const uint8_t* img = (side ? right : left) + (int64_t)frame * frame_stride;
+  unsigned long long* full = (side ? fr : fl) + (int64_t)frame * gf.fstride + gf.origin;
+  unsigned long long* red = side ? sr : sl;
+  if (red) red += (int64_t)frame * gs.fstride + gs.origin;
+  const int x0 = blockIdx.x * X2_TX, y0 = blockIdx.y * X2_TY;
+  // ---- V rows y0-3 .. : V[r][c] = half2(1024 + I(c, r), 1024 + I(c, r + 1)), word wk at index 4 + 4 wk
+  const int wk = threadIdx.x % X2_WORDS, run = threadIdx.x / X2_WORDS;
+  if (run < X2_RUNS) {
+    const int kw = min(max((x0 - 4) / 4 + wk, 0), (w + 3) / 4 - 1);
+    const int pw = pitch / 4;
+    const int r0 = run * X2_RUN, ya = y0 - 3 + r0 - sh;
+    uint32_t wv[X2_RUN + 1];
+    if (ya >= 0 && ya + X2_RUN <= h - 1) {
+      const uint32_t* col = reinterpret_cast<const uint32_t*>(img) + (int64_t)ya * pw + kw;
+#pragma unroll
+      for (int t = 0; t <= X2_RUN; ++t, col += pw) wv[t] = __ldg(col);
+    } else {
+      const uint32_t* col = reinterpret_cast<const uint32_t*>(img) + kw;
+#pragma unroll
+      for (int t = 0; t <= X2_RUN; ++t) wv[t] = __ldg(col + (int64_t)min(max(ya + t, 0), h - 1) * pw);
+    }
+    uint4* vrow = reinterpret_cast<uint4*>(V + r0 * X2_VW + 4) + wk;
+#pragma unroll
+    for (int t = 0; t < X2_RUN; ++t) {
+      const uint32_t a = wv[t], b = wv[t + 1];
+      vrow[t * (X2_VW / 4)] = make_uint4(c2_vpair(a, b, 0), c2_vpair(a, b, 1), c2_vpair(a, b, 2), c2_vpair(a, b, 3));
+    }
+  }
+  __syncthreads();
+  const int ys = y0 + 2 * (threadIdx.x >> 5) * X2_PR;
+  if (ys >= h) return;
+  const bool edge = x0 < 4 || x0 + X2_TX + 4 > w - 5 || ys < 3 || ys + 2 * X2_PR + 2 > h - 4;
+  if (__any_sync(0xffffffffu, edge))
+    c64_strip<true>(V, full, red, gf, gs, x0, y0, w, h);
+  else
+    c64_strip<false>(V, full, red, gf, gs, x0, y0, w, h);
+}
+
 // census_transform_rois mask (census.hpp:111-136): keep codes inside the
 // union of the clipped rectangles, zero elsewhere.  Kept codes leave in the
 // reference layout (sentinel bit 25) whichever layout they were computed in.
@@ -690,6 +841,21 @@ cudaError_t launch_census64_frames(const uint8_t* left, const uint8_t* right, in
                                    const PadGeom& gs, const int32_t* inv_x, const int32_t* inv_y,
                                    const int32_t* lshift, cudaStream_t s) {
   if (n_frames <= 0) return cudaSuccess;
+  static const bool scalar = getenv("RG_CENSUS64_SCALAR") != nullptr;  // A/B knob: the per-pixel kernel
+  const bool aligned = (pitch % 4 == 0) && (w % 4 == 0) && (frame_stride % 4 == 0) &&
+                       (reinterpret_cast<uintptr_t>(left) % 4 == 0) &&
+                       (!right || reinterpret_cast<uintptr_t>(right) % 4 == 0) && gf.pitch % 2 == 0 &&
+                       gf.origin % 2 == 0 && w >= 12 && h >= 8;
+  const bool half = !sl || (gs.w * 2 == w && gs.h * 2 == h && gs.pitch % 2 == 0 && gs.origin % 2 == 0);
+  if (aligned && half && !scalar) {
+    static SmemAttr attr;
+    const cudaError_t e = attr.ensure((const void*)census64_pairs_kernel, X2_SMEM);
+    if (e != cudaSuccess) return e;
+    dim3 grid((w + X2_TX - 1) / X2_TX, (h + X2_TY - 1) / X2_TY, (right ? 2 : 1) * n_frames);
+    census64_pairs_kernel<<<grid, X2_WARPS * 32, X2_SMEM, s>>>(left, right, frame_stride, pitch, w, h, fl, fr, gf,
+                                                               sl, sr, gs, lshift);
+    return cudaGetLastError();
+  }
   dim3 grid((w + X_TX - 1) / X_TX, (h + X_TY - 1) / X_TY, (right ? 2 : 1) * n_frames);
   census64_kernel<<<grid, X_TPB, 0, s>>>(left, right, frame_stride, pitch, w, h, fl, fr, gf, sl, sr, gs, inv_x,
                                          inv_y, lshift);
