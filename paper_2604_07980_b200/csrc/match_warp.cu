@@ -44,6 +44,9 @@ namespace {
 #ifndef RG_MW_NOINLINE
 #define RG_MW_NOINLINE 0
 #endif
+#ifndef RG_MW_CSA  // carry-save groups of 3 points in FAST sweeps: measured 1.22 vs 0.90 ms (loses the
+#define RG_MW_CSA 0  // one-point-ahead load pipelining; at 40 registers it spills) -- kept as an A/B knob
+#endif
 constexpr int kPipeUnroll = RG_MW_PIPE_UNROLL;
 constexpr int kWarpOcc = 32;
 constexpr int kLatencyFrames = 4;  // batches up to this size use the latency-mode matcher      // occluder boxes per warp kept in smem
@@ -128,6 +131,41 @@ __device__ __forceinline__ void sweep(const VPoint<CT>* __restrict__ vp, int nv,
   int s[K], n[K];
 #pragma unroll
   for (int c = 0; c < K; ++c) s[c] = n[c] = 0;
+  const int nv_all = nv;
+#if RG_MW_CSA
+  // FAST sweeps take the points three at a time through a carry-save adder:
+  // popc(a) + popc(b) + popc(c) = popc(a ^ b ^ c) + 2 popc(maj(a, b, c)), so
+  // 2 POPC per 3 evaluations -- the point loop is POPC-bound (a warp POPC
+  // occupies its pipe 8 cycles; tools/hamming_probe.cu: 15.4 -> 21.5
+  // evaluations / clk / SM); the remaining nv % 3 points take the loop below
+  if (MODE == M_FAST && sizeof(CT) == 4 && PF == 0) {
+    int s2[K];
+#pragma unroll
+    for (int c = 0; c < K; ++c) s2[c] = 0;
+    const int n3 = nv - nv % 3;
+    int k = 0;
+    for (; k < n3; k += 3) {
+      const VPoint<CT> qa = vp[k], qb = vp[k + 1], qc = vp[k + 2];
+      const CT* pa = reinterpret_cast<const CT*>(reinterpret_cast<const char*>(base) + qa.off);
+      const CT* pb = reinterpret_cast<const CT*>(reinterpret_cast<const char*>(base) + qb.off);
+      const CT* pc = reinterpret_cast<const CT*>(reinterpret_cast<const char*>(base) + qc.off);
+      CT ra[K], rb[K], rc[K];
+#pragma unroll
+      for (int c = 0; c < K; ++c) ra[c] = __ldg(pa - 32 * c), rb[c] = __ldg(pb - 32 * c), rc[c] = __ldg(pc - 32 * c);
+#pragma unroll
+      for (int c = 0; c < K; ++c) {
+        const uint32_t x = (uint32_t)(qa.code ^ ra[c]), y = (uint32_t)(qb.code ^ rb[c]),
+                       z = (uint32_t)(qc.code ^ rc[c]);
+        s[c] += __popc(x ^ y ^ z);
+        s2[c] += __popc((x & y) | (z & (x | y)));
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < K; ++c) s[c] += 2 * s2[c];
+    vp += n3;
+    nv -= n3;
+  }
+#endif
 #if RG_MW_PIPE
   // software-pipelined: the samples of point k+1 are in flight while point k
   // is consumed (the last prefetch re-reads point nv-1, harmless)
@@ -201,7 +239,7 @@ __device__ __forceinline__ void sweep(const VPoint<CT>* __restrict__ vp, int nv,
     const int ix = lane + 32 * (c0 + c);
     if (MODE == M_FAST) {
       if (ix < ndx) {
-        evals += nv;  // Hamming evaluations, census.hpp:209-221
+        evals += nv_all;  // Hamming evaluations, census.hpp:209-221
         const unsigned long long key = fast_key(s[c], dx_min + ix, dy);
         bkey = key < bkey ? key : bkey;
       }
