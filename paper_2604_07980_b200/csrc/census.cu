@@ -341,7 +341,8 @@ constexpr int RM_T = 128;
 __global__ void __launch_bounds__(RM_T) census_rows_kernel(const rg_detection* __restrict__ dets,
                                                           const int32_t* __restrict__ det_off, int w, int h,
                                                           double tau_s, int cw, int ch, int wf, int wr,
-                                                          uint32_t* __restrict__ mask) {
+                                                          uint32_t* __restrict__ mask, int tf, int tr, int tf_max,
+                                                          int tile_stride, int32_t* __restrict__ tiles) {
   extern __shared__ uint32_t sm_rows[];
   const int f = blockIdx.x;
   for (int i = threadIdx.x; i < wf + wr; i += RM_T) sm_rows[i] = 0u;
@@ -371,6 +372,29 @@ __global__ void __launch_bounds__(RM_T) census_rows_kernel(const rg_detection* _
   }
   __syncthreads();
   for (int i = threadIdx.x; i < wf + wr; i += RM_T) mask[(int64_t)f * (wf + wr) + i] = sm_rows[i];
+  // compacted warp-tile lists: greedy even-aligned tiles of tf (full) / tr
+  // (reduced) rows covering every needed row, disjoint; tiles[f] = {n_full,
+  // n_red, full starts (tf_max), reduced starts}
+  if (threadIdx.x < 2) {
+    const int side = threadIdx.x;
+    const uint32_t* m = sm_rows + (side ? wf : 0);
+    const int rows = side ? ch : h, step = side ? tr : tf;
+    int32_t* rec = tiles + (int64_t)f * tile_stride;
+    int32_t* list = rec + 2 + (side ? tf_max : 0);
+    int n = 0;
+    for (int cur = 0; cur < rows;) {
+      int wd = cur >> 5;
+      uint32_t bits = m[wd] & (0xFFFFFFFFu << (cur & 31));
+      while (!bits && ++wd < (rows + 31) / 32) bits = m[wd];
+      if (!bits) break;
+      const int t = (wd << 5) + __ffs(bits) - 1;
+      if (t >= rows) break;
+      const int start = t & ~1;
+      list[n++] = start;
+      cur = start + step;
+    }
+    rec[side] = n;
+  }
 }
 
 // Warp-tile "vertical pair" census for ROI rows: every warp owns a tile of
@@ -409,18 +433,22 @@ template <bool S31, int STRIDE>
 __global__ void __launch_bounds__(rw_wpb<STRIDE>() * 32) census_rowtile_kernel(
     const uint8_t* __restrict__ left, const uint8_t* __restrict__ right, int64_t frame_stride, int pitch, int w,
     int h, uint32_t* __restrict__ ol, uint32_t* __restrict__ orr, PadGeom g, const int32_t* __restrict__ lshift,
-    const uint32_t* __restrict__ rmask, int mstride) {
+    const int32_t* __restrict__ tiles, int tile_stride, int list_off) {
   constexpr int NV = rw_nv<STRIDE>(), NI = NV + STRIDE;  // V rows, image rows
   constexpr int RW_PR = rw_pr<STRIDE>();
   extern __shared__ __align__(16) uint32_t Vall[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int sides = right ? 2 : 1;
   const int frame = blockIdx.z / sides, side = blockIdx.z - frame * sides;
-  const int Y0 = (blockIdx.y * rw_wpb<STRIDE>() + wid) * 2 * RW_PR;  // first output row of this warp's tile
-  if (Y0 >= g.h) return;
-  const uint32_t* fm = rmask + (int64_t)frame * mstride;
-  if (!rows_any(fm, Y0, min(Y0 + 2 * RW_PR, g.h))) return;
+  // this warp walks its share of the frame's compacted tile list (every
+  // listed tile has a needed row; no CTA is launched for an empty one)
+  const int32_t* rec = tiles + (int64_t)frame * tile_stride;
+  const int n_tiles = rec[STRIDE - 1];
+  const int32_t* list = rec + list_off;
   uint32_t* V = Vall + wid * NV * RW_VW;
+  for (int ti = blockIdx.y * rw_wpb<STRIDE>() + wid; ti < n_tiles; ti += gridDim.y * rw_wpb<STRIDE>()) {
+  const int Y0 = list[ti];  // first output row of this tile (even)
+  __syncwarp();  // the previous tile's window reads are done before V is rebuilt
   const int sh = (side == 0 && lshift) ? lshift[frame] : 0;  // shift_vertical of the left image
   const uint8_t* img = (side ? right : left) + (int64_t)frame * frame_stride;
   uint32_t* out = (side ? orr : ol) + (int64_t)frame * g.fstride + g.origin;
@@ -462,7 +490,7 @@ __global__ void __launch_bounds__(rw_wpb<STRIDE>() * 32) census_rowtile_kernel(
   constexpr int NQ = 4 / STRIDE;
   const int xs = x0 + 4 * lane;     // source column of this lane's first output
   const int xo = xs / STRIDE;       // its output column
-  if (lane >= RW_TX / 4 || xo >= g.w) return;
+  if (lane >= RW_TX / 4 || xo >= g.w) continue;  // (such lanes only help build V)
   const bool edge = x0 < 2 || x0 + RW_TX + 2 > w - 3 || STRIDE * Y0 < 2 || STRIDE * (Y0 + 2 * RW_PR) > h - 3;
   const uint32_t* vbase = V + 4 + 4 * lane;  // V index of source column xs - 2
   // consecutive pairs' windows overlap by 5 - 2 STRIDE V rows (3 full, 1
@@ -517,6 +545,7 @@ __global__ void __launch_bounds__(rw_wpb<STRIDE>() * 32) census_rowtile_kernel(
         if (two) o[g.pitch + q] = hi[q];
       }
     }
+  }
   }
 }
 
@@ -773,6 +802,12 @@ cudaError_t launch_census_frames(const uint8_t* left, const uint8_t* right, int 
   return cudaGetLastError();
 }
 
+// 32-bit words of the row masks + tile lists of launch_census_rois
+size_t census_rois_scratch_words(int n_frames, int h, int ch) {
+  const int tf = 2 * rw_pr<1>(), tr = 2 * rw_pr<2>();
+  return (size_t)n_frames * ((h + 31) / 32 + (ch + 31) / 32 + 2 + (h + tf - 1) / tf + (ch + tr - 1) / tr);
+}
+
 // ROI-row census of a batch (see census_rows_kernel): the row masks, the
 // full raster on FAR ROI rows and the reduced raster on CLOSE ROI rows.
 // cudaErrorNotSupported when the fast layout does not apply (the caller then
@@ -792,8 +827,13 @@ cudaError_t launch_census_rois(const uint8_t* left, const uint8_t* right, int n_
                     gs.w >= 4 && gs.h >= 4;
   if (!aligned || !half || !masks || !dets) return cudaErrorNotSupported;
   const int wf = (h + 31) / 32, wr = (gs.h + 31) / 32;
+  const int tf = 2 * rw_pr<1>(), tr = 2 * rw_pr<2>();                 // output rows per warp tile
+  const int tf_max = (h + tf - 1) / tf, tr_max = (gs.h + tr - 1) / tr;
+  const int tile_stride = 2 + tf_max + tr_max;
+  int32_t* tiles = reinterpret_cast<int32_t*>(masks + (size_t)n_frames * (wf + wr));
   census_rows_kernel<<<n_frames, RM_T, sizeof(uint32_t) * (wf + wr), s>>>(dets, det_off, w, h, tau_s, gs.w, gs.h,
-                                                                         wf, wr, masks);
+                                                                         wf, wr, masks, tf, tr, tf_max,
+                                                                         tile_stride, tiles);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   static const int mode = [] {
@@ -813,24 +853,28 @@ cudaError_t launch_census_rois(const uint8_t* left, const uint8_t* right, int n_
                                               masks, wf + wr);
     return cudaGetLastError();
   }
+  // a fixed number of single-warp CTAs per (column tile, frame, side) walk the
+  // compacted lists (C2: ~40 full and ~80 reduced tiles per frame and side);
+  // 16 / 32 walkers measured best (4..48 / 8..96 tried: 1.069-1.12 ms per 256
+  // C2 frames, against 1.178 for one CTA per 10-row tile and mask skips)
   auto rowtile = [&](auto kern, size_t smem, SmemAttr& attr, uint32_t* a, uint32_t* b, const PadGeom& g,
-                     const uint32_t* m, int pr, int wpb) -> cudaError_t {
+                     int walkers, int list_off, int wpb) -> cudaError_t {
     cudaError_t e2 = attr.ensure((const void*)kern, smem);
     if (e2 != cudaSuccess) return e2;
-    const int ty = 2 * pr * wpb;  // output rows per CTA
-    dim3 grid((w + RW_TX - 1) / RW_TX, (g.h + ty - 1) / ty, sides * n_frames);
-    kern<<<grid, wpb * 32, smem, s>>>(left, right, frame_stride, pitch, w, h, a, b, g, lshift, m, wf + wr);
+    dim3 grid((w + RW_TX - 1) / RW_TX, walkers, sides * n_frames);
+    kern<<<grid, wpb * 32, smem, s>>>(left, right, frame_stride, pitch, w, h, a, b, g, lshift, tiles,
+                                              tile_stride, list_off);
     return cudaGetLastError();
   };
+  static const int walk_f = [] { const char* v = getenv("RG_ROWTILE_WALK1"); return v ? atoi(v) : 16; }();
+  static const int walk_r = [] { const char* v = getenv("RG_ROWTILE_WALK2"); return v ? atoi(v) : 32; }();
   static SmemAttr attr[4];
-  e = internal ? rowtile(census_rowtile_kernel<true, 1>, rw_smem<1>(), attr[0], fl, fr, gf, masks, rw_pr<1>(),
-                         rw_wpb<1>())
-               : rowtile(census_rowtile_kernel<false, 1>, rw_smem<1>(), attr[1], fl, fr, gf, masks, rw_pr<1>(),
-                         rw_wpb<1>());
+  e = internal ? rowtile(census_rowtile_kernel<true, 1>, rw_smem<1>(), attr[0], fl, fr, gf, walk_f, 2, rw_wpb<1>())
+               : rowtile(census_rowtile_kernel<false, 1>, rw_smem<1>(), attr[1], fl, fr, gf, walk_f, 2, rw_wpb<1>());
   if (e != cudaSuccess) return e;
-  e = internal ? rowtile(census_rowtile_kernel<true, 2>, rw_smem<2>(), attr[2], sl, sr, gs, masks + wf, rw_pr<2>(),
+  e = internal ? rowtile(census_rowtile_kernel<true, 2>, rw_smem<2>(), attr[2], sl, sr, gs, walk_r, 2 + tf_max,
                          rw_wpb<2>())
-               : rowtile(census_rowtile_kernel<false, 2>, rw_smem<2>(), attr[3], sl, sr, gs, masks + wf, rw_pr<2>(),
+               : rowtile(census_rowtile_kernel<false, 2>, rw_smem<2>(), attr[3], sl, sr, gs, walk_r, 2 + tf_max,
                          rw_wpb<2>());
   return e;
 }

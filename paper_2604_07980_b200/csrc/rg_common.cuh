@@ -205,6 +205,7 @@ cudaError_t launch_census_frames(const uint8_t* left, const uint8_t* right, int 
                                  uint32_t* sr, const PadGeom& gs, const int32_t* inv_x,
                                  const int32_t* inv_y, const int32_t* lshift, bool internal,
                                  cudaStream_t s);
+size_t census_rois_scratch_words(int n_frames, int h, int ch);
 cudaError_t launch_census_rois(const uint8_t* left, const uint8_t* right, int n_frames, int64_t frame_stride,
                                int pitch, int w, int h, uint32_t* fl, uint32_t* fr, const PadGeom& gf, uint32_t* sl,
                                uint32_t* sr, const PadGeom& gs, const int32_t* lshift, bool internal,
