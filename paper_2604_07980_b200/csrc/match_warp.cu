@@ -329,6 +329,11 @@ __device__ __forceinline__ void sweep_range(
     const VPoint<CT>* vp, int nv, const CT* R, const PadGeom& g,
                                             const rg_search_range& rg, int lane, Cand& best,
                                             unsigned long long& bkey, int& evals, int part = 0, int nparts = 1) {
+#ifdef RG_MW_SKIP_SWEEP  // measurement skeleton only: everything but the sweeps (results invalid)
+  if (lane == 0) best = Cand{1, 1, rg.dx_min, rg.dy_min};
+  bkey = fast_key(1, rg.dx_min, rg.dy_min);
+  return;
+#endif
   // lane-parallel chunks in balanced groups of <= CMAX; a short tail chunk
   // goes point-parallel.  nparts > 1: this warp sweeps the chunks
   // [part * nfull / nparts, (part + 1) * nfull / nparts) of every row offset

@@ -15,6 +15,8 @@
 // single verified block, CLOSE sorts the verified sub-block disparities
 // (x close_scale, :353) and keeps the longest tight run (:126-148); the range
 // z = f / ((1/b) d) is the canonical reprojection (geometry.hpp:124-146).
+#include <cstdlib>
+
 #include "rg_common.cuh"
 #include "rg_device.cuh"
 
@@ -306,6 +308,92 @@ __global__ void aggregate_values_kernel(const double* __restrict__ v, int n, dou
   }
 }
 
+// K4, warp per object (the default): FAR reads its one block; CLOSE
+// gathers its verified sub-block disparities (x close_scale) into a per-warp
+// shared-memory array of up to 64 (ballot compaction), sorts them with a
+// warp bitonic network (two elements per lane) and lane 0 runs the
+// longest-run scan (template_match.hpp:116-148).  Objects with more than 64
+// CLOSE blocks use the global scratch and a warp rank sort.  One launch of
+// F * out_stride warps instead of as many 128-thread CTAs.
+constexpr int kAggWarps = 8, kAggWarpCap = 64;
+__global__ void __launch_bounds__(kAggWarps * 32) aggregate_warp_kernel(
+    const ObjEntry* __restrict__ objs, const int32_t* __restrict__ out_count, int out_stride, int n_obj,
+    const rg_match_result* __restrict__ res, int slot_capacity, rg_ranger_config cfg, double focal,
+    double baseline, double* __restrict__ scratch, rg_object_disparity* __restrict__ out,
+    const int32_t* __restrict__ counters) {
+  __shared__ double vals[kAggWarps][kAggWarpCap];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int g = blockIdx.x * kAggWarps + wid;
+  if (g >= n_obj) return;
+  const int f = g / out_stride, k = g - f * out_stride;
+  if (k >= out_count[f] || counters[1]) return;  // no object / overflowed plan (re-run follows)
+  const ObjEntry e = objs[g];
+  if (e.slot_base + e.n_slots > slot_capacity) return;
+  int valid = 0, used = 0;
+  double disp = 0.0;
+  if (e.kind == RG_KIND_FAR) {
+    if (lane == 0) {  // template_match.hpp:338-347: the single FAR block, verified or invalid
+      const rg_match_result r = res[e.slot_base];
+      if (r.n_points >= 4 && r.has_value && r.verified) valid = 1, disp = r.dx_subpix, used = 1;
+    }
+  } else {
+    const bool big = e.n_slots > kAggWarpCap;
+    double* dst = big ? scratch + e.slot_base : vals[wid];
+    int m = 0;
+    for (int t0 = 0; t0 < e.n_slots; t0 += 32) {
+      const int t = t0 + lane;
+      bool ok = false;
+      double v = 0.0;
+      if (t < e.n_slots) {
+        const rg_match_result r = res[e.slot_base + t];
+        ok = r.n_points >= 4 && r.has_value && r.verified;
+        v = __dmul_rn(r.dx_subpix, (double)cfg.close_scale);  // template_match.hpp:353
+      }
+      const unsigned bal = __ballot_sync(0xffffffffu, ok);
+      if (ok) dst[m + __popc(bal & ((1u << lane) - 1u))] = v;
+      m += __popc(bal);
+    }
+    __syncwarp();
+    if (!big) {  // bitonic sort of 64 (padded with +inf), two elements per lane
+      const double inf = __longlong_as_double(0x7ff0000000000000LL);
+      for (int i = m + lane; i < kAggWarpCap; i += 32) dst[i] = inf;
+      __syncwarp();
+      for (int kk = 2; kk <= kAggWarpCap; kk <<= 1)
+        for (int j = kk >> 1; j > 0; j >>= 1) {
+          // compare-exchange pair p of 32: (i, i ^ j) with i the lower index
+          const int i = ((lane & ~(j - 1)) << 1) | (lane & (j - 1));
+          const int q = i ^ j;
+          const bool up = (i & kk) == 0;
+          const double a = dst[i], b = dst[q];
+          __syncwarp();
+          if ((a > b) == up) dst[i] = b, dst[q] = a;
+          __syncwarp();
+        }
+    } else {  // rank sort into the mirror region (scratch holds 2 * slot_capacity doubles)
+      double* o = scratch + slot_capacity + e.slot_base;
+      for (int i = lane; i < m; i += 32) {
+        const double x = dst[i];
+        int rank = 0;
+        for (int q = 0; q < m; ++q) rank += (dst[q] < x) || (dst[q] == x && q < i);
+        o[rank] = x;
+      }
+      __syncwarp();
+      dst = o;
+    }
+    if (lane == 0) dev_runs(dst, m, cfg.tau_d, cfg.n_min, &valid, &disp, &used);
+  }
+  if (lane == 0) {
+    rg_object_disparity od = out[g];
+    od.valid = valid;
+    od.disparity = disp;
+    od.n_blocks_used = used;
+    od.z_cam = 0.0;
+    if (valid && disp > 0 && focal > 0 && baseline > 0)
+      od.z_cam = __ddiv_rn(focal, __dmul_rn(__ddiv_rn(1.0, baseline), disp));
+    out[g] = od;
+  }
+}
+
 }  // namespace
 
 cudaError_t launch_plan_frames(const rg_detection* dets, const int32_t* det_off, int n_frames, int w,
@@ -324,9 +412,15 @@ cudaError_t launch_aggregate(const ObjEntry* objs, const int32_t* out_count, int
                              rg_ranger_config cfg, double focal, double baseline, double* scratch,
                              rg_object_disparity* out, const int32_t* counters, cudaStream_t s) {
   if (n_frames <= 0 || out_stride <= 0) return cudaSuccess;
-  aggregate_kernel<<<n_frames * out_stride, 128, 0, s>>>(objs, out_count, out_stride, res,
-                                                         slot_capacity, cfg, focal, baseline,
-                                                         scratch, out, counters);
+  static const bool cta = getenv("RG_AGG_CTA") != nullptr;  // A/B knob: the CTA-per-object kernel
+  const int n_obj = n_frames * out_stride;
+  if (!cta) {
+    aggregate_warp_kernel<<<(n_obj + kAggWarps - 1) / kAggWarps, kAggWarps * 32, 0, s>>>(
+        objs, out_count, out_stride, n_obj, res, slot_capacity, cfg, focal, baseline, scratch, out, counters);
+    return cudaGetLastError();
+  }
+  aggregate_kernel<<<n_obj, 128, 0, s>>>(objs, out_count, out_stride, res, slot_capacity, cfg, focal, baseline,
+                                         scratch, out, counters);
   return cudaGetLastError();
 }
 

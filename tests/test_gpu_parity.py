@@ -313,3 +313,23 @@ def test_auto_rect_search_downscale_on_device(ctx, chk, voff, ds):
     st, want, wc = chk.autorect(L, R, (200, 120, 440, 280), -3, 3, p.to_c())
     assert st == 0 and got == want
     assert counts == list(wc)
+
+
+@pytest.mark.parametrize("scale_m", [2.0, 6.0, 12.0])
+def test_close_object_with_many_sub_blocks(ctx, chk, scale_m):
+    """A large CLOSE box has rows x cols = (h / 24) x (w / 24) sub-blocks
+    (template_match.hpp:189-197): 2.0 m at 12 m gives ~8 x 12, 12 m ~ 27 x 40
+    (> 64: the aggregation's global-scratch rank sort); objects, kinds, block
+    counts and disparities bit-exact against the reference."""
+    sc = S.SceneConfig(width=960, height=640, seed=5, noise_sigma=2.0)
+    sc.objects = [S.place(sc, 1, 480, 320, 12.0, width_m=scale_m, height_m=scale_m * 0.7),
+                  S.place(sc, 2, 200, 150, 150.0)]
+    L, R = S.render_stereo_pair(sc)
+    dets = S.ground_truth_detections(sc)
+    cfg = rg.RangerConfig(max_objects=8, dx_max_far=128, dx_max_close=128)
+    got = rg.estimate_object_disparities(L, R, dets, cfg, focal_px=S.F_PX, baseline_m=S.BASELINE_M, ctx=ctx)
+    want, _ = chk.estimate(L, R, [det_c(d) for d in dets], cfg.to_c(), S.F_PX, S.BASELINE_M)
+    assert len(got) == len(want)
+    for g, w in zip(got, want):
+        assert (g.det_id, g.kind, g.n_blocks_used, g.valid) == (w.det_id, w.kind, w.n_blocks_used, bool(w.valid))
+        assert np.float64(g.disparity).tobytes() == np.float64(w.disparity).tobytes()
