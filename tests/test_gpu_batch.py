@@ -395,3 +395,33 @@ def test_large_blocks_fit_the_device_matcher(ctx, chk, grid, maxp, frames):
     for f in range(frames):
         want = _want(chk, L[f], R[f], D[f], cfg)
         assert int(cnt[f]) * 32 == len(want) and o[f, :len(want)].tobytes() == want
+
+
+@pytest.mark.parametrize("name,n", [("c1", 16), ("c2", 12), ("c3", 12)])
+def test_roi_census_batches_match_reference(ctx, chk, name, n):
+    """Batches of >= 12 frames take the ROI-row census (census_rows_kernel +
+    the warp row-tile kernels, compacted tile lists); a per-frame left shift
+    (rect correction) and detection lists that differ per frame included.
+    Every record equals the reference's."""
+    import torch
+
+    fn = {"c1": S.scene_c1, "c2": S.scene_c2, "c3": S.scene_c3}[name]
+    L, R, D, cfg, sc = _frames(fn, n)
+    D = [d if i % 3 else list(reversed(d[: max(1, len(d) - i)])) for i, d in enumerate(D)]
+    shifts = ((np.arange(n) % 5) - 2).astype(np.int32)
+    maxd = max(len(d) for d in D)
+    eng = FrameEngine(sc.width, sc.height, cfg, maxd, S.F_PX, S.BASELINE_M, ctx=ctx)
+    recs, offs = pack_detections(D)
+    dev = torch.device("cuda", 0)
+    dL, dR = torch.from_numpy(L).to(dev), torch.from_numpy(R).to(dev)
+    d_recs, d_offs = torch.from_numpy(recs.view(np.uint8)).to(dev), torch.from_numpy(offs).to(dev)
+    for sh in (None, shifts):
+        out = torch.zeros(n * eng.out_stride * 32, dtype=torch.uint8, device=dev)
+        cnt = torch.zeros(n, dtype=torch.int32, device=dev)
+        eng.range_device(dL, dR, d_recs, d_offs, out, cnt,
+                         left_shift=torch.from_numpy(sh).to(dev) if sh is not None else None)
+        o = out.cpu().numpy().reshape(n, -1)
+        for f in range(n):
+            Lf = L[f] if sh is None else np.ascontiguousarray(shift_vertical(L[f], int(sh[f])))
+            want = _want(chk, Lf, R[f], D[f], cfg)
+            assert int(cnt[f]) * 32 == len(want) and o[f, :len(want)].tobytes() == want, (name, f)
