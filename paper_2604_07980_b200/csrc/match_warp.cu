@@ -44,11 +44,17 @@ namespace {
 #ifndef RG_MW_NOINLINE
 #define RG_MW_NOINLINE 0
 #endif
+#ifndef RG_MW_DY2  // two row offsets per FAST point pass (sweep2): measured 0.98 vs 0.895 ms per
+#define RG_MW_DY2 0  // 256 C2 frames (1.30 vs 1.00 at 8 warps x 4 CTAs) -- an A/B knob
+#endif
 #ifndef RG_MW_CSA  // carry-save groups of 3 points in FAST sweeps: measured 1.22 vs 0.90 ms (loses the
 #define RG_MW_CSA 0  // one-point-ahead load pipelining; at 40 registers it spills) -- kept as an A/B knob
 #endif
 constexpr int kPipeUnroll = RG_MW_PIPE_UNROLL;
-constexpr int kWarpOcc = 32;
+#ifndef RG_MW_OCC
+#define RG_MW_OCC 32
+#endif
+constexpr int kWarpOcc = RG_MW_OCC;  // occluder boxes per warp in smem (more: the per-point scan of every detection)
 constexpr int kLatencyFrames = 4;  // batches up to this size use the latency-mode matcher      // occluder boxes per warp kept in smem
 constexpr int CMAX = RG_MW_CMAX;  // 32-wide dx chunks per sweep (balanced groups)
 constexpr int TAIL = RG_MW_TAIL;  // a last chunk with <= TAIL candidates goes point-parallel
@@ -251,6 +257,66 @@ __device__ __forceinline__ void sweep(const VPoint<CT>* __restrict__ vp, int nv,
   }
 }
 
+// FAST sweep of K dx-chunks for TWO row offsets dy, dy + 1 in one pass over
+// the points: one point record and one address per point feed 2K samples, and
+// twice as many independent loads are in flight (the point loop is bound by
+// the L1 latency of its one-point-ahead pipeline, ncu: long-scoreboard).
+template <typename CT, int K>
+__device__ __forceinline__ void sweep2(const VPoint<CT>* __restrict__ vp, int nv, const CT* base, int64_t pitch_b,
+                                       int lane, int c0, int ndx, int dx_min, int dy, unsigned long long& bkey,
+                                       int& evals) {
+  int s0[K], s1[K];
+#pragma unroll
+  for (int c = 0; c < K; ++c) s0[c] = s1[c] = 0;
+  VPoint<CT> qn = vp[0];
+  CT rn0[K], rn1[K];
+  {
+    const CT* a = reinterpret_cast<const CT*>(reinterpret_cast<const char*>(base) + qn.off);
+    const CT* b = reinterpret_cast<const CT*>(reinterpret_cast<const char*>(a) + pitch_b);
+#pragma unroll
+    for (int c = 0; c < K; ++c) rn0[c] = __ldg(a - 32 * c), rn1[c] = __ldg(b - 32 * c);
+  }
+#pragma unroll 2
+  for (int k = 0; k < nv; ++k) {
+    const CT l = qn.code;
+    CT r0[K], r1[K];
+#pragma unroll
+    for (int c = 0; c < K; ++c) r0[c] = rn0[c], r1[c] = rn1[c];
+    qn = vp[k + 1];  // vp[nv] duplicates vp[nv - 1] (warp_pass)
+    const CT* a = reinterpret_cast<const CT*>(reinterpret_cast<const char*>(base) + qn.off);
+    const CT* b = reinterpret_cast<const CT*>(reinterpret_cast<const char*>(a) + pitch_b);
+#pragma unroll
+    for (int c = 0; c < K; ++c) rn0[c] = __ldg(a - 32 * c), rn1[c] = __ldg(b - 32 * c);
+#pragma unroll
+    for (int c = 0; c < K; ++c) {
+      s0[c] += popc(l ^ r0[c]);
+      s1[c] += popc(l ^ r1[c]);
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < K; ++c) {
+    const int ix = lane + 32 * (c0 + c);
+    if (ix < ndx) {
+      evals += 2 * nv;  // Hamming evaluations, census.hpp:209-221
+      const unsigned long long k0 = fast_key(s0[c], dx_min + ix, dy), k1 = fast_key(s1[c], dx_min + ix, dy + 1);
+      bkey = k0 < bkey ? k0 : bkey;
+      bkey = k1 < bkey ? k1 : bkey;
+    }
+  }
+}
+
+template <typename CT>
+__device__ __forceinline__ void sweep2_chunks(const VPoint<CT>* vp, int nv, const CT* base, int64_t pitch_b,
+                                              int lane, int c0, int k, int ndx, int dx_min, int dy,
+                                              unsigned long long& bkey, int& evals) {
+  switch (k) {
+    case 1: sweep2<CT, 1>(vp, nv, base, pitch_b, lane, c0, ndx, dx_min, dy, bkey, evals); break;
+    case 2: sweep2<CT, 2>(vp, nv, base, pitch_b, lane, c0, ndx, dx_min, dy, bkey, evals); break;
+    case 3: sweep2<CT, 3>(vp, nv, base, pitch_b, lane, c0, ndx, dx_min, dy, bkey, evals); break;
+    default: sweep2<CT, 4>(vp, nv, base, pitch_b, lane, c0, ndx, dx_min, dy, bkey, evals); break;
+  }
+}
+
 template <typename CT, int MODE, int PF = 0>
 __device__ __forceinline__ void sweep_chunks(const VPoint<CT>* vp, int nv, const CT* base, int lane,
                                              int c0, int k, int ndx, int dx_min, int dy, Cand& best,
@@ -347,12 +413,23 @@ __device__ __forceinline__ void sweep_range(
   const int groups = (nmine + CMAX - 1) / CMAX;
   const int gq = groups ? nmine / groups : 0, gr = groups ? nmine - gq * groups : 0;  // balanced group sizes
   for (int dy = rg.dy_min; dy <= rg.dy_max; ++dy) {
+    // FAST throughput sweeps take two row offsets per pass over the points
+    const bool two = RG_MW_DY2 && MODE == M_FAST && PF == 0 && nparts == 1 && sizeof(CT) == 4 &&
+                     CMAX <= 4 && dy + 1 <= rg.dy_max;
     for (int gi = 0, c0 = cb; gi < groups; ++gi) {
       const int k = gq + (gi < gr ? 1 : 0);
       const CT* base = R + (int64_t)dy * g.pitch - rg.dx_min - lane - 32 * c0;
-      sweep_chunks<CT, MODE, PF>(vp, nv, base, lane, c0, k, ndx, rg.dx_min, dy, best, bkey, evals);
+      if (two)
+        sweep2_chunks<CT>(vp, nv, base, (int64_t)g.pitch * (int64_t)sizeof(CT), lane, c0, k, ndx, rg.dx_min, dy,
+                          bkey, evals);
+      else
+        sweep_chunks<CT, MODE, PF>(vp, nv, base, lane, c0, k, ndx, rg.dx_min, dy, best, bkey, evals);
       c0 += k;
     }
+    if (two && ptail && part == nparts - 1)  // the tail of row offset dy (dy + 1's follows below)
+      sweep_tail<CT, MODE>(vp, nv, R + (int64_t)dy * g.pitch, rg.dx_min + 32 * nfull, mt, dy, lane, best, bkey,
+                           evals);
+    if (two) ++dy;
     if (ptail && part == nparts - 1)
       sweep_tail<CT, MODE>(vp, nv, R + (int64_t)dy * g.pitch, rg.dx_min + 32 * nfull, mt, dy, lane, best, bkey,
                            evals);
