@@ -338,62 +338,89 @@ __global__ void RG_C2_BOUNDS census_pairs_kernel(
 // Every detection of the frame contributes (a superset of the selected ones:
 // the planner runs after the census).
 constexpr int RM_T = 128;
+constexpr int RW_TX = 120;  // source columns per warp tile (lanes 0..29 emit codes)
 __global__ void __launch_bounds__(RM_T) census_rows_kernel(const rg_detection* __restrict__ dets,
                                                           const int32_t* __restrict__ det_off, int w, int h,
                                                           double tau_s, int cw, int ch, int wf, int wr,
-                                                          uint32_t* __restrict__ mask, int tf, int tr, int tf_max,
-                                                          int tile_stride, int32_t* __restrict__ tiles) {
-  extern __shared__ uint32_t sm_rows[];
+                                                          uint32_t* __restrict__ mask, int dxf, int dxs, int nxt,
+                                                          int tf, int tr, int rtf, int rtr, int tile_stride,
+                                                          int32_t* __restrict__ tiles) {
+  extern __shared__ uint32_t sm_rows[];  // row masks (wf + wr), then the 2-D tile bitmaps (bf + br)
+  const int bf = (rtf * nxt + 31) / 32, br = (rtr * nxt + 31) / 32;
+  uint32_t* tbm = sm_rows + wf + wr;
+  __shared__ int s_pos[RM_T + 1];
   const int f = blockIdx.x;
-  for (int i = threadIdx.x; i < wf + wr; i += RM_T) sm_rows[i] = 0u;
+  for (int i = threadIdx.x; i < wf + wr + bf + br; i += RM_T) sm_rows[i] = 0u;
   __syncthreads();
   const int d0 = det_off[f], n = det_off[f + 1] - d0;
   const double sy = __ddiv_rn((double)ch, (double)h);  // template_match.hpp:305 double(ch) / h
+  const double sx = __ddiv_rn((double)cw, (double)w);  // template_match.hpp:305 double(cw) / w
   auto clampi = [](double v) { return (int)fmin(fmax(v, -1.0e9), 1.0e9); };
   for (int i = threadIdx.x; i < n; i += RM_T) {
     const rg_detection d = dets[d0 + i];
     const PBox b = pixel_box(d, w, h);
-    int a, e;
-    uint32_t* m;
-    if (dev_classify(d, w, h, tau_s) == RG_KIND_FAR) {  // add_roi(far_rois, box, 1, 1, .., 3, w, h)
+    int a, e, c0, c1, rows_per_tile, cols_per_tile, ntr;
+    uint32_t *m, *bm;
+    if (dev_classify(d, w, h, tau_s) == RG_KIND_FAR) {  // add_roi(far_rois, box, 1, 1, dx_max_far + 2, 3, w, h)
       a = max(0, clampi(floor(b.y0)) - 3);
       e = min(h, clampi(ceil(b.y1)) + 3 + 1);
-      m = sm_rows;
-    } else {  // add_roi(scaled_rois, box, cw / w, ch / h, .., 3, cw, ch)
+      c0 = max(0, clampi(floor(b.x0)) - (dxf + 2));
+      c1 = min(w, clampi(ceil(b.x1)) + (dxf + 2) + 1);
+      m = sm_rows, bm = tbm, rows_per_tile = tf, cols_per_tile = RW_TX, ntr = rtf;
+    } else {  // add_roi(scaled_rois, box, cw / w, ch / h, dx_scaled + 2, 3, cw, ch)
       a = max(0, clampi(floor(__dmul_rn(b.y0, sy))) - 3);
       e = min(ch, clampi(ceil(__dmul_rn(b.y1, sy))) + 3 + 1);
-      m = sm_rows + wf;
+      c0 = max(0, clampi(floor(__dmul_rn(b.x0, sx))) - (dxs + 2));
+      c1 = min(cw, clampi(ceil(__dmul_rn(b.x1, sx))) + (dxs + 2) + 1);
+      m = sm_rows + wf, bm = tbm + bf, rows_per_tile = tr, cols_per_tile = RW_TX / 2, ntr = rtr;
     }
     for (int y = a; y < e;) {
       const int wd = y >> 5, b0 = y & 31, nb = min(32 - b0, e - y);
       atomicOr(&m[wd], (nb == 32 ? 0xFFFFFFFFu : ((1u << nb) - 1u)) << b0);
       y += nb;
     }
+    if (a < e && c0 < c1)  // the warp tiles (fixed grid) the ROI rectangle touches
+      for (int rt = a / rows_per_tile; rt <= (e - 1) / rows_per_tile && rt < ntr; ++rt)
+        for (int xt = c0 / cols_per_tile; xt <= (c1 - 1) / cols_per_tile && xt < nxt; ++xt) {
+          const int bit = rt * nxt + xt;
+          atomicOr(&bm[bit >> 5], 1u << (bit & 31));
+        }
   }
   __syncthreads();
   for (int i = threadIdx.x; i < wf + wr; i += RM_T) mask[(int64_t)f * (wf + wr) + i] = sm_rows[i];
-  // compacted warp-tile lists: greedy even-aligned tiles of tf (full) / tr
-  // (reduced) rows covering every needed row, disjoint; tiles[f] = {n_full,
-  // n_red, full starts (tf_max), reduced starts}
-  if (threadIdx.x < 2) {
-    const int side = threadIdx.x;
-    const uint32_t* m = sm_rows + (side ? wf : 0);
-    const int rows = side ? ch : h, step = side ? tr : tf;
-    int32_t* rec = tiles + (int64_t)f * tile_stride;
-    int32_t* list = rec + 2 + (side ? tf_max : 0);
-    int n = 0;
-    for (int cur = 0; cur < rows;) {
-      int wd = cur >> 5;
-      uint32_t bits = m[wd] & (0xFFFFFFFFu << (cur & 31));
-      while (!bits && ++wd < (rows + 31) / 32) bits = m[wd];
-      if (!bits) break;
-      const int t = (wd << 5) + __ffs(bits) - 1;
-      if (t >= rows) break;
-      const int start = t & ~1;
-      list[n++] = start;
-      cur = start + step;
+  // compacted lists of the needed (row tile, column tile) pairs: entry =
+  // row_tile << 16 | column_tile; tiles[f] = {n_full, n_red, full list
+  // (rtf * nxt), reduced list (rtr * nxt)}
+  int32_t* rec = tiles + (int64_t)f * tile_stride;
+  for (int side = 0; side < 2; ++side) {
+    const uint32_t* bm = tbm + (side ? bf : 0);
+    const int nw = side ? br : bf;
+    int32_t* list = rec + 2 + (side ? rtf * nxt : 0);
+    int base = 0;
+    for (int w0 = 0; w0 < nw; w0 += RM_T) {
+      const int wd = w0 + threadIdx.x;
+      const uint32_t bits = wd < nw ? bm[wd] : 0u;
+      s_pos[threadIdx.x] = __popc(bits);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        int acc = 0;
+        for (int t = 0; t < RM_T; ++t) {
+          const int c = s_pos[t];
+          s_pos[t] = acc;
+          acc += c;
+        }
+        s_pos[RM_T] = acc;
+      }
+      __syncthreads();
+      int pos = base + s_pos[threadIdx.x];
+      for (uint32_t r = bits; r; r &= r - 1) {
+        const int bit = wd * 32 + __ffs(r) - 1;
+        list[pos++] = ((bit / nxt) << 16) | (bit % nxt);
+      }
+      base += s_pos[RM_T];
+      __syncthreads();
     }
-    rec[side] = n;
+    if (threadIdx.x == 0) rec[side] = base;
   }
 }
 
@@ -422,7 +449,6 @@ template <int STRIDE>
 #define RG_RW_PR2 3
 #endif
 __host__ __device__ constexpr int rw_pr() { return STRIDE == 1 ? 5 : RG_RW_PR2; }  // row pairs per warp tile
-constexpr int RW_TX = 120;  // source columns per warp tile (lanes 0..29 emit codes)
 constexpr int RW_VW = 136;  // V row stride: index 4 = source column x0 - 2
 template <int STRIDE>
 __host__ __device__ constexpr int rw_nv() { return 2 * STRIDE * (rw_pr<STRIDE>() - 1) + 5; }  // V rows (13 / 13)
@@ -440,19 +466,21 @@ __global__ void __launch_bounds__(rw_wpb<STRIDE>() * 32) census_rowtile_kernel(
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int sides = right ? 2 : 1;
   const int frame = blockIdx.z / sides, side = blockIdx.z - frame * sides;
-  // this warp walks its share of the frame's compacted tile list (every
-  // listed tile has a needed row; no CTA is launched for an empty one)
+  // this warp walks its share of the frame's compacted list of (row tile,
+  // column tile) pairs that some ROI rectangle touches (no CTA is launched
+  // for an empty tile)
   const int32_t* rec = tiles + (int64_t)frame * tile_stride;
   const int n_tiles = rec[STRIDE - 1];
   const int32_t* list = rec + list_off;
   uint32_t* V = Vall + wid * NV * RW_VW;
-  for (int ti = blockIdx.y * rw_wpb<STRIDE>() + wid; ti < n_tiles; ti += gridDim.y * rw_wpb<STRIDE>()) {
-  const int Y0 = list[ti];  // first output row of this tile (even)
+  for (int ti = blockIdx.x * rw_wpb<STRIDE>() + wid; ti < n_tiles; ti += gridDim.x * rw_wpb<STRIDE>()) {
+  const int ent = list[ti];
+  const int Y0 = (ent >> 16) * 2 * RW_PR;  // first output row of this tile (even)
+  const int x0 = (ent & 0xFFFF) * RW_TX;   // source column origin
   __syncwarp();  // the previous tile's window reads are done before V is rebuilt
   const int sh = (side == 0 && lshift) ? lshift[frame] : 0;  // shift_vertical of the left image
   const uint8_t* img = (side ? right : left) + (int64_t)frame * frame_stride;
   uint32_t* out = (side ? orr : ol) + (int64_t)frame * g.fstride + g.origin;
-  const int x0 = blockIdx.x * RW_TX;  // source column origin
   const int S0 = STRIDE * Y0 - 2;   // source row of V row 0
   // ---- V rows: word column k of image rows S0 .. S0 + NI - 1 (clamped);
   // entry (s, c) = half2(1024 + I(c, s), 1024 + I(c, s + STRIDE))
@@ -803,9 +831,9 @@ cudaError_t launch_census_frames(const uint8_t* left, const uint8_t* right, int 
 }
 
 // 32-bit words of the row masks + tile lists of launch_census_rois
-size_t census_rois_scratch_words(int n_frames, int h, int ch) {
-  const int tf = 2 * rw_pr<1>(), tr = 2 * rw_pr<2>();
-  return (size_t)n_frames * ((h + 31) / 32 + (ch + 31) / 32 + 2 + (h + tf - 1) / tf + (ch + tr - 1) / tr);
+size_t census_rois_scratch_words(int n_frames, int w, int h, int ch) {
+  const int tf = 2 * rw_pr<1>(), tr = 2 * rw_pr<2>(), nxt = (w + RW_TX - 1) / RW_TX;
+  return (size_t)n_frames * ((h + 31) / 32 + (ch + 31) / 32 + 2 + ((h + tf - 1) / tf + (ch + tr - 1) / tr) * nxt);
 }
 
 // ROI-row census of a batch (see census_rows_kernel): the row masks, the
@@ -815,8 +843,8 @@ size_t census_rois_scratch_words(int n_frames, int h, int ch) {
 cudaError_t launch_census_rois(const uint8_t* left, const uint8_t* right, int n_frames, int64_t frame_stride,
                                int pitch, int w, int h, uint32_t* fl, uint32_t* fr, const PadGeom& gf, uint32_t* sl,
                                uint32_t* sr, const PadGeom& gs, const int32_t* lshift, bool internal,
-                               const rg_detection* dets, const int32_t* det_off, double tau_s, uint32_t* masks,
-                               cudaStream_t s) {
+                               const rg_detection* dets, const int32_t* det_off, double tau_s, int dx_far,
+                               int dx_close_scaled, uint32_t* masks, cudaStream_t s) {
   if (n_frames <= 0) return cudaSuccess;
   const int sides = right ? 2 : 1;
   const bool aligned = (pitch % 4 == 0) && (w % 4 == 0) && (frame_stride % 4 == 0) &&
@@ -827,13 +855,15 @@ cudaError_t launch_census_rois(const uint8_t* left, const uint8_t* right, int n_
                     gs.w >= 4 && gs.h >= 4;
   if (!aligned || !half || !masks || !dets) return cudaErrorNotSupported;
   const int wf = (h + 31) / 32, wr = (gs.h + 31) / 32;
-  const int tf = 2 * rw_pr<1>(), tr = 2 * rw_pr<2>();                 // output rows per warp tile
-  const int tf_max = (h + tf - 1) / tf, tr_max = (gs.h + tr - 1) / tr;
-  const int tile_stride = 2 + tf_max + tr_max;
+  const int tf = 2 * rw_pr<1>(), tr = 2 * rw_pr<2>();  // output rows per warp tile
+  const int nxt = (w + RW_TX - 1) / RW_TX;              // column tiles (reduced: RW_TX / 2 columns)
+  const int rtf = (h + tf - 1) / tf, rtr = (gs.h + tr - 1) / tr;
+  const int tile_stride = 2 + (rtf + rtr) * nxt;
   int32_t* tiles = reinterpret_cast<int32_t*>(masks + (size_t)n_frames * (wf + wr));
-  census_rows_kernel<<<n_frames, RM_T, sizeof(uint32_t) * (wf + wr), s>>>(dets, det_off, w, h, tau_s, gs.w, gs.h,
-                                                                         wf, wr, masks, tf, tr, tf_max,
-                                                                         tile_stride, tiles);
+  const int bmw = (rtf * nxt + 31) / 32 + (rtr * nxt + 31) / 32;
+  census_rows_kernel<<<n_frames, RM_T, sizeof(uint32_t) * (wf + wr + bmw), s>>>(
+      dets, det_off, w, h, tau_s, gs.w, gs.h, wf, wr, masks, dx_far, dx_close_scaled, nxt, tf, tr, rtf, rtr,
+      tile_stride, tiles);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   static const int mode = [] {
@@ -853,28 +883,26 @@ cudaError_t launch_census_rois(const uint8_t* left, const uint8_t* right, int n_
                                               masks, wf + wr);
     return cudaGetLastError();
   }
-  // a fixed number of single-warp CTAs per (column tile, frame, side) walk the
-  // compacted lists (C2: ~40 full and ~80 reduced tiles per frame and side);
-  // 16 / 32 walkers measured best (4..48 / 8..96 tried: 1.069-1.12 ms per 256
-  // C2 frames, against 1.178 for one CTA per 10-row tile and mask skips)
+  // a fixed number of single-warp CTAs per (frame, side) walk the compacted
+  // 2-D tile lists
   auto rowtile = [&](auto kern, size_t smem, SmemAttr& attr, uint32_t* a, uint32_t* b, const PadGeom& g,
                      int walkers, int list_off, int wpb) -> cudaError_t {
     cudaError_t e2 = attr.ensure((const void*)kern, smem);
     if (e2 != cudaSuccess) return e2;
-    dim3 grid((w + RW_TX - 1) / RW_TX, walkers, sides * n_frames);
+    dim3 grid(walkers, 1, sides * n_frames);
     kern<<<grid, wpb * 32, smem, s>>>(left, right, frame_stride, pitch, w, h, a, b, g, lshift, tiles,
-                                              tile_stride, list_off);
+                                      tile_stride, list_off);
     return cudaGetLastError();
   };
-  static const int walk_f = [] { const char* v = getenv("RG_ROWTILE_WALK1"); return v ? atoi(v) : 16; }();
-  static const int walk_r = [] { const char* v = getenv("RG_ROWTILE_WALK2"); return v ? atoi(v) : 32; }();
+  static const int walk_f = [] { const char* v = getenv("RG_ROWTILE_WALK1"); return v ? atoi(v) : 256; }();
+  static const int walk_r = [] { const char* v = getenv("RG_ROWTILE_WALK2"); return v ? atoi(v) : 256; }();
   static SmemAttr attr[4];
   e = internal ? rowtile(census_rowtile_kernel<true, 1>, rw_smem<1>(), attr[0], fl, fr, gf, walk_f, 2, rw_wpb<1>())
                : rowtile(census_rowtile_kernel<false, 1>, rw_smem<1>(), attr[1], fl, fr, gf, walk_f, 2, rw_wpb<1>());
   if (e != cudaSuccess) return e;
-  e = internal ? rowtile(census_rowtile_kernel<true, 2>, rw_smem<2>(), attr[2], sl, sr, gs, walk_r, 2 + tf_max,
+  e = internal ? rowtile(census_rowtile_kernel<true, 2>, rw_smem<2>(), attr[2], sl, sr, gs, walk_r, 2 + rtf * nxt,
                          rw_wpb<2>())
-               : rowtile(census_rowtile_kernel<false, 2>, rw_smem<2>(), attr[3], sl, sr, gs, walk_r, 2 + tf_max,
+               : rowtile(census_rowtile_kernel<false, 2>, rw_smem<2>(), attr[3], sl, sr, gs, walk_r, 2 + rtf * nxt,
                          rw_wpb<2>());
   return e;
 }

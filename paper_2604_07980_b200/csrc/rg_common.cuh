@@ -205,12 +205,12 @@ cudaError_t launch_census_frames(const uint8_t* left, const uint8_t* right, int 
                                  uint32_t* sr, const PadGeom& gs, const int32_t* inv_x,
                                  const int32_t* inv_y, const int32_t* lshift, bool internal,
                                  cudaStream_t s);
-size_t census_rois_scratch_words(int n_frames, int h, int ch);
+size_t census_rois_scratch_words(int n_frames, int w, int h, int ch);
 cudaError_t launch_census_rois(const uint8_t* left, const uint8_t* right, int n_frames, int64_t frame_stride,
                                int pitch, int w, int h, uint32_t* fl, uint32_t* fr, const PadGeom& gf, uint32_t* sl,
                                uint32_t* sr, const PadGeom& gs, const int32_t* lshift, bool internal,
-                               const rg_detection* dets, const int32_t* det_off, double tau_s, uint32_t* masks,
-                               cudaStream_t s);
+                               const rg_detection* dets, const int32_t* det_off, double tau_s, int dx_far,
+                               int dx_close_scaled, uint32_t* masks, cudaStream_t s);
 cudaError_t launch_census64_frames(const uint8_t* left, const uint8_t* right, int n_frames, int64_t frame_stride,
                                    int pitch, int w, int h, unsigned long long* fl, unsigned long long* fr,
                                    const PadGeom& gf, unsigned long long* sl, unsigned long long* sr,
