@@ -45,25 +45,30 @@ def popc_peak_per_clk():
 N_SM = 148
 
 
-def census_required_bytes(dets, w, h, tau_s=48.0, scale=2):
+def census_required_bytes(dets, w, h, tau_s=48.0, scale=2, dx_far=256, dx_close=256):
     """Bytes K1 must move for one frame when it computes the reference's ROI
-    census (census_transform_rois rows, template_match.hpp:245-321): the two
-    images read once, full codes on the rows of FAR ROIs (box rows dilated by
-    3) and reduced codes on the rows of CLOSE ROIs, 4 B each, both sides.
-    -> (required bytes, FAR rows, CLOSE reduced rows)."""
+    census (census_transform_rois, template_match.hpp:245-321): the two images
+    read once, full codes inside the FAR ROI rectangles (box dilated by
+    dx_max_far + 2 columns and 3 rows) and reduced codes inside the CLOSE ROI
+    rectangles (reduced coordinates, dilated by ceil(dx_max_close / s) + 2 and
+    3), 4 B each, both sides.  -> (required bytes, FAR ROI pixels, CLOSE ROI
+    reduced pixels)."""
     import math
     cw, ch = w // scale, h // scale
-    full, red = np.zeros(h, bool), np.zeros(ch, bool)
-    sy = ch / h
+    full, red = np.zeros((h, w), bool), np.zeros((ch, cw), bool)
+    sx, sy = cw / w, ch / h
+    dxs = (dx_close + scale - 1) // scale
     for d in dets:
         x0, x1 = (d.cx - d.w / 2) * w, (d.cx + d.w / 2) * w
         y0, y1 = (d.cy - d.h / 2) * h, (d.cy + d.h / 2) * h
         if max(d.w * w, d.h * h) < tau_s:  # classify_far_close
-            full[max(0, math.floor(y0) - 3):min(h, math.ceil(y1) + 4)] = True
+            full[max(0, math.floor(y0) - 3):min(h, math.ceil(y1) + 4),
+                 max(0, math.floor(x0) - dx_far - 2):min(w, math.ceil(x1) + dx_far + 3)] = True
         else:
-            red[max(0, math.floor(y0 * sy) - 3):min(ch, math.ceil(y1 * sy) + 4)] = True
+            red[max(0, math.floor(y0 * sy) - 3):min(ch, math.ceil(y1 * sy) + 4),
+                max(0, math.floor(x0 * sx) - dxs - 2):min(cw, math.ceil(x1 * sx) + dxs + 3)] = True
     nf, nr = int(full.sum()), int(red.sum())
-    return 2 * (w * h + 4 * nf * w + 4 * nr * cw), nf, nr
+    return 2 * (w * h + 4 * nf + 4 * nr), nf, nr
 
 
 def peaks():
@@ -865,14 +870,14 @@ def main():
                    "kernel": "census_rows_kernel + census_rowtile_kernel<1> (FAR ROI rows, full raster) + "
                              "census_rowtile_kernel<2> (CLOSE ROI rows, reduced raster)",
                    "peak_source": peak_kind, "algorithmic_bytes_per_launch": req_frame * F,
-                   "algorithmic_bytes": "the reference's ROI census (census_transform_rois rows): both images read, "
-                                        f"{req_rows_full} full rows and {req_rows_red} reduced rows of 4-B codes "
-                                        "per image",
+                   "algorithmic_bytes": "the reference's ROI census (census_transform_rois rectangles): both "
+                                        f"images read, {req_rows_full} full-raster and {req_rows_red} reduced-raster "
+                                        "4-B codes per image",
                    "ms_per_launch": census_ms, "frac_of_nominal_8000_gbs": census_req_gbs / 8000.0,
                    "full_frame_equivalent": {
-                       "bytes_per_launch": CENSUS_BYTES_PER_FRAME * F, "achieved_gbs": census_gbs,
-                       "frac": census_gbs / hbm_peak,
-                       "note": "SURVEY 8(d) full-frame census bytes (24,883,200 per C2 frame) over the same time"}}
+                       "bytes_per_launch": CENSUS_BYTES_PER_FRAME * F, "effective_gbs": census_gbs,
+                       "note": "SURVEY 8(d) full-frame census bytes (24,883,200 per C2 frame) over the same time: "
+                               "an effective rate, not traffic (the ROI census computes a fraction of the frame)"}}
     match_roof = {"bound": "int/popc", "achieved": match_rate / 1e12, "peak": popc_peak / 1e12,
                   "unit": "Tevals/s", "frac": match_rate / popc_peak, "kernel": "match_slots_warp_kernel",
                   "hamming_evals_per_launch": evals_per_launch, "ms_per_launch": match_ms,
