@@ -874,19 +874,84 @@ __device__ __forceinline__ void finish(const Pass& p, rg_match_result& r) {  // 
   }
 }
 
+// Occluders of `det` (index self) among the frame's detections [d0, d1)
+// (find_occluders, template_match.hpp:71-89) into the warp's box list occ;
+// returns whether any did not fit (the sampler then scans every detection).
+__device__ __forceinline__ bool warp_occluders(const rg_detection& det, int self, const rg_detection* dets,
+                                               int d0, int d1, int img_w, int img_h, double* occ, int* nocc,
+                                               int lane) {
+  if (lane == 0) *nocc = 0;
+  __syncwarp();
+  bool overflow = false;
+  for (int j = d0 + lane; j < d1; j += 32) {
+    if (j == self) continue;
+    const rg_detection dj = dets[j];
+    if (!dev_occludes(det, dj)) continue;
+    const int k = atomicAdd(nocc, 1);
+    if (k < kWarpOcc) {
+      const PBox b = pixel_box(dj, img_w, img_h);
+      occ[4 * k] = b.x0;
+      occ[4 * k + 1] = b.y0;
+      occ[4 * k + 2] = b.x1;
+      occ[4 * k + 3] = b.y1;
+    } else {
+      overflow = true;
+    }
+  }
+  __syncwarp();
+  return __any_sync(0xffffffffu, overflow);
+}
+
+// K2a slot sampler: the QueryBlock points of every planned slot
+// (sample_query_points, template_match.hpp:155-223, in the reference's grid
+// order), one warp per slot, to pts[slot * maxp ...] with the count in
+// slots[slot].pad.  Run ahead of the matcher so the FP64 geometry and the
+// occluder scan execute at full occupancy instead of in front of each
+// matcher warp's sweeps.  FAR slots are [0, counters[0]), CLOSE slots
+// [capacity - counters[4], capacity) (plan.cu); an overflowed plan is left to
+// the matcher, which flags it.
+template <int WPB>
+__global__ void __launch_bounds__(WPB * 32) sample_slots_kernel(
+    Slot* __restrict__ slots, const int32_t* __restrict__ counters, const ObjEntry* __restrict__ objs,
+    const rg_detection* __restrict__ dets, const int32_t* __restrict__ det_off, int img_w, int img_h,
+    rg_ranger_config cfg, int2* __restrict__ pts_out, rg_ranger_stats* __restrict__ stats, int maxp,
+    int capacity) {
+  __shared__ double occ[WPB][4 * kWarpOcc];
+  __shared__ int nocc[WPB];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int slot = blockIdx.x * WPB + warp;
+  const int n_lo = counters[0], n_hi = counters[4];
+  if (n_lo + n_hi > capacity || counters[1]) return;
+  if ((slot >= n_lo && slot < capacity - n_hi) || slot >= capacity) return;  // warp-uniform
+  const Slot s = slots[slot];
+  const ObjEntry e = objs[s.obj];
+  const rg_detection det = dets[e.det];
+  const int d0 = det_off[s.frame], d1 = det_off[s.frame + 1];
+  const bool all = warp_occluders(det, e.det, dets, d0, d1, img_w, img_h, occ[warp], &nocc[warp], lane);
+  const int cols = max(e.cols, 1);
+  const int np = dev_sample_block_warp(det, e.kind, s.sub / cols, s.sub % cols, e.rows, e.cols, occ[warp],
+                                       min(nocc[warp], kWarpOcc), all ? dets + d0 : nullptr, d1 - d0,
+                                       e.det - d0, cfg, img_w, img_h, pts_out + (size_t)slot * maxp);
+  if (lane == 0) {
+    slots[slot].pad = np;
+    if (stats && np >= 4)
+      atomicAdd(reinterpret_cast<unsigned long long*>(&stats[s.frame].query_points), (unsigned long long)np);
+  }
+}
+
 // COOP (latency mode): a CTA per FAR block, its warps splitting the dx
 // chunks of both passes (the FAR block is the critical path of a small
 // batch: ~5x a CLOSE sub-block); CLOSE sub-blocks stay one per warp.
-template <typename CT, int WPB, int MINB, int PF = 0, bool COOP = false, bool V2 = false>
+template <typename CT, int WPB, int MINB, int PF = 0, bool COOP = false, bool V2 = false, bool PRE = false>
 __global__ void __launch_bounds__(WPB * 32, MINB) match_slots_warp_kernel(
-    const Slot* __restrict__ slots, int32_t* __restrict__ counters, const ObjEntry* __restrict__ objs,
+    const int2* __restrict__ pre_pts, const Slot* __restrict__ slots, int32_t* __restrict__ counters, const ObjEntry* __restrict__ objs,
     const rg_detection* __restrict__ dets, const int32_t* __restrict__ det_off,
     const CT* __restrict__ fl, const CT* __restrict__ fr, PadGeom gf,
     const CT* __restrict__ sl, const CT* __restrict__ sr, PadGeom gs, int img_w,
     int img_h, int trusted, rg_ranger_config cfg, rg_match_result* __restrict__ res,
     rg_ranger_stats* __restrict__ stats, int maxp, int capacity) {
   extern __shared__ __align__(16) unsigned char wsm_raw[];
-  __shared__ double occ[WPB][4 * kWarpOcc];
+  __shared__ double occ[PRE ? 1 : WPB][4 * kWarpOcc];
   __shared__ int nocc[WPB];
   __shared__ Cand xc[WPB];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -907,34 +972,23 @@ __global__ void __launch_bounds__(WPB * 32, MINB) match_slots_warp_kernel(
     int2* pts = reinterpret_cast<int2*>(wbase);
     VPoint<CT>* vp = reinterpret_cast<VPoint<CT>*>(wbase + sizeof(int2) * maxp);
     const Slot s = slots[slot];
-    const ObjEntry e = objs[s.obj];
-    const rg_detection det = dets[e.det];
-    const int d0 = det_off[s.frame], d1 = det_off[s.frame + 1];
-    // occluders of this detection among the frame's detections (:71-89)
-    if (lane == 0) nocc[warp] = 0;
-    __syncwarp();
-    bool overflow = false;
-    for (int j = d0 + lane; j < d1; j += 32) {
-      if (j == e.det) continue;
-      const rg_detection dj = dets[j];
-      if (!dev_occludes(det, dj)) continue;
-      const int k = atomicAdd(&nocc[warp], 1);
-      if (k < kWarpOcc) {
-        const PBox b = pixel_box(dj, img_w, img_h);
-        occ[warp][4 * k] = b.x0;
-        occ[warp][4 * k + 1] = b.y0;
-        occ[warp][4 * k + 2] = b.x1;
-        occ[warp][4 * k + 3] = b.y1;
-      } else {
-        overflow = true;
-      }
+    int np;
+    bool far;
+    if constexpr (PRE) {  // K2a sampled the slot (FAR slots sit below n_lo)
+      np = s.pad;
+      far = slot < n_lo;
+      pts = const_cast<int2*>(pre_pts) + (size_t)slot * maxp;
+    } else {
+      const ObjEntry e = objs[s.obj];
+      const rg_detection det = dets[e.det];
+      const int d0 = det_off[s.frame], d1 = det_off[s.frame + 1];
+      const bool all = warp_occluders(det, e.det, dets, d0, d1, img_w, img_h, occ[warp], &nocc[warp], lane);
+      const int cols = max(e.cols, 1);
+      np = dev_sample_block_warp(det, e.kind, s.sub / cols, s.sub % cols, e.rows, e.cols, occ[warp],
+                                 min(nocc[warp], kWarpOcc), all ? dets + d0 : nullptr, d1 - d0, e.det - d0, cfg,
+                                 img_w, img_h, pts);
+      far = e.kind == RG_KIND_FAR;
     }
-    __syncwarp();
-    const bool all = __any_sync(0xffffffffu, overflow);
-    const int cols = max(e.cols, 1);
-    const int np = dev_sample_block_warp(det, e.kind, s.sub / cols, s.sub % cols, e.rows, e.cols,
-                                         occ[warp], min(nocc[warp], kWarpOcc), all ? dets + d0 : nullptr,
-                                         d1 - d0, e.det - d0, cfg, img_w, img_h, pts);
     rg_match_result r;
     r.dx_int = r.dy_int = 0;
     r.dx_subpix = r.cost = 0.0;
@@ -943,7 +997,6 @@ __global__ void __launch_bounds__(WPB * 32, MINB) match_slots_warp_kernel(
     r.n_points = np;
     int evals = 0;
     if (np >= 4) {  // blocks with < 4 points are dropped (:185, :219)
-      const bool far = e.kind == RG_KIND_FAR;
       const PadGeom& g = far ? gf : gs;
       const int64_t fo = (int64_t)s.frame * g.fstride + g.origin;
       const CT* L = (far ? fl : sl) + fo;
@@ -975,8 +1028,8 @@ __global__ void __launch_bounds__(WPB * 32, MINB) match_slots_warp_kernel(
       if (evals) atomicAdd(reinterpret_cast<unsigned long long*>(counters + 2), (unsigned long long)evals);
       if (part == 0) {
         res[slot] = r;
-        if (stats && np >= 4) atomicAdd(reinterpret_cast<unsigned long long*>(&stats[s.frame].query_points),
-                                        (unsigned long long)np);
+        if (!PRE && stats && np >= 4)
+          atomicAdd(reinterpret_cast<unsigned long long*>(&stats[s.frame].query_points), (unsigned long long)np);
       }
     }
   };
@@ -997,14 +1050,14 @@ __global__ void __launch_bounds__(WPB * 32, MINB) match_slots_warp_kernel(
   }
 }
 
-template <typename CT, int WPB, int MINB, int PF = 0, bool COOP = false, bool V2 = false>
-cudaError_t launch_variant(const Slot* slots, int32_t* counters, int slot_capacity,
+template <typename CT, int WPB, int MINB, int PF = 0, bool COOP = false, bool V2 = false, bool PRE = false>
+cudaError_t launch_variant(int2* slot_pts, Slot* slots, int32_t* counters, int slot_capacity,
                                   const ObjEntry* objs, const rg_detection* dets, const int32_t* det_off,
                                   const void* fl, const void* fr, const PadGeom& gf, const void* sl,
                                   const void* sr, const PadGeom& gs, int img_w, int img_h, int trusted,
                                   rg_ranger_config cfg, rg_match_result* res, rg_ranger_stats* stats,
                                   int max_points, cudaStream_t s) {
-  auto kern = match_slots_warp_kernel<CT, WPB, MINB, PF, COOP, V2>;
+  auto kern = match_slots_warp_kernel<CT, WPB, MINB, PF, COOP, V2, PRE>;
   max_points = (max_points + 1) & ~1;  // keeps every warp's VPoint array 16-B aligned
   const size_t smem = (sizeof(int2) * (size_t)max_points + sizeof(VPoint<CT>) * (size_t)(max_points + 1)) * WPB;
   // the opt-in covers static + dynamic shared memory (occluder boxes etc. are static)
@@ -1021,7 +1074,13 @@ cudaError_t launch_variant(const Slot* slots, int32_t* counters, int slot_capaci
   // COOP: about one wave of CTAs walks the work items (their count is only
   // known on the device)
   const int grid = COOP ? std::min(slot_capacity, 148 * MINB) : (slot_capacity + WPB - 1) / WPB;
-  kern<<<grid, WPB * 32, smem, s>>>(slots, counters, objs, dets, det_off, static_cast<const CT*>(fl),
+  if (PRE) {
+    if (!slot_pts) return cudaErrorInvalidValue;
+    constexpr int SW = 8;
+    sample_slots_kernel<SW><<<(slot_capacity + SW - 1) / SW, SW * 32, 0, s>>>(
+        slots, counters, objs, dets, det_off, img_w, img_h, cfg, slot_pts, stats, max_points, slot_capacity);
+  }
+  kern<<<grid, WPB * 32, smem, s>>>(slot_pts, slots, counters, objs, dets, det_off, static_cast<const CT*>(fl),
                                     static_cast<const CT*>(fr), gf, static_cast<const CT*>(sl),
                                     static_cast<const CT*>(sr), gs, img_w, img_h, trusted, cfg, res, stats,
                                     max_points, slot_capacity);
@@ -1030,19 +1089,25 @@ cudaError_t launch_variant(const Slot* slots, int32_t* counters, int slot_capaci
 
 }  // namespace
 
-cudaError_t launch_match_slots(const Slot* slots, int32_t* counters, int slot_capacity,
+cudaError_t launch_match_slots(int2* slot_pts, Slot* slots, int32_t* counters, int slot_capacity,
                                const ObjEntry* objs, const rg_detection* dets, const int32_t* det_off,
                                const void* fl, const void* fr, const PadGeom& gf, const void* sl,
                                const void* sr, const PadGeom& gs, int img_w, int img_h, int trusted,
                                int wide, rg_ranger_config cfg, rg_match_result* res,
                                rg_ranger_stats* stats, int max_points, cudaStream_t s,
-                               int n_frames) {
+                               int n_frames, int* launches) {
+  if (launches) *launches = 1;
   if (slot_capacity <= 0) return cudaSuccess;
   static int variant = [] {
     const char* v = getenv("RG_MATCH_VARIANT");
     return v ? atoi(v) : 0;
   }();
-#define RG_ARGS slots, counters, slot_capacity, objs, dets, det_off, fl, fr, gf, sl, sr, gs, img_w, img_h, \
+  // K2a ahead of the matcher (default) or the in-warp sampler (RG_MATCH_PRE=0)
+  static const bool pre = [] {
+    const char* v = getenv("RG_MATCH_PRE");
+    return v ? atoi(v) != 0 : true;
+  }();
+#define RG_ARGS slot_pts, slots, counters, slot_capacity, objs, dets, det_off, fl, fr, gf, sl, sr, gs, img_w, img_h, \
                 trusted, cfg, res, stats, max_points, s
   // blocks too large for the default warps per CTA fall back to fewer
   // (shared memory holds every warp's points: 16 or 24 B per point)
@@ -1081,7 +1146,10 @@ cudaError_t launch_match_slots(const Slot* slots, int32_t* counters, int slot_ca
     case 8: return launch_variant<uint32_t, 16, 3, 0, false, true>(RG_ARGS);
     case 9: return launch_variant<uint32_t, 8, 4, 0, false, true>(RG_ARGS);
     case 10: return launch_variant<uint32_t, 16, 2, 0, false, true>(RG_ARGS);
-    default: return small(launch_variant<uint32_t, 16, 3>(RG_ARGS));
+    default:
+      if (launches && pre && slot_pts) *launches = 2;
+      return small(pre && slot_pts ? launch_variant<uint32_t, 16, 3, 0, false, false, true>(RG_ARGS)
+                                   : launch_variant<uint32_t, 16, 3>(RG_ARGS));
   }
 #undef RG_ARGS
 }

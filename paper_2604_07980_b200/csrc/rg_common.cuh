@@ -150,8 +150,8 @@ struct rg_ctx {
   int slot_capacity = 0;    // grows on RG_EOVERFLOW
   int64_t last_slots = 0;   // slots used by the last batch
   // grow-only device scratch, keyed by role
-  void* buf[40] = {};
-  size_t cap[40] = {};
+  void* buf[48] = {};
+  size_t cap[48] = {};
   // pinned host scratch
   void* hbuf[8] = {};
   size_t hcap[8] = {};
@@ -178,7 +178,7 @@ enum BufId {
   B_OBJ, B_SLOTS, B_SLOT_RES, B_OUT, B_OUT_CNT, B_COUNTERS, B_MAPX, B_MAPY,
   B_PTS, B_OFFS, B_RANGES, B_MRES, B_TMP0, B_TMP1, B_TMP2, B_TMP3, B_STATS,
   B_BM_L, B_BM_R, B_BM_OUT, B_BM_CNT, B_ROIS, B_STAGE_L, B_STAGE_R, B_SHIFT,
-  B_SEQ, B_SGM_COST, B_SGM_ACC, B_BOX_IDX, B_BOX_OUT, B_SYNTH, B_ROWMASK, B_COUNT
+  B_SEQ, B_SGM_COST, B_SGM_ACC, B_BOX_IDX, B_BOX_OUT, B_SYNTH, B_ROWMASK, B_SLOT_PTS, B_COUNT
 };
 
 // error helpers (defined in api.cu)
@@ -228,14 +228,16 @@ cudaError_t launch_match_blocks64(Raster64 L, Raster64 R, const int32_t* pts, co
                                   const rg_search_range* ranges, int n_blocks, int mode,
                                   double tau_v, rg_match_result* out, int max_points,
                                   cudaStream_t s);
-cudaError_t launch_match_slots(const Slot* slots, int32_t* counters, int slot_capacity,
+// slot_pts: capacity x ((max_points + 1) & ~1) points for the slot sampler
+// (nullptr: the matcher samples in-warp)
+cudaError_t launch_match_slots(int2* slot_pts, Slot* slots, int32_t* counters, int slot_capacity,
                                const ObjEntry* objs, const rg_detection* dets,
                                const int32_t* det_off, const void* fl, const void* fr,
                                const PadGeom& gf, const void* sl, const void* sr,
                                const PadGeom& gs, int img_w, int img_h, int trusted, int wide,
                                rg_ranger_config cfg, rg_match_result* res,
                                rg_ranger_stats* stats, int max_points, cudaStream_t s,
-                               int n_frames = 0);
+                               int n_frames = 0, int* launches = nullptr);
 
 // box statistics of dense maps (dense.cu)
 cudaError_t launch_radar_votes(const int16_t* raw, int w, const int32_t* boxes, const double* d_radar, int n,
