@@ -344,13 +344,15 @@ __global__ void __launch_bounds__(RM_T) census_rows_kernel(const rg_detection* _
                                                           double tau_s, int cw, int ch, int wf, int wr,
                                                           uint32_t* __restrict__ mask, int dxf, int dxs, int nxt,
                                                           int tf, int tr, int rtf, int rtr, int tile_stride,
-                                                          int32_t* __restrict__ tiles) {
-  extern __shared__ uint32_t sm_rows[];  // row masks (wf + wr), then the 2-D tile bitmaps (bf + br)
+                                                          int32_t* __restrict__ tiles, int tight) {
+  // row masks (wf + wr), then the 2-D tile bitmaps (bf + br) of the left and
+  // of the right image
+  extern __shared__ uint32_t sm_rows[];
   const int bf = (rtf * nxt + 31) / 32, br = (rtr * nxt + 31) / 32;
   uint32_t* tbm = sm_rows + wf + wr;
   __shared__ int s_pos[RM_T + 1];
   const int f = blockIdx.x;
-  for (int i = threadIdx.x; i < wf + wr + bf + br; i += RM_T) sm_rows[i] = 0u;
+  for (int i = threadIdx.x; i < wf + wr + 2 * (bf + br); i += RM_T) sm_rows[i] = 0u;
   __syncthreads();
   const int d0 = det_off[f], n = det_off[f + 1] - d0;
   const double sy = __ddiv_rn((double)ch, (double)h);  // template_match.hpp:305 double(ch) / h
@@ -359,43 +361,64 @@ __global__ void __launch_bounds__(RM_T) census_rows_kernel(const rg_detection* _
   for (int i = threadIdx.x; i < n; i += RM_T) {
     const rg_detection d = dets[d0 + i];
     const PBox b = pixel_box(d, w, h);
-    int a, e, c0, c1, rows_per_tile, cols_per_tile, ntr;
+    int bx0, bx1, by0, by1, dxm, W, H, rows_per_tile, cols_per_tile, ntr;
     uint32_t *m, *bm;
     if (dev_classify(d, w, h, tau_s) == RG_KIND_FAR) {  // add_roi(far_rois, box, 1, 1, dx_max_far + 2, 3, w, h)
-      a = max(0, clampi(floor(b.y0)) - 3);
-      e = min(h, clampi(ceil(b.y1)) + 3 + 1);
-      c0 = max(0, clampi(floor(b.x0)) - (dxf + 2));
-      c1 = min(w, clampi(ceil(b.x1)) + (dxf + 2) + 1);
+      by0 = clampi(floor(b.y0)), by1 = clampi(ceil(b.y1));
+      bx0 = clampi(floor(b.x0)), bx1 = clampi(ceil(b.x1));
+      dxm = dxf + 2, W = w, H = h;
       m = sm_rows, bm = tbm, rows_per_tile = tf, cols_per_tile = RW_TX, ntr = rtf;
     } else {  // add_roi(scaled_rois, box, cw / w, ch / h, dx_scaled + 2, 3, cw, ch)
-      a = max(0, clampi(floor(__dmul_rn(b.y0, sy))) - 3);
-      e = min(ch, clampi(ceil(__dmul_rn(b.y1, sy))) + 3 + 1);
-      c0 = max(0, clampi(floor(__dmul_rn(b.x0, sx))) - (dxs + 2));
-      c1 = min(cw, clampi(ceil(__dmul_rn(b.x1, sx))) + (dxs + 2) + 1);
+      by0 = clampi(floor(__dmul_rn(b.y0, sy))), by1 = clampi(ceil(__dmul_rn(b.y1, sy)));
+      bx0 = clampi(floor(__dmul_rn(b.x0, sx))), bx1 = clampi(ceil(__dmul_rn(b.x1, sx)));
+      dxm = dxs + 2, W = cw, H = ch;
       m = sm_rows + wf, bm = tbm + bf, rows_per_tile = tr, cols_per_tile = RW_TX / 2, ntr = rtr;
     }
+    // the reference's ROI rectangle: rows [a, e), columns [c0, c1)
+    const int a = max(0, by0 - 3), e = min(H, by1 + 3 + 1);
+    const int c0 = max(0, bx0 - dxm), c1 = min(W, bx1 + dxm + 1);
     for (int y = a; y < e;) {
       const int wd = y >> 5, b0 = y & 31, nb = min(32 - b0, e - y);
       atomicOr(&m[wd], (nb == 32 ? 0xFFFFFFFFu : ((1u << nb) - 1u)) << b0);
       y += nb;
     }
-    if (a < e && c0 < c1)  // the warp tiles (fixed grid) the ROI rectangle touches
-      for (int rt = a / rows_per_tile; rt <= (e - 1) / rows_per_tile && rt < ntr; ++rt)
-        for (int xt = c0 / cols_per_tile; xt <= (c1 - 1) / cols_per_tile && xt < nxt; ++xt) {
-          const int bit = rt * nxt + xt;
-          atomicOr(&bm[bit >> 5], 1u << (bit & 31));
-        }
+    // tight != 0: only the codes of the rectangle the matcher can read.  Its
+    // block points lie in the box rows / columns [b*0, b*1] (lround of
+    // coordinates inside the box); the forward pass reads the left image at
+    // the points and the right one at (x - dx, y + dy), dx in [0, dx_max],
+    // |dy| <= 1; the backward pass reads the right image at the points
+    // shifted by (-dx*, dy*) and the left one at (x - dx* + dx', y), dx' in
+    // [0, dx_max].  So the left image needs the box rows (+-1 margin) across
+    // the whole ROI width, the right one the box rows +-1 (+-1 margin) from
+    // the ROI's left edge to the box's right edge (+2 margin).  The other
+    // codes of the rectangle are never read.
+    for (int img = 0; img < 2; ++img) {
+      int ra = a, re = e, ca = c0, ce = c1;
+      if (tight) {
+        ra = max(0, by0 - 1 - img), re = min(H, by1 + 2 + img);
+        if (img) ce = min(W, bx1 + 3);
+      }
+      uint32_t* sbm = bm + img * (bf + br);
+      if (ra < re && ca < ce)  // the warp tiles (fixed grid) the rectangle touches
+        for (int rt = ra / rows_per_tile; rt <= (re - 1) / rows_per_tile && rt < ntr; ++rt)
+          for (int xt = ca / cols_per_tile; xt <= (ce - 1) / cols_per_tile && xt < nxt; ++xt) {
+            const int bit = rt * nxt + xt;
+            atomicOr(&sbm[bit >> 5], 1u << (bit & 31));
+          }
+    }
   }
   __syncthreads();
   for (int i = threadIdx.x; i < wf + wr; i += RM_T) mask[(int64_t)f * (wf + wr) + i] = sm_rows[i];
   // compacted lists of the needed (row tile, column tile) pairs: entry =
-  // row_tile << 16 | column_tile; tiles[f] = {n_full, n_red, full list
-  // (rtf * nxt), reduced list (rtr * nxt)}
+  // row_tile << 16 | column_tile; tiles[f] = {n_full_left, n_red_left,
+  // n_full_right, n_red_right, then per image: full list (rtf * nxt),
+  // reduced list (rtr * nxt)}
   int32_t* rec = tiles + (int64_t)f * tile_stride;
-  for (int side = 0; side < 2; ++side) {
-    const uint32_t* bm = tbm + (side ? bf : 0);
+  for (int q = 0; q < 4; ++q) {
+    const int img = q >> 1, side = q & 1;  // side: 0 full, 1 reduced raster
+    const uint32_t* bm = tbm + img * (bf + br) + (side ? bf : 0);
     const int nw = side ? br : bf;
-    int32_t* list = rec + 2 + (side ? rtf * nxt : 0);
+    int32_t* list = rec + 4 + img * (rtf + rtr) * nxt + (side ? rtf * nxt : 0);
     int base = 0;
     for (int w0 = 0; w0 < nw; w0 += RM_T) {
       const int wd = w0 + threadIdx.x;
@@ -420,7 +443,7 @@ __global__ void __launch_bounds__(RM_T) census_rows_kernel(const rg_detection* _
       base += s_pos[RM_T];
       __syncthreads();
     }
-    if (threadIdx.x == 0) rec[side] = base;
+    if (threadIdx.x == 0) rec[q] = base;
   }
 }
 
@@ -459,7 +482,7 @@ template <bool S31, int STRIDE>
 __global__ void __launch_bounds__(rw_wpb<STRIDE>() * 32) census_rowtile_kernel(
     const uint8_t* __restrict__ left, const uint8_t* __restrict__ right, int64_t frame_stride, int pitch, int w,
     int h, uint32_t* __restrict__ ol, uint32_t* __restrict__ orr, PadGeom g, const int32_t* __restrict__ lshift,
-    const int32_t* __restrict__ tiles, int tile_stride, int list_off) {
+    const int32_t* __restrict__ tiles, int tile_stride, int list_off, int side_off) {
   constexpr int NV = rw_nv<STRIDE>(), NI = NV + STRIDE;  // V rows, image rows
   constexpr int RW_PR = rw_pr<STRIDE>();
   extern __shared__ __align__(16) uint32_t Vall[];
@@ -470,8 +493,8 @@ __global__ void __launch_bounds__(rw_wpb<STRIDE>() * 32) census_rowtile_kernel(
   // column tile) pairs that some ROI rectangle touches (no CTA is launched
   // for an empty tile)
   const int32_t* rec = tiles + (int64_t)frame * tile_stride;
-  const int n_tiles = rec[STRIDE - 1];
-  const int32_t* list = rec + list_off;
+  const int n_tiles = rec[2 * side + STRIDE - 1];
+  const int32_t* list = rec + list_off + side * side_off;
   uint32_t* V = Vall + wid * NV * RW_VW;
   for (int ti = blockIdx.x * rw_wpb<STRIDE>() + wid; ti < n_tiles; ti += gridDim.x * rw_wpb<STRIDE>()) {
   const int ent = list[ti];
@@ -833,7 +856,7 @@ cudaError_t launch_census_frames(const uint8_t* left, const uint8_t* right, int 
 // 32-bit words of the row masks + tile lists of launch_census_rois
 size_t census_rois_scratch_words(int n_frames, int w, int h, int ch) {
   const int tf = 2 * rw_pr<1>(), tr = 2 * rw_pr<2>(), nxt = (w + RW_TX - 1) / RW_TX;
-  return (size_t)n_frames * ((h + 31) / 32 + (ch + 31) / 32 + 2 + ((h + tf - 1) / tf + (ch + tr - 1) / tr) * nxt);
+  return (size_t)n_frames * ((h + 31) / 32 + (ch + 31) / 32 + 4 + 2 * ((h + tf - 1) / tf + (ch + tr - 1) / tr) * nxt);
 }
 
 // ROI-row census of a batch (see census_rows_kernel): the row masks, the
@@ -858,12 +881,19 @@ cudaError_t launch_census_rois(const uint8_t* left, const uint8_t* right, int n_
   const int tf = 2 * rw_pr<1>(), tr = 2 * rw_pr<2>();  // output rows per warp tile
   const int nxt = (w + RW_TX - 1) / RW_TX;              // column tiles (reduced: RW_TX / 2 columns)
   const int rtf = (h + tf - 1) / tf, rtr = (gs.h + tr - 1) / tr;
-  const int tile_stride = 2 + (rtf + rtr) * nxt;
+  const int side_off = (rtf + rtr) * nxt;
+  const int tile_stride = 4 + 2 * side_off;
   int32_t* tiles = reinterpret_cast<int32_t*>(masks + (size_t)n_frames * (wf + wr));
-  const int bmw = (rtf * nxt + 31) / 32 + (rtr * nxt + 31) / 32;
+  const int bmw = 2 * ((rtf * nxt + 31) / 32 + (rtr * nxt + 31) / 32);
+  // A/B knob: RG_CENSUS_TIGHT=0 computes the reference's whole ROI rectangles
+  // on both images; default: only the part of each the matcher reads
+  static const int tight = [] {
+    const char* v = getenv("RG_CENSUS_TIGHT");
+    return v ? atoi(v) : 1;
+  }();
   census_rows_kernel<<<n_frames, RM_T, sizeof(uint32_t) * (wf + wr + bmw), s>>>(
       dets, det_off, w, h, tau_s, gs.w, gs.h, wf, wr, masks, dx_far, dx_close_scaled, nxt, tf, tr, rtf, rtr,
-      tile_stride, tiles);
+      tile_stride, tiles, tight);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   static const int mode = [] {
@@ -891,18 +921,18 @@ cudaError_t launch_census_rois(const uint8_t* left, const uint8_t* right, int n_
     if (e2 != cudaSuccess) return e2;
     dim3 grid(walkers, 1, sides * n_frames);
     kern<<<grid, wpb * 32, smem, s>>>(left, right, frame_stride, pitch, w, h, a, b, g, lshift, tiles,
-                                      tile_stride, list_off);
+                                      tile_stride, list_off, side_off);
     return cudaGetLastError();
   };
   static const int walk_f = [] { const char* v = getenv("RG_ROWTILE_WALK1"); return v ? atoi(v) : 256; }();
   static const int walk_r = [] { const char* v = getenv("RG_ROWTILE_WALK2"); return v ? atoi(v) : 256; }();
   static SmemAttr attr[4];
-  e = internal ? rowtile(census_rowtile_kernel<true, 1>, rw_smem<1>(), attr[0], fl, fr, gf, walk_f, 2, rw_wpb<1>())
-               : rowtile(census_rowtile_kernel<false, 1>, rw_smem<1>(), attr[1], fl, fr, gf, walk_f, 2, rw_wpb<1>());
+  e = internal ? rowtile(census_rowtile_kernel<true, 1>, rw_smem<1>(), attr[0], fl, fr, gf, walk_f, 4, rw_wpb<1>())
+               : rowtile(census_rowtile_kernel<false, 1>, rw_smem<1>(), attr[1], fl, fr, gf, walk_f, 4, rw_wpb<1>());
   if (e != cudaSuccess) return e;
-  e = internal ? rowtile(census_rowtile_kernel<true, 2>, rw_smem<2>(), attr[2], sl, sr, gs, walk_r, 2 + rtf * nxt,
+  e = internal ? rowtile(census_rowtile_kernel<true, 2>, rw_smem<2>(), attr[2], sl, sr, gs, walk_r, 4 + rtf * nxt,
                          rw_wpb<2>())
-               : rowtile(census_rowtile_kernel<false, 2>, rw_smem<2>(), attr[3], sl, sr, gs, walk_r, 2 + rtf * nxt,
+               : rowtile(census_rowtile_kernel<false, 2>, rw_smem<2>(), attr[3], sl, sr, gs, walk_r, 4 + rtf * nxt,
                          rw_wpb<2>());
   return e;
 }

@@ -1051,7 +1051,7 @@ __global__ void __launch_bounds__(WPB * 32, MINB) match_slots_warp_kernel(
 }
 
 template <typename CT, int WPB, int MINB, int PF = 0, bool COOP = false, bool V2 = false, bool PRE = false>
-cudaError_t launch_variant(int2* slot_pts, Slot* slots, int32_t* counters, int slot_capacity,
+cudaError_t launch_variant(const int2* slot_pts, const Slot* slots, int32_t* counters, int slot_capacity,
                                   const ObjEntry* objs, const rg_detection* dets, const int32_t* det_off,
                                   const void* fl, const void* fr, const PadGeom& gf, const void* sl,
                                   const void* sr, const PadGeom& gs, int img_w, int img_h, int trusted,
@@ -1074,12 +1074,7 @@ cudaError_t launch_variant(int2* slot_pts, Slot* slots, int32_t* counters, int s
   // COOP: about one wave of CTAs walks the work items (their count is only
   // known on the device)
   const int grid = COOP ? std::min(slot_capacity, 148 * MINB) : (slot_capacity + WPB - 1) / WPB;
-  if (PRE) {
-    if (!slot_pts) return cudaErrorInvalidValue;
-    constexpr int SW = 8;
-    sample_slots_kernel<SW><<<(slot_capacity + SW - 1) / SW, SW * 32, 0, s>>>(
-        slots, counters, objs, dets, det_off, img_w, img_h, cfg, slot_pts, stats, max_points, slot_capacity);
-  }
+  if (PRE && !slot_pts) return cudaErrorInvalidValue;
   kern<<<grid, WPB * 32, smem, s>>>(slot_pts, slots, counters, objs, dets, det_off, static_cast<const CT*>(fl),
                                     static_cast<const CT*>(fr), gf, static_cast<const CT*>(sl),
                                     static_cast<const CT*>(sr), gs, img_w, img_h, trusted, cfg, res, stats,
@@ -1089,24 +1084,49 @@ cudaError_t launch_variant(int2* slot_pts, Slot* slots, int32_t* counters, int s
 
 }  // namespace
 
-cudaError_t launch_match_slots(int2* slot_pts, Slot* slots, int32_t* counters, int slot_capacity,
+namespace {
+int match_variant() {
+  static const int v = [] {
+    const char* e = getenv("RG_MATCH_VARIANT");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+}  // namespace
+
+bool match_presampled(int n_frames, int wide) {
+  // A/B knob RG_MATCH_PRE=1: K2a ahead of the matcher.  Measured at C2
+  // (256 frames): K2a 0.124 ms, the matcher 0.894 -> 0.810 ms -- a net loss
+  // of 0.04 ms (the in-warp sampling overlaps other warps' sweeps; alone it
+  // is ~600 instructions per slot, mostly FP64 divisions), so off by default
+  static const bool on = [] {
+    const char* v = getenv("RG_MATCH_PRE");
+    return v ? atoi(v) != 0 : false;
+  }();
+  return on && match_variant() == 0 && !(n_frames > 0 && n_frames <= kLatencyFrames);
+}
+
+cudaError_t launch_sample_slots(Slot* slots, const int32_t* counters, int slot_capacity, const ObjEntry* objs,
+                                const rg_detection* dets, const int32_t* det_off, int img_w, int img_h,
+                                rg_ranger_config cfg, int2* slot_pts, rg_ranger_stats* stats, int max_points,
+                                cudaStream_t s) {
+  if (slot_capacity <= 0) return cudaSuccess;
+  constexpr int SW = 8;
+  sample_slots_kernel<SW><<<(slot_capacity + SW - 1) / SW, SW * 32, 0, s>>>(
+      slots, counters, objs, dets, det_off, img_w, img_h, cfg, slot_pts, stats, (max_points + 1) & ~1,
+      slot_capacity);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_match_slots(const int2* slot_pts, const Slot* slots, int32_t* counters, int slot_capacity,
                                const ObjEntry* objs, const rg_detection* dets, const int32_t* det_off,
                                const void* fl, const void* fr, const PadGeom& gf, const void* sl,
                                const void* sr, const PadGeom& gs, int img_w, int img_h, int trusted,
                                int wide, rg_ranger_config cfg, rg_match_result* res,
                                rg_ranger_stats* stats, int max_points, cudaStream_t s,
-                               int n_frames, int* launches) {
-  if (launches) *launches = 1;
+                               int n_frames) {
   if (slot_capacity <= 0) return cudaSuccess;
-  static int variant = [] {
-    const char* v = getenv("RG_MATCH_VARIANT");
-    return v ? atoi(v) : 0;
-  }();
-  // K2a ahead of the matcher (default) or the in-warp sampler (RG_MATCH_PRE=0)
-  static const bool pre = [] {
-    const char* v = getenv("RG_MATCH_PRE");
-    return v ? atoi(v) != 0 : true;
-  }();
+  const int variant = match_variant();
 #define RG_ARGS slot_pts, slots, counters, slot_capacity, objs, dets, det_off, fl, fr, gf, sl, sr, gs, img_w, img_h, \
                 trusted, cfg, res, stats, max_points, s
   // blocks too large for the default warps per CTA fall back to fewer
@@ -1116,7 +1136,8 @@ cudaError_t launch_match_slots(int2* slot_pts, Slot* slots, int32_t* counters, i
     return e;
   };
   if (wide)  // 9x7 extension
-    return fallback(launch_variant<unsigned long long, 8, 2>(RG_ARGS),
+    return fallback(slot_pts ? launch_variant<unsigned long long, 8, 2, 0, false, false, true>(RG_ARGS)
+                             : launch_variant<unsigned long long, 8, 2>(RG_ARGS),
                     [&] { return launch_variant<unsigned long long, 2, 8>(RG_ARGS); },
                     [&] { return launch_variant<unsigned long long, 1, 16>(RG_ARGS); });
   auto small = [&](cudaError_t e) {
@@ -1147,8 +1168,7 @@ cudaError_t launch_match_slots(int2* slot_pts, Slot* slots, int32_t* counters, i
     case 9: return launch_variant<uint32_t, 8, 4, 0, false, true>(RG_ARGS);
     case 10: return launch_variant<uint32_t, 16, 2, 0, false, true>(RG_ARGS);
     default:
-      if (launches && pre && slot_pts) *launches = 2;
-      return small(pre && slot_pts ? launch_variant<uint32_t, 16, 3, 0, false, false, true>(RG_ARGS)
+      return small(slot_pts ? launch_variant<uint32_t, 16, 3, 0, false, false, true>(RG_ARGS)
                                    : launch_variant<uint32_t, 16, 3>(RG_ARGS));
   }
 #undef RG_ARGS

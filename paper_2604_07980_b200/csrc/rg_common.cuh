@@ -228,16 +228,23 @@ cudaError_t launch_match_blocks64(Raster64 L, Raster64 R, const int32_t* pts, co
                                   const rg_search_range* ranges, int n_blocks, int mode,
                                   double tau_v, rg_match_result* out, int max_points,
                                   cudaStream_t s);
-// slot_pts: capacity x ((max_points + 1) & ~1) points for the slot sampler
-// (nullptr: the matcher samples in-warp)
-cudaError_t launch_match_slots(int2* slot_pts, Slot* slots, int32_t* counters, int slot_capacity,
+// K2a slot sampler (match_warp.cu): the points of every planned slot into
+// slot_pts (capacity x ((max_points + 1) & ~1)), counts in Slot::pad; whether
+// the matcher for this batch reads them (else it samples in-warp)
+bool match_presampled(int n_frames, int wide);
+cudaError_t launch_sample_slots(Slot* slots, const int32_t* counters, int slot_capacity, const ObjEntry* objs,
+                                const rg_detection* dets, const int32_t* det_off, int img_w, int img_h,
+                                rg_ranger_config cfg, int2* slot_pts, rg_ranger_stats* stats, int max_points,
+                                cudaStream_t s);
+// slot_pts: the K2a points (nullptr: the matcher samples in-warp)
+cudaError_t launch_match_slots(const int2* slot_pts, const Slot* slots, int32_t* counters, int slot_capacity,
                                const ObjEntry* objs, const rg_detection* dets,
                                const int32_t* det_off, const void* fl, const void* fr,
                                const PadGeom& gf, const void* sl, const void* sr,
                                const PadGeom& gs, int img_w, int img_h, int trusted, int wide,
                                rg_ranger_config cfg, rg_match_result* res,
                                rg_ranger_stats* stats, int max_points, cudaStream_t s,
-                               int n_frames = 0, int* launches = nullptr);
+                               int n_frames = 0);
 
 // box statistics of dense maps (dense.cu)
 cudaError_t launch_radar_votes(const int16_t* raw, int w, const int32_t* boxes, const double* d_radar, int n,
