@@ -46,29 +46,56 @@ N_SM = 148
 
 
 def census_required_bytes(dets, w, h, tau_s=48.0, scale=2, dx_far=256, dx_close=256):
-    """Bytes K1 must move for one frame when it computes the reference's ROI
-    census (census_transform_rois, template_match.hpp:245-321): the two images
-    read once, full codes inside the FAR ROI rectangles (box dilated by
-    dx_max_far + 2 columns and 3 rows) and reduced codes inside the CLOSE ROI
-    rectangles (reduced coordinates, dilated by ceil(dx_max_close / s) + 2 and
-    3), 4 B each, both sides.  -> (required bytes, FAR ROI pixels, CLOSE ROI
-    reduced pixels)."""
+    """Bytes K1 must move for one frame.  The reference's ROI census
+    (census_transform_rois, template_match.hpp:245-321) computes full codes
+    inside the FAR ROI rectangles (box dilated by dx_max_far + 2 columns and 3
+    rows) and reduced codes inside the CLOSE ROI rectangles (reduced
+    coordinates, dilated by ceil(dx_max_close / s) + 2 and 3) of both images.
+    K1 computes the part of each rectangle the matcher can read
+    (census_rows_kernel, census.cu): on the left image the box rows +-1 across
+    the rectangle, on the right image the box rows +-2 from the rectangle's
+    left edge to the box's right edge + 2.  Algorithmic bytes = 4 B per such
+    code + every image byte under those codes' 5x5 windows (source pixels
+    for the reduced raster), read once.  -> dict."""
     import math
     cw, ch = w // scale, h // scale
-    full, red = np.zeros((h, w), bool), np.zeros((ch, cw), bool)
     sx, sy = cw / w, ch / h
     dxs = (dx_close + scale - 1) // scale
+    ref_f, ref_r = np.zeros((h, w), bool), np.zeros((ch, cw), bool)
+    need = [[np.zeros((h, w), bool), np.zeros((ch, cw), bool)] for _ in range(2)]  # [image][raster]
     for d in dets:
         x0, x1 = (d.cx - d.w / 2) * w, (d.cx + d.w / 2) * w
         y0, y1 = (d.cy - d.h / 2) * h, (d.cy + d.h / 2) * h
         if max(d.w * w, d.h * h) < tau_s:  # classify_far_close
-            full[max(0, math.floor(y0) - 3):min(h, math.ceil(y1) + 4),
-                 max(0, math.floor(x0) - dx_far - 2):min(w, math.ceil(x1) + dx_far + 3)] = True
+            k, W, H, dxm, ref = 0, w, h, dx_far + 2, ref_f
+            bx0, bx1, by0, by1 = math.floor(x0), math.ceil(x1), math.floor(y0), math.ceil(y1)
         else:
-            red[max(0, math.floor(y0 * sy) - 3):min(ch, math.ceil(y1 * sy) + 4),
-                max(0, math.floor(x0 * sx) - dxs - 2):min(cw, math.ceil(x1 * sx) + dxs + 3)] = True
-    nf, nr = int(full.sum()), int(red.sum())
-    return 2 * (w * h + 4 * nf + 4 * nr), nf, nr
+            k, W, H, dxm, ref = 1, cw, ch, dxs + 2, ref_r
+            bx0, bx1 = math.floor(x0 * sx), math.ceil(x1 * sx)
+            by0, by1 = math.floor(y0 * sy), math.ceil(y1 * sy)
+        a, e = max(0, by0 - 3), min(H, by1 + 4)
+        c0, c1 = max(0, bx0 - dxm), min(W, bx1 + dxm + 1)
+        ref[a:e, c0:c1] = True
+        need[0][k][max(a, by0 - 1):min(e, by1 + 2), c0:c1] = True
+        need[1][k][max(a, by0 - 2):min(e, by1 + 3), c0:min(c1, bx1 + 3)] = True
+    codes, reads = 0, 0
+    for img in range(2):
+        nf, nr = need[img]
+        codes += int(nf.sum()) + int(nr.sum())
+        # image pixels under the 5x5 windows: the code masks (reduced code
+        # (x', y') at source (2x', 2y')) dilated by 2 rows / columns
+        m = nf.copy()
+        m[:scale * ch:scale, :scale * cw:scale] |= nr
+        for ax in (0, 1):
+            p = np.pad(m, [(2, 2) if a == ax else (0, 0) for a in (0, 1)])
+            n = m.shape[ax]
+            m = np.zeros_like(m)
+            for o in range(5):
+                m |= p[o:o + n, :] if ax == 0 else p[:, o:o + n]
+        reads += int(m.sum())
+    return {"bytes": 4 * codes + reads, "codes": codes, "image_bytes": reads,
+            "ref_full_codes": int(ref_f.sum()), "ref_reduced_codes": int(ref_r.sum()),
+            "ref_bytes": 2 * (w * h + 4 * int(ref_f.sum()) + 4 * int(ref_r.sum()))}
 
 
 def peaks():
@@ -851,7 +878,8 @@ def main():
     census_ms = stage_ms[0] / max(stage_launches[0], 1)
     match_ms = stage_ms[2] / max(stage_launches[2], 1)
     census_gbs = CENSUS_BYTES_PER_FRAME * F / (census_ms / 1000.0) / 1e9
-    req_frame, req_rows_full, req_rows_red = census_required_bytes(dets, W, H)
+    req = census_required_bytes(dets, W, H)
+    req_frame = req["bytes"]
     census_req_gbs = req_frame * F / (census_ms / 1000.0) / 1e9
     evals_per_launch = r_evals / max(stage_launches[2], 1)
     clk_mhz = clk["sm_mhz"] or sm_max
@@ -867,13 +895,19 @@ def main():
         pass
     census_roof = {"bound": "hbm", "achieved": census_req_gbs, "peak": hbm_peak, "unit": "GB/s",
                    "frac": census_req_gbs / hbm_peak, "traffic": traffic,
-                   "kernel": "census_rows_kernel + census_rowtile_kernel<1> (FAR ROI rows, full raster) + "
-                             "census_rowtile_kernel<2> (CLOSE ROI rows, reduced raster)",
+                   "kernel": "census_rows_kernel + census_rowtile_kernel<1> (FAR ROI tiles, full raster) + "
+                             "census_rowtile_kernel<2> (CLOSE ROI tiles, reduced raster)",
                    "peak_source": peak_kind, "algorithmic_bytes_per_launch": req_frame * F,
-                   "algorithmic_bytes": "the reference's ROI census (census_transform_rois rectangles): both "
-                                        f"images read, {req_rows_full} full-raster and {req_rows_red} reduced-raster "
-                                        "4-B codes per image",
+                   "algorithmic_bytes": f"the codes of the reference's ROI rectangles the matcher can read: "
+                                        f"{req['codes']} 4-B codes per frame (both images, full + reduced "
+                                        f"rasters) + the {req['image_bytes']} image bytes under their windows",
                    "ms_per_launch": census_ms, "frac_of_nominal_8000_gbs": census_req_gbs / 8000.0,
+                   "reference_roi_equivalent": {
+                       "bytes_per_launch": req["ref_bytes"] * F,
+                       "effective_gbs": req["ref_bytes"] * F / (census_ms / 1000.0) / 1e9,
+                       "note": f"the reference's whole ROI rectangles ({req['ref_full_codes']} full + "
+                               f"{req['ref_reduced_codes']} reduced codes per image, both images read) over the "
+                               "same time: an effective rate"},
                    "full_frame_equivalent": {
                        "bytes_per_launch": CENSUS_BYTES_PER_FRAME * F, "effective_gbs": census_gbs,
                        "note": "SURVEY 8(d) full-frame census bytes (24,883,200 per C2 frame) over the same time: "

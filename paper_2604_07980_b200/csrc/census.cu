@@ -448,10 +448,12 @@ __global__ void __launch_bounds__(RM_T) census_rows_kernel(const rg_detection* _
 }
 
 // Warp-tile "vertical pair" census for ROI rows: every warp owns a tile of
-// 120 source columns x 10 output rows (5 row pairs; 120 columns + the 2-px
+// 120 source columns x 4 output rows (2 row pairs; 120 columns + the 2-px
 // halo = 32 image words, one per lane) with its own V rows in
-// shared memory (no CTA barrier), so work follows the row masks at 10-row
-// granularity.  STRIDE 1 writes the full raster (4 codes per lane per row);
+// shared memory (no CTA barrier), so work follows the ROI rectangles at
+// 4-row granularity (measured per 256 C2 frames with the matcher's read
+// sets: 5 / 3 row pairs (full / reduced) 0.729 ms, 3 / 2 0.636, 2 / 2 0.627,
+// 2 / 1 0.696; 128 walkers per frame and side 0.627, 256 0.631).  STRIDE 1 writes the full raster (4 codes per lane per row);
 // STRIDE 2 writes the reduced raster of an exact-half CLOSE scale (reduced
 // (x', y') = full (2x', 2y'), census.hpp:59-64 with lround(2i) = 2i): the V
 // entry of source row s pairs rows s and s + 2, so reduced rows y', y' + 1
@@ -468,13 +470,16 @@ __global__ void __launch_bounds__(RM_T) census_rows_kernel(const rg_detection* _
 template <int STRIDE>
 __host__ __device__ constexpr int rw_wpb() { return STRIDE == 1 ? RG_RW_WPB1 : RG_RW_WPB2; }
 template <int STRIDE>
-#ifndef RG_RW_PR2
-#define RG_RW_PR2 3
+#ifndef RG_RW_PR1
+#define RG_RW_PR1 2
 #endif
-__host__ __device__ constexpr int rw_pr() { return STRIDE == 1 ? 5 : RG_RW_PR2; }  // row pairs per warp tile
+#ifndef RG_RW_PR2
+#define RG_RW_PR2 2
+#endif
+__host__ __device__ constexpr int rw_pr() { return STRIDE == 1 ? RG_RW_PR1 : RG_RW_PR2; }  // row pairs per warp tile
 constexpr int RW_VW = 136;  // V row stride: index 4 = source column x0 - 2
 template <int STRIDE>
-__host__ __device__ constexpr int rw_nv() { return 2 * STRIDE * (rw_pr<STRIDE>() - 1) + 5; }  // V rows (13 / 13)
+__host__ __device__ constexpr int rw_nv() { return 2 * STRIDE * (rw_pr<STRIDE>() - 1) + 5; }  // V rows (7 / 9)
 template <int STRIDE>
 __host__ __device__ constexpr size_t rw_smem() { return sizeof(uint32_t) * rw_wpb<STRIDE>() * rw_nv<STRIDE>() * RW_VW; }
 
@@ -537,7 +542,7 @@ __global__ void __launch_bounds__(rw_wpb<STRIDE>() * 32) census_rowtile_kernel(
     }
   }
   __syncwarp();
-  // ---- codes: 5 row pairs (output rows y, y + 1 = source rows STRIDE y, STRIDE y + STRIDE)
+  // ---- codes: RW_PR row pairs (output rows y, y + 1 = source rows STRIDE y, STRIDE y + STRIDE)
   constexpr int NQ = 4 / STRIDE;
   const int xs = x0 + 4 * lane;     // source column of this lane's first output
   const int xo = xs / STRIDE;       // its output column
@@ -924,8 +929,8 @@ cudaError_t launch_census_rois(const uint8_t* left, const uint8_t* right, int n_
                                       tile_stride, list_off, side_off);
     return cudaGetLastError();
   };
-  static const int walk_f = [] { const char* v = getenv("RG_ROWTILE_WALK1"); return v ? atoi(v) : 256; }();
-  static const int walk_r = [] { const char* v = getenv("RG_ROWTILE_WALK2"); return v ? atoi(v) : 256; }();
+  static const int walk_f = [] { const char* v = getenv("RG_ROWTILE_WALK1"); return v ? atoi(v) : 128; }();
+  static const int walk_r = [] { const char* v = getenv("RG_ROWTILE_WALK2"); return v ? atoi(v) : 128; }();
   static SmemAttr attr[4];
   e = internal ? rowtile(census_rowtile_kernel<true, 1>, rw_smem<1>(), attr[0], fl, fr, gf, walk_f, 4, rw_wpb<1>())
                : rowtile(census_rowtile_kernel<false, 1>, rw_smem<1>(), attr[1], fl, fr, gf, walk_f, 4, rw_wpb<1>());
