@@ -45,7 +45,7 @@ def popc_peak_per_clk():
 N_SM = 148
 
 
-def census_required_bytes(dets, w, h, tau_s=48.0, scale=2, dx_far=256, dx_close=256):
+def census_required_bytes(dets, w, h, tau_s=48.0, scale=2, dx_far=256, dx_close=256, code_bytes=4, rx=2, ry=2):
     """Bytes K1 must move for one frame.  The reference's ROI census
     (census_transform_rois, template_match.hpp:245-321) computes full codes
     inside the FAR ROI rectangles (box dilated by dx_max_far + 2 columns and 3
@@ -54,9 +54,10 @@ def census_required_bytes(dets, w, h, tau_s=48.0, scale=2, dx_far=256, dx_close=
     K1 computes the part of each rectangle the matcher can read
     (census_rows_kernel, census.cu): on the left image the box rows +-1 across
     the rectangle, on the right image the box rows +-2 from the rectangle's
-    left edge to the box's right edge + 2.  Algorithmic bytes = 4 B per such
-    code + every image byte under those codes' 5x5 windows (source pixels
-    for the reduced raster), read once.  -> dict."""
+    left edge to the box's right edge + 2.  Algorithmic bytes = code_bytes
+    per such code (4; 8 for the 9x7 extension) + every image byte under those
+    codes' (2 rx + 1) x (2 ry + 1) windows (source pixels for the reduced
+    raster), read once.  -> dict."""
     import math
     cw, ch = w // scale, h // scale
     sx, sy = cw / w, ch / h
@@ -82,20 +83,20 @@ def census_required_bytes(dets, w, h, tau_s=48.0, scale=2, dx_far=256, dx_close=
     for img in range(2):
         nf, nr = need[img]
         codes += int(nf.sum()) + int(nr.sum())
-        # image pixels under the 5x5 windows: the code masks (reduced code
-        # (x', y') at source (2x', 2y')) dilated by 2 rows / columns
+        # image pixels under the windows: the code masks (reduced code
+        # (x', y') at source (2x', 2y')) dilated by ry rows / rx columns
         m = nf.copy()
         m[:scale * ch:scale, :scale * cw:scale] |= nr
-        for ax in (0, 1):
-            p = np.pad(m, [(2, 2) if a == ax else (0, 0) for a in (0, 1)])
+        for ax, r in ((0, ry), (1, rx)):
+            p = np.pad(m, [(r, r) if a == ax else (0, 0) for a in (0, 1)])
             n = m.shape[ax]
             m = np.zeros_like(m)
-            for o in range(5):
+            for o in range(2 * r + 1):
                 m |= p[o:o + n, :] if ax == 0 else p[:, o:o + n]
         reads += int(m.sum())
-    return {"bytes": 4 * codes + reads, "codes": codes, "image_bytes": reads,
+    return {"bytes": code_bytes * codes + reads, "codes": codes, "image_bytes": reads,
             "ref_full_codes": int(ref_f.sum()), "ref_reduced_codes": int(ref_r.sum()),
-            "ref_bytes": 2 * (w * h + 4 * int(ref_f.sum()) + 4 * int(ref_r.sum()))}
+            "ref_bytes": 2 * (w * h + code_bytes * int(ref_f.sum()) + code_bytes * int(ref_r.sum()))}
 
 
 def peaks():
@@ -443,13 +444,20 @@ def config_c1_9x7(args, ctx, dev, stream):
     stage_ms, stage_launches, _ = ctx.counters()
     ms = e0.elapsed_time(e1) / reps
     boxes = int(cnt.sum().item())
-    cen_bytes = 2 * (w * h + 8 * w * h + 8 * (w // 2) * (h // 2))  # B = 8 for 9x7
+    full_bytes = 2 * (w * h + 8 * w * h + 8 * (w // 2) * (h // 2))  # B = 8 for 9x7
+    req = census_required_bytes(dets, w, h, cfg.tau_s, cfg.close_scale, cfg.dx_max_far, cfg.dx_max_close,
+                                code_bytes=8, rx=4, ry=3)
     cen_ms = stage_ms[0] / max(stage_launches[0], 1)
     res = {"config": f"C1 9x7: {w}x{h}, {len(dets)} boxes (5 FAR + 3 CLOSE) at integer disparities, dx_max 64, "
                      f"9x7 census / uint64 descriptors, {F1} device-rendered distinct frames (noise 2.0) per call",
            "ms_per_step": ms, "boxes_per_sec": boxes / (ms / 1e3), "frames_per_sec": F1 / (ms / 1e3),
-           "census64": {"ms_per_launch": cen_ms, "achieved_gbs": cen_bytes * F1 / (cen_ms / 1e3) / 1e9,
-                        "algorithmic_bytes_per_frame": cen_bytes}}
+           "census64": {"ms_per_launch": cen_ms, "kernel": "census_rows_kernel + census64_rowtile_kernel<1, 2> "
+                                                           "(ROI tiles of the matcher's read sets)",
+                        "achieved_gbs": req["bytes"] * F1 / (cen_ms / 1e3) / 1e9,
+                        "algorithmic_bytes_per_frame": req["bytes"],
+                        "algorithmic_bytes": f"{req['codes']} 8-B codes per frame (both images) + the "
+                                             f"{req['image_bytes']} image bytes under their 9x7 windows",
+                        "full_frame_equivalent_gbs": full_bytes * F1 / (cen_ms / 1e3) / 1e9}}
     if not args.no_parity:
         sys.path.insert(0, os.path.join(ROOT, "tests"))
         import oracle_lib

@@ -808,6 +808,154 @@ __global__ void __launch_bounds__(X2_WARPS * 32) census64_pairs_kernel(
     c64_strip<false>(V, full, red, gf, gs, x0, y0, w, h);
 }
 
+// 9x7 ROI census on the same compacted (row tile, column tile) lists as
+// census_rowtile_kernel (4 output rows x 120 source columns per warp tile):
+// the 64-bit codes of c64_strip (one fp16 accumulator per window row, row y
+// and row y + STRIDE in the two lanes), V rows built per warp from 32 image
+// words (word k = V entries 4k .. 4k + 3 = source columns x0 - 4 + 4k ..),
+// so lane l reads its 12 window columns as three aligned 16-B groups.
+// STRIDE 2: the reduced raster of an exact-half scale (reduced (x', y') =
+// full (2x', 2y')): V entries pair source rows s and s + 2, each lane emits
+// the source columns c, c + 2.
+template <int STRIDE>
+__host__ __device__ constexpr int c64_nv() { return 2 * STRIDE * (rw_pr<STRIDE>() - 1) + 7; }  // V rows (9 / 11)
+template <int STRIDE>
+__host__ __device__ constexpr size_t c64_smem() { return sizeof(uint32_t) * c64_nv<STRIDE>() * RW_VW; }
+
+template <int STRIDE>
+__global__ void __launch_bounds__(32) census64_rowtile_kernel(
+    const uint8_t* __restrict__ left, const uint8_t* __restrict__ right, int64_t frame_stride, int pitch, int w,
+    int h, unsigned long long* __restrict__ ol, unsigned long long* __restrict__ orr, PadGeom g,
+    const int32_t* __restrict__ lshift, const int32_t* __restrict__ tiles, int tile_stride, int list_off,
+    int side_off) {
+  constexpr int NV = c64_nv<STRIDE>(), NI = NV + STRIDE;  // V rows, image rows
+  constexpr int PR = rw_pr<STRIDE>();
+  constexpr int NQ = 4 / STRIDE;  // codes per lane per row
+  extern __shared__ __align__(16) uint32_t V[];
+  const int lane = threadIdx.x & 31;
+  const int sides = right ? 2 : 1;
+  const int frame = blockIdx.z / sides, side = blockIdx.z - frame * sides;
+  const int32_t* rec = tiles + (int64_t)frame * tile_stride;
+  const int n_tiles = rec[2 * side + STRIDE - 1];
+  const int32_t* list = rec + list_off + side * side_off;
+  const int sh = (side == 0 && lshift) ? lshift[frame] : 0;  // shift_vertical of the left image
+  const uint8_t* img = (side ? right : left) + (int64_t)frame * frame_stride;
+  unsigned long long* out = (side ? orr : ol) + (int64_t)frame * g.fstride + g.origin;
+  const __half2 two = __float2half2_rn(2.0f), four = __float2half2_rn(4.0f);
+  const int pw = pitch / 4;
+  for (int ti = blockIdx.x; ti < n_tiles; ti += gridDim.x) {
+    const int ent = list[ti];
+    const int Y0 = (ent >> 16) * 2 * PR;  // first output row of this tile (even)
+    const int x0 = (ent & 0xFFFF) * RW_TX;
+    __syncwarp();  // the previous tile's window reads are done before V is rebuilt
+    const int S0 = STRIDE * Y0 - 3;  // source row of V row 0
+    {
+      const int kw = min(max((x0 - 4) / 4 + lane, 0), (w + 3) / 4 - 1);
+      const int ya = S0 - sh;
+      uint32_t wv[NI];
+      if (ya >= 0 && ya + NI - 1 <= h - 1) {
+        const uint32_t* col = reinterpret_cast<const uint32_t*>(img) + (int64_t)ya * pw + kw;
+#pragma unroll
+        for (int t = 0; t < NI; ++t, col += pw) wv[t] = __ldg(col);
+      } else {
+        const uint32_t* col = reinterpret_cast<const uint32_t*>(img) + kw;
+#pragma unroll
+        for (int t = 0; t < NI; ++t) wv[t] = __ldg(col + (int64_t)min(max(ya + t, 0), h - 1) * pw);
+      }
+      uint4* vrow = reinterpret_cast<uint4*>(V) + lane;
+#pragma unroll
+      for (int t = 0; t < NV; ++t) {
+        const uint32_t a = wv[t], b = wv[t + STRIDE];
+        vrow[t * (RW_VW / 4)] = make_uint4(c2_vpair(a, b, 0), c2_vpair(a, b, 1), c2_vpair(a, b, 2),
+                                           c2_vpair(a, b, 3));
+      }
+    }
+    __syncwarp();
+    const int xs = x0 + 4 * lane;  // source column of this lane's first output
+    const int xo = xs / STRIDE;
+    if (lane >= RW_TX / 4 || xo >= g.w) continue;  // (such lanes only help build V)
+    const bool edge = x0 < 4 || x0 + RW_TX + 4 > w - 5 || STRIDE * Y0 < 3 || STRIDE * (Y0 + 2 * PR) > h - 4;
+    const uint32_t* vbase = V + 4 * lane;  // V index of source column xs - 4
+#pragma unroll 1
+    for (int p = 0; p < PR; ++p) {
+      const int y = Y0 + 2 * p;
+      if (y >= g.h) break;
+      uint32_t clo[NQ], chi[NQ], dlo[NQ], dhi[NQ];
+      __half2 cen[NQ];
+      {
+        const uint4 c4 = *reinterpret_cast<const uint4*>(vbase + (2 * STRIDE * p + 3) * RW_VW + 4);  // xs .. xs+3
+        const uint32_t cc[4] = {c4.x, c4.y, c4.z, c4.w};
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) cen[q] = *reinterpret_cast<const __half2*>(&cc[STRIDE * q]);
+      }
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) clo[q] = dlo[q] = 0u, chi[q] = dhi[q] = 0x80000000u;  // sentinel bit 63
+#pragma unroll
+      for (int r = 0; r < 7; ++r) {
+        uint32_t e[12];
+        const uint4* src = reinterpret_cast<const uint4*>(vbase + (2 * STRIDE * p + r) * RW_VW);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          const uint4 a = src[k];
+          e[4 * k] = a.x, e[4 * k + 1] = a.y, e[4 * k + 2] = a.z, e[4 * k + 3] = a.w;
+        }
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+          __half2 acc = two;
+#pragma unroll
+          for (int c = 0; c < 9; ++c) {
+            if (r == 3 && c == 4) continue;  // centre: its 0 bit is folded into the next step's x4
+            const __half2 v = *reinterpret_cast<const __half2*>(&e[STRIDE * q + c]);
+            const __half2 m = ((r * 9 + c) % 6 == 0) ? __hsub2_sat(v, cen[q]) : __hgt2(v, cen[q]);
+            acc = __hfma2(acc, (r == 3 && c == 5) ? four : two, m);
+          }
+          const uint32_t u = *reinterpret_cast<const uint32_t*>(&acc);
+          const uint32_t bl = u & 0x1FFu, bh = (u >> 16) & 0x1FFu;
+          const int pos = 54 - 9 * r;  // bit 54 - 9r of the 64-bit code (c64_strip)
+          if (pos >= 32) {
+            chi[q] |= bl << (pos - 32);
+            dhi[q] |= bh << (pos - 32);
+          } else if (pos + 9 > 32) {
+            clo[q] |= bl << pos, chi[q] |= bl >> (32 - pos);
+            dlo[q] |= bh << pos, dhi[q] |= bh >> (32 - pos);
+          } else {
+            clo[q] |= bl << pos;
+            dlo[q] |= bh << pos;
+          }
+        }
+      }
+      unsigned long long lo[NQ], hi[NQ];
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        lo[q] = ((unsigned long long)chi[q] << 32) | clo[q];
+        hi[q] = ((unsigned long long)dhi[q] << 32) | dlo[q];
+        if (edge) {  // 0 where the 9x7 window leaves the image
+          const int sx = xs + STRIDE * q, sy0 = STRIDE * y, sy1 = STRIDE * y + STRIDE;
+          const bool xin = sx >= 4 && sx <= w - 5;
+          if (!(xin && sy0 >= 3 && sy0 <= h - 4)) lo[q] = 0ull;
+          if (!(xin && sy1 >= 3 && sy1 <= h - 4)) hi[q] = 0ull;
+        }
+      }
+      unsigned long long* o = out + (int64_t)y * g.pitch + xo;
+      const bool two_rows = y + 1 < g.h;
+      if (xo + NQ <= g.w) {
+#pragma unroll
+        for (int q = 0; q < NQ; q += 2) {
+          reinterpret_cast<ulonglong2*>(o)[q / 2] = make_ulonglong2(lo[q], lo[q + 1]);
+          if (two_rows) reinterpret_cast<ulonglong2*>(o + g.pitch)[q / 2] = make_ulonglong2(hi[q], hi[q + 1]);
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+          if (xo + q >= g.w) break;
+          o[q] = lo[q];
+          if (two_rows) o[g.pitch + q] = hi[q];
+        }
+      }
+    }
+  }
+}
+
 // census_transform_rois mask (census.hpp:111-136): keep codes inside the
 // union of the clipped rectangles, zero elsewhere.  Kept codes leave in the
 // reference layout (sentinel bit 25) whichever layout they were computed in.
@@ -868,20 +1016,17 @@ size_t census_rois_scratch_words(int n_frames, int w, int h, int ch) {
 // full raster on FAR ROI rows and the reduced raster on CLOSE ROI rows.
 // cudaErrorNotSupported when the fast layout does not apply (the caller then
 // runs the full-frame launch_census_frames).
-cudaError_t launch_census_rois(const uint8_t* left, const uint8_t* right, int n_frames, int64_t frame_stride,
-                               int pitch, int w, int h, uint32_t* fl, uint32_t* fr, const PadGeom& gf, uint32_t* sl,
-                               uint32_t* sr, const PadGeom& gs, const int32_t* lshift, bool internal,
-                               const rg_detection* dets, const int32_t* det_off, double tau_s, int dx_far,
-                               int dx_close_scaled, uint32_t* masks, cudaStream_t s) {
-  if (n_frames <= 0) return cudaSuccess;
-  const int sides = right ? 2 : 1;
-  const bool aligned = (pitch % 4 == 0) && (w % 4 == 0) && (frame_stride % 4 == 0) &&
-                       (reinterpret_cast<uintptr_t>(left) % 4 == 0) &&
-                       (!right || reinterpret_cast<uintptr_t>(right) % 4 == 0) && gf.pitch % 4 == 0 &&
-                       gf.origin % 4 == 0 && w >= 8 && h >= 8;
-  const bool half = sl && gs.w * 2 == w && gs.h * 2 == h && gs.pitch % 2 == 0 && gs.origin % 2 == 0 &&
-                    gs.w >= 4 && gs.h >= 4;
-  if (!aligned || !half || !masks || !dets) return cudaErrorNotSupported;
+namespace {
+// census_rows_kernel over a batch: row masks + per-image compacted tile lists
+// of the warp tiles (RW_TX columns x 2 rw_pr rows; reduced: RW_TX / 2) the
+// ROI rectangles touch.  Returns the list geometry for the tile kernels.
+struct RoiLists {
+  int32_t* tiles;
+  int tile_stride, side_off, red_off;
+};
+cudaError_t roi_lists(int n_frames, int w, int h, const PadGeom& gs, const rg_detection* dets,
+                      const int32_t* det_off, double tau_s, int dx_far, int dx_close_scaled, uint32_t* masks,
+                      cudaStream_t s, RoiLists* out) {
   const int wf = (h + 31) / 32, wr = (gs.h + 31) / 32;
   const int tf = 2 * rw_pr<1>(), tr = 2 * rw_pr<2>();  // output rows per warp tile
   const int nxt = (w + RW_TX - 1) / RW_TX;              // column tiles (reduced: RW_TX / 2 columns)
@@ -899,8 +1044,31 @@ cudaError_t launch_census_rois(const uint8_t* left, const uint8_t* right, int n_
   census_rows_kernel<<<n_frames, RM_T, sizeof(uint32_t) * (wf + wr + bmw), s>>>(
       dets, det_off, w, h, tau_s, gs.w, gs.h, wf, wr, masks, dx_far, dx_close_scaled, nxt, tf, tr, rtf, rtr,
       tile_stride, tiles, tight);
-  cudaError_t e = cudaGetLastError();
+  *out = {tiles, tile_stride, side_off, 4 + rtf * nxt};
+  return cudaGetLastError();
+}
+}  // namespace
+
+cudaError_t launch_census_rois(const uint8_t* left, const uint8_t* right, int n_frames, int64_t frame_stride,
+                               int pitch, int w, int h, uint32_t* fl, uint32_t* fr, const PadGeom& gf, uint32_t* sl,
+                               uint32_t* sr, const PadGeom& gs, const int32_t* lshift, bool internal,
+                               const rg_detection* dets, const int32_t* det_off, double tau_s, int dx_far,
+                               int dx_close_scaled, uint32_t* masks, cudaStream_t s) {
+  if (n_frames <= 0) return cudaSuccess;
+  const int sides = right ? 2 : 1;
+  const bool aligned = (pitch % 4 == 0) && (w % 4 == 0) && (frame_stride % 4 == 0) &&
+                       (reinterpret_cast<uintptr_t>(left) % 4 == 0) &&
+                       (!right || reinterpret_cast<uintptr_t>(right) % 4 == 0) && gf.pitch % 4 == 0 &&
+                       gf.origin % 4 == 0 && w >= 8 && h >= 8;
+  const bool half = sl && gs.w * 2 == w && gs.h * 2 == h && gs.pitch % 2 == 0 && gs.origin % 2 == 0 &&
+                    gs.w >= 4 && gs.h >= 4;
+  if (!aligned || !half || !masks || !dets) return cudaErrorNotSupported;
+  RoiLists rl;
+  cudaError_t e = roi_lists(n_frames, w, h, gs, dets, det_off, tau_s, dx_far, dx_close_scaled, masks, s, &rl);
   if (e != cudaSuccess) return e;
+  int32_t* tiles = rl.tiles;
+  const int tile_stride = rl.tile_stride, side_off = rl.side_off;
+  const int wf = (h + 31) / 32, wr = (gs.h + 31) / 32;
   static const int mode = [] {
     // A/B knob: 1 warp row tiles (default), 0 the full-frame pair tiles storing
     // only ROI rows (measured: no faster than storing every row -- K1 is
@@ -935,9 +1103,9 @@ cudaError_t launch_census_rois(const uint8_t* left, const uint8_t* right, int n_
   e = internal ? rowtile(census_rowtile_kernel<true, 1>, rw_smem<1>(), attr[0], fl, fr, gf, walk_f, 4, rw_wpb<1>())
                : rowtile(census_rowtile_kernel<false, 1>, rw_smem<1>(), attr[1], fl, fr, gf, walk_f, 4, rw_wpb<1>());
   if (e != cudaSuccess) return e;
-  e = internal ? rowtile(census_rowtile_kernel<true, 2>, rw_smem<2>(), attr[2], sl, sr, gs, walk_r, 4 + rtf * nxt,
+  e = internal ? rowtile(census_rowtile_kernel<true, 2>, rw_smem<2>(), attr[2], sl, sr, gs, walk_r, rl.red_off,
                          rw_wpb<2>())
-               : rowtile(census_rowtile_kernel<false, 2>, rw_smem<2>(), attr[3], sl, sr, gs, walk_r, 4 + rtf * nxt,
+               : rowtile(census_rowtile_kernel<false, 2>, rw_smem<2>(), attr[3], sl, sr, gs, walk_r, rl.red_off,
                          rw_wpb<2>());
   return e;
 }
@@ -966,6 +1134,44 @@ cudaError_t launch_census64_frames(const uint8_t* left, const uint8_t* right, in
   dim3 grid((w + X_TX - 1) / X_TX, (h + X_TY - 1) / X_TY, (right ? 2 : 1) * n_frames);
   census64_kernel<<<grid, X_TPB, 0, s>>>(left, right, frame_stride, pitch, w, h, fl, fr, gf, sl, sr, gs, inv_x,
                                          inv_y, lshift);
+  return cudaGetLastError();
+}
+
+// 9x7 ROI census of a batch: census_rows_kernel's lists, the full raster on
+// the FAR tiles and the reduced raster on the CLOSE tiles
+// (census64_rowtile_kernel).  cudaErrorNotSupported when the layout does not
+// apply (the caller then runs launch_census64_frames).
+cudaError_t launch_census64_rois(const uint8_t* left, const uint8_t* right, int n_frames, int64_t frame_stride,
+                                 int pitch, int w, int h, unsigned long long* fl, unsigned long long* fr,
+                                 const PadGeom& gf, unsigned long long* sl, unsigned long long* sr,
+                                 const PadGeom& gs, const int32_t* lshift, const rg_detection* dets,
+                                 const int32_t* det_off, double tau_s, int dx_far, int dx_close_scaled,
+                                 uint32_t* masks, cudaStream_t s) {
+  if (n_frames <= 0) return cudaSuccess;
+  const bool aligned = (pitch % 4 == 0) && (w % 4 == 0) && (frame_stride % 4 == 0) &&
+                       (reinterpret_cast<uintptr_t>(left) % 4 == 0) &&
+                       (!right || reinterpret_cast<uintptr_t>(right) % 4 == 0) && gf.pitch % 2 == 0 &&
+                       gf.origin % 2 == 0 && w >= 12 && h >= 8;
+  const bool half = sl && gs.w * 2 == w && gs.h * 2 == h && gs.pitch % 2 == 0 && gs.origin % 2 == 0 &&
+                    gs.w >= 4 && gs.h >= 4;
+  if (!aligned || !half || !masks || !dets) return cudaErrorNotSupported;
+  RoiLists rl;
+  cudaError_t e = roi_lists(n_frames, w, h, gs, dets, det_off, tau_s, dx_far, dx_close_scaled, masks, s, &rl);
+  if (e != cudaSuccess) return e;
+  static SmemAttr attr[2];
+  static const int walkers = [] { const char* v = getenv("RG_ROWTILE_WALK64"); return v ? atoi(v) : 128; }();
+  const dim3 grid(walkers, 1, (right ? 2 : 1) * n_frames);
+  e = attr[0].ensure((const void*)census64_rowtile_kernel<1>, c64_smem<1>());
+  if (e != cudaSuccess) return e;
+  census64_rowtile_kernel<1><<<grid, 32, c64_smem<1>(), s>>>(left, right, frame_stride, pitch, w, h, fl, fr, gf,
+                                                             lshift, rl.tiles, rl.tile_stride, 4, rl.side_off);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  e = attr[1].ensure((const void*)census64_rowtile_kernel<2>, c64_smem<2>());
+  if (e != cudaSuccess) return e;
+  census64_rowtile_kernel<2><<<grid, 32, c64_smem<2>(), s>>>(left, right, frame_stride, pitch, w, h, sl, sr, gs,
+                                                             lshift, rl.tiles, rl.tile_stride, rl.red_off,
+                                                             rl.side_off);
   return cudaGetLastError();
 }
 

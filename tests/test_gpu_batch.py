@@ -397,16 +397,19 @@ def test_large_blocks_fit_the_device_matcher(ctx, chk, grid, maxp, frames):
         assert int(cnt[f]) * 32 == len(want) and o[f, :len(want)].tobytes() == want
 
 
-@pytest.mark.parametrize("name,n", [("c1", 16), ("c2", 12), ("c3", 12)])
-def test_roi_census_batches_match_reference(ctx, chk, name, n):
-    """Batches of >= 12 frames take the ROI-row census (census_rows_kernel +
-    the warp row-tile kernels, compacted tile lists); a per-frame left shift
-    (rect correction) and detection lists that differ per frame included.
-    Every record equals the reference's."""
+@pytest.mark.parametrize("name,n,wide", [("c1", 16, False), ("c2", 12, False), ("c3", 12, False),
+                                         ("c1", 16, True), ("c2", 12, True), ("c3", 12, True)])
+def test_roi_census_batches_match_reference(ctx, chk, name, n, wide):
+    """Batches of >= 12 frames take the ROI census (census_rows_kernel + the
+    warp tile kernels over compacted tile lists; 9x7: census64_rowtile_kernel);
+    a per-frame left shift (rect correction) and detection lists that differ
+    per frame included.  Every record equals the reference's (9x7: the
+    restatement's)."""
     import torch
 
     fn = {"c1": S.scene_c1, "c2": S.scene_c2, "c3": S.scene_c3}[name]
     L, R, D, cfg, sc = _frames(fn, n)
+    cfg.census_9x7 = wide
     D = [d if i % 3 else list(reversed(d[: max(1, len(d) - i)])) for i, d in enumerate(D)]
     shifts = ((np.arange(n) % 5) - 2).astype(np.int32)
     maxd = max(len(d) for d in D)
