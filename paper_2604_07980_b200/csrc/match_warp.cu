@@ -411,7 +411,9 @@ __device__ __forceinline__ void sweep_range(
   const int nfull = ptail ? ndx >> 5 : nch;
   const int cb = part * nfull / nparts, ce = (part + 1) * nfull / nparts, nmine = ce - cb;
   const int groups = (nmine + CMAX - 1) / CMAX;
-  const int gq = groups ? nmine / groups : 0, gr = groups ? nmine - gq * groups : 0;  // balanced group sizes
+  // balanced group sizes (nmine / groups without a division for 1-2 groups)
+  const int gq = groups == 1 ? nmine : groups == 2 ? nmine >> 1 : groups ? nmine / groups : 0;
+  const int gr = groups ? nmine - gq * groups : 0;
   for (int dy = rg.dy_min; dy <= rg.dy_max; ++dy) {
     // FAST throughput sweeps take two row offsets per pass over the points
     const bool two = RG_MW_DY2 && MODE == M_FAST && PF == 0 && nparts == 1 && sizeof(CT) == 4 &&
@@ -914,7 +916,7 @@ template <int WPB>
 __global__ void __launch_bounds__(WPB * 32) sample_slots_kernel(
     Slot* __restrict__ slots, const int32_t* __restrict__ counters, const ObjEntry* __restrict__ objs,
     const rg_detection* __restrict__ dets, const int32_t* __restrict__ det_off, int img_w, int img_h,
-    rg_ranger_config cfg, int2* __restrict__ pts_out, rg_ranger_stats* __restrict__ stats, int maxp,
+    SampleConst sk, int2* __restrict__ pts_out, rg_ranger_stats* __restrict__ stats, int maxp,
     int capacity) {
   __shared__ double occ[WPB][4 * kWarpOcc];
   __shared__ int nocc[WPB];
@@ -928,10 +930,10 @@ __global__ void __launch_bounds__(WPB * 32) sample_slots_kernel(
   const rg_detection det = dets[e.det];
   const int d0 = det_off[s.frame], d1 = det_off[s.frame + 1];
   const bool all = warp_occluders(det, e.det, dets, d0, d1, img_w, img_h, occ[warp], &nocc[warp], lane);
-  const int cols = max(e.cols, 1);
-  const int np = dev_sample_block_warp(det, e.kind, s.sub / cols, s.sub % cols, e.rows, e.cols, occ[warp],
-                                       min(nocc[warp], kWarpOcc), all ? dets + d0 : nullptr, d1 - d0,
-                                       e.det - d0, cfg, img_w, img_h, pts_out + (size_t)slot * maxp);
+  const int np = dev_sample_block_warp_g(
+      dev_sample_geom_k(det, e.kind, s.pad >> 16, s.pad & 0xFFFF, e.rows, e.cols, sk, img_w, img_h), det, occ[warp],
+      min(nocc[warp], kWarpOcc), all ? dets + d0 : nullptr, d1 - d0, e.det - d0, img_w, img_h,
+      pts_out + (size_t)slot * maxp);
   if (lane == 0) {
     slots[slot].pad = np;
     if (stats && np >= 4)
@@ -948,7 +950,7 @@ __global__ void __launch_bounds__(WPB * 32, MINB) match_slots_warp_kernel(
     const rg_detection* __restrict__ dets, const int32_t* __restrict__ det_off,
     const CT* __restrict__ fl, const CT* __restrict__ fr, PadGeom gf,
     const CT* __restrict__ sl, const CT* __restrict__ sr, PadGeom gs, int img_w,
-    int img_h, int trusted, rg_ranger_config cfg, rg_match_result* __restrict__ res,
+    int img_h, int trusted, rg_ranger_config cfg, SampleConst sk, rg_match_result* __restrict__ res,
     rg_ranger_stats* __restrict__ stats, int maxp, int capacity) {
   extern __shared__ __align__(16) unsigned char wsm_raw[];
   __shared__ double occ[PRE ? 1 : WPB][4 * kWarpOcc];
@@ -983,10 +985,9 @@ __global__ void __launch_bounds__(WPB * 32, MINB) match_slots_warp_kernel(
       const rg_detection det = dets[e.det];
       const int d0 = det_off[s.frame], d1 = det_off[s.frame + 1];
       const bool all = warp_occluders(det, e.det, dets, d0, d1, img_w, img_h, occ[warp], &nocc[warp], lane);
-      const int cols = max(e.cols, 1);
-      np = dev_sample_block_warp(det, e.kind, s.sub / cols, s.sub % cols, e.rows, e.cols, occ[warp],
-                                 min(nocc[warp], kWarpOcc), all ? dets + d0 : nullptr, d1 - d0, e.det - d0, cfg,
-                                 img_w, img_h, pts);
+      np = dev_sample_block_warp_g(
+          dev_sample_geom_k(det, e.kind, s.pad >> 16, s.pad & 0xFFFF, e.rows, e.cols, sk, img_w, img_h), det,
+          occ[warp], min(nocc[warp], kWarpOcc), all ? dets + d0 : nullptr, d1 - d0, e.det - d0, img_w, img_h, pts);
       far = e.kind == RG_KIND_FAR;
     }
     rg_match_result r;
@@ -1001,9 +1002,8 @@ __global__ void __launch_bounds__(WPB * 32, MINB) match_slots_warp_kernel(
       const int64_t fo = (int64_t)s.frame * g.fstride + g.origin;
       const CT* L = (far ? fl : sl) + fo;
       const CT* R = (far ? fr : sr) + fo;
-      const int sc = cfg.close_scale;
       const rg_search_range rg = far ? rg_search_range{0, cfg.dx_max_far, -1, 1}
-                                     : rg_search_range{0, (cfg.dx_max_close + sc - 1) / sc, -1, 1};
+                                     : rg_search_range{0, sk.dxc, -1, 1};
       auto pass = [&](int sx, int sy, const CT* A, const CT* B, const rg_search_range& q) -> Pass {
         if constexpr (V2 && sizeof(CT) == 4) {
           if (trusted && nparts == 1)
@@ -1077,7 +1077,8 @@ cudaError_t launch_variant(const int2* slot_pts, const Slot* slots, int32_t* cou
   if (PRE && !slot_pts) return cudaErrorInvalidValue;
   kern<<<grid, WPB * 32, smem, s>>>(slot_pts, slots, counters, objs, dets, det_off, static_cast<const CT*>(fl),
                                     static_cast<const CT*>(fr), gf, static_cast<const CT*>(sl),
-                                    static_cast<const CT*>(sr), gs, img_w, img_h, trusted, cfg, res, stats,
+                                    static_cast<const CT*>(sr), gs, img_w, img_h, trusted, cfg,
+                                    make_sample_const(cfg, img_w, img_h), res, stats,
                                     max_points, slot_capacity);
   return cudaGetLastError();
 }
@@ -1113,8 +1114,8 @@ cudaError_t launch_sample_slots(Slot* slots, const int32_t* counters, int slot_c
   if (slot_capacity <= 0) return cudaSuccess;
   constexpr int SW = 8;
   sample_slots_kernel<SW><<<(slot_capacity + SW - 1) / SW, SW * 32, 0, s>>>(
-      slots, counters, objs, dets, det_off, img_w, img_h, cfg, slot_pts, stats, (max_points + 1) & ~1,
-      slot_capacity);
+      slots, counters, objs, dets, det_off, img_w, img_h, make_sample_const(cfg, img_w, img_h), slot_pts, stats,
+      (max_points + 1) & ~1, slot_capacity);
   return cudaGetLastError();
 }
 

@@ -154,7 +154,12 @@ __global__ void __launch_bounds__(PT) plan_frames_kernel(
       if (sb < 0 || sb + ns > slot_capacity) {
         counters[1] = 1;  // overflow: the host grows the list and re-runs
       } else {
-        for (int t = 0; t < ns; ++t) slots[sb + t] = Slot{f, g, t, 0};
+        // pad = sub-block row << 16 | column (the matcher skips the division)
+        const int cq = max(cols, 1);
+        for (int t = 0, r = 0, c = 0; t < ns; ++t) {
+          slots[sb + t] = Slot{f, g, t, (r << 16) | c};
+          if (++c == cq) c = 0, ++r;
+        }
       }
       if (kind == RG_KIND_FAR)
         ++n_far;

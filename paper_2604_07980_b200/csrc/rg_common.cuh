@@ -121,7 +121,7 @@ struct Slot {
   int32_t frame;
   int32_t obj;  // index into the object table
   int32_t sub;  // r*cols + c for CLOSE, 0 for FAR
-  int32_t pad;
+  int32_t pad;  // r << 16 | c (planner); K2a overwrites it with the point count
 };
 
 }  // namespace rg

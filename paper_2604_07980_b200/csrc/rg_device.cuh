@@ -100,8 +100,32 @@ struct SampleGeom {
   PBox box;
   double bw, bh, sx0, sy0, sw, sh;
   int n, cw, ch;
+  uint32_t magic;  // ceil(2^32 / n): idx / n = umulhi(idx, magic) (0: divide)
   bool far;
 };
+
+// Per-launch integer constants of the sampler, computed once on the host
+// (the divisions / square root of dev_sample_geom without the per-slot cost).
+struct SampleConst {
+  int cw, ch;      // reduced raster: w / close_scale, h / close_scale (:189-190)
+  int nf, nc;      // grid side points of FAR blocks / CLOSE sub-blocks (:165-168, :192-194)
+  uint32_t mf, mc; // ceil(2^32 / nf), ceil(2^32 / nc)
+  int dxc;         // ceil(dx_max_close / close_scale) (:218)
+};
+inline SampleConst make_sample_const(const rg_ranger_config& c, int w, int h) {
+  SampleConst k;
+  int cap = (int)sqrt((double)c.max_total_points);  // dev_cap
+  if (cap < 1) cap = 1;
+  k.cw = w / c.close_scale;
+  k.ch = h / c.close_scale;
+  k.nf = c.grid_side_points < cap ? c.grid_side_points : cap;
+  k.nc = c.close_block_side_points < cap ? c.close_block_side_points : cap;
+  // exact for idx < n^2 while n^3 < 2^32 (error idx * (magic * n - 2^32) < 2^32)
+  k.mf = k.nf > 1 && k.nf <= 1024 ? (uint32_t)(0xFFFFFFFFu / (uint32_t)k.nf) + 1u : 0u;
+  k.mc = k.nc > 1 && k.nc <= 1024 ? (uint32_t)(0xFFFFFFFFu / (uint32_t)k.nc) + 1u : 0u;
+  k.dxc = (c.dx_max_close + c.close_scale - 1) / c.close_scale;
+  return k;
+}
 
 __device__ __forceinline__ SampleGeom dev_sample_geom(const rg_detection& det, int kind, int r, int c,
                                                       int rows, int cols, const rg_ranger_config& cfg,
@@ -115,6 +139,29 @@ __device__ __forceinline__ SampleGeom dev_sample_geom(const rg_detection& det, i
   g.n = g.far ? min(cfg.grid_side_points, cap) : min(cfg.close_block_side_points, cap);
   g.cw = w / cfg.close_scale;
   g.ch = h / cfg.close_scale;
+  g.magic = 0;
+  g.sx0 = g.sy0 = g.sw = g.sh = 0;
+  if (!g.far) {
+    g.sx0 = __dadd_rn(g.box.x0, __ddiv_rn(__dmul_rn((double)c, g.bw), (double)cols));
+    g.sy0 = __dadd_rn(g.box.y0, __ddiv_rn(__dmul_rn((double)r, g.bh), (double)rows));
+    g.sw = __ddiv_rn(g.bw, (double)cols);
+    g.sh = __ddiv_rn(g.bh, (double)rows);
+  }
+  return g;
+}
+
+// dev_sample_geom with the integer constants taken from k
+__device__ __forceinline__ SampleGeom dev_sample_geom_k(const rg_detection& det, int kind, int r, int c, int rows,
+                                                        int cols, const SampleConst& k, int w, int h) {
+  SampleGeom g;
+  g.box = pixel_box(det, w, h);
+  g.bw = __dsub_rn(g.box.x1, g.box.x0);
+  g.bh = __dsub_rn(g.box.y1, g.box.y0);
+  g.far = kind == RG_KIND_FAR;
+  g.n = g.far ? k.nf : k.nc;
+  g.magic = g.far ? k.mf : k.mc;
+  g.cw = k.cw;
+  g.ch = k.ch;
   g.sx0 = g.sy0 = g.sw = g.sh = 0;
   if (!g.far) {
     g.sx0 = __dadd_rn(g.box.x0, __ddiv_rn(__dmul_rn((double)c, g.bw), (double)cols));
@@ -131,7 +178,7 @@ __device__ __forceinline__ SampleGeom dev_sample_geom(const rg_detection& det, i
 __device__ __forceinline__ bool dev_sample_point(const SampleGeom& g, int idx, const rg_detection& det,
                                                  const double* occ, int n_occ, const rg_detection* occ_all,
                                                  int n_all, int self, int w, int h, int* px, int* py) {
-  const int j = idx / g.n, i = idx - j * g.n;
+  const int j = g.magic ? (int)__umulhi((uint32_t)idx, g.magic) : idx / g.n, i = idx - j * g.n;
   double fx, fy;
   if (g.far) {
     fy = __dadd_rn(g.box.y0, div_n(__dmul_rn(__dadd_rn((double)j, 0.5), g.bh), g.n));
@@ -195,12 +242,20 @@ __device__ __forceinline__ int dev_sample_block(const rg_detection& det, int kin
 }
 
 // Warp-wide sampler: same points, same order; returns the count (warp-uniform).
+__device__ __forceinline__ int dev_sample_block_warp_g(const SampleGeom& g, const rg_detection& det,
+                                                       const double* occ, int n_occ, const rg_detection* occ_all,
+                                                       int n_all, int self, int w, int h, int2* pts);
 __device__ __forceinline__ int dev_sample_block_warp(const rg_detection& det, int kind, int r, int c,
                                                      int rows, int cols, const double* occ, int n_occ,
                                                      const rg_detection* occ_all, int n_all, int self,
                                                      const rg_ranger_config& cfg, int w, int h,
                                                      int2* pts) {
-  const SampleGeom g = dev_sample_geom(det, kind, r, c, rows, cols, cfg, w, h);
+  return dev_sample_block_warp_g(dev_sample_geom(det, kind, r, c, rows, cols, cfg, w, h), det, occ, n_occ, occ_all,
+                                 n_all, self, w, h, pts);
+}
+__device__ __forceinline__ int dev_sample_block_warp_g(const SampleGeom& g, const rg_detection& det,
+                                                       const double* occ, int n_occ, const rg_detection* occ_all,
+                                                       int n_all, int self, int w, int h, int2* pts) {
   const int lane = threadIdx.x & 31;
   int base = 0;
   for (int c0 = 0; c0 < g.n * g.n; c0 += 32) {
