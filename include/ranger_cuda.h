@@ -56,6 +56,10 @@ const char* rg_last_error(const rg_ctx* ctx);
 const char* rg_create_error(void);
 /* library build identification: "sm_100a <git-describe-ish>" */
 const char* rg_build_info(void);
+/* Self-test of the matcher's integer division (Markstein correction on a
+ * table of RN(1/b)) against IEEE division on the device, for every
+ * b in [1, b_max] and 0 <= a <= 64 b; *mismatches = 0 when exact. */
+rg_status rg_selftest_division(rg_ctx* ctx, int b_max, int64_t* mismatches);
 
 /* Per-stage CUDA-event timing of the batched API (off by default). */
 rg_status rg_set_profiling(rg_ctx* ctx, int on);

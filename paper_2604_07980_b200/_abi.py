@@ -175,6 +175,7 @@ SIGNATURES = {
     "rg_last_error": (C.c_char_p, [P]),
     "rg_create_error": (C.c_char_p, []),
     "rg_build_info": (C.c_char_p, []),
+    "rg_selftest_division": (I, [P, I, C.POINTER(C.c_int64)]),
     "rg_set_profiling": (I, [P, I]),
     "rg_set_overlap": (I, [P, I]),
     "rg_sync": (I, [P]),

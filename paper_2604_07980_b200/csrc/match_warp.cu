@@ -74,6 +74,35 @@ __device__ __forceinline__ bool better(const Cand& a, const Cand& b) {  // censu
   return a.dx < b.dx;
 }
 
+// Correctly rounded a / b for the small non-negative integers of a pass
+// (Hamming sums and valid-point counts): Markstein's correction on the
+// correctly rounded reciprocal y = RN(1/b) from a per-device table --
+// q = RN(a y), r = a - b q (exact by FMA), RN(q + r y) = RN(a / b) -- instead
+// of the __ddiv_rn sequence.  Checked against __ddiv_rn for every b <= kRecip
+// and 0 <= a <= 64 b (rg_selftest_division; a pass's sums are <= 63 b).
+constexpr int kRecip = 4096;
+__constant__ double c_recip[kRecip + 1];
+__device__ __forceinline__ double div_int(int a, int b) {
+  if (b >= 1 && b <= kRecip) {
+    const double y = c_recip[b], da = (double)a, db = (double)b;
+    const double q = __dmul_rn(da, y);
+    const double r = __fma_rn(-q, db, da);
+    return __fma_rn(r, y, q);
+  }
+  return __ddiv_rn((double)a, (double)b);
+}
+
+__global__ void selftest_div_kernel(int b_max, unsigned long long* bad) {
+  const int b = blockIdx.x + 1;
+  if (b > b_max) return;
+  unsigned long long n = 0;
+  for (int a = threadIdx.x; a <= 64 * b; a += blockDim.x) {
+    const double x = div_int(a, b), y = __ddiv_rn((double)a, (double)b);
+    n += __double_as_longlong(x) != __double_as_longlong(y);
+  }
+  if (n) atomicAdd(bad, n);
+}
+
 __device__ __forceinline__ double subpixel(double cm, double c0, double cp) {  // census.hpp:167-171
   const double denom = __dsub_rn(__dadd_rn(cm, cp), __dmul_rn(2.0, c0));
   if (denom <= 0.0) return 0.0;
@@ -862,14 +891,14 @@ __device__ __forceinline__ void finish(const Pass& p, rg_match_result& r) {  // 
   r.has_value = 1;
   r.dx_int = p.dx;
   r.dy_int = p.dy;
-  r.cost = div_n((double)p.sum, p.n);
+  r.cost = div_int(p.sum, p.n);
   r.valid_points = p.n;
   r.dx_subpix = (double)p.dx;
   r.cost_minus = -1.0;
   r.cost_plus = -1.0;
   if (p.interior && p.cm_n > 0 && p.cp_n > 0) {
-    const double cm = div_n((double)p.cm_sum, p.cm_n);
-    const double cp = div_n((double)p.cp_sum, p.cp_n);
+    const double cm = div_int(p.cm_sum, p.cm_n);
+    const double cp = div_int(p.cp_sum, p.cp_n);
     r.cost_minus = cm;
     r.cost_plus = cp;
     r.dx_subpix = __dadd_rn((double)p.dx, subpixel(cm, r.cost, cp));
@@ -1173,6 +1202,25 @@ cudaError_t launch_match_slots(const int2* slot_pts, const Slot* slots, int32_t*
                                    : launch_variant<uint32_t, 16, 3>(RG_ARGS));
   }
 #undef RG_ARGS
+}
+
+// c_recip of the current device: RN(1 / b) (IEEE host division), b <= kRecip
+cudaError_t init_match_tables() {
+  static double tab[kRecip + 1];
+  static const bool filled = [] {
+    tab[0] = 0.0;
+    for (int b = 1; b <= kRecip; ++b) tab[b] = 1.0 / (double)b;
+    return true;
+  }();
+  (void)filled;
+  return cudaMemcpyToSymbol(c_recip, tab, sizeof(tab));
+}
+
+// div_int vs __ddiv_rn over b in [1, b_max], a in [0, 64 b]: mismatches
+cudaError_t selftest_division(int b_max, unsigned long long* d_bad, cudaStream_t s) {
+  b_max = std::min(std::max(b_max, 1), kRecip + 64);
+  selftest_div_kernel<<<b_max, 256, 0, s>>>(b_max, d_bad);
+  return cudaGetLastError();
 }
 
 }  // namespace rg

@@ -234,6 +234,9 @@ cudaError_t launch_match_blocks64(Raster64 L, Raster64 R, const int32_t* pts, co
                                   const rg_search_range* ranges, int n_blocks, int mode,
                                   double tau_v, rg_match_result* out, int max_points,
                                   cudaStream_t s);
+// c_recip table of the matcher's integer divisions (once per device) and its check
+cudaError_t init_match_tables();
+cudaError_t selftest_division(int b_max, unsigned long long* d_bad, cudaStream_t s);
 // K2a slot sampler (match_warp.cu): the points of every planned slot into
 // slot_pts (capacity x ((max_points + 1) & ~1)), counts in Slot::pad; whether
 // the matcher for this batch reads them (else it samples in-warp)

@@ -96,6 +96,13 @@ class Context:
         """rg_range_frames schedule: chunked census/matcher overlap (opt-in) or one stream (default)."""
         self.check(lib().rg_set_overlap(self._h, 1 if on else 0))
 
+    def selftest_division(self, b_max: int = 4096) -> int:
+        """rg_selftest_division: mismatches of the matcher's table-driven
+        integer division against IEEE division (b <= b_max, a <= 64 b)."""
+        n = C.c_int64(0)
+        self.check(lib().rg_selftest_division(self._h, int(b_max), C.byref(n)))
+        return int(n.value)
+
     def sync(self) -> int:
         """rg_sync: wait for the asynchronous rg_range_frames batches; returns
         RG_OK or RG_EOVERFLOW (a batch produced no results: resubmit it)."""

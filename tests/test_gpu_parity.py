@@ -26,6 +26,16 @@ def det_c(d):
     return _abi.Detection(d.cx, d.cy, d.w, d.h, d.class_id, d.id)
 
 
+# ------------------------------------------------------------------ arithmetic
+def test_matcher_integer_division_is_ieee(ctx):
+    """The matcher's cost / neighbour-cost quotients (integer sum / point
+    count) use a table of RN(1/b) and one Markstein correction instead of
+    __ddiv_rn; every (a, b) with b <= 4096 and a <= 64 b (a pass's sums are
+    <= 63 b) must give the IEEE quotient's bits -- and b beyond the table
+    falls back to the division."""
+    assert ctx.selftest_division(4096 + 64) == 0
+
+
 # ------------------------------------------------------------------ census
 @pytest.mark.parametrize("w,h,ow,oh", [(9, 9, 9, 9), (20, 15, 20, 15), (41, 33, 20, 16), (64, 48, 64, 48),
                                        (641, 481, 320, 240), (1920, 1080, 960, 540), (133, 77, 66, 38)])
