@@ -82,6 +82,8 @@ __device__ __forceinline__ bool better(const Cand& a, const Cand& b) {  // censu
 // and 0 <= a <= 64 b (rg_selftest_division; a pass's sums are <= 63 b).
 constexpr int kRecip = 4096;
 __constant__ double c_recip[kRecip + 1];
+// RN(1/b) for div_rc (0 outside the table: the IEEE division)
+__device__ __forceinline__ double recip(int b) { return b >= 1 && b <= kRecip ? c_recip[b] : 0.0; }
 __device__ __forceinline__ double div_int(int a, int b) {
   if (b >= 1 && b <= kRecip) {
     const double y = c_recip[b], da = (double)a, db = (double)b;
@@ -98,6 +100,19 @@ __global__ void selftest_div_kernel(int b_max, unsigned long long* bad) {
   unsigned long long n = 0;
   for (int a = threadIdx.x; a <= 64 * b; a += blockDim.x) {
     const double x = div_int(a, b), y = __ddiv_rn((double)a, (double)b);
+    n += __double_as_longlong(x) != __double_as_longlong(y);
+  }
+  // div_rc with arbitrary numerators (the sampler's coordinates): 64 b
+  // pseudo-random doubles of magnitude 2^-12 .. 2^20 (either sign) per b
+  const double rb = recip(b);
+  for (int t = threadIdx.x; t <= 64 * b; t += blockDim.x) {
+    unsigned long long z = (unsigned long long)b * 0x9E3779B97F4A7C15ull + (unsigned long long)t * 0xBF58476D1CE4E5B9ull;
+    z ^= z >> 31;
+    z *= 0x94D049BB133111EBull;
+    z ^= z >> 29;
+    const int ex = (int)((z >> 53) % 33) - 12;
+    const double a = ldexp(1.0 + (double)(z & 0xFFFFFFFFFFFFFull) * 0x1p-52, ex) * ((z >> 52) & 1 ? -1.0 : 1.0);
+    const double x = div_rc(a, (double)b, rb), y = __ddiv_rn(a, (double)b);
     n += __double_as_longlong(x) != __double_as_longlong(y);
   }
   if (n) atomicAdd(bad, n);
@@ -960,8 +975,9 @@ __global__ void __launch_bounds__(WPB * 32) sample_slots_kernel(
   const int d0 = det_off[s.frame], d1 = det_off[s.frame + 1];
   const bool all = warp_occluders(det, e.det, dets, d0, d1, img_w, img_h, occ[warp], &nocc[warp], lane);
   const int np = dev_sample_block_warp_g(
-      dev_sample_geom_k(det, e.kind, s.pad >> 16, s.pad & 0xFFFF, e.rows, e.cols, sk, img_w, img_h), det, occ[warp],
-      min(nocc[warp], kWarpOcc), all ? dets + d0 : nullptr, d1 - d0, e.det - d0, img_w, img_h,
+      dev_sample_geom_k(det, e.kind, s.pad >> 16, s.pad & 0xFFFF, e.rows, e.cols, sk, img_w, img_h, recip(e.cols),
+                        recip(e.rows)),
+      det, occ[warp], min(nocc[warp], kWarpOcc), all ? dets + d0 : nullptr, d1 - d0, e.det - d0, img_w, img_h,
       pts_out + (size_t)slot * maxp);
   if (lane == 0) {
     slots[slot].pad = np;
@@ -1014,9 +1030,10 @@ __global__ void __launch_bounds__(WPB * 32, MINB) match_slots_warp_kernel(
       const rg_detection det = dets[e.det];
       const int d0 = det_off[s.frame], d1 = det_off[s.frame + 1];
       const bool all = warp_occluders(det, e.det, dets, d0, d1, img_w, img_h, occ[warp], &nocc[warp], lane);
-      np = dev_sample_block_warp_g(
-          dev_sample_geom_k(det, e.kind, s.pad >> 16, s.pad & 0xFFFF, e.rows, e.cols, sk, img_w, img_h), det,
-          occ[warp], min(nocc[warp], kWarpOcc), all ? dets + d0 : nullptr, d1 - d0, e.det - d0, img_w, img_h, pts);
+      np = dev_sample_block_warp_g(dev_sample_geom_k(det, e.kind, s.pad >> 16, s.pad & 0xFFFF, e.rows, e.cols, sk,
+                                                     img_w, img_h, recip(e.cols), recip(e.rows)),
+                                   det, occ[warp], min(nocc[warp], kWarpOcc), all ? dets + d0 : nullptr, d1 - d0,
+                                   e.det - d0, img_w, img_h, pts);
       far = e.kind == RG_KIND_FAR;
     }
     rg_match_result r;

@@ -22,6 +22,17 @@ __device__ __forceinline__ double half_of(double v) { return __dmul_rn(v, 0.5); 
 __device__ __forceinline__ double div_n(double x, int n) {
   return (n & (n - 1)) == 0 ? __dmul_rn(x, 1.0 / (double)n) : __ddiv_rn(x, (double)n);
 }
+// RN(a / b) for an integer-valued divisor b given rb = RN(1 / b) (0: the IEEE
+// division): q = RN(a rb) is within an ulp of a / b, r = a - b q is exact by
+// FMA, and RN(q + r rb) = RN(a / b + e) with |e| <= 2^-53 ulp, while a / b
+// is never a rounding midpoint (b M would need 54 significant bits) and a
+// non-midpoint quotient lies >= ulp / (2 b) from one (Markstein's correction).
+__device__ __forceinline__ double div_rc(double a, double b, double rb) {
+  if (rb == 0.0) return __ddiv_rn(a, b);
+  const double q = __dmul_rn(a, rb);
+  const double r = __fma_rn(-q, b, a);
+  return __fma_rn(r, rb, q);
+}
 __device__ __forceinline__ double dmin(double a, double b) { return b < a ? b : a; }  // std::min
 __device__ __forceinline__ double dmax(double a, double b) { return a < b ? b : a; }  // std::max
 
@@ -99,6 +110,7 @@ __device__ __forceinline__ void dev_close_grid(const PBox& b, const rg_ranger_co
 struct SampleGeom {
   PBox box;
   double bw, bh, sx0, sy0, sw, sh;
+  double rn, rw, rh;  // RN(1/n), RN(1/w), RN(1/h) for div_rc (0: IEEE division)
   int n, cw, ch;
   uint32_t magic;  // ceil(2^32 / n): idx / n = umulhi(idx, magic) (0: divide)
   bool far;
@@ -111,6 +123,7 @@ struct SampleConst {
   int nf, nc;      // grid side points of FAR blocks / CLOSE sub-blocks (:165-168, :192-194)
   uint32_t mf, mc; // ceil(2^32 / nf), ceil(2^32 / nc)
   int dxc;         // ceil(dx_max_close / close_scale) (:218)
+  double rnf, rnc, rw, rh;  // RN(1/nf), RN(1/nc), RN(1/w), RN(1/h) (IEEE host divisions)
 };
 inline SampleConst make_sample_const(const rg_ranger_config& c, int w, int h) {
   SampleConst k;
@@ -124,6 +137,10 @@ inline SampleConst make_sample_const(const rg_ranger_config& c, int w, int h) {
   k.mf = k.nf > 1 && k.nf <= 1024 ? (uint32_t)(0xFFFFFFFFu / (uint32_t)k.nf) + 1u : 0u;
   k.mc = k.nc > 1 && k.nc <= 1024 ? (uint32_t)(0xFFFFFFFFu / (uint32_t)k.nc) + 1u : 0u;
   k.dxc = (c.dx_max_close + c.close_scale - 1) / c.close_scale;
+  k.rnf = 1.0 / (double)k.nf;
+  k.rnc = 1.0 / (double)k.nc;
+  k.rw = 1.0 / (double)w;
+  k.rh = 1.0 / (double)h;
   return k;
 }
 
@@ -140,6 +157,7 @@ __device__ __forceinline__ SampleGeom dev_sample_geom(const rg_detection& det, i
   g.cw = w / cfg.close_scale;
   g.ch = h / cfg.close_scale;
   g.magic = 0;
+  g.rn = g.rw = g.rh = 0.0;
   g.sx0 = g.sy0 = g.sw = g.sh = 0;
   if (!g.far) {
     g.sx0 = __dadd_rn(g.box.x0, __ddiv_rn(__dmul_rn((double)c, g.bw), (double)cols));
@@ -151,8 +169,10 @@ __device__ __forceinline__ SampleGeom dev_sample_geom(const rg_detection& det, i
 }
 
 // dev_sample_geom with the integer constants taken from k
+// (rcols, rrows: RN(1/cols), RN(1/rows) or 0)
 __device__ __forceinline__ SampleGeom dev_sample_geom_k(const rg_detection& det, int kind, int r, int c, int rows,
-                                                        int cols, const SampleConst& k, int w, int h) {
+                                                        int cols, const SampleConst& k, int w, int h,
+                                                        double rcols = 0.0, double rrows = 0.0) {
   SampleGeom g;
   g.box = pixel_box(det, w, h);
   g.bw = __dsub_rn(g.box.x1, g.box.x0);
@@ -160,14 +180,17 @@ __device__ __forceinline__ SampleGeom dev_sample_geom_k(const rg_detection& det,
   g.far = kind == RG_KIND_FAR;
   g.n = g.far ? k.nf : k.nc;
   g.magic = g.far ? k.mf : k.mc;
+  g.rn = g.far ? k.rnf : k.rnc;
+  g.rw = k.rw;
+  g.rh = k.rh;
   g.cw = k.cw;
   g.ch = k.ch;
   g.sx0 = g.sy0 = g.sw = g.sh = 0;
   if (!g.far) {
-    g.sx0 = __dadd_rn(g.box.x0, __ddiv_rn(__dmul_rn((double)c, g.bw), (double)cols));
-    g.sy0 = __dadd_rn(g.box.y0, __ddiv_rn(__dmul_rn((double)r, g.bh), (double)rows));
-    g.sw = __ddiv_rn(g.bw, (double)cols);
-    g.sh = __ddiv_rn(g.bh, (double)rows);
+    g.sx0 = __dadd_rn(g.box.x0, div_rc(__dmul_rn((double)c, g.bw), (double)cols, rcols));
+    g.sy0 = __dadd_rn(g.box.y0, div_rc(__dmul_rn((double)r, g.bh), (double)rows, rrows));
+    g.sw = div_rc(g.bw, (double)cols, rcols);
+    g.sh = div_rc(g.bh, (double)rows, rrows);
   }
   return g;
 }
@@ -181,14 +204,14 @@ __device__ __forceinline__ bool dev_sample_point(const SampleGeom& g, int idx, c
   const int j = g.magic ? (int)__umulhi((uint32_t)idx, g.magic) : idx / g.n, i = idx - j * g.n;
   double fx, fy;
   if (g.far) {
-    fy = __dadd_rn(g.box.y0, div_n(__dmul_rn(__dadd_rn((double)j, 0.5), g.bh), g.n));
-    fx = __dadd_rn(g.box.x0, div_n(__dmul_rn(__dadd_rn((double)i, 0.5), g.bw), g.n));
+    fy = __dadd_rn(g.box.y0, div_rc(__dmul_rn(__dadd_rn((double)j, 0.5), g.bh), (double)g.n, g.rn));
+    fx = __dadd_rn(g.box.x0, div_rc(__dmul_rn(__dadd_rn((double)i, 0.5), g.bw), (double)g.n, g.rn));
     *px = (int)lround(fx);
     *py = (int)lround(fy);
     if (*px < 0 || *px >= w || *py < 0 || *py >= h) return false;
   } else {
-    fy = __dadd_rn(g.sy0, div_n(__dmul_rn(__dadd_rn((double)j, 0.5), g.sh), g.n));
-    fx = __dadd_rn(g.sx0, div_n(__dmul_rn(__dadd_rn((double)i, 0.5), g.sw), g.n));
+    fy = __dadd_rn(g.sy0, div_rc(__dmul_rn(__dadd_rn((double)j, 0.5), g.sh), (double)g.n, g.rn));
+    fx = __dadd_rn(g.sx0, div_rc(__dmul_rn(__dadd_rn((double)i, 0.5), g.sw), (double)g.n, g.rn));
     if (fx < 0 || fx >= w || fy < 0 || fy >= h) return false;
   }
   // occluded points drop (template_match.hpp:159-163, 181, 212)
@@ -203,8 +226,8 @@ __device__ __forceinline__ bool dev_sample_point(const SampleGeom& g, int idx, c
       if (box_contains(occ[4 * k], occ[4 * k + 1], occ[4 * k + 2], occ[4 * k + 3], fx, fy)) return false;
   }
   if (!g.far) {  // map into the reduced raster (template_match.hpp:213-215)
-    *px = (int)lround(__ddiv_rn(__dmul_rn(fx, (double)g.cw), (double)w));
-    *py = (int)lround(__ddiv_rn(__dmul_rn(fy, (double)g.ch), (double)h));
+    *px = (int)lround(div_rc(__dmul_rn(fx, (double)g.cw), (double)w, g.rw));
+    *py = (int)lround(div_rc(__dmul_rn(fy, (double)g.ch), (double)h, g.rh));
     if (*px < 0 || *px >= g.cw || *py < 0 || *py >= g.ch) return false;
   }
   return true;
