@@ -923,9 +923,27 @@ __device__ __forceinline__ void finish(const Pass& p, rg_match_result& r) {  // 
 // Occluders of `det` (index self) among the frame's detections [d0, d1)
 // (find_occluders, template_match.hpp:71-89) into the warp's box list occ;
 // returns whether any did not fit (the sampler then scans every detection).
-__device__ __forceinline__ bool warp_occluders(const rg_detection& det, int self, const rg_detection* dets,
-                                               int d0, int d1, int img_w, int img_h, double* occ, int* nocc,
-                                               int lane) {
+// From the planner's mask when it has one (frames of <= 64 detections).
+__device__ __forceinline__ bool warp_occluders(const ObjEntry& e, const rg_detection& det, int self,
+                                               const rg_detection* dets, int d0, int d1, int img_w, int img_h,
+                                               double* occ, int* nocc, int lane) {
+  if (e.occ_known) {
+    const unsigned long long m = ((unsigned long long)e.occ_hi << 32) | e.occ_lo;
+    const int k = __popcll(m);
+    if (k > kWarpOcc) return true;
+    if (lane < k) {  // lane k takes the k-th set bit
+      unsigned long long r = m;
+      for (int t = 0; t < lane; ++t) r &= r - 1;
+      const PBox b = pixel_box(dets[d0 + __ffsll((long long)r) - 1], img_w, img_h);
+      occ[4 * lane] = b.x0;
+      occ[4 * lane + 1] = b.y0;
+      occ[4 * lane + 2] = b.x1;
+      occ[4 * lane + 3] = b.y1;
+    }
+    if (lane == 0) *nocc = k;
+    __syncwarp();
+    return false;
+  }
   if (lane == 0) *nocc = 0;
   __syncwarp();
   bool overflow = false;
@@ -973,7 +991,7 @@ __global__ void __launch_bounds__(WPB * 32) sample_slots_kernel(
   const ObjEntry e = objs[s.obj];
   const rg_detection det = dets[e.det];
   const int d0 = det_off[s.frame], d1 = det_off[s.frame + 1];
-  const bool all = warp_occluders(det, e.det, dets, d0, d1, img_w, img_h, occ[warp], &nocc[warp], lane);
+  const bool all = warp_occluders(e, det, e.det, dets, d0, d1, img_w, img_h, occ[warp], &nocc[warp], lane);
   const int np = dev_sample_block_warp_g(
       dev_sample_geom_k(det, e.kind, s.pad >> 16, s.pad & 0xFFFF, e.rows, e.cols, sk, img_w, img_h, recip(e.cols),
                         recip(e.rows)),
@@ -1029,7 +1047,7 @@ __global__ void __launch_bounds__(WPB * 32, MINB) match_slots_warp_kernel(
       const ObjEntry e = objs[s.obj];
       const rg_detection det = dets[e.det];
       const int d0 = det_off[s.frame], d1 = det_off[s.frame + 1];
-      const bool all = warp_occluders(det, e.det, dets, d0, d1, img_w, img_h, occ[warp], &nocc[warp], lane);
+      const bool all = warp_occluders(e, det, e.det, dets, d0, d1, img_w, img_h, occ[warp], &nocc[warp], lane);
       np = dev_sample_block_warp_g(dev_sample_geom_k(det, e.kind, s.pad >> 16, s.pad & 0xFFFF, e.rows, e.cols, sk,
                                                      img_w, img_h, recip(e.cols), recip(e.rows)),
                                    det, occ[warp], min(nocc[warp], kWarpOcc), all ? dets + d0 : nullptr, d1 - d0,

@@ -139,7 +139,13 @@ __global__ void __launch_bounds__(PT) plan_frames_kernel(
       e.rows = rows;
       e.cols = cols;
       e.frame = f;
-      e.pad = 0;
+      // occluders among the frame's detections (find_occluders,
+      // template_match.hpp:71-89), once per object instead of once per slot
+      e.occ_known = n <= 64;
+      e.occ_lo = e.occ_hi = 0u;
+      if (n <= 64)
+        for (int j = 0; j < n; ++j)
+          if (j != i && dev_occludes(di, D[j])) (j < 32 ? e.occ_lo : e.occ_hi) |= 1u << (j & 31);
       const int g = f * out_stride + k;
       objs[g] = e;
       rg_object_disparity od;

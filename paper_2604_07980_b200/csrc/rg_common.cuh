@@ -113,7 +113,8 @@ struct ObjEntry {
   int32_t n_slots;    // FAR 1, CLOSE rows*cols
   int32_t rows, cols; // CLOSE sub-block grid
   int32_t frame;
-  int32_t pad;
+  int32_t occ_known;  // 1: occ_lo/hi hold the occluders (frames of <= 64 detections)
+  uint32_t occ_lo, occ_hi;  // bit j: detection d0 + j of the frame occludes this one
 };
 
 // a slot = one potential QueryBlock (FAR block or CLOSE sub-block)
