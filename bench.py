@@ -730,19 +730,24 @@ def main():
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
+    x0 = ctx.transfer()
     t0 = time.perf_counter()
     e2e_steps = max(2, args.steps // 2)
     for _ in range(e2e_steps):
         eng.range_host(hL, hR, h_recs, h_offs, h_out, h_cnt, chunk=32, stream=stream.cuda_stream)
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
+    x1 = ctx.transfer()
     te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_value = int(h_cnt.sum()) * e2e_steps * world / float(te.item())
     e2e_parity = bool(h_out.tobytes() == d_out.cpu().numpy().tobytes()[:h_out.nbytes])
-    h2d = int(hL.nbytes + hR.nbytes + h_recs.nbytes + h_offs.nbytes)
-    d2h = int(h_out.nbytes + h_cnt.nbytes)
+    # bytes the library moved per step (rg_get_transfer): the zero-copy
+    # gathers fetch only the image bytes the ROI census reads
+    h2d = (x1[0] - x0[0]) // e2e_steps
+    d2h = (x1[1] - x0[1]) // e2e_steps
+    h2d_full = int(hL.nbytes + hR.nbytes + h_recs.nbytes + h_offs.nbytes)
     # the e2e bound: this box's pinned host -> device copy bandwidth (one
     # 256 MiB copy stream, CUDA events, best of 6 x 16 copies)
     pcie_gbs = None
@@ -949,6 +954,10 @@ def main():
             "feed": "device-resident HBM ring, every frame rendered on the GPU by rg_render_frames_device",
             "e2e": {"value": e2e_value, "unit": "boxes/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "api": "rg_range_frames_host (pinned host frames, chunked H2D/compute/D2H)",
+                    "h2d": "bytes the library moved (rg_get_transfer): detections and offsets by copy, and of "
+                           "the frames only the 16-B segments of the image rows the ROI census reads, fetched "
+                           "zero-copy by gather_rows_kernel",
+                    "h2d_full_frame_bytes_per_step": h2d_full,
                     "records_equal_device_path": e2e_parity,
                     "bound": {"kind": "pcie_h2d", "achieved_gbs": e2e_h2d_gbs, "peak_gbs": pcie_gbs,
                               "frac": (e2e_h2d_gbs / pcie_gbs) if pcie_gbs else None,

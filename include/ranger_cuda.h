@@ -79,6 +79,12 @@ rg_status rg_reset_counters(rg_ctx* ctx);
  * evaluations (sum over blocks and candidates of contributing points,
  * census.hpp:209-221, forward + backward) and planned blocks (slots). */
 rg_status rg_get_work(rg_ctx* ctx, int64_t* hamming_evals, int64_t* blocks);
+/* Host <-> device bytes moved by rg_range_frames_host since the last
+ * rg_reset_counters (frames, detections, offsets, shifts in; records and
+ * counts out).  With pinned caller frames and batches that take the ROI
+ * census, only the image bytes the census reads are fetched (zero-copy, in
+ * 16-B segments); otherwise whole frames are copied. */
+rg_status rg_get_transfer(rg_ctx* ctx, int64_t* h2d_bytes, int64_t* d2h_bytes);
 
 /* ---------------------------------------------------------------- types */
 

@@ -176,6 +176,7 @@ SIGNATURES = {
     "rg_create_error": (C.c_char_p, []),
     "rg_build_info": (C.c_char_p, []),
     "rg_selftest_division": (I, [P, I, C.POINTER(C.c_int64)]),
+    "rg_get_transfer": (I, [P, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "rg_set_profiling": (I, [P, I]),
     "rg_set_overlap": (I, [P, I]),
     "rg_sync": (I, [P]),

@@ -956,6 +956,75 @@ __global__ void __launch_bounds__(32) census64_rowtile_kernel(
   }
 }
 
+// Host-fed batches (rg_range_frames_host): the image bytes the ROI census
+// reads for the matcher, fetched straight from the caller's pinned frames
+// over PCIe (zero-copy) instead of copy-engine transfers of whole frames.
+// Per detection and image the rectangle of census_rows_kernel (tight: the
+// matcher's read set; else the reference's ROI rectangle), in source pixels
+// and dilated by the census window (RX columns, RY rows each side) plus one
+// pixel, at 16-B granularity.  One warp per (image row, side, frame): it
+// marks the row's needed 16-B segments from every detection of the frame,
+// then copies them.  Bytes moved are added to bytes[frame & 63].
+constexpr int GR_WARPS = 4;
+constexpr int GR_SEGW = 8;  // mask words per row: <= 4096 columns
+template <int RX, int RY>
+__global__ void __launch_bounds__(GR_WARPS * 32) gather_rows_kernel(
+    const uint8_t* __restrict__ hl, const uint8_t* __restrict__ hr, int64_t src_stride, int src_pitch,
+    uint8_t* __restrict__ dl, uint8_t* __restrict__ dr, int64_t dst_stride, int dst_pitch, int w, int h,
+    const rg_detection* __restrict__ dets, const int32_t* __restrict__ det_off, double tau_s, int cw, int ch,
+    int dxf, int dxs, int tight, const int32_t* __restrict__ lshift, unsigned long long* __restrict__ bytes) {
+  __shared__ uint32_t mask[GR_WARPS][GR_SEGW];
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r = blockIdx.x * GR_WARPS + wid, side = blockIdx.y, f = blockIdx.z;
+  if (r >= h) return;  // warp-uniform
+  if (lane < GR_SEGW) mask[wid][lane] = 0u;
+  __syncwarp();
+  const int sh = (side == 0 && lshift) ? lshift[f] : 0;
+  const double sy = __ddiv_rn((double)ch, (double)h), sx = __ddiv_rn((double)cw, (double)w);
+  auto clampi = [](double v) { return (int)fmin(fmax(v, -1.0e9), 1.0e9); };
+  const int d0 = det_off[f], n = det_off[f + 1] - d0;
+  for (int i = lane; i < n; i += 32) {
+    const rg_detection d = dets[d0 + i];
+    const PBox b = pixel_box(d, w, h);
+    const bool far = dev_classify(d, w, h, tau_s) == RG_KIND_FAR;
+    int bx0, bx1, by0, by1, dxm, W, H, s;
+    if (far) {
+      by0 = clampi(floor(b.y0)), by1 = clampi(ceil(b.y1)), bx0 = clampi(floor(b.x0)), bx1 = clampi(ceil(b.x1));
+      dxm = dxf + 2, W = w, H = h, s = 1;
+    } else {
+      by0 = clampi(floor(__dmul_rn(b.y0, sy))), by1 = clampi(ceil(__dmul_rn(b.y1, sy)));
+      bx0 = clampi(floor(__dmul_rn(b.x0, sx))), bx1 = clampi(ceil(__dmul_rn(b.x1, sx)));
+      dxm = dxs + 2, W = cw, H = ch, s = 2;
+    }
+    const int a = max(0, by0 - 3), e = min(H, by1 + 4), c0 = max(0, bx0 - dxm), c1 = min(W, bx1 + dxm + 1);
+    int ra = a, re = e, ce = c1;
+    if (tight) {
+      ra = max(0, by0 - 1 - side), re = min(H, by1 + 2 + side);
+      if (side) ce = min(W, bx1 + 3);
+    }
+    if (ra >= re || c0 >= ce) continue;
+    // raster rows [ra, re) -> image rows read by their windows (left image:
+    // shifted by sh and clamped like the census row loads)
+    int ya = s * ra - RY - 1, ye = s * (re - 1) + RY + 1;
+    ya = min(max(ya - sh, 0), h - 1), ye = min(max(ye - sh, 0), h - 1);
+    if (r < ya || r > ye) continue;
+    const int xa = max(0, s * c0 - RX - 1), xe = min(w - 1, s * (ce - 1) + RX + 1);
+    for (int sg = xa >> 4; sg <= (xe >> 4); ++sg) atomicOr(&mask[wid][sg >> 5], 1u << (sg & 31));
+  }
+  __syncwarp();
+  const uint8_t* src = (side ? hr : hl) + (int64_t)f * src_stride + (int64_t)r * src_pitch;
+  uint8_t* dst = (side ? dr : dl) + (int64_t)f * dst_stride + (int64_t)r * dst_pitch;
+  const int nseg = (w + 15) >> 4;
+  int moved = 0;
+  for (int sg = lane; sg < nseg; sg += 32) {
+    if (!((mask[wid][sg >> 5] >> (sg & 31)) & 1u)) continue;
+    *reinterpret_cast<uint4*>(dst + 16 * sg) = __ldcs(reinterpret_cast<const uint4*>(src + 16 * sg));
+    ++moved;
+  }
+  moved = __reduce_add_sync(0xffffffffu, moved);
+  if (lane == 0 && moved) atomicAdd(bytes + (f & 63), 16ull * (unsigned long long)moved);
+}
+
 // census_transform_rois mask (census.hpp:111-136): keep codes inside the
 // union of the clipped rectangles, zero elsewhere.  Kept codes leave in the
 // reference layout (sentinel bit 25) whichever layout they were computed in.
@@ -1172,6 +1241,36 @@ cudaError_t launch_census64_rois(const uint8_t* left, const uint8_t* right, int 
   census64_rowtile_kernel<2><<<grid, 32, c64_smem<2>(), s>>>(left, right, frame_stride, pitch, w, h, sl, sr, gs,
                                                              lshift, rl.tiles, rl.tile_stride, rl.red_off,
                                                              rl.side_off);
+  return cudaGetLastError();
+}
+
+// Zero-copy gather of the census read sets of n_frames pinned host frames
+// (see gather_rows_kernel); cudaErrorNotSupported when the layout does not
+// allow 16-B segments (the caller then copies whole frames).
+cudaError_t launch_gather_rows(const uint8_t* hl, const uint8_t* hr, int64_t src_stride, int src_pitch, uint8_t* dl,
+                               uint8_t* dr, int64_t dst_stride, int dst_pitch, int w, int h, int n_frames,
+                               const rg_detection* dets, const int32_t* det_off, double tau_s, int close_scale,
+                               int dx_far, int dx_close_scaled, bool wide, const int32_t* lshift,
+                               unsigned long long* bytes, cudaStream_t s) {
+  if (n_frames <= 0) return cudaSuccess;
+  const auto al = [](const void* p) { return reinterpret_cast<uintptr_t>(p) % 16 == 0; };
+  if (src_pitch % 16 || dst_pitch % 16 || src_stride % 16 || dst_stride % 16 || !al(hl) || !al(hr) || !al(dl) ||
+      !al(dr) || w > 32 * GR_SEGW * 16 || w % 16)
+    return cudaErrorNotSupported;
+  static const int tight = [] {
+    const char* v = getenv("RG_CENSUS_TIGHT");
+    return v ? atoi(v) : 1;
+  }();
+  const dim3 grid((h + GR_WARPS - 1) / GR_WARPS, 2, n_frames);
+  const int cw = w / close_scale, ch = h / close_scale;
+  if (wide)
+    gather_rows_kernel<4, 3><<<grid, GR_WARPS * 32, 0, s>>>(hl, hr, src_stride, src_pitch, dl, dr, dst_stride,
+                                                            dst_pitch, w, h, dets, det_off, tau_s, cw, ch, dx_far,
+                                                            dx_close_scaled, tight, lshift, bytes);
+  else
+    gather_rows_kernel<2, 2><<<grid, GR_WARPS * 32, 0, s>>>(hl, hr, src_stride, src_pitch, dl, dr, dst_stride,
+                                                            dst_pitch, w, h, dets, det_off, tau_s, cw, ch, dx_far,
+                                                            dx_close_scaled, tight, lshift, bytes);
   return cudaGetLastError();
 }
 

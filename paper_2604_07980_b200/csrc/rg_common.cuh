@@ -147,6 +147,7 @@ struct rg_ctx {
   int64_t total_launches = 0;
   int64_t hamming_evals = 0;  // algorithmic matcher work of the batched path
   int64_t slots_total = 0;    // potential QueryBlocks planned
+  int64_t h2d_bytes = 0, d2h_bytes = 0;  // host <-> device bytes of rg_range_frames_host
   cudaEvent_t ev[12] = {};
   int slot_capacity = 0;    // grows on RG_EOVERFLOW
   int64_t last_slots = 0;   // slots used by the last batch
@@ -179,7 +180,7 @@ enum BufId {
   B_OBJ, B_SLOTS, B_SLOT_RES, B_OUT, B_OUT_CNT, B_COUNTERS, B_MAPX, B_MAPY,
   B_PTS, B_OFFS, B_RANGES, B_MRES, B_TMP0, B_TMP1, B_TMP2, B_TMP3, B_STATS,
   B_BM_L, B_BM_R, B_BM_OUT, B_BM_CNT, B_ROIS, B_STAGE_L, B_STAGE_R, B_SHIFT,
-  B_SEQ, B_SGM_COST, B_SGM_ACC, B_BOX_IDX, B_BOX_OUT, B_SYNTH, B_ROWMASK, B_SLOT_PTS, B_COUNT
+  B_SEQ, B_SGM_COST, B_SGM_ACC, B_BOX_IDX, B_BOX_OUT, B_SYNTH, B_ROWMASK, B_SLOT_PTS, B_XFER, B_COUNT
 };
 
 // error helpers (defined in api.cu)
@@ -212,6 +213,11 @@ cudaError_t launch_census_rois(const uint8_t* left, const uint8_t* right, int n_
                                uint32_t* sr, const PadGeom& gs, const int32_t* lshift, bool internal,
                                const rg_detection* dets, const int32_t* det_off, double tau_s, int dx_far,
                                int dx_close_scaled, uint32_t* masks, cudaStream_t s);
+cudaError_t launch_gather_rows(const uint8_t* hl, const uint8_t* hr, int64_t src_stride, int src_pitch, uint8_t* dl,
+                               uint8_t* dr, int64_t dst_stride, int dst_pitch, int w, int h, int n_frames,
+                               const rg_detection* dets, const int32_t* det_off, double tau_s, int close_scale,
+                               int dx_far, int dx_close_scaled, bool wide, const int32_t* lshift,
+                               unsigned long long* bytes, cudaStream_t s);
 cudaError_t launch_census64_rois(const uint8_t* left, const uint8_t* right, int n_frames, int64_t frame_stride,
                                  int pitch, int w, int h, unsigned long long* fl, unsigned long long* fr,
                                  const PadGeom& gf, unsigned long long* sl, unsigned long long* sr,

@@ -96,6 +96,13 @@ class Context:
         """rg_range_frames schedule: chunked census/matcher overlap (opt-in) or one stream (default)."""
         self.check(lib().rg_set_overlap(self._h, 1 if on else 0))
 
+    def transfer(self) -> Tuple[int, int]:
+        """rg_get_transfer: (host->device, device->host) bytes moved by
+        rg_range_frames_host since the last reset_counters()."""
+        a, b = C.c_int64(0), C.c_int64(0)
+        self.check(lib().rg_get_transfer(self._h, C.byref(a), C.byref(b)))
+        return int(a.value), int(b.value)
+
     def selftest_division(self, b_max: int = 4096) -> int:
         """rg_selftest_division: mismatches of the matcher's table-driven
         integer division against IEEE division (b <= b_max, a <= 64 b)."""

@@ -64,6 +64,49 @@ def test_range_frames_device_and_host(ctx, chk, name):
         assert ho[f, :len(want)].tobytes() == want
 
 
+@pytest.mark.parametrize("name,n,wide,shift", [("c2", 12, False, False), ("c2", 13, False, True),
+                                               ("c3", 12, False, False), ("c1", 16, True, True),
+                                               ("c1", 16, False, False)])
+def test_range_host_zero_copy_gather(ctx, chk, name, n, wide, shift):
+    """rg_range_frames_host with pinned frames and chunks that take the ROI
+    census fetches only the image bytes the census reads (gather_rows_kernel,
+    zero-copy): the records equal the reference's, the staging buffers hold
+    junk elsewhere (a previous batch of other frames), and fewer bytes than
+    the frames cross the bus (rg_get_transfer)."""
+    import torch
+
+    fn = {"c1": S.scene_c1, "c2": S.scene_c2, "c3": S.scene_c3}[name]
+    L, R, D, cfg, sc = _frames(fn, n)
+    cfg.census_9x7 = wide
+    D = [d if i % 3 else list(reversed(d[: max(1, len(d) - i)])) for i, d in enumerate(D)]
+    sh = ((np.arange(n) % 5) - 2).astype(np.int32) if shift else None
+    maxd = max(len(d) for d in D)
+    eng = FrameEngine(sc.width, sc.height, cfg, maxd, S.F_PX, S.BASELINE_M, ctx=ctx)
+    recs, offs = pack_detections(D)
+
+    def pinned(a):
+        t = torch.empty(a.nbytes, dtype=torch.uint8).pin_memory()
+        v = t.numpy().view(a.dtype).reshape(a.shape)
+        v[...] = a
+        return t, v
+    keep = []
+    for noise in (255 - L, L):  # first fill the staging with other frames
+        tl, hL = pinned(noise if noise is not L else L)
+        tr, hR = pinned(255 - R if noise is not L else R)
+        keep += [tl, tr]
+        h_out = np.zeros(n * eng.out_stride, OUT_DTYPE)
+        h_cnt = np.zeros(n, np.int32)
+        x0 = ctx.transfer()
+        eng.range_host(hL, hR, recs, offs, h_out, h_cnt, chunk=n, left_shift=sh)
+        x1 = ctx.transfer()
+    assert 0 < x1[0] - x0[0] < L.nbytes + R.nbytes
+    ho = h_out.view(np.uint8).reshape(n, eng.out_stride * 32)
+    for f in range(n):
+        Lf = L[f] if sh is None else np.ascontiguousarray(shift_vertical(L[f], int(sh[f])))
+        want = _want(chk, Lf, R[f], D[f], cfg)
+        assert int(h_cnt[f]) * 32 == len(want) and ho[f, :len(want)].tobytes() == want, (name, f)
+
+
 def shift_vertical(img, dy):
     """image.hpp:145-154: out(x, y) = in(x, clamp(y - dy, 0, H - 1))."""
     h = img.shape[0]
