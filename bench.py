@@ -587,6 +587,7 @@ def main():
     ap.add_argument("--no-parity", action="store_true", help="skip the parity sweeps against oracle/_ref")
     ap.add_argument("--parity-c5-frames", type=int, default=256)
     ap.add_argument("--latency-runs", type=int, default=1000)
+    ap.add_argument("--e2e-chunk", type=int, default=64, help="frames per rg_range_frames_host chunk")
     ap.add_argument("--c3-frames", type=int, default=32, help="C3 frames per call (0: skip the C3 line)")
     ap.add_argument("--c3-parity-frames", type=int, default=16)
     ap.add_argument("--c1-frames", type=int, default=1024, help="9x7 C1 frames per call (0: skip)")
@@ -726,7 +727,7 @@ def main():
     h_out = pin(np.zeros(F * eng.out_stride, OUT_DTYPE))
     h_cnt = pin(np.zeros(F, np.int32))
     for _ in range(2):
-        eng.range_host(hL, hR, h_recs, h_offs, h_out, h_cnt, chunk=32, stream=stream.cuda_stream)
+        eng.range_host(hL, hR, h_recs, h_offs, h_out, h_cnt, chunk=args.e2e_chunk, stream=stream.cuda_stream)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -734,7 +735,7 @@ def main():
     t0 = time.perf_counter()
     e2e_steps = max(2, args.steps // 2)
     for _ in range(e2e_steps):
-        eng.range_host(hL, hR, h_recs, h_offs, h_out, h_cnt, chunk=32, stream=stream.cuda_stream)
+        eng.range_host(hL, hR, h_recs, h_offs, h_out, h_cnt, chunk=args.e2e_chunk, stream=stream.cuda_stream)
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
     x1 = ctx.transfer()

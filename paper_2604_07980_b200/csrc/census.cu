@@ -972,11 +972,15 @@ __global__ void __launch_bounds__(GR_WARPS * 32) gather_rows_kernel(
     const uint8_t* __restrict__ hl, const uint8_t* __restrict__ hr, int64_t src_stride, int src_pitch,
     uint8_t* __restrict__ dl, uint8_t* __restrict__ dr, int64_t dst_stride, int dst_pitch, int w, int h,
     const rg_detection* __restrict__ dets, const int32_t* __restrict__ det_off, double tau_s, int cw, int ch,
-    int dxf, int dxs, int tight, const int32_t* __restrict__ lshift, unsigned long long* __restrict__ bytes) {
+    int dxf, int dxs, int tight, const int32_t* __restrict__ lshift, unsigned long long* __restrict__ bytes,
+    int n_frames) {
   __shared__ uint32_t mask[GR_WARPS][GR_SEGW];
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int r = blockIdx.x * GR_WARPS + wid, side = blockIdx.y, f = blockIdx.z;
-  if (r >= h) return;  // warp-uniform
+  // a persistent grid (a few CTAs per SM, resident while the previous
+  // chunk's compute kernels run): warps stride over (row, side, frame)
+  for (int item = blockIdx.x * GR_WARPS + wid; item < h * 2 * n_frames; item += gridDim.x * GR_WARPS) {
+  const int r = item % h, side = (item / h) & 1, f = item / (2 * h);
+  __syncwarp();
   if (lane < GR_SEGW) mask[wid][lane] = 0u;
   __syncwarp();
   const int sh = (side == 0 && lshift) ? lshift[f] : 0;
@@ -1015,14 +1019,25 @@ __global__ void __launch_bounds__(GR_WARPS * 32) gather_rows_kernel(
   const uint8_t* src = (side ? hr : hl) + (int64_t)f * src_stride + (int64_t)r * src_pitch;
   uint8_t* dst = (side ? dr : dl) + (int64_t)f * dst_stride + (int64_t)r * dst_pitch;
   const int nseg = (w + 15) >> 4;
+  // every load of the lane in flight before the first store (PCIe latency)
+  uint4 v[GR_SEGW];
   int moved = 0;
-  for (int sg = lane; sg < nseg; sg += 32) {
-    if (!((mask[wid][sg >> 5] >> (sg & 31)) & 1u)) continue;
-    *reinterpret_cast<uint4*>(dst + 16 * sg) = __ldcs(reinterpret_cast<const uint4*>(src + 16 * sg));
-    ++moved;
+#pragma unroll
+  for (int t = 0; t < GR_SEGW; ++t) {
+    const int sg = lane + 32 * t;
+    if (sg < nseg && ((mask[wid][t] >> lane) & 1u)) v[t] = __ldcs(reinterpret_cast<const uint4*>(src + 16 * sg));
+  }
+#pragma unroll
+  for (int t = 0; t < GR_SEGW; ++t) {
+    const int sg = lane + 32 * t;
+    if (sg < nseg && ((mask[wid][t] >> lane) & 1u)) {
+      *reinterpret_cast<uint4*>(dst + 16 * sg) = v[t];
+      ++moved;
+    }
   }
   moved = __reduce_add_sync(0xffffffffu, moved);
   if (lane == 0 && moved) atomicAdd(bytes + (f & 63), 16ull * (unsigned long long)moved);
+  }
 }
 
 // census_transform_rois mask (census.hpp:111-136): keep codes inside the
@@ -1261,16 +1276,18 @@ cudaError_t launch_gather_rows(const uint8_t* hl, const uint8_t* hr, int64_t src
     const char* v = getenv("RG_CENSUS_TIGHT");
     return v ? atoi(v) : 1;
   }();
-  const dim3 grid((h + GR_WARPS - 1) / GR_WARPS, 2, n_frames);
+  static const int ctas = [] { const char* v = getenv("RG_GATHER_CTAS"); return v ? atoi(v) : 4 * 148; }();
+  const int items = h * 2 * n_frames;
+  const int grid = std::max(1, std::min(ctas, (items + GR_WARPS - 1) / GR_WARPS));
   const int cw = w / close_scale, ch = h / close_scale;
   if (wide)
     gather_rows_kernel<4, 3><<<grid, GR_WARPS * 32, 0, s>>>(hl, hr, src_stride, src_pitch, dl, dr, dst_stride,
                                                             dst_pitch, w, h, dets, det_off, tau_s, cw, ch, dx_far,
-                                                            dx_close_scaled, tight, lshift, bytes);
+                                                            dx_close_scaled, tight, lshift, bytes, n_frames);
   else
     gather_rows_kernel<2, 2><<<grid, GR_WARPS * 32, 0, s>>>(hl, hr, src_stride, src_pitch, dl, dr, dst_stride,
                                                             dst_pitch, w, h, dets, det_off, tau_s, cw, ch, dx_far,
-                                                            dx_close_scaled, tight, lshift, bytes);
+                                                            dx_close_scaled, tight, lshift, bytes, n_frames);
   return cudaGetLastError();
 }
 
