@@ -66,13 +66,15 @@ def test_range_frames_device_and_host(ctx, chk, name):
 
 @pytest.mark.parametrize("name,n,wide,shift", [("c2", 12, False, False), ("c2", 13, False, True),
                                                ("c3", 12, False, False), ("c1", 16, True, True),
-                                               ("c1", 16, False, False)])
+                                               ("c1", 16, False, False), ("c2", 1, False, False),
+                                               ("c2", 3, False, True), ("c1", 2, True, False)])
 def test_range_host_zero_copy_gather(ctx, chk, name, n, wide, shift):
-    """rg_range_frames_host with pinned frames and chunks that take the ROI
-    census fetches only the image bytes the census reads (gather_rows_kernel,
-    zero-copy): the records equal the reference's, the staging buffers hold
-    junk elsewhere (a previous batch of other frames), and fewer bytes than
-    the frames cross the bus (rg_get_transfer)."""
+    """rg_range_frames_host with pinned frames fetches only the image bytes
+    the census reads for the matcher (gather_rows_kernel, zero-copy; batches
+    of >= 12 frames take the ROI census, smaller ones the full-frame census
+    over partly stale staging): the records equal the reference's, the
+    staging buffers hold junk elsewhere (a previous batch of other frames),
+    and fewer bytes than the frames cross the bus (rg_get_transfer)."""
     import torch
 
     fn = {"c1": S.scene_c1, "c2": S.scene_c2, "c3": S.scene_c3}[name]
