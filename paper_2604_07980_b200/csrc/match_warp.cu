@@ -923,24 +923,20 @@ __device__ __forceinline__ void finish(const Pass& p, rg_match_result& r) {  // 
 // Occluders of `det` (index self) among the frame's detections [d0, d1)
 // (find_occluders, template_match.hpp:71-89) into the warp's box list occ;
 // returns whether any did not fit (the sampler then scans every detection).
-// From the planner's mask when it has one (frames of <= 64 detections).
-__device__ __forceinline__ bool warp_occluders(const ObjEntry& e, const rg_detection& det, int self,
-                                               const rg_detection* dets, int d0, int d1, int img_w, int img_h,
-                                               double* occ, int* nocc, int lane) {
-  if (e.occ_known) {
-    const unsigned long long m = ((unsigned long long)e.occ_hi << 32) | e.occ_lo;
-    const int k = __popcll(m);
-    if (k > kWarpOcc) return true;
-    if (lane < k) {  // lane k takes the k-th set bit
-      unsigned long long r = m;
-      for (int t = 0; t < lane; ++t) r &= r - 1;
-      const PBox b = pixel_box(dets[d0 + __ffsll((long long)r) - 1], img_w, img_h);
+// From the planner's list (ol, e.occ_n of them) when it has one.
+__device__ __forceinline__ bool warp_occluders(const ObjEntry& e, const int16_t* ol, const rg_detection& det,
+                                               int self, const rg_detection* dets, int d0, int d1, int img_w,
+                                               int img_h, double* occ, int* nocc, int lane) {
+  static_assert(kOccMax <= kWarpOcc, "the planner's list must fit the warp's boxes");
+  if (e.occ_n >= 0) {
+    if (lane < e.occ_n) {
+      const PBox b = pixel_box(dets[d0 + ol[lane]], img_w, img_h);
       occ[4 * lane] = b.x0;
       occ[4 * lane + 1] = b.y0;
       occ[4 * lane + 2] = b.x1;
       occ[4 * lane + 3] = b.y1;
     }
-    if (lane == 0) *nocc = k;
+    if (lane == 0) *nocc = e.occ_n;
     __syncwarp();
     return false;
   }
@@ -977,7 +973,7 @@ __device__ __forceinline__ bool warp_occluders(const ObjEntry& e, const rg_detec
 template <int WPB>
 __global__ void __launch_bounds__(WPB * 32) sample_slots_kernel(
     Slot* __restrict__ slots, const int32_t* __restrict__ counters, const ObjEntry* __restrict__ objs,
-    const rg_detection* __restrict__ dets, const int32_t* __restrict__ det_off, int img_w, int img_h,
+    const int16_t* __restrict__ occ_list, const rg_detection* __restrict__ dets, const int32_t* __restrict__ det_off, int img_w, int img_h,
     SampleConst sk, int2* __restrict__ pts_out, rg_ranger_stats* __restrict__ stats, int maxp,
     int capacity) {
   __shared__ double occ[WPB][4 * kWarpOcc];
@@ -991,7 +987,8 @@ __global__ void __launch_bounds__(WPB * 32) sample_slots_kernel(
   const ObjEntry e = objs[s.obj];
   const rg_detection det = dets[e.det];
   const int d0 = det_off[s.frame], d1 = det_off[s.frame + 1];
-  const bool all = warp_occluders(e, det, e.det, dets, d0, d1, img_w, img_h, occ[warp], &nocc[warp], lane);
+  const bool all = warp_occluders(e, occ_list + (int64_t)s.obj * kOccMax, det, e.det, dets, d0, d1, img_w, img_h,
+                                  occ[warp], &nocc[warp], lane);
   const int np = dev_sample_block_warp_g(
       dev_sample_geom_k(det, e.kind, s.pad >> 16, s.pad & 0xFFFF, e.rows, e.cols, sk, img_w, img_h, recip(e.cols),
                         recip(e.rows)),
@@ -1009,7 +1006,8 @@ __global__ void __launch_bounds__(WPB * 32) sample_slots_kernel(
 // batch: ~5x a CLOSE sub-block); CLOSE sub-blocks stay one per warp.
 template <typename CT, int WPB, int MINB, int PF = 0, bool COOP = false, bool V2 = false, bool PRE = false>
 __global__ void __launch_bounds__(WPB * 32, MINB) match_slots_warp_kernel(
-    const int2* __restrict__ pre_pts, const Slot* __restrict__ slots, int32_t* __restrict__ counters, const ObjEntry* __restrict__ objs,
+    const int2* __restrict__ pre_pts, const Slot* __restrict__ slots, int32_t* __restrict__ counters,
+    const ObjEntry* __restrict__ objs, const int16_t* __restrict__ occ_list,
     const rg_detection* __restrict__ dets, const int32_t* __restrict__ det_off,
     const CT* __restrict__ fl, const CT* __restrict__ fr, PadGeom gf,
     const CT* __restrict__ sl, const CT* __restrict__ sr, PadGeom gs, int img_w,
@@ -1047,7 +1045,8 @@ __global__ void __launch_bounds__(WPB * 32, MINB) match_slots_warp_kernel(
       const ObjEntry e = objs[s.obj];
       const rg_detection det = dets[e.det];
       const int d0 = det_off[s.frame], d1 = det_off[s.frame + 1];
-      const bool all = warp_occluders(e, det, e.det, dets, d0, d1, img_w, img_h, occ[warp], &nocc[warp], lane);
+      const bool all = warp_occluders(e, occ_list + (int64_t)s.obj * kOccMax, det, e.det, dets, d0, d1, img_w, img_h,
+                                  occ[warp], &nocc[warp], lane);
       np = dev_sample_block_warp_g(dev_sample_geom_k(det, e.kind, s.pad >> 16, s.pad & 0xFFFF, e.rows, e.cols, sk,
                                                      img_w, img_h, recip(e.cols), recip(e.rows)),
                                    det, occ[warp], min(nocc[warp], kWarpOcc), all ? dets + d0 : nullptr, d1 - d0,
@@ -1116,7 +1115,8 @@ __global__ void __launch_bounds__(WPB * 32, MINB) match_slots_warp_kernel(
 
 template <typename CT, int WPB, int MINB, int PF = 0, bool COOP = false, bool V2 = false, bool PRE = false>
 cudaError_t launch_variant(const int2* slot_pts, const Slot* slots, int32_t* counters, int slot_capacity,
-                                  const ObjEntry* objs, const rg_detection* dets, const int32_t* det_off,
+                                  const ObjEntry* objs, const int16_t* occ_list, const rg_detection* dets,
+                                  const int32_t* det_off,
                                   const void* fl, const void* fr, const PadGeom& gf, const void* sl,
                                   const void* sr, const PadGeom& gs, int img_w, int img_h, int trusted,
                                   rg_ranger_config cfg, rg_match_result* res, rg_ranger_stats* stats,
@@ -1139,7 +1139,8 @@ cudaError_t launch_variant(const int2* slot_pts, const Slot* slots, int32_t* cou
   // known on the device)
   const int grid = COOP ? std::min(slot_capacity, 148 * MINB) : (slot_capacity + WPB - 1) / WPB;
   if (PRE && !slot_pts) return cudaErrorInvalidValue;
-  kern<<<grid, WPB * 32, smem, s>>>(slot_pts, slots, counters, objs, dets, det_off, static_cast<const CT*>(fl),
+  kern<<<grid, WPB * 32, smem, s>>>(slot_pts, slots, counters, objs, occ_list, dets, det_off,
+                                    static_cast<const CT*>(fl),
                                     static_cast<const CT*>(fr), gf, static_cast<const CT*>(sl),
                                     static_cast<const CT*>(sr), gs, img_w, img_h, trusted, cfg,
                                     make_sample_const(cfg, img_w, img_h), res, stats,
@@ -1172,19 +1173,20 @@ bool match_presampled(int n_frames, int wide) {
 }
 
 cudaError_t launch_sample_slots(Slot* slots, const int32_t* counters, int slot_capacity, const ObjEntry* objs,
-                                const rg_detection* dets, const int32_t* det_off, int img_w, int img_h,
+                                const int16_t* occ_list, const rg_detection* dets, const int32_t* det_off, int img_w, int img_h,
                                 rg_ranger_config cfg, int2* slot_pts, rg_ranger_stats* stats, int max_points,
                                 cudaStream_t s) {
   if (slot_capacity <= 0) return cudaSuccess;
   constexpr int SW = 8;
   sample_slots_kernel<SW><<<(slot_capacity + SW - 1) / SW, SW * 32, 0, s>>>(
-      slots, counters, objs, dets, det_off, img_w, img_h, make_sample_const(cfg, img_w, img_h), slot_pts, stats,
+      slots, counters, objs, occ_list, dets, det_off, img_w, img_h, make_sample_const(cfg, img_w, img_h), slot_pts,
+      stats,
       (max_points + 1) & ~1, slot_capacity);
   return cudaGetLastError();
 }
 
 cudaError_t launch_match_slots(const int2* slot_pts, const Slot* slots, int32_t* counters, int slot_capacity,
-                               const ObjEntry* objs, const rg_detection* dets, const int32_t* det_off,
+                               const ObjEntry* objs, const int16_t* occ_list, const rg_detection* dets, const int32_t* det_off,
                                const void* fl, const void* fr, const PadGeom& gf, const void* sl,
                                const void* sr, const PadGeom& gs, int img_w, int img_h, int trusted,
                                int wide, rg_ranger_config cfg, rg_match_result* res,
@@ -1192,7 +1194,7 @@ cudaError_t launch_match_slots(const int2* slot_pts, const Slot* slots, int32_t*
                                int n_frames) {
   if (slot_capacity <= 0) return cudaSuccess;
   const int variant = match_variant();
-#define RG_ARGS slot_pts, slots, counters, slot_capacity, objs, dets, det_off, fl, fr, gf, sl, sr, gs, img_w, img_h, \
+#define RG_ARGS slot_pts, slots, counters, slot_capacity, objs, occ_list, dets, det_off, fl, fr, gf, sl, sr, gs, img_w, img_h, \
                 trusted, cfg, res, stats, max_points, s
   // blocks too large for the default warps per CTA fall back to fewer
   // (shared memory holds every warp's points: 16 or 24 B per point)

@@ -139,14 +139,8 @@ __global__ void __launch_bounds__(PT) plan_frames_kernel(
       e.rows = rows;
       e.cols = cols;
       e.frame = f;
-      // occluders among the frame's detections (find_occluders,
-      // template_match.hpp:71-89), once per object instead of once per slot
-      e.occ_known = n <= 64;
-      e.occ_lo = e.occ_hi = 0u;
-      if (n <= 64)
-        for (int j = 0; j < n; ++j)
-          if (j != i && dev_occludes(di, D[j])) (j < 32 ? e.occ_lo : e.occ_hi) |= 1u << (j & 31);
       const int g = f * out_stride + k;
+      e.occ_n = 0;  // occluders_kernel
       objs[g] = e;
       rg_object_disparity od;
       od.det_id = di.id;
@@ -200,6 +194,34 @@ __global__ void __launch_bounds__(PT) plan_frames_kernel(
       stats[f].n_close = b;
     }
   }
+}
+
+// Occluders of every selected object among its frame's detections
+// (find_occluders, template_match.hpp:71-89), once per object instead of once
+// per slot: a warp per object (grid over frames x objects, after K3), lanes
+// over the detections, frame-local indices in detection order; more than
+// kOccMax -> occ_n = -1 (the matcher then scans every detection itself).
+constexpr int OC_WARPS = 8;
+__global__ void __launch_bounds__(OC_WARPS * 32) occluders_kernel(
+    const rg_detection* __restrict__ dets, const int32_t* __restrict__ det_off, int out_stride,
+    const int32_t* __restrict__ out_count, ObjEntry* __restrict__ objs, int16_t* __restrict__ occ_list) {
+  const int f = blockIdx.y, k = blockIdx.x * OC_WARPS + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (k >= out_count[f]) return;  // warp-uniform
+  const int d0 = det_off[f], n = det_off[f + 1] - d0;
+  const int g = f * out_stride + k;
+  const int self = objs[g].det - d0;
+  const rg_detection di = dets[d0 + self];
+  int16_t* ol = occ_list + (int64_t)g * kOccMax;
+  int no = 0;
+  for (int j0 = 0; j0 < n && no <= kOccMax; j0 += 32) {
+    const int j = j0 + lane;
+    const bool occl = j < n && j != self && dev_occludes(di, dets[d0 + j]);
+    const unsigned bal = __ballot_sync(0xffffffffu, occl);
+    const int pos = no + __popc(bal & ((1u << lane) - 1u));
+    if (occl && pos < kOccMax) ol[pos] = (int16_t)j;
+    no += __popc(bal);
+  }
+  if (lane == 0) objs[g].occ_n = no <= kOccMax ? no : -1;
 }
 
 __global__ void __launch_bounds__(128) aggregate_kernel(
@@ -411,10 +433,14 @@ cudaError_t launch_plan_frames(const rg_detection* dets, const int32_t* det_off,
                                int h, rg_ranger_config cfg, int out_stride, ObjEntry* objs,
                                rg_object_disparity* out, int32_t* out_count, Slot* slots,
                                int slot_capacity, int32_t* counters, rg_ranger_stats* stats,
-                               int32_t* out_index, cudaStream_t s) {
+                               int32_t* out_index, int16_t* occ_list, cudaStream_t s) {
   if (n_frames <= 0) return cudaSuccess;
   plan_frames_kernel<<<n_frames, PT, 0, s>>>(dets, det_off, w, h, cfg, out_stride, objs, out,
                                              out_count, slots, slot_capacity, counters, stats, out_index);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess || out_stride <= 0) return e;
+  occluders_kernel<<<dim3((out_stride + OC_WARPS - 1) / OC_WARPS, n_frames), OC_WARPS * 32, 0, s>>>(
+      dets, det_off, out_stride, out_count, objs, occ_list);
   return cudaGetLastError();
 }
 

@@ -113,9 +113,9 @@ struct ObjEntry {
   int32_t n_slots;    // FAR 1, CLOSE rows*cols
   int32_t rows, cols; // CLOSE sub-block grid
   int32_t frame;
-  int32_t occ_known;  // 1: occ_lo/hi hold the occluders (frames of <= 64 detections)
-  uint32_t occ_lo, occ_hi;  // bit j: detection d0 + j of the frame occludes this one
+  int32_t occ_n;  // occluders in the planner's list (occ_list[g * kOccMax ..]); -1: more than kOccMax
 };
+constexpr int kOccMax = 32;  // occluders per object listed by the planner
 
 // a slot = one potential QueryBlock (FAR block or CLOSE sub-block)
 struct Slot {
@@ -180,7 +180,7 @@ enum BufId {
   B_OBJ, B_SLOTS, B_SLOT_RES, B_OUT, B_OUT_CNT, B_COUNTERS, B_MAPX, B_MAPY,
   B_PTS, B_OFFS, B_RANGES, B_MRES, B_TMP0, B_TMP1, B_TMP2, B_TMP3, B_STATS,
   B_BM_L, B_BM_R, B_BM_OUT, B_BM_CNT, B_ROIS, B_STAGE_L, B_STAGE_R, B_SHIFT,
-  B_SEQ, B_SGM_COST, B_SGM_ACC, B_BOX_IDX, B_BOX_OUT, B_SYNTH, B_ROWMASK, B_SLOT_PTS, B_XFER, B_COUNT
+  B_SEQ, B_SGM_COST, B_SGM_ACC, B_BOX_IDX, B_BOX_OUT, B_SYNTH, B_ROWMASK, B_SLOT_PTS, B_XFER, B_OCC, B_COUNT
 };
 
 // error helpers (defined in api.cu)
@@ -249,12 +249,12 @@ cudaError_t selftest_division(int b_max, unsigned long long* d_bad, cudaStream_t
 // the matcher for this batch reads them (else it samples in-warp)
 bool match_presampled(int n_frames, int wide);
 cudaError_t launch_sample_slots(Slot* slots, const int32_t* counters, int slot_capacity, const ObjEntry* objs,
-                                const rg_detection* dets, const int32_t* det_off, int img_w, int img_h,
+                                const int16_t* occ_list, const rg_detection* dets, const int32_t* det_off, int img_w, int img_h,
                                 rg_ranger_config cfg, int2* slot_pts, rg_ranger_stats* stats, int max_points,
                                 cudaStream_t s);
 // slot_pts: the K2a points (nullptr: the matcher samples in-warp)
 cudaError_t launch_match_slots(const int2* slot_pts, const Slot* slots, int32_t* counters, int slot_capacity,
-                               const ObjEntry* objs, const rg_detection* dets,
+                               const ObjEntry* objs, const int16_t* occ_list, const rg_detection* dets,
                                const int32_t* det_off, const void* fl, const void* fr,
                                const PadGeom& gf, const void* sl, const void* sr,
                                const PadGeom& gs, int img_w, int img_h, int trusted, int wide,
@@ -286,7 +286,7 @@ cudaError_t launch_plan_frames(const rg_detection* dets, const int32_t* det_off,
                                int w, int h, rg_ranger_config cfg, int out_stride, ObjEntry* objs,
                                rg_object_disparity* out, int32_t* out_count, Slot* slots,
                                int slot_capacity, int32_t* counters, rg_ranger_stats* stats,
-                               int32_t* out_index, cudaStream_t s);
+                               int32_t* out_index, int16_t* occ_list, cudaStream_t s);
 cudaError_t launch_aggregate(const ObjEntry* objs, const int32_t* out_count, int n_frames,
                              int out_stride, const rg_match_result* res, int slot_capacity,
                              rg_ranger_config cfg, double focal, double baseline, double* scratch,
