@@ -140,7 +140,7 @@ __global__ void __launch_bounds__(PT) plan_frames_kernel(
       e.cols = cols;
       e.frame = f;
       const int g = f * out_stride + k;
-      e.occ_n = 0;  // occluders_kernel
+      e.occ_n = -1;  // occluders_kernel lists them (else the matcher scans per slot)
       objs[g] = e;
       rg_object_disparity od;
       od.det_id = di.id;
@@ -433,12 +433,12 @@ cudaError_t launch_plan_frames(const rg_detection* dets, const int32_t* det_off,
                                int h, rg_ranger_config cfg, int out_stride, ObjEntry* objs,
                                rg_object_disparity* out, int32_t* out_count, Slot* slots,
                                int slot_capacity, int32_t* counters, rg_ranger_stats* stats,
-                               int32_t* out_index, int16_t* occ_list, cudaStream_t s) {
+                               int32_t* out_index, int16_t* occ_list, bool list_occluders, cudaStream_t s) {
   if (n_frames <= 0) return cudaSuccess;
   plan_frames_kernel<<<n_frames, PT, 0, s>>>(dets, det_off, w, h, cfg, out_stride, objs, out,
                                              out_count, slots, slot_capacity, counters, stats, out_index);
   const cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess || out_stride <= 0) return e;
+  if (e != cudaSuccess || out_stride <= 0 || !list_occluders) return e;
   occluders_kernel<<<dim3((out_stride + OC_WARPS - 1) / OC_WARPS, n_frames), OC_WARPS * 32, 0, s>>>(
       dets, det_off, out_stride, out_count, objs, occ_list);
   return cudaGetLastError();

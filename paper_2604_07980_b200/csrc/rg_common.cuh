@@ -286,7 +286,7 @@ cudaError_t launch_plan_frames(const rg_detection* dets, const int32_t* det_off,
                                int w, int h, rg_ranger_config cfg, int out_stride, ObjEntry* objs,
                                rg_object_disparity* out, int32_t* out_count, Slot* slots,
                                int slot_capacity, int32_t* counters, rg_ranger_stats* stats,
-                               int32_t* out_index, int16_t* occ_list, cudaStream_t s);
+                               int32_t* out_index, int16_t* occ_list, bool list_occluders, cudaStream_t s);
 cudaError_t launch_aggregate(const ObjEntry* objs, const int32_t* out_count, int n_frames,
                              int out_stride, const rg_match_result* res, int slot_capacity,
                              rg_ranger_config cfg, double focal, double baseline, double* scratch,
