@@ -447,7 +447,7 @@ def config_c1_9x7(args, ctx, dev, stream):
     full_bytes = 2 * (w * h + 8 * w * h + 8 * (w // 2) * (h // 2))  # B = 8 for 9x7
     req = census_required_bytes(dets, w, h, cfg.tau_s, cfg.close_scale, cfg.dx_max_far, cfg.dx_max_close,
                                 code_bytes=8, rx=4, ry=3)
-    cen_ms = stage_ms[0] / max(stage_launches[0], 1)
+    cen_ms = stage_ms[0] / reps  # per call (the ROI census is 3 kernel launches)
     res = {"config": f"C1 9x7: {w}x{h}, {len(dets)} boxes (5 FAR + 3 CLOSE) at integer disparities, dx_max 64, "
                      f"9x7 census / uint64 descriptors, {F1} device-rendered distinct frames (noise 2.0) per call",
            "ms_per_step": ms, "boxes_per_sec": boxes / (ms / 1e3), "frames_per_sec": F1 / (ms / 1e3),
@@ -889,13 +889,14 @@ def main():
 
     # ---- roofline of the dominant kernel (stage times from CUDA events on our stream)
     hbm_peak, sm_max, peak_kind = peaks()
-    census_ms = stage_ms[0] / max(stage_launches[0], 1)
-    match_ms = stage_ms[2] / max(stage_launches[2], 1)
+    # per step: each profiled step is one rg_range_frames call (one pipeline)
+    census_ms = stage_ms[0] / roof_steps
+    match_ms = stage_ms[2] / roof_steps
     census_gbs = CENSUS_BYTES_PER_FRAME * F / (census_ms / 1000.0) / 1e9
     req = census_required_bytes(dets, W, H)
     req_frame = req["bytes"]
     census_req_gbs = req_frame * F / (census_ms / 1000.0) / 1e9
-    evals_per_launch = r_evals / max(stage_launches[2], 1)
+    evals_per_launch = r_evals / roof_steps
     clk_mhz = clk["sm_mhz"] or sm_max
     popc_clk, popc_src = popc_peak_per_clk()
     popc_peak = popc_clk * N_SM * clk_mhz * 1e6
