@@ -695,6 +695,22 @@ def main():
     ctx.set_profiling(False)
     stage_ms, stage_launches, _ = ctx.counters()
     r_evals, _ = ctx.work()
+    # the full-frame census kernel (census_pairs_kernel: batches under 12
+    # frames, the single-image API, SGM) on the same 256-frame steps
+    # (rg_set_census_rois(0)): SURVEY 8(d)'s full-frame bytes over its time
+    ctx.set_census_rois(False)
+    step()
+    assert ctx.sync() == 0
+    torch.cuda.synchronize()
+    ctx.reset_counters()
+    ctx.set_profiling(True)
+    for _ in range(roof_steps):
+        step()
+    torch.cuda.synchronize()
+    ctx.set_profiling(False)
+    ctx.set_census_rois(True)
+    ff = F
+    ff_ms = ctx.counters()[0][0] / roof_steps
 
     # ---- parity sweep: every ring frame of every rank, re-ranged by the
     # reference (oracle/_ref) on the host cores, vs the gathered records
@@ -923,6 +939,14 @@ def main():
                        "note": f"the reference's whole ROI rectangles ({req['ref_full_codes']} full + "
                                f"{req['ref_reduced_codes']} reduced codes per image, both images read) over the "
                                "same time: an effective rate"},
+                   "full_frame_kernel": {
+                       "kernel": "census_pairs_kernel (batches under 12 frames, single-image API, SGM; "
+                                 "here the same 256-frame steps with rg_set_census_rois(0))",
+                       "frames": ff, "ms_per_launch": ff_ms,
+                       "achieved_gbs": CENSUS_BYTES_PER_FRAME * ff / (ff_ms / 1000.0) / 1e9,
+                       "frac": CENSUS_BYTES_PER_FRAME * ff / (ff_ms / 1000.0) / 1e9 / hbm_peak,
+                       "bytes": "SURVEY 8(d): 24,883,200 B per C2 frame (both images read, full + reduced "
+                                "rasters written)"},
                    "full_frame_equivalent": {
                        "bytes_per_launch": CENSUS_BYTES_PER_FRAME * F, "effective_gbs": census_gbs,
                        "note": "SURVEY 8(d) full-frame census bytes (24,883,200 per C2 frame) over the same time: "

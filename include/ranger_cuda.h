@@ -69,6 +69,10 @@ rg_status rg_set_profiling(rg_ctx* ctx, int on);
  * are identical; on B200 the overlap measured 5-10 % SLOWER (the streaming
  * census evicts the matcher's L2-resident rows), so it is opt-in. */
 rg_status rg_set_overlap(rg_ctx* ctx, int on);
+/* on (default): batches of >= 12 frames compute only the census codes the
+ * matcher reads (ROI tiles); off: the full-frame census for every batch
+ * (same records; a measurement / comparison switch). */
+rg_status rg_set_census_rois(rg_ctx* ctx, int on);
 /* Accumulated stage milliseconds and launch counts since the last reset:
  * times[0..4] = census, plan, match, aggregate, autorect;
  * launches[0..4] likewise; returns the total kernel launch count in *total. */

@@ -179,6 +179,7 @@ SIGNATURES = {
     "rg_get_transfer": (I, [P, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "rg_set_profiling": (I, [P, I]),
     "rg_set_overlap": (I, [P, I]),
+    "rg_set_census_rois": (I, [P, I]),
     "rg_sync": (I, [P]),
     "rg_set_sync_mode": (I, [P, I]),
     "rg_get_counters": (I, [P, P, P, P]),

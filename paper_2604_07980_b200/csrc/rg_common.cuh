@@ -135,6 +135,7 @@ struct rg_ctx {
   cudaStream_t census_stream = nullptr;  // K1 of chunk k+1 while K2 of chunk k runs (rg_range_frames)
   cudaStream_t match_stream = nullptr;   // K3/K2/K4 chunks (highest priority), joined back to the caller
   bool overlap = false;                  // chunked census/matcher overlap in rg_range_frames (opt-in)
+  bool census_rois = true;               // ROI-tile census for batches of >= 12 frames (rg_set_census_rois)
   cudaEvent_t ev_sync[6] = {};           // cross-stream ordering events (no timing)
   cudaEvent_t ev_prof[40] = {};          // per-chunk stage timing when profiling
   int map_key[4] = {-1, -1, -1, -1};  // geometry of the cached inverse maps

@@ -96,6 +96,11 @@ class Context:
         """rg_range_frames schedule: chunked census/matcher overlap (opt-in) or one stream (default)."""
         self.check(lib().rg_set_overlap(self._h, 1 if on else 0))
 
+    def set_census_rois(self, on: bool) -> None:
+        """rg_set_census_rois: ROI-tile census for big batches (default) or
+        the full-frame census always."""
+        self.check(lib().rg_set_census_rois(self._h, 1 if on else 0))
+
     def transfer(self) -> Tuple[int, int]:
         """rg_get_transfer: (host->device, device->host) bytes moved by
         rg_range_frames_host since the last reset_counters()."""

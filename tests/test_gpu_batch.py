@@ -109,6 +109,28 @@ def test_range_host_zero_copy_gather(ctx, chk, name, n, wide, shift):
         assert int(h_cnt[f]) * 32 == len(want) and ho[f, :len(want)].tobytes() == want, (name, f)
 
 
+def test_census_rois_switch_same_records(ctx):
+    """rg_set_census_rois(0) (full-frame census for every batch) and the
+    default ROI tiles give byte-identical records on a 12-frame C2 batch."""
+    import torch
+
+    L, R, D, cfg, sc = _frames(S.scene_c2, 12)
+    eng = FrameEngine(sc.width, sc.height, cfg, max(len(d) for d in D), S.F_PX, S.BASELINE_M, ctx=ctx)
+    recs, offs = pack_detections(D)
+    dev = torch.device("cuda", 0)
+    args = (torch.from_numpy(L).to(dev), torch.from_numpy(R).to(dev), torch.from_numpy(recs.view(np.uint8)).to(dev),
+            torch.from_numpy(offs).to(dev))
+    outs = []
+    for on in (True, False, True):
+        ctx.set_census_rois(on)
+        out = torch.zeros(12 * eng.out_stride * 32, dtype=torch.uint8, device=dev)
+        cnt = torch.zeros(12, dtype=torch.int32, device=dev)
+        eng.range_device(*args, out, cnt)
+        outs.append((out.cpu().numpy().tobytes(), cnt.cpu().numpy().tobytes()))
+    ctx.set_census_rois(True)
+    assert outs[0] == outs[1] == outs[2]
+
+
 def shift_vertical(img, dy):
     """image.hpp:145-154: out(x, y) = in(x, clamp(y - dy, 0, H - 1))."""
     h = img.shape[0]
