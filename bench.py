@@ -52,9 +52,9 @@ def census_required_bytes(dets, w, h, tau_s=48.0, scale=2, dx_far=256, dx_close=
     rows) and reduced codes inside the CLOSE ROI rectangles (reduced
     coordinates, dilated by ceil(dx_max_close / s) + 2 and 3) of both images.
     K1 computes the part of each rectangle the matcher can read
-    (census_rows_kernel, census.cu): on the left image the box rows +-1 across
-    the rectangle, on the right image the box rows +-2 from the rectangle's
-    left edge to the box's right edge + 2.  Algorithmic bytes = code_bytes
+    (read_rect, census.cu): on the left image the box rows across
+    [x0 - dx_max, x1 + dx_max], on the right image the box rows +-1 across
+    [x0 - dx_max, x1].  Algorithmic bytes = code_bytes
     per such code (4; 8 for the 9x7 extension) + every image byte under those
     codes' (2 rx + 1) x (2 ry + 1) windows (source pixels for the reduced
     raster), read once.  -> dict."""
@@ -77,8 +77,9 @@ def census_required_bytes(dets, w, h, tau_s=48.0, scale=2, dx_far=256, dx_close=
         a, e = max(0, by0 - 3), min(H, by1 + 4)
         c0, c1 = max(0, bx0 - dxm), min(W, bx1 + dxm + 1)
         ref[a:e, c0:c1] = True
-        need[0][k][max(a, by0 - 1):min(e, by1 + 2), c0:c1] = True
-        need[1][k][max(a, by0 - 2):min(e, by1 + 3), c0:min(c1, bx1 + 3)] = True
+        dxr = dxm - 2  # census.cu read_rect (tight 2)
+        need[0][k][max(a, by0):min(e, by1 + 1), max(c0, bx0 - dxr):min(c1, bx1 + dxr + 1)] = True
+        need[1][k][max(a, by0 - 1):min(e, by1 + 2), max(c0, bx0 - dxr):min(c1, bx1 + 1)] = True
     codes, reads = 0, 0
     for img in range(2):
         nf, nr = need[img]

@@ -337,6 +337,29 @@ __global__ void RG_C2_BOUNDS census_pairs_kernel(
 // (FAR ROI), bit y' of words [wf, wf + wr) = reduced row y' (CLOSE ROI).
 // Every detection of the frame contributes (a superset of the selected ones:
 // the planner runs after the census).
+// The rectangle [ra, re) x [ca, ce) (raster coordinates) of a detection box
+// (integer bounds bx0..bx1, by0..by1, search range dxr) whose codes the
+// matcher can read in image img (0 left, 1 right).  The block points lie on
+// the box rows / columns (lround of coordinates inside the box); the forward
+// pass reads the left image at the points and the right one at
+// (x - dx, y + dy), dx in [0, dxr], |dy| <= 1; the backward pass reads the
+// right image at the points shifted by (-dx*, dy*) and the left one at
+// (x - dx* + dx', y), dx' in [0, dxr].  So: left = the box rows across
+// [bx0 - dxr, bx1 + dxr], right = the box rows +-1 across [bx0 - dxr, bx1].
+// tight 2 (default): exactly that; 1: +-1 row / +-2 column margins; 0: the
+// reference's whole ROI rectangle (detail::add_roi, template_match.hpp:245-253).
+__device__ __forceinline__ void read_rect(int bx0, int bx1, int by0, int by1, int dxr, int W, int H, int img,
+                                          int tight, int& ra, int& re, int& ca, int& ce) {
+  const int dxm = dxr + 2;
+  ra = max(0, by0 - 3), re = min(H, by1 + 4), ca = max(0, bx0 - dxm), ce = min(W, bx1 + dxm + 1);
+  if (tight) {
+    const int mg = tight == 1;
+    ra = max(ra, by0 - img - mg), re = min(re, by1 + 1 + img + mg);
+    ca = max(ca, bx0 - dxr - 2 * mg);
+    ce = min(ce, img ? bx1 + 1 + 2 * mg : bx1 + dxr + 1 + 2 * mg);
+  }
+}
+
 constexpr int RM_T = 128;
 constexpr int RW_TX = 120;  // source columns per warp tile (lanes 0..29 emit codes)
 __global__ void __launch_bounds__(RM_T) census_rows_kernel(const rg_detection* __restrict__ dets,
@@ -374,30 +397,17 @@ __global__ void __launch_bounds__(RM_T) census_rows_kernel(const rg_detection* _
       dxm = dxs + 2, W = cw, H = ch;
       m = sm_rows + wf, bm = tbm + bf, rows_per_tile = tr, cols_per_tile = RW_TX / 2, ntr = rtr;
     }
-    // the reference's ROI rectangle: rows [a, e), columns [c0, c1)
+    // the reference's ROI rows [a, e) (row masks of the A/B pair kernel)
     const int a = max(0, by0 - 3), e = min(H, by1 + 3 + 1);
-    const int c0 = max(0, bx0 - dxm), c1 = min(W, bx1 + dxm + 1);
     for (int y = a; y < e;) {
       const int wd = y >> 5, b0 = y & 31, nb = min(32 - b0, e - y);
       atomicOr(&m[wd], (nb == 32 ? 0xFFFFFFFFu : ((1u << nb) - 1u)) << b0);
       y += nb;
     }
-    // tight != 0: only the codes of the rectangle the matcher can read.  Its
-    // block points lie in the box rows / columns [b*0, b*1] (lround of
-    // coordinates inside the box); the forward pass reads the left image at
-    // the points and the right one at (x - dx, y + dy), dx in [0, dx_max],
-    // |dy| <= 1; the backward pass reads the right image at the points
-    // shifted by (-dx*, dy*) and the left one at (x - dx* + dx', y), dx' in
-    // [0, dx_max].  So the left image needs the box rows (+-1 margin) across
-    // the whole ROI width, the right one the box rows +-1 (+-1 margin) from
-    // the ROI's left edge to the box's right edge (+2 margin).  The other
-    // codes of the rectangle are never read.
+    // only the codes the matcher can read (read_rect)
     for (int img = 0; img < 2; ++img) {
-      int ra = a, re = e, ca = c0, ce = c1;
-      if (tight) {
-        ra = max(0, by0 - 1 - img), re = min(H, by1 + 2 + img);
-        if (img) ce = min(W, bx1 + 3);
-      }
+      int ra, re, ca, ce;
+      read_rect(bx0, bx1, by0, by1, dxm - 2, W, H, img, tight, ra, re, ca, ce);
       uint32_t* sbm = bm + img * (bf + br);
       if (ra < re && ca < ce)  // the warp tiles (fixed grid) the rectangle touches
         for (int rt = ra / rows_per_tile; rt <= (re - 1) / rows_per_tile && rt < ntr; ++rt)
@@ -1000,19 +1010,17 @@ __global__ void __launch_bounds__(GR_WARPS * 32) gather_rows_kernel(
       bx0 = clampi(floor(__dmul_rn(b.x0, sx))), bx1 = clampi(ceil(__dmul_rn(b.x1, sx)));
       dxm = dxs + 2, W = cw, H = ch, s = 2;
     }
-    const int a = max(0, by0 - 3), e = min(H, by1 + 4), c0 = max(0, bx0 - dxm), c1 = min(W, bx1 + dxm + 1);
-    int ra = a, re = e, ce = c1;
-    if (tight) {
-      ra = max(0, by0 - 1 - side), re = min(H, by1 + 2 + side);
-      if (side) ce = min(W, bx1 + 3);
-    }
+    int ra, re, c0, ce;
+    read_rect(bx0, bx1, by0, by1, dxm - 2, W, H, side, tight, ra, re, c0, ce);
     if (ra >= re || c0 >= ce) continue;
     // raster rows [ra, re) -> image rows read by their windows (left image:
-    // shifted by sh and clamped like the census row loads)
-    int ya = s * ra - RY - 1, ye = s * (re - 1) + RY + 1;
+    // shifted by sh and clamped like the census row loads); the margin-less
+    // read sets (tight 2) take no extra pixel either
+    const int gm = tight == 2 ? 0 : 1;
+    int ya = s * ra - RY - gm, ye = s * (re - 1) + RY + gm;
     ya = min(max(ya - sh, 0), h - 1), ye = min(max(ye - sh, 0), h - 1);
     if (r < ya || r > ye) continue;
-    const int xa = max(0, s * c0 - RX - 1), xe = min(w - 1, s * (ce - 1) + RX + 1);
+    const int xa = max(0, s * c0 - RX - gm), xe = min(w - 1, s * (ce - 1) + RX + gm);
     for (int sg = xa >> 4; sg <= (xe >> 4); ++sg) atomicOr(&mask[wid][sg >> 5], 1u << (sg & 31));
   }
   __syncwarp();
@@ -1123,7 +1131,7 @@ cudaError_t roi_lists(int n_frames, int w, int h, const PadGeom& gs, const rg_de
   // on both images; default: only the part of each the matcher reads
   static const int tight = [] {
     const char* v = getenv("RG_CENSUS_TIGHT");
-    return v ? atoi(v) : 1;
+    return v ? atoi(v) : 2;
   }();
   census_rows_kernel<<<n_frames, RM_T, sizeof(uint32_t) * (wf + wr + bmw), s>>>(
       dets, det_off, w, h, tau_s, gs.w, gs.h, wf, wr, masks, dx_far, dx_close_scaled, nxt, tf, tr, rtf, rtr,
@@ -1274,7 +1282,7 @@ cudaError_t launch_gather_rows(const uint8_t* hl, const uint8_t* hr, int64_t src
     return cudaErrorNotSupported;
   static const int tight = [] {
     const char* v = getenv("RG_CENSUS_TIGHT");
-    return v ? atoi(v) : 1;
+    return v ? atoi(v) : 2;
   }();
   static const int ctas = [] { const char* v = getenv("RG_GATHER_CTAS"); return v ? atoi(v) : 4 * 148; }();
   const int items = h * 2 * n_frames;
