@@ -224,7 +224,7 @@ def test_integration_example_program():
     assert any("delta* 2" in l for l in lines) and "shift 0" in lines[0]
 
 
-def _batch_vs_oracle(ctx, chk, L, R, D, cfg, focal=0.0, base=0.0):
+def _batch_vs_oracle(ctx, chk, L, R, D, cfg, focal=0.0, base=0.0, host=False):
     import torch
 
     n, h, w = L.shape
@@ -238,6 +238,16 @@ def _batch_vs_oracle(ctx, chk, L, R, D, cfg, focal=0.0, base=0.0):
                      torch.from_numpy(recs.view(np.uint8)).to(dev), torch.from_numpy(offs).to(dev), out, cnt)
     torch.cuda.synchronize()
     o = out.cpu().numpy().reshape(n, eng.out_stride * 32)
+    if host:  # the same batch from pinned host frames (zero-copy read-set gather when it applies)
+        tl = torch.from_numpy(np.ascontiguousarray(L)).pin_memory()
+        tr = torch.from_numpy(np.ascontiguousarray(R)).pin_memory()
+        h_out = np.zeros(n * eng.out_stride, OUT_DTYPE)
+        h_cnt = np.zeros(n, np.int32)
+        eng.range_host(tl.numpy(), tr.numpy(), recs, offs, h_out, h_cnt, chunk=n)
+        assert h_cnt.tobytes() == cnt.cpu().numpy().tobytes()
+        ho = h_out.view(np.uint8).reshape(n, -1)
+        for f in range(n):  # records past a frame's count are unspecified
+            assert ho[f, :32 * int(h_cnt[f])].tobytes() == o[f, :32 * int(h_cnt[f])].tobytes(), f
     for f in range(n):
         got_n = int(cnt[f])
         if D[f]:
@@ -251,14 +261,17 @@ def _batch_vs_oracle(ctx, chk, L, R, D, cfg, focal=0.0, base=0.0):
         assert o[f, :len(want)].tobytes() == want, f
 
 
+@pytest.mark.parametrize("batch", ["small", "roi"])
 @pytest.mark.parametrize("case", ["odd_width", "empty_frames", "degenerate_boxes", "selection_overflow",
                                   "zero_range", "wide_range", "close_only_scale3"])
-def test_range_frames_edge_cases(ctx, chk, case):
+def test_range_frames_edge_cases(ctx, chk, case, batch):
     """Batched path vs the oracle on the shapes the planner/census/matcher
     special-case: non-multiple-of-4 widths (general census kernel), frames
     without detections, boxes leaving or degenerate in the image, more boxes
     than max_objects, one-candidate and >256-candidate search ranges, a
-    non-half close scale (gather-mapped reduced raster)."""
+    non-half close scale (gather-mapped reduced raster).  batch "roi": the
+    frames repeated to a 12+ frame batch (ROI-tile census, exact read sets)
+    and also fed from pinned host frames (read-set gather)."""
     rng = np.random.default_rng(hash(case) % 1000)
     sc, cfg = S.scene_c1(seed=81, noise=2.0)
     L, R = S.render_stereo_pair(sc)
@@ -288,9 +301,11 @@ def test_range_frames_edge_cases(ctx, chk, case):
         cfg.close_scale = 3
         cfg.tau_s = 1e9  # everything CLOSE
         frames = [(L, R, dets)]
+    if batch == "roi":
+        frames = (frames * 12)[:max(12, len(frames))]
     Ls = np.stack([f[0] for f in frames])
     Rs = np.stack([f[1] for f in frames])
-    _batch_vs_oracle(ctx, chk, Ls, Rs, [f[2] for f in frames], cfg, S.F_PX, S.BASELINE_M)
+    _batch_vs_oracle(ctx, chk, Ls, Rs, [f[2] for f in frames], cfg, S.F_PX, S.BASELINE_M, host=batch == "roi")
 
 
 @pytest.mark.parametrize("overlap", [True, False])
@@ -391,6 +406,12 @@ def test_random_configs_both_matchers_match_oracle(ctx, chk, k):
         want = _want(chk, L[f], R[f], D[f], cfg)
         assert big[f] == want, (f, cfg)
         assert small[f] == want, (f, cfg)
+    # a 15-frame batch (the 5 frames three times): the ROI-tile census with
+    # the read sets of this config
+    L, R, D = np.concatenate([L] * 3), np.concatenate([R] * 3), D * 3
+    roi = run(0, 15)
+    for f in range(15):
+        assert roi[f] == big[f % 5], (f, cfg)
 
 
 def test_multi_example_program():
