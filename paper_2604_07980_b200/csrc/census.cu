@@ -1021,7 +1021,11 @@ __global__ void __launch_bounds__(GR_WARPS * 32) gather_rows_kernel(
     ya = min(max(ya - sh, 0), h - 1), ye = min(max(ye - sh, 0), h - 1);
     if (r < ya || r > ye) continue;
     const int xa = max(0, s * c0 - RX - gm), xe = min(w - 1, s * (ce - 1) + RX + gm);
-    for (int sg = xa >> 4; sg <= (xe >> 4); ++sg) atomicOr(&mask[wid][sg >> 5], 1u << (sg & 31));
+    const int sa = xa >> 4, sb = xe >> 4;  // segments [sa, sb]: one atomic per mask word
+    for (int wd = sa >> 5; wd <= (sb >> 5); ++wd) {
+      const int lo = max(sa - 32 * wd, 0), hi = min(sb - 32 * wd, 31);
+      atomicOr(&mask[wid][wd], (hi == 31 ? 0xFFFFFFFFu : ((2u << hi) - 1u)) & ~((1u << lo) - 1u));
+    }
   }
   __syncwarp();
   const uint8_t* src = (side ? hr : hl) + (int64_t)f * src_stride + (int64_t)r * src_pitch;
