@@ -686,16 +686,20 @@ def main():
     value = boxes_step * args.steps / (ms_max / 1000.0)
     fps = F * args.steps * world / (ms_max / 1000.0)
 
-    # ---- kernel rooflines: the same steps with per-stage CUDA events
-    ctx.reset_counters()
-    ctx.set_profiling(True)
+    # ---- kernel rooflines: the same steps with per-stage CUDA events, each
+    # step read out alone; stage times are the per-stage medians over the
+    # steps (robust to a one-off disturbance of a single step)
     roof_steps = max(3, min(args.steps, 10))
+    per_step, r_evals = [], 0
+    ctx.set_profiling(True)
     for _ in range(roof_steps):
+        ctx.reset_counters()
         step()
-    torch.cuda.synchronize()
+        torch.cuda.synchronize()
+        per_step.append(ctx.counters()[0])
+        r_evals += ctx.work()[0]
     ctx.set_profiling(False)
-    stage_ms, stage_launches, _ = ctx.counters()
-    r_evals, _ = ctx.work()
+    stage_ms = [statistics.median(p[i] for p in per_step) * roof_steps for i in range(len(per_step[0]))]
     # the full-frame census kernel (census_pairs_kernel: batches under 12
     # frames, the single-image API, SGM) on the same 256-frame steps
     # (rg_set_census_rois(0)): SURVEY 8(d)'s full-frame bytes over its time
@@ -993,7 +997,7 @@ def main():
             "timed_batches_overflowed": bool(overflow_in_timed),
             "roofline": dominant,
             "kernels": {"census": census_roof, "matcher": match_roof,
-                        "timing": f"per-stage CUDA events over {roof_steps} extra steps (one stream)",
+                        "timing": f"per-stage CUDA events, median over {roof_steps} extra steps (one stream)",
                         "stage_ms_per_step": {k: v / roof_steps for k, v in
                                               zip(["census", "plan", "match", "aggregate"], stage_ms[:4])}},
             "hamming_evals_per_frame": evals / max(F * args.steps, 1),
