@@ -323,20 +323,23 @@ __global__ void RG_C2_BOUNDS census_pairs_kernel(
 }
 
 // ---------------------------------------------------------------------------
-// ROI-row census (the reference's census_transform_rois, census.hpp:100-138,
-// as estimate_object_disparities calls it, template_match.hpp:300-321): the
-// full-resolution raster only on rows of FAR census ROIs (box dilated by 3
-// rows, detail::add_roi :245-253) and the reduced raster only on rows of
-// CLOSE ROIs, computed by a stride-2 kernel instead of being gathered from a
-// full-frame transform.  Codes on those rows are bit-identical to the full
-// transform; the matcher never reads another row (its
-// samples lie within the box rows +-1).  At C2 this is 27 % of the full rows
-// and 87 % of the reduced rows: about half the bytes and compares of K1.
-
-// Row masks per frame: bit y of words [0, wf) = full raster row y needed
-// (FAR ROI), bit y' of words [wf, wf + wr) = reduced row y' (CLOSE ROI).
-// Every detection of the frame contributes (a superset of the selected ones:
-// the planner runs after the census).
+// ROI census (the reference's census_transform_rois, census.hpp:100-138, as
+// estimate_object_disparities calls it, template_match.hpp:300-321): the
+// full-resolution raster only inside FAR census ROIs (box dilated by
+// (dx_max_far + 2, 3), detail::add_roi :245-253) and the reduced raster only
+// inside CLOSE ROIs, the latter by a stride-2 kernel instead of being
+// gathered from a full-frame transform -- and of each rectangle only the
+// codes the matcher can read (read_rect).  Codes computed are bit-identical
+// to the full transform; nothing reads the others.  At C2
+// this is 931 k of the 1.28 M ROI codes (both images) of 2.59 M full-frame
+// ones per frame.
+//
+// census_rows_kernel, per frame: the reference's ROI row masks (bit y of
+// words [0, wf) = full raster row y, [wf, wf + wr) = reduced rows; only the
+// A/B pair kernel uses them) and, per image, the compacted lists of the
+// (4-row, 120-column) warp tiles the read sets touch.  Every detection of the
+// frame contributes (a superset of the selected ones: the planner runs after
+// the census).
 // The rectangle [ra, re) x [ca, ce) (raster coordinates) of a detection box
 // (integer bounds bx0..bx1, by0..by1, search range dxr) whose codes the
 // matcher can read in image img (0 left, 1 right).  The block points lie on
@@ -457,7 +460,7 @@ __global__ void __launch_bounds__(RM_T) census_rows_kernel(const rg_detection* _
   }
 }
 
-// Warp-tile "vertical pair" census for ROI rows: every warp owns a tile of
+// Warp-tile "vertical pair" census for the ROI tiles: every warp owns a tile of
 // 120 source columns x 4 output rows (2 row pairs; 120 columns + the 2-px
 // halo = 32 image words, one per lane) with its own V rows in
 // shared memory (no CTA barrier), so work follows the ROI rectangles at
@@ -1108,8 +1111,8 @@ size_t census_rois_scratch_words(int n_frames, int w, int h, int ch) {
   return (size_t)n_frames * ((h + 31) / 32 + (ch + 31) / 32 + 4 + 2 * ((h + tf - 1) / tf + (ch + tr - 1) / tr) * nxt);
 }
 
-// ROI-row census of a batch (see census_rows_kernel): the row masks, the
-// full raster on FAR ROI rows and the reduced raster on CLOSE ROI rows.
+// ROI census of a batch (see census_rows_kernel): the tile lists, the full
+// raster on the FAR tiles and the reduced raster on the CLOSE tiles.
 // cudaErrorNotSupported when the fast layout does not apply (the caller then
 // runs the full-frame launch_census_frames).
 namespace {
