@@ -423,7 +423,7 @@ __global__ void __launch_bounds__(RM_T) census_rows_kernel(const rg_detection* _
   __syncthreads();
   for (int i = threadIdx.x; i < wf + wr; i += RM_T) mask[(int64_t)f * (wf + wr) + i] = sm_rows[i];
   // compacted lists of the needed (row tile, column tile) pairs: entry =
-  // row_tile << 16 | column_tile; tiles[f] = {n_full_left, n_red_left,
+  // (first row / 2) << 16 | column_tile; tiles[f] = {n_full_left, n_red_left,
   // n_full_right, n_red_right, then per image: full list (rtf * nxt),
   // reduced list (rtr * nxt)}
   int32_t* rec = tiles + (int64_t)f * tile_stride;
@@ -451,12 +451,113 @@ __global__ void __launch_bounds__(RM_T) census_rows_kernel(const rg_detection* _
       int pos = base + s_pos[threadIdx.x];
       for (uint32_t r = bits; r; r &= r - 1) {
         const int bit = wd * 32 + __ffs(r) - 1;
-        list[pos++] = ((bit / nxt) << 16) | (bit % nxt);
+        list[pos++] = (((bit / nxt) * (side ? tr : tf) / 2) << 16) | (bit % nxt);
       }
       base += s_pos[RM_T];
       __syncthreads();
     }
     if (threadIdx.x == 0) rec[q] = base;
+  }
+}
+
+// census_rows_kernel with the warp tiles placed per column instead of on a
+// fixed row grid (RG_CENSUS_GREEDY, default): for every (image, raster,
+// 120-column tile) the rows the read sets need, then a greedy cover by
+// tiles of 2 rw_pr rows starting at the next needed row (rounded down to
+// even) -- a 13-row box costs 4 tiles wherever it sits instead of 4 or 5.
+// Same list layout and entry format ((first row / 2) << 16 | column tile).
+__global__ void __launch_bounds__(RM_T) census_cols_kernel(const rg_detection* __restrict__ dets,
+                                                          const int32_t* __restrict__ det_off, int w, int h,
+                                                          double tau_s, int cw, int ch, int wf, int wr,
+                                                          uint32_t* __restrict__ mask, int dxf, int dxs, int nxt,
+                                                          int tf, int tr, int rtf, int rtr, int tile_stride,
+                                                          int32_t* __restrict__ tiles, int tight) {
+  // reference row masks (wf + wr), then per (image, column tile) the needed
+  // rows of the full raster (wf words each) and of the reduced one (wr)
+  extern __shared__ uint32_t sm_cols[];
+  uint32_t* cf = sm_cols + wf + wr;
+  uint32_t* cr = cf + 2 * nxt * wf;
+  __shared__ int s_cnt[4 * 64 + 1];
+  const int f = blockIdx.x;
+  const int total_words = wf + wr + 2 * nxt * (wf + wr);
+  for (int i = threadIdx.x; i < total_words; i += RM_T) sm_cols[i] = 0u;
+  __syncthreads();
+  const int d0 = det_off[f], n = det_off[f + 1] - d0;
+  const double sy = __ddiv_rn((double)ch, (double)h);  // template_match.hpp:305 double(ch) / h
+  const double sx = __ddiv_rn((double)cw, (double)w);  // template_match.hpp:305 double(cw) / w
+  auto clampi = [](double v) { return (int)fmin(fmax(v, -1.0e9), 1.0e9); };
+  auto set_rows = [](uint32_t* col, int a, int e) {
+    for (int y = a; y < e;) {
+      const int wd = y >> 5, b0 = y & 31, nb = min(32 - b0, e - y);
+      atomicOr(&col[wd], (nb == 32 ? 0xFFFFFFFFu : ((1u << nb) - 1u)) << b0);
+      y += nb;
+    }
+  };
+  for (int i = threadIdx.x; i < n; i += RM_T) {
+    const rg_detection d = dets[d0 + i];
+    const PBox b = pixel_box(d, w, h);
+    const bool far = dev_classify(d, w, h, tau_s) == RG_KIND_FAR;
+    int bx0, bx1, by0, by1, dxm, W, H, cols_per_tile, nw;
+    uint32_t *m, *cb;
+    if (far) {  // add_roi(far_rois, box, 1, 1, dx_max_far + 2, 3, w, h)
+      by0 = clampi(floor(b.y0)), by1 = clampi(ceil(b.y1));
+      bx0 = clampi(floor(b.x0)), bx1 = clampi(ceil(b.x1));
+      dxm = dxf + 2, W = w, H = h, m = sm_cols, cb = cf, cols_per_tile = RW_TX, nw = wf;
+    } else {  // add_roi(scaled_rois, box, cw / w, ch / h, dx_scaled + 2, 3, cw, ch)
+      by0 = clampi(floor(__dmul_rn(b.y0, sy))), by1 = clampi(ceil(__dmul_rn(b.y1, sy)));
+      bx0 = clampi(floor(__dmul_rn(b.x0, sx))), bx1 = clampi(ceil(__dmul_rn(b.x1, sx)));
+      dxm = dxs + 2, W = cw, H = ch, m = sm_cols + wf, cb = cr, cols_per_tile = RW_TX / 2, nw = wr;
+    }
+    set_rows(m, max(0, by0 - 3), min(H, by1 + 3 + 1));  // the reference's ROI rows
+    for (int img = 0; img < 2; ++img) {
+      int ra, re, ca, ce;
+      read_rect(bx0, bx1, by0, by1, dxm - 2, W, H, img, tight, ra, re, ca, ce);
+      if (ra >= re || ca >= ce) continue;
+      for (int xt = ca / cols_per_tile; xt <= (ce - 1) / cols_per_tile && xt < nxt; ++xt)
+        set_rows(cb + (img * nxt + xt) * nw, ra, re);
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < wf + wr; i += RM_T) mask[(int64_t)f * (wf + wr) + i] = sm_cols[i];
+  // greedy cover of every column (q = (img * 2 + raster) * nxt + xt): count, scan, write
+  int32_t* rec = tiles + (int64_t)f * tile_stride;
+  const int ncol = 4 * nxt;
+  auto cover = [&](int q, int32_t* out) -> int {
+    const int img = q / (2 * nxt), raster = (q / nxt) & 1, xt = q % nxt;
+    const int nw = raster ? wr : wf, T = raster ? tr : tf;
+    const uint32_t* col = (raster ? cr : cf) + (img * nxt + xt) * nw;
+    int y = 0, cnt = 0;
+    for (;;) {
+      int wd = y >> 5;
+      if (wd >= nw) break;
+      uint32_t bits = col[wd] & (0xFFFFFFFFu << (y & 31));
+      while (!bits && ++wd < nw) bits = col[wd];
+      if (!bits) break;
+      const int y0 = (wd * 32 + __ffs(bits) - 1) & ~1;
+      if (out) out[cnt] = ((y0 >> 1) << 16) | xt;
+      ++cnt;
+      y = y0 + T;
+    }
+    return cnt;
+  };
+  for (int q = threadIdx.x; q < ncol; q += RM_T) s_cnt[q] = cover(q, nullptr);
+  __syncthreads();
+  if (threadIdx.x == 0) {  // exclusive scan within each (image, raster) list
+    for (int l = 0; l < 4; ++l) {
+      int acc = 0;
+      for (int xt = 0; xt < nxt; ++xt) {
+        const int c = s_cnt[l * nxt + xt];
+        s_cnt[l * nxt + xt] = acc;
+        acc += c;
+      }
+      rec[(l >> 1) * 2 + (l & 1)] = acc;  // l = img * 2 + raster -> rec[img * 2 + raster]
+    }
+  }
+  __syncthreads();
+  for (int q = threadIdx.x; q < ncol; q += RM_T) {
+    const int img = q / (2 * nxt), raster = (q / nxt) & 1;
+    int32_t* list = rec + 4 + img * (rtf + rtr) * nxt + (raster ? rtf * nxt : 0);
+    cover(q, list + s_cnt[q]);
   }
 }
 
@@ -516,7 +617,7 @@ __global__ void __launch_bounds__(rw_wpb<STRIDE>() * 32) census_rowtile_kernel(
   uint32_t* V = Vall + wid * NV * RW_VW;
   for (int ti = blockIdx.x * rw_wpb<STRIDE>() + wid; ti < n_tiles; ti += gridDim.x * rw_wpb<STRIDE>()) {
   const int ent = list[ti];
-  const int Y0 = (ent >> 16) * 2 * RW_PR;  // first output row of this tile (even)
+  const int Y0 = (ent >> 16) * 2;  // first output row of this tile (even)
   const int x0 = (ent & 0xFFFF) * RW_TX;   // source column origin
   __syncwarp();  // the previous tile's window reads are done before V is rebuilt
   const int sh = (side == 0 && lshift) ? lshift[frame] : 0;  // shift_vertical of the left image
@@ -858,7 +959,7 @@ __global__ void __launch_bounds__(32) census64_rowtile_kernel(
   const int pw = pitch / 4;
   for (int ti = blockIdx.x; ti < n_tiles; ti += gridDim.x) {
     const int ent = list[ti];
-    const int Y0 = (ent >> 16) * 2 * PR;  // first output row of this tile (even)
+    const int Y0 = (ent >> 16) * 2;  // first output row of this tile (even)
     const int x0 = (ent & 0xFFFF) * RW_TX;
     __syncwarp();  // the previous tile's window reads are done before V is rebuilt
     const int S0 = STRIDE * Y0 - 3;  // source row of V row 0
@@ -1140,10 +1241,21 @@ cudaError_t roi_lists(int n_frames, int w, int h, const PadGeom& gs, const rg_de
     const char* v = getenv("RG_CENSUS_TIGHT");
     return v ? atoi(v) : 2;
   }();
+  static const bool greedy = [] { const char* v = getenv("RG_CENSUS_GREEDY"); return v ? atoi(v) != 0 : true; }();
+  *out = {tiles, tile_stride, side_off, 4 + rtf * nxt};
+  if (greedy && nxt <= 64) {
+    const size_t smem = sizeof(uint32_t) * (size_t)(wf + wr + 2 * nxt * (wf + wr));
+    static SmemAttr attr;
+    const cudaError_t e = attr.ensure((const void*)census_cols_kernel, smem);
+    if (e != cudaSuccess) return e;
+    census_cols_kernel<<<n_frames, RM_T, smem, s>>>(dets, det_off, w, h, tau_s, gs.w, gs.h, wf, wr, masks, dx_far,
+                                                    dx_close_scaled, nxt, tf, tr, rtf, rtr, tile_stride, tiles,
+                                                    tight);
+    return cudaGetLastError();
+  }
   census_rows_kernel<<<n_frames, RM_T, sizeof(uint32_t) * (wf + wr + bmw), s>>>(
       dets, det_off, w, h, tau_s, gs.w, gs.h, wf, wr, masks, dx_far, dx_close_scaled, nxt, tf, tr, rtf, rtr,
       tile_stride, tiles, tight);
-  *out = {tiles, tile_stride, side_off, 4 + rtf * nxt};
   return cudaGetLastError();
 }
 }  // namespace
