@@ -1264,7 +1264,7 @@ cudaError_t launch_census_rois(const uint8_t* left, const uint8_t* right, int n_
                                int pitch, int w, int h, uint32_t* fl, uint32_t* fr, const PadGeom& gf, uint32_t* sl,
                                uint32_t* sr, const PadGeom& gs, const int32_t* lshift, bool internal,
                                const rg_detection* dets, const int32_t* det_off, double tau_s, int dx_far,
-                               int dx_close_scaled, uint32_t* masks, cudaStream_t s) {
+                               int dx_close_scaled, uint32_t* masks, cudaStream_t s, cudaEvent_t full_done) {
   if (n_frames <= 0) return cudaSuccess;
   const int sides = right ? 2 : 1;
   const bool aligned = (pitch % 4 == 0) && (w % 4 == 0) && (frame_stride % 4 == 0) &&
@@ -1314,6 +1314,10 @@ cudaError_t launch_census_rois(const uint8_t* left, const uint8_t* right, int n_
   e = internal ? rowtile(census_rowtile_kernel<true, 1>, rw_smem<1>(), attr[0], fl, fr, gf, walk_f, 4, rw_wpb<1>())
                : rowtile(census_rowtile_kernel<false, 1>, rw_smem<1>(), attr[1], fl, fr, gf, walk_f, 4, rw_wpb<1>());
   if (e != cudaSuccess) return e;
+  if (full_done) {  // the full raster is complete (the FAR matcher may start)
+    e = cudaEventRecord(full_done, s);
+    if (e != cudaSuccess) return e;
+  }
   e = internal ? rowtile(census_rowtile_kernel<true, 2>, rw_smem<2>(), attr[2], sl, sr, gs, walk_r, rl.red_off,
                          rw_wpb<2>())
                : rowtile(census_rowtile_kernel<false, 2>, rw_smem<2>(), attr[3], sl, sr, gs, walk_r, rl.red_off,

@@ -1012,7 +1012,7 @@ __global__ void __launch_bounds__(WPB * 32, MINB) match_slots_warp_kernel(
     const CT* __restrict__ fl, const CT* __restrict__ fr, PadGeom gf,
     const CT* __restrict__ sl, const CT* __restrict__ sr, PadGeom gs, int img_w,
     int img_h, int trusted, rg_ranger_config cfg, SampleConst sk, rg_match_result* __restrict__ res,
-    rg_ranger_stats* __restrict__ stats, int maxp, int capacity) {
+    rg_ranger_stats* __restrict__ stats, int maxp, int capacity, int region) {
   extern __shared__ __align__(16) unsigned char wsm_raw[];
   __shared__ double occ[PRE ? 1 : WPB][4 * kWarpOcc];
   __shared__ int nocc[WPB];
@@ -1109,7 +1109,8 @@ __global__ void __launch_bounds__(WPB * 32, MINB) match_slots_warp_kernel(
       }
     }
   } else if (!((slot0 >= n_lo && slot0 < capacity - n_hi) || slot0 >= capacity)) {  // warp-uniform
-    run_slot(slot0, 0, 1);
+    // region 1: FAR slots only, 2: CLOSE slots only (split launches), 0: all
+    if (region == 0 || (region == 1) == (slot0 < n_lo)) run_slot(slot0, 0, 1);
   }
 }
 
@@ -1120,7 +1121,7 @@ cudaError_t launch_variant(const int2* slot_pts, const Slot* slots, int32_t* cou
                                   const void* fl, const void* fr, const PadGeom& gf, const void* sl,
                                   const void* sr, const PadGeom& gs, int img_w, int img_h, int trusted,
                                   rg_ranger_config cfg, rg_match_result* res, rg_ranger_stats* stats,
-                                  int max_points, cudaStream_t s) {
+                                  int max_points, cudaStream_t s, int region = 0) {
   auto kern = match_slots_warp_kernel<CT, WPB, MINB, PF, COOP, V2, PRE>;
   max_points = (max_points + 1) & ~1;  // keeps every warp's VPoint array 16-B aligned
   const size_t smem = (sizeof(int2) * (size_t)max_points + sizeof(VPoint<CT>) * (size_t)(max_points + 1)) * WPB;
@@ -1144,7 +1145,7 @@ cudaError_t launch_variant(const int2* slot_pts, const Slot* slots, int32_t* cou
                                     static_cast<const CT*>(fr), gf, static_cast<const CT*>(sl),
                                     static_cast<const CT*>(sr), gs, img_w, img_h, trusted, cfg,
                                     make_sample_const(cfg, img_w, img_h), res, stats,
-                                    max_points, slot_capacity);
+                                    max_points, slot_capacity, region);
   return cudaGetLastError();
 }
 
@@ -1191,11 +1192,11 @@ cudaError_t launch_match_slots(const int2* slot_pts, const Slot* slots, int32_t*
                                const void* sr, const PadGeom& gs, int img_w, int img_h, int trusted,
                                int wide, rg_ranger_config cfg, rg_match_result* res,
                                rg_ranger_stats* stats, int max_points, cudaStream_t s,
-                               int n_frames) {
+                               int n_frames, int region) {
   if (slot_capacity <= 0) return cudaSuccess;
   const int variant = match_variant();
 #define RG_ARGS slot_pts, slots, counters, slot_capacity, objs, occ_list, dets, det_off, fl, fr, gf, sl, sr, gs, img_w, img_h, \
-                trusted, cfg, res, stats, max_points, s
+                trusted, cfg, res, stats, max_points, s, region
   // blocks too large for the default warps per CTA fall back to fewer
   // (shared memory holds every warp's points: 16 or 24 B per point)
   auto fallback = [&](cudaError_t e, auto... launchers) {

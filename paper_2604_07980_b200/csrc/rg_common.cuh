@@ -136,7 +136,7 @@ struct rg_ctx {
   cudaStream_t match_stream = nullptr;   // K3/K2/K4 chunks (highest priority), joined back to the caller
   bool overlap = false;                  // chunked census/matcher overlap in rg_range_frames (opt-in)
   bool census_rois = true;               // ROI-tile census for batches of >= 12 frames (rg_set_census_rois)
-  cudaEvent_t ev_sync[6] = {};           // cross-stream ordering events (no timing)
+  cudaEvent_t ev_sync[10] = {};          // cross-stream ordering events (no timing)
   cudaEvent_t ev_prof[40] = {};          // per-chunk stage timing when profiling
   int map_key[4] = {-1, -1, -1, -1};  // geometry of the cached inverse maps
   rg::PadGeom pad_key{}, pad_key_s{};  // layout of the zeroed census rasters
@@ -213,7 +213,8 @@ cudaError_t launch_census_rois(const uint8_t* left, const uint8_t* right, int n_
                                int pitch, int w, int h, uint32_t* fl, uint32_t* fr, const PadGeom& gf, uint32_t* sl,
                                uint32_t* sr, const PadGeom& gs, const int32_t* lshift, bool internal,
                                const rg_detection* dets, const int32_t* det_off, double tau_s, int dx_far,
-                               int dx_close_scaled, uint32_t* masks, cudaStream_t s);
+                               int dx_close_scaled, uint32_t* masks, cudaStream_t s,
+                               cudaEvent_t full_done = nullptr);
 cudaError_t launch_gather_rows(const uint8_t* hl, const uint8_t* hr, int64_t src_stride, int src_pitch, uint8_t* dl,
                                uint8_t* dr, int64_t dst_stride, int dst_pitch, int w, int h, int n_frames,
                                const rg_detection* dets, const int32_t* det_off, double tau_s, int close_scale,
@@ -261,7 +262,7 @@ cudaError_t launch_match_slots(const int2* slot_pts, const Slot* slots, int32_t*
                                const PadGeom& gs, int img_w, int img_h, int trusted, int wide,
                                rg_ranger_config cfg, rg_match_result* res,
                                rg_ranger_stats* stats, int max_points, cudaStream_t s,
-                               int n_frames = 0);
+                               int n_frames = 0, int region = 0);
 
 // box statistics of dense maps (dense.cu)
 cudaError_t launch_radar_votes(const int16_t* raw, int w, const int32_t* boxes, const double* d_radar, int n,
