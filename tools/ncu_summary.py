@@ -103,8 +103,10 @@ def main():
             sc = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
             b = sum(float(d[m].replace(",", "")) * sc.get(units.get(m, "byte"), 1.0)
                     for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
-            traffic["census_dram_bytes_per_launch"] += b
-            traffic["per_kernel"][name + " " + d.get("Grid Size", d.get("launch__grid_size", ""))] = b
+            key = name + " " + d.get("Grid Size", d.get("launch__grid_size", ""))
+            if key not in traffic["per_kernel"]:  # one launch of each kernel (the capture may hold two batches)
+                traffic["census_dram_bytes_per_launch"] += b
+                traffic["per_kernel"][key] = b
             traffic["source"] = f"{os.path.basename(rep)}: {cmd}"
     if lcsv and os.path.exists(lcsv):
         agg = launches(lcsv)

@@ -8,4 +8,4 @@ B="python bench.py --steps 2 --warmup 3 --frames 32 --stream-frames 0 --c3-frame
 $B > gpurun_out/plain_r2.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_r2.csv $B > gpurun_out/ncu_l_r2.log 2>&1; echo launches=$?
 python tools/stage_time.py 256 2 > gpurun_out/st_r2.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:"census_rowtile|census_rows_kernel|match_slots_warp|sample_slots|plan_frames|aggregate_warp" -c 6 -o gpurun_out/prof_r2 python tools/stage_time.py 256 1 > gpurun_out/ncu_f_r2.log 2>&1; echo full=$?
+ncu --set full --clock-control none --import-source on -k regex:"census_rowtile|census_rows_kernel|census_cols_kernel|match_slots_warp|sample_slots|plan_frames|occluders|aggregate_warp" -c 8 -o gpurun_out/prof_r2 python tools/stage_time.py 256 1 > gpurun_out/ncu_f_r2.log 2>&1; echo full=$?
