@@ -1264,7 +1264,8 @@ cudaError_t launch_census_rois(const uint8_t* left, const uint8_t* right, int n_
                                int pitch, int w, int h, uint32_t* fl, uint32_t* fr, const PadGeom& gf, uint32_t* sl,
                                uint32_t* sr, const PadGeom& gs, const int32_t* lshift, bool internal,
                                const rg_detection* dets, const int32_t* det_off, double tau_s, int dx_far,
-                               int dx_close_scaled, uint32_t* masks, cudaStream_t s, cudaEvent_t full_done) {
+                               int dx_close_scaled, uint32_t* masks, cudaStream_t s, cudaEvent_t full_done,
+                               cudaStream_t side, cudaEvent_t ev_lists, cudaEvent_t ev_red) {
   if (n_frames <= 0) return cudaSuccess;
   const int sides = right ? 2 : 1;
   const bool aligned = (pitch % 4 == 0) && (w % 4 == 0) && (frame_stride % 4 == 0) &&
@@ -1300,28 +1301,46 @@ cudaError_t launch_census_rois(const uint8_t* left, const uint8_t* right, int n_
   // a fixed number of single-warp CTAs per (frame, side) walk the compacted
   // 2-D tile lists
   auto rowtile = [&](auto kern, size_t smem, SmemAttr& attr, uint32_t* a, uint32_t* b, const PadGeom& g,
-                     int walkers, int list_off, int wpb) -> cudaError_t {
+                     int walkers, int list_off, int wpb, cudaStream_t ks) -> cudaError_t {
     cudaError_t e2 = attr.ensure((const void*)kern, smem);
     if (e2 != cudaSuccess) return e2;
     dim3 grid(walkers, 1, sides * n_frames);
-    kern<<<grid, wpb * 32, smem, s>>>(left, right, frame_stride, pitch, w, h, a, b, g, lshift, tiles,
-                                      tile_stride, list_off, side_off);
+    kern<<<grid, wpb * 32, smem, ks>>>(left, right, frame_stride, pitch, w, h, a, b, g, lshift, tiles,
+                                       tile_stride, list_off, side_off);
     return cudaGetLastError();
   };
+  // par (side stream + two events): the reduced-raster tiles run on the side
+  // stream alongside the full-raster ones, s waits for them at the end
+  const bool par = side && ev_lists && ev_red && !full_done;
+  if (par) {
+    e = cudaEventRecord(ev_lists, s);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(side, ev_lists, 0);
+    if (e != cudaSuccess) return e;
+  }
   static const int walk_f = [] { const char* v = getenv("RG_ROWTILE_WALK1"); return v ? atoi(v) : 128; }();
   static const int walk_r = [] { const char* v = getenv("RG_ROWTILE_WALK2"); return v ? atoi(v) : 128; }();
   static SmemAttr attr[4];
-  e = internal ? rowtile(census_rowtile_kernel<true, 1>, rw_smem<1>(), attr[0], fl, fr, gf, walk_f, 4, rw_wpb<1>())
-               : rowtile(census_rowtile_kernel<false, 1>, rw_smem<1>(), attr[1], fl, fr, gf, walk_f, 4, rw_wpb<1>());
+  if (par) {
+    e = internal ? rowtile(census_rowtile_kernel<true, 2>, rw_smem<2>(), attr[2], sl, sr, gs, walk_r, rl.red_off,
+                           rw_wpb<2>(), side)
+                 : rowtile(census_rowtile_kernel<false, 2>, rw_smem<2>(), attr[3], sl, sr, gs, walk_r, rl.red_off,
+                           rw_wpb<2>(), side);
+    if (e == cudaSuccess) e = cudaEventRecord(ev_red, side);
+    if (e != cudaSuccess) return e;
+  }
+  e = internal ? rowtile(census_rowtile_kernel<true, 1>, rw_smem<1>(), attr[0], fl, fr, gf, walk_f, 4, rw_wpb<1>(), s)
+               : rowtile(census_rowtile_kernel<false, 1>, rw_smem<1>(), attr[1], fl, fr, gf, walk_f, 4, rw_wpb<1>(),
+                         s);
   if (e != cudaSuccess) return e;
+  if (par) return cudaStreamWaitEvent(s, ev_red, 0);
   if (full_done) {  // the full raster is complete (the FAR matcher may start)
     e = cudaEventRecord(full_done, s);
     if (e != cudaSuccess) return e;
   }
   e = internal ? rowtile(census_rowtile_kernel<true, 2>, rw_smem<2>(), attr[2], sl, sr, gs, walk_r, rl.red_off,
-                         rw_wpb<2>())
+                         rw_wpb<2>(), s)
                : rowtile(census_rowtile_kernel<false, 2>, rw_smem<2>(), attr[3], sl, sr, gs, walk_r, rl.red_off,
-                         rw_wpb<2>());
+                         rw_wpb<2>(), s);
   return e;
 }
 

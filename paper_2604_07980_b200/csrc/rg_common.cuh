@@ -214,7 +214,8 @@ cudaError_t launch_census_rois(const uint8_t* left, const uint8_t* right, int n_
                                uint32_t* sr, const PadGeom& gs, const int32_t* lshift, bool internal,
                                const rg_detection* dets, const int32_t* det_off, double tau_s, int dx_far,
                                int dx_close_scaled, uint32_t* masks, cudaStream_t s,
-                               cudaEvent_t full_done = nullptr);
+                               cudaEvent_t full_done = nullptr, cudaStream_t side = nullptr,
+                               cudaEvent_t ev_lists = nullptr, cudaEvent_t ev_red = nullptr);
 cudaError_t launch_gather_rows(const uint8_t* hl, const uint8_t* hr, int64_t src_stride, int src_pitch, uint8_t* dl,
                                uint8_t* dr, int64_t dst_stride, int dst_pitch, int w, int h, int n_frames,
                                const rg_detection* dets, const int32_t* det_off, double tau_s, int close_scale,
