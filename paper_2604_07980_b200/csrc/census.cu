@@ -1380,7 +1380,8 @@ cudaError_t launch_census64_rois(const uint8_t* left, const uint8_t* right, int 
                                  const PadGeom& gf, unsigned long long* sl, unsigned long long* sr,
                                  const PadGeom& gs, const int32_t* lshift, const rg_detection* dets,
                                  const int32_t* det_off, double tau_s, int dx_far, int dx_close_scaled,
-                                 uint32_t* masks, cudaStream_t s) {
+                                 uint32_t* masks, cudaStream_t s, cudaStream_t side, cudaEvent_t ev_lists,
+                                 cudaEvent_t ev_red) {
   if (n_frames <= 0) return cudaSuccess;
   const bool aligned = (pitch % 4 == 0) && (w % 4 == 0) && (frame_stride % 4 == 0) &&
                        (reinterpret_cast<uintptr_t>(left) % 4 == 0) &&
@@ -1397,16 +1398,26 @@ cudaError_t launch_census64_rois(const uint8_t* left, const uint8_t* right, int 
   const dim3 grid(walkers, 1, (right ? 2 : 1) * n_frames);
   e = attr[0].ensure((const void*)census64_rowtile_kernel<1>, c64_smem<1>());
   if (e != cudaSuccess) return e;
+  const bool par0 = side && ev_lists && ev_red;
+  if (par0) {  // the lists are done: the reduced tiles may start on the side stream
+    e = cudaEventRecord(ev_lists, s);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(side, ev_lists, 0);
+    if (e != cudaSuccess) return e;
+  }
   census64_rowtile_kernel<1><<<grid, 32, c64_smem<1>(), s>>>(left, right, frame_stride, pitch, w, h, fl, fr, gf,
                                                              lshift, rl.tiles, rl.tile_stride, 4, rl.side_off);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   e = attr[1].ensure((const void*)census64_rowtile_kernel<2>, c64_smem<2>());
   if (e != cudaSuccess) return e;
-  census64_rowtile_kernel<2><<<grid, 32, c64_smem<2>(), s>>>(left, right, frame_stride, pitch, w, h, sl, sr, gs,
-                                                             lshift, rl.tiles, rl.tile_stride, rl.red_off,
-                                                             rl.side_off);
-  return cudaGetLastError();
+  // par: the reduced-raster tiles on the side stream alongside the full ones
+  const bool par = par0;
+  census64_rowtile_kernel<2><<<grid, 32, c64_smem<2>(), par ? side : s>>>(
+      left, right, frame_stride, pitch, w, h, sl, sr, gs, lshift, rl.tiles, rl.tile_stride, rl.red_off, rl.side_off);
+  e = cudaGetLastError();
+  if (e != cudaSuccess || !par) return e;
+  e = cudaEventRecord(ev_red, side);
+  return e == cudaSuccess ? cudaStreamWaitEvent(s, ev_red, 0) : e;
 }
 
 // Zero-copy gather of the census read sets of n_frames pinned host frames

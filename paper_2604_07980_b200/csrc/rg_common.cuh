@@ -226,7 +226,8 @@ cudaError_t launch_census64_rois(const uint8_t* left, const uint8_t* right, int 
                                  const PadGeom& gf, unsigned long long* sl, unsigned long long* sr,
                                  const PadGeom& gs, const int32_t* lshift, const rg_detection* dets,
                                  const int32_t* det_off, double tau_s, int dx_far, int dx_close_scaled,
-                                 uint32_t* masks, cudaStream_t s);
+                                 uint32_t* masks, cudaStream_t s, cudaStream_t side = nullptr,
+                                 cudaEvent_t ev_lists = nullptr, cudaEvent_t ev_red = nullptr);
 cudaError_t launch_census64_frames(const uint8_t* left, const uint8_t* right, int n_frames, int64_t frame_stride,
                                    int pitch, int w, int h, unsigned long long* fl, unsigned long long* fr,
                                    const PadGeom& gf, unsigned long long* sl, unsigned long long* sr,
