@@ -369,6 +369,42 @@ __global__ void __launch_bounds__(kAggWarps * 32) aggregate_warp_kernel(
       const rg_match_result r = res[e.slot_base];
       if (r.n_points >= 4 && r.has_value && r.verified) valid = 1, disp = r.dx_subpix, used = 1;
     }
+  } else if (e.n_slots <= 32) {
+    // up to 32 sub-blocks (every CLOSE object at C2): one value per lane,
+    // bitonic sort by shuffles, runs by ballots -- aggregate_close_disparities
+    // (template_match.hpp:126-148) without shared memory or a serial scan
+    const double inf = __longlong_as_double(0x7ff0000000000000LL);
+    double x = inf;
+    bool ok = false;
+    if (lane < e.n_slots) {
+      const rg_match_result r = res[e.slot_base + lane];
+      ok = r.n_points >= 4 && r.has_value && r.verified;
+      if (ok) x = __dmul_rn(r.dx_subpix, (double)cfg.close_scale);  // template_match.hpp:353
+    }
+    const int m = __popc(__ballot_sync(0xffffffffu, ok));
+#pragma unroll
+    for (int kk = 2; kk <= 32; kk <<= 1)
+#pragma unroll
+      for (int j = kk >> 1; j > 0; j >>= 1) {
+        const double y = __shfl_xor_sync(0xffffffffu, x, j);
+        const bool keep_min = ((lane & j) == 0) == ((lane & kk) == 0);
+        x = keep_min ? (y < x ? y : x) : (x < y ? y : x);
+      }
+    // runs of the ascending values: a new run where v[i] - v[i-1] >= tau_d
+    // (dev_runs); the longest wins, ties to the later run
+    const double xp = __shfl_up_sync(0xffffffffu, x, 1);
+    const bool start = lane < m && (lane == 0 || __dsub_rn(x, xp) >= cfg.tau_d);
+    const unsigned sm = __ballot_sync(0xffffffffu, start);
+    unsigned key = 0;
+    if (start) {
+      const unsigned later = sm & ~((2u << lane) - 1u);
+      const int next = later ? __ffs(later) - 1 : m;
+      key = ((unsigned)(next - lane) << 8) | (unsigned)lane;
+    }
+    key = __reduce_max_sync(0xffffffffu, key);
+    const int blen = (int)(key >> 8), bstart = (int)(key & 0xFFu);
+    const double med = __shfl_sync(0xffffffffu, x, (bstart + blen / 2) & 31);
+    if (m > 0 && blen >= cfg.n_min) valid = 1, disp = med, used = blen;
   } else {
     const bool big = e.n_slots > kAggWarpCap;
     double* dst = big ? scratch + e.slot_base : vals[wid];
