@@ -430,6 +430,9 @@ __device__ __forceinline__ void sweep_tail(const VPoint<CT>* vp, int nv, const C
 #ifndef RG_MW_RANGE_NOINLINE
 #define RG_MW_RANGE_NOINLINE 0
 #endif
+#ifndef RG_MW_COOP_ITEMS  // cooperative blocks split (row offset, chunk) units, not chunks
+#define RG_MW_COOP_ITEMS 1
+#endif
 template <typename CT, int MODE, int PF = 0>
 #if RG_MW_RANGE_NOINLINE
 __device__ __noinline__ void sweep_range(
@@ -453,6 +456,29 @@ __device__ __forceinline__ void sweep_range(
   const int mt = ndx & 31;
   const bool ptail = mt != 0 && mt <= TAIL;
   const int nfull = ptail ? ndx >> 5 : nch;
+  if (nparts > 1 && RG_MW_COOP_ITEMS) {
+    // cooperative blocks: the (row offset, chunk) units split contiguously
+    // over the parts, so more warps than chunks shorten the critical path;
+    // the tail of a row offset goes with its last chunk
+    const int ndy = rg.dy_max - rg.dy_min + 1;
+    const int U = ndy * nfull, u0 = part * U / nparts, u1 = (part + 1) * U / nparts;
+    for (int dyi = 0; dyi < ndy; ++dyi) {
+      const int dy = rg.dy_min + dyi;
+      const int a = max(u0, dyi * nfull) - dyi * nfull, b = min(u1, (dyi + 1) * nfull) - dyi * nfull;
+      for (int c0 = a; c0 < b;) {
+        const int k = min(CMAX, b - c0);
+        sweep_chunks<CT, MODE, PF>(vp, nv, R + (int64_t)dy * g.pitch - rg.dx_min - lane - 32 * c0, lane, c0, k, ndx,
+                                   rg.dx_min, dy, best, bkey, evals);
+        c0 += k;
+      }
+      const bool tail_mine = nfull ? (dyi * nfull + nfull - 1 >= u0 && dyi * nfull + nfull - 1 < u1)
+                                   : (dyi % nparts == part);
+      if (ptail && tail_mine)
+        sweep_tail<CT, MODE>(vp, nv, R + (int64_t)dy * g.pitch, rg.dx_min + 32 * nfull, mt, dy, lane, best, bkey,
+                             evals);
+    }
+    return;
+  }
   const int cb = part * nfull / nparts, ce = (part + 1) * nfull / nparts, nmine = ce - cb;
   const int groups = (nmine + CMAX - 1) / CMAX;
   // balanced group sizes (nmine / groups without a division for 1-2 groups)
@@ -1219,8 +1245,15 @@ cudaError_t launch_match_slots(const int2* slot_pts, const Slot* slots, int32_t*
   // ahead paid 2 us until the padded rasters got 128-B aligned rows; now it
   // costs 2 us (variant 7 keeps it); 8 or 16 warps per FAR block measured
   // 47 / 80 us (variants 5, 6).
-  if (variant == 0 && n_frames > 0 && n_frames <= kLatencyFrames)
-    return small(launch_variant<uint32_t, 4, 12, 0, true>(RG_ARGS));
+  if (variant == 0 && n_frames > 0 && n_frames <= kLatencyFrames) {
+    static const int lw = [] { const char* v = getenv("RG_LAT_WARPS"); return v ? atoi(v) : 4; }();
+    switch (lw) {
+      case 8: return small(launch_variant<uint32_t, 8, 6, 0, true>(RG_ARGS));
+      case 12: return small(launch_variant<uint32_t, 12, 4, 0, true>(RG_ARGS));
+      case 16: return small(launch_variant<uint32_t, 16, 3, 0, true>(RG_ARGS));
+      default: return small(launch_variant<uint32_t, 4, 12, 0, true>(RG_ARGS));
+    }
+  }
   switch (variant) {  // A/B knobs; default measured best (tools/census_time.py with RG_MATCH_VARIANT)
     case 1: return launch_variant<uint32_t, 8, 4>(RG_ARGS);
     case 2: return launch_variant<uint32_t, 8, 5>(RG_ARGS);
