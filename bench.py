@@ -200,8 +200,8 @@ def workload_config(F: int, world: int) -> dict:
                         "dx_max_far = dx_max_close = 256, tau_v 1.0, fwd-bwd + sub-pixel, range z",
             "frames_per_step_per_gpu": F, "noise_sigma": 2.0,
             "frame_seeds": "global frame g = rank * frames_per_step + i has seed 1 + g (all distinct)",
-            "l2": f"inputs {2 * F * W * H / 1e6:.0f} MB + census {F * CENSUS_BYTES_PER_FRAME / 1e6:.0f} MB "
-                  f"per step per GPU > 126 MB L2 (no flush needed)",
+            "l2": f"inputs {2 * F * W * H / 1e6:.0f} MB per step per GPU (every frame distinct) > 126 MB L2 "
+                  f"(no flush needed)",
             "parallelism": f"frame-sharded dp{world}, per-box results all_gathered"}
 
 
