@@ -109,6 +109,40 @@ def test_range_host_zero_copy_gather(ctx, chk, name, n, wide, shift):
         assert int(h_cnt[f]) * 32 == len(want) and ho[f, :len(want)].tobytes() == want, (name, f)
 
 
+def test_range_host_gather_padded_frames_and_partial_chunks(ctx, chk):
+    """rg_range_frames_host over pinned frames with a padded pitch and frame
+    stride (row and frame padding the gather must skip), 30 frames in chunks
+    of 13 (a partial last chunk): records equal the reference's."""
+    import ctypes as C
+    import torch
+
+    n, chunk = 30, 13
+    L, R, D, cfg, sc = _frames(S.scene_c2, n)
+    h, w = L.shape[1:]
+    pitch, fstride = w + 64, (w + 64) * h + 4096
+    eng = FrameEngine(w, h, cfg, max(len(d) for d in D), S.F_PX, S.BASELINE_M, ctx=ctx)
+    recs, offs = pack_detections(D)
+    bufs = []
+    for img in (L, R):
+        t = torch.zeros(n * fstride, dtype=torch.uint8).pin_memory()
+        v = t.numpy()
+        for f in range(n):
+            v[f * fstride:f * fstride + pitch * h].reshape(h, pitch)[:, :w] = img[f]
+        bufs.append(t)
+    h_out = np.zeros(n * eng.out_stride, OUT_DTYPE)
+    h_cnt = np.zeros(n, np.int32)
+    b = eng._batch(n, pitch, fstride, bufs[0].data_ptr(), bufs[1].data_ptr(), recs.ctypes.data, offs.ctypes.data,
+                   h_out.ctypes.data, h_cnt.ctypes.data)
+    x0 = ctx.transfer()
+    ctx.check(rg.lib().rg_range_frames_host(ctx.handle, C.byref(b), C.byref(eng._c), chunk, None))
+    x1 = ctx.transfer()
+    assert 0 < x1[0] - x0[0] < L.nbytes + R.nbytes
+    ho = h_out.view(np.uint8).reshape(n, -1)
+    for f in range(n):
+        want = _want(chk, L[f], R[f], D[f], cfg)
+        assert int(h_cnt[f]) * 32 == len(want) and ho[f, :len(want)].tobytes() == want, f
+
+
 def test_census_rois_switch_same_records(ctx):
     """rg_set_census_rois(0) (full-frame census for every batch) and the
     default ROI tiles give byte-identical records on a 12-frame C2 batch."""
